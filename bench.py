@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: BFS GTEPS on R-MAT (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scale 24] [--algo bfs|sssp|pr|cc|tc] [--source 0]
+
+One step = one full ``bfs(A, source)`` through the public API on the R-MAT
+graph of the reference generator (io.py:275-295, seed 1, a/b/c/d =
+.57/.19/.19/.05, edge factor 16, symmetrised).  The graph is generated on the
+GPU and resident in HBM before timing (cli.py:200-214 excludes load time).
+TEPS = stored edges / time (cli.py:222).
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement for every field.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "BFS GTEPS on RMAT scale-24"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--algo", default="bfs", choices=["bfs"])
+    ap.add_argument("--source", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-cap-s", type=float, default=120.0,
+                    help="wall-clock cap for CPU timing legs")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.15)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# roofline bookkeeping
+# ---------------------------------------------------------------------------
+
+
+def measured_peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def committed_traffic(kernel):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(HERE, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get(kernel)
+
+
+def push_level_bytes(n, k, flops, k_next):
+    """Algorithmic bytes of one push SpMSpV level: frontier ids +
+    two int64 offsets per frontier vertex, one int32 column index per edge,
+    the visited bitmap probe (n/8) and the next-frontier bitmap (n/8)."""
+    return k * (4 + 2 * 8) + flops * 4 + n / 8 + n / 8 + k_next * (4 + 8)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200 import _lib
+    from paper_1908_01407_b200.io import rmat_matrix
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = _lib.context()
+
+    t0 = time.perf_counter()
+    A = rmat_matrix(args.scale)
+    torch.cuda.synchronize()
+    ctx.trim()
+    build_s = time.perf_counter() - t0
+    n, m = A.nrows, A.nnz
+
+    def step():
+        return gb.bfs(A, args.source)
+
+    for _ in range(max(args.warmup, 3)):
+        lv = step()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: exactly K steps -----------------------------
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches()
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            lv = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = (ctx.launches() - launches0) // max(args.steps, 1)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = m / (ms * 1e-3) / 1e9  # GTEPS
+
+    # ---- per-level kernel timing (separate, untimed pass) -------------------
+    desc = gb.Descriptor()
+    ctx.profiling(True)
+    lv = gb.bfs(A, args.source, desc=desc)
+    prof = ctx.prof_read()
+    ctx.profiling(False)
+    trace = [(d.chosen, d.frontier_nvals) for d in desc.direction_log]
+    levels_host = lv.values
+    counts = np.bincount(levels_host, minlength=len(trace) + 2)
+    roof = None
+    peak, peak_src = measured_peaks()
+    push_times = [(arg, t) for (kind, arg, t) in prof if kind == 1]
+    if push_times:
+        # dominant launch: the push expansion with the largest frontier (level 2 at s24)
+        k, t_ms = max(push_times, key=lambda x: x[0])
+        lvl = next(i for i, (c, nv) in enumerate(trace) if c == "push" and nv == k)
+        deg = np.diff(A._csr.offsets.cpu().numpy())
+        front = np.flatnonzero(levels_host == lvl + 1)
+        flops = int(deg[front].sum())
+        k_next = int(counts[lvl + 2]) if lvl + 2 < counts.size else 0
+        bytes_alg = push_level_bytes(n, k, flops, k_next)
+        achieved = bytes_alg / (t_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "lbs_expand<PushMark> (push SpMSpV, level %d)" % (lvl + 1),
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                "traffic": committed_traffic("lbs_expand"),
+                "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4),
+                "frontier": int(k), "flops": flops,
+                "level_ms": [(kind, a, round(t, 4)) for (kind, a, t) in prof]}
+
+    # ---- end-to-end through the public API (host result every step) --------
+    t_e2e = []
+    for i in range(args.steps):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        out = gb.bfs(A, args.source).values      # levels -> host numpy (pinned D2H)
+        t_e2e.append(time.perf_counter() - t1)
+    e2e_ms = float(np.mean(t_e2e)) * 1e3
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- CPU baseline: the C port of the reference algorithm, same CSR ------
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import cgraph
+        rp = A._csr.offsets.cpu().numpy()
+        ci = A._csr.indices.cpu().numpy()
+        cgraph.lib()
+        threads = cgraph.threads()
+        times = []
+        tstart = time.perf_counter()
+        ref_lv = None
+        while len(times) < 3 and (time.perf_counter() - tstart) < args.cpu_cap_s:
+            t1 = time.perf_counter()
+            ref_lv, ref_trace = cgraph.bfs(rp, ci, args.source)
+            times.append(time.perf_counter() - t1)
+        cpu_s = float(np.mean(times))
+        parity = bool(np.array_equal(ref_lv, levels_host)) and \
+            [t[:2] for t in ref_trace] == [tuple(t) for t in trace]
+        cpu = {"value": round(m / cpu_s / 1e9, 4), "unit": "GTEPS", "cores": threads,
+               "kind": "port",
+               "sample": f"full BFS from vertex {args.source} on the same s{args.scale} CSR, "
+                         f"oracle/cgraph.c og_bfs with {threads} OpenMP threads, mean of {len(times)} runs",
+               "ms_per_bfs": round(cpu_s * 1e3, 2), "cpu": platform.processor() or platform.machine()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "u32/i64 (bitmaps, int32 indices, int64 levels)",
+            "data": "synthetic R-MAT (reference SplitMix64 generator, seed 1), generated on GPU",
+            "config": {"workload": f"bfs(A, {args.source}) on rmat-s{args.scale}-e16 symmetrised",
+                       "n": n, "nnz": m, "global_batch": 1, "seq_len": None,
+                       "parallelism": f"1d-vertex-partition x{world}" if world > 1 else "single-gpu",
+                       "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB)" % ((m * 4 + (n + 1) * 8) / 1e9),
+                       "build_s": round(build_s, 2), "trace": trace},
+            "clocks": clocks.summary(),
+            "e2e": {"value": round(m / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GTEPS",
+                    "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": 8,
+                    "d2h_bytes_per_step": int(n * 8),
+                    "what": "bfs(A, src).values through the public API: source id in, "
+                            "int64 level vector (n*8 B) out to host every step"},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "parity_vs_oracle": parity,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the C port of the reference algorithm on the host cores
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle import cgraph
+    cgraph.lib()
+    threads = cgraph.threads()
+    t0 = time.perf_counter()
+    rp, ci = cgraph.rmat_csr(args.scale)
+    build_s = time.perf_counter() - t0
+    n, m = rp.size - 1, ci.size
+    tw = []
+    for _ in range(max(args.warmup, 1)):
+        t1 = time.perf_counter()
+        cgraph.bfs(rp, ci, args.source)
+        tw.append(time.perf_counter() - t1)
+    per = float(np.mean(tw))
+    k = args.steps
+    if per * k > args.cpu_cap_s:
+        k = max(1, int(args.cpu_cap_s / per))
+    t1 = time.perf_counter()
+    for _ in range(k):
+        cgraph.bfs(rp, ci, args.source)
+    total = time.perf_counter() - t1
+    ms = total / k * 1e3
+    value = m / (ms * 1e-3) / 1e9
+    sample = (f"full BFS from vertex {args.source} on rmat-s{args.scale} per step; "
+              f"{k} of {args.steps} steps timed (cap {args.cpu_cap_s:.0f}s)")
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world,
+            "steps": k, "warmup": max(args.warmup, 1), "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8/i64", "data": "synthetic R-MAT (reference generator, seed 1)",
+            "impl": "reference",
+            "config": {"workload": f"bfs(A, {args.source}) on rmat-s{args.scale}-e16 symmetrised",
+                       "n": n, "nnz": m, "build_s": round(build_s, 2)},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GTEPS", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

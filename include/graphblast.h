@@ -1,0 +1,236 @@
+/*
+ * libgraphblast_sm100a -- C ABI of the B200-native GraphBLAST backend.
+ *
+ * The reference (/root/reference/pkg/src/graphalg) is a Python package whose
+ * operator layer is kernels.py.  Its "plugin boundary" is the set of module
+ * functions listed in __init__.py:70-85.  This header is what those functions
+ * bind to (via ctypes): each entry point below names the
+ * reference function it replaces (file:line relative to pkg/src/graphalg/).
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless its name ends in `_host`.
+ *     Buffers are owned by the caller (PyTorch tensors on the Python side);
+ *     the library only borrows them for the duration of the call, plus a
+ *     grow-only scratch pool owned by the context.
+ *   - Index arrays: offsets are int64, column/row/vector indices int32
+ *     (vertex counts < 2^31).  Values are int64 or float64 (`dtype`).
+ *   - A matrix orientation with `values == NULL` is "iso": every stored entry
+ *     equals `iso_i64` / `iso_f64` (structure-only storage).
+ *   - Calls are asynchronous on the context's stream except where they return
+ *     a host scalar (documented per function).
+ *   - Return codes: GB_OK or a negative gb_status; gb_last_error() has text.
+ */
+#ifndef GRAPHBLAST_H
+#define GRAPHBLAST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t gb_status;
+enum {
+  GB_OK = 0,
+  GB_ERR_SHAPE = -1,       /* errors.py ShapeError       */
+  GB_ERR_FORMAT = -2,      /* errors.py FormatError      */
+  GB_ERR_INDEX = -3,       /* IndexError                 */
+  GB_ERR_VALUE = -4,       /* ValueError                 */
+  GB_ERR_UNSUPPORTED = -5, /* NotImplementedError        */
+  GB_ERR_CUDA = -6,
+  GB_ERR_OOM = -7,
+  GB_ERR_ARG = -8
+};
+
+/* value dtypes */
+enum { GB_I64 = 0, GB_F64 = 1 };
+
+/* operator ids (algebra.py:146-158) */
+enum {
+  GB_OP_PLUS = 0,      /* builtin Plus: saturating when pairwise         */
+  GB_OP_PLUS_WRAP = 1, /* a user op on np.add without the saturating fn  */
+  GB_OP_MINUS = 2,
+  GB_OP_TIMES = 3,
+  GB_OP_MIN = 4,
+  GB_OP_MAX = 5,
+  GB_OP_LOR = 6,
+  GB_OP_LAND = 7,
+  GB_OP_LESS = 8,
+  GB_OP_NE = 9,
+  GB_OP_SECOND = 10,
+  GB_OP_FIRST = 11
+};
+
+/* direction policy (containers.py:32-35) and chosen direction */
+enum { GB_DIR_AUTO = 0, GB_DIR_PUSH = 1, GB_DIR_PULL = 2 };
+/* pull partitioning (containers.py:43-46) */
+enum { GB_PART_NONZERO = 0, GB_PART_ROW = 1 };
+
+typedef struct gb_ctx gb_ctx;
+
+/* One orientation of a sparse matrix: `n` rows of A (CSR) or of A^T (CSC). */
+typedef struct gb_csr {
+  int64_t nrows;
+  int64_t ncols;
+  int64_t nnz;
+  const int64_t* offsets; /* [nrows+1] */
+  const int32_t* indices; /* [nnz]     */
+  const void* values;     /* [nnz] of dtype, or NULL when iso */
+  int32_t dtype;
+  int32_t pad_;
+  int64_t iso_i64;
+  double iso_f64;
+} gb_csr;
+
+/* ----------------------------------------------------------------------------
+ * context
+ * --------------------------------------------------------------------------*/
+gb_status gb_ctx_create(int device, gb_ctx** out);
+gb_status gb_ctx_destroy(gb_ctx* ctx);
+gb_status gb_ctx_set_stream(gb_ctx* ctx, void* cuda_stream);
+/* Synchronize the stream; reports a device-detected error (GB_ERR_INDEX). */
+gb_status gb_ctx_sync(gb_ctx* ctx);
+const char* gb_last_error(gb_ctx* ctx);
+int32_t gb_abi_version(void);
+/* bytes currently held by the context's scratch pool */
+int64_t gb_scratch_bytes(gb_ctx* ctx);
+/* release the scratch pool (e.g. after a large graph build) */
+gb_status gb_ctx_trim(gb_ctx* ctx);
+/* number of kernels this context has launched (all entry points) */
+int64_t gb_launch_count(gb_ctx* ctx);
+/* Event timing of the fused drivers' main kernels: when on, each main kernel
+ * launch records (kind, arg, ms); gb_prof_read returns and clears them. */
+gb_status gb_ctx_set_profiling(gb_ctx* ctx, int32_t on);
+int32_t gb_prof_read(gb_ctx* ctx, int32_t max, int32_t* kind_host, int64_t* arg_host,
+                     float* ms_host);
+
+/* ----------------------------------------------------------------------------
+ * matrix construction   (containers.py:307-364, io.py:220-315)
+ * --------------------------------------------------------------------------*/
+
+/* SparseMatrix.from_tuples (containers.py:307-345): stable sort by (row, col),
+ * fold duplicates with `dedup_op`, emit CSR.  Outputs are sized nnz_in; the
+ * kept count is written to *nnz_out_host (synchronizes).  Returns
+ * GB_ERR_INDEX when a coordinate is out of range. */
+gb_status gb_build_csr(gb_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz_in,
+                       const int64_t* rows, const int64_t* cols, const void* vals,
+                       int32_t dtype, int32_t dedup_op, int64_t* out_offsets,
+                       int32_t* out_indices, void* out_vals, int64_t* nnz_out_host);
+
+/* SparseMatrix._build_csc (containers.py:357-364): the other orientation,
+ * stable in row order.  `vals`/`out_vals` may be NULL (iso). */
+gb_status gb_transpose_csr(gb_ctx* ctx, const gb_csr* a, int64_t* out_offsets,
+                           int32_t* out_indices, void* out_vals);
+
+/* 1 when the two orientations hold identical arrays (A == A^T);
+ * algorithms.py:41-45 _require_symmetric.  Synchronizes. */
+gb_status gb_csr_equal(gb_ctx* ctx, const gb_csr* a, const gb_csr* b, int32_t* equal_host);
+
+/* 1 when every stored value equals the first one (iso detection). Sync. */
+gb_status gb_values_iso(gb_ctx* ctx, int64_t n, const void* vals, int32_t dtype,
+                        int32_t* iso_host);
+
+/* min / max of a value array (sssp weight check, algorithms.py:92). Sync. */
+gb_status gb_values_minmax(gb_ctx* ctx, int64_t n, const void* vals, int32_t dtype,
+                           double* min_host, double* max_host);
+
+/* generate_rmat (io.py:275-295): edge e, level l uses SplitMix64 draw
+ * e*scale+l; thresholds are the caller's double sums a, a+b, a+b+c. */
+gb_status gb_rmat_generate(gb_ctx* ctx, int32_t scale, int64_t nedges, uint64_t seed,
+                           double a, double t_ab, double t_abc, int32_t* src, int32_t* dst);
+
+/* preprocess + edges_to_matrix (io.py:220-249, 298-315) for pattern edges:
+ * drop self loops, optionally mirror, sort by (src,dst), dedup -> CSR.
+ * out_indices must hold 2*nedges (mirrored) entries. Synchronizes. */
+gb_status gb_edges_to_csr(gb_ctx* ctx, int64_t n, int64_t nedges, const int32_t* src,
+                          const int32_t* dst, int32_t make_undirected, int64_t* out_offsets,
+                          int32_t* out_indices, int64_t* nnz_out_host);
+
+/* assign_weights (io.py:252-272): one integer weight in [low, high] per
+ * unordered pair, drawn from SplitMix64(seed) in order of the pair's first
+ * appearance in the (src, dst) list; both directions get the same value.
+ * Writes float64 weights in list order. Synchronizes. */
+gb_status gb_assign_weights(gb_ctx* ctx, int64_t n, int64_t nedges, const int32_t* src,
+                            const int32_t* dst, uint64_t seed, int64_t low, int64_t high,
+                            double* out_weights);
+
+/* row id of every stored entry of a CSR (extract_tuples, containers.py:404-407) */
+gb_status gb_csr_row_ids(gb_ctx* ctx, int64_t nrows, int64_t nnz, const int64_t* offsets,
+                         int32_t* out_rows);
+
+/* ----------------------------------------------------------------------------
+ * vectors and masks   (containers.py:175-252, kernels.py:67-84)
+ * --------------------------------------------------------------------------*/
+
+/* Vector.nvals_for on dense storage: count of values != zero. Synchronizes. */
+gb_status gb_count_ne(gb_ctx* ctx, int64_t n, const void* vals, int32_t dtype,
+                      const void* zero_host, int64_t* count_host);
+
+/* to_sparse (containers.py:242-252): keep entries != zero (dense input when
+ * idx == NULL; sparse input of k entries otherwise).  Writes the kept count
+ * to *count_host (synchronizes). */
+gb_status gb_compact(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx, const void* vals,
+                     int32_t dtype, const void* zero_host, int32_t* out_idx, void* out_vals,
+                     int64_t* count_host);
+
+/* to_dense (containers.py:230-240): fill `zero`, scatter k entries. */
+gb_status gb_scatter_dense(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx,
+                           const void* vals, int32_t dtype, const void* zero_host,
+                           void* out_vals);
+
+/* _effective_mask (kernels.py:67-84) as a bitmap of ceil(n/32) words: a stored
+ * entry allows its position iff its value != 0; complement flips. */
+gb_status gb_mask_bitmap(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx,
+                         const void* vals, int32_t dtype, int32_t complement, uint32_t* out);
+
+/* bitmap of rows with at least one stored entry */
+gb_status gb_nonempty_rows(gb_ctx* ctx, int64_t n, const int64_t* offsets, uint32_t* out);
+
+/* ----------------------------------------------------------------------------
+ * matrix-vector   (kernels.py:108-322)
+ * --------------------------------------------------------------------------*/
+
+/* decide_direction (kernels.py:108-126): pure host function, exported so the
+ * rule has exactly one implementation shared by every fused driver. */
+int32_t gb_decide_direction(int64_t nnz, int64_t nrows, int64_t nnz_u, double switch_ratio,
+                            int32_t policy, int64_t* estimate_out);
+
+/* Pull SpMV (kernels.py:153-229): for every row i of `a` allowed by `mask`
+ * (NULL = all), out[i] = fold over stored (i,j) with u[j] != identity of
+ * mult(a_ij, u[j]); rows without contributions get the identity.  `u` and
+ * `out` are dense of dtype T = a->dtype.  counters (may be NULL) accumulates
+ * {entries read, multiplies, adds} exactly as the reference counts them. */
+gb_status gb_mxv_pull(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                      const void* u, const uint32_t* mask, int32_t early_exit,
+                      int32_t partition, void* out, int64_t* counters);
+
+/* Push SpMSpV (kernels.py:242-280): expand the columns named by the sparse u
+ * (k entries), multiply, fold per output row, drop identity results, apply
+ * the mask.  `a` is the column orientation (rows of `a` = the columns walked).
+ * Output is sorted by index; count written to *count_host (synchronizes). */
+gb_status gb_mxv_push(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                      int64_t out_size, int64_t k, const int32_t* u_idx, const void* u_vals,
+                      const uint32_t* mask, int32_t* out_idx, void* out_vals,
+                      int64_t* count_host, int64_t* counters);
+
+/* ----------------------------------------------------------------------------
+ * fused algorithms   (algorithms.py)
+ * --------------------------------------------------------------------------*/
+
+/* bfs (algorithms.py:48-77) fused: levels (int64[n], written entirely) get the
+ * 1-based level, 0 = unreached.  `push` is the orientation walked by push
+ * (rows = out-edges), `pull` the orientation walked by pull (rows = in-edges)
+ * with `pull_nonempty` its nonempty-row bitmap.  One decision per iteration
+ * is written to log_dir/log_nvals/log_est (host arrays of max_iters entries);
+ * *iters_host receives the number of decisions. */
+gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                 const uint32_t* pull_nonempty, int64_t source, int64_t max_iters,
+                 double switch_ratio, int32_t policy, int64_t* levels,
+                 int32_t* log_dir_host, int64_t* log_nvals_host, int64_t* log_est_host,
+                 int64_t* iters_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAPHBLAST_H */

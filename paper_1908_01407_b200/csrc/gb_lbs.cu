@@ -1,0 +1,53 @@
+#include <cub/cub.cuh>
+
+#include "gb_lbs.cuh"
+
+namespace gb {
+
+__global__ void lbs_degrees(int64_t K, const int32_t* __restrict__ ids,
+                            const int64_t* __restrict__ off, int64_t* __restrict__ rowstart,
+                            int64_t* __restrict__ deg) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = ids[k];
+    const int64_t a = off[v], b = off[v + 1];
+    rowstart[k] = a;
+    deg[k] = b - a;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) deg[K] = 0;
+}
+
+__global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S,
+                               int32_t* __restrict__ tile_first) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = S[k], b = S[k + 1];
+    if (b <= a) continue;
+    // tiles whose first edge t*TE lies in [a, b)
+    int64_t t = (a + kLbsTile - 1) / kLbsTile;
+    for (; t * kLbsTile < b; ++t) tile_first[t] = (int32_t)k;
+  }
+}
+
+gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
+                      const int64_t* off, int64_t max_edges, LbsPlan* plan) {
+  cudaStream_t s = stream_of(ctx);
+  plan->K = K;
+  plan->rowstart = ar.alloc<int64_t>(K + 1);
+  int64_t* deg = ar.alloc<int64_t>(K + 1);
+  plan->S = ar.alloc<int64_t>(K + 1);
+  plan->tile_first = ar.alloc<int32_t>(max_edges / kLbsTile + 2);
+  GB_ARENA_CHECK(ctx, ar);
+  lbs_degrees<<<grid_for(ctx, K + 1, 256), 256, 0, s>>>(K, ids, off, plan->rowstart, deg);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, plan->S, K + 1, s);
+  void* tmp = ar.raw(tb);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, deg, plan->S, K + 1, s));
+  lbs_tile_first<<<grid_for(ctx, K, 256), 256, 0, s>>>(K, plan->S, plan->tile_first);
+  GB_LAUNCH_CHECK(ctx);
+  plan->grid = sm_count(ctx) * 4;
+  return GB_OK;
+}
+
+}  // namespace gb

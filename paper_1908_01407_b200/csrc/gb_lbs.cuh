@@ -1,0 +1,98 @@
+// Load-balanced expansion of a frontier's adjacency lists (edge-balanced
+// partitioning, the GPU form of the reference's nonzero split,
+// kernels.py:133-150, applied to the push gather kernels.py:254-262).
+//
+// Given K frontier entries ids[0..K) and the walked orientation `off`,
+// the expansion space is the concatenation of their adjacency ranges:
+// E = sum_k deg(ids[k]).  It is cut into tiles of exactly TE edges; every
+// CTA processes whole tiles.  Owner lookup inside a tile is a shared-memory
+// table filled cooperatively (one warp per frontier entry), so each edge
+// costs one LDS for its owner plus a coalesced load of its column index.
+#pragma once
+
+#include "gb_common.cuh"
+
+namespace gb {
+
+constexpr int kLbsThreads = 256;
+constexpr int kLbsItems = 16;
+constexpr int kLbsTile = kLbsThreads * kLbsItems;  // 4096 edges per tile
+constexpr int kLbsCap = kLbsTile;                  // frontier entries per tile (fast path)
+
+// rowstart[k] = off[ids[k]], deg[k] = off[ids[k]+1] - off[ids[k]]
+__global__ void lbs_degrees(int64_t K, const int32_t* __restrict__ ids,
+                            const int64_t* __restrict__ off, int64_t* __restrict__ rowstart,
+                            int64_t* __restrict__ deg);
+
+// S = exclusive scan of deg (K+1 entries, S[K] = E); tile_first[t] = the
+// frontier entry whose range contains edge t*TE.
+__global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S,
+                               int32_t* __restrict__ tile_first);
+
+// Expansion kernel.  f(k, p, e) is called once per edge e of the expansion,
+// where k is the frontier position and p the position in the orientation's
+// index/value arrays.
+template <class F>
+__global__ void __launch_bounds__(kLbsThreads)
+lbs_expand(int64_t K, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
+           const int32_t* __restrict__ tile_first, F f) {
+  __shared__ int64_t s_delta[kLbsCap];
+  __shared__ uint16_t s_own[kLbsTile];
+  const int64_t E = S[K];
+  const int64_t ntiles = (E + kLbsTile - 1) / kLbsTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = kLbsThreads / 32;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t e0 = t * kLbsTile;
+    const int64_t e1 = e0 + kLbsTile < E ? e0 + kLbsTile : E;
+    const int64_t k0 = tile_first[t];
+    const int64_t k1 = t + 1 < ntiles ? tile_first[t + 1] : K - 1;
+    const int64_t nk = k1 - k0 + 1;
+    if (nk <= kLbsCap) {
+      for (int64_t i = warp; i < nk; i += nwarps) {
+        const int64_t k = k0 + i;
+        const int64_t sk = S[k], sk1 = S[k + 1];
+        const int64_t lo = sk > e0 ? sk : e0;
+        const int64_t hi = sk1 < e1 ? sk1 : e1;
+        if (lane == 0) s_delta[i] = rowstart[k] - sk;
+        for (int64_t e = lo + lane; e < hi; e += 32) s_own[e - e0] = (uint16_t)i;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int r = 0; r < kLbsItems; ++r) {
+        const int64_t el = (int64_t)r * kLbsThreads + threadIdx.x;
+        const int64_t e = e0 + el;
+        if (e < e1) {
+          const int i = s_own[el];
+          f(k0 + i, s_delta[i] + e, e);
+        }
+      }
+      __syncthreads();
+    } else {
+      // many empty frontier entries inside one tile: binary search per edge
+      for (int64_t e = e0 + threadIdx.x; e < e1; e += kLbsThreads) {
+        int64_t lo = k0, hi = k1;  // largest k with S[k] <= e
+        while (lo < hi) {
+          int64_t mid = (lo + hi + 1) >> 1;
+          if (S[mid] <= e) lo = mid; else hi = mid - 1;
+        }
+        f(lo, rowstart[lo] + (e - S[lo]), e);
+      }
+    }
+  }
+}
+
+// Host helper: degrees + scan + tile_first for K frontier entries.  Leaves
+// S (K+1 entries, device) so the caller can read E = S[K] if it needs it.
+struct LbsPlan {
+  int64_t K = 0;
+  int64_t* rowstart = nullptr;
+  int64_t* S = nullptr;
+  int32_t* tile_first = nullptr;
+  int grid = 0;
+};
+
+gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
+                      const int64_t* off, int64_t max_edges, LbsPlan* plan);
+
+}  // namespace gb

@@ -1,0 +1,281 @@
+// Generic masked matrix-vector multiply over any device-encodable semiring.
+//
+//   gb_mxv_pull   _spmv_pull / _pull_span   kernels.py:153-229
+//   gb_mxv_push   _spmspv_push             kernels.py:242-280
+//
+// These are the unfused operator-layer kernels behind mxv / vxm / spmv_pull /
+// spmspv_push.  They reproduce the reference exactly, including its work
+// counters; the algorithms use their own fused drivers instead.
+#include <type_traits>
+
+#include <cub/cub.cuh>
+
+#include "gb_common.cuh"
+#include "gb_lbs.cuh"
+
+namespace gb {
+
+__host__ __device__ __forceinline__ bool fold_is_commutative(int op) {
+  return op == GB_OP_PLUS || op == GB_OP_PLUS_WRAP || op == GB_OP_TIMES || op == GB_OP_MIN ||
+         op == GB_OP_MAX || op == GB_OP_LOR || op == GB_OP_LAND;
+}
+
+template <class T>
+__device__ __forceinline__ T aval(const T* vals, T iso, int64_t p) {
+  return vals ? vals[p] : iso;
+}
+
+// Warp per row.  counters: [entries read, multiplies, adds]
+template <class T>
+__global__ void __launch_bounds__(256)
+mv_pull_rows(int64_t nrows, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+             const T* __restrict__ vals, T iso, const T* __restrict__ u,
+             const uint32_t* __restrict__ mask, int add_op, int mult_op, int early,
+             T* __restrict__ out, unsigned long long* __restrict__ counters) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T ident = op_identity<T>(add_op);
+  const bool comm = fold_is_commutative(add_op);
+  for (int64_t i = w0; i < nrows; i += nw) {
+    if (mask && !((mask[i >> 5] >> (i & 31)) & 1u)) {
+      if (lane == 0) out[i] = ident;
+      continue;
+    }
+    const int64_t lo = off[i], hi = off[i + 1];
+    T acc = ident;
+    long long incl = 0;
+    int64_t first_hit = hi;  // position of the first hit (early-exit read count)
+    if (comm) {
+      for (int64_t base = lo; base < hi; base += 32) {
+        const int64_t p = base + lane;
+        bool hit = false;
+        if (p < hi) {
+          const T uj = u[idx[p]];
+          if (uj != ident) {
+            const T prod = op_pair<T>(mult_op, aval(vals, iso, p), uj);
+            acc = op_fold<T>(add_op, acc, prod);
+            ++incl;
+            hit = prod != ident;
+          }
+        }
+        if (early) {
+          const uint32_t hits = __ballot_sync(GB_FULL, hit);
+          if (hits && first_hit == hi) first_hit = base + __ffs(hits) - 1;
+          if (hits && !counters) break;  // results never depend on the rest
+        }
+      }
+      acc = warp_fold<T>(add_op, acc);
+    } else if (lane == 0) {
+      // order-dependent fold (e.g. a user monoid on SelectSecond): sequential
+      bool any = false;
+      for (int64_t p = lo; p < hi; ++p) {
+        const T uj = u[idx[p]];
+        if (uj == ident) continue;
+        const T prod = op_pair<T>(mult_op, aval(vals, iso, p), uj);
+        acc = any ? op_fold<T>(add_op, acc, prod) : op_fold1<T>(add_op, prod);
+        any = true;
+        ++incl;
+        if (early && prod != ident && first_hit == hi) first_hit = p;
+      }
+    }
+    if (lane == 0) out[i] = acc;
+    if (counters) {
+      incl = warp_sum_ll(incl);
+      if (lane == 0) {
+        const long long reads = early ? (first_hit < hi ? first_hit - lo + 1 : hi - lo) : hi - lo;
+        atomicAdd(counters + 0, (unsigned long long)reads);
+        atomicAdd(counters + 1, (unsigned long long)incl);
+        if (incl > 0) atomicAdd(counters + 2, (unsigned long long)(incl - 1));
+      }
+    }
+  }
+}
+
+template <class T>
+struct PushExpand {
+  const int32_t* __restrict__ idx;
+  const T* __restrict__ vals;
+  T iso;
+  const T* __restrict__ u_vals;
+  int mult_op;
+  int32_t* __restrict__ rows;
+  T* __restrict__ prods;
+  __device__ __forceinline__ void operator()(int64_t k, int64_t p, int64_t e) const {
+    rows[e] = idx[p];
+    prods[e] = op_pair<T>(mult_op, aval(vals, iso, p), u_vals[k]);
+  }
+};
+
+__global__ void seg_flags(int64_t n, const int32_t* __restrict__ keys, int32_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// One thread per segment: fold in stable (expansion) order, keep non-identity,
+// allowed results.  keep[s] = 1 when segment s survives.
+template <class T>
+__global__ void seg_fold(int64_t n, const int32_t* __restrict__ keys, const int32_t* __restrict__ flags,
+                         const int64_t* __restrict__ segpos, const T* __restrict__ prods, int add_op,
+                         const uint32_t* __restrict__ mask, int32_t* __restrict__ seg_row,
+                         T* __restrict__ seg_val, int32_t* __restrict__ keep) {
+  const T ident = op_identity<T>(add_op);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!flags[i]) continue;
+    const int32_t r = keys[i];
+    T acc = prods[i];
+    int64_t j = i + 1;
+    if (j < n && keys[j] == r) {
+      for (; j < n && keys[j] == r; ++j) acc = op_fold<T>(add_op, acc, prods[j]);
+    } else {
+      acc = op_fold1<T>(add_op, acc);
+    }
+    const int64_t s = segpos[i];
+    seg_row[s] = r;
+    seg_val[s] = acc;
+    bool ok = acc != ident;
+    if (ok && mask) ok = (mask[r >> 5] >> (r & 31)) & 1u;
+    keep[s] = ok ? 1 : 0;
+  }
+}
+
+template <class T>
+__global__ void select_kept(int64_t nseg, const int32_t* __restrict__ keep,
+                            const int64_t* __restrict__ pos, const int32_t* __restrict__ seg_row,
+                            const T* __restrict__ seg_val, int32_t* __restrict__ out_idx,
+                            T* __restrict__ out_vals) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
+       s += (int64_t)gridDim.x * blockDim.x)
+    if (keep[s]) {
+      out_idx[pos[s]] = seg_row[s];
+      out_vals[pos[s]] = seg_val[s];
+    }
+}
+
+static int bits_for(int64_t n) {
+  int b = 1;
+  while (((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+template <class T>
+static gb_status push_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a, int64_t out_size,
+                        int64_t k, const int32_t* u_idx, const T* u_vals, const uint32_t* mask,
+                        int32_t* out_idx, T* out_vals, int64_t* count, int64_t* counters) {
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  *count = 0;
+  if (k == 0) return GB_OK;
+  LbsPlan plan;
+  GB_TRY(lbs_prepare(ctx, ar, k, u_idx, a->offsets, a->nnz, &plan));
+  int64_t E = 0;
+  GB_TRY(read_i64(ctx, plan.S + k, &E));
+  if (counters) {
+    int64_t c[3];
+    GB_TRY(read_i64(ctx, counters, c, 3));
+    c[1] += E;
+    GB_CUDA(ctx, cudaMemcpyAsync(counters, c, 24, cudaMemcpyHostToDevice, s));
+  }
+  if (E == 0) return GB_OK;
+  int32_t* ka = ar.alloc<int32_t>(E);
+  int32_t* kb = ar.alloc<int32_t>(E);
+  T* va = ar.alloc<T>(E);
+  T* vb = ar.alloc<T>(E);
+  int32_t* flags = ar.alloc<int32_t>(E);
+  int64_t* segpos = ar.alloc<int64_t>(E);
+  GB_ARENA_CHECK(ctx, ar);
+  T iso = std::is_same<T, double>::value ? (T)a->iso_f64 : (T)a->iso_i64;
+  PushExpand<T> f{a->indices, (const T*)a->values, iso, u_vals, mult_op, ka, va};
+  lbs_expand<PushExpand<T>><<<plan.grid, kLbsThreads, 0, s>>>(k, plan.S, plan.rowstart,
+                                                              plan.tile_first, f);
+  cub::DoubleBuffer<int32_t> dk(ka, kb);
+  cub::DoubleBuffer<T> dv(va, vb);
+  size_t tb = 0;
+  const int bits = bits_for(out_size > 1 ? out_size : 2);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, E, 0, bits, s);
+  void* tmp = ar.raw(tb);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, E, 0, bits, s));
+  const int32_t* keys = dk.Current();
+  const T* prods = dv.Current();
+  seg_flags<<<grid_for(ctx, E, 256), 256, 0, s>>>(E, keys, flags);
+  size_t tb2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb2, flags, segpos, E, s);
+  void* tmp2 = ar.raw(tb2);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp2, tb2, flags, segpos, E, s));
+  int64_t nseg = 0;
+  GB_TRY(read_i64(ctx, segpos + E - 1, &nseg));
+  nseg += 1;
+  if (counters) {
+    int64_t c[3];
+    GB_TRY(read_i64(ctx, counters, c, 3));
+    c[2] += E - nseg;
+    GB_CUDA(ctx, cudaMemcpyAsync(counters, c, 24, cudaMemcpyHostToDevice, s));
+  }
+  int32_t* seg_row = ar.alloc<int32_t>(nseg);
+  T* seg_val = ar.alloc<T>(nseg);
+  int32_t* keep = ar.alloc<int32_t>(nseg + 1);
+  int64_t* kpos = ar.alloc<int64_t>(nseg + 1);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cudaMemsetAsync(keep + nseg, 0, sizeof(int32_t), s));
+  seg_fold<T><<<grid_for(ctx, E, 256), 256, 0, s>>>(E, keys, flags, segpos, prods, add_op, mask,
+                                                    seg_row, seg_val, keep);
+  size_t tb3 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb3, keep, kpos, nseg + 1, s);
+  void* tmp3 = ar.raw(tb3);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp3, tb3, keep, kpos, nseg + 1, s));
+  select_kept<T><<<grid_for(ctx, nseg, 256), 256, 0, s>>>(nseg, keep, kpos, seg_row, seg_val,
+                                                          out_idx, out_vals);
+  GB_LAUNCH_CHECK(ctx);
+  GB_TRY(read_i64(ctx, kpos + nseg, count));
+  count_launch(ctx, 12);
+  return GB_OK;
+}
+
+}  // namespace gb
+
+using namespace gb;
+
+extern "C" {
+
+gb_status gb_mxv_pull(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                      const void* u, const uint32_t* mask, int32_t early_exit, int32_t partition,
+                      void* out, int64_t* counters) {
+  (void)partition;  // row-split warp-per-row kernel for both partition modes
+  cudaStream_t s = stream_of(ctx);
+  const int64_t n = a->nrows;
+  if (n == 0) return GB_OK;
+  const int early = early_exit && add_op == GB_OP_LOR;
+  const int grid = grid_for(ctx, n * 32, 256, 16);
+  const int ps = prof_begin(ctx, PROF_MV, n);
+  if (a->dtype == GB_I64)
+    mv_pull_rows<int64_t><<<grid, 256, 0, s>>>(n, a->offsets, a->indices,
+                                               (const int64_t*)a->values, a->iso_i64,
+                                               (const int64_t*)u, mask, add_op, mult_op, early,
+                                               (int64_t*)out, (unsigned long long*)counters);
+  else
+    mv_pull_rows<double><<<grid, 256, 0, s>>>(n, a->offsets, a->indices, (const double*)a->values,
+                                              a->iso_f64, (const double*)u, mask, add_op, mult_op,
+                                              early, (double*)out, (unsigned long long*)counters);
+  prof_end(ctx, ps);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  return GB_OK;
+}
+
+gb_status gb_mxv_push(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                      int64_t out_size, int64_t k, const int32_t* u_idx, const void* u_vals,
+                      const uint32_t* mask, int32_t* out_idx, void* out_vals, int64_t* count,
+                      int64_t* counters) {
+  if (a->dtype == GB_I64)
+    return push_t<int64_t>(ctx, add_op, mult_op, a, out_size, k, u_idx, (const int64_t*)u_vals,
+                           mask, out_idx, (int64_t*)out_vals, count, counters);
+  return push_t<double>(ctx, add_op, mult_op, a, out_size, k, u_idx, (const double*)u_vals, mask,
+                        out_idx, (double*)out_vals, count, counters);
+}
+
+}  // extern "C"

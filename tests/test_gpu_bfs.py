@@ -1,0 +1,179 @@
+"""GPU parity: R-MAT generator and fused BFS against the reference goldens and the C oracle."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from golden_io import load_json
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gb():
+    import paper_1908_01407_b200 as gb
+    return gb
+
+
+def csr_digest(rp, ci):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(rp, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(ci, dtype=np.int64).tobytes())
+    return h.hexdigest()
+
+
+def digest(vec):
+    idx, vals = vec.extract_tuples()
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(idx).tobytes())
+    h.update(np.ascontiguousarray(np.round(np.asarray(vals, dtype=np.float64), 9)).tobytes())
+    return h.hexdigest()
+
+
+def trace(desc):
+    return [[d.chosen, d.frontier_nvals, d.estimated_frontier_edges, d.threshold_edges]
+            for d in desc.direction_log]
+
+
+@pytest.mark.parametrize("key", ["rmat_s8", "rmat_s10", "rmat_s12", "rmat_s14", "rmat_s16",
+                                 "uniform_s8", "uniform_s10", "uniform_s12", "uniform_s14"])
+def test_generator_matches_reference(gb, key):
+    g = load_json("rmat_graphs.json")["graphs"][key]
+    kw = dict(a=0.25, b=0.25, c=0.25, d=0.25) if key.startswith("uniform") else {}
+    A = gb.io.rmat_matrix(g["scale"], **kw)
+    assert A.nnz == g["nnz"]
+    assert csr_digest(A.row_offsets, A.col_indices) == g["csr"]
+    assert A.is_symmetric()
+    if g["weights"] is not None:
+        W = gb.io.rmat_matrix(g["scale"], weighted=True, **kw)
+        assert hashlib.sha256(W.csr_values.tobytes()).hexdigest() == g["weights"]
+
+
+@pytest.mark.parametrize("s", [8, 10, 12, 14, 16])
+def test_bfs_golden(gb, s):
+    gold = load_json("algorithms.json")
+    A = gb.io.rmat_matrix(s)
+    desc = gb.Descriptor()
+    lv = gb.bfs(A, 0, desc=desc)
+    assert digest(lv) == gold[f"bfs_s{s}"]["digest"]
+    assert trace(desc) == gold[f"bfs_s{s}"]["trace"]
+    if "values" in gold[f"bfs_s{s}"]:
+        assert lv.values.tolist() == gold[f"bfs_s{s}"]["values"]
+    other = [k for k in gold if k.startswith(f"bfs_s{s}_src")][0]
+    src = gold[other]["source"]
+    desc = gb.Descriptor()
+    lv = gb.bfs(A, src, desc=desc)
+    assert digest(lv) == gold[other]["digest"]
+    assert trace(desc) == gold[other]["trace"]
+
+
+@pytest.mark.parametrize("s", [10, 12])
+def test_bfs_uniform_golden(gb, s):
+    gold = load_json("algorithms.json")[f"uniform_bfs_s{s}"]
+    A = gb.io.rmat_matrix(s, a=0.25, b=0.25, c=0.25, d=0.25)
+    desc = gb.Descriptor()
+    assert digest(gb.bfs(A, 0, desc=desc)) == gold["digest"]
+    assert trace(desc) == gold["trace"]
+
+
+@pytest.mark.parametrize("s", [18, 20])
+def test_bfs_matches_c_oracle(gb, s):
+    from oracle import cgraph
+    A = gb.io.rmat_matrix(s)
+    rp, ci = cgraph.rmat_csr(s)
+    assert np.array_equal(A.row_offsets, rp) and np.array_equal(A.col_indices, ci)
+    for src in (0, 1, int(np.argmax(np.diff(rp) == 1))):
+        desc = gb.Descriptor()
+        lv = gb.bfs(A, src, desc=desc)
+        want, tr = cgraph.bfs(rp, ci, src)
+        assert np.array_equal(lv.values, want)
+        assert [(d.chosen, d.frontier_nvals, d.estimated_frontier_edges) for d in desc.direction_log] == tr
+
+
+def test_bfs_s24_properties(gb):
+    """Size-independent checks at the benchmark scale (SURVEY §8 input table)."""
+    from oracle import cgraph
+    import torch
+    A = gb.io.rmat_matrix(24)
+    assert A.nnz == 520_756_042
+    deg = torch.diff(A._csr.offsets)
+    assert int(deg.max()) == 405_970 and int(deg.argmax()) == 0
+    assert int((deg == 0).sum()) == 7_906_093
+    desc = gb.Descriptor()
+    lv = gb.bfs(A, 0, desc=desc)
+    vals = lv.values
+    assert int(np.count_nonzero(vals)) == 8_865_184
+    assert [d.chosen for d in desc.direction_log] == ["push", "push", "pull", "push", "push", "push"]
+    assert [d.frontier_nvals for d in desc.direction_log] == [1, 405_970, 7_612_546, 843_624, 3_034, 9]
+    rp = A._csr.offsets.cpu().numpy()
+    ci = A._csr.indices.cpu().numpy()
+    want, _ = cgraph.bfs(rp, ci, 0)
+    assert np.array_equal(vals, want)
+
+
+# ---------------------------------------------------------------------------
+# edge cases the reference semantics define
+# ---------------------------------------------------------------------------
+
+
+def test_bfs_isolated_source(gb):
+    A = gb.matrix_build([(1, 2, 1), (2, 1, 1)], 4, 4)
+    desc = gb.Descriptor()
+    lv = gb.bfs(A, 0, desc=desc)
+    assert lv.values.tolist() == [1, 0, 0, 0]
+    assert [d.chosen for d in desc.direction_log] == ["push"]
+
+
+def test_bfs_path_graph_spec_example(gb):
+    # SPEC example: path 0-1-2 from 0 gives [1, 2, 3]
+    A = gb.matrix_build([(0, 1, 1), (1, 0, 1), (1, 2, 1), (2, 1, 1)], 3, 3)
+    assert gb.bfs(A, 0).values.tolist() == [1, 2, 3]
+
+
+def test_bfs_directed_graph_uses_both_orientations(gb):
+    from oracle import port
+    rng = np.random.default_rng(5)
+    n = 300
+    r = rng.integers(0, n, 3000)
+    c = rng.integers(0, n, 3000)
+    A = gb.SparseMatrix.from_tuples(r, c, np.ones(r.size, np.int64), n, n)
+    assert not A.is_symmetric()
+    P = port.mat_from_tuples(r, c, np.ones(r.size, np.int64), n, n)
+    for policy in (gb.Direction.AUTO, gb.Direction.FORCE_PUSH, gb.Direction.FORCE_PULL):
+        desc = gb.Descriptor(direction=policy)
+        got = gb.bfs(A, 3, desc=desc)
+        pd = port.Desc(direction=policy.value)
+        want = port.bfs(P, 3, pd)
+        assert np.array_equal(got.values, want.vals)
+        assert [d.chosen for d in desc.direction_log] == [x[0] for x in pd.log]
+
+
+def test_bfs_max_niter_cap(gb):
+    from oracle import port
+    A = gb.io.rmat_matrix(10)
+    rp, ci, n = port.rmat_csr(10)
+    P = port.mat_from_csr(rp, ci, np.ones(ci.size, np.int64), n)
+    for cap in (1, 2, 3):
+        desc = gb.Descriptor(max_niter=cap)
+        got = gb.bfs(A, 0, desc=desc)
+        pd = port.Desc(max_niter=cap)
+        want = port.bfs(P, 0, pd)
+        assert np.array_equal(got.values, want.vals)
+        assert len(desc.direction_log) == len(pd.log)
+
+
+def test_bfs_zero_valued_edges_do_not_propagate(gb):
+    # LogicalAnd(0, 1) is false: a stored 0 is not an edge for traversal
+    A = gb.matrix_build([(0, 1, 0), (1, 0, 0), (0, 2, 1), (2, 0, 1), (2, 3, 5), (3, 2, 5)], 4, 4)
+    assert gb.bfs(A, 0).values.tolist() == [1, 0, 2, 3]
+    for policy in (gb.Direction.FORCE_PUSH, gb.Direction.FORCE_PULL):
+        assert gb.bfs(A, 0, gb.Descriptor(direction=policy)).values.tolist() == [1, 0, 2, 3]
+
+
+def test_bfs_bad_source(gb):
+    A = gb.io.rmat_matrix(6)
+    with pytest.raises(IndexError):
+        gb.bfs(A, 64)
+    with pytest.raises(gb.ShapeError):
+        gb.bfs(gb.matrix_build([(0, 1, 1)], 2, 3), 0)
