@@ -21,6 +21,8 @@
 #include "gb_common.cuh"
 #include "gb_lbs.cuh"
 
+#include <cub/cub.cuh>
+
 namespace gb {
 
 // A stored entry participates in LogicalAnd(a, u) iff a != 0.
@@ -34,132 +36,365 @@ struct EdgeOn {
   }
 };
 
-struct PushMark {
+// ---------------------------------------------------------------------------
+// push: load-balanced expansion of the frontier's out-edges
+// ---------------------------------------------------------------------------
+constexpr int kExpThreads = 256;
+constexpr int kExpItems = 16;
+constexpr int kExpTile = kExpThreads * kExpItems;  // 4096 edges per tile
+constexpr int kExpVcap = 1024;                     // frontier entries per tile (owner-map path)
+static_assert(kExpTile == kLbsTile, "tile_first is computed for kLbsTile");
+
+// One CTA per tile of kExpTile consecutive expansion slots.  Owner lookup is a
+// shared-memory table built by marking each frontier entry's first slot and a
+// block-wide max-scan, so every edge costs one LDS for its owner and its column
+// index load is coalesced with its neighbours'.  The 16 column loads of a
+// thread are issued before any probe (memory-level parallelism).
+// Marking: the live visited bitmap `vbm` is probed through L2 (ld.cg, always
+// current) and a clear bit is set with one atomicOr, so a vertex reached by
+// many frontier edges costs one read per edge but (almost) one write in total.
+// bfs_finalize recovers the new frontier as vbm & ~vprev.
+__device__ __forceinline__ void mark(uint32_t* vbm, int32_t v, uint32_t word) {
+  const uint32_t bit = 1u << (v & 31);
+  if (!(word & bit)) atomicOr(vbm + (v >> 5), bit);
+}
+
+template <bool VALS>
+__global__ void __launch_bounds__(kExpThreads, 4)
+bfs_expand(int64_t K, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
+           const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx, EdgeOn on,
+           uint32_t* __restrict__ vbm) {
+  using BlockScan = cub::BlockScan<int, kExpThreads>;
+  __shared__ int64_t s_delta[kExpVcap];
+  __shared__ __align__(16) uint16_t s_own[kExpTile];
+  __shared__ typename BlockScan::TempStorage s_scan;
+  const int tid = threadIdx.x;
+  const int64_t E = S[K];
+  const int64_t ntiles = (E + kExpTile - 1) / kExpTile;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t e0 = t * kExpTile;
+    const int64_t e1 = e0 + kExpTile < E ? e0 + kExpTile : E;
+    const int64_t k0 = tile_first[t];
+    const int64_t k1 = t + 1 < ntiles ? tile_first[t + 1] : K - 1;
+    const int64_t nk = k1 - k0 + 1;
+    if (nk <= kExpVcap) {
+      uint4* own4 = reinterpret_cast<uint4*>(s_own);
+      own4[2 * tid] = make_uint4(0, 0, 0, 0);
+      own4[2 * tid + 1] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+      for (int64_t i = tid; i < nk; i += kExpThreads) {
+        const int64_t k = k0 + i;
+        const int64_t sk = S[k], sk1 = S[k + 1];
+        s_delta[i] = rowstart[k] - sk;
+        if (sk1 > sk) {
+          const int64_t st = (sk > e0 ? sk : e0) - e0;
+          if (st < e1 - e0) s_own[st] = (uint16_t)(i + 1);
+        }
+      }
+      __syncthreads();
+      // block max-scan over s_own: thread tid owns slots [16 tid, 16 tid + 16)
+      uint4 a = own4[2 * tid], b = own4[2 * tid + 1];
+      uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      int run = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        run = max(run, (int)(wv[j] & 0xffffu));
+        run = max(run, (int)(wv[j] >> 16));
+      }
+      int pre;
+      BlockScan(s_scan).ExclusiveScan(run, pre, 0, cub::Max());
+      run = pre;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int lo16 = max(run, (int)(wv[j] & 0xffffu));
+        int hi16 = max(lo16, (int)(wv[j] >> 16));
+        run = hi16;
+        wv[j] = (uint32_t)lo16 | ((uint32_t)hi16 << 16);
+      }
+      __syncthreads();
+      own4[2 * tid] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      own4[2 * tid + 1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+      __syncthreads();
+#pragma unroll
+      for (int half = 0; half < kExpItems; half += kExpItems / 2) {
+        constexpr int B = kExpItems / 2;
+        int32_t v[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+          const int el = (half + r) * kExpThreads + tid;
+          v[r] = -1;
+          if (e0 + el < e1) {
+            const int i = (int)s_own[el] - 1;
+            const int64_t p = s_delta[i] + e0 + el;
+            const int32_t c = ld_stream(idx + p);
+            v[r] = (!VALS || on(p)) ? c : -1;
+          }
+        }
+        uint32_t word[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) word[r] = v[r] >= 0 ? ld_probe(vbm + (v[r] >> 5)) : ~0u;
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+          if (v[r] >= 0) mark(vbm, v[r], word[r]);
+      }
+      __syncthreads();
+    } else {
+      // many tiny adjacency lists in one tile: one thread per frontier entry
+      for (int64_t i = tid; i < nk; i += kExpThreads) {
+        const int64_t k = k0 + i;
+        const int64_t sk = S[k], sk1 = S[k + 1];
+        const int64_t lo = sk > e0 ? sk : e0;
+        const int64_t hi = sk1 < e1 ? sk1 : e1;
+        const int64_t base = rowstart[k] - sk;
+        for (int64_t e = lo; e < hi; ++e) {
+          const int64_t p = base + e;
+          const int32_t u = __ldg(idx + p);
+          if (!VALS || on(p)) mark(vbm, u, ld_probe(vbm + (u >> 5)));
+        }
+      }
+    }
+  }
+}
+
+// Warp-tile push expansion (no shared memory, no barriers): a batch of
+// column loads is issued before any visited probe.
+template <bool VALS>
+struct PushBits {
   const int32_t* __restrict__ idx;
   EdgeOn on;
-  const uint32_t* __restrict__ vbm;
-  uint8_t* __restrict__ nf;
-  __device__ __forceinline__ void operator()(int64_t k, int64_t p, int64_t e) const {
-    const int32_t v = __ldg(idx + p);
-    if (!on(p)) return;
-    if ((__ldg(vbm + (v >> 5)) >> (v & 31)) & 1u) return;
-    nf[v] = 1;
+  uint32_t* __restrict__ vbm;
+  template <int B>
+  __device__ __forceinline__ void batch(const int64_t (&p)[B], const bool (&live)[B]) {
+    int32_t v[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      v[r] = -1;
+      if (live[r]) {
+        const int32_t c = ld_stream(idx + p[r]);
+        v[r] = (!VALS || on(p[r])) ? c : -1;
+      }
+    }
+    uint32_t word[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) word[r] = v[r] >= 0 ? ld_probe(vbm + (v[r] >> 5)) : ~0u;
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+      if (v[r] >= 0) mark(vbm, v[r], word[r]);
+  }
+  __device__ __forceinline__ void visit(int64_t p) {
+    const int32_t u = ld_stream(idx + p);
+    if (!VALS || on(p)) mark(vbm, u, ld_probe(vbm + (u >> 5)));
   }
 };
 
-__global__ void bfs_init(int64_t source, int64_t* levels, uint32_t* vbm, uint32_t* fbm,
-                         int32_t* F) {
+template <bool VALS>
+__global__ void __launch_bounds__(256)
+bfs_expand_warp(int64_t K, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
+                const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
+                EdgeOn on, uint32_t* __restrict__ vbm) {
+  PushBits<VALS> f{idx, on, vbm};
+  warp_tiles(K, S, rowstart, tile_first, f);
+}
+
+__global__ void bfs_init(int64_t source, int64_t* levels, uint32_t* vbm, uint32_t* vprev,
+                         uint32_t* fbm, int32_t* F) {
   levels[source] = 1;
   vbm[source >> 5] |= 1u << (source & 31);
+  vprev[source >> 5] |= 1u << (source & 31);
   fbm[source >> 5] |= 1u << (source & 31);
   F[0] = (int32_t)source;
 }
 
-// One thread per 32-vertex word: mark bytes -> next frontier.
-__global__ void bfs_finalize(int64_t n, int64_t depth, uint8_t* __restrict__ nf,
-                             uint32_t* __restrict__ vbm, uint32_t* __restrict__ fbm_next,
-                             int64_t* __restrict__ levels, int32_t* __restrict__ F,
-                             unsigned long long* __restrict__ count,
-                             unsigned long long* __restrict__ count_clear) {
+// Warp per 32 words (1024 vertices): lane l diffs word w0+l of the live
+// visited bitmap against the level-start snapshot, then the warp walks the
+// non-empty words so level stamps and frontier-list writes are coalesced.
+__global__ void __launch_bounds__(256)
+bfs_finalize(int64_t n, int64_t depth, const uint32_t* __restrict__ vbm,
+             uint32_t* __restrict__ vprev, uint32_t* __restrict__ fbm_next,
+             int64_t* __restrict__ levels, int32_t* __restrict__ F,
+             unsigned long long* __restrict__ count,
+             unsigned long long* __restrict__ count_clear) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
+  const int lane = threadIdx.x & 31;
   const int64_t W = (n + 31) / 32;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint4* p = reinterpret_cast<uint4*>(nf + w * 32);
-    uint4 a = p[0], b = p[1];
+  const int64_t G = (W + 31) / 32;
+  const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = g0; g < G; g += ng) {
+    const int64_t w = g * 32 + lane;
     uint32_t bits = 0;
-    if ((a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) != 0) {
-      uint32_t q[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if ((q[j] >> (8 * c)) & 0xffu) bits |= 1u << (4 * j + c);
-      p[0] = make_uint4(0, 0, 0, 0);
-      p[1] = make_uint4(0, 0, 0, 0);
-      bits &= ~vbm[w];
-      vbm[w] |= bits;
+    if (w < W) {
+      const uint32_t cur = vbm[w], old = vprev[w];
+      bits = cur & ~old;
+      if (bits) vprev[w] = cur;
+      fbm_next[w] = bits;
     }
-    fbm_next[w] = bits;
-    int c = __popc(bits);
-    long long slot = warp_reserve(count, c);
-    while (bits) {
-      int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      int64_t v = w * 32 + b;
-      levels[v] = depth;
-      F[slot++] = (int32_t)v;
+    // frontier list slots for the whole group, in word order
+    const int c = __popc(bits);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(GB_FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(GB_FULL, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total) base = atomicAdd(count, (unsigned long long)total);
+    base = __shfl_sync(GB_FULL, base, 31);
+    uint32_t nonzero = __ballot_sync(GB_FULL, bits != 0);
+    while (nonzero) {
+      const int j = __ffs(nonzero) - 1;
+      nonzero &= nonzero - 1;
+      const uint32_t wb = __shfl_sync(GB_FULL, bits, j);
+      const int start = __shfl_sync(GB_FULL, incl - c, j);
+      if ((wb >> lane) & 1u) {
+        const int64_t v = (g * 32 + j) * 32 + lane;
+        levels[v] = depth;
+        F[base + start + __popc(wb & ((1u << lane) - 1u))] = (int32_t)v;
+      }
     }
   }
 }
 
-// Pull: warp per word of 32 candidate rows; lane = row.
-constexpr int kPullSerial = 8;  // entries a lane scans alone before the warp helps
+// ---------------------------------------------------------------------------
+// pull: warp per 32 words; candidate rows are compacted into a shared list
+// and processed 8 per lane with their first loads batched
+// ---------------------------------------------------------------------------
+constexpr int kPullBatch = 8;                // rows per lane per pass
+constexpr int kPullList = 32 * kPullBatch;   // rows per warp per pass
+constexpr int kPullSerial = 8;               // entries a lane scans alone before the warp helps
 
 __global__ void __launch_bounds__(256)
 bfs_pull(int64_t n, int64_t depth, const int64_t* __restrict__ off,
          const int32_t* __restrict__ idx, EdgeOn on, const uint32_t* __restrict__ nonempty,
-         uint32_t* __restrict__ vbm, const uint32_t* __restrict__ fbm,
+         uint32_t* __restrict__ vbm, uint32_t* __restrict__ vprev, const uint32_t* __restrict__ fbm,
          uint32_t* __restrict__ fbm_next, int64_t* __restrict__ levels,
          int32_t* __restrict__ F, unsigned long long* __restrict__ count,
          unsigned long long* __restrict__ count_clear) {
+  __shared__ int32_t s_list[8][kPullList];
+  __shared__ uint32_t s_new[8][32];
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
   const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
   const int64_t W = (n + 31) / 32;
-  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = warp0; w < W; w += nwarps) {
-    const uint32_t cand = ~vbm[w] & __ldg(nonempty + w);
-    uint32_t found = 0;
-    if (cand) {
-      const int64_t v = w * 32 + lane;
-      bool mine = (cand >> lane) & 1u;
-      int64_t p = 0, hi = 0;
-      bool hit = false;
-      if (mine) {
-        p = __ldg(off + v);
-        hi = __ldg(off + v + 1);
-        int64_t stop = p + kPullSerial < hi ? p + kPullSerial : hi;
-        for (; p < stop; ++p) {
-          const int32_t j = __ldg(idx + p);
-          if (((__ldg(fbm + (j >> 5)) >> (j & 31)) & 1u) && on(p)) { hit = true; break; }
+  const int64_t G = (W + 31) / 32;
+  const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int32_t* list = s_list[wid];
+  uint32_t* nw = s_new[wid];
+  for (int64_t g = g0; g < G; g += ng) {
+    const int64_t w = g * 32 + lane;
+    uint32_t rem = w < W ? (~vbm[w] & __ldg(nonempty + w)) : 0u;
+    nw[lane] = 0;
+    __syncwarp();
+    while (true) {
+      const int c = __popc(rem);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(GB_FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(GB_FULL, incl, 31);
+      if (total == 0) break;
+      int slot = incl - c;
+      while (rem && slot < kPullList) {
+        const int b = __ffs(rem) - 1;
+        rem &= rem - 1;
+        list[slot++] = (int32_t)(w * 32 + b);
+      }
+      __syncwarp();
+      const int take = total < kPullList ? total : kPullList;
+      int64_t lo[kPullBatch], hi[kPullBatch];
+      int32_t v[kPullBatch];
+#pragma unroll
+      for (int r = 0; r < kPullBatch; ++r) {
+        const int q = r * 32 + lane;
+        v[r] = q < take ? list[q] : -1;
+        lo[r] = hi[r] = 0;
+        if (v[r] >= 0) {
+          lo[r] = __ldg(off + v[r]);
+          hi[r] = __ldg(off + v[r] + 1);
         }
       }
-      // rows still unresolved after the serial phase: the warp scans them together
-      uint32_t todo = __ballot_sync(GB_FULL, mine && !hit && p < hi);
-      while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        int64_t q = __shfl_sync(GB_FULL, p, src);
-        const int64_t qhi = __shfl_sync(GB_FULL, hi, src);
-        bool h = false;
-        for (q += lane; ; q += 32) {
-          bool mh = false;
-          if (q < qhi) {
-            const int32_t j = __ldg(idx + q);
-            mh = ((__ldg(fbm + (j >> 5)) >> (j & 31)) & 1u) && on(q);
+      int32_t j0[kPullBatch];
+#pragma unroll
+      for (int r = 0; r < kPullBatch; ++r) j0[r] = lo[r] < hi[r] ? __ldg(idx + lo[r]) : 0;
+      uint32_t todo = 0;
+#pragma unroll
+      for (int r = 0; r < kPullBatch; ++r) {
+        bool hit = false;
+        if (lo[r] < hi[r]) {
+          hit = ((__ldg(fbm + (j0[r] >> 5)) >> (j0[r] & 31)) & 1u) && on(lo[r]);
+          int64_t p = lo[r] + 1;
+          const int64_t stop = lo[r] + kPullSerial < hi[r] ? lo[r] + kPullSerial : hi[r];
+          for (; !hit && p < stop; ++p) {
+            const int32_t j = __ldg(idx + p);
+            hit = ((__ldg(fbm + (j >> 5)) >> (j & 31)) & 1u) && on(p);
           }
-          const uint32_t any = __ballot_sync(GB_FULL, mh);
-          if (any) { h = true; break; }
-          if (__shfl_sync(GB_FULL, q, 0) + 32 >= qhi) break;
+          lo[r] = p;
+          if (!hit && p < hi[r]) todo |= 1u << r;
         }
-        if (lane == src) hit = h;
+        if (hit) {
+          atomicOr(&nw[(v[r] >> 5) - g * 32], 1u << (v[r] & 31));
+          levels[v[r]] = depth;
+        }
       }
-      found = __ballot_sync(GB_FULL, hit);
-      if (hit) levels[v] = depth;
+      // long rows still unresolved: the warp scans them together
+      for (int r = 0; r < kPullBatch; ++r) {
+        uint32_t lanes = __ballot_sync(GB_FULL, (todo >> r) & 1u);
+        while (lanes) {
+          const int src = __ffs(lanes) - 1;
+          lanes &= lanes - 1;
+          const int64_t qlo = __shfl_sync(GB_FULL, lo[r], src);
+          const int64_t qhi = __shfl_sync(GB_FULL, hi[r], src);
+          const int32_t vv = __shfl_sync(GB_FULL, v[r], src);
+          bool h = false;
+          for (int64_t base = qlo; base < qhi && !h; base += 32) {
+            const int64_t q = base + lane;
+            bool mh = false;
+            if (q < qhi) {
+              const int32_t j = __ldg(idx + q);
+              mh = ((__ldg(fbm + (j >> 5)) >> (j & 31)) & 1u) && on(q);
+            }
+            h = __ballot_sync(GB_FULL, mh) != 0;
+          }
+          if (h && lane == src) {
+            atomicOr(&nw[(vv >> 5) - g * 32], 1u << (vv & 31));
+            levels[vv] = depth;
+          }
+        }
+      }
+      __syncwarp();
     }
-    if (lane == 0) {
-      fbm_next[w] = found;
-      if (found) vbm[w] |= found;
+    __syncwarp();
+    const uint32_t bits = nw[lane];
+    if (w < W) {
+      fbm_next[w] = bits;
+      if (bits) {
+        vbm[w] |= bits;
+        vprev[w] |= bits;
+      }
     }
-    const int c = lane == 0 ? __popc(found) : 0;
-    long long base = 0;
-    if (lane == 0 && c) base = (long long)atomicAdd(count, (unsigned long long)c);
-    base = __shfl_sync(GB_FULL, base, 0);
-    if ((found >> lane) & 1u) {
-      const int rank = __popc(found & ((1u << lane) - 1u));
-      F[base + rank] = (int32_t)(w * 32 + lane);
+    const int c = __popc(bits);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(GB_FULL, incl, o);
+      if (lane >= o) incl += y;
     }
+    const int total = __shfl_sync(GB_FULL, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total) base = atomicAdd(count, (unsigned long long)total);
+    base = __shfl_sync(GB_FULL, base, 31);
+    int slot = incl - c;
+    uint32_t b2 = bits;
+    while (b2) {
+      const int b = __ffs(b2) - 1;
+      b2 &= b2 - 1;
+      F[base + slot++] = (int32_t)(w * 32 + b);
+    }
+    __syncwarp();
   }
 }
 
@@ -200,15 +435,15 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
   uint32_t* vbm = ar.alloc<uint32_t>(W);
   uint32_t* fbm[2] = {ar.alloc<uint32_t>(W), ar.alloc<uint32_t>(W)};
   int32_t* F = ar.alloc<int32_t>(n);
-  uint8_t* nf = ar.alloc<uint8_t>(W * 32);
+  uint32_t* vprev = ar.alloc<uint32_t>(W);
   unsigned long long* cnt = ar.alloc<unsigned long long>(2);
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cudaMemsetAsync(levels, 0, sizeof(int64_t) * n, s));
   GB_CUDA(ctx, cudaMemsetAsync(vbm, 0, sizeof(uint32_t) * W, s));
   GB_CUDA(ctx, cudaMemsetAsync(fbm[0], 0, sizeof(uint32_t) * W, s));
-  GB_CUDA(ctx, cudaMemsetAsync(nf, 0, (size_t)W * 32, s));
+  GB_CUDA(ctx, cudaMemsetAsync(vprev, 0, sizeof(uint32_t) * W, s));
   GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
-  bfs_init<<<1, 1, 0, s>>>(source, levels, vbm, fbm[0], F);
+  bfs_init<<<1, 1, 0, s>>>(source, levels, vbm, vprev, fbm[0], F);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 6);  // 5 memsets + init
 
@@ -234,10 +469,10 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
         GB_CUDA(ctx, cudaMemsetAsync(c, 0, 8, s));
         GB_CUDA(ctx, cudaMemsetAsync(c_next, 0, 8, s));
       } else {
-        const int grid = grid_for(ctx, W * 32, 256, 16);
+        const int grid = grid_for(ctx, W, 256, 8);
         const int ps = prof_begin(ctx, PROF_BFS_PULL, K);
         bfs_pull<<<grid, 256, 0, s>>>(n, depth + 1, pull->offsets, pull->indices, pull_on,
-                                      pull_nonempty, vbm, fbm[cur], fbm[cur ^ 1], levels, F,
+                                      pull_nonempty, vbm, vprev, fbm[cur], fbm[cur ^ 1], levels, F,
                                       c, c_next);
         prof_end(ctx, ps);
         count_launch(ctx, 1);
@@ -245,16 +480,19 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     } else {
       if (!push_dead) {
         LbsPlan plan;
-        GB_TRY(lbs_prepare(ctx, ar, K, F, push->offsets, push->nnz, &plan));
-        PushMark f{push->indices, push_on, vbm, nf};
+        GB_TRY(lbs_prepare(ctx, ar, K, F, push->offsets, push->nnz, &plan, kWarpTile));
         const int ps = prof_begin(ctx, PROF_BFS_PUSH, K);
-        lbs_expand<PushMark><<<plan.grid, kLbsThreads, 0, s>>>(K, plan.S, plan.rowstart,
-                                                                plan.tile_first, f);
+        if (push->values)
+          bfs_expand_warp<true><<<resident_grid(ctx, bfs_expand_warp<true>, 256), 256, 0, s>>>(K, plan.S, plan.rowstart, plan.tile_first,
+                                                  push->indices, push_on, vbm);
+        else
+          bfs_expand_warp<false><<<resident_grid(ctx, bfs_expand_warp<false>, 256), 256, 0, s>>>(K, plan.S, plan.rowstart, plan.tile_first,
+                                                   push->indices, push_on, vbm);
         prof_end(ctx, ps);
         count_launch(ctx, 5);  // degrees, scan (2), tile_first, expand
       }
       const int pf = prof_begin(ctx, PROF_BFS_FINALIZE, K);
-      bfs_finalize<<<grid_for(ctx, W, 256), 256, 0, s>>>(n, depth + 1, nf, vbm, fbm[cur ^ 1],
+      bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, depth + 1, vbm, vprev, fbm[cur ^ 1],
                                                          levels, F, c, c_next);
       prof_end(ctx, pf);
       count_launch(ctx, 1);

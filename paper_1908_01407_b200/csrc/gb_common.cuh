@@ -246,6 +246,19 @@ __device__ __forceinline__ long long warp_reserve(unsigned long long* counter, i
   return (long long)base + pre - want;
 }
 
+// streaming read-only load that does not allocate in L1 (column-index streams)
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+// L1-cached probe of a word other threads may be setting (staleness is benign)
+__device__ __forceinline__ uint32_t ld_probe(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.ca.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ bool bit_test(const uint32_t* bm, int64_t i) {
   return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
 }
@@ -277,6 +290,16 @@ int sm_count(gb_ctx* ctx);
 // pinned host scratch for small device->host reads (>= 64 int64 slots)
 int64_t* pinned_slots(gb_ctx* ctx);
 gb_status read_i64(gb_ctx* ctx, const int64_t* dptr, int64_t* out, int count = 1);
+
+// grid that fills every SM exactly once at the kernel's achievable occupancy
+template <class Kernel>
+inline int resident_grid(gb_ctx* ctx, Kernel kernel, int block, size_t smem = 0) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  return per_sm * sm_count(ctx);
+}
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

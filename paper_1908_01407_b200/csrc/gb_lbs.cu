@@ -17,26 +17,26 @@ __global__ void lbs_degrees(int64_t K, const int32_t* __restrict__ ids,
   if (blockIdx.x == 0 && threadIdx.x == 0) deg[K] = 0;
 }
 
-__global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S,
+__global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S, int64_t tile,
                                int32_t* __restrict__ tile_first) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = S[k], b = S[k + 1];
     if (b <= a) continue;
     // tiles whose first edge t*TE lies in [a, b)
-    int64_t t = (a + kLbsTile - 1) / kLbsTile;
-    for (; t * kLbsTile < b; ++t) tile_first[t] = (int32_t)k;
+    int64_t t = (a + tile - 1) / tile;
+    for (; t * tile < b; ++t) tile_first[t] = (int32_t)k;
   }
 }
 
 gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
-                      const int64_t* off, int64_t max_edges, LbsPlan* plan) {
+                      const int64_t* off, int64_t max_edges, LbsPlan* plan, int64_t tile) {
   cudaStream_t s = stream_of(ctx);
   plan->K = K;
   plan->rowstart = ar.alloc<int64_t>(K + 1);
   int64_t* deg = ar.alloc<int64_t>(K + 1);
   plan->S = ar.alloc<int64_t>(K + 1);
-  plan->tile_first = ar.alloc<int32_t>(max_edges / kLbsTile + 2);
+  plan->tile_first = ar.alloc<int32_t>(max_edges / tile + 2);
   GB_ARENA_CHECK(ctx, ar);
   lbs_degrees<<<grid_for(ctx, K + 1, 256), 256, 0, s>>>(K, ids, off, plan->rowstart, deg);
   size_t tb = 0;
@@ -44,7 +44,7 @@ gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
   void* tmp = ar.raw(tb);
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, deg, plan->S, K + 1, s));
-  lbs_tile_first<<<grid_for(ctx, K, 256), 256, 0, s>>>(K, plan->S, plan->tile_first);
+  lbs_tile_first<<<grid_for(ctx, K, 256), 256, 0, s>>>(K, plan->S, tile, plan->tile_first);
   GB_LAUNCH_CHECK(ctx);
   plan->grid = sm_count(ctx) * 4;
   return GB_OK;

@@ -26,7 +26,7 @@ __global__ void lbs_degrees(int64_t K, const int32_t* __restrict__ ids,
 
 // S = exclusive scan of deg (K+1 entries, S[K] = E); tile_first[t] = the
 // frontier entry whose range contains edge t*TE.
-__global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S,
+__global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S, int64_t tile,
                                int32_t* __restrict__ tile_first);
 
 // Expansion kernel.  f(k, p, e) is called once per edge e of the expansion,
@@ -93,6 +93,75 @@ struct LbsPlan {
 };
 
 gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
-                      const int64_t* off, int64_t max_edges, LbsPlan* plan);
+                      const int64_t* off, int64_t max_edges, LbsPlan* plan,
+                      int64_t tile = kLbsTile);
+
+// ---------------------------------------------------------------------------
+// Warp tiles: each warp owns kWarpTile consecutive expansion slots and finds
+// the owner of each slot by a 5-step binary search over the (at most 32)
+// frontier entries of the tile, held one per lane and read with shuffles --
+// no shared memory and no block barriers.  Tiles that touch more than 32
+// frontier entries (many tiny adjacency lists) walk them one lane per entry.
+// f.visit(k, p) is called for every edge; F must provide
+//   template <int B> void batch(const int64_t (&p)[B], const bool (&live)[B])
+// for the batched fast path.
+// ---------------------------------------------------------------------------
+constexpr int kWarpItems = 16;
+constexpr int kWarpTile = 32 * kWarpItems;  // 512 slots
+
+template <class F>
+__device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* __restrict__ S,
+                                           const int64_t* __restrict__ rowstart,
+                                           const int32_t* __restrict__ tile_first, F& f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t E = S[K];
+  const int64_t ntiles = (E + kWarpTile - 1) / kWarpTile;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = w0; t < ntiles; t += nw) {
+    const int64_t e0 = t * kWarpTile;
+    const int64_t e1 = e0 + kWarpTile < E ? e0 + kWarpTile : E;
+    const int64_t k0 = tile_first[t];
+    const int64_t k1 = t + 1 < ntiles ? tile_first[t + 1] : K - 1;
+    const int64_t nk = k1 - k0 + 1;
+    if (nk <= 32) {
+      int64_t st = INT64_MAX, base = 0;
+      if (lane < nk) {
+        st = S[k0 + lane];
+        base = rowstart[k0 + lane] - st;
+      }
+      // empty entries share their start with the next one; the search picks
+      // the last entry whose start is <= e, which is always non-empty
+#pragma unroll
+      for (int h = 0; h < kWarpItems; h += kWarpItems / 2) {
+        constexpr int B = kWarpItems / 2;
+        int64_t p[B];
+        bool live[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+          const int64_t e = e0 + (int64_t)(h + r) * 32 + lane;
+          live[r] = e < e1;
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int64_t sv = __shfl_sync(GB_FULL, st, (lo + step) & 31);
+            if (lo + step < 32 && sv <= e) lo += step;
+          }
+          p[r] = __shfl_sync(GB_FULL, base, lo) + e;
+        }
+        f.template batch<B>(p, live);
+      }
+    } else {
+      for (int64_t i = lane; i < nk; i += 32) {
+        const int64_t k = k0 + i;
+        const int64_t sk = S[k], sk1 = S[k + 1];
+        const int64_t lo = sk > e0 ? sk : e0;
+        const int64_t hi = sk1 < e1 ? sk1 : e1;
+        const int64_t b = rowstart[k] - sk;
+        for (int64_t e = lo; e < hi; ++e) f.visit(b + e);
+      }
+    }
+  }
+}
 
 }  // namespace gb
