@@ -184,6 +184,9 @@ gb_status gb_scatter_dense(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx
 gb_status gb_mask_bitmap(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx,
                          const void* vals, int32_t dtype, int32_t complement, uint32_t* out);
 
+/* number of set bits in the first n bits of a bitmap. Synchronizes. */
+gb_status gb_bitmap_count(gb_ctx* ctx, int64_t n, const uint32_t* bitmap, int64_t* count_host);
+
 /* bitmap of rows with at least one stored entry */
 gb_status gb_nonempty_rows(gb_ctx* ctx, int64_t n, const int64_t* offsets, uint32_t* out);
 
@@ -215,8 +218,120 @@ gb_status gb_mxv_push(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr
                       int64_t* count_host, int64_t* counters);
 
 /* ----------------------------------------------------------------------------
+ * masked matrix-matrix   (kernels.py:329-391)
+ * --------------------------------------------------------------------------*/
+
+/* mxm_masked: for every stored mask entry (i, j) whose value is non-zero,
+ * C(i,j) = fold over k in A(i,:) & B(:,j) of mult(A(i,k), B(k,j)).  `b` is the
+ * orientation whose row j is column j of B.  Entries with no match are kept
+ * (value = identity) only when the identity is non-zero.  Output is CSR in
+ * mask order (out_offsets: m->nrows+1; indices/values sized m->nnz).
+ * *nnz_host receives the kept count (synchronizes). */
+gb_status gb_mxm_masked(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                        const gb_csr* b, const gb_csr* m, int64_t* out_offsets,
+                        int32_t* out_indices, void* out_vals, int64_t* nnz_host,
+                        int64_t* counters);
+
+/* 1 when some row i stores column i (triangle_count check, algorithms.py:229-231). */
+gb_status gb_has_diagonal(gb_ctx* ctx, const gb_csr* a, int32_t* found_host);
+
+/* ----------------------------------------------------------------------------
+ * element-wise, assign, gather, apply, reduce   (kernels.py:422-665)
+ * --------------------------------------------------------------------------*/
+
+/* out[i] = mask[i] ? op(a[i], b[i] or *b_scalar_host) : *zero_host (swap: op(b, a)). */
+gb_status gb_ewise_dense(gb_ctx* ctx, int32_t op, int32_t dtype, int64_t n, const void* a,
+                         const void* b, const void* b_scalar_host, int32_t swap,
+                         const uint32_t* mask, const void* zero_host, void* out);
+
+/* ewise_add sparse+sparse (kernels.py:454-466): union of two sorted index
+ * sets; shared indices fold op(a, b), single entries fold alone (logical ops
+ * give 0/1).  Output sized ka+kb; *count_host = union size (synchronizes). */
+gb_status gb_union_sparse(gb_ctx* ctx, int32_t op, int32_t dtype, int64_t ka, const int32_t* ia,
+                          const void* va, int64_t kb, const int32_t* ib, const void* vb,
+                          int32_t* out_idx, void* out_vals, int64_t* count_host);
+
+/* ewise_mult sparse*sparse: op(a, b) on shared indices, then the mask. */
+gb_status gb_intersect_sparse(gb_ctx* ctx, int32_t op, int32_t dtype, int64_t ka,
+                              const int32_t* ia, const void* va, int64_t kb, const int32_t* ib,
+                              const void* vb, const uint32_t* mask, int32_t* out_idx,
+                              void* out_vals, int64_t* count_host);
+
+/* ewise_mult sparse*dense: out[i] = op(vals[i], dense[idx[i]]) (swap: op(dense, vals)). */
+gb_status gb_gather_pair(gb_ctx* ctx, int32_t op, int32_t dtype, int64_t k, const int32_t* idx,
+                         const void* vals, const void* dense, int32_t swap, void* out);
+
+/* _mask_sparse_result (kernels.py:414-419): keep sparse entries the mask allows. */
+gb_status gb_filter_mask(gb_ctx* ctx, int32_t dtype, int64_t k, const int32_t* idx,
+                         const void* vals, const uint32_t* mask, int32_t* out_idx, void* out_vals,
+                         int64_t* count_host);
+
+/* assign (kernels.py:519-535): w[i] = value where the mask allows (NULL = all). */
+gb_status gb_assign_scalar(gb_ctx* ctx, int32_t dtype, int64_t n, void* w,
+                           const void* value_host, const uint32_t* mask);
+
+/* 1 when some t[i] is outside [0, n). Synchronizes. */
+gb_status gb_check_bounds(gb_ctx* ctx, int64_t k, const int64_t* t, int64_t n, int32_t* bad_host);
+
+/* assign_scatter (kernels.py:538-583): w[tgt[i]] = min over colliding i of
+ * vals[i] (overwrite), targets filtered by the mask; GB_ERR_INDEX when a
+ * target is out of range. */
+gb_status gb_scatter_min(gb_ctx* ctx, int32_t dtype, int64_t n, void* w, int64_t k,
+                         const int64_t* tgt, const void* vals, const uint32_t* mask);
+
+/* extract_gather (kernels.py:586-619), dense source: out[i] = src[tgt[i]]. */
+gb_status gb_gather(gb_ctx* ctx, int32_t dtype, int64_t k, const int64_t* tgt, int64_t usize,
+                    const void* src, void* out);
+
+/* extract_gather with a sparse source: present[i] = tgt[i] is stored in u. */
+gb_status gb_gather_sparse(gb_ctx* ctx, int32_t dtype, int64_t k, const int64_t* tgt,
+                           int64_t usize, int64_t uk, const int32_t* uidx, const void* uval,
+                           int32_t* present, void* out);
+
+/* apply (kernels.py:622-639) for affine maps: out = in * scale + shift. */
+gb_status gb_apply_affine(gb_ctx* ctx, int32_t dtype, int64_t n, const void* in,
+                          const void* scale_host, const void* shift_host, void* out);
+
+/* reduce / reduce_scalar_matrix (kernels.py:642-647, 663-665): fold values
+ * (skipping those equal to *zero_host when given) into *out_host; the number
+ * of folded values goes to *count_host.  Synchronizes. */
+gb_status gb_reduce(gb_ctx* ctx, int32_t op, int32_t dtype, int64_t n, const void* vals,
+                    const void* zero_host, void* out_host, int64_t* count_host);
+
+/* reduce_rows (kernels.py:650-660): per-row fold, identity for empty rows. */
+gb_status gb_reduce_rows(gb_ctx* ctx, int32_t op, const gb_csr* a, void* out);
+
+/* ----------------------------------------------------------------------------
  * fused algorithms   (algorithms.py)
  * --------------------------------------------------------------------------*/
+
+/* Per-iteration host callback of the fused drivers (the sssp on_iteration hook). */
+typedef void (*gb_iter_cb)(int64_t iteration, void* user);
+
+/* sssp (algorithms.py:80-119): dist (float64[n]) receives the distances
+ * (+inf unreached).  Weights must be positive (checked by the caller). */
+gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t source,
+                  int64_t max_iters, double switch_ratio, int32_t policy, double* dist,
+                  int32_t* log_dir_host, int64_t* log_nvals_host, int64_t* log_est_host,
+                  int64_t* iters_host, gb_iter_cb cb, void* user);
+
+/* pagerank (algorithms.py:132-162): `pull` is the in-edge orientation (CSC of
+ * A), out_offsets the CSR offsets of A (out-degrees).  err_host[i] = L2 step
+ * of iteration i. */
+gb_status gb_pagerank(gb_ctx* ctx, const gb_csr* pull, const int64_t* out_offsets, double alpha,
+                      double eps, int64_t max_iters, double switch_ratio, int32_t policy,
+                      double* ranks, int32_t* log_dir_host, int64_t* log_nvals_host,
+                      int64_t* log_est_host, double* err_host, int64_t* iters_host);
+
+/* connected_components (algorithms.py:165-203): parent (int64[n]) receives
+ * the minimum vertex id of each component.  rows = CSR, cols = CSC. */
+gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max_iters,
+                double switch_ratio, int32_t policy, int32_t sparsify, int64_t* parent,
+                int32_t* log_dir_host, int64_t* log_nvals_host, int64_t* log_est_host,
+                int64_t* iters_host);
+
+/* triangle_count (algorithms.py:221-240) of a symmetric pattern matrix. Sync. */
+gb_status gb_tc(gb_ctx* ctx, const gb_csr* a, int64_t* count_host);
 
 /* bfs (algorithms.py:48-77) fused: levels (int64[n], written entirely) get the
  * 1-based level, 0 = unreached.  `push` is the orientation walked by push

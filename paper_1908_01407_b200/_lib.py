@@ -87,7 +87,36 @@ SIGNATURES = {
     "gb_decide_direction": (i32, [i64, i64, i64, f64, i32, pi64]),
     "gb_bfs": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), vp, i64, i64, f64, i32, vp,
                      vp, vp, vp, pi64]),
+    "gb_mxv_pull": (i32, [vp, i32, i32, C.POINTER(gb_csr), vp, vp, i32, i32, vp, vp]),
+    "gb_mxv_push": (i32, [vp, i32, i32, C.POINTER(gb_csr), i64, i64, vp, vp, vp, vp, vp, pi64,
+                          vp]),
+    "gb_mxm_masked": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_csr),
+                            C.POINTER(gb_csr), vp, vp, vp, pi64, vp]),
+    "gb_has_diagonal": (i32, [vp, C.POINTER(gb_csr), pi32]),
+    "gb_ewise_dense": (i32, [vp, i32, i32, i64, vp, vp, vp, i32, vp, vp, vp]),
+    "gb_union_sparse": (i32, [vp, i32, i32, i64, vp, vp, i64, vp, vp, vp, vp, pi64]),
+    "gb_intersect_sparse": (i32, [vp, i32, i32, i64, vp, vp, i64, vp, vp, vp, vp, vp, pi64]),
+    "gb_gather_pair": (i32, [vp, i32, i32, i64, vp, vp, vp, i32, vp]),
+    "gb_filter_mask": (i32, [vp, i32, i64, vp, vp, vp, vp, vp, pi64]),
+    "gb_assign_scalar": (i32, [vp, i32, i64, vp, vp, vp]),
+    "gb_check_bounds": (i32, [vp, i64, vp, i64, pi32]),
+    "gb_scatter_min": (i32, [vp, i32, i64, vp, i64, vp, vp, vp]),
+    "gb_gather": (i32, [vp, i32, i64, vp, i64, vp, vp]),
+    "gb_gather_sparse": (i32, [vp, i32, i64, vp, i64, i64, vp, vp, vp, vp]),
+    "gb_apply_affine": (i32, [vp, i32, i64, vp, vp, vp, vp]),
+    "gb_reduce": (i32, [vp, i32, i32, i64, vp, vp, vp, pi64]),
+    "gb_reduce_rows": (i32, [vp, i32, C.POINTER(gb_csr), vp]),
+    "gb_sssp": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, i64, f64, i32, vp, vp, vp,
+                      vp, pi64, "ITER_CB", vp]),
+    "gb_pagerank": (i32, [vp, C.POINTER(gb_csr), vp, f64, f64, i64, f64, i32, vp, vp, vp, vp,
+                          vp, pi64]),
+    "gb_cc": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, f64, i32, i32, vp, vp, vp,
+                    vp, pi64]),
+    "gb_tc": (i32, [vp, C.POINTER(gb_csr), pi64]),
+    "gb_bitmap_count": (i32, [vp, i64, vp, pi64]),
 }
+
+ITER_CB = C.CFUNCTYPE(None, C.c_int64, C.c_void_p)
 
 _lib = None
 _lib_err = None
@@ -108,7 +137,7 @@ def load(path: str = LIB_PATH):
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res
-            fn.argtypes = args
+            fn.argtypes = [ITER_CB if a == "ITER_CB" else a for a in args]
         _lib = lib
         return lib
 

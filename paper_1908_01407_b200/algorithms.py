@@ -118,17 +118,263 @@ def _bfs_composed(A, source, desc):
     return visited
 
 
-def sssp(A, source, desc=None, on_iteration=None):
-    raise NotImplementedError("sssp is not wired yet")
 
 
-def pagerank(A, alpha=0.85, eps=1e-7, max_iters=10_000, desc=None):
-    raise NotImplementedError("pagerank is not wired yet")
+# ---------------------------------------------------------------------------
+# SSSP
+# ---------------------------------------------------------------------------
 
 
-def connected_components(A, desc=None, sparsify=True):
-    raise NotImplementedError("connected_components is not wired yet")
+def sssp(A: SparseMatrix, source: int, desc=None, on_iteration=None) -> Vector:
+    """Single-source shortest distances by frontier-sparsified relaxation (algorithms.py:80-119)."""
+    _require_square(A)
+    if not 0 <= source < A.nrows:
+        raise IndexError(f"source {source} out of range")
+    if A.nnz and _min_value(A) <= 0:
+        raise ValueError("edge weights must be positive")
+    desc = desc if desc is not None else Descriptor()
+    if not desc.fused:
+        return _sssp_composed(A, source, desc, on_iteration)
+    n = A.nrows
+    iters = min(desc.max_niter, n)
+    dist = empty(n, np.float64)
+    push, _k1 = A.orient(False).csr_struct()
+    pull_o = A.orient(True) if A.has_csc else None
+    pull, _k2 = pull_o.csr_struct() if pull_o is not None else (None, None)
+    cap = max(iters, 1)
+    dirs, nv, est = np.zeros(cap, np.int32), np.zeros(cap, np.int64), np.zeros(cap, np.int64)
+    done = C.c_int64(0)
+    cb = None
+    if on_iteration is not None:
+        def _hook(it, _user):
+            on_iteration(int(it), Vector._wrap(n, None, dist.clone(), np.inf, np.float64))
+        cb = _lib.ITER_CB(_hook)
+    _lib.context().call(
+        "gb_sssp", C.byref(push), C.byref(pull) if pull is not None else None, int(source),
+        int(iters), float(desc.switch_ratio), _POLICY[desc.direction], _lib.ptr(dist),
+        dirs.ctypes.data_as(C.c_void_p), nv.ctypes.data_as(C.c_void_p),
+        est.ctypes.data_as(C.c_void_p), C.byref(done), cb, None)
+    _log_decisions(desc, A, dirs, nv, est, int(done.value))
+    return Vector._wrap(n, None, dist, np.inf, np.float64)
 
 
-def triangle_count(A, desc=None):
-    raise NotImplementedError("triangle_count is not wired yet")
+def _min_value(A):
+    o = A.orient(False)
+    if o.values is None:
+        return o.iso
+    lo, hi = C.c_double(), C.c_double()
+    _lib.context().call("gb_values_minmax", o.nnz, _lib.ptr(o.values), _lib.dtype_code(o.dt),
+                        C.byref(lo), C.byref(hi))
+    return lo.value
+
+
+def _sssp_composed(A, source, desc, on_iteration):
+    min_plus = builtin_semiring("MinPlus")
+    minimum = builtin_monoid("Minimum")
+    plus = builtin_monoid("Plus")
+    n = A.nrows
+    dist = Vector.filled(n, np.inf, dtype=np.float64)
+    dist.zero = np.float64(np.inf)
+    dist.set_element(source, 0.0)
+    frontier = Vector.from_entries([source], [0.0], n, dtype=np.float64)
+    ceiling = Vector.filled(n, np.finfo(np.float64).max)
+    succ_last = -1.0
+    for it in range(min(desc.max_niter, n)):
+        candidates = vxm(min_plus, frontier, A, desc=desc)
+        improved = ewise_mult(LESS, candidates, dist, desc=desc)
+        dist = ewise_add(minimum, dist, candidates, desc=desc)
+        frontier = apply(lambda x: x, candidates, mask=improved, desc=desc)
+        if on_iteration is not None:
+            on_iteration(it, dist.dup())
+        reached = ewise_mult(builtin_semiring("PlusLess"), dist, ceiling, desc=desc)
+        succ = float(reduce(plus, reached))
+        if succ == succ_last and frontier.nvals == 0:
+            break
+        succ_last = succ
+    return dist
+
+
+# ---------------------------------------------------------------------------
+# PageRank
+# ---------------------------------------------------------------------------
+
+
+def pagerank(A: SparseMatrix, alpha=0.85, eps=1e-7, max_iters=10_000, desc=None) -> Vector:
+    """Damped rank scores; iterates until the L2 step delta is <= eps (algorithms.py:132-162).
+
+    The fused driver multiplies with the pull kernel (the reference dispatch
+    always pulls a PageRank iterate: every rank is >= (1-alpha)/n > 0, so the
+    estimate is nnz > switch_ratio*nnz); FORCE_PUSH replays the composition."""
+    _require_square(A)
+    if not 0.0 < alpha < 1.0:
+        raise ValueError(f"alpha must be in (0, 1), got {alpha}")
+    if eps <= 0.0:
+        raise ValueError(f"eps must be positive, got {eps}")
+    desc = desc if desc is not None else Descriptor()
+    if not desc.fused or desc.direction is Direction.FORCE_PUSH or A.nnz == 0:
+        return _pagerank_composed(A, alpha, eps, max_iters, desc)
+    n = A.nrows
+    ranks = empty(n, np.float64)
+    pull_o = A.orient(True)
+    pull, _k = pull_o.csr_struct()
+    cap = max(max_iters, 1)
+    dirs, nv, est = np.zeros(cap, np.int32), np.zeros(cap, np.int64), np.zeros(cap, np.int64)
+    errs = np.zeros(cap, np.float64)
+    done = C.c_int64(0)
+    _lib.context().call(
+        "gb_pagerank", C.byref(pull), _lib.ptr(A.orient(False).offsets), float(alpha), float(eps),
+        int(max_iters), float(desc.switch_ratio), _POLICY[desc.direction], _lib.ptr(ranks),
+        dirs.ctypes.data_as(C.c_void_p), nv.ctypes.data_as(C.c_void_p),
+        est.ctypes.data_as(C.c_void_p), errs.ctypes.data_as(C.c_void_p), C.byref(done))
+    _log_decisions(desc, A, dirs, nv, est, int(done.value))
+    return Vector._wrap(n, None, ranks, 0.0, np.float64)
+
+
+def _scale_rows(A, alpha):
+    """algorithms.py:122-129: Â(i, j) = alpha / outdegree(i), as a device matrix."""
+    o = A.orient(False)
+    deg = torch.diff(o.offsets)
+    inv = torch.zeros(A.nrows, dtype=torch.float64, device=deg.device)
+    nz = deg > 0
+    inv[nz] = alpha / deg[nz].to(torch.float64)
+    vals = torch.repeat_interleave(inv, deg)
+    return SparseMatrix.from_csr(A.nrows, A.ncols, o.offsets, o.indices, vals)
+
+
+def _pagerank_composed(A, alpha, eps, max_iters, desc):
+    plus_times = builtin_semiring("PlusMultiplies")
+    plus = builtin_monoid("Plus")
+    n = A.nrows
+    scaled = _scale_rows(A, alpha)
+    teleport = (1.0 - alpha) / n
+    ranks = Vector.filled(n, 1.0 / n)
+    for _ in range(max_iters):
+        previous = ranks
+        spread = vxm(plus_times, previous, scaled, desc=desc)
+        ranks = ewise_add(plus_times, spread, teleport, desc=desc)
+        delta = ewise_mult(MINUS, ranks, previous, desc=desc)
+        squared = ewise_add(TIMES, delta, delta, desc=desc)
+        error = math.sqrt(float(reduce(plus, squared)))
+        if error <= eps:
+            break
+    return ranks
+
+
+# ---------------------------------------------------------------------------
+# Connected components (FastSV)
+# ---------------------------------------------------------------------------
+
+
+def connected_components(A: SparseMatrix, desc=None, sparsify=True) -> Vector:
+    """Component labels = minimum vertex id per component (algorithms.py:165-203)."""
+    _require_square(A)
+    _require_symmetric(A)
+    desc = desc if desc is not None else Descriptor()
+    if not desc.fused:
+        return _cc_composed(A, desc, sparsify)
+    n = A.nrows
+    parent = empty(n, np.int64)
+    rows, _k1 = A.orient(False).csr_struct()
+    cols, _k2 = A.orient(True).csr_struct()
+    cap = max(desc.max_niter, 1)
+    dirs, nv, est = np.zeros(cap, np.int32), np.zeros(cap, np.int64), np.zeros(cap, np.int64)
+    done = C.c_int64(0)
+    if desc.max_niter <= 0:
+        return Vector._wrap(n, None, torch.arange(n, dtype=torch.int64, device=parent.device), 0,
+                            np.int64)
+    _lib.context().call(
+        "gb_cc", C.byref(rows), C.byref(cols), int(desc.max_niter), float(desc.switch_ratio),
+        _POLICY[desc.direction], 1 if sparsify else 0, _lib.ptr(parent),
+        dirs.ctypes.data_as(C.c_void_p), nv.ctypes.data_as(C.c_void_p),
+        est.ctypes.data_as(C.c_void_p), C.byref(done))
+    _log_decisions(desc, A, dirs, nv, est, int(done.value))
+    return Vector._wrap(n, None, parent, _INT_INF, np.int64)
+
+
+def _cc_composed(A, desc, sparsify):
+    min_second = builtin_semiring("MinimumSelectSecond")
+    min_fold = builtin_monoid("Minimum")
+    not_equal = builtin_semiring("MinimumNotEqualTo")
+    plus = builtin_monoid("Plus")
+    n = A.nrows
+    parent = Vector.dense_of(np.arange(n, dtype=np.int64), 0)
+    min_neighbor = parent.dup()
+    grandparent = parent.dup()
+    grandparent_prev = parent.dup()
+    for _ in range(desc.max_niter):
+        parent_prev = parent.dup()
+        hooked = mxv(min_second, A, grandparent, desc=desc)
+        min_neighbor = ewise_add(min_fold, min_neighbor, hooked, desc=desc)
+        assign_scatter(parent, min_neighbor, parent_prev, desc=desc)
+        parent = ewise_add(min_fold, parent, min_neighbor, desc=desc)
+        parent = ewise_add(min_fold, parent, parent_prev, desc=desc)
+        extract_gather(grandparent, parent, parent, desc=desc)
+        changed = ewise_mult(not_equal, grandparent_prev, grandparent, desc=desc)
+        if int(reduce(plus, changed)) == 0:
+            break
+        grandparent_prev = grandparent.dup()
+        if sparsify:
+            desc.toggle("mask")
+            assign(grandparent, _INT_INF, mask=changed, desc=desc)
+            desc.toggle("mask")
+    return parent
+
+
+# ---------------------------------------------------------------------------
+# Triangle counting
+# ---------------------------------------------------------------------------
+
+
+def _has_diagonal(A):
+    s, _k = A.orient(False).csr_struct()
+    f = C.c_int32(0)
+    _lib.context().call("gb_has_diagonal", C.byref(s), C.byref(f))
+    return bool(f.value)
+
+
+def triangle_count(A: SparseMatrix, desc=None) -> int:
+    """Triangles of an undirected simple graph, each counted once (algorithms.py:221-240).
+
+    Fused: one device pass ranks vertices by (degree, id), keeps each vertex's
+    higher-ranked neighbours and counts sorted-list intersections -- the same
+    integer the reference's masked product L.L^T.*L reduces to."""
+    _require_square(A)
+    _require_symmetric(A)
+    if _has_diagonal(A):
+        raise ValueError("adjacency matrix must have an empty diagonal")
+    desc = desc if desc is not None else Descriptor()
+    if not desc.fused:
+        return _tc_composed(A, desc)
+    o = A.orient(False)
+    if o.values is not None or (o.iso is not None and o.iso != 1):
+        # weighted entries: the product sums value products, not a count
+        return _tc_composed(A, desc)
+    s, _k = o.csr_struct()
+    c = C.c_int64(0)
+    _lib.context().call("gb_tc", C.byref(s), C.byref(c))
+    return int(c.value)
+
+
+def _degree_sorted_lower_triangle(A):
+    """algorithms.py:206-218 on the device."""
+    o = A.orient(False)
+    deg = torch.diff(o.offsets)
+    order = torch.sort(deg, stable=True).indices
+    position = torch.empty_like(order)
+    position[order] = torch.arange(A.nrows, device=order.device)
+    rows = A.row_ids().to(torch.int64)
+    cols = o.indices.to(torch.int64)
+    pr, pc = position[rows], position[cols]
+    keep = pr > pc
+    vals = o.dense_values()
+    return SparseMatrix.from_tuples(pr[keep], pc[keep], vals[keep], A.nrows, A.ncols)
+
+
+def _tc_composed(A, desc):
+    plus_times = builtin_semiring("PlusMultiplies")
+    plus = builtin_monoid("Plus")
+    lower = _degree_sorted_lower_triangle(A)
+    desc.toggle("inp1")
+    closed = mxm_masked(plus_times, lower, lower, mask=lower, desc=desc)
+    desc.toggle("inp1")
+    return int(reduce_scalar_matrix(plus, closed))

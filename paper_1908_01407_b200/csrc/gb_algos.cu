@@ -1,0 +1,511 @@
+// Fused SSSP, PageRank and connected-components drivers.
+//
+//   gb_sssp      algorithms.py:80-119   min-plus relaxation, frontier = strictly
+//                improved vertices.  Push: atomicMin on the distance bits
+//                (non-negative doubles order like int64); the winning write
+//                marks the vertex changed.  Pull: warp per row over in-edges.
+//   gb_pagerank  algorithms.py:122-162  alpha/outdeg folded into a per-source
+//                scale vector (products identical to the reference's
+//                pre-scaled matrix), edge-balanced row tiles for the SpMV, the
+//                teleport / delta / error / next-scale epilogue in one pass.
+//   gb_cc        algorithms.py:165-203  FastSV: hooking SpMV (pull tiles or
+//                push atomics), scatter-min folded into atomics on the parent
+//                vector, grandparent + change count + sparsification in one
+//                pass.
+// Every driver logs the reference direction rule (gb_decide_direction) per
+// multiply and synchronizes once per iteration for the loop-exit scalar.
+#include <math.h>
+#include <string.h>
+
+#include <type_traits>
+
+#include <cub/cub.cuh>
+
+#include "gb_common.cuh"
+#include "gb_lbs.cuh"
+#include "gb_rowtiles.cuh"
+
+extern "C" int32_t gb_decide_direction(int64_t nnz, int64_t nrows, int64_t nnz_u, double ratio,
+                                       int32_t policy, int64_t* estimate_out);
+
+namespace gb {
+
+// ---------------------------------------------------------------------------
+// SSSP
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double ld_weight(const void* vals, int dtype, double iso, int64_t p) {
+  if (!vals) return iso;
+  return dtype == GB_I64 ? (double)__ldg((const long long*)vals + p) : __ldg((const double*)vals + p);
+}
+
+__global__ void sssp_init(int64_t n, double* __restrict__ dist, double* __restrict__ fvd,
+                          int64_t source, int32_t* __restrict__ F, double* __restrict__ Fv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    dist[i] = i == source ? 0.0 : INFINITY;
+    fvd[i] = INFINITY;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    F[0] = (int32_t)source;
+    Fv[0] = 0.0;
+  }
+}
+
+// improve dist[v] to nd; returns true when this call lowered it.  Distances
+// are >= 0 (positive weights are validated on the host), so the IEEE bit
+// pattern orders like a signed integer.
+__device__ __forceinline__ bool relax(double* dist, int32_t v, double nd,
+                                      unsigned long long* reached) {
+  long long* a = reinterpret_cast<long long*>(dist + v);
+  const long long nb = __double_as_longlong(nd);
+  if (nb >= *reinterpret_cast<volatile long long*>(a)) return false;
+  const long long old = atomicMin(a, nb);
+  if (nb < old) {
+    if (old == 0x7ff0000000000000ll) atomicAdd(reached, 1ull);
+    return true;
+  }
+  return false;
+}
+
+struct SsspPush {
+  const int32_t* idx;
+  const void* vals;
+  int dtype;
+  double iso;
+  const double* Fv;
+  double* dist;
+  uint32_t* changed;
+  unsigned long long* reached;
+  __device__ __forceinline__ void operator()(int64_t k, int64_t p, int64_t e) const {
+    const int32_t v = __ldg(idx + p);
+    const double nd = ld_weight(vals, dtype, iso, p) + Fv[k];  // mult(A value, u value)
+    if (relax(dist, v, nd, reached)) atomicOr(changed + (v >> 5), 1u << (v & 31));
+  }
+};
+
+// warp per row over in-edges; contributions only from frontier vertices
+__global__ void __launch_bounds__(256)
+sssp_pull(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+          const void* vals, int dtype, double iso, const double* __restrict__ fvd,
+          double* __restrict__ dist, uint32_t* __restrict__ changed,
+          unsigned long long* __restrict__ reached) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < n; i += nw) {
+    double best = INFINITY;
+    for (int64_t p = off[i] + lane; p < off[i + 1]; p += 32) {
+      const double u = fvd[__ldg(idx + p)];
+      if (u != INFINITY) best = fmin(best, ld_weight(vals, dtype, iso, p) + u);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) best = fmin(best, __shfl_xor_sync(GB_FULL, best, o));
+    if (lane == 0 && best < dist[i]) {
+      if (dist[i] == INFINITY) atomicAdd(reached, 1ull);
+      dist[i] = best;
+      atomicOr(changed + (i >> 5), 1u << (i & 31));
+    }
+  }
+}
+
+// changed bitmap -> frontier list (+ values) and dense frontier values
+__global__ void sssp_finalize(int64_t n, uint32_t* __restrict__ changed,
+                              const double* __restrict__ dist, int32_t* __restrict__ F,
+                              double* __restrict__ Fv, double* __restrict__ fvd,
+                              unsigned long long* __restrict__ count) {
+  const int64_t W = (n + 31) / 32;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bits = changed[w];
+    if (bits) changed[w] = 0;
+    const int c = __popc(bits);
+    long long slot = warp_reserve(count, c);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int64_t v = w * 32 + b;
+      F[slot] = (int32_t)v;
+      Fv[slot] = dist[v];
+      fvd[v] = dist[v];
+      ++slot;
+    }
+  }
+}
+
+__global__ void reset_fvd(int64_t K, const int32_t* __restrict__ F, double* __restrict__ fvd) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
+       i += (int64_t)gridDim.x * blockDim.x)
+    fvd[F[i]] = INFINITY;
+}
+
+// ---------------------------------------------------------------------------
+// PageRank
+// ---------------------------------------------------------------------------
+__global__ void pr_init(int64_t n, const int64_t* __restrict__ out_off, double alpha,
+                        double* __restrict__ inv, double* __restrict__ rank,
+                        double* __restrict__ y, double* __restrict__ spread) {
+  const double r0 = 1.0 / (double)n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = out_off[i + 1] - out_off[i];
+    const double s = d > 0 ? alpha / (double)d : 0.0;  // algorithms.py:124-127
+    inv[i] = s;
+    rank[i] = r0;
+    y[i] = s * r0;
+    spread[i] = 0.0;
+  }
+}
+
+struct PrSum {
+  const double* __restrict__ y;
+  double* __restrict__ spread;
+  __device__ __forceinline__ double identity() const { return 0.0; }
+  __device__ __forceinline__ double load(int64_t, int32_t col) const { return __ldg(y + col); }
+  __device__ __forceinline__ double fold(double a, double x) const { return a + x; }
+  __device__ __forceinline__ void emit(int64_t row, double acc, bool whole) const {
+    if (whole) spread[row] = acc;
+    else atomicAdd(spread + row, acc);
+  }
+};
+
+__global__ void __launch_bounds__(256)
+pr_spmv(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+        const int32_t* __restrict__ tile_first, const double* __restrict__ y,
+        double* __restrict__ spread) {
+  PrSum red{y, spread};
+  row_tiles<double>(n, off, idx, tile_first, red);
+}
+
+// ranks = spread + teleport; error^2 += (ranks - prev)^2; y = inv * ranks;
+// spread reset for the next iteration; count of non-zero ranks (next decision)
+__global__ void __launch_bounds__(256)
+pr_epilogue(int64_t n, double tele, const double* __restrict__ inv, double* __restrict__ spread,
+            const double* __restrict__ prev, double* __restrict__ rank, double* __restrict__ y,
+            double* __restrict__ err2, unsigned long long* __restrict__ nz) {
+  __shared__ double s_e[8];
+  __shared__ long long s_c[8];
+  double e = 0.0;
+  long long c = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double r = spread[j] + tele;
+    spread[j] = 0.0;
+    const double d = r - prev[j];
+    e += d * d;
+    rank[j] = r;
+    y[j] = inv[j] * r;
+    c += r != 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    e += __shfl_xor_sync(GB_FULL, e, o);
+    c += __shfl_xor_sync(GB_FULL, c, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { s_e[wid] = e; s_c[wid] = c; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double te = 0.0;
+    long long tc = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { te += s_e[i]; tc += s_c[i]; }
+    atomicAdd(err2, te);
+    atomicAdd(nz, (unsigned long long)tc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Connected components (FastSV)
+// ---------------------------------------------------------------------------
+constexpr long long kImax = 0x7fffffffffffffffll;
+
+struct CcMin {
+  const long long* __restrict__ gp;
+  long long* __restrict__ hook;
+  __device__ __forceinline__ long long identity() const { return kImax; }
+  __device__ __forceinline__ long long load(int64_t, int32_t col) const { return __ldg(gp + col); }
+  __device__ __forceinline__ long long fold(long long a, long long x) const { return x < a ? x : a; }
+  __device__ __forceinline__ void emit(int64_t row, long long acc, bool whole) const {
+    if (acc == kImax) return;  // hook was reset to the identity
+    if (whole) hook[row] = acc;
+    else atomicMin(hook + row, acc);
+  }
+};
+
+__global__ void __launch_bounds__(256)
+cc_pull(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+        const int32_t* __restrict__ tile_first, const long long* __restrict__ gp,
+        long long* __restrict__ hook) {
+  CcMin red{gp, hook};
+  row_tiles<long long>(n, off, idx, tile_first, red);
+}
+
+struct CcPush {
+  const int32_t* idx;
+  const int32_t* F;
+  const long long* gp;
+  long long* hook;
+  __device__ __forceinline__ void operator()(int64_t k, int64_t p, int64_t e) const {
+    const int32_t i = __ldg(idx + p);
+    const long long g = gp[F[k]];
+    if (g < hook[i]) atomicMin(hook + i, g);
+  }
+};
+
+__global__ void iota_i32(int64_t n, int32_t* __restrict__ a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (int32_t)i;
+}
+
+__global__ void fill_i64(int64_t n, long long v, long long* __restrict__ a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+__global__ void cc_init(int64_t n, long long* __restrict__ parent, long long* __restrict__ mn,
+                        long long* __restrict__ gp, long long* __restrict__ gpp) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    parent[i] = mn[i] = gp[i] = gpp[i] = i;
+}
+
+// mn = min(mn, hooked); parent = min(parent, mn); parent[pp[k]] = min(.., mn[k])
+// (the scatter-min overwrite of kernels.py:538-583 followed by the two Min
+// folds of algorithms.py:192-193 equals this atomic min)
+__global__ void cc_hook(int64_t n, const long long* __restrict__ hook, long long* __restrict__ mn,
+                        const long long* __restrict__ pp, long long* __restrict__ parent) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    long long m = mn[k];
+    const long long h = hook[k];
+    if (h < m) { m = h; mn[k] = m; }
+    atomicMin(parent + k, m);
+    atomicMin(parent + pp[k], m);
+  }
+}
+
+// gp = parent[parent]; changed = gp != gp_prev; gp_prev = gp; sparsify;
+// frontier list of gp != MAX for a following push
+__global__ void cc_shortcut(int64_t n, const long long* __restrict__ parent,
+                            long long* __restrict__ gp, long long* __restrict__ gpp, int sparsify,
+                            int32_t* __restrict__ F, unsigned long long* __restrict__ changed,
+                            unsigned long long* __restrict__ live) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const long long g = parent[parent[k]];
+    const bool c = g != gpp[k];
+    gpp[k] = g;
+    const long long out = (sparsify && !c) ? kImax : g;
+    gp[k] = out;
+    const unsigned m1 = __ballot_sync(__activemask(), c);
+    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && m1) atomicAdd(changed, (unsigned long long)__popc(m1));
+    const bool l = out != kImax;
+    const long long slot = warp_reserve(live, l ? 1 : 0);
+    if (l) F[slot] = (int32_t)k;
+  }
+}
+
+}  // namespace gb
+
+using namespace gb;
+
+extern "C" {
+
+typedef void (*gb_iter_cb)(int64_t iteration, void* user);
+
+gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t source,
+                  int64_t max_iters, double ratio, int32_t policy, double* dist,
+                  int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out,
+                  gb_iter_cb cb, void* user) {
+  const int64_t n = push->nrows;
+  if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source out of range");
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  const int64_t W = (n + 31) / 32;
+  uint32_t* changed = ar.alloc<uint32_t>(W);
+  int32_t* F = ar.alloc<int32_t>(n);
+  double* Fv = ar.alloc<double>(n);
+  double* fvd = ar.alloc<double>(n);
+  unsigned long long* cnt = ar.alloc<unsigned long long>(2);  // [frontier, reached]
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cudaMemsetAsync(changed, 0, sizeof(uint32_t) * W, s));
+  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
+  sssp_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, dist, fvd, source, F, Fv);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 3);
+  // the frontier's dense copy starts with the source
+  const double zero = 0.0;
+  GB_CUDA(ctx, cudaMemcpyAsync(fvd + source, &zero, 8, cudaMemcpyHostToDevice, s));
+  int64_t K = 1, reached = 1, succ_last = -1, iters = 0;
+  const double push_iso = push->iso_f64, pull_iso = pull ? pull->iso_f64 : 0.0;
+  for (int64_t it = 0; it < max_iters; ++it) {
+    int64_t est = 0;
+    const int32_t dir = gb_decide_direction(push->nnz, push->nrows, K, ratio, policy, &est);
+    log_dir[it] = dir;
+    log_nvals[it] = K;
+    log_est[it] = est;
+    iters = it + 1;
+    GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 8, s));
+    if (dir == GB_DIR_PULL) {
+      if (!pull) return set_error(ctx, GB_ERR_FORMAT, "column-oriented storage missing");
+      const int ps = prof_begin(ctx, PROF_SSSP, K);
+      sssp_pull<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(
+          n, pull->offsets, pull->indices, pull->values, pull->dtype, pull_iso, fvd, dist,
+          changed, cnt + 1);
+      prof_end(ctx, ps);
+      count_launch(ctx, 1);
+    } else if (K > 0) {
+      LbsPlan plan;
+      GB_TRY(lbs_prepare(ctx, ar, K, F, push->offsets, push->nnz, &plan));
+      SsspPush f{push->indices, push->values, push->dtype, push_iso, Fv, dist, changed, cnt + 1};
+      const int ps = prof_begin(ctx, PROF_SSSP, K);
+      lbs_expand<SsspPush><<<plan.grid, kLbsThreads, 0, s>>>(K, plan.S, plan.rowstart,
+                                                             plan.tile_first, f);
+      prof_end(ctx, ps);
+      count_launch(ctx, 5);
+    }
+    reset_fvd<<<grid_for(ctx, K > 0 ? K : 1, 256), 256, 0, s>>>(K, F, fvd);
+    sssp_finalize<<<grid_for(ctx, W, 256), 256, 0, s>>>(n, changed, dist, F, Fv, fvd, cnt);
+    GB_LAUNCH_CHECK(ctx);
+    count_launch(ctx, 2);
+    int64_t h[2];
+    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 2));
+    K = h[0];
+    reached += h[1];
+    GB_CUDA(ctx, cudaMemsetAsync(cnt + 1, 0, 8, s));
+    if (cb) cb(it, user);
+    // algorithms.py:114-118: count of finite distances stable and no frontier
+    if (reached == succ_last && K == 0) break;
+    succ_last = reached;
+  }
+  *iters_out = iters;
+  return GB_OK;
+}
+
+gb_status gb_pagerank(gb_ctx* ctx, const gb_csr* pull, const int64_t* out_offsets, double alpha,
+                      double eps, int64_t max_iters, double ratio, int32_t policy,
+                      double* ranks_out, int32_t* log_dir, int64_t* log_nvals, int64_t* log_est,
+                      double* err_out, int64_t* iters_out) {
+  const int64_t n = pull->nrows;
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  double* inv = ar.alloc<double>(n);
+  double* y = ar.alloc<double>(n);
+  double* spread = ar.alloc<double>(n);
+  double* rk[2] = {ar.alloc<double>(n), ranks_out};
+  double* scal = ar.alloc<double>(2);
+  int32_t* tile_first = ar.alloc<int32_t>(pull->nnz / kRowTile + 2);
+  GB_ARENA_CHECK(ctx, ar);
+  pr_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, out_offsets, alpha, inv, rk[0], y, spread);
+  lbs_tile_first<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, pull->offsets, kRowTile, tile_first);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2);
+  const double tele = (1.0 - alpha) / (double)n;
+  const int spmv_grid = resident_grid(ctx, pr_spmv, 256);
+  int64_t nz = n, iters = 0;
+  int cur = 0;
+  for (int64_t it = 0; it < max_iters; ++it) {
+    int64_t est = 0;
+    const int32_t dir = gb_decide_direction(pull->nnz, pull->nrows, nz, ratio, policy, &est);
+    log_dir[it] = dir;
+    log_nvals[it] = nz;
+    log_est[it] = est;
+    iters = it + 1;
+    GB_CUDA(ctx, cudaMemsetAsync(scal, 0, 16, s));
+    const int ps = prof_begin(ctx, PROF_PR, pull->nnz);
+    if (pull->nnz) pr_spmv<<<spmv_grid, 256, 0, s>>>(n, pull->offsets, pull->indices, tile_first, y, spread);
+    prof_end(ctx, ps);
+    // the last iteration must land in ranks_out: pick buffers so it does
+    double* prev = rk[cur];
+    double* next = rk[cur ^ 1];
+    pr_epilogue<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(n, tele, inv, spread, prev, next, y,
+                                                         scal, (unsigned long long*)(scal + 1));
+    GB_LAUNCH_CHECK(ctx);
+    count_launch(ctx, 3);
+    int64_t h[2];
+    GB_TRY(read_i64(ctx, (const int64_t*)scal, h, 2));
+    double e2;
+    memcpy(&e2, &h[0], 8);
+    nz = h[1];
+    const double err = sqrt(e2);
+    if (err_out) err_out[it] = err;
+    cur ^= 1;
+    if (err <= eps) break;
+  }
+  if (rk[cur] != ranks_out)
+    GB_CUDA(ctx, cudaMemcpyAsync(ranks_out, rk[cur], sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (iters == 0)
+    GB_CUDA(ctx, cudaMemcpyAsync(ranks_out, rk[0], sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  *iters_out = iters;
+  return GB_OK;
+}
+
+gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max_iters,
+                double ratio, int32_t policy, int32_t sparsify, int64_t* parent,
+                int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
+  const int64_t n = rows->nrows;
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  long long* P = reinterpret_cast<long long*>(parent);
+  long long* mn = ar.alloc<long long>(n);
+  long long* gp = ar.alloc<long long>(n);
+  long long* gpp = ar.alloc<long long>(n);
+  long long* pp = ar.alloc<long long>(n);
+  long long* hook = ar.alloc<long long>(n);
+  int32_t* F = ar.alloc<int32_t>(n);
+  unsigned long long* cnt = ar.alloc<unsigned long long>(2);  // [changed, live]
+  int32_t* tile_first = ar.alloc<int32_t>(rows->nnz / kRowTile + 2);
+  GB_ARENA_CHECK(ctx, ar);
+  cc_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, P, mn, gp, gpp);
+  lbs_tile_first<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, rows->offsets, kRowTile, tile_first);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2);
+  const int pull_grid = resident_grid(ctx, cc_pull, 256);
+  int64_t live = n, iters = 0, frontier_listed = 0;
+  for (int64_t it = 0; it < max_iters; ++it) {
+    int64_t est = 0;
+    const int32_t dir = gb_decide_direction(rows->nnz, rows->nrows, live, ratio, policy, &est);
+    log_dir[it] = dir;
+    log_nvals[it] = live;
+    log_est[it] = est;
+    iters = it + 1;
+    GB_CUDA(ctx, cudaMemcpyAsync(pp, P, sizeof(long long) * n, cudaMemcpyDeviceToDevice, s));
+    fill_i64<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, kImax, hook);
+    const int ps = prof_begin(ctx, PROF_CC, live);
+    if (dir == GB_DIR_PULL) {
+      // mxv pull walks rows of A (kernels.py:313-316, row_view(False))
+      if (rows->nnz) cc_pull<<<pull_grid, 256, 0, s>>>(n, rows->offsets, rows->indices, tile_first, gp, hook);
+      count_launch(ctx, 1);
+    } else if (live > 0) {
+      // push walks columns of A: rows of the CSC orientation
+      if (!cols) return set_error(ctx, GB_ERR_FORMAT, "column-oriented storage missing");
+      if (!frontier_listed) {
+        // first iteration: every grandparent is live (gp = arange)
+        iota_i32<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, F);
+        count_launch(ctx, 1);
+      }
+      LbsPlan plan;
+      GB_TRY(lbs_prepare(ctx, ar, live, F, cols->offsets, cols->nnz, &plan));
+      CcPush f{cols->indices, F, gp, hook};
+      lbs_expand<CcPush><<<plan.grid, kLbsThreads, 0, s>>>(live, plan.S, plan.rowstart,
+                                                           plan.tile_first, f);
+      count_launch(ctx, 5);
+    }
+    prof_end(ctx, ps);
+    cc_hook<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, hook, mn, pp, P);
+    GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
+    cc_shortcut<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, P, gp, gpp, sparsify, F, cnt, cnt + 1);
+    GB_LAUNCH_CHECK(ctx);
+    count_launch(ctx, 5);
+    int64_t h[2];
+    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 2));
+    frontier_listed = 1;
+    if (h[0] == 0) break;  // algorithms.py:196-197
+    live = h[1];
+  }
+  *iters_out = iters;
+  return GB_OK;
+}
+
+}  // extern "C"

@@ -221,3 +221,27 @@ gb_status gb_nonempty_rows(gb_ctx* ctx, int64_t n, const int64_t* offsets, uint3
 }
 
 }  // extern "C"
+
+namespace gb {
+__global__ void popc_kernel(int64_t W, const uint32_t* __restrict__ bm,
+                            unsigned long long* __restrict__ out) {
+  long long c = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x)
+    c += __popc(bm[w]);
+  c = warp_sum_ll(c);
+  if (lane_id() == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+}  // namespace gb
+
+extern "C" gb_status gb_bitmap_count(gb_ctx* ctx, int64_t n, const uint32_t* bm, int64_t* count) {
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  int64_t* c = ar.alloc<int64_t>(1);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cudaMemsetAsync(c, 0, 8, s));
+  const int64_t W = (n + 31) / 32;
+  if (W) popc_kernel<<<grid_for(ctx, W, 256), 256, 0, s>>>(W, bm, (unsigned long long*)c);
+  GB_LAUNCH_CHECK(ctx);
+  return read_i64(ctx, c, count);
+}
