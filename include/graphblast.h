@@ -167,8 +167,8 @@ gb_status gb_csr_row_ids(gb_ctx* ctx, int64_t nrows, int64_t nnz, const int64_t*
 gb_status gb_count_ne(gb_ctx* ctx, int64_t n, const void* vals, int32_t dtype,
                       const void* zero_host, int64_t* count_host);
 
-/* to_sparse (containers.py:242-252): keep entries != zero (dense input when
- * idx == NULL; sparse input of k entries otherwise).  Writes the kept count
+/* to_sparse (containers.py:242-252): keep entries != zero (dense input of n
+ * values when k < 0; sparse input of k entries with indices idx otherwise).  Writes the kept count
  * to *count_host (synchronizes). */
 gb_status gb_compact(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx, const void* vals,
                      int32_t dtype, const void* zero_host, int32_t* out_idx, void* out_vals,
@@ -180,7 +180,8 @@ gb_status gb_scatter_dense(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx
                            void* out_vals);
 
 /* _effective_mask (kernels.py:67-84) as a bitmap of ceil(n/32) words: a stored
- * entry allows its position iff its value != 0; complement flips. */
+ * entry allows its position iff its value != 0; complement flips.  k < 0: a
+ * dense mask of n values; otherwise k sparse entries (idx, vals). */
 gb_status gb_mask_bitmap(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx,
                          const void* vals, int32_t dtype, int32_t complement, uint32_t* out);
 

@@ -144,7 +144,7 @@ def sssp(A: SparseMatrix, source: int, desc=None, on_iteration=None) -> Vector:
     cap = max(iters, 1)
     dirs, nv, est = np.zeros(cap, np.int32), np.zeros(cap, np.int64), np.zeros(cap, np.int64)
     done = C.c_int64(0)
-    cb = None
+    cb = _lib.ITER_CB()  # NULL function pointer
     if on_iteration is not None:
         def _hook(it, _user):
             on_iteration(int(it), Vector._wrap(n, None, dist.clone(), np.inf, np.float64))

@@ -387,7 +387,7 @@ def compact(vals_t, idx_t, dt, zero, size):
         return out_idx, out_vals
     ctx = _lib.context()
     cnt = C.c_int64(0)
-    ctx.call("gb_compact", int(size), k, _lib.ptr(idx_t), _lib.ptr(vals_t), _lib.dtype_code(dt),
+    ctx.call("gb_compact", int(size), k if idx_t is not None else -1, _lib.ptr(idx_t), _lib.ptr(vals_t), _lib.dtype_code(dt),
              _zero_buf(zero, dt), _lib.ptr(out_idx), _lib.ptr(out_vals), C.byref(cnt))
     c = int(cnt.value)
     return out_idx[:c], out_vals[:c]
@@ -438,8 +438,10 @@ class _Orient:
         keep = None
         if self.values is None:
             s.values = None
-            s.iso_i64 = int(self.iso) if self.iso is not None else 0
-            s.iso_f64 = float(self.iso) if self.iso is not None else 0.0
+            iso = 0 if self.iso is None else self.iso
+            s.iso_f64 = float(iso)
+            # the int view of a float iso value is only read for int compute dtypes
+            s.iso_i64 = int(iso) if np.isfinite(float(iso)) and abs(float(iso)) < 2**63 else 0
         else:
             keep = self.values_as(dt)
             s.values = keep.data_ptr() if self.nnz else 0

@@ -397,8 +397,8 @@ gb_status gb_build_csr(gb_ctx* ctx, int64_t nrows, int64_t ncols, int64_t n,
   uint64_t* kb = ar.alloc<uint64_t>(n);
   int64_t* pa = ar.alloc<int64_t>(n);
   int64_t* pb = ar.alloc<int64_t>(n);
-  int32_t* flags = ar.alloc<int32_t>(n);
-  int64_t* pos = ar.alloc<int64_t>(n);
+  int32_t* flags = ar.alloc<int32_t>(n + 1);
+  int64_t* pos = ar.alloc<int64_t>(n + 1);
   uint64_t* ukeys = ar.alloc<uint64_t>(n);
   GB_ARENA_CHECK(ctx, ar);
   coo_keys<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, rows, cols, bits, ka);
@@ -413,15 +413,13 @@ gb_status gb_build_csr(gb_ctx* ctx, int64_t nrows, int64_t ncols, int64_t n,
   const uint64_t* keys = dk.Current();
   const int64_t* perm = dv.Current();
   unique_flags<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, keys, flags);
-  // exclusive positions of unique keys
-  int64_t* flags64 = ar.alloc<int64_t>(n);
-  GB_ARENA_CHECK(ctx, ar);
+  // exclusive positions of unique keys; flags[n] = 0 so pos[n] = unique count
+  GB_CUDA(ctx, cudaMemsetAsync(flags + n, 0, sizeof(int32_t), s));
   size_t tb2 = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb2, flags, pos, n, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb2, flags, pos, n + 1, s);
   void* tmp2 = ar.raw(tb2);
   GB_ARENA_CHECK(ctx, ar);
-  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp2, tb2, flags, pos, n, s));
-  (void)flags64;
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp2, tb2, flags, pos, n + 1, s));
   uint64_t cmask = ((uint64_t)1 << bits) - 1;
   if (dtype == GB_I64)
     fold_segments<int64_t><<<grid_for(ctx, n, 256), 256, 0, s>>>(
@@ -431,9 +429,8 @@ gb_status gb_build_csr(gb_ctx* ctx, int64_t nrows, int64_t ncols, int64_t n,
     fold_segments<double><<<grid_for(ctx, n, 256), 256, 0, s>>>(
         n, keys, flags, pos, perm, (const double*)vals, dedup_op, bits, cmask, out_indices,
         ukeys, (double*)out_vals);
-  int64_t last_pos = 0;
-  GB_TRY(read_i64(ctx, pos + n - 1, &last_pos));
-  int64_t nu = last_pos + 1;  // the last sorted key always ends a segment
+  int64_t nu = 0;
+  GB_TRY(read_i64(ctx, pos + n, &nu));
   offsets_from_sorted_rows<<<grid_for(ctx, nu + 1, 256), 256, 0, s>>>(nu, nrows,
                                                                       KeyRow{ukeys, bits},
                                                                       out_offsets);

@@ -183,8 +183,8 @@ static gb_status push_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a, i
   int32_t* kb = ar.alloc<int32_t>(E);
   T* va = ar.alloc<T>(E);
   T* vb = ar.alloc<T>(E);
-  int32_t* flags = ar.alloc<int32_t>(E);
-  int64_t* segpos = ar.alloc<int64_t>(E);
+  int32_t* flags = ar.alloc<int32_t>(E + 1);
+  int64_t* segpos = ar.alloc<int64_t>(E + 1);
   GB_ARENA_CHECK(ctx, ar);
   T iso = std::is_same<T, double>::value ? (T)a->iso_f64 : (T)a->iso_i64;
   PushExpand<T> f{a->indices, (const T*)a->values, iso, u_vals, mult_op, ka, va};
@@ -201,14 +201,15 @@ static gb_status push_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a, i
   const int32_t* keys = dk.Current();
   const T* prods = dv.Current();
   seg_flags<<<grid_for(ctx, E, 256), 256, 0, s>>>(E, keys, flags);
+  GB_CUDA(ctx, cudaMemsetAsync(flags + E, 0, sizeof(int32_t), s));
   size_t tb2 = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb2, flags, segpos, E, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb2, flags, segpos, E + 1, s);
   void* tmp2 = ar.raw(tb2);
   GB_ARENA_CHECK(ctx, ar);
-  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp2, tb2, flags, segpos, E, s));
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp2, tb2, flags, segpos, E + 1, s));
   int64_t nseg = 0;
-  GB_TRY(read_i64(ctx, segpos + E - 1, &nseg));
-  nseg += 1;
+  GB_TRY(read_i64(ctx, segpos + E, &nseg));
+  // flags[E] = 0, so segpos[E] counts every segment
   if (counters) {
     int64_t c[3];
     GB_TRY(read_i64(ctx, counters, c, 3));

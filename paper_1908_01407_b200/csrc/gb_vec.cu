@@ -117,7 +117,9 @@ static gb_status compact_t(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx
                            int64_t* count) {
   Arena ar(ctx);
   cudaStream_t s = stream_of(ctx);
-  int64_t len = idx ? k : n;
+  const bool dense = k < 0;  // k < 0: dense input (n values); else k sparse entries
+  if (dense) idx = nullptr;
+  int64_t len = dense ? n : k;
   if (len == 0) { *count = 0; return GB_OK; }
   int64_t* pos = ar.alloc<int64_t>(len);
   int64_t* cnt = ar.alloc<int64_t>(1);
@@ -193,7 +195,7 @@ gb_status gb_mask_bitmap(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx,
   cudaStream_t s = stream_of(ctx);
   int64_t W = (n + 31) / 32;
   if (W == 0) return GB_OK;
-  if (!idx) {
+  if (k < 0) {  // dense mask of n values
     if (dtype == GB_I64)
       mask_dense_kernel<int64_t><<<grid_for(ctx, W, 256), 256, 0, s>>>(n, (const int64_t*)vals, complement, out);
     else

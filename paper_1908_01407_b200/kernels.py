@@ -93,7 +93,7 @@ def _mask_bitmap(mask, size, mode):
         raise ShapeError(f"mask size {mask.size} does not match output size {size}")
     W = max((size + 31) // 32, 1)
     out = torch.empty(W, dtype=torch.int32, device=mask._vals.device)
-    k = 0 if mask._idx is None else int(mask._idx.numel())
+    k = -1 if mask._idx is None else int(mask._idx.numel())  # -1: dense mask
     _ctx().call("gb_mask_bitmap", int(size), k, _lib.ptr(mask._idx), _lib.ptr(mask._vals),
                 _code(mask._dt), 1 if mode is MaskMode.COMPLEMENT else 0, _lib.ptr(out))
     return out
