@@ -83,6 +83,58 @@ struct SsspPush {
   }
 };
 
+// Pull relaxation on edge-balanced row tiles: cand[row] = min over in-edges
+// from frontier vertices of w + fvd[src] (non-negative doubles compare as
+// int64 bits), then sssp_pull_apply folds cand into dist.
+struct SsspMin {
+  const void* vals;
+  int dtype;
+  double iso;
+  const double* __restrict__ fvd;
+  long long* __restrict__ cand;
+  __device__ __forceinline__ double identity() const { return INFINITY; }
+  __device__ __forceinline__ double load(int64_t p, int32_t col) const {
+    const double u = __ldg(fvd + col);
+    return u == INFINITY ? INFINITY : ld_weight(vals, dtype, iso, p) + u;
+  }
+  __device__ __forceinline__ double fold(double a, double x) const { return fmin(a, x); }
+  __device__ __forceinline__ void emit(int64_t row, double acc, bool whole) const {
+    if (acc == INFINITY) return;
+    const long long b = __double_as_longlong(acc);
+    if (whole) cand[row] = b;
+    else atomicMin(cand + row, b);
+  }
+};
+
+__global__ void __launch_bounds__(256)
+sssp_pull_tiles(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
+                const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
+                const void* vals, int dtype, double iso, const double* __restrict__ fvd,
+                long long* __restrict__ cand) {
+  SsspMin red{vals, dtype, iso, fvd, cand};
+  row_tiles<double>(R, nz_rows, nz_off, idx, tile_first, red);
+}
+
+constexpr long long kInfBits = 0x7ff0000000000000ll;
+
+__global__ void sssp_pull_apply(int64_t n, long long* __restrict__ cand, double* __restrict__ dist,
+                                uint32_t* __restrict__ changed,
+                                unsigned long long* __restrict__ reached) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const long long c = cand[i];
+    if (c == kInfBits) continue;
+    cand[i] = kInfBits;
+    const double nd = __longlong_as_double(c);
+    const double od = dist[i];
+    if (nd < od) {
+      if (od == INFINITY) atomicAdd(reached, 1ull);
+      dist[i] = nd;
+      atomicOr(changed + (i >> 5), 1u << (i & 31));
+    }
+  }
+}
+
 // warp per row over in-edges; contributions only from frontier vertices
 __global__ void __launch_bounds__(256)
 sssp_pull(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
@@ -169,11 +221,11 @@ struct PrSum {
 };
 
 __global__ void __launch_bounds__(256)
-pr_spmv(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
-        const int32_t* __restrict__ tile_first, const double* __restrict__ y,
-        double* __restrict__ spread) {
+pr_spmv(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
+        const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
+        const double* __restrict__ y, double* __restrict__ spread) {
   PrSum red{y, spread};
-  row_tiles<double>(n, off, idx, tile_first, red);
+  row_tiles<double>(R, nz_rows, nz_off, idx, tile_first, red);
 }
 
 // ranks = spread + teleport; error^2 += (ranks - prev)^2; y = inv * ranks;
@@ -232,11 +284,11 @@ struct CcMin {
 };
 
 __global__ void __launch_bounds__(256)
-cc_pull(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
-        const int32_t* __restrict__ tile_first, const long long* __restrict__ gp,
-        long long* __restrict__ hook) {
+cc_pull(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
+        const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
+        const long long* __restrict__ gp, long long* __restrict__ hook) {
   CcMin red{gp, hook};
-  row_tiles<long long>(n, off, idx, tile_first, red);
+  row_tiles<long long>(R, nz_rows, nz_off, idx, tile_first, red);
 }
 
 struct CcPush {
@@ -280,8 +332,12 @@ __global__ void cc_hook(int64_t n, const long long* __restrict__ hook, long long
     long long m = mn[k];
     const long long h = hook[k];
     if (h < m) { m = h; mn[k] = m; }
-    atomicMin(parent + k, m);
-    atomicMin(parent + pp[k], m);
+    // read first: most targets already hold a smaller label (the giant
+    // component's root is the target of millions of k), so the atomic --
+    // which serialises on one L2 slice per address -- is rarely issued
+    if (m < *reinterpret_cast<volatile long long*>(parent + k)) atomicMin(parent + k, m);
+    const long long t = pp[k];
+    if (m < *reinterpret_cast<volatile long long*>(parent + t)) atomicMin(parent + t, m);
   }
 }
 
@@ -337,6 +393,8 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
   // the frontier's dense copy starts with the source
   const double zero = 0.0;
   GB_CUDA(ctx, cudaMemcpyAsync(fvd + source, &zero, 8, cudaMemcpyHostToDevice, s));
+  RowTilesPlan pull_plan;    // built on the first pull iteration
+  long long* cand = nullptr;  // pull candidates (+inf bits between iterations)
   int64_t K = 1, reached = 1, succ_last = -1, iters = 0;
   const double push_iso = push->iso_f64, pull_iso = pull ? pull->iso_f64 : 0.0;
   for (int64_t it = 0; it < max_iters; ++it) {
@@ -350,11 +408,19 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
     if (dir == GB_DIR_PULL) {
       if (!pull) return set_error(ctx, GB_ERR_FORMAT, "column-oriented storage missing");
       const int ps = prof_begin(ctx, PROF_SSSP, K);
-      sssp_pull<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(
-          n, pull->offsets, pull->indices, pull->values, pull->dtype, pull_iso, fvd, dist,
-          changed, cnt + 1);
+      if (!pull_plan.nz_rows) {
+        GB_TRY(row_tiles_plan(ctx, ar, n, pull->offsets, pull->nnz, &pull_plan));
+        cand = ar.alloc<long long>(n);
+        GB_ARENA_CHECK(ctx, ar);
+        fill_i64<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, kInfBits, cand);
+      }
+      if (pull_plan.R)
+        sssp_pull_tiles<<<resident_grid(ctx, sssp_pull_tiles, 256), 256, 0, s>>>(
+            pull_plan.R, pull_plan.nz_rows, pull_plan.nz_off, pull->indices, pull_plan.tile_first,
+            pull->values, pull->dtype, pull_iso, fvd, cand);
+      sssp_pull_apply<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, cand, dist, changed, cnt + 1);
       prof_end(ctx, ps);
-      count_launch(ctx, 1);
+      count_launch(ctx, 2);
     } else if (K > 0) {
       LbsPlan plan;
       GB_TRY(lbs_prepare(ctx, ar, K, F, push->offsets, push->nnz, &plan));
@@ -395,12 +461,12 @@ gb_status gb_pagerank(gb_ctx* ctx, const gb_csr* pull, const int64_t* out_offset
   double* spread = ar.alloc<double>(n);
   double* rk[2] = {ar.alloc<double>(n), ranks_out};
   double* scal = ar.alloc<double>(2);
-  int32_t* tile_first = ar.alloc<int32_t>(pull->nnz / kRowTile + 2);
   GB_ARENA_CHECK(ctx, ar);
+  RowTilesPlan plan;
+  GB_TRY(row_tiles_plan(ctx, ar, n, pull->offsets, pull->nnz, &plan));
   pr_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, out_offsets, alpha, inv, rk[0], y, spread);
-  lbs_tile_first<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, pull->offsets, kRowTile, tile_first);
   GB_LAUNCH_CHECK(ctx);
-  count_launch(ctx, 2);
+  count_launch(ctx, 1);
   const double tele = (1.0 - alpha) / (double)n;
   const int spmv_grid = resident_grid(ctx, pr_spmv, 256);
   int64_t nz = n, iters = 0;
@@ -414,7 +480,8 @@ gb_status gb_pagerank(gb_ctx* ctx, const gb_csr* pull, const int64_t* out_offset
     iters = it + 1;
     GB_CUDA(ctx, cudaMemsetAsync(scal, 0, 16, s));
     const int ps = prof_begin(ctx, PROF_PR, pull->nnz);
-    if (pull->nnz) pr_spmv<<<spmv_grid, 256, 0, s>>>(n, pull->offsets, pull->indices, tile_first, y, spread);
+    if (plan.R) pr_spmv<<<spmv_grid, 256, 0, s>>>(plan.R, plan.nz_rows, plan.nz_off, pull->indices,
+                                                  plan.tile_first, y, spread);
     prof_end(ctx, ps);
     // the last iteration must land in ranks_out: pick buffers so it does
     double* prev = rk[cur];
@@ -455,12 +522,12 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   long long* hook = ar.alloc<long long>(n);
   int32_t* F = ar.alloc<int32_t>(n);
   unsigned long long* cnt = ar.alloc<unsigned long long>(2);  // [changed, live]
-  int32_t* tile_first = ar.alloc<int32_t>(rows->nnz / kRowTile + 2);
   GB_ARENA_CHECK(ctx, ar);
+  RowTilesPlan plan;
+  GB_TRY(row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &plan));
   cc_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, P, mn, gp, gpp);
-  lbs_tile_first<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, rows->offsets, kRowTile, tile_first);
   GB_LAUNCH_CHECK(ctx);
-  count_launch(ctx, 2);
+  count_launch(ctx, 1);
   const int pull_grid = resident_grid(ctx, cc_pull, 256);
   int64_t live = n, iters = 0, frontier_listed = 0;
   for (int64_t it = 0; it < max_iters; ++it) {
@@ -475,7 +542,8 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
     const int ps = prof_begin(ctx, PROF_CC, live);
     if (dir == GB_DIR_PULL) {
       // mxv pull walks rows of A (kernels.py:313-316, row_view(False))
-      if (rows->nnz) cc_pull<<<pull_grid, 256, 0, s>>>(n, rows->offsets, rows->indices, tile_first, gp, hook);
+      if (plan.R) cc_pull<<<pull_grid, 256, 0, s>>>(plan.R, plan.nz_rows, plan.nz_off, rows->indices,
+                                                    plan.tile_first, gp, hook);
       count_launch(ctx, 1);
     } else if (live > 0) {
       // push walks columns of A: rows of the CSC orientation
