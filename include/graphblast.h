@@ -306,6 +306,36 @@ gb_status gb_reduce_rows(gb_ctx* ctx, int32_t op, const gb_csr* a, void* out);
  * fused algorithms   (algorithms.py)
  * --------------------------------------------------------------------------*/
 
+/* ---- 1D-partitioned BFS (multi-GPU; one rank's steps, see distributed.py).
+ * Rank p owns vertices [lo, hi); lo is a multiple of 1024.  Buffers levels
+ * (int64[n]), vbm/vprev/fbm/xbm (uint32[ceil(n/32)]) and F (int32[n]) are
+ * global-sized and replicated; only xbm is exchanged (all-reduce SUM: the
+ * ranks' owned words are disjoint). */
+gb_status gb_bfs_dist_init(gb_ctx* ctx, int64_t n, int64_t source, int64_t* levels,
+                           uint32_t* vbm, uint32_t* vprev, uint32_t* fbm, int32_t* F);
+/* push over the rank's column block (all n rows of A, columns in [lo,hi)) */
+gb_status gb_bfs_dist_push(gb_ctx* ctx, const gb_csr* colblock, int64_t K, const int32_t* F,
+                           uint32_t* vbm);
+/* xbm = owned words of vbm & ~vprev, zero elsewhere (after a push) */
+gb_status gb_bfs_dist_collect(gb_ctx* ctx, int64_t n, int64_t lo, int64_t hi,
+                              const uint32_t* vbm, const uint32_t* vprev, uint32_t* xbm);
+/* pull over the rank's row block (rows lo..hi-1 of A^T); owned new bits -> xbm */
+gb_status gb_bfs_dist_pull(gb_ctx* ctx, const gb_csr* rowblock, int64_t lo, int64_t hi,
+                           const uint32_t* nonempty_block, int64_t n, int64_t depth,
+                           uint32_t* vbm, uint32_t* vprev, const uint32_t* fbm, uint32_t* xbm,
+                           int64_t* levels);
+/* apply the exchanged new-frontier bitmap xbm: stamp `depth`, rebuild F and
+ * fbm; *K_host = global frontier size (synchronizes) */
+gb_status gb_bfs_dist_apply(gb_ctx* ctx, int64_t n, int64_t depth, const uint32_t* xbm,
+                            uint32_t* vbm, uint32_t* vprev, uint32_t* fbm, int64_t* levels,
+                            int32_t* F, int64_t* K_host);
+/* clear the levels of the K vertices in F (loop cap reached, algorithms.py:69) */
+gb_status gb_bfs_dist_unstamp(gb_ctx* ctx, int64_t K, const int32_t* F, int64_t* levels);
+/* entries of every row of `a` whose column lies in [lo, hi): CSR with the
+ * same row count (out_offsets: nrows+1); pass out_indices = NULL to size. */
+gb_status gb_csr_column_block(gb_ctx* ctx, const gb_csr* a, int64_t lo, int64_t hi,
+                              int64_t* out_offsets, int32_t* out_indices, int64_t* nnz_host);
+
 /* Per-iteration host callback of the fused drivers (the sssp on_iteration hook). */
 typedef void (*gb_iter_cb)(int64_t iteration, void* user);
 

@@ -114,6 +114,13 @@ SIGNATURES = {
                     vp, pi64]),
     "gb_tc": (i32, [vp, C.POINTER(gb_csr), pi64]),
     "gb_bitmap_count": (i32, [vp, i64, vp, pi64]),
+    "gb_bfs_dist_init": (i32, [vp, i64, i64, vp, vp, vp, vp, vp]),
+    "gb_bfs_dist_push": (i32, [vp, C.POINTER(gb_csr), i64, vp, vp]),
+    "gb_bfs_dist_collect": (i32, [vp, i64, i64, i64, vp, vp, vp]),
+    "gb_bfs_dist_pull": (i32, [vp, C.POINTER(gb_csr), i64, i64, vp, i64, i64, vp, vp, vp, vp, vp]),
+    "gb_bfs_dist_apply": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, pi64]),
+    "gb_bfs_dist_unstamp": (i32, [vp, i64, vp, vp]),
+    "gb_csr_column_block": (i32, [vp, C.POINTER(gb_csr), i64, i64, vp, vp, pi64]),
 }
 
 ITER_CB = C.CFUNCTYPE(None, C.c_int64, C.c_void_p)

@@ -209,11 +209,13 @@ __global__ void bfs_init(int64_t source, int64_t* levels, uint32_t* vbm, uint32_
 // visited bitmap against the level-start snapshot, then the warp walks the
 // non-empty words so level stamps and frontier-list writes are coalesced.
 __global__ void __launch_bounds__(256)
-bfs_finalize(int64_t n, int64_t depth, const uint32_t* __restrict__ vbm,
+bfs_finalize(int64_t n, int64_t depth, uint32_t* __restrict__ vbm,
              uint32_t* __restrict__ vprev, uint32_t* __restrict__ fbm_next,
              int64_t* __restrict__ levels, int32_t* __restrict__ F,
              unsigned long long* __restrict__ count,
-             unsigned long long* __restrict__ count_clear) {
+             unsigned long long* __restrict__ count_clear, const uint32_t* __restrict__ xbm) {
+  // xbm == NULL: new frontier = vbm & ~vprev (single GPU).  xbm != NULL: the
+  // all-reduced new-frontier bitmap of a 1D-partitioned run is authoritative.
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
   const int lane = threadIdx.x & 31;
   const int64_t W = (n + 31) / 32;
@@ -224,9 +226,17 @@ bfs_finalize(int64_t n, int64_t depth, const uint32_t* __restrict__ vbm,
     const int64_t w = g * 32 + lane;
     uint32_t bits = 0;
     if (w < W) {
-      const uint32_t cur = vbm[w], old = vprev[w];
-      bits = cur & ~old;
-      if (bits) vprev[w] = cur;
+      if (xbm) {
+        bits = xbm[w];
+        if (bits) {
+          vbm[w] |= bits;
+          vprev[w] |= bits;
+        }
+      } else {
+        const uint32_t cur = vbm[w], old = vprev[w];
+        bits = cur & ~old;
+        if (bits) vprev[w] = cur;
+      }
       fbm_next[w] = bits;
     }
     // frontier list slots for the whole group, in word order
@@ -270,19 +280,21 @@ bfs_pull(int64_t n, int64_t depth, const int64_t* __restrict__ off,
          uint32_t* __restrict__ vbm, uint32_t* __restrict__ vprev, const uint32_t* __restrict__ fbm,
          uint32_t* __restrict__ fbm_next, int64_t* __restrict__ levels,
          int32_t* __restrict__ F, unsigned long long* __restrict__ count,
-         unsigned long long* __restrict__ count_clear) {
+         unsigned long long* __restrict__ count_clear, int64_t g_lo, int64_t g_hi) {
+  // [g_lo, g_hi): groups of 32 words (1024 vertices) this launch owns; a
+  // 1D-partitioned rank passes its vertex block with `off`/`nonempty`
+  // pointers rebased so global vertex ids index them directly.
   __shared__ int32_t s_list[8][kPullList];
   __shared__ uint32_t s_new[8][32];
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int64_t W = (n + 31) / 32;
-  const int64_t G = (W + 31) / 32;
   const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int32_t* list = s_list[wid];
   uint32_t* nw = s_new[wid];
-  for (int64_t g = g0; g < G; g += ng) {
+  for (int64_t g = g_lo + g0; g < g_hi; g += ng) {
     const int64_t w = g * 32 + lane;
     uint32_t rem = w < W ? (~vbm[w] & __ldg(nonempty + w)) : 0u;
     nw[lane] = 0;
@@ -473,7 +485,7 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
         const int ps = prof_begin(ctx, PROF_BFS_PULL, K);
         bfs_pull<<<grid, 256, 0, s>>>(n, depth + 1, pull->offsets, pull->indices, pull_on,
                                       pull_nonempty, vbm, vprev, fbm[cur], fbm[cur ^ 1], levels, F,
-                                      c, c_next);
+                                      c, c_next, 0, (W + 31) / 32);
         prof_end(ctx, ps);
         count_launch(ctx, 1);
       }
@@ -493,7 +505,7 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
       }
       const int pf = prof_begin(ctx, PROF_BFS_FINALIZE, K);
       bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, depth + 1, vbm, vprev, fbm[cur ^ 1],
-                                                         levels, F, c, c_next);
+                                                         levels, F, c, c_next, nullptr);
       prof_end(ctx, pf);
       count_launch(ctx, 1);
     }
@@ -511,6 +523,184 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     }
   }
   *iters_out = iters;
+  return GB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// 1D-partitioned BFS steps (one rank of P; the host loop and the NCCL
+// exchange of the new-frontier bitmap live in distributed.py).  Rank p owns
+// vertices [lo, hi) (lo, hi multiples of 1024 except hi = n) and stores
+//   rowblock: rows lo..hi-1 of A^T (in-edges of owned vertices) for pull,
+//   colblock: all n rows of A restricted to columns in [lo, hi) for push.
+// Every bitmap / levels / frontier buffer is global-sized and replicated.
+// ---------------------------------------------------------------------------
+
+__global__ void bfs_collect(int64_t w_lo, int64_t w_hi, const uint32_t* __restrict__ vbm,
+                            const uint32_t* __restrict__ vprev, uint32_t* __restrict__ xbm) {
+  for (int64_t w = w_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < w_hi;
+       w += (int64_t)gridDim.x * blockDim.x)
+    xbm[w] = vbm[w] & ~vprev[w];
+}
+
+gb_status gb_bfs_dist_init(gb_ctx* ctx, int64_t n, int64_t source, int64_t* levels,
+                           uint32_t* vbm, uint32_t* vprev, uint32_t* fbm, int32_t* F) {
+  if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source out of range");
+  cudaStream_t s = stream_of(ctx);
+  const int64_t W = (n + 31) / 32;
+  GB_CUDA(ctx, cudaMemsetAsync(levels, 0, sizeof(int64_t) * n, s));
+  GB_CUDA(ctx, cudaMemsetAsync(vbm, 0, sizeof(uint32_t) * W, s));
+  GB_CUDA(ctx, cudaMemsetAsync(vprev, 0, sizeof(uint32_t) * W, s));
+  GB_CUDA(ctx, cudaMemsetAsync(fbm, 0, sizeof(uint32_t) * W, s));
+  bfs_init<<<1, 1, 0, s>>>(source, levels, vbm, vprev, fbm, F);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 5);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_push(gb_ctx* ctx, const gb_csr* colblock, int64_t K, const int32_t* F,
+                           uint32_t* vbm) {
+  if (K == 0 || colblock->nnz == 0) return GB_OK;
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  LbsPlan plan;
+  GB_TRY(lbs_prepare(ctx, ar, K, F, colblock->offsets, colblock->nnz, &plan, kWarpTile));
+  const EdgeOn on{colblock->values, colblock->dtype};
+  const int ps = prof_begin(ctx, PROF_BFS_PUSH, K);
+  if (colblock->values)
+    bfs_expand_warp<true><<<resident_grid(ctx, bfs_expand_warp<true>, 256), 256, 0, s>>>(
+        K, plan.S, plan.rowstart, plan.tile_first, colblock->indices, on, vbm);
+  else
+    bfs_expand_warp<false><<<resident_grid(ctx, bfs_expand_warp<false>, 256), 256, 0, s>>>(
+        K, plan.S, plan.rowstart, plan.tile_first, colblock->indices, on, vbm);
+  prof_end(ctx, ps);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 5);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_collect(gb_ctx* ctx, int64_t n, int64_t lo, int64_t hi,
+                              const uint32_t* vbm, const uint32_t* vprev, uint32_t* xbm) {
+  cudaStream_t s = stream_of(ctx);
+  const int64_t W = (n + 31) / 32;
+  const int64_t w_lo = lo / 32, w_hi = (hi + 31) / 32;
+  GB_CUDA(ctx, cudaMemsetAsync(xbm, 0, sizeof(uint32_t) * W, s));
+  if (w_hi > w_lo)
+    bfs_collect<<<grid_for(ctx, w_hi - w_lo, 256), 256, 0, s>>>(w_lo, w_hi, vbm, vprev, xbm);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_pull(gb_ctx* ctx, const gb_csr* rowblock, int64_t lo, int64_t hi,
+                           const uint32_t* nonempty_block, int64_t n, int64_t depth,
+                           uint32_t* vbm, uint32_t* vprev, const uint32_t* fbm, uint32_t* xbm,
+                           int64_t* levels) {
+  if (lo % 1024) return set_error(ctx, GB_ERR_ARG, "partition start must be a multiple of 1024");
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  const int64_t W = (n + 31) / 32;
+  int32_t* F = ar.alloc<int32_t>(hi - lo + 1);
+  unsigned long long* cnt = ar.alloc<unsigned long long>(2);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cudaMemsetAsync(xbm, 0, sizeof(uint32_t) * W, s));
+  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
+  if (hi > lo && rowblock->nnz) {
+    const EdgeOn on{rowblock->values, rowblock->dtype};
+    // rebase so global vertex ids index the block's offsets / nonempty words
+    const int64_t* off = rowblock->offsets - lo;
+    const uint32_t* ne = nonempty_block - lo / 32;
+    const int64_t g_lo = lo / 1024, g_hi = (hi + 1023) / 1024;
+    const int ps = prof_begin(ctx, PROF_BFS_PULL, 0);
+    bfs_pull<<<grid_for(ctx, (g_hi - g_lo) * 32, 256, 8), 256, 0, s>>>(
+        hi, depth, off, rowblock->indices, on, ne, vbm, vprev, fbm, xbm, levels, F, cnt, cnt + 1,
+        g_lo, g_hi);
+    prof_end(ctx, ps);
+  }
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 3);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_apply(gb_ctx* ctx, int64_t n, int64_t depth, const uint32_t* xbm,
+                            uint32_t* vbm, uint32_t* vprev, uint32_t* fbm, int64_t* levels,
+                            int32_t* F, int64_t* K_host) {
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  const int64_t W = (n + 31) / 32;
+  unsigned long long* cnt = ar.alloc<unsigned long long>(2);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
+  bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, depth, vbm, vprev, fbm, levels, F, cnt,
+                                                        cnt + 1, xbm);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2);
+  return read_i64(ctx, (const int64_t*)cnt, K_host);
+}
+
+gb_status gb_bfs_dist_unstamp(gb_ctx* ctx, int64_t K, const int32_t* F, int64_t* levels) {
+  if (K <= 0) return GB_OK;
+  bfs_unstamp<<<grid_for(ctx, K, 256), 256, 0, stream_of(ctx)>>>(K, F, levels);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  return GB_OK;
+}
+
+// Column block of a CSR: every row keeps only its entries with column in
+// [lo, hi) (columns stay global).  Two passes: counts, then copy.
+__global__ void colblock_count(int64_t n, const int64_t* __restrict__ off,
+                               const int32_t* __restrict__ idx, int32_t lo, int32_t hi,
+                               int64_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w0; r < n; r += nw) {
+    long long c = 0;
+    for (int64_t p = off[r] + lane; p < off[r + 1]; p += 32) c += idx[p] >= lo && idx[p] < hi;
+    c = warp_sum_ll(c);
+    if (lane == 0) cnt[r] = c;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[n] = 0;
+}
+
+__global__ void colblock_fill(int64_t n, const int64_t* __restrict__ off,
+                              const int32_t* __restrict__ idx, int32_t lo, int32_t hi,
+                              const int64_t* __restrict__ out_off, int32_t* __restrict__ out_idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w0; r < n; r += nw) {
+    int64_t o = out_off[r];
+    for (int64_t base = off[r]; base < off[r + 1]; base += 32) {
+      const int64_t p = base + lane;
+      const bool keep = p < off[r + 1] && idx[p] >= lo && idx[p] < hi;
+      const uint32_t bal = __ballot_sync(GB_FULL, keep);
+      if (keep) out_idx[o + __popc(bal & ((1u << lane) - 1u))] = idx[p];
+      o += __popc(bal);
+    }
+  }
+}
+
+gb_status gb_csr_column_block(gb_ctx* ctx, const gb_csr* a, int64_t lo, int64_t hi,
+                              int64_t* out_offsets, int32_t* out_indices, int64_t* nnz_host) {
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  const int64_t n = a->nrows;
+  int64_t* cnt = ar.alloc<int64_t>(n + 1);
+  GB_ARENA_CHECK(ctx, ar);
+  colblock_count<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(n, a->offsets, a->indices,
+                                                                (int32_t)lo, (int32_t)hi, cnt);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, out_offsets, n + 1, s);
+  void* tmp = ar.raw(tb);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, out_offsets, n + 1, s));
+  GB_TRY(read_i64(ctx, out_offsets + n, nnz_host));
+  if (out_indices)
+    colblock_fill<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(n, a->offsets, a->indices,
+                                                                 (int32_t)lo, (int32_t)hi,
+                                                                 out_offsets, out_indices);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 4);
   return GB_OK;
 }
 

@@ -1,0 +1,204 @@
+"""1D-partitioned multi-GPU BFS (north star: "the graph is 1D row-partitioned
+across GPUs, and each iteration's frontier is exchanged with NCCL").
+
+One process per GPU (torchrun), ``torch.distributed`` over NCCL for the
+plumbing.  Rank p owns the contiguous vertex block [lo, hi); block boundaries
+put ~nnz/P stored entries in every block -- the reference's nonzero split
+(kernels.py:133-150) lifted from threads to GPUs -- and are multiples of
+1024 so bitmap words (and the 32-word groups the kernels walk) never straddle
+two ranks.  Each rank stores
+
+* ``rowblock`` -- rows lo..hi-1 of A^T (in-edges of its vertices): the pull
+  direction walks them against the replicated frontier bitmap;
+* ``colblock`` -- all n rows of A restricted to columns in [lo, hi): the push
+  direction expands the replicated frontier list over it, so only owned
+  vertices are ever marked.
+
+Per BFS level there is ONE collective: the ranks' owned words of the
+new-frontier bitmap (n/8 bytes; disjoint across ranks) are combined with an
+all-reduce SUM.  Every rank then applies the same global bitmap, so the
+frontier count, the push/pull decision (the reference rule,
+kernels.py:108-126) and the level vector are identical and replicated -- no
+all-to-all and no allgatherv are needed.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .containers import Descriptor, Direction, SparseMatrix, Vector, _Orient
+from .kernels import DirectionDecision, direction_rule
+
+ALIGN = 1024
+
+
+def partition_bounds(row_offsets, world: int, align: int = ALIGN):
+    """Edge-balanced vertex blocks: world+1 boundaries, multiples of ``align``
+    (except the last = n), non-decreasing."""
+    off = np.asarray(row_offsets, dtype=np.int64)
+    n = off.size - 1
+    total = int(off[-1])
+    targets = np.arange(world + 1, dtype=np.float64) * total / world
+    b = np.searchsorted(off, targets, side="left").astype(np.int64)
+    b = (b + align // 2) // align * align
+    b = np.clip(b, 0, n // align * align)  # inner boundaries stay aligned
+    b[0], b[-1] = 0, n
+    return np.maximum.accumulate(b).tolist()
+
+
+@dataclass
+class BlockGraph:
+    """One rank's share of a square matrix (device tensors)."""
+
+    n: int
+    nnz: int                    # global stored entries (the direction rule's nnz)
+    lo: int
+    hi: int
+    bounds: list
+    row_off: torch.Tensor       # [hi-lo+1], rebased
+    row_idx: torch.Tensor       # global column ids
+    row_nonempty: torch.Tensor  # ceil((hi-lo)/32) words
+    col_off: torch.Tensor       # [n+1]
+    col_idx: torch.Tensor       # global column ids in [lo, hi)
+    values_iso: object = 1
+
+    @classmethod
+    def from_matrix(cls, A: SparseMatrix, rank: int, world: int, bounds=None):
+        if A.nrows != A.ncols:
+            raise ValueError("1D partitioning needs a square matrix")
+        if A._csr.values is not None:
+            raise NotImplementedError("distributed BFS takes a pattern (iso-valued) matrix")
+        n = A.nrows
+        csr = A.orient(False)
+        csc = A.orient(True)
+        if bounds is None:
+            bounds = partition_bounds(csr.offsets.cpu().numpy(), world)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        ctx = _lib.context()
+        # pull block: rows lo..hi-1 of the in-edge orientation
+        a, b = int(csc.offsets[lo].item()), int(csc.offsets[hi].item())
+        row_off = (csc.offsets[lo:hi + 1] - a).contiguous()
+        row_idx = csc.indices[a:b].clone()
+        W = max((hi - lo + 31) // 32, 1)
+        ne = torch.zeros(W, dtype=torch.int32, device=row_off.device)
+        if hi > lo:
+            ctx.call("gb_nonempty_rows", hi - lo, _lib.ptr(row_off), _lib.ptr(ne))
+        # push block: rows of A, columns in [lo, hi)
+        s, _k = csr.csr_struct()
+        col_off = torch.empty(n + 1, dtype=torch.int64, device=row_off.device)
+        cnt = C.c_int64(0)
+        ctx.call("gb_csr_column_block", C.byref(s), lo, hi, _lib.ptr(col_off), None, C.byref(cnt))
+        col_idx = torch.empty(max(int(cnt.value), 1), dtype=torch.int32, device=row_off.device)
+        ctx.call("gb_csr_column_block", C.byref(s), lo, hi, _lib.ptr(col_off), _lib.ptr(col_idx),
+                 C.byref(cnt))
+        return cls(n, A.nnz, lo, hi, list(bounds), row_off, row_idx, ne, col_off,
+                   col_idx[:int(cnt.value)], csr.iso)
+
+    def _orient(self, which):
+        if which == "row":
+            return _Orient(self.hi - self.lo, self.n, self.row_off, self.row_idx, None,
+                           self.values_iso, np.int64)
+        return _Orient(self.n, self.n, self.col_off, self.col_idx, None, self.values_iso, np.int64)
+
+
+class NativeSteps:
+    """The per-rank level steps, executed by libgraphblast_sm100a."""
+
+    def __init__(self, g: BlockGraph):
+        self.g = g
+        self.ctx = _lib.context()
+        self.rows, self._k1 = g._orient("row").csr_struct()
+        self.cols, self._k2 = g._orient("col").csr_struct()
+        n = g.n
+        W = (n + 31) // 32
+        dev = g.row_off.device
+        self.levels = torch.empty(n, dtype=torch.int64, device=dev)
+        self.vbm = torch.empty(W, dtype=torch.int32, device=dev)
+        self.vprev = torch.empty(W, dtype=torch.int32, device=dev)
+        self.fbm = torch.empty(W, dtype=torch.int32, device=dev)
+        self.xbm = torch.empty(W, dtype=torch.int32, device=dev)
+        self.F = torch.empty(n, dtype=torch.int32, device=dev)
+
+    def init(self, source):
+        p = _lib.ptr
+        self.ctx.call("gb_bfs_dist_init", self.g.n, int(source), p(self.levels), p(self.vbm),
+                      p(self.vprev), p(self.fbm), p(self.F))
+
+    def push(self, K):
+        g, p = self.g, _lib.ptr
+        self.ctx.call("gb_bfs_dist_push", C.byref(self.cols), int(K), p(self.F), p(self.vbm))
+        self.ctx.call("gb_bfs_dist_collect", g.n, g.lo, g.hi, p(self.vbm), p(self.vprev), p(self.xbm))
+
+    def pull(self, depth):
+        g, p = self.g, _lib.ptr
+        self.ctx.call("gb_bfs_dist_pull", C.byref(self.rows), g.lo, g.hi, p(g.row_nonempty), g.n,
+                      int(depth), p(self.vbm), p(self.vprev), p(self.fbm), p(self.xbm),
+                      p(self.levels))
+
+    def apply(self, depth):
+        p = _lib.ptr
+        K = C.c_int64(0)
+        self.ctx.call("gb_bfs_dist_apply", self.g.n, int(depth), p(self.xbm), p(self.vbm),
+                      p(self.vprev), p(self.fbm), p(self.levels), p(self.F), C.byref(K))
+        return int(K.value)
+
+    def unstamp(self, K):
+        self.ctx.call("gb_bfs_dist_unstamp", int(K), _lib.ptr(self.F), _lib.ptr(self.levels))
+
+
+class TorchExchange:
+    """The frontier exchange: all-reduce SUM of the disjoint owned bitmap words."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def allreduce_words(self, xbm: torch.Tensor):
+        import torch.distributed as dist
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(xbm, op=dist.ReduceOp.SUM, group=self.group)
+
+
+def bfs_partitioned(g: BlockGraph, source: int, desc=None, steps=None, exchange=None):
+    """algorithms.py:48-77 on a 1D-partitioned graph.  Returns (levels tensor,
+    replicated on every rank, int64[n]) and appends the reference direction
+    trace to ``desc.direction_log``."""
+    if not 0 <= source < g.n:
+        raise IndexError(f"source {source} out of range")
+    desc = desc if desc is not None else Descriptor()
+    steps = steps if steps is not None else NativeSteps(g)
+    exchange = exchange if exchange is not None else TorchExchange()
+    steps.init(source)
+    K, depth = 1, 1
+    iters = min(desc.max_niter, g.n + 1)
+    for it in range(iters):
+        chosen, est, thr = direction_rule(g.nnz, g.n, K, desc.switch_ratio, desc.direction)
+        desc.direction_log.append(DirectionDecision(chosen, K, est, g.nnz, thr))
+        if chosen == "pull":
+            steps.pull(depth + 1)
+        else:
+            steps.push(K)
+        exchange.allreduce_words(steps.xbm)
+        K = steps.apply(depth + 1)
+        if K == 0:
+            break
+        depth += 1
+        if it + 1 == iters:
+            steps.unstamp(K)  # the reference stamps a frontier at the next iteration
+    return steps.levels
+
+
+def bfs(A_or_block, source, desc=None, group=None):
+    """Public entry: bfs on this rank's block; returns the (replicated) level Vector."""
+    g = A_or_block
+    if isinstance(A_or_block, SparseMatrix):
+        import torch.distributed as dist
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        g = BlockGraph.from_matrix(A_or_block, rank, world)
+    levels = bfs_partitioned(g, source, desc, exchange=TorchExchange(group))
+    return Vector._wrap(g.n, None, levels, 0, np.int64)

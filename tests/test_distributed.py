@@ -1,0 +1,165 @@
+"""Multi-rank host logic of the 1D-partitioned BFS, on CPU with gloo.
+
+The partition, the level loop, the reference direction rule on global
+counts, the bitmap exchange (all-reduce SUM of disjoint owned words) and the
+loop-cap handling are the product code (paper_1908_01407_b200.distributed).
+The per-rank level steps -- CUDA kernels in the product -- are replaced here
+by a numpy restatement with the same contract, so world_size-2 runs execute
+on this CPU-only box.  Results must equal the single-process oracle BFS.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import port
+from paper_1908_01407_b200.distributed import ALIGN, TorchExchange, bfs_partitioned, partition_bounds
+
+
+def test_partition_bounds_properties():
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        n = int(rng.integers(1, 20000))
+        deg = rng.integers(0, 50, size=n)
+        deg[:5] *= 100  # hubs at low ids, like R-MAT
+        off = np.r_[0, np.cumsum(deg)]
+        for P in (1, 2, 3, 4, 8):
+            b = partition_bounds(off, P)
+            assert b[0] == 0 and b[-1] == n and len(b) == P + 1
+            assert all(x <= y for x, y in zip(b, b[1:]))
+            assert all(x % ALIGN == 0 for x in b[:-1])
+    # balance on a large uniform graph: every block within one alignment unit
+    off = np.arange(0, 1 << 20, dtype=np.int64) * 16
+    b = partition_bounds(off, 8)
+    sizes = np.diff([off[x] for x in b])
+    assert sizes.max() - sizes.min() <= 16 * ALIGN
+
+
+class Block:
+    """Numpy stand-in for BlockGraph (same fields the loop reads)."""
+
+    def __init__(self, rp, ci, lo, hi):
+        self.n = rp.size - 1
+        self.nnz = int(rp[-1])
+        self.lo, self.hi = lo, hi
+        self.rp, self.ci = rp, ci   # symmetric: in-edges == out-edges
+
+
+class NumpySteps:
+    """Same contract as NativeSteps (gb_bfs_dist_*), restated in numpy."""
+
+    def __init__(self, g):
+        self.g = g
+        n = g.n
+        W = (n + 31) // 32
+        self.levels = np.zeros(n, np.int64)
+        self.vbm = np.zeros(W, np.uint32)
+        self.vprev = np.zeros(W, np.uint32)
+        self.fbm = np.zeros(W, np.uint32)
+        self.xbm = torch.zeros(W, dtype=torch.int32)
+        self.F = np.zeros(0, np.int64)
+
+    @staticmethod
+    def _set(bm, v):
+        bm[v >> 5] |= np.uint32(1) << np.uint32(v & 31)
+
+    @staticmethod
+    def _get(bm, v):
+        return (int(bm[v >> 5]) >> (v & 31)) & 1
+
+    def _x(self):
+        return self.xbm.numpy().view(np.uint32)
+
+    def init(self, s):
+        self.levels[s] = 1
+        for bm in (self.vbm, self.vprev, self.fbm):
+            self._set(bm, s)
+        self.F = np.array([s])
+
+    def push(self, K):
+        g = self.g
+        for u in self.F[:K]:
+            for v in g.ci[g.rp[u]:g.rp[u + 1]]:
+                if g.lo <= v < g.hi and not self._get(self.vbm, v):
+                    self._set(self.vbm, v)
+        x = self._x()
+        x[:] = 0
+        wl, wh = g.lo // 32, (g.hi + 31) // 32
+        x[wl:wh] = self.vbm[wl:wh] & ~self.vprev[wl:wh]
+
+    def pull(self, depth):
+        g = self.g
+        x = self._x()
+        x[:] = 0
+        for v in range(g.lo, g.hi):
+            if self._get(self.vbm, v):
+                continue
+            nb = g.ci[g.rp[v]:g.rp[v + 1]]
+            if any(self._get(self.fbm, int(j)) for j in nb):
+                for bm in (self.vbm, self.vprev, x):
+                    self._set(bm, v)
+                self.levels[v] = depth
+
+    def apply(self, depth):
+        x = self._x().copy()
+        self.vbm |= x
+        self.vprev |= x
+        self.fbm[:] = x
+        bits = np.unpackbits(x.view(np.uint8), bitorder="little")[: self.g.n]
+        F = np.flatnonzero(bits)
+        self.levels[F] = depth
+        self.F = F
+        return int(F.size)
+
+    def unstamp(self, K):
+        self.levels[self.F[:K]] = 0
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port_, scale, source, cap, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rp, ci, n = port.rmat_csr(scale)
+    bounds = partition_bounds(rp, world)
+    g = Block(rp, ci, bounds[rank], bounds[rank + 1])
+    from paper_1908_01407_b200.containers import Descriptor
+    desc = Descriptor(max_niter=cap)
+    levels = bfs_partitioned(g, source, desc, steps=NumpySteps(g), exchange=TorchExchange())
+    results[rank] = (levels.copy(), [(d.chosen, d.frontier_nvals, d.estimated_frontier_edges)
+                                     for d in desc.direction_log])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scale,source,cap", [(10, 0, 10_000), (11, 5, 10_000), (10, 0, 2)])
+def test_partitioned_bfs_world2_matches_oracle(scale, source, cap):
+    ctx = mp.get_context("spawn")
+    manager = ctx.Manager()
+    results = manager.dict()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_, scale, source, cap, results))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    rp, ci, n = port.rmat_csr(scale)
+    P = port.mat_from_csr(rp, ci, np.ones(ci.size, np.int64), n)
+    pd = port.Desc(max_niter=cap)
+    want = port.bfs(P, source, pd)
+    for r in range(2):
+        levels, trace = results[r]
+        assert np.array_equal(levels, want.vals)
+        assert [t[0] for t in trace] == [x[0] for x in pd.log]
+        assert [t[1:] for t in trace] == [tuple(x[1:3]) for x in pd.log]

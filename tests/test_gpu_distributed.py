@@ -1,0 +1,75 @@
+"""The 1D-partitioned BFS steps on one GPU: P ranks simulated in lock step.
+
+Each simulated rank owns a BlockGraph and NativeSteps (its own device
+buffers); the exchange sums the ranks' new-frontier words exactly as the
+NCCL all-reduce does.  Levels and the direction trace must equal the
+single-GPU fused BFS for P = 1, 2, 3, 4, 8.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def lockstep_bfs(A, P, source, desc):
+    from paper_1908_01407_b200.distributed import BlockGraph, NativeSteps, partition_bounds
+    from paper_1908_01407_b200.kernels import DirectionDecision, direction_rule
+    bounds = partition_bounds(A._csr.offsets.cpu().numpy(), P)
+    ranks = [NativeSteps(BlockGraph.from_matrix(A, r, P, bounds)) for r in range(P)]
+    g = ranks[0].g
+    for st in ranks:
+        st.init(source)
+    K, depth = 1, 1
+    iters = min(desc.max_niter, g.n + 1)
+    for it in range(iters):
+        chosen, est, thr = direction_rule(g.nnz, g.n, K, desc.switch_ratio, desc.direction)
+        desc.direction_log.append(DirectionDecision(chosen, K, est, g.nnz, thr))
+        for st in ranks:
+            if chosen == "pull":
+                st.pull(depth + 1)
+            else:
+                st.push(K)
+        total = torch.zeros_like(ranks[0].xbm)
+        for st in ranks:
+            total += st.xbm
+        for st in ranks:
+            st.xbm.copy_(total)
+        Ks = [st.apply(depth + 1) for st in ranks]
+        assert len(set(Ks)) == 1
+        K = Ks[0]
+        if K == 0:
+            break
+        depth += 1
+        if it + 1 == iters:
+            for st in ranks:
+                st.unstamp(K)
+    out = [st.levels.cpu().numpy() for st in ranks]
+    for o in out[1:]:
+        assert np.array_equal(o, out[0])
+    return out[0]
+
+
+@pytest.mark.parametrize("scale", [12, 16, 20])
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_partitioned_equals_single(scale, P):
+    import paper_1908_01407_b200 as gb
+    A = gb.io.rmat_matrix(scale)
+    for src in (0, 7):
+        d1, d2 = gb.Descriptor(), gb.Descriptor()
+        want = gb.bfs(A, src, desc=d1).values
+        got = lockstep_bfs(A, P, src, d2)
+        assert np.array_equal(got, want)
+        assert [(x.chosen, x.frontier_nvals) for x in d1.direction_log] == \
+            [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
+
+
+def test_partitioned_world1_entry_point():
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200 import distributed
+    A = gb.io.rmat_matrix(14)
+    d = gb.Descriptor(max_niter=3)
+    got = distributed.bfs(A, 0, desc=d).values
+    want = gb.bfs(A, 0, desc=gb.Descriptor(max_niter=3)).values
+    assert np.array_equal(got, want)
