@@ -233,10 +233,10 @@ def run_ours(args):
         k_next = int(counts[lvl + 2]) if lvl + 2 < counts.size else 0
         bytes_alg = push_level_bytes(n, k, flops, k_next)
         achieved = bytes_alg / (t_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "lbs_expand<PushMark> (push SpMSpV, level %d)" % (lvl + 1),
+        roof = {"bound": "hbm", "kernel": "bfs_expand_warp (push SpMSpV, level %d)" % (lvl + 1),
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
-                "traffic": committed_traffic("lbs_expand"),
+                "traffic": committed_traffic("bfs_expand_warp"),
                 "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4),
                 "frontier": int(k), "flops": flops,
                 "level_ms": [(kind, a, round(t, 4)) for (kind, a, t) in prof]}
