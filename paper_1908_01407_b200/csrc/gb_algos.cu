@@ -238,15 +238,32 @@ pr_epilogue(int64_t n, double tele, const double* __restrict__ inv, double* __re
   __shared__ long long s_c[8];
   double e = 0.0;
   long long c = 0;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const double r = spread[j] + tele;
-    spread[j] = 0.0;
-    const double d = r - prev[j];
-    e += d * d;
-    rank[j] = r;
-    y[j] = inv[j] * r;
-    c += r != 0.0;
+  // 4 independent elements per thread per step: all loads issued first
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < n; j0 += 4 * stride) {
+    double sp[4], pv[4], iv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j < n) {
+        sp[u] = __ldcs(spread + j);
+        pv[u] = __ldcs(prev + j);
+        iv[u] = __ldg(inv + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u * stride;
+      if (j < n) {
+        const double r = sp[u] + tele;
+        const double d = r - pv[u];
+        e += d * d;
+        c += r != 0.0;
+        spread[j] = 0.0;
+        rank[j] = r;
+        y[j] = iv[u] * r;
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -268,16 +285,21 @@ pr_epilogue(int64_t n, double tele, const double* __restrict__ inv, double* __re
 // ---------------------------------------------------------------------------
 // Connected components (FastSV)
 // ---------------------------------------------------------------------------
-constexpr long long kImax = 0x7fffffffffffffffll;
+// Labels are vertex ids < n < 2^31: the driver keeps parent / grandparent /
+// min-neighbour vectors as int32 (half the gather bytes, the 67 MB label
+// vector of s24 stays L2-resident) and widens the result to int64 at the end.
+// INT32_MAX plays the reference's INT64_MAX sparsification sentinel
+// (algorithms.py:33, 201); it is never a valid label.
+constexpr int kImax32 = 0x7fffffff;
 
 struct CcMin {
-  const long long* __restrict__ gp;
-  long long* __restrict__ hook;
-  __device__ __forceinline__ long long identity() const { return kImax; }
-  __device__ __forceinline__ long long load(int64_t, int32_t col) const { return __ldg(gp + col); }
-  __device__ __forceinline__ long long fold(long long a, long long x) const { return x < a ? x : a; }
-  __device__ __forceinline__ void emit(int64_t row, long long acc, bool whole) const {
-    if (acc == kImax) return;  // hook was reset to the identity
+  const int* __restrict__ gp;
+  int* __restrict__ hook;
+  __device__ __forceinline__ int identity() const { return kImax32; }
+  __device__ __forceinline__ int load(int64_t, int32_t col) const { return __ldg(gp + col); }
+  __device__ __forceinline__ int fold(int a, int x) const { return x < a ? x : a; }
+  __device__ __forceinline__ void emit(int64_t row, int acc, bool whole) const {
+    if (acc == kImax32) return;  // hook was reset to the identity
     if (whole) hook[row] = acc;
     else atomicMin(hook + row, acc);
   }
@@ -286,19 +308,19 @@ struct CcMin {
 __global__ void __launch_bounds__(256)
 cc_pull(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
         const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
-        const long long* __restrict__ gp, long long* __restrict__ hook) {
+        const int* __restrict__ gp, int* __restrict__ hook) {
   CcMin red{gp, hook};
-  row_tiles<long long>(R, nz_rows, nz_off, idx, tile_first, red);
+  row_tiles<int>(R, nz_rows, nz_off, idx, tile_first, red);
 }
 
 struct CcPush {
   const int32_t* idx;
   const int32_t* F;
-  const long long* gp;
-  long long* hook;
+  const int* gp;
+  int* hook;
   __device__ __forceinline__ void operator()(int64_t k, int64_t p, int64_t e) const {
     const int32_t i = __ldg(idx + p);
-    const long long g = gp[F[k]];
+    const int g = gp[F[k]];
     if (g < hook[i]) atomicMin(hook + i, g);
   }
 };
@@ -315,51 +337,85 @@ __global__ void fill_i64(int64_t n, long long v, long long* __restrict__ a) {
     a[i] = v;
 }
 
-__global__ void cc_init(int64_t n, long long* __restrict__ parent, long long* __restrict__ mn,
-                        long long* __restrict__ gp, long long* __restrict__ gpp) {
+__global__ void fill_i32(int64_t n, int v, int* __restrict__ a) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    parent[i] = mn[i] = gp[i] = gpp[i] = i;
+    a[i] = v;
+}
+
+__global__ void cc_init(int64_t n, int* __restrict__ parent, int* __restrict__ mn,
+                        int* __restrict__ gp, int* __restrict__ gpp) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    parent[i] = mn[i] = gp[i] = gpp[i] = (int)i;
 }
 
 // mn = min(mn, hooked); parent = min(parent, mn); parent[pp[k]] = min(.., mn[k])
 // (the scatter-min overwrite of kernels.py:538-583 followed by the two Min
 // folds of algorithms.py:192-193 equals this atomic min)
-__global__ void cc_hook(int64_t n, const long long* __restrict__ hook, long long* __restrict__ mn,
-                        const long long* __restrict__ pp, long long* __restrict__ parent) {
+__global__ void cc_hook(int64_t n, const int* __restrict__ hook, int* __restrict__ mn,
+                        const int* __restrict__ pp, int* __restrict__ parent) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
-    long long m = mn[k];
-    const long long h = hook[k];
+    int m = mn[k];
+    const int h = hook[k];
     if (h < m) { m = h; mn[k] = m; }
     // read first: most targets already hold a smaller label (the giant
     // component's root is the target of millions of k), so the atomic --
     // which serialises on one L2 slice per address -- is rarely issued
-    if (m < *reinterpret_cast<volatile long long*>(parent + k)) atomicMin(parent + k, m);
-    const long long t = pp[k];
-    if (m < *reinterpret_cast<volatile long long*>(parent + t)) atomicMin(parent + t, m);
+    if (m < *reinterpret_cast<volatile int*>(parent + k)) atomicMin(parent + k, m);
+    const int t = pp[k];
+    if (m < *reinterpret_cast<volatile int*>(parent + t)) atomicMin(parent + t, m);
   }
 }
 
-// gp = parent[parent]; changed = gp != gp_prev; gp_prev = gp; sparsify;
-// frontier list of gp != MAX for a following push
-__global__ void cc_shortcut(int64_t n, const long long* __restrict__ parent,
-                            long long* __restrict__ gp, long long* __restrict__ gpp, int sparsify,
-                            int32_t* __restrict__ F, unsigned long long* __restrict__ changed,
-                            unsigned long long* __restrict__ live) {
+// gp = parent[parent]; changed = gp != gp_prev; gp_prev = gp; sparsify.
+// Counts are reduced per block (one atomic per block, not per warp: the two
+// counters are single addresses every block hits).
+__global__ void __launch_bounds__(256)
+cc_shortcut(int64_t n, const int* __restrict__ parent, int* __restrict__ gp,
+            int* __restrict__ gpp, int sparsify, unsigned long long* __restrict__ changed,
+            unsigned long long* __restrict__ live) {
+  __shared__ long long s_c[8], s_l[8];
+  long long c = 0, l = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const long long g = parent[parent[k]];
-    const bool c = g != gpp[k];
+    const int g = parent[parent[k]];
+    const bool ch = g != gpp[k];
     gpp[k] = g;
-    const long long out = (sparsify && !c) ? kImax : g;
+    const int out = (sparsify && !ch) ? kImax32 : g;
     gp[k] = out;
-    const unsigned m1 = __ballot_sync(__activemask(), c);
-    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && m1) atomicAdd(changed, (unsigned long long)__popc(m1));
-    const bool l = out != kImax;
-    const long long slot = warp_reserve(live, l ? 1 : 0);
+    c += ch;
+    l += out != kImax32;
+  }
+  c = warp_sum_ll(c);
+  l = warp_sum_ll(l);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { s_c[wid] = c; s_l[wid] = l; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tc = 0, tl = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { tc += s_c[i]; tl += s_l[i]; }
+    if (tc) atomicAdd(changed, (unsigned long long)tc);
+    if (tl) atomicAdd(live, (unsigned long long)tl);
+  }
+}
+
+// frontier list of live grandparents (gp != sentinel) for a push iteration
+__global__ void cc_list(int64_t n, const int* __restrict__ gp, int32_t* __restrict__ F,
+                        unsigned long long* __restrict__ count) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const bool l = gp[k] != kImax32;
+    const long long slot = warp_reserve(count, l ? 1 : 0);
     if (l) F[slot] = (int32_t)k;
   }
+}
+
+__global__ void widen_i32(int64_t n, const int* __restrict__ a, long long* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i];
 }
 
 }  // namespace gb
@@ -486,7 +542,7 @@ gb_status gb_pagerank(gb_ctx* ctx, const gb_csr* pull, const int64_t* out_offset
     // the last iteration must land in ranks_out: pick buffers so it does
     double* prev = rk[cur];
     double* next = rk[cur ^ 1];
-    pr_epilogue<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(n, tele, inv, spread, prev, next, y,
+    pr_epilogue<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, tele, inv, spread, prev, next, y,
                                                          scal, (unsigned long long*)(scal + 1));
     GB_LAUNCH_CHECK(ctx);
     count_launch(ctx, 3);
@@ -512,16 +568,17 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
                 double ratio, int32_t policy, int32_t sparsify, int64_t* parent,
                 int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   const int64_t n = rows->nrows;
+  if (n >= kImax32) return set_error(ctx, GB_ERR_UNSUPPORTED, "cc needs n < 2^31 - 1");
   Arena ar(ctx);
   cudaStream_t s = stream_of(ctx);
-  long long* P = reinterpret_cast<long long*>(parent);
-  long long* mn = ar.alloc<long long>(n);
-  long long* gp = ar.alloc<long long>(n);
-  long long* gpp = ar.alloc<long long>(n);
-  long long* pp = ar.alloc<long long>(n);
-  long long* hook = ar.alloc<long long>(n);
+  int* P = ar.alloc<int>(n);
+  int* mn = ar.alloc<int>(n);
+  int* gp = ar.alloc<int>(n);
+  int* gpp = ar.alloc<int>(n);
+  int* pp = ar.alloc<int>(n);
+  int* hook = ar.alloc<int>(n);
   int32_t* F = ar.alloc<int32_t>(n);
-  unsigned long long* cnt = ar.alloc<unsigned long long>(2);  // [changed, live]
+  unsigned long long* cnt = ar.alloc<unsigned long long>(3);  // [changed, live, listed]
   GB_ARENA_CHECK(ctx, ar);
   RowTilesPlan plan;
   GB_TRY(row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &plan));
@@ -529,7 +586,8 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 1);
   const int pull_grid = resident_grid(ctx, cc_pull, 256);
-  int64_t live = n, iters = 0, frontier_listed = 0;
+  const int vec_grid = grid_for(ctx, n, 256, 8);
+  int64_t live = n, iters = 0;
   for (int64_t it = 0; it < max_iters; ++it) {
     int64_t est = 0;
     const int32_t dir = gb_decide_direction(rows->nnz, rows->nrows, live, ratio, policy, &est);
@@ -537,8 +595,8 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
     log_nvals[it] = live;
     log_est[it] = est;
     iters = it + 1;
-    GB_CUDA(ctx, cudaMemcpyAsync(pp, P, sizeof(long long) * n, cudaMemcpyDeviceToDevice, s));
-    fill_i64<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, kImax, hook);
+    GB_CUDA(ctx, cudaMemcpyAsync(pp, P, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+    fill_i32<<<vec_grid, 256, 0, s>>>(n, kImax32, hook);
     const int ps = prof_begin(ctx, PROF_CC, live);
     if (dir == GB_DIR_PULL) {
       // mxv pull walks rows of A (kernels.py:313-316, row_view(False))
@@ -546,32 +604,31 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
                                                     plan.tile_first, gp, hook);
       count_launch(ctx, 1);
     } else if (live > 0) {
-      // push walks columns of A: rows of the CSC orientation
+      // push walks columns of A (rows of the CSC orientation) from the live
+      // grandparents, listed on demand
       if (!cols) return set_error(ctx, GB_ERR_FORMAT, "column-oriented storage missing");
-      if (!frontier_listed) {
-        // first iteration: every grandparent is live (gp = arange)
-        iota_i32<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, F);
-        count_launch(ctx, 1);
-      }
-      LbsPlan plan;
-      GB_TRY(lbs_prepare(ctx, ar, live, F, cols->offsets, cols->nnz, &plan));
+      GB_CUDA(ctx, cudaMemsetAsync(cnt + 2, 0, 8, s));
+      cc_list<<<vec_grid, 256, 0, s>>>(n, gp, F, cnt + 2);
+      LbsPlan lp;
+      GB_TRY(lbs_prepare(ctx, ar, live, F, cols->offsets, cols->nnz, &lp));
       CcPush f{cols->indices, F, gp, hook};
-      lbs_expand<CcPush><<<plan.grid, kLbsThreads, 0, s>>>(live, plan.S, plan.rowstart,
-                                                           plan.tile_first, f);
-      count_launch(ctx, 5);
+      lbs_expand<CcPush><<<lp.grid, kLbsThreads, 0, s>>>(live, lp.S, lp.rowstart, lp.tile_first, f);
+      count_launch(ctx, 7);
     }
     prof_end(ctx, ps);
-    cc_hook<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, hook, mn, pp, P);
+    cc_hook<<<vec_grid, 256, 0, s>>>(n, hook, mn, pp, P);
     GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
-    cc_shortcut<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, P, gp, gpp, sparsify, F, cnt, cnt + 1);
+    cc_shortcut<<<vec_grid, 256, 0, s>>>(n, P, gp, gpp, sparsify, cnt, cnt + 1);
     GB_LAUNCH_CHECK(ctx);
     count_launch(ctx, 5);
     int64_t h[2];
     GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 2));
-    frontier_listed = 1;
     if (h[0] == 0) break;  // algorithms.py:196-197
     live = h[1];
   }
+  widen_i32<<<vec_grid, 256, 0, s>>>(n, P, reinterpret_cast<long long*>(parent));
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
   *iters_out = iters;
   return GB_OK;
 }

@@ -19,13 +19,21 @@ __global__ void lbs_degrees(int64_t K, const int32_t* __restrict__ ids,
 
 __global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S, int64_t tile,
                                int32_t* __restrict__ tile_first) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = S[k], b = S[k + 1];
-    if (b <= a) continue;
-    // tiles whose first edge t*TE lies in [a, b)
-    int64_t t = (a + tile - 1) / tile;
-    for (; t * tile < b; ++t) tile_first[t] = (int32_t)k;
+  // one thread per TILE: binary search for the last entry whose start is <= the
+  // tile's first slot (empty entries share a start with the next entry, so the
+  // last one found is never empty).  Parallel over tiles, so a hub whose list
+  // spans thousands of tiles costs no more than any other entry.
+  const int64_t E = S[K];
+  const int64_t ntiles = (E + tile - 1) / tile;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t * tile;
+    int64_t lo = 0, hi = K - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (S[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    tile_first[t] = (int32_t)lo;
   }
 }
 
@@ -44,7 +52,8 @@ gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
   void* tmp = ar.raw(tb);
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, deg, plan->S, K + 1, s));
-  lbs_tile_first<<<grid_for(ctx, K, 256), 256, 0, s>>>(K, plan->S, tile, plan->tile_first);
+  lbs_tile_first<<<grid_for(ctx, max_edges / tile + 1, 256), 256, 0, s>>>(K, plan->S, tile,
+                                                                         plan->tile_first);
   GB_LAUNCH_CHECK(ctx);
   plan->grid = sm_count(ctx) * 4;
   return GB_OK;

@@ -152,13 +152,34 @@ __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* __restrict_
         f.template batch<B>(p, live);
       }
     } else {
-      for (int64_t i = lane; i < nk; i += 32) {
-        const int64_t k = k0 + i;
-        const int64_t sk = S[k], sk1 = S[k + 1];
-        const int64_t lo = sk > e0 ? sk : e0;
-        const int64_t hi = sk1 < e1 ? sk1 : e1;
-        const int64_t b = rowstart[k] - sk;
-        for (int64_t e = lo; e < hi; ++e) f.visit(b + e);
+      // many short lists: 8 entries per lane at a time, their bounds and first
+      // edges batched (one round trip for 256 entries), the rest walked
+      constexpr int B = 8;
+      for (int64_t i0 = 0; i0 < nk; i0 += 32 * B) {
+        int64_t lo[B], hi[B], base[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+          const int64_t i = i0 + r * 32 + lane;
+          lo[r] = hi[r] = base[r] = 0;
+          if (i < nk) {
+            const int64_t k = k0 + i;
+            const int64_t sk = S[k], sk1 = S[k + 1];
+            lo[r] = sk > e0 ? sk : e0;
+            hi[r] = sk1 < e1 ? sk1 : e1;
+            base[r] = rowstart[k] - sk;
+          }
+        }
+        int64_t p[B];
+        bool live[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+          live[r] = lo[r] < hi[r];
+          p[r] = base[r] + lo[r];
+        }
+        f.template batch<B>(p, live);
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+          for (int64_t e = lo[r] + 1; e < hi[r]; ++e) f.visit(base[r] + e);
       }
     }
   }
