@@ -336,6 +336,23 @@ gb_status gb_bfs_dist_unstamp(gb_ctx* ctx, int64_t K, const int32_t* F, int64_t*
 gb_status gb_csr_column_block(gb_ctx* ctx, const gb_csr* a, int64_t lo, int64_t hi,
                               int64_t* out_offsets, int32_t* out_indices, int64_t* nnz_host);
 
+/* ---- 1D-partitioned connected components (one rank's FastSV steps).
+ * int32 label vectors parent/mn/gp/gpp/pp/hook/prop are global-sized and
+ * replicated; `prop` is exchanged with an all-reduce MIN after
+ * gb_cc_dist_propose.  rowblock / colblock as for the partitioned BFS. */
+gb_status gb_cc_dist_init(gb_ctx* ctx, int64_t n, int32_t* parent, int32_t* mn, int32_t* gp,
+                          int32_t* gpp);
+gb_status gb_cc_dist_hook(gb_ctx* ctx, int32_t pull, const gb_csr* rowblock,
+                          const gb_csr* colblock, int64_t lo, int64_t hi, int64_t n,
+                          const int32_t* gp, const int32_t* parent, int32_t* pp, int32_t* hook);
+gb_status gb_cc_dist_propose(gb_ctx* ctx, int64_t n, int64_t lo, int64_t hi, const int32_t* hook,
+                             int32_t* mn, const int32_t* pp, int32_t* prop);
+gb_status gb_cc_dist_shortcut(gb_ctx* ctx, int64_t n, const int32_t* pp, const int32_t* prop,
+                              int32_t* parent, int32_t* gp, int32_t* gpp, int32_t sparsify,
+                              int64_t* changed_host, int64_t* live_host);
+/* int32 -> int64 widening of a label vector (the API returns int64 labels) */
+gb_status gb_widen_i32(gb_ctx* ctx, int64_t n, const int32_t* in, int64_t* out);
+
 /* Per-iteration host callback of the fused drivers (the sssp on_iteration hook). */
 typedef void (*gb_iter_cb)(int64_t iteration, void* user);
 

@@ -121,6 +121,12 @@ SIGNATURES = {
     "gb_bfs_dist_apply": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, pi64]),
     "gb_bfs_dist_unstamp": (i32, [vp, i64, vp, vp]),
     "gb_csr_column_block": (i32, [vp, C.POINTER(gb_csr), i64, i64, vp, vp, pi64]),
+    "gb_cc_dist_init": (i32, [vp, i64, vp, vp, vp, vp]),
+    "gb_cc_dist_hook": (i32, [vp, i32, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, i64, i64, vp,
+                              vp, vp, vp]),
+    "gb_cc_dist_propose": (i32, [vp, i64, i64, i64, vp, vp, vp, vp]),
+    "gb_cc_dist_shortcut": (i32, [vp, i64, vp, vp, vp, vp, vp, i32, pi64, pi64]),
+    "gb_widen_i32": (i32, [vp, i64, vp, vp]),
 }
 
 ITER_CB = C.CFUNCTYPE(None, C.c_int64, C.c_void_p)

@@ -634,3 +634,150 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// 1D-partitioned connected components (one rank's steps; the loop and the
+// all-reduce MIN of the parent proposals live in distributed.py).  Label
+// vectors are int32, global-sized and replicated; hook/mn are meaningful on
+// the rank's own vertices [lo, hi) only.
+// ---------------------------------------------------------------------------
+namespace gb {
+
+struct CcMinBlock {
+  const int* __restrict__ gp;
+  int* __restrict__ hook;  // rebased: local row r writes hook[lo + r]
+  __device__ __forceinline__ int identity() const { return kImax32; }
+  __device__ __forceinline__ int load(int64_t, int32_t col) const { return __ldg(gp + col); }
+  __device__ __forceinline__ int fold(int a, int x) const { return x < a ? x : a; }
+  __device__ __forceinline__ void emit(int64_t row, int acc, bool whole) const {
+    if (acc == kImax32) return;
+    if (whole) hook[row] = acc;
+    else atomicMin(hook + row, acc);
+  }
+};
+
+__global__ void __launch_bounds__(256)
+cc_pull_block(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
+              const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
+              const int* __restrict__ gp, int* __restrict__ hook_rebased) {
+  CcMinBlock red{gp, hook_rebased};
+  row_tiles<int>(R, nz_rows, nz_off, idx, tile_first, red);
+}
+
+// owned k: mn[k] = min(mn[k], hook[k]); prop[k] min= mn[k]; prop[pp[k]] min= mn[k]
+__global__ void cc_propose(int64_t lo, int64_t hi, const int* __restrict__ hook,
+                           int* __restrict__ mn, const int* __restrict__ pp,
+                           int* __restrict__ prop) {
+  for (int64_t k = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < hi;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int m = mn[k];
+    const int h = hook[k];
+    if (h < m) { m = h; mn[k] = m; }
+    if (m < *reinterpret_cast<volatile int*>(prop + k)) atomicMin(prop + k, m);
+    const int t = pp[k];
+    if (m < *reinterpret_cast<volatile int*>(prop + t)) atomicMin(prop + t, m);
+  }
+}
+
+// parent = min(pp, all-reduced proposals)
+__global__ void cc_merge(int64_t n, const int* __restrict__ pp, const int* __restrict__ prop,
+                         int* __restrict__ parent) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    parent[k] = min(pp[k], prop[k]);
+}
+
+}  // namespace gb
+
+extern "C" {
+
+gb_status gb_cc_dist_init(gb_ctx* ctx, int64_t n, int32_t* parent, int32_t* mn, int32_t* gp,
+                          int32_t* gpp) {
+  if (n >= kImax32) return set_error(ctx, GB_ERR_UNSUPPORTED, "cc needs n < 2^31 - 1");
+  cc_init<<<grid_for(ctx, n, 256, 8), 256, 0, stream_of(ctx)>>>(n, parent, mn, gp, gpp);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  return GB_OK;
+}
+
+// hooked values of the owned vertices (pull over the row block, or push over
+// the column block from the live grandparents).  hook is reset to the
+// sentinel first; pp <- parent (the iteration's parent_prev snapshot).
+gb_status gb_cc_dist_hook(gb_ctx* ctx, int32_t pull, const gb_csr* rowblock,
+                          const gb_csr* colblock, int64_t lo, int64_t hi, int64_t n,
+                          const int32_t* gp, const int32_t* parent, int32_t* pp, int32_t* hook) {
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  const int vg = grid_for(ctx, n, 256, 8);
+  GB_CUDA(ctx, cudaMemcpyAsync(pp, parent, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  fill_i32<<<vg, 256, 0, s>>>(n, kImax32, hook);
+  count_launch(ctx, 2);
+  if (pull) {
+    if (rowblock->nnz == 0 || hi <= lo) return GB_OK;
+    RowTilesPlan plan;
+    GB_TRY(row_tiles_plan(ctx, ar, hi - lo, rowblock->offsets, rowblock->nnz, &plan));
+    if (plan.R)
+      cc_pull_block<<<resident_grid(ctx, cc_pull_block, 256), 256, 0, s>>>(
+          plan.R, plan.nz_rows, plan.nz_off, rowblock->indices, plan.tile_first, gp, hook + lo);
+    count_launch(ctx, 1);
+  } else {
+    if (colblock->nnz == 0) return GB_OK;
+    int32_t* F = ar.alloc<int32_t>(n);
+    unsigned long long* cnt = ar.alloc<unsigned long long>(1);
+    GB_ARENA_CHECK(ctx, ar);
+    GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 8, s));
+    cc_list<<<vg, 256, 0, s>>>(n, gp, F, cnt);
+    int64_t K = 0;
+    GB_TRY(read_i64(ctx, (const int64_t*)cnt, &K));
+    if (K > 0) {
+      LbsPlan lp;
+      GB_TRY(lbs_prepare(ctx, ar, K, F, colblock->offsets, colblock->nnz, &lp));
+      CcPush f{colblock->indices, F, gp, hook};
+      lbs_expand<CcPush><<<lp.grid, kLbsThreads, 0, s>>>(K, lp.S, lp.rowstart, lp.tile_first, f);
+      count_launch(ctx, 6);
+    }
+  }
+  GB_LAUNCH_CHECK(ctx);
+  return GB_OK;
+}
+
+// proposals of the owned vertices for the all-reduce MIN (prop reset first)
+gb_status gb_cc_dist_propose(gb_ctx* ctx, int64_t n, int64_t lo, int64_t hi, const int32_t* hook,
+                             int32_t* mn, const int32_t* pp, int32_t* prop) {
+  cudaStream_t s = stream_of(ctx);
+  fill_i32<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, kImax32, prop);
+  if (hi > lo) cc_propose<<<grid_for(ctx, hi - lo, 256, 8), 256, 0, s>>>(lo, hi, hook, mn, pp, prop);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2);
+  return GB_OK;
+}
+
+// parent = min(pp, prop); gp = parent[parent]; changed / live counts (sync)
+gb_status gb_cc_dist_shortcut(gb_ctx* ctx, int64_t n, const int32_t* pp, const int32_t* prop,
+                              int32_t* parent, int32_t* gp, int32_t* gpp, int32_t sparsify,
+                              int64_t* changed_host, int64_t* live_host) {
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  unsigned long long* cnt = ar.alloc<unsigned long long>(2);
+  GB_ARENA_CHECK(ctx, ar);
+  const int vg = grid_for(ctx, n, 256, 8);
+  cc_merge<<<vg, 256, 0, s>>>(n, pp, prop, parent);
+  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
+  cc_shortcut<<<vg, 256, 0, s>>>(n, parent, gp, gpp, sparsify, cnt, cnt + 1);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 3);
+  int64_t h[2];
+  GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 2));
+  *changed_host = h[0];
+  *live_host = h[1];
+  return GB_OK;
+}
+
+gb_status gb_widen_i32(gb_ctx* ctx, int64_t n, const int32_t* in, int64_t* out) {
+  if (n) widen_i32<<<grid_for(ctx, n, 256, 8), 256, 0, stream_of(ctx)>>>(n, in, (long long*)out);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  return GB_OK;
+}
+
+}  // extern "C"

@@ -120,6 +120,96 @@ class NumpySteps:
         self.levels[self.F[:K]] = 0
 
 
+class NumpyCCSteps:
+    """Same contract as NativeCCSteps (gb_cc_dist_*), restated in numpy."""
+
+    MAX = np.iinfo(np.int32).max
+
+    def __init__(self, g):
+        self.g = g
+        n = g.n
+        self.parent = np.arange(n, dtype=np.int64)
+        self.mn = self.parent.copy()
+        self.gp = self.parent.copy()
+        self.gpp = self.parent.copy()
+        self.pp = self.parent.copy()
+        self.prop = torch.full((n,), self.MAX, dtype=torch.int32)
+
+    def init(self):
+        pass
+
+    def hook_and_propose(self, pull):
+        g, M = self.g, self.MAX
+        self.pp = self.parent.copy()
+        hook = np.full(g.n, M, np.int64)
+        if pull:
+            for i in range(g.lo, g.hi):
+                nb = self.gp[g.ci[g.rp[i]:g.rp[i + 1]]]
+                nb = nb[nb != M]
+                if nb.size:
+                    hook[i] = nb.min()
+        else:
+            for j in np.flatnonzero(self.gp != M):
+                for i in g.ci[g.rp[j]:g.rp[j + 1]]:
+                    if g.lo <= i < g.hi:
+                        hook[i] = min(hook[i], self.gp[j])
+        prop = np.full(g.n, M, np.int64)
+        for k in range(g.lo, g.hi):
+            m = min(self.mn[k], hook[k])
+            self.mn[k] = m
+            prop[k] = min(prop[k], m)
+            prop[self.pp[k]] = min(prop[self.pp[k]], m)
+        self.prop[:] = torch.from_numpy(prop.astype(np.int32))
+
+    def shortcut(self, sparsify):
+        self.parent = np.minimum(self.pp, self.prop.numpy().astype(np.int64))
+        g = self.parent[self.parent]
+        changed = g != self.gpp
+        self.gpp = g.copy()
+        self.gp = np.where(changed | (not sparsify), g, self.MAX)
+        return int(changed.sum()), int((self.gp != self.MAX).sum())
+
+    def result(self):
+        return self.parent.copy()
+
+
+def _cc_worker(rank, world, port_, scale, sparsify, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1908_01407_b200.containers import Descriptor
+    from paper_1908_01407_b200.distributed import TorchMinExchange, cc_partitioned
+    rp, ci, n = port.rmat_csr(scale)
+    bounds = partition_bounds(rp, world)
+    g = Block(rp, ci, bounds[rank], bounds[rank + 1])
+    desc = Descriptor()
+    labels = cc_partitioned(g, desc, sparsify, steps=NumpyCCSteps(g), exchange=TorchMinExchange())
+    results[rank] = (labels, [(d.chosen, d.frontier_nvals) for d in desc.direction_log])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scale,sparsify", [(10, True), (11, False)])
+def test_partitioned_cc_world2_matches_oracle(scale, sparsify):
+    ctx = mp.get_context("spawn")
+    results = ctx.Manager().dict()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_cc_worker, args=(r, 2, port_, scale, sparsify, results))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    rp, ci, n = port.rmat_csr(scale)
+    P = port.mat_from_csr(rp, ci, np.ones(ci.size, np.int64), n)
+    pd = port.Desc()
+    want = port.connected_components(P, pd, sparsify=sparsify)
+    for r in range(2):
+        labels, trace = results[r]
+        assert np.array_equal(labels, want.vals)
+        assert trace == [(x[0], x[1]) for x in pd.log]
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

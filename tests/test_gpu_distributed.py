@@ -65,6 +65,50 @@ def test_partitioned_equals_single(scale, P):
             [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
 
 
+def lockstep_cc(A, P, desc, sparsify=True):
+    from paper_1908_01407_b200.distributed import BlockGraph, NativeCCSteps, partition_bounds
+    from paper_1908_01407_b200.kernels import DirectionDecision, direction_rule
+    bounds = partition_bounds(A._csr.offsets.cpu().numpy(), P)
+    ranks = [NativeCCSteps(BlockGraph.from_matrix(A, r, P, bounds)) for r in range(P)]
+    g = ranks[0].g
+    for st in ranks:
+        st.init()
+    live = g.n
+    for _ in range(desc.max_niter):
+        chosen, est, thr = direction_rule(g.nnz, g.n, live, desc.switch_ratio, desc.direction)
+        desc.direction_log.append(DirectionDecision(chosen, live, est, g.nnz, thr))
+        for st in ranks:
+            st.hook_and_propose(chosen == "pull")
+        total = ranks[0].prop.clone()
+        for st in ranks[1:]:
+            total = torch.minimum(total, st.prop)
+        for st in ranks:
+            st.prop.copy_(total)
+        outs = [st.shortcut(sparsify) for st in ranks]
+        assert len(set(outs)) == 1
+        changed, live = outs[0]
+        if changed == 0:
+            break
+    res = [st.result().cpu().numpy() for st in ranks]
+    for r in res[1:]:
+        assert np.array_equal(r, res[0])
+    return res[0]
+
+
+@pytest.mark.parametrize("scale", [12, 18])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_partitioned_cc_equals_single(scale, P):
+    import paper_1908_01407_b200 as gb
+    A = gb.io.rmat_matrix(scale)
+    for sparsify in (True, False):
+        d1, d2 = gb.Descriptor(), gb.Descriptor()
+        want = gb.connected_components(A, desc=d1, sparsify=sparsify).values
+        got = lockstep_cc(A, P, d2, sparsify)
+        assert np.array_equal(got, want)
+        assert [(x.chosen, x.frontier_nvals) for x in d1.direction_log] == \
+            [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
+
+
 def test_partitioned_world1_entry_point():
     import paper_1908_01407_b200 as gb
     from paper_1908_01407_b200 import distributed
