@@ -39,121 +39,14 @@ struct EdgeOn {
 // ---------------------------------------------------------------------------
 // push: load-balanced expansion of the frontier's out-edges
 // ---------------------------------------------------------------------------
-constexpr int kExpThreads = 256;
-constexpr int kExpItems = 16;
-constexpr int kExpTile = kExpThreads * kExpItems;  // 4096 edges per tile
-constexpr int kExpVcap = 1024;                     // frontier entries per tile (owner-map path)
-static_assert(kExpTile == kLbsTile, "tile_first is computed for kLbsTile");
-
-// One CTA per tile of kExpTile consecutive expansion slots.  Owner lookup is a
-// shared-memory table built by marking each frontier entry's first slot and a
-// block-wide max-scan, so every edge costs one LDS for its owner and its column
-// index load is coalesced with its neighbours'.  The 16 column loads of a
-// thread are issued before any probe (memory-level parallelism).
-// Marking: the live visited bitmap `vbm` is probed through L2 (ld.cg, always
-// current) and a clear bit is set with one atomicOr, so a vertex reached by
-// many frontier edges costs one read per edge but (almost) one write in total.
-// bfs_finalize recovers the new frontier as vbm & ~vprev.
+// Marking: the live visited bitmap `vbm` is probed through L1 (ld.ca: a stale
+// clear bit only costs a redundant atomic) and a clear bit is set with one
+// atomicOr, so a vertex reached by many frontier edges costs one read per edge
+// but (almost) one write in total.  bfs_finalize recovers the new frontier as
+// vbm & ~vprev.
 __device__ __forceinline__ void mark(uint32_t* vbm, int32_t v, uint32_t word) {
   const uint32_t bit = 1u << (v & 31);
   if (!(word & bit)) atomicOr(vbm + (v >> 5), bit);
-}
-
-template <bool VALS>
-__global__ void __launch_bounds__(kExpThreads, 4)
-bfs_expand(int64_t K, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
-           const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx, EdgeOn on,
-           uint32_t* __restrict__ vbm) {
-  using BlockScan = cub::BlockScan<int, kExpThreads>;
-  __shared__ int64_t s_delta[kExpVcap];
-  __shared__ __align__(16) uint16_t s_own[kExpTile];
-  __shared__ typename BlockScan::TempStorage s_scan;
-  const int tid = threadIdx.x;
-  const int64_t E = S[K];
-  const int64_t ntiles = (E + kExpTile - 1) / kExpTile;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t e0 = t * kExpTile;
-    const int64_t e1 = e0 + kExpTile < E ? e0 + kExpTile : E;
-    const int64_t k0 = tile_first[t];
-    const int64_t k1 = t + 1 < ntiles ? tile_first[t + 1] : K - 1;
-    const int64_t nk = k1 - k0 + 1;
-    if (nk <= kExpVcap) {
-      uint4* own4 = reinterpret_cast<uint4*>(s_own);
-      own4[2 * tid] = make_uint4(0, 0, 0, 0);
-      own4[2 * tid + 1] = make_uint4(0, 0, 0, 0);
-      __syncthreads();
-      for (int64_t i = tid; i < nk; i += kExpThreads) {
-        const int64_t k = k0 + i;
-        const int64_t sk = S[k], sk1 = S[k + 1];
-        s_delta[i] = rowstart[k] - sk;
-        if (sk1 > sk) {
-          const int64_t st = (sk > e0 ? sk : e0) - e0;
-          if (st < e1 - e0) s_own[st] = (uint16_t)(i + 1);
-        }
-      }
-      __syncthreads();
-      // block max-scan over s_own: thread tid owns slots [16 tid, 16 tid + 16)
-      uint4 a = own4[2 * tid], b = own4[2 * tid + 1];
-      uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      int run = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        run = max(run, (int)(wv[j] & 0xffffu));
-        run = max(run, (int)(wv[j] >> 16));
-      }
-      int pre;
-      BlockScan(s_scan).ExclusiveScan(run, pre, 0, cub::Max());
-      run = pre;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        int lo16 = max(run, (int)(wv[j] & 0xffffu));
-        int hi16 = max(lo16, (int)(wv[j] >> 16));
-        run = hi16;
-        wv[j] = (uint32_t)lo16 | ((uint32_t)hi16 << 16);
-      }
-      __syncthreads();
-      own4[2 * tid] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-      own4[2 * tid + 1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
-      __syncthreads();
-#pragma unroll
-      for (int half = 0; half < kExpItems; half += kExpItems / 2) {
-        constexpr int B = kExpItems / 2;
-        int32_t v[B];
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-          const int el = (half + r) * kExpThreads + tid;
-          v[r] = -1;
-          if (e0 + el < e1) {
-            const int i = (int)s_own[el] - 1;
-            const int64_t p = s_delta[i] + e0 + el;
-            const int32_t c = ld_stream(idx + p);
-            v[r] = (!VALS || on(p)) ? c : -1;
-          }
-        }
-        uint32_t word[B];
-#pragma unroll
-        for (int r = 0; r < B; ++r) word[r] = v[r] >= 0 ? ld_probe(vbm + (v[r] >> 5)) : ~0u;
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-          if (v[r] >= 0) mark(vbm, v[r], word[r]);
-      }
-      __syncthreads();
-    } else {
-      // many tiny adjacency lists in one tile: one thread per frontier entry
-      for (int64_t i = tid; i < nk; i += kExpThreads) {
-        const int64_t k = k0 + i;
-        const int64_t sk = S[k], sk1 = S[k + 1];
-        const int64_t lo = sk > e0 ? sk : e0;
-        const int64_t hi = sk1 < e1 ? sk1 : e1;
-        const int64_t base = rowstart[k] - sk;
-        for (int64_t e = lo; e < hi; ++e) {
-          const int64_t p = base + e;
-          const int32_t u = __ldg(idx + p);
-          if (!VALS || on(p)) mark(vbm, u, ld_probe(vbm + (u >> 5)));
-        }
-      }
-    }
-  }
 }
 
 // Warp-tile push expansion (no shared memory, no barriers): a batch of
@@ -416,6 +309,23 @@ __global__ void bfs_unstamp(int64_t K, const int32_t* __restrict__ F, int64_t* _
     levels[F[i]] = 0;
 }
 
+// (A shared-memory cache of the low-id visited words was tried here and lost:
+// bank conflicts and halved occupancy cost more than the saved L1 sectors.)
+template <bool VALS>
+static gb_status launch_push_t(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
+                               EdgeOn on, uint32_t* vbm) {
+  bfs_expand_warp<VALS><<<resident_grid(ctx, bfs_expand_warp<VALS>, 256), 256, 0, stream_of(ctx)>>>(
+      K, plan.S, plan.rowstart, plan.tile_first, a->indices, on, vbm);
+  GB_LAUNCH_CHECK(ctx);
+  return GB_OK;
+}
+
+static gb_status launch_push(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
+                             EdgeOn on, uint32_t* vbm) {
+  return a->values ? launch_push_t<true>(ctx, K, plan, a, on, vbm)
+                   : launch_push_t<false>(ctx, K, plan, a, on, vbm);
+}
+
 }  // namespace gb
 
 using namespace gb;
@@ -494,12 +404,7 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
         LbsPlan plan;
         GB_TRY(lbs_prepare(ctx, ar, K, F, push->offsets, push->nnz, &plan, kWarpTile));
         const int ps = prof_begin(ctx, PROF_BFS_PUSH, K);
-        if (push->values)
-          bfs_expand_warp<true><<<resident_grid(ctx, bfs_expand_warp<true>, 256), 256, 0, s>>>(K, plan.S, plan.rowstart, plan.tile_first,
-                                                  push->indices, push_on, vbm);
-        else
-          bfs_expand_warp<false><<<resident_grid(ctx, bfs_expand_warp<false>, 256), 256, 0, s>>>(K, plan.S, plan.rowstart, plan.tile_first,
-                                                   push->indices, push_on, vbm);
+        GB_TRY(launch_push(ctx, K, plan, push, push_on, vbm));
         prof_end(ctx, ps);
         count_launch(ctx, 5);  // degrees, scan (2), tile_first, expand
       }
@@ -566,12 +471,7 @@ gb_status gb_bfs_dist_push(gb_ctx* ctx, const gb_csr* colblock, int64_t K, const
   GB_TRY(lbs_prepare(ctx, ar, K, F, colblock->offsets, colblock->nnz, &plan, kWarpTile));
   const EdgeOn on{colblock->values, colblock->dtype};
   const int ps = prof_begin(ctx, PROF_BFS_PUSH, K);
-  if (colblock->values)
-    bfs_expand_warp<true><<<resident_grid(ctx, bfs_expand_warp<true>, 256), 256, 0, s>>>(
-        K, plan.S, plan.rowstart, plan.tile_first, colblock->indices, on, vbm);
-  else
-    bfs_expand_warp<false><<<resident_grid(ctx, bfs_expand_warp<false>, 256), 256, 0, s>>>(
-        K, plan.S, plan.rowstart, plan.tile_first, colblock->indices, on, vbm);
+  GB_TRY(launch_push(ctx, K, plan, colblock, on, vbm));
   prof_end(ctx, ps);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 5);
