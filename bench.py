@@ -154,6 +154,7 @@ def run_ours(args):
 
     import paper_1908_01407_b200 as gb
     from paper_1908_01407_b200 import _lib
+    from paper_1908_01407_b200.containers import to_host
     from paper_1908_01407_b200.io import rmat_matrix
 
     rank, world, local = env_rank()
@@ -224,8 +225,8 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     push_times = [(arg, t) for (kind, arg, t) in prof if kind == 1]
     if push_times:
-        # dominant launch: the push expansion with the largest frontier (level 2 at s24)
-        k, t_ms = max(push_times, key=lambda x: x[0])
+        # dominant launch: the longest push expansion (level 2 at s24)
+        k, t_ms = max(push_times, key=lambda x: x[1])
         lvl = next(i for i, (c, nv) in enumerate(trace) if c == "push" and nv == k)
         deg = np.diff(A._csr.offsets.cpu().numpy())
         front = np.flatnonzero(levels_host == lvl + 1)
@@ -242,12 +243,17 @@ def run_ours(args):
                 "level_ms": [(kind, a, round(t, 4)) for (kind, a, t) in prof]}
 
     # ---- end-to-end through the public API (host result every step) --------
+    # warm-up: the first calls allocate the pinned staging blocks (~57 ms each
+    # for 134 MB); torch's caching host allocator reuses them afterwards
+    for i in range(max(args.warmup, 2)):
+        out = to_host(step()) if world > 1 else gb.bfs(A, args.source).values
+    torch.cuda.synchronize()
     t_e2e = []
     for i in range(args.steps):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         if world > 1:
-            out = step().cpu().numpy()           # replicated levels -> host
+            out = to_host(step())                # replicated levels -> host (pinned D2H)
         else:
             out = gb.bfs(A, args.source).values  # levels -> host numpy (pinned D2H)
         t_e2e.append(time.perf_counter() - t1)
