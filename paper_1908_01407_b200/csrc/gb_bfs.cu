@@ -4,19 +4,24 @@
 //
 // Per level the reference does  assign(visited, depth, mask=f)  ->
 // vxm(LogicalOrAnd, f, A, mask=~visited)  ->  reduce(Plus, f).  Here:
-//   push level:  lbs_expand over the frontier list marks unvisited
-//                neighbours in a byte array (plain stores, idempotent OR),
-//                then bfs_finalize turns the marks into the next frontier
-//                (bitmap + list + count), stamps levels and the visited
-//                bitmap in one pass.
+//   push level:  warp-tile expansion of the frontier list sets unvisited
+//                neighbours' bits in the visited bitmap (probe, then
+//                atomicOr), then bfs_finalize turns vbm & ~vprev into the
+//                next frontier (bitmap + list + count) and stamps levels.
 //   pull level:  bfs_pull walks in-edges of unvisited, non-isolated rows
-//                (one lane per row, warp per 32 rows) and stops at the first
-//                frontier hit (early exit, kernels.py:169-178); it writes the
-//                next frontier directly -- no separate finalize.
-// The direction of every level is decided on the host with the reference
-// rule (gb_decide_direction) from the exact frontier count, so the direction
-// trace equals the reference's.
+//                (candidate lists per warp of 32 words) and stops at the
+//                first frontier hit (early exit, kernels.py:169-178); it
+//                writes the next frontier directly -- no separate finalize.
+// The direction of every level follows the reference rule on the exact
+// frontier count, so the direction trace equals the reference's.  The level
+// loop runs on the device inside one CUDA graph (bfs_graph_run); the
+// host-driven loop below it remains for per-kernel profiling and the
+// 1D-partitioned steps.
 #include <math.h>
+#include <stddef.h>
+#include <stdlib.h>
+
+#include <vector>
 
 #include "gb_common.cuh"
 #include "gb_lbs.cuh"
@@ -82,9 +87,10 @@ struct PushBits {
 
 template <bool VALS>
 __global__ void __launch_bounds__(256)
-bfs_expand_warp(int64_t K, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
+bfs_expand_warp(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
                 const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
                 EdgeOn on, uint32_t* __restrict__ vbm) {
+  const int64_t K = Kd.get();
   PushBits<VALS> f{idx, on, vbm};
   warp_tiles(K, S, rowstart, tile_first, f);
 }
@@ -102,14 +108,16 @@ __global__ void bfs_init(int64_t source, int64_t* levels, uint32_t* vbm, uint32_
 // visited bitmap against the level-start snapshot, then the warp walks the
 // non-empty words so level stamps and frontier-list writes are coalesced.
 __global__ void __launch_bounds__(256)
-bfs_finalize(int64_t n, int64_t depth, uint32_t* __restrict__ vbm,
+bfs_finalize(int64_t n, DevI64 depth_d, uint32_t* __restrict__ vbm,
              uint32_t* __restrict__ vprev, uint32_t* __restrict__ fbm_next,
-             int64_t* __restrict__ levels, int32_t* __restrict__ F,
+             DevP64 levels_d, int32_t* __restrict__ F,
              unsigned long long* __restrict__ count,
              unsigned long long* __restrict__ count_clear, const uint32_t* __restrict__ xbm) {
   // xbm == NULL: new frontier = vbm & ~vprev (single GPU).  xbm != NULL: the
   // all-reduced new-frontier bitmap of a 1D-partitioned run is authoritative.
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
+  const int64_t depth = depth_d.get();
+  int64_t* __restrict__ levels = levels_d.get();
   const int lane = threadIdx.x & 31;
   const int64_t W = (n + 31) / 32;
   const int64_t G = (W + 31) / 32;
@@ -168,10 +176,10 @@ constexpr int kPullList = 32 * kPullBatch;   // rows per warp per pass
 constexpr int kPullSerial = 8;               // entries a lane scans alone before the warp helps
 
 __global__ void __launch_bounds__(256)
-bfs_pull(int64_t n, int64_t depth, const int64_t* __restrict__ off,
+bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
          const int32_t* __restrict__ idx, EdgeOn on, const uint32_t* __restrict__ nonempty,
          uint32_t* __restrict__ vbm, uint32_t* __restrict__ vprev, const uint32_t* __restrict__ fbm,
-         uint32_t* __restrict__ fbm_next, int64_t* __restrict__ levels,
+         uint32_t* __restrict__ fbm_next, DevP64 levels_d,
          int32_t* __restrict__ F, unsigned long long* __restrict__ count,
          unsigned long long* __restrict__ count_clear, int64_t g_lo, int64_t g_hi) {
   // [g_lo, g_hi): groups of 32 words (1024 vertices) this launch owns; a
@@ -180,6 +188,8 @@ bfs_pull(int64_t n, int64_t depth, const int64_t* __restrict__ off,
   __shared__ int32_t s_list[8][kPullList];
   __shared__ uint32_t s_new[8][32];
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
+  const int64_t depth = depth_d.get();
+  int64_t* __restrict__ levels = levels_d.get();
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int64_t W = (n + 31) / 32;
@@ -303,7 +313,8 @@ bfs_pull(int64_t n, int64_t depth, const int64_t* __restrict__ off,
   }
 }
 
-__global__ void bfs_unstamp(int64_t K, const int32_t* __restrict__ F, int64_t* __restrict__ levels) {
+__global__ void bfs_unstamp(DevI64 Kd, const int32_t* __restrict__ F, int64_t* __restrict__ levels) {
+  const int64_t K = Kd.get();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
        i += (int64_t)gridDim.x * blockDim.x)
     levels[F[i]] = 0;
@@ -315,7 +326,7 @@ template <bool VALS>
 static gb_status launch_push_t(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
                                EdgeOn on, uint32_t* vbm) {
   bfs_expand_warp<VALS><<<resident_grid(ctx, bfs_expand_warp<VALS>, 256), 256, 0, stream_of(ctx)>>>(
-      K, plan.S, plan.rowstart, plan.tile_first, a->indices, on, vbm);
+      dval(K), plan.S, plan.rowstart, plan.tile_first, a->indices, on, vbm);
   GB_LAUNCH_CHECK(ctx);
   return GB_OK;
 }
@@ -324,6 +335,483 @@ static gb_status launch_push(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const 
                              EdgeOn on, uint32_t* vbm) {
   return a->values ? launch_push_t<true>(ctx, K, plan, a, on, vbm)
                    : launch_push_t<false>(ctx, K, plan, a, on, vbm);
+}
+
+// ---------------------------------------------------------------------------
+// Device-driven BFS.  The whole level loop is one CUDA
+// graph: a WHILE conditional node whose body holds two unrolled iterations
+// (even / odd, so the frontier-bitmap double buffer and the level counters
+// are static pointers), each
+//     decide  ->  IF push ELSE pull  ->  advance
+// The reference direction rule (kernels.py:108-126, rint = half-even like
+// Python round), the decision log, the loop cap min(max_niter, n+1) and the
+// unstamp of the last frontier (algorithms.py:69-76) all run on the device,
+// so a BFS is one graph launch plus one readback instead of a host round trip
+// per level.  The push body's degree scan reads the frontier size from device
+// memory (three small kernels instead of CUB, whose item count is a host
+// value).  The instantiated graph and its scratch are cached per context and
+// matrix; per-call inputs (source, cap, output and log pointers, rule
+// parameters) live in a device state block written before each launch.
+// ---------------------------------------------------------------------------
+struct BfsState {
+  int64_t* levels;      // per call
+  int64_t* log;         // per call: [iters, (dir, K, est) x cap]
+  int64_t source, cap;  // per call
+  double ratio;         // per call
+  int32_t policy, pad_;
+  int64_t it, K, depth, dnext, unstamp;  // loop state
+};
+
+constexpr int kGScanBlocks = 592;  // <= 1024 (single-block top scan)
+constexpr int kGScanThreads = 256;
+constexpr int kGScanItems = 4;
+constexpr int64_t kGraphMaxCap = 1 << 20;  // longer loop caps use the host-driven path
+
+__device__ __forceinline__ void g_range(int64_t K, int64_t* lo, int64_t* hi) {
+  const int64_t per = (K + gridDim.x - 1) / gridDim.x;
+  *lo = blockIdx.x * per;
+  *hi = *lo + per < K ? *lo + per : K;
+}
+
+__global__ void __launch_bounds__(kGScanThreads)
+g_scan_partials(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
+                const int64_t* __restrict__ off, int64_t* __restrict__ part) {
+  using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
+  __shared__ typename BlockReduce::TempStorage tmp;
+  int64_t lo, hi;
+  g_range(*Kp, &lo, &hi);
+  int64_t sum = 0;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += kGScanThreads) {
+    const int64_t v = F[k];
+    sum += __ldg(off + v + 1) - __ldg(off + v);
+  }
+  const int64_t tot = BlockReduce(tmp).Sum(sum);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) g_scan_top(int nb, int64_t* __restrict__ part) {
+  using BlockScan = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  const int64_t x = threadIdx.x < nb ? part[threadIdx.x] : 0;
+  int64_t pre, agg;
+  BlockScan(tmp).ExclusiveSum(x, pre, agg);
+  if (threadIdx.x < nb) part[threadIdx.x] = pre;
+  if (threadIdx.x == 0) part[nb] = agg;
+}
+
+// rowstart[k] = off[F[k]], S = exclusive scan of the degrees, S[K] = E
+__global__ void __launch_bounds__(kGScanThreads)
+g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
+             const int64_t* __restrict__ off, const int64_t* __restrict__ part,
+             int64_t* __restrict__ rowstart, int64_t* __restrict__ S) {
+  using BlockScan = cub::BlockScan<int64_t, kGScanThreads>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  const int64_t K = *Kp;
+  int64_t lo, hi;
+  g_range(K, &lo, &hi);
+  if (blockIdx.x == 0 && threadIdx.x == 0) S[K] = part[gridDim.x];
+  int64_t run = part[blockIdx.x];
+  for (int64_t base = lo; base < hi; base += kGScanThreads * kGScanItems) {
+    int64_t d[kGScanItems];
+    int64_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kGScanItems; ++i) {
+      const int64_t k = base + threadIdx.x * kGScanItems + i;
+      d[i] = 0;
+      if (k < hi) {
+        const int64_t v = F[k];
+        const int64_t a = __ldg(off + v);
+        d[i] = __ldg(off + v + 1) - a;
+        rowstart[k] = a;
+      }
+      sum += d[i];
+    }
+    int64_t pre, agg;
+    BlockScan(tmp).ExclusiveSum(sum, pre, agg);
+    int64_t acc = run + pre;
+#pragma unroll
+    for (int i = 0; i < kGScanItems; ++i) {
+      const int64_t k = base + threadIdx.x * kGScanItems + i;
+      if (k < hi) S[k] = acc;
+      acc += d[i];
+    }
+    run += agg;
+    __syncthreads();
+  }
+}
+
+__global__ void g_tile_first(const int64_t* __restrict__ Kp, const int64_t* __restrict__ S,
+                             int32_t* __restrict__ tile_first) {
+  const int64_t K = *Kp;
+  const int64_t E = S[K];
+  const int64_t ntiles = (E + kWarpTile - 1) / kWarpTile;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t * kWarpTile;
+    int64_t lo = 0, hi = K - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (S[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    tile_first[t] = (int32_t)lo;
+  }
+}
+
+__global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
+  int64_t* lv = st->levels;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lv[i] = 0;
+}
+
+__global__ void g_start(BfsState* st, uint32_t* vbm, uint32_t* vprev, uint32_t* fbm0, int32_t* F,
+                        cudaGraphConditionalHandle h_loop) {
+  const int64_t s = st->source;
+  st->levels[s] = 1;
+  const uint32_t bit = 1u << (s & 31);
+  vbm[s >> 5] |= bit;
+  vprev[s >> 5] |= bit;
+  fbm0[s >> 5] |= bit;
+  F[0] = (int32_t)s;
+  st->it = 0;
+  st->K = 1;
+  st->depth = 1;
+  st->unstamp = 0;
+  st->log[0] = 0;
+  cudaGraphSetConditional(h_loop, st->cap > 0 ? 1u : 0u);
+}
+
+__global__ void g_decide(BfsState* st, int64_t nnz, int64_t nrows, unsigned long long* c,
+                         cudaGraphConditionalHandle h_push) {
+  const int64_t K = st->K, it = st->it;
+  const double d = nrows ? (double)nnz / (double)nrows : 0.0;
+  const int64_t est = (int64_t)rint(d * (double)K);
+  const double thr = (double)nnz * st->ratio;
+  int32_t dir = (double)est > thr ? GB_DIR_PULL : GB_DIR_PUSH;
+  if (st->policy == GB_DIR_PUSH) dir = GB_DIR_PUSH;
+  if (st->policy == GB_DIR_PULL) dir = GB_DIR_PULL;
+  int64_t* e = st->log + 1 + 3 * it;
+  e[0] = dir;
+  e[1] = K;
+  e[2] = est;
+  st->dnext = st->depth + 1;
+  *c = 0;
+  cudaGraphSetConditional(h_push, dir == GB_DIR_PUSH ? 1u : 0u);
+}
+
+// after a level: new frontier size, loop continuation, cap handling
+__global__ void g_advance(BfsState* st, const unsigned long long* c,
+                          cudaGraphConditionalHandle h_a, cudaGraphConditionalHandle h_b) {
+  const int64_t K = (int64_t)*c;
+  const int64_t it = st->it;
+  st->log[0] = it + 1;
+  st->K = K;
+  unsigned cont = 0;
+  if (K != 0) {
+    st->depth += 1;
+    if (it + 1 == st->cap) st->unstamp = 1;
+    else cont = 1;
+  }
+  st->it = it + 1;
+  cudaGraphSetConditional(h_a, cont);
+  cudaGraphSetConditional(h_b, cont);
+}
+
+__global__ void g_unstamp(const BfsState* __restrict__ st, const int32_t* __restrict__ F) {
+  if (!st->unstamp) return;
+  const int64_t K = st->K;
+  int64_t* lv = st->levels;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lv[F[i]] = 0;
+}
+
+struct BfsGraph {
+  // key: the matrix orientations the graph was built for
+  gb_csr push{}, pull{};
+  const uint32_t* nonempty = nullptr;
+  // scratch (one allocation)
+  void* mem = nullptr;
+  uint32_t *vbm = nullptr, *vprev = nullptr, *fbm[2] = {nullptr, nullptr};
+  int32_t* F = nullptr;
+  int32_t* tile_first = nullptr;
+  unsigned long long* cnt = nullptr;
+  int64_t *rowstart = nullptr, *S = nullptr, *part = nullptr;
+  BfsState* st = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int launches_push = 0, launches_pull = 0, launches_fixed = 0;
+};
+
+static void bfs_graph_free(void* p) {
+  auto* g = static_cast<BfsGraph*>(p);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->mem) cudaFree(g->mem);
+  delete g;
+}
+
+static bool same_csr(const gb_csr& a, const gb_csr& b) {
+  return a.nrows == b.nrows && a.ncols == b.ncols && a.nnz == b.nnz && a.offsets == b.offsets &&
+         a.indices == b.indices && a.values == b.values && a.dtype == b.dtype &&
+         a.iso_i64 == b.iso_i64 && a.iso_f64 == b.iso_f64;
+}
+
+template <class Fn>
+static cudaError_t capture_into(cudaGraph_t g, cudaStream_t cs, Fn fn) {
+  cudaError_t e = cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) return e;
+  cudaError_t e2 = fn();
+  cudaGraph_t out = g;
+  e = cudaStreamEndCapture(cs, &out);
+  return e2 != cudaSuccess ? e2 : e;
+}
+
+#define GB_GTRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
+
+static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t* cs) {
+  const gb_csr& push = G->push;
+  const gb_csr& pull = G->pull;
+  const int64_t n = push.nrows;
+  const int64_t W = (n + 31) / 32;
+  const EdgeOn push_on{push.values, push.dtype};
+  const EdgeOn pull_on{pull.values, pull.dtype};
+  const bool push_dead = !push.values && push.iso_i64 == 0 && push.iso_f64 == 0.0;
+  const bool pull_dead = !pull.values && pull.iso_i64 == 0 && pull.iso_f64 == 0.0;
+  BfsState* st = G->st;
+  const int grid_w = grid_for(ctx, W, 256, 8);
+  const int grid_tiles = grid_for(ctx, push.nnz / kWarpTile + 1, 256);
+  const int grid_expand = push.values ? resident_grid(ctx, bfs_expand_warp<true>, 256)
+                                      : resident_grid(ctx, bfs_expand_warp<false>, 256);
+  G->launches_push = 5 + (push_dead ? 0 : 1);
+  G->launches_pull = pull_dead ? 3 : 1;
+  G->launches_fixed = 8;  // 4 memsets, zero, start, unstamp (+1 per level: decide/advance below)
+
+  auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
+    g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part);
+    g_scan_top<<<1, 1024, 0, s>>>(kGScanBlocks, G->part);
+    g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part,
+                                                        G->rowstart, G->S);
+    g_tile_first<<<grid_tiles, 256, 0, s>>>(&st->K, G->S, G->tile_first);
+    if (!push_dead) {
+      if (push.values)
+        bfs_expand_warp<true><<<grid_expand, 256, 0, s>>>(dptr(&st->K), G->S, G->rowstart,
+                                                          G->tile_first, push.indices, push_on, G->vbm);
+      else
+        bfs_expand_warp<false><<<grid_expand, 256, 0, s>>>(dptr(&st->K), G->S, G->rowstart,
+                                                           G->tile_first, push.indices, push_on, G->vbm);
+    }
+    bfs_finalize<<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev, G->fbm[h ^ 1],
+                                        pptr(&st->levels), G->F, G->cnt + h, G->cnt + (h ^ 1),
+                                        nullptr);
+    return cudaGetLastError();
+  };
+  auto pull_body = [&](int h, cudaStream_t s) -> cudaError_t {
+    if (pull_dead) {
+      GB_GTRY(cudaMemsetAsync(G->fbm[h ^ 1], 0, sizeof(uint32_t) * W, s));
+      GB_GTRY(cudaMemsetAsync(G->cnt + h, 0, 8, s));
+      GB_GTRY(cudaMemsetAsync(G->cnt + (h ^ 1), 0, 8, s));
+    } else {
+      bfs_pull<<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices, pull_on,
+                                      G->nonempty, G->vbm, G->vprev, G->fbm[h], G->fbm[h ^ 1],
+                                      pptr(&st->levels), G->F, G->cnt + h, G->cnt + (h ^ 1), 0,
+                                      (W + 31) / 32);
+    }
+    return cudaGetLastError();
+  };
+  // one iteration on stream s (capturing into the graph that should hold it)
+  auto iteration = [&](int h, cudaStream_t s, cudaStream_t s_inner,
+                       cudaGraphConditionalHandle h_a, cudaGraphConditionalHandle h_b) -> cudaError_t {
+    cudaGraphConditionalHandle h_push;
+    cudaGraph_t br[2];
+    // decide sets h_push before the IF node reads it: create the handle first
+    cudaStreamCaptureStatus status;
+    cudaGraph_t g;
+    GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
+    GB_GTRY(cudaGraphConditionalHandleCreate(&h_push, g, 0, cudaGraphCondAssignDefault));
+    g_decide<<<1, 1, 0, s>>>(st, push.nnz, push.nrows, G->cnt + h, h_push);
+    GB_GTRY(cudaGetLastError());
+    {
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, &deps, &nd));
+      cudaGraphNodeParams p = {};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = h_push;
+      p.conditional.type = cudaGraphCondTypeIf;
+      p.conditional.size = 2;
+      cudaGraphNode_t node;
+      GB_GTRY(cudaGraphAddNode(&node, g, deps, nd, &p));
+      br[0] = p.conditional.phGraph_out[0];
+      br[1] = p.conditional.phGraph_out[1];
+      GB_GTRY(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    }
+    GB_GTRY(capture_into(br[0], s_inner, [&] { return push_body(h, s_inner); }));
+    GB_GTRY(capture_into(br[1], s_inner, [&] { return pull_body(h, s_inner); }));
+    g_advance<<<1, 1, 0, s>>>(st, G->cnt + h, h_a, h_b);
+    return cudaGetLastError();
+  };
+
+  cudaGraph_t top;
+  GB_GTRY(cudaGraphCreate(&top, 0));
+  cudaError_t err = capture_into(top, cs[0], [&]() -> cudaError_t {
+    cudaStream_t s = cs[0];
+    GB_GTRY(cudaMemsetAsync(G->vbm, 0, sizeof(uint32_t) * W, s));
+    GB_GTRY(cudaMemsetAsync(G->vprev, 0, sizeof(uint32_t) * W, s));
+    GB_GTRY(cudaMemsetAsync(G->fbm[0], 0, sizeof(uint32_t) * W, s));
+    GB_GTRY(cudaMemsetAsync(G->cnt, 0, 16, s));
+    g_zero_levels<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, st);
+    cudaStreamCaptureStatus status;
+    cudaGraph_t g;
+    GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
+    cudaGraphConditionalHandle h_loop;
+    GB_GTRY(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
+    g_start<<<1, 1, 0, s>>>(st, G->vbm, G->vprev, G->fbm[0], G->F, h_loop);
+    GB_GTRY(cudaGetLastError());
+    cudaGraph_t body;
+    {
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, &deps, &nd));
+      cudaGraphNodeParams p = {};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = h_loop;
+      p.conditional.type = cudaGraphCondTypeWhile;
+      p.conditional.size = 1;
+      cudaGraphNode_t node;
+      GB_GTRY(cudaGraphAddNode(&node, g, deps, nd, &p));
+      body = p.conditional.phGraph_out[0];
+      GB_GTRY(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    }
+    GB_GTRY(capture_into(body, cs[1], [&]() -> cudaError_t {
+      // even iteration; its advance gates the odd one (and the loop)
+      cudaGraphConditionalHandle h_odd;
+      cudaStreamCaptureStatus st2;
+      cudaGraph_t gb;
+      GB_GTRY(cudaStreamGetCaptureInfo(cs[1], &st2, nullptr, &gb, nullptr, nullptr));
+      GB_GTRY(cudaGraphConditionalHandleCreate(&h_odd, gb, 0, cudaGraphCondAssignDefault));
+      GB_GTRY(iteration(0, cs[1], cs[2], h_odd, h_loop));
+      cudaGraph_t odd;
+      {
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        GB_GTRY(cudaStreamGetCaptureInfo(cs[1], &st2, nullptr, &gb, &deps, &nd));
+        cudaGraphNodeParams p = {};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = h_odd;
+        p.conditional.type = cudaGraphCondTypeIf;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        GB_GTRY(cudaGraphAddNode(&node, gb, deps, nd, &p));
+        odd = p.conditional.phGraph_out[0];
+        GB_GTRY(cudaStreamUpdateCaptureDependencies(cs[1], &node, 1, cudaStreamSetCaptureDependencies));
+      }
+      return capture_into(odd, cs[3], [&] { return iteration(1, cs[3], cs[2], h_loop, h_loop); });
+    }));
+    g_unstamp<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(st, G->F);
+    return cudaGetLastError();
+  });
+  if (err == cudaSuccess) err = cudaGraphInstantiate(&G->exec, top, 0);
+  cudaGraphDestroy(top);
+  return err;
+}
+
+// Returns GB_OK after running the BFS, or GB_ERR_UNSUPPORTED when the graph
+// path cannot be used (the caller then runs the host-driven loop).
+static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                               const uint32_t* nonempty, int64_t source, int64_t cap,
+                               double ratio, int32_t policy, int64_t* levels, int32_t* log_dir,
+                               int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
+  void** slot = ctx_slot(ctx, SLOT_BFS_GRAPH, bfs_graph_free);
+  BfsGraph* G = static_cast<BfsGraph*>(*slot);
+  if (G && !(same_csr(G->push, *push) && same_csr(G->pull, *pull) && G->nonempty == nonempty)) {
+    cudaStreamSynchronize(stream_of(ctx));
+    bfs_graph_free(G);
+    G = nullptr;
+    *slot = nullptr;
+  }
+  if (!G) {
+    G = new BfsGraph();
+    G->push = *push;
+    G->pull = *pull;
+    G->nonempty = nonempty;
+    const int64_t n = push->nrows;
+    const int64_t W = (n + 31) / 32;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+    const size_t o_vbm = take(4 * W), o_vprev = take(4 * W), o_f0 = take(4 * W), o_f1 = take(4 * W);
+    const size_t o_F = take(4 * (size_t)n), o_tf = take(4 * (size_t)(push->nnz / kWarpTile + 2));
+    const size_t o_cnt = take(16), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
+    const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
+    if (cudaMalloc(&G->mem, off) != cudaSuccess) {
+      cudaGetLastError();
+      delete G;
+      return GB_ERR_UNSUPPORTED;
+    }
+    char* m = static_cast<char*>(G->mem);
+    G->vbm = (uint32_t*)(m + o_vbm);
+    G->vprev = (uint32_t*)(m + o_vprev);
+    G->fbm[0] = (uint32_t*)(m + o_f0);
+    G->fbm[1] = (uint32_t*)(m + o_f1);
+    G->F = (int32_t*)(m + o_F);
+    G->tile_first = (int32_t*)(m + o_tf);
+    G->cnt = (unsigned long long*)(m + o_cnt);
+    G->rowstart = (int64_t*)(m + o_rs);
+    G->S = (int64_t*)(m + o_S);
+    G->part = (int64_t*)(m + o_part);
+    G->st = (BfsState*)(m + o_st);
+    cudaStream_t cs[4];
+    for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    const cudaError_t e = bfs_graph_build(ctx, G, cs);
+    for (auto& x : cs) cudaStreamDestroy(x);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      bfs_graph_free(G);
+      return set_error(ctx, GB_ERR_CUDA, "bfs graph build: %s", cudaGetErrorString(e));
+    }
+    *slot = G;
+  }
+  cudaStream_t s = stream_of(ctx);
+  Arena ar(ctx);
+  int64_t* log = ar.alloc<int64_t>(1 + 3 * cap);
+  GB_ARENA_CHECK(ctx, ar);
+  BfsState h{};
+  h.levels = levels;
+  h.log = log;
+  h.source = source;
+  h.cap = cap;
+  h.ratio = ratio;
+  h.policy = policy;
+  // the state block's per-call head (everything before the loop state)
+  GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(BfsState, it), cudaMemcpyHostToDevice, s));
+  GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
+  // one readback: iteration count and up to 21 decisions
+  int64_t* pin = pinned_slots(ctx);
+  const int64_t first = cap < 21 ? cap : 21;
+  GB_CUDA(ctx, cudaMemcpyAsync(pin, log, sizeof(int64_t) * (1 + 3 * first), cudaMemcpyDeviceToHost, s));
+  GB_CUDA(ctx, cudaStreamSynchronize(s));
+  const int64_t iters = pin[0];
+  for (int64_t i = 0; i < iters && i < first; ++i) {
+    log_dir[i] = (int32_t)pin[1 + 3 * i];
+    log_nvals[i] = pin[2 + 3 * i];
+    log_est[i] = pin[3 + 3 * i];
+  }
+  if (iters > first) {
+    std::vector<int64_t> rest(3 * (iters - first));
+    GB_CUDA(ctx, cudaMemcpyAsync(rest.data(), log + 1 + 3 * first, sizeof(int64_t) * rest.size(),
+                                 cudaMemcpyDeviceToHost, s));
+    GB_CUDA(ctx, cudaStreamSynchronize(s));
+    for (int64_t i = first; i < iters; ++i) {
+      log_dir[i] = (int32_t)rest[3 * (i - first)];
+      log_nvals[i] = rest[3 * (i - first) + 1];
+      log_est[i] = rest[3 * (i - first) + 2];
+    }
+  }
+  *iters_out = iters;
+  int64_t nl = G->launches_fixed;
+  for (int64_t i = 0; i < iters; ++i)
+    nl += 2 + (log_dir[i] == GB_DIR_PUSH ? G->launches_push : G->launches_pull);
+  count_launch(ctx, (int)nl);
+  return GB_OK;
 }
 
 }  // namespace gb
@@ -351,6 +839,15 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                  int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   const int64_t n = push->nrows;
   if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
+  // device-driven loop (one graph launch) unless profiling per kernel, the
+  // pull orientation is missing (the host loop reports that error when pull
+  // is chosen), or GB_BFS_GRAPH=0 asks for the host-driven loop
+  static const bool graph_off = getenv("GB_BFS_GRAPH") && atoi(getenv("GB_BFS_GRAPH")) == 0;
+  if (pull && !graph_off && !prof_enabled(ctx) && max_iters >= 1 && max_iters <= kGraphMaxCap) {
+    const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, source, max_iters, ratio,
+                                       policy, levels, log_dir, log_nvals, log_est, iters_out);
+    if (st != GB_ERR_UNSUPPORTED) return st;
+  }
   Arena ar(ctx);
   cudaStream_t s = stream_of(ctx);
   const int64_t W = (n + 31) / 32;
@@ -393,8 +890,8 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
       } else {
         const int grid = grid_for(ctx, W, 256, 8);
         const int ps = prof_begin(ctx, PROF_BFS_PULL, K);
-        bfs_pull<<<grid, 256, 0, s>>>(n, depth + 1, pull->offsets, pull->indices, pull_on,
-                                      pull_nonempty, vbm, vprev, fbm[cur], fbm[cur ^ 1], levels, F,
+        bfs_pull<<<grid, 256, 0, s>>>(n, dval(depth + 1), pull->offsets, pull->indices, pull_on,
+                                      pull_nonempty, vbm, vprev, fbm[cur], fbm[cur ^ 1], pval(levels), F,
                                       c, c_next, 0, (W + 31) / 32);
         prof_end(ctx, ps);
         count_launch(ctx, 1);
@@ -409,8 +906,8 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
         count_launch(ctx, 5);  // degrees, scan (2), tile_first, expand
       }
       const int pf = prof_begin(ctx, PROF_BFS_FINALIZE, K);
-      bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, depth + 1, vbm, vprev, fbm[cur ^ 1],
-                                                         levels, F, c, c_next, nullptr);
+      bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, dval(depth + 1), vbm, vprev, fbm[cur ^ 1],
+                                                         pval(levels), F, c, c_next, nullptr);
       prof_end(ctx, pf);
       count_launch(ctx, 1);
     }
@@ -422,7 +919,7 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     if (it + 1 == max_iters) {
       // loop cap reached: the reference never stamps the last frontier
       // (its assign happens at the start of the next iteration)
-      bfs_unstamp<<<grid_for(ctx, K, 256), 256, 0, s>>>(K, F, levels);
+      bfs_unstamp<<<grid_for(ctx, K, 256), 256, 0, s>>>(dval(K), F, levels);
       GB_LAUNCH_CHECK(ctx);
       count_launch(ctx, 1);
     }
@@ -512,7 +1009,7 @@ gb_status gb_bfs_dist_pull(gb_ctx* ctx, const gb_csr* rowblock, int64_t lo, int6
     const int64_t g_lo = lo / 1024, g_hi = (hi + 1023) / 1024;
     const int ps = prof_begin(ctx, PROF_BFS_PULL, 0);
     bfs_pull<<<grid_for(ctx, (g_hi - g_lo) * 32, 256, 8), 256, 0, s>>>(
-        hi, depth, off, rowblock->indices, on, ne, vbm, vprev, fbm, xbm, levels, F, cnt, cnt + 1,
+        hi, dval(depth), off, rowblock->indices, on, ne, vbm, vprev, fbm, xbm, pval(levels), F, cnt, cnt + 1,
         g_lo, g_hi);
     prof_end(ctx, ps);
   }
@@ -530,8 +1027,8 @@ gb_status gb_bfs_dist_apply(gb_ctx* ctx, int64_t n, int64_t depth, const uint32_
   unsigned long long* cnt = ar.alloc<unsigned long long>(2);
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
-  bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, depth, vbm, vprev, fbm, levels, F, cnt,
-                                                        cnt + 1, xbm);
+  bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, dval(depth), vbm, vprev, fbm, pval(levels), F,
+                                                        cnt, cnt + 1, xbm);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 2);
   return read_i64(ctx, (const int64_t*)cnt, K_host);
@@ -539,7 +1036,7 @@ gb_status gb_bfs_dist_apply(gb_ctx* ctx, int64_t n, int64_t depth, const uint32_
 
 gb_status gb_bfs_dist_unstamp(gb_ctx* ctx, int64_t K, const int32_t* F, int64_t* levels) {
   if (K <= 0) return GB_OK;
-  bfs_unstamp<<<grid_for(ctx, K, 256), 256, 0, stream_of(ctx)>>>(K, F, levels);
+  bfs_unstamp<<<grid_for(ctx, K, 256), 256, 0, stream_of(ctx)>>>(dval(K), F, levels);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 1);
   return GB_OK;

@@ -287,6 +287,11 @@ enum { PROF_BFS_PUSH = 1, PROF_BFS_PULL = 2, PROF_BFS_FINALIZE = 3, PROF_SSSP = 
 int prof_begin(gb_ctx* ctx, int kind, int64_t arg);
 void prof_end(gb_ctx* ctx, int slot);
 int sm_count(gb_ctx* ctx);
+bool prof_enabled(gb_ctx* ctx);
+// Per-context cached objects (e.g. instantiated CUDA graphs) that live until
+// the context is destroyed: slot i holds a pointer and its destructor.
+enum { SLOT_BFS_GRAPH = 0, kCtxSlots = 4 };
+void** ctx_slot(gb_ctx* ctx, int i, void (*destroy)(void*));
 // pinned host scratch for small device->host reads (>= 64 int64 slots)
 int64_t* pinned_slots(gb_ctx* ctx);
 gb_status read_i64(gb_ctx* ctx, const int64_t* dptr, int64_t* out, int count = 1);
@@ -302,6 +307,24 @@ inline int resident_grid(gb_ctx* ctx, Kernel kernel, int block, size_t smem = 0)
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// A scalar kernel argument that is either a value known at launch or a device
+// location read when the kernel starts (graph-driven loops).
+struct DevI64 {
+  int64_t v;
+  const int64_t* p;
+  __device__ __forceinline__ int64_t get() const { return p ? *p : v; }
+};
+inline DevI64 dval(int64_t v) { return DevI64{v, nullptr}; }
+inline DevI64 dptr(const int64_t* p) { return DevI64{0, p}; }
+// Same for an output array pointer.
+struct DevP64 {
+  int64_t* v;
+  int64_t* const* p;
+  __device__ __forceinline__ int64_t* get() const { return p ? *p : v; }
+};
+inline DevP64 pval(int64_t* v) { return DevP64{v, nullptr}; }
+inline DevP64 pptr(int64_t* const* p) { return DevP64{nullptr, p}; }
 
 // grid for a grid-stride kernel over n items
 inline int grid_for(gb_ctx* ctx, int64_t n, int block, int per_sm = 8) {

@@ -31,6 +31,8 @@ struct gb_ctx {
   std::vector<int> prof_kind;
   std::vector<int64_t> prof_arg;
   size_t prof_used = 0;
+  void* slot[gb::kCtxSlots] = {nullptr};
+  void (*slot_free[gb::kCtxSlots])(void*) = {nullptr};
 };
 
 namespace gb {
@@ -71,6 +73,11 @@ void prof_end(gb_ctx* ctx, int slot) {
   cudaEventRecord(ctx->ev_pool[2 * slot + 1], ctx->stream);
 }
 int sm_count(gb_ctx* ctx) { return ctx->sms; }
+bool prof_enabled(gb_ctx* ctx) { return ctx->prof; }
+void** ctx_slot(gb_ctx* ctx, int i, void (*destroy)(void*)) {
+  if (destroy) ctx->slot_free[i] = destroy;
+  return &ctx->slot[i];
+}
 int64_t* pinned_slots(gb_ctx* ctx) { return ctx->pinned; }
 
 gb_status read_i64(gb_ctx* ctx, const int64_t* dptr, int64_t* out, int count) {
@@ -150,6 +157,8 @@ gb_status gb_ctx_destroy(gb_ctx* ctx) {
   if (!ctx) return GB_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (int i = 0; i < gb::kCtxSlots; ++i)
+    if (ctx->slot[i] && ctx->slot_free[i]) ctx->slot_free[i](ctx->slot[i]);
   for (auto& b : ctx->blocks) cudaFree(b.ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->dev_err) cudaFree(ctx->dev_err);

@@ -113,6 +113,69 @@ def test_bfs_s24_properties(gb):
 
 
 # ---------------------------------------------------------------------------
+# device-driven loop (one CUDA graph) vs the host-driven loop
+# ---------------------------------------------------------------------------
+
+
+def _run_both(gb, A, src, **kw):
+    from paper_1908_01407_b200 import _lib
+    ctx = _lib.context()
+    d1 = gb.Descriptor(**kw)
+    g = gb.bfs(A, src, desc=d1).values            # graph path
+    ctx.profiling(True)                            # per-kernel events force the host loop
+    try:
+        d2 = gb.Descriptor(**kw)
+        h = gb.bfs(A, src, desc=d2).values
+    finally:
+        ctx.profiling(False)
+        ctx.prof_read()
+    t1 = [(d.chosen, d.frontier_nvals, d.estimated_frontier_edges) for d in d1.direction_log]
+    t2 = [(d.chosen, d.frontier_nvals, d.estimated_frontier_edges) for d in d2.direction_log]
+    return g, h, t1, t2
+
+
+@pytest.mark.parametrize("s", [6, 12, 16, 20])
+def test_bfs_graph_loop_equals_host_loop(gb, s):
+    A = gb.io.rmat_matrix(s)
+    for src in (0, 5, A.nrows - 1):
+        for kw in ({}, {"max_niter": 1}, {"max_niter": 2}, {"max_niter": 3},
+                   {"direction": gb.Direction.FORCE_PUSH}, {"direction": gb.Direction.FORCE_PULL},
+                   {"switch_ratio": 0.0}, {"switch_ratio": 1.0}):
+            g, h, t1, t2 = _run_both(gb, A, src, **kw)
+            assert np.array_equal(g, h), (src, kw)
+            assert t1 == t2, (src, kw)
+
+
+def test_bfs_graph_cache_follows_the_matrix(gb):
+    """The cached graph is keyed by the matrix: alternating matrices and
+    sources gives each one's own answer."""
+    from oracle import cgraph
+    mats = [gb.io.rmat_matrix(10), gb.io.rmat_matrix(11), gb.io.rmat_matrix(10, a=0.25, b=0.25, c=0.25, d=0.25)]
+    for _ in range(2):
+        for A in mats:
+            rp = A._csr.offsets.cpu().numpy()
+            ci = A._csr.indices.cpu().numpy()
+            for src in (0, 9):
+                want, _ = cgraph.bfs(rp, ci, src)
+                assert np.array_equal(gb.bfs(A, src).values, want)
+
+
+def test_bfs_graph_long_path(gb):
+    """A path graph runs one level per vertex: many WHILE iterations, both
+    halves of the unrolled body, and more than 21 logged decisions."""
+    n = 300
+    r = np.r_[np.arange(n - 1), np.arange(1, n)]
+    c = np.r_[np.arange(1, n), np.arange(n - 1)]
+    A = gb.SparseMatrix.from_tuples(r, c, np.ones(r.size, np.int64), n, n)
+    g, h, t1, t2 = _run_both(gb, A, 0)
+    assert g.tolist() == list(range(1, n + 1))
+    assert np.array_equal(g, h) and t1 == t2 and len(t1) == n
+    for cap in (20, 21, 22, 23, 150):
+        g, h, t1, t2 = _run_both(gb, A, 0, max_niter=cap)
+        assert np.array_equal(g, h) and t1 == t2 and len(t1) == cap
+
+
+# ---------------------------------------------------------------------------
 # edge cases the reference semantics define
 # ---------------------------------------------------------------------------
 
