@@ -200,14 +200,32 @@ gb_status gb_nonempty_rows(gb_ctx* ctx, int64_t n, const int64_t* offsets, uint3
 int32_t gb_decide_direction(int64_t nnz, int64_t nrows, int64_t nnz_u, double switch_ratio,
                             int32_t policy, int64_t* estimate_out);
 
+/* Edge-balanced work plan of one orientation (the nonzero split,
+ * kernels.py:133-150): the non-empty rows (nz_rows[R], their offsets
+ * nz_off[R+1]) and, for every 512-entry tile, the plan row holding its first
+ * entry (tile_first[nnz/512 + 2]).  Built once per matrix orientation by the
+ * caller (gb_row_plan_build) and passed to the pull kernels; NULL = build it
+ * per call. */
+typedef struct gb_row_plan {
+  int64_t nrows_nz;
+  const int32_t* nz_rows;
+  const int64_t* nz_off;
+  const int32_t* tile_first;
+} gb_row_plan;
+
+/* fill caller buffers nz_rows[nrows], nz_off[nrows+1], tile_first[nnz/512+2];
+ * *nrows_nz_host = R. Synchronizes. */
+gb_status gb_row_plan_build(gb_ctx* ctx, const gb_csr* a, int32_t* nz_rows, int64_t* nz_off,
+                            int32_t* tile_first, int64_t* nrows_nz_host);
+
 /* Pull SpMV (kernels.py:153-229): for every row i of `a` allowed by `mask`
  * (NULL = all), out[i] = fold over stored (i,j) with u[j] != identity of
  * mult(a_ij, u[j]); rows without contributions get the identity.  `u` and
  * `out` are dense of dtype T = a->dtype.  counters (may be NULL) accumulates
  * {entries read, multiplies, adds} exactly as the reference counts them. */
 gb_status gb_mxv_pull(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
-                      const void* u, const uint32_t* mask, int32_t early_exit,
-                      int32_t partition, void* out, int64_t* counters);
+                      const gb_row_plan* plan, const void* u, const uint32_t* mask,
+                      int32_t early_exit, int32_t partition, void* out, int64_t* counters);
 
 /* Push SpMSpV (kernels.py:242-280): expand the columns named by the sparse u
  * (k entries), multiply, fold per output row, drop identity results, apply

@@ -57,6 +57,10 @@ class gb_csr(C.Structure):
     ]
 
 
+class gb_row_plan(C.Structure):
+    _fields_ = [("nrows_nz", i64), ("nz_rows", vp), ("nz_off", vp), ("tile_first", vp)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "gb_abi_version": (i32, []),
@@ -87,7 +91,9 @@ SIGNATURES = {
     "gb_decide_direction": (i32, [i64, i64, i64, f64, i32, pi64]),
     "gb_bfs": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), vp, i64, i64, f64, i32, vp,
                      vp, vp, vp, pi64]),
-    "gb_mxv_pull": (i32, [vp, i32, i32, C.POINTER(gb_csr), vp, vp, i32, i32, vp, vp]),
+    "gb_mxv_pull": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_row_plan), vp, vp, i32,
+                          i32, vp, vp]),
+    "gb_row_plan_build": (i32, [vp, C.POINTER(gb_csr), vp, vp, vp, pi64]),
     "gb_mxv_push": (i32, [vp, i32, i32, C.POINTER(gb_csr), i64, i64, vp, vp, vp, vp, vp, pi64,
                           vp]),
     "gb_mxm_masked": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_csr),

@@ -412,7 +412,7 @@ class _Orient:
     """One orientation on the device: rows of A (CSR) or of A^T (CSC)."""
 
     __slots__ = ("nrows", "ncols", "offsets", "indices", "values", "iso", "dt", "_nonempty",
-                 "__weakref__")
+                 "_plan", "__weakref__")
 
     def __init__(self, nrows, ncols, offsets, indices, values, iso, dt):
         self.nrows, self.ncols = int(nrows), int(ncols)
@@ -420,10 +420,31 @@ class _Orient:
         self.iso = iso  # python scalar when values is None
         self.dt = np.dtype(dt)
         self._nonempty = None
+        self._plan = None
 
     @property
     def nnz(self):
         return int(self.indices.numel())
+
+    def row_plan(self):
+        """Edge-balanced work plan of this orientation (gb_row_plan_build):
+        the non-empty rows and the first plan row of every 512-entry tile,
+        built once.  Returns (gb_row_plan, keepalive)."""
+        if self._plan is None:
+            n = self.nrows
+            nz_rows = empty(max(n, 1), np.int32)
+            nz_off = empty(n + 1, np.int64)
+            tile_first = empty(self.nnz // 512 + 2, np.int32)
+            R = C.c_int64(0)
+            s, _keep = self.csr_struct()
+            _lib.context().call("gb_row_plan_build", C.byref(s), _lib.ptr(nz_rows),
+                                _lib.ptr(nz_off), _lib.ptr(tile_first), C.byref(R))
+            p = _lib.gb_row_plan()
+            p.nrows_nz = R.value
+            p.nz_rows, p.nz_off, p.tile_first = (nz_rows.data_ptr(), nz_off.data_ptr(),
+                                                 tile_first.data_ptr())
+            self._plan = (p, (nz_rows, nz_off, tile_first))
+        return self._plan
 
     def csr_struct(self, as_dtype=None):
         """(gb_csr, keepalive) -- values converted to ``as_dtype`` when given.

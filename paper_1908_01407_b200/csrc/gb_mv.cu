@@ -12,6 +12,7 @@
 
 #include "gb_common.cuh"
 #include "gb_lbs.cuh"
+#include "gb_rowtiles.cuh"
 
 namespace gb {
 
@@ -90,6 +91,192 @@ mv_pull_rows(int64_t nrows, const int64_t* __restrict__ off, const int32_t* __re
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Edge-balanced masked pull (commutative folds, no early exit): the row-tile
+// layout of gb_rowtiles.cuh (512-entry warp tiles over the non-empty rows,
+// 16 consecutive column indices per lane via 16-byte loads) with the mask
+// applied per entry: a lane first walks its entries' rows in shared memory
+// to flag the allowed ones, then issues all their u gathers (and value loads)
+// at once, then folds row by row.  `out` holds the identity beforehand (rows
+// that are masked out, empty or without contributions keep it); whole rows
+// are stored, rows split across lanes are combined with an atomic fold.
+// Counters are exact: reads and multiplies are block-reduced; a row split
+// across lanes marks `hasmul` so that rows with >= 1 multiply are counted
+// once (adds = multiplies - such rows, kernels.py:185-189).
+// ---------------------------------------------------------------------------
+// ADD / MUL >= 0 fix the semiring at compile time (the builtin semirings,
+// algebra.py:161-179); -1 reads add_op / mult_op at run time.  VALS = false
+// for iso (structure-only) matrices.
+template <class T, int ADD, int MUL, bool VALS>
+__global__ void __launch_bounds__(256, 3)
+mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
+              const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
+              const T* __restrict__ vals, T iso, const T* __restrict__ u,
+              const uint32_t* __restrict__ mask, int add_rt, int mult_rt, T* __restrict__ out,
+              unsigned long long* __restrict__ counters, uint32_t* __restrict__ hasmul) {
+  const int add_op = ADD >= 0 ? ADD : add_rt;
+  const int mult_op = MUL >= 0 ? MUL : mult_rt;
+  __shared__ uint16_t s_st[8][kRowTile + 8];
+  __shared__ uint8_t s_ok[8][kRowTile + 8];  // mask bit of each tile row
+  __shared__ unsigned long long s_cnt[3];
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint16_t* st = s_st[threadIdx.x >> 5];
+  uint8_t* okr = s_ok[threadIdx.x >> 5];
+  const T ident = op_identity<T>(add_op);
+  const int64_t E = nz_off[R_rows];
+  const int64_t ntiles = (E + kRowTile - 1) / kRowTile;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long c_reads = 0, c_muls = 0, c_rows = 0;
+  for (int64_t t = w0; t < ntiles; t += nw) {
+    const int64_t e0 = t * kRowTile;
+    const int64_t e1 = e0 + kRowTile < E ? e0 + kRowTile : E;
+    const int64_t my0 = e0 + (int64_t)lane * kRowItems;
+    const int64_t my1 = my0 + kRowItems < e1 ? my0 + kRowItems : e1;
+    int32_t cols[kRowItems];
+    if (my0 + kRowItems <= e1) {
+      const int4* p4 = reinterpret_cast<const int4*>(idx + my0);
+#pragma unroll
+      for (int q = 0; q < kRowItems / 4; ++q) {
+        int4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
+        cols[4 * q] = v.x; cols[4 * q + 1] = v.y; cols[4 * q + 2] = v.z; cols[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kRowItems; ++q) cols[q] = my0 + q < e1 ? ld_stream(idx + my0 + q) : 0;
+    }
+    const int64_t r0 = tile_first[t];
+    const int64_t r1 = t + 1 < ntiles ? tile_first[t + 1] : R_rows - 1;
+    const int nr = (int)(r1 - r0 + 1);
+    for (int i = lane; i <= nr; i += 32) {
+      const int64_t o = nz_off[r0 + i] - e0;
+      st[i] = (uint16_t)(o < 0 ? 0 : (o > kRowTile ? kRowTile : o));
+      if (i < nr) {
+        const int32_t row = nz_rows[r0 + i];
+        okr[i] = !mask || ((__ldg(mask + (row >> 5)) >> (row & 31)) & 1u);
+      }
+    }
+    __syncwarp();
+    if (my0 < e1) {
+      const int rel0 = lane * kRowItems, rel1 = (int)(my1 - e0);
+      int lo = 0, hi = nr - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (st[mid] <= rel0) lo = mid; else hi = mid - 1;
+      }
+      // pass 1: which of my entries belong to allowed rows
+      uint32_t allowed = 0;
+      {
+        int cur = lo, next = st[lo + 1];
+        bool ok = okr[cur];
+#pragma unroll
+        for (int q = 0; q < kRowItems; ++q) {
+          const int e = rel0 + q;
+          if (e < rel1) {
+            while (e >= next) {
+              ++cur;
+              next = st[cur + 1];
+              ok = okr[cur];
+            }
+            if (ok) allowed |= 1u << q;
+          }
+        }
+      }
+      // pass 2: gathers for the allowed entries, all issued before any use
+      T uv[kRowItems];
+#pragma unroll
+      for (int q = 0; q < kRowItems; ++q) uv[q] = (allowed >> q) & 1u ? __ldg(u + cols[q]) : ident;
+      // pass 3: fold row by row
+      int cur = lo;
+      int row_start = st[cur];
+      int next = st[cur + 1];
+      T acc = ident;
+      long long incl = 0;
+      bool row_ok = false;
+      c_reads += __popc(allowed);
+      auto flush = [&](bool whole) {
+        const int32_t row = nz_rows[r0 + cur];
+        if (!row_ok) return;
+        c_muls += incl;
+        if (whole) {
+          out[row] = acc;
+          if (incl > 0) ++c_rows;
+        } else if (incl > 0) {
+          atomic_fold<T>(add_op, out + row, acc);
+          atomicOr(hasmul + (row >> 5), 1u << (row & 31));
+        }
+      };
+#pragma unroll
+      for (int q = 0; q < kRowItems; ++q) {
+        const int e = rel0 + q;
+        if (e < rel1) {
+          while (e >= next) {
+            flush(row_start >= rel0 && next <= rel1 && (cur > 0 || nz_off[r0] >= e0));
+            acc = ident;
+            incl = 0;
+            ++cur;
+            row_start = next;
+            next = st[cur + 1];
+          }
+          if ((allowed >> q) & 1u) {
+            row_ok = true;
+            if (uv[q] != ident) {
+              const T a = VALS ? __ldg(vals + my0 + q) : iso;
+              acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, a, uv[q]));
+              ++incl;
+            }
+          } else {
+            row_ok = false;
+          }
+        }
+      }
+      flush(row_start >= rel0 && next <= rel1 && next < kRowTile + 1 &&
+            (cur > 0 || nz_off[r0] >= e0) && (cur < nr - 1 || nz_off[r1 + 1] <= e1));
+    }
+    __syncwarp();
+  }
+  if (counters) {
+    c_reads = warp_sum_ll((long long)c_reads);
+    c_muls = warp_sum_ll((long long)c_muls);
+    c_rows = warp_sum_ll((long long)c_rows);
+    if (lane == 0) {
+      atomicAdd(&s_cnt[0], c_reads);
+      atomicAdd(&s_cnt[1], c_muls);
+      atomicAdd(&s_cnt[2], c_rows);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(counters + 0, s_cnt[0]);
+      atomicAdd(counters + 1, s_cnt[1]);
+      // rows with a multiply so far (whole rows); split rows are added from
+      // `hasmul` by mv_pull_finish; adds = multiplies - rows
+      atomicAdd(counters + 2, s_cnt[1] - s_cnt[2]);
+    }
+  }
+}
+
+template <class T>
+__global__ void fill_value(int64_t n, T v, T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v;
+}
+
+// counters[2] -= rows that were split across lanes and had a multiply
+__global__ void mv_pull_finish(int64_t W, const uint32_t* __restrict__ hasmul,
+                               unsigned long long* __restrict__ counters) {
+  long long c = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x)
+    c += __popc(hasmul[w]);
+  c = warp_sum_ll(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(counters + 2, (unsigned long long)(-c));
 }
 
 template <class T>
@@ -237,6 +424,87 @@ static gb_status push_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a, i
   return GB_OK;
 }
 
+template <class T, int ADD, int MUL, bool VALS>
+static gb_status launch_tiles_k(gb_ctx* ctx, int add_op, int mult_op, const RowTilesPlan& plan,
+                                const gb_csr* a, T iso, const T* u, const uint32_t* mask, T* out,
+                                unsigned long long* counters, uint32_t* hasmul) {
+  auto k = mv_pull_tiles<T, ADD, MUL, VALS>;
+  k<<<resident_grid(ctx, k, 256), 256, 0, stream_of(ctx)>>>(
+      plan.R, plan.nz_rows, plan.nz_off, plan.tile_first, a->indices, (const T*)a->values, iso, u,
+      mask, add_op, mult_op, out, counters, hasmul);
+  return GB_OK;
+}
+
+template <class T, int ADD, int MUL>
+static gb_status launch_tiles_v(gb_ctx* ctx, int add_op, int mult_op, bool vals,
+                                const RowTilesPlan& plan, const gb_csr* a, T iso, const T* u,
+                                const uint32_t* mask, T* out, unsigned long long* counters,
+                                uint32_t* hasmul) {
+  return vals ? launch_tiles_k<T, ADD, MUL, true>(ctx, add_op, mult_op, plan, a, iso, u, mask, out,
+                                                  counters, hasmul)
+              : launch_tiles_k<T, ADD, MUL, false>(ctx, add_op, mult_op, plan, a, iso, u, mask, out,
+                                                   counters, hasmul);
+}
+
+// the builtin semirings get their own instantiation; anything else is generic
+template <class T>
+static gb_status launch_pull_tiles(gb_ctx* ctx, int add_op, int mult_op, bool vals,
+                                   const RowTilesPlan& plan, const gb_csr* a, T iso, const T* u,
+                                   const uint32_t* mask, T* out, unsigned long long* counters,
+                                   uint32_t* hasmul) {
+#define GB_SR(A_, M_)                                                                         \
+  if (add_op == A_ && mult_op == M_)                                                          \
+    return launch_tiles_v<T, A_, M_>(ctx, add_op, mult_op, vals, plan, a, iso, u, mask, out, \
+                                     counters, hasmul);
+  GB_SR(GB_OP_PLUS, GB_OP_TIMES)    // PlusMultiplies
+  GB_SR(GB_OP_LOR, GB_OP_LAND)      // LogicalOrAnd
+  GB_SR(GB_OP_MIN, GB_OP_PLUS)      // MinPlus
+  GB_SR(GB_OP_MAX, GB_OP_PLUS)      // MaxPlus
+  GB_SR(GB_OP_MIN, GB_OP_TIMES)     // MinMultiplies
+  GB_SR(GB_OP_MIN, GB_OP_SECOND)    // MinimumSelectSecond
+  GB_SR(GB_OP_PLUS, GB_OP_LESS)     // PlusLess
+  GB_SR(GB_OP_MIN, GB_OP_NE)        // MinimumNotEqualTo
+#undef GB_SR
+  return launch_tiles_v<T, -1, -1>(ctx, add_op, mult_op, vals, plan, a, iso, u, mask, out, counters,
+                                   hasmul);
+}
+
+template <class T>
+static gb_status pull_tiles_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a,
+                              const gb_row_plan* given, const T* u, const uint32_t* mask, T* out,
+                              int64_t* counters) {
+  cudaStream_t s = stream_of(ctx);
+  const int64_t n = a->nrows;
+  const int64_t W = (n + 31) / 32;
+  Arena ar(ctx);
+  RowTilesPlan plan;
+  if (given) {
+    plan.R = given->nrows_nz;
+    plan.nz_rows = const_cast<int32_t*>(given->nz_rows);
+    plan.nz_off = const_cast<int64_t*>(given->nz_off);
+    plan.tile_first = const_cast<int32_t*>(given->tile_first);
+  } else {
+    GB_TRY(row_tiles_plan(ctx, ar, n, a->offsets, a->nnz, &plan));
+  }
+  uint32_t* hasmul = counters ? ar.alloc<uint32_t>(W) : nullptr;
+  GB_ARENA_CHECK(ctx, ar);
+  const T ident = op_identity<T>(add_op);
+  const T iso = std::is_same<T, double>::value ? (T)a->iso_f64 : (T)a->iso_i64;
+  if (hasmul) GB_CUDA(ctx, cudaMemsetAsync(hasmul, 0, sizeof(uint32_t) * W, s));
+  fill_value<T><<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, ident, out);
+  const int ps = prof_begin(ctx, PROF_MV, a->nnz);
+  if (plan.R > 0)
+    GB_TRY(launch_pull_tiles<T>(ctx, add_op, mult_op, a->values != nullptr, plan, a, iso, u, mask,
+                                out, (unsigned long long*)counters, hasmul));
+  prof_end(ctx, ps);
+  if (counters)
+    mv_pull_finish<<<grid_for(ctx, W, 256, 4), 256, 0, s>>>(W, hasmul,
+                                                             (unsigned long long*)counters);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2 + (counters ? 2 : 0));
+  return GB_OK;
+}
+
 }  // namespace gb
 
 using namespace gb;
@@ -244,13 +512,20 @@ using namespace gb;
 extern "C" {
 
 gb_status gb_mxv_pull(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
-                      const void* u, const uint32_t* mask, int32_t early_exit, int32_t partition,
-                      void* out, int64_t* counters) {
-  (void)partition;  // row-split warp-per-row kernel for both partition modes
+                      const gb_row_plan* plan, const void* u, const uint32_t* mask,
+                      int32_t early_exit, int32_t partition, void* out, int64_t* counters) {
+  (void)partition;  // both partition modes get the edge-balanced tiles (or warp per row)
   cudaStream_t s = stream_of(ctx);
   const int64_t n = a->nrows;
   if (n == 0) return GB_OK;
   const int early = early_exit && add_op == GB_OP_LOR;
+  if (!early && fold_is_commutative(add_op)) {
+    if (a->dtype == GB_I64)
+      return pull_tiles_t<int64_t>(ctx, add_op, mult_op, a, plan, (const int64_t*)u, mask,
+                                   (int64_t*)out, counters);
+    return pull_tiles_t<double>(ctx, add_op, mult_op, a, plan, (const double*)u, mask,
+                                (double*)out, counters);
+  }
   const int grid = grid_for(ctx, n * 32, 256, 16);
   const int ps = prof_begin(ctx, PROF_MV, n);
   if (a->dtype == GB_I64)

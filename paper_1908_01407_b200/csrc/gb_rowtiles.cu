@@ -29,9 +29,10 @@ gb_status row_tiles_plan(gb_ctx* ctx, Arena& ar, int64_t n, const int64_t* off, 
   cudaStream_t s = stream_of(ctx);
   int32_t* flag = ar.alloc<int32_t>(n + 1);
   int64_t* pos = ar.alloc<int64_t>(n + 1);
-  plan->nz_rows = ar.alloc<int32_t>(n + 1);
-  plan->nz_off = ar.alloc<int64_t>(n + 1);
-  plan->tile_first = ar.alloc<int32_t>(nnz / kRowTile + 2);
+  // caller-provided output buffers are kept (gb_row_plan_build)
+  if (!plan->nz_rows) plan->nz_rows = ar.alloc<int32_t>(n + 1);
+  if (!plan->nz_off) plan->nz_off = ar.alloc<int64_t>(n + 1);
+  if (!plan->tile_first) plan->tile_first = ar.alloc<int32_t>(nnz / kRowTile + 2);
   GB_ARENA_CHECK(ctx, ar);
   nz_rows_flags<<<grid_for(ctx, n + 1, 256), 256, 0, s>>>(n, off, flag);
   size_t tb = 0;
@@ -51,3 +52,16 @@ gb_status row_tiles_plan(gb_ctx* ctx, Arena& ar, int64_t n, const int64_t* off, 
 }
 
 }  // namespace gb
+
+extern "C" gb_status gb_row_plan_build(gb_ctx* ctx, const gb_csr* a, int32_t* nz_rows,
+                                       int64_t* nz_off, int32_t* tile_first,
+                                       int64_t* nrows_nz_host) {
+  gb::Arena ar(ctx);
+  gb::RowTilesPlan plan;
+  plan.nz_rows = nz_rows;
+  plan.nz_off = nz_off;
+  plan.tile_first = tile_first;
+  GB_TRY(gb::row_tiles_plan(ctx, ar, a->nrows, a->offsets, a->nnz, &plan));
+  *nrows_nz_host = plan.R;
+  return GB_OK;
+}

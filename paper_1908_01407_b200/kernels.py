@@ -180,8 +180,9 @@ def _spmv_pull(semiring, A, u, mask, desc, transpose):
     out = empty(o.nrows, dtype)
     cnt = _counters_tensor()
     part = _lib.PART_ROW if desc.partition is Partition.ROW_SPLIT else _lib.PART_NONZERO
-    _ctx().call("gb_mxv_pull", add, mult, C.byref(s), _lib.ptr(uv), _lib.ptr(bm), early, part,
-                _lib.ptr(out), _lib.ptr(cnt))
+    plan, _pk = o.row_plan()
+    _ctx().call("gb_mxv_pull", add, mult, C.byref(s), C.byref(plan), _lib.ptr(uv), _lib.ptr(bm),
+                early, part, _lib.ptr(out), _lib.ptr(cnt))
     _merge_counters(desc, cnt)
     return Vector._wrap(o.nrows, None, out, identity, dtype)
 
