@@ -16,6 +16,7 @@ Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement for every field.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import platform
@@ -42,6 +43,7 @@ def parse():
     ap.add_argument("--algo", default="bfs", choices=["bfs"])
     ap.add_argument("--source", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-spmv", action="store_true", help="skip the masked SpMV measurement")
     ap.add_argument("--cpu-cap-s", type=float, default=120.0,
                     help="wall-clock cap for CPU timing legs")
     return ap.parse_args()
@@ -143,6 +145,58 @@ def push_level_bytes(n, k, flops, k_next):
     return k * (4 + 2 * 8) + flops * 4 + n / 8 + n / 8 + k_next * (4 + 8)
 
 
+def masked_spmv(gb, A, ctx, peak, peak_src, reps=10, density=0.5):
+    """The second half of the BASELINE metric: masked pull SpMV at the bench
+    scale through the public API, w<!m> = A (+.*) x (x dense f64, m a seeded
+    50 % mask, complemented; forced pull), timed per kernel with events.
+    Algorithmic bytes per SURVEY §8(d): n/8 (mask) + min(2R, n+1)*8 (offsets
+    of the R allowed rows) + E_read*4 (their column indices; pattern matrix,
+    no values) + n*8 (x, once) + n*8 (w).  Checked against torch index_add."""
+    import torch
+    from paper_1908_01407_b200.containers import MaskMode, Vector
+    n = A.nrows
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) + 0.5
+    mbits = (torch.rand(n, device="cuda", generator=g) < density).to(torch.int64)
+    u = Vector._wrap(n, None, x, 0.0, np.float64)
+    mask = Vector._wrap(n, None, mbits, 0, np.int64)
+    sr = gb.builtin_semiring("PlusMultiplies")
+
+    def run():
+        d = gb.Descriptor(mask_mode=MaskMode.COMPLEMENT, direction=gb.Direction.FORCE_PULL)
+        return gb.mxv(sr, A, u, mask=mask, desc=d), d
+
+    run()
+    run()
+    torch.cuda.synchronize()
+    ctx.profiling(True)
+    for _ in range(reps):
+        w, d = run()
+    torch.cuda.synchronize()
+    prof = ctx.prof_read()
+    ctx.profiling(False)
+    t_ms = float(np.median([t for (kind, _a, t) in prof if kind == 8]))
+    off = A._csr.offsets
+    deg = torch.diff(off)
+    allowed = mbits == 0
+    R = int(((deg > 0) & allowed).sum())
+    e_read = d.counters.matrix_entries_read
+    bytes_alg = n / 8 + min(2 * R, n + 1) * 8 + e_read * 4 + n * 8 + n * 8
+    rows = torch.repeat_interleave(torch.arange(n, device="cuda"), deg)
+    keep = allowed[rows]
+    ref = torch.zeros(n, dtype=torch.float64, device="cuda")
+    ref.index_add_(0, rows[keep], x[A._csr.indices.long()[keep]])
+    rel = float(((w._vals - ref).abs() / ref.abs().clamp_min(1e-300)).max())
+    del rows, keep, ref
+    achieved = bytes_alg / (t_ms * 1e-3) / 1e9
+    return {"workload": "mxv(PlusMultiplies f64, A, x dense, mask=~m, m 50 % seeded), forced pull",
+            "kernel": "mv_pull_tiles", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
+            "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4), "allowed_rows": R,
+            "entries_read": int(e_read), "multiplies": int(d.counters.semiring_multiplies),
+            "max_rel_err_vs_torch": rel, "tolerance": 1e-12, "parity": rel <= 1e-12}
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -241,6 +295,19 @@ def run_ours(args):
                 "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4),
                 "frontier": int(k), "flops": flops,
                 "level_ms": [(kind, a, round(t, 4)) for (kind, a, t) in prof]}
+        # the push is bound by scattered 4 B probes of the visited bitmap, not
+        # by HBM: report it against the random-probe rate of this GPU too
+        rate = ctypes.c_double(0.0)
+        ctx.call("gb_probe_rate", (n + 31) // 32, 1 << 30, ctypes.byref(rate))
+        probes_s = flops / (t_ms * 1e-3)
+        roof["probe_ceiling"] = {
+            "what": "uniformly random 4 B ld.global.ca probes of an n-bit bitmap on all SMs "
+                    "(gb_probe_rate, measured in this run); the push does one probe per edge",
+            "ceiling_Gprobe_s": round(rate.value / 1e9, 1),
+            "achieved_Gprobe_s": round(probes_s / 1e9, 1),
+            "frac": round(probes_s / rate.value, 3)}
+
+    mspmv = masked_spmv(gb, A, ctx, peak, peak_src) if world == 1 and not args.no_spmv else None
 
     # ---- end-to-end through the public API (host result every step) --------
     # warm-up: the first calls allocate the pinned staging blocks (~57 ms each
@@ -312,6 +379,7 @@ def run_ours(args):
                             "int64 level vector (n*8 B) out to host every step"},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "masked_spmv": mspmv,
             "cpu_baseline": cpu,
             "parity_vs_oracle": parity,
         }

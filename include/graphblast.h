@@ -411,6 +411,15 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                  int32_t* log_dir_host, int64_t* log_nvals_host, int64_t* log_est_host,
                  int64_t* iters_host);
 
+/* ----------------------------------------------------------------------------
+ * measurement support (bench.py)
+ * --------------------------------------------------------------------------*/
+
+/* Random-probe ceiling: uniformly random 4-byte ld.global.ca probes of a
+ * `words`-word bitmap (>= min_probes of them) at full occupancy; writes
+ * probes per second.  Synchronizes. */
+gb_status gb_probe_rate(gb_ctx* ctx, int64_t words, int64_t min_probes, double* probes_per_s_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,7 @@ SIGNATURES = {
     "gb_mxv_pull": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_row_plan), vp, vp, i32,
                           i32, vp, vp]),
     "gb_row_plan_build": (i32, [vp, C.POINTER(gb_csr), vp, vp, vp, pi64]),
+    "gb_probe_rate": (i32, [vp, i64, i64, C.POINTER(f64)]),
     "gb_mxv_push": (i32, [vp, i32, i32, C.POINTER(gb_csr), i64, i64, vp, vp, vp, vp, vp, pi64,
                           vp]),
     "gb_mxm_masked": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_csr),
