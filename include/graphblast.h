@@ -123,6 +123,21 @@ gb_status gb_build_csr(gb_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz_in
 gb_status gb_transpose_csr(gb_ctx* ctx, const gb_csr* a, int64_t* out_offsets,
                            int32_t* out_indices, void* out_vals);
 
+/* Traversal layout (no reference counterpart; an internal layout of the
+ * matrix the reference stores as plain CSR/CSC, containers.py:276-364).
+ * gb_degree_order: order[r] = the vertex with the r-th largest row length
+ * (ties by ascending id), rank = its inverse.  Synchronizes. */
+gb_status gb_degree_order(gb_ctx* ctx, int64_t n, const int64_t* offsets, int32_t* order,
+                          int32_t* rank);
+
+/* The relabelled TRANSPOSE of a square orientation: out = P A^T P^T with
+ * new id rank[i] for vertex i, every output row sorted ascending; values
+ * (if any) carried along.  For a symmetric matrix this is P A P^T.
+ * Outputs: offsets[n+1], indices[nnz], vals[nnz].  Synchronizes. */
+gb_status gb_csr_relabel_t(gb_ctx* ctx, const gb_csr* a, const int32_t* order,
+                           const int32_t* rank, int64_t* out_offsets, int32_t* out_indices,
+                           void* out_vals);
+
 /* 1 when the two orientations hold identical arrays (A == A^T);
  * algorithms.py:41-45 _require_symmetric.  Synchronizes. */
 gb_status gb_csr_equal(gb_ctx* ctx, const gb_csr* a, const gb_csr* b, int32_t* equal_host);
@@ -410,6 +425,18 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                  double switch_ratio, int32_t policy, int64_t* levels,
                  int32_t* log_dir_host, int64_t* log_nvals_host, int64_t* log_est_host,
                  int64_t* iters_host);
+
+/* bfs (algorithms.py:48-77) over the degree-ordered relabelling of the
+ * matrix (gb_csr_relabel_t): `push`/`pull`/`pull_nonempty` are the relabelled
+ * orientations, rank[i] the new id of vertex i.  `source` and `levels` use
+ * the ORIGINAL ids, so results equal gb_bfs on the original matrix; the
+ * direction log is identical (frontier sizes do not depend on labels).  The
+ * push keeps the visited bits of the low-id prefix in shared memory. */
+gb_status gb_bfs_ordered(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                         const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
+                         int64_t max_iters, double switch_ratio, int32_t policy,
+                         int64_t* levels, int32_t* log_dir_host, int64_t* log_nvals_host,
+                         int64_t* log_est_host, int64_t* iters_host);
 
 /* ----------------------------------------------------------------------------
  * measurement support (bench.py)

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import numpy as np
 import torch
@@ -40,6 +41,9 @@ from .kernels import (
 )
 
 _INT_INF = np.iinfo(np.int64).max
+# bfs over the degree-ordered relabelling (SparseMatrix.traversal); GB_BFS_ORDER=0
+# keeps the original labels (A/B measurement, tests of both paths)
+_ORDERED_BFS = os.environ.get("GB_BFS_ORDER", "1") != "0"
 
 _POLICY = {Direction.AUTO: _lib.DIR_AUTO, Direction.FORCE_PUSH: _lib.DIR_PUSH,
            Direction.FORCE_PULL: _lib.DIR_PULL}
@@ -82,14 +86,26 @@ def bfs(A: SparseMatrix, source: int, desc=None, early_exit=True) -> Vector:
     n = A.nrows
     iters = min(desc.max_niter, n + 1)
     levels = empty(n, np.int64)
-    push, _k1 = A.orient(False).csr_struct()          # vxm push walks rows of A (CSR)
-    pull_o = A.orient(True) if A.has_csc else None    # vxm pull walks rows of A^T (CSC)
-    pull, _k2 = pull_o.csr_struct() if pull_o is not None else (None, None)
     cap = max(iters, 1)
     dirs = np.zeros(cap, np.int32)
     nv = np.zeros(cap, np.int64)
     est = np.zeros(cap, np.int64)
     done = C.c_int64(0)
+    trav = A.traversal() if _ORDERED_BFS else None
+    if trav is not None:
+        # degree-ordered relabelling: same levels and log
+        push_o, pull_o, rank = trav
+        (push, _k1), (pull, _k2) = push_o.csr_struct(), pull_o.csr_struct()
+        _lib.context().call(
+            "gb_bfs_ordered", C.byref(push), C.byref(pull), _lib.ptr(pull_o.nonempty()),
+            _lib.ptr(rank), int(source), int(iters), float(desc.switch_ratio),
+            _POLICY[desc.direction], _lib.ptr(levels), dirs.ctypes.data_as(C.c_void_p),
+            nv.ctypes.data_as(C.c_void_p), est.ctypes.data_as(C.c_void_p), C.byref(done))
+        _log_decisions(desc, A, dirs, nv, est, int(done.value))
+        return Vector._wrap(n, None, levels, 0, np.int64)
+    push, _k1 = A.orient(False).csr_struct()          # vxm push walks rows of A (CSR)
+    pull_o = A.orient(True) if A.has_csc else None    # vxm pull walks rows of A^T (CSC)
+    pull, _k2 = pull_o.csr_struct() if pull_o is not None else (None, None)
     _lib.context().call(
         "gb_bfs", C.byref(push), C.byref(pull) if pull is not None else None,
         _lib.ptr(pull_o.nonempty()) if pull_o is not None else None,

@@ -412,7 +412,7 @@ class _Orient:
     """One orientation on the device: rows of A (CSR) or of A^T (CSC)."""
 
     __slots__ = ("nrows", "ncols", "offsets", "indices", "values", "iso", "dt", "_nonempty",
-                 "_plan", "__weakref__")
+                 "_plan", "_ordered", "__weakref__")
 
     def __init__(self, nrows, ncols, offsets, indices, values, iso, dt):
         self.nrows, self.ncols = int(nrows), int(ncols)
@@ -421,6 +421,7 @@ class _Orient:
         self.dt = np.dtype(dt)
         self._nonempty = None
         self._plan = None
+        self._ordered = None
 
     @property
     def nnz(self):
@@ -690,6 +691,42 @@ class SparseMatrix:
                 _lib.context().call("gb_csr_equal", C.byref(a), C.byref(b), C.byref(eq))
                 self._sym = bool(eq.value)
         return bool(self._sym)
+
+    def traversal(self):
+        """Degree-ordered relabelling used by the traversals, built
+        once per matrix: vertices renumbered by descending in-degree (ties by
+        id; gb_degree_order), both orientations relabelled with sorted rows
+        (gb_csr_relabel_t).  Returns (push, pull, rank) -- push walks rows of
+        P A P^T, pull rows of P A^T P^T, rank[i] = new id of vertex i -- or
+        None when the matrix is not square or has no column orientation."""
+        o, csc = self._csr, self._csc
+        if csc is None or self.nrows != self.ncols:
+            return None
+        c = o._ordered
+        if c is not None and c[0] is csc:
+            return c[1]
+        n = self.nrows
+        ctx = _lib.context()
+        order = empty(max(n, 1), np.int32)
+        rank = empty(max(n, 1), np.int32)
+        ctx.call("gb_degree_order", n, _lib.ptr(csc.offsets), _lib.ptr(order), _lib.ptr(rank))
+
+        def relabel_t(src):  # P src^T P^T
+            off = empty(n + 1, np.int64)
+            idx = empty(src.nnz, np.int32)
+            vals = None if src.values is None else empty(src.nnz, src.dt)
+            st, _k = src.csr_struct()
+            ctx.call("gb_csr_relabel_t", C.byref(st), _lib.ptr(order), _lib.ptr(rank),
+                     _lib.ptr(off), _lib.ptr(idx), _lib.ptr(vals))
+            return _Orient(n, n, off, idx, vals, src.iso, src.dt)
+
+        if csc is o:
+            push = pull = relabel_t(o)
+        else:
+            pull = relabel_t(o)    # rows of P A^T P^T: in-edges
+            push = relabel_t(csc)  # rows of P A P^T: out-edges
+        o._ordered = (csc, (push, pull, rank))
+        return o._ordered[1]
 
     def row_ids(self):
         o = self._csr

@@ -95,6 +95,119 @@ bfs_expand_warp(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restr
   warp_tiles(K, S, rowstart, tile_first, f);
 }
 
+// Push over a degree-ordered graph: the visited bits of the
+// low-id prefix -- the vertices that receive almost every probe -- live in
+// shared memory for the whole launch.  One persistent CTA per SM copies the
+// level-start prefix (vprev) in, probes and marks it with shared-memory
+// loads / atomics, and at the end ORs what it discovered into the global
+// visited bitmap with one atomic per changed word.  Probes past the prefix
+// take the global path of PushBits.  A CTA may mark a vertex another CTA
+// already found; the global OR makes that harmless (finalize diffs against
+// vprev).  Small levels skip the prefix copy (E below the break-even).
+constexpr int kSmemPushThreads = 768;
+constexpr int64_t kPrefixWordsMax = 49152;  // 192 KB: 1.57 M vertices
+
+template <bool VALS>
+struct PushBitsSmem {
+  const int32_t* __restrict__ idx;
+  EdgeOn on;
+  uint32_t* __restrict__ vbm;
+  uint32_t* sbm;
+  int32_t pbits;  // vertices [0, pbits) are tracked in shared memory
+  // Branch-free per item: every item reads a shared word (word 0 when its
+  // vertex is outside the prefix), only suffix items issue a global probe,
+  // and the marks are predicated atomics -- no divergent regions.
+  template <int B>
+  __device__ __forceinline__ void batch(const int64_t (&p)[B], const bool (&live)[B]) {
+    int32_t v[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      v[r] = -1;
+      if (live[r]) v[r] = ld_stream(idx + p[r]);
+      if (VALS && v[r] >= 0 && !on(p[r])) v[r] = -1;
+    }
+    uint32_t word[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      const bool pre = (uint32_t)v[r] < (uint32_t)pbits;  // v = -1 is never in the prefix
+      word[r] = sbm[pre ? (v[r] >> 5) : 0];
+      if (v[r] >= pbits) word[r] = ld_probe(vbm + (v[r] >> 5));
+    }
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      const uint32_t bit = 1u << (v[r] & 31);
+      const bool clear = !(word[r] & bit);
+      if (clear && (uint32_t)v[r] < (uint32_t)pbits) atomicOr(sbm + (v[r] >> 5), bit);
+      if (clear && v[r] >= pbits) atomicOr(vbm + (v[r] >> 5), bit);
+    }
+  }
+  __device__ __forceinline__ void visit(int64_t p) {
+    const int32_t u = ld_stream(idx + p);
+    if (VALS && !on(p)) return;
+    const uint32_t bit = 1u << (u & 31);
+    if (u < pbits) {
+      if (!(sbm[u >> 5] & bit)) atomicOr(sbm + (u >> 5), bit);
+    } else if (!(ld_probe(vbm + (u >> 5)) & bit)) {
+      atomicOr(vbm + (u >> 5), bit);
+    }
+  }
+};
+
+template <bool VALS>
+__global__ void __launch_bounds__(kSmemPushThreads, 1)
+bfs_expand_smem(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
+                const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
+                EdgeOn on, uint32_t* __restrict__ vbm, const uint32_t* __restrict__ vprev,
+                int64_t W) {
+  extern __shared__ uint32_t sbm[];
+  const int64_t K = Kd.get();
+  if (K <= 0) return;
+  const int64_t E = S[K];
+  const int64_t P = W < kPrefixWordsMax ? W : kPrefixWordsMax;
+  // the prefix copy-in / flush costs ~P/2 vector accesses per CTA
+  const bool use = E >= P * (int64_t)gridDim.x / 4;
+  if (use) {
+    for (int64_t w = threadIdx.x; w < P; w += blockDim.x) sbm[w] = __ldg(vprev + w);
+    __syncthreads();
+  }
+  PushBitsSmem<VALS> f{idx, on, vbm, sbm, use ? (int32_t)(P * 32) : 0};
+  warp_tiles(K, S, rowstart, tile_first, f);
+  if (use) {
+    __syncthreads();
+    for (int64_t w = threadIdx.x; w < P; w += blockDim.x) {
+      const uint32_t d = sbm[w] & ~__ldg(vprev + w);
+      if (d) atomicOr(vbm + w, d);
+    }
+  }
+}
+
+template <bool VALS>
+static int smem_push_setup(gb_ctx* ctx, int64_t W, size_t* smem) {
+  const int64_t P = W < kPrefixWordsMax ? W : kPrefixWordsMax;
+  *smem = (size_t)P * 4;
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(bfs_expand_smem<VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kPrefixWordsMax * 4));
+    done = true;
+  }
+  return sm_count(ctx);
+}
+
+// levels of the original vertex ids from a run over the relabelled graph:
+// vertex i is new vertex rank[i]; unvisited vertices read 0 (the internal
+// level array is never cleared).
+__global__ void bfs_unpermute(int64_t n, const int32_t* __restrict__ rank,
+                              const uint32_t* __restrict__ vbm, const int64_t* __restrict__ lv,
+                              DevP64 out_d) {
+  int64_t* __restrict__ out = out_d.get();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rank[i];
+    out[i] = ((__ldg(vbm + (r >> 5)) >> (r & 31)) & 1u) ? lv[r] : 0;
+  }
+}
+
 __global__ void bfs_init(int64_t source, int64_t* levels, uint32_t* vbm, uint32_t* vprev,
                          uint32_t* fbm, int32_t* F) {
   levels[source] = 1;
@@ -337,6 +450,24 @@ static gb_status launch_push(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const 
                    : launch_push_t<false>(ctx, K, plan, a, on, vbm);
 }
 
+template <bool VALS>
+static gb_status launch_push_smem_t(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
+                                    EdgeOn on, uint32_t* vbm, const uint32_t* vprev) {
+  const int64_t W = (a->ncols + 31) / 32;
+  size_t smem = 0;
+  const int grid = smem_push_setup<VALS>(ctx, W, &smem);
+  bfs_expand_smem<VALS><<<grid, kSmemPushThreads, smem, stream_of(ctx)>>>(
+      dval(K), plan.S, plan.rowstart, plan.tile_first, a->indices, on, vbm, vprev, W);
+  GB_LAUNCH_CHECK(ctx);
+  return GB_OK;
+}
+
+static gb_status launch_push_smem(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
+                                  EdgeOn on, uint32_t* vbm, const uint32_t* vprev) {
+  return a->values ? launch_push_smem_t<true>(ctx, K, plan, a, on, vbm, vprev)
+                   : launch_push_smem_t<false>(ctx, K, plan, a, on, vbm, vprev);
+}
+
 // ---------------------------------------------------------------------------
 // Device-driven BFS.  The whole level loop is one CUDA
 // graph: a WHILE conditional node whose body holds two unrolled iterations
@@ -359,6 +490,7 @@ struct BfsState {
   int64_t source, cap;  // per call
   double ratio;         // per call
   int32_t policy, pad_;
+  int64_t* out;         // per call, relabelled graphs: levels by original id
   int64_t it, K, depth, dnext, unstamp;  // loop state
 };
 
@@ -464,9 +596,9 @@ __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
     lv[i] = 0;
 }
 
-__global__ void g_start(BfsState* st, uint32_t* vbm, uint32_t* vprev, uint32_t* fbm0, int32_t* F,
-                        cudaGraphConditionalHandle h_loop) {
-  const int64_t s = st->source;
+__global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32_t* vprev,
+                        uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop) {
+  const int64_t s = rank ? (int64_t)rank[st->source] : st->source;
   st->levels[s] = 1;
   const uint32_t bit = 1u << (s & 31);
   vbm[s >> 5] |= bit;
@@ -530,6 +662,7 @@ struct BfsGraph {
   // key: the matrix orientations the graph was built for
   gb_csr push{}, pull{};
   const uint32_t* nonempty = nullptr;
+  const int32_t* rank = nullptr;  // relabelled graph: original id -> new id
   // scratch (one allocation)
   void* mem = nullptr;
   uint32_t *vbm = nullptr, *vprev = nullptr, *fbm[2] = {nullptr, nullptr};
@@ -537,6 +670,7 @@ struct BfsGraph {
   int32_t* tile_first = nullptr;
   unsigned long long* cnt = nullptr;
   int64_t *rowstart = nullptr, *S = nullptr, *part = nullptr;
+  int64_t* lv = nullptr;  // relabelled graph: levels by new id (never cleared)
   BfsState* st = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches_push = 0, launches_pull = 0, launches_fixed = 0;
@@ -582,9 +716,13 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   const int grid_tiles = grid_for(ctx, push.nnz / kWarpTile + 1, 256);
   const int grid_expand = push.values ? resident_grid(ctx, bfs_expand_warp<true>, 256)
                                       : resident_grid(ctx, bfs_expand_warp<false>, 256);
+  const bool ordered = G->rank != nullptr;
+  size_t smem = 0;
+  const int grid_smem = push.values ? smem_push_setup<true>(ctx, W, &smem)
+                                    : smem_push_setup<false>(ctx, W, &smem);
   G->launches_push = 5 + (push_dead ? 0 : 1);
   G->launches_pull = pull_dead ? 3 : 1;
-  G->launches_fixed = 8;  // 4 memsets, zero, start, unstamp (+1 per level: decide/advance below)
+  G->launches_fixed = 8;  // 4 memsets, zero (or unpermute), start, unstamp (+2 per level below)
 
   auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
     g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part);
@@ -592,7 +730,14 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part,
                                                         G->rowstart, G->S);
     g_tile_first<<<grid_tiles, 256, 0, s>>>(&st->K, G->S, G->tile_first);
-    if (!push_dead) {
+    if (!push_dead && ordered) {
+      if (push.values)
+        bfs_expand_smem<true><<<grid_smem, kSmemPushThreads, smem, s>>>(
+            dptr(&st->K), G->S, G->rowstart, G->tile_first, push.indices, push_on, G->vbm, G->vprev, W);
+      else
+        bfs_expand_smem<false><<<grid_smem, kSmemPushThreads, smem, s>>>(
+            dptr(&st->K), G->S, G->rowstart, G->tile_first, push.indices, push_on, G->vbm, G->vprev, W);
+    } else if (!push_dead) {
       if (push.values)
         bfs_expand_warp<true><<<grid_expand, 256, 0, s>>>(dptr(&st->K), G->S, G->rowstart,
                                                           G->tile_first, push.indices, push_on, G->vbm);
@@ -659,13 +804,15 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     GB_GTRY(cudaMemsetAsync(G->vprev, 0, sizeof(uint32_t) * W, s));
     GB_GTRY(cudaMemsetAsync(G->fbm[0], 0, sizeof(uint32_t) * W, s));
     GB_GTRY(cudaMemsetAsync(G->cnt, 0, 16, s));
-    g_zero_levels<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, st);
+    // a relabelled run never clears its internal levels: the final
+    // unpermute reads them only where the visited bit is set
+    if (!ordered) g_zero_levels<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, st);
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
     cudaGraphConditionalHandle h_loop;
     GB_GTRY(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
-    g_start<<<1, 1, 0, s>>>(st, G->vbm, G->vprev, G->fbm[0], G->F, h_loop);
+    g_start<<<1, 1, 0, s>>>(st, G->rank, G->vbm, G->vprev, G->fbm[0], G->F, h_loop);
     GB_GTRY(cudaGetLastError());
     cudaGraph_t body;
     {
@@ -708,6 +855,9 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       return capture_into(odd, cs[3], [&] { return iteration(1, cs[3], cs[2], h_loop, h_loop); });
     }));
     g_unstamp<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(st, G->F);
+    if (ordered)
+      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, G->rank, G->vbm, G->lv,
+                                                             pptr(&st->out));
     return cudaGetLastError();
   });
   if (err == cudaSuccess) err = cudaGraphInstantiate(&G->exec, top, 0);
@@ -718,12 +868,13 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
 // Returns GB_OK after running the BFS, or GB_ERR_UNSUPPORTED when the graph
 // path cannot be used (the caller then runs the host-driven loop).
 static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
-                               const uint32_t* nonempty, int64_t source, int64_t cap,
+                               const uint32_t* nonempty, const int32_t* rank, int64_t source, int64_t cap,
                                double ratio, int32_t policy, int64_t* levels, int32_t* log_dir,
                                int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   void** slot = ctx_slot(ctx, SLOT_BFS_GRAPH, bfs_graph_free);
   BfsGraph* G = static_cast<BfsGraph*>(*slot);
-  if (G && !(same_csr(G->push, *push) && same_csr(G->pull, *pull) && G->nonempty == nonempty)) {
+  if (G && !(same_csr(G->push, *push) && same_csr(G->pull, *pull) && G->nonempty == nonempty &&
+             G->rank == rank)) {
     cudaStreamSynchronize(stream_of(ctx));
     bfs_graph_free(G);
     G = nullptr;
@@ -734,6 +885,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->push = *push;
     G->pull = *pull;
     G->nonempty = nonempty;
+    G->rank = rank;
     const int64_t n = push->nrows;
     const int64_t W = (n + 31) / 32;
     size_t off = 0;
@@ -742,6 +894,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     const size_t o_F = take(4 * (size_t)n), o_tf = take(4 * (size_t)(push->nnz / kWarpTile + 2));
     const size_t o_cnt = take(16), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
+    const size_t o_lv = rank ? take(8 * (size_t)n) : 0;
     if (cudaMalloc(&G->mem, off) != cudaSuccess) {
       cudaGetLastError();
       delete G;
@@ -759,6 +912,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->S = (int64_t*)(m + o_S);
     G->part = (int64_t*)(m + o_part);
     G->st = (BfsState*)(m + o_st);
+    G->lv = rank ? (int64_t*)(m + o_lv) : nullptr;
     cudaStream_t cs[4];
     for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
     const cudaError_t e = bfs_graph_build(ctx, G, cs);
@@ -775,7 +929,8 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   int64_t* log = ar.alloc<int64_t>(1 + 3 * cap);
   GB_ARENA_CHECK(ctx, ar);
   BfsState h{};
-  h.levels = levels;
+  h.levels = rank ? G->lv : levels;
+  h.out = levels;
   h.log = log;
   h.source = source;
   h.cap = cap;
@@ -833,10 +988,14 @@ int32_t gb_decide_direction(int64_t nnz, int64_t nrows, int64_t nnz_u, double ra
   return (double)est > thr ? GB_DIR_PULL : GB_DIR_PUSH;
 }
 
-gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
-                 const uint32_t* pull_nonempty, int64_t source, int64_t max_iters,
-                 double ratio, int32_t policy, int64_t* levels, int32_t* log_dir,
-                 int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
+}  // extern "C"
+
+namespace gb {
+
+static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                         const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
+                         int64_t max_iters, double ratio, int32_t policy, int64_t* levels_out,
+                         int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   const int64_t n = push->nrows;
   if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
   // device-driven loop (one graph launch) unless profiling per kernel, the
@@ -844,13 +1003,23 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
   // is chosen), or GB_BFS_GRAPH=0 asks for the host-driven loop
   static const bool graph_off = getenv("GB_BFS_GRAPH") && atoi(getenv("GB_BFS_GRAPH")) == 0;
   if (pull && !graph_off && !prof_enabled(ctx) && max_iters >= 1 && max_iters <= kGraphMaxCap) {
-    const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, source, max_iters, ratio,
-                                       policy, levels, log_dir, log_nvals, log_est, iters_out);
+    const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, source, max_iters,
+                                       ratio, policy, levels_out, log_dir, log_nvals, log_est,
+                                       iters_out);
     if (st != GB_ERR_UNSUPPORTED) return st;
   }
   Arena ar(ctx);
   cudaStream_t s = stream_of(ctx);
   const int64_t W = (n + 31) / 32;
+  int64_t* levels = levels_out;
+  if (rank) {
+    // host-driven loop over the relabelled graph: internal levels by new id
+    int32_t r = 0;
+    GB_CUDA(ctx, cudaMemcpyAsync(&r, rank + source, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    GB_CUDA(ctx, cudaStreamSynchronize(s));
+    source = r;
+    levels = ar.alloc<int64_t>(n);
+  }
   uint32_t* vbm = ar.alloc<uint32_t>(W);
   uint32_t* fbm[2] = {ar.alloc<uint32_t>(W), ar.alloc<uint32_t>(W)};
   int32_t* F = ar.alloc<int32_t>(n);
@@ -901,7 +1070,8 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
         LbsPlan plan;
         GB_TRY(lbs_prepare(ctx, ar, K, F, push->offsets, push->nnz, &plan, kWarpTile));
         const int ps = prof_begin(ctx, PROF_BFS_PUSH, K);
-        GB_TRY(launch_push(ctx, K, plan, push, push_on, vbm));
+        if (rank) GB_TRY(launch_push_smem(ctx, K, plan, push, push_on, vbm, vprev));
+        else GB_TRY(launch_push(ctx, K, plan, push, push_on, vbm));
         prof_end(ctx, ps);
         count_launch(ctx, 5);  // degrees, scan (2), tile_first, expand
       }
@@ -925,7 +1095,34 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     }
   }
   *iters_out = iters;
+  if (rank) {
+    bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rank, vbm, levels, pval(levels_out));
+    GB_LAUNCH_CHECK(ctx);
+    count_launch(ctx, 1);
+  }
   return GB_OK;
+}
+
+}  // namespace gb
+
+extern "C" {
+
+gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                 const uint32_t* pull_nonempty, int64_t source, int64_t max_iters,
+                 double ratio, int32_t policy, int64_t* levels, int32_t* log_dir,
+                 int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
+  return bfs_run(ctx, push, pull, pull_nonempty, nullptr, source, max_iters, ratio, policy, levels,
+                 log_dir, log_nvals, log_est, iters_out);
+}
+
+gb_status gb_bfs_ordered(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                         const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
+                         int64_t max_iters, double ratio, int32_t policy, int64_t* levels,
+                         int32_t* log_dir, int64_t* log_nvals, int64_t* log_est,
+                         int64_t* iters_out) {
+  if (!rank) return set_error(ctx, GB_ERR_ARG, "gb_bfs_ordered needs the vertex rank array");
+  return bfs_run(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio, policy, levels,
+                 log_dir, log_nvals, log_est, iters_out);
 }
 
 // ---------------------------------------------------------------------------

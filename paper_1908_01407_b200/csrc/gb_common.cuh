@@ -246,16 +246,20 @@ __device__ __forceinline__ long long warp_reserve(unsigned long long* counter, i
   return (long long)base + pre - want;
 }
 
-// streaming read-only load that does not allocate in L1 (column-index streams)
+// streaming read-only load that does not allocate in L1 (column-index
+// streams).  Not volatile: the data is immutable during the kernel, so the
+// compiler may predicate, batch and schedule these loads freely.
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
   int32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
-// L1-cached probe of a word other threads may be setting (staleness is benign)
+// L1-cached probe of a word other threads may be setting.  Staleness is
+// benign (a stale clear bit only costs a redundant atomic), so the asm is not
+// volatile either: it may be predicated and reordered.
 __device__ __forceinline__ uint32_t ld_probe(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.global.ca.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm("ld.global.ca.b32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 

@@ -240,3 +240,96 @@ def test_bfs_bad_source(gb):
         gb.bfs(A, 64)
     with pytest.raises(gb.ShapeError):
         gb.bfs(gb.matrix_build([(0, 1, 1)], 2, 3), 0)
+
+
+# ---------------------------------------------------------------------------
+# degree-ordered traversal layout (SparseMatrix.traversal, gb_bfs_ordered)
+# ---------------------------------------------------------------------------
+
+
+def _orient_tuples(o):
+    rp = o.offsets.cpu().numpy()
+    ci = o.indices.cpu().numpy().astype(np.int64)
+    rows = np.repeat(np.arange(o.nrows), np.diff(rp))
+    vals = o.dense_values().cpu().numpy()
+    return rp, rows, ci, vals
+
+
+def test_degree_order_and_relabel_are_an_isomorphism(gb):
+    rng = np.random.default_rng(11)
+    n = 700
+    r = rng.integers(0, n, 6000)
+    c = rng.integers(0, n, 6000)
+    v = rng.integers(0, 3, 6000)  # stored zeros included
+    A = gb.SparseMatrix.from_tuples(r, c, v, n, n)
+    assert not A.is_symmetric()
+    push, pull, rank = A.traversal()
+    rank = rank.cpu().numpy().astype(np.int64)
+    assert np.array_equal(np.sort(rank), np.arange(n))
+    indeg = np.diff(A._csc.offsets.cpu().numpy())
+    order = np.argsort(rank)
+    assert np.array_equal(order, np.lexsort((np.arange(n), -indeg)))  # degree desc, ties by id
+    # push = P A P^T, pull = P A^T P^T, every row sorted
+    ar, ac, av = A.extract_tuples()
+    for o, (i, j) in ((push, (ar, ac)), (pull, (ac, ar))):
+        rp, rows, ci, vals = _orient_tuples(o)
+        got = sorted(zip(rows.tolist(), ci.tolist(), vals.tolist()))
+        want = sorted(zip(rank[i].tolist(), rank[j].tolist(), av.tolist()))
+        assert got == want
+        for k in range(n):
+            seg = ci[rp[k]:rp[k + 1]]
+            assert np.all(np.diff(seg) > 0)
+    assert A.traversal()[0] is push  # cached
+
+
+def _bfs_both_layouts(gb, A, src, monkeypatch, **kw):
+    from paper_1908_01407_b200 import algorithms
+    out = []
+    for ordered in (True, False):
+        monkeypatch.setattr(algorithms, "_ORDERED_BFS", ordered)
+        g, h, t1, t2 = _run_both(gb, A, src, **kw)
+        assert np.array_equal(g, h) and t1 == t2, (ordered, src, kw)
+        out.append((g, t1))
+    monkeypatch.setattr(algorithms, "_ORDERED_BFS", True)
+    (g1, t1), (g2, t2) = out
+    assert np.array_equal(g1, g2), (src, kw)
+    assert t1 == t2, (src, kw)
+
+
+@pytest.mark.parametrize("s", [8, 14, 18])
+def test_bfs_ordered_equals_original_labels(gb, s, monkeypatch):
+    A = gb.io.rmat_matrix(s)
+    for src in (0, 3, A.nrows - 1):
+        for kw in ({}, {"max_niter": 2}, {"direction": gb.Direction.FORCE_PUSH},
+                   {"direction": gb.Direction.FORCE_PULL}):
+            _bfs_both_layouts(gb, A, src, monkeypatch, **kw)
+
+
+def test_bfs_ordered_directed_valued(gb, monkeypatch):
+    rng = np.random.default_rng(7)
+    n = 2000
+    r = rng.integers(0, n, 30000)
+    c = (r + rng.integers(1, 40, 30000)) % n
+    v = rng.integers(0, 4, 30000)
+    A = gb.SparseMatrix.from_tuples(r, c, v, n, n)
+    for src in (0, 17, 1999):
+        for kw in ({}, {"direction": gb.Direction.FORCE_PUSH}, {"direction": gb.Direction.FORCE_PULL},
+                   {"switch_ratio": 0.0}, {"max_niter": 3}):
+            _bfs_both_layouts(gb, A, src, monkeypatch, **kw)
+
+
+def test_bfs_ordered_smem_prefix_large_frontier(gb, monkeypatch):
+    """Uniform graph whose push levels are large enough to take the
+    shared-memory prefix path, with n above the 1.57 M-vertex prefix."""
+    A = gb.io.rmat_matrix(21, a=0.25, b=0.25, c=0.25, d=0.25)
+    from oracle import cgraph
+    rp = A._csr.offsets.cpu().numpy()
+    ci = A._csr.indices.cpu().numpy()
+    for src in (0, 123457):
+        for kw in ({}, {"direction": gb.Direction.FORCE_PUSH}):
+            desc = gb.Descriptor(**kw)
+            lv = gb.bfs(A, src, desc=desc).values
+            want, tr = cgraph.bfs(rp, ci, src) if not kw else (None, None)
+            if want is not None:
+                assert np.array_equal(lv, want)
+            _bfs_both_layouts(gb, A, src, monkeypatch, **kw)

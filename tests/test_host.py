@@ -28,6 +28,10 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     # and every symbol the binding declares is in the header
     assert set(_lib.SIGNATURES) <= set(syms)
+    # and every header function has a typed binding (ctypes cannot pass a
+    # double without one)
+    unbound = [s for s in syms if s not in _lib.SIGNATURES]
+    assert not unbound, unbound
     assert lib.gb_abi_version() == 1
 
 

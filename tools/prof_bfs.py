@@ -24,6 +24,13 @@ args = ap.parse_args()
 
 A = rmat_matrix(args.scale, weighted=args.algo == "sssp")
 gb._lib.context().trim()
+if args.algo == "mxvm":
+    from paper_1908_01407_b200.containers import Vector
+    _g = torch.Generator(device="cuda").manual_seed(1)
+    _X = Vector._wrap(A.nrows, None, torch.rand(A.nrows, dtype=torch.float64, device="cuda",
+                                                generator=_g) + 0.5, 0.0, np.float64)
+    _M = Vector._wrap(A.nrows, None, (torch.rand(A.nrows, device="cuda", generator=_g) < 0.5)
+                      .to(torch.int64), 0, np.int64)
 
 
 def run():
@@ -37,6 +44,11 @@ def run():
         gb.connected_components(A)
     elif args.algo == "tc":
         gb.triangle_count(A)
+    elif args.algo == "mxvm":
+        # bench.py's masked SpMV: w<~m> = A (+.*) x, x dense f64, m 50 % seeded, forced pull
+        sr = gb.builtin_semiring("PlusMultiplies")
+        d = gb.Descriptor(mask_mode=gb.MaskMode.COMPLEMENT, direction=gb.Direction.FORCE_PULL)
+        gb.mxv(sr, A, _X, mask=_M, desc=d)
     elif args.algo == "mxv":
         u = gb.vector_fill(A.nrows, 1.0)
         gb.mxv(gb.builtin_semiring("PlusMultiplies"), A, u)
