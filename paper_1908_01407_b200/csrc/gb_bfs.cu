@@ -51,7 +51,7 @@ struct EdgeOn {
 // vbm & ~vprev.
 __device__ __forceinline__ void mark(uint32_t* vbm, int32_t v, uint32_t word) {
   const uint32_t bit = 1u << (v & 31);
-  if (!(word & bit)) atomicOr(vbm + (v >> 5), bit);
+  red_or_if(!(word & bit), vbm + (v >> 5), bit);
 }
 
 // Warp-tile push expansion (no shared memory, no barriers): a batch of
@@ -76,8 +76,7 @@ struct PushBits {
 #pragma unroll
     for (int r = 0; r < B; ++r) word[r] = v[r] >= 0 ? ld_probe(vbm + (v[r] >> 5)) : ~0u;
 #pragma unroll
-    for (int r = 0; r < B; ++r)
-      if (v[r] >= 0) mark(vbm, v[r], word[r]);
+    for (int r = 0; r < B; ++r) mark(vbm, v[r] >= 0 ? v[r] : 0, word[r]);  // dead: word = ~0
   }
   __device__ __forceinline__ void visit(int64_t p) {
     const int32_t u = ld_stream(idx + p);
@@ -137,8 +136,9 @@ struct PushBitsSmem {
     for (int r = 0; r < B; ++r) {
       const uint32_t bit = 1u << (v[r] & 31);
       const bool clear = !(word[r] & bit);
-      if (clear && (uint32_t)v[r] < (uint32_t)pbits) atomicOr(sbm + (v[r] >> 5), bit);
-      if (clear && v[r] >= pbits) atomicOr(vbm + (v[r] >> 5), bit);
+      const int32_t w = v[r] >= 0 ? v[r] >> 5 : 0;
+      red_or_shared_if(clear && (uint32_t)v[r] < (uint32_t)pbits, sbm + (w < pbits / 32 ? w : 0), bit);
+      red_or_if(clear && v[r] >= pbits, vbm + w, bit);
     }
   }
   __device__ __forceinline__ void visit(int64_t p) {
@@ -462,8 +462,16 @@ static gb_status launch_push_smem_t(gb_ctx* ctx, int64_t K, const LbsPlan& plan,
   return GB_OK;
 }
 
+// The ordered graph uses the global-probe push (its hot prefix stays in L1);
+// GB_PUSH_SMEM=1 selects the shared-memory prefix kernel instead (A/B).
+static bool push_smem_enabled() {
+  static const bool on = getenv("GB_PUSH_SMEM") && atoi(getenv("GB_PUSH_SMEM")) == 1;
+  return on;
+}
+
 static gb_status launch_push_smem(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
                                   EdgeOn on, uint32_t* vbm, const uint32_t* vprev) {
+  if (!push_smem_enabled()) return launch_push(ctx, K, plan, a, on, vbm);
   return a->values ? launch_push_smem_t<true>(ctx, K, plan, a, on, vbm, vprev)
                    : launch_push_smem_t<false>(ctx, K, plan, a, on, vbm, vprev);
 }
@@ -717,6 +725,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   const int grid_expand = push.values ? resident_grid(ctx, bfs_expand_warp<true>, 256)
                                       : resident_grid(ctx, bfs_expand_warp<false>, 256);
   const bool ordered = G->rank != nullptr;
+  const bool use_smem = ordered && push_smem_enabled();
   size_t smem = 0;
   const int grid_smem = push.values ? smem_push_setup<true>(ctx, W, &smem)
                                     : smem_push_setup<false>(ctx, W, &smem);
@@ -730,7 +739,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part,
                                                         G->rowstart, G->S);
     g_tile_first<<<grid_tiles, 256, 0, s>>>(&st->K, G->S, G->tile_first);
-    if (!push_dead && ordered) {
+    if (!push_dead && use_smem) {
       if (push.values)
         bfs_expand_smem<true><<<grid_smem, kSmemPushThreads, smem, s>>>(
             dptr(&st->K), G->S, G->rowstart, G->tile_first, push.indices, push_on, G->vbm, G->vprev, W);

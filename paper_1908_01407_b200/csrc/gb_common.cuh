@@ -263,6 +263,17 @@ __device__ __forceinline__ uint32_t ld_probe(const uint32_t* p) {
   return v;
 }
 
+// Predicated fire-and-forget OR (one RED instruction, no branch region).
+__device__ __forceinline__ void red_or_if(bool pred, uint32_t* addr, uint32_t bits) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p red.global.or.b32 [%0], %1; }"
+               :: "l"(addr), "r"(bits), "r"((uint32_t)pred));
+}
+__device__ __forceinline__ void red_or_shared_if(bool pred, uint32_t* addr, uint32_t bits) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(addr);
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p red.shared.or.b32 [%0], %1; }"
+               :: "r"(a), "r"(bits), "r"((uint32_t)pred));
+}
+
 __device__ __forceinline__ bool bit_test(const uint32_t* bm, int64_t i) {
   return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
 }
