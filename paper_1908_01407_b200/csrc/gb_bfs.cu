@@ -502,7 +502,7 @@ struct BfsState {
   int64_t it, K, depth, dnext, unstamp;  // loop state
 };
 
-constexpr int kGScanBlocks = 592;  // <= 1024 (single-block top scan)
+constexpr int kGScanBlocks = 592;  // partial sums; each apply block folds its predecessors
 constexpr int kGScanThreads = 256;
 constexpr int kGScanItems = 4;
 constexpr int64_t kGraphMaxCap = 1 << 20;  // longer loop caps use the host-driven path
@@ -529,28 +529,37 @@ g_scan_partials(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(1024) g_scan_top(int nb, int64_t* __restrict__ part) {
-  using BlockScan = cub::BlockScan<int64_t, 1024>;
-  __shared__ typename BlockScan::TempStorage tmp;
-  const int64_t x = threadIdx.x < nb ? part[threadIdx.x] : 0;
-  int64_t pre, agg;
-  BlockScan(tmp).ExclusiveSum(x, pre, agg);
-  if (threadIdx.x < nb) part[threadIdx.x] = pre;
-  if (threadIdx.x == 0) part[nb] = agg;
-}
-
-// rowstart[k] = off[F[k]], S = exclusive scan of the degrees, S[K] = E
+// rowstart[k] = off[F[k]], S = exclusive scan of the degrees, S[K] = E, and
+// tile_first[t] = the entry holding expansion slot t*kWarpTile.  Each block
+// derives its own carry-in from the partials (no separate top-level scan),
+// and every non-empty entry stamps the tiles that start inside its range, so
+// one launch replaces scan-top / scan-apply / tile-first.
 __global__ void __launch_bounds__(kGScanThreads)
 g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
              const int64_t* __restrict__ off, const int64_t* __restrict__ part,
-             int64_t* __restrict__ rowstart, int64_t* __restrict__ S) {
+             int64_t* __restrict__ rowstart, int64_t* __restrict__ S,
+             int32_t* __restrict__ tile_first) {
   using BlockScan = cub::BlockScan<int64_t, kGScanThreads>;
-  __shared__ typename BlockScan::TempStorage tmp;
+  using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
+  __shared__ union {
+    typename BlockScan::TempStorage scan;
+    typename BlockReduce::TempStorage red;
+  } tmp;
+  __shared__ int64_t s_run;
   const int64_t K = *Kp;
   int64_t lo, hi;
   g_range(K, &lo, &hi);
-  if (blockIdx.x == 0 && threadIdx.x == 0) S[K] = part[gridDim.x];
-  int64_t run = part[blockIdx.x];
+  {
+    int64_t c = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += kGScanThreads) c += part[i];
+    const int64_t run0 = BlockReduce(tmp.red).Sum(c);
+    if (threadIdx.x == 0) {
+      s_run = run0;
+      if (blockIdx.x == gridDim.x - 1) S[K] = run0 + part[blockIdx.x];
+    }
+    __syncthreads();
+  }
+  int64_t run = s_run;
   for (int64_t base = lo; base < hi; base += kGScanThreads * kGScanItems) {
     int64_t d[kGScanItems];
     int64_t sum = 0;
@@ -567,33 +576,22 @@ g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
       sum += d[i];
     }
     int64_t pre, agg;
-    BlockScan(tmp).ExclusiveSum(sum, pre, agg);
+    BlockScan(tmp.scan).ExclusiveSum(sum, pre, agg);
     int64_t acc = run + pre;
 #pragma unroll
     for (int i = 0; i < kGScanItems; ++i) {
       const int64_t k = base + threadIdx.x * kGScanItems + i;
-      if (k < hi) S[k] = acc;
+      if (k < hi) {
+        S[k] = acc;
+        if (d[i] > 0) {
+          for (int64_t t = (acc + kWarpTile - 1) / kWarpTile; t * kWarpTile < acc + d[i]; ++t)
+            tile_first[t] = (int32_t)k;
+        }
+      }
       acc += d[i];
     }
     run += agg;
     __syncthreads();
-  }
-}
-
-__global__ void g_tile_first(const int64_t* __restrict__ Kp, const int64_t* __restrict__ S,
-                             int32_t* __restrict__ tile_first) {
-  const int64_t K = *Kp;
-  const int64_t E = S[K];
-  const int64_t ntiles = (E + kWarpTile - 1) / kWarpTile;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = t * kWarpTile;
-    int64_t lo = 0, hi = K - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (S[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    tile_first[t] = (int32_t)lo;
   }
 }
 
@@ -721,7 +719,6 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   const bool pull_dead = !pull.values && pull.iso_i64 == 0 && pull.iso_f64 == 0.0;
   BfsState* st = G->st;
   const int grid_w = grid_for(ctx, W, 256, 8);
-  const int grid_tiles = grid_for(ctx, push.nnz / kWarpTile + 1, 256);
   const int grid_expand = push.values ? resident_grid(ctx, bfs_expand_warp<true>, 256)
                                       : resident_grid(ctx, bfs_expand_warp<false>, 256);
   const bool ordered = G->rank != nullptr;
@@ -729,16 +726,14 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   size_t smem = 0;
   const int grid_smem = push.values ? smem_push_setup<true>(ctx, W, &smem)
                                     : smem_push_setup<false>(ctx, W, &smem);
-  G->launches_push = 5 + (push_dead ? 0 : 1);
+  G->launches_push = 3 + (push_dead ? 0 : 1);
   G->launches_pull = pull_dead ? 3 : 1;
   G->launches_fixed = 8;  // 4 memsets, zero (or unpermute), start, unstamp (+2 per level below)
 
   auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
     g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part);
-    g_scan_top<<<1, 1024, 0, s>>>(kGScanBlocks, G->part);
     g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part,
-                                                        G->rowstart, G->S);
-    g_tile_first<<<grid_tiles, 256, 0, s>>>(&st->K, G->S, G->tile_first);
+                                                        G->rowstart, G->S, G->tile_first);
     if (!push_dead && use_smem) {
       if (push.values)
         bfs_expand_smem<true><<<grid_smem, kSmemPushThreads, smem, s>>>(
