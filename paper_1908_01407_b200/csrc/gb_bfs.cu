@@ -62,6 +62,14 @@ struct PushBits {
   EdgeOn on;
   uint32_t* __restrict__ vbm;
   template <int B>
+  __device__ __forceinline__ void probe_mark(const int32_t (&v)[B]) {
+    uint32_t word[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) word[r] = v[r] >= 0 ? ld_probe(vbm + (v[r] >> 5)) : ~0u;
+#pragma unroll
+    for (int r = 0; r < B; ++r) mark(vbm, v[r] >= 0 ? v[r] : 0, word[r]);  // dead: word = ~0
+  }
+  template <int B>
   __device__ __forceinline__ void batch(const int64_t (&p)[B], const bool (&live)[B]) {
     int32_t v[B];
 #pragma unroll
@@ -72,11 +80,26 @@ struct PushBits {
         v[r] = (!VALS || on(p[r])) ? c : -1;
       }
     }
-    uint32_t word[B];
+    probe_mark<B>(v);
+  }
+  // slots h + r*32 + lane of a tile inside one or two lists (warp_tiles):
+  // positions are formed on the fly, no per-item 64-bit array
+  template <int B>
+  __device__ __forceinline__ void batch2(int64_t b0, int64_t b1, int32_t st1, int32_t rel_end,
+                                         int32_t h) {
+    const int32_t lane = threadIdx.x & 31;
+    int32_t v[B];
 #pragma unroll
-    for (int r = 0; r < B; ++r) word[r] = v[r] >= 0 ? ld_probe(vbm + (v[r] >> 5)) : ~0u;
-#pragma unroll
-    for (int r = 0; r < B; ++r) mark(vbm, v[r] >= 0 ? v[r] : 0, word[r]);  // dead: word = ~0
+    for (int r = 0; r < B; ++r) {
+      const int32_t er = h + r * 32 + lane;
+      const int64_t pos = (er >= st1 ? b1 : b0) + er;
+      v[r] = -1;
+      if (er < rel_end) {
+        const int32_t c = ld_stream(idx + pos);
+        v[r] = (!VALS || on(pos)) ? c : -1;
+      }
+    }
+    probe_mark<B>(v);
   }
   __device__ __forceinline__ void visit(int64_t p) {
     const int32_t u = ld_stream(idx + p);
@@ -84,14 +107,34 @@ struct PushBits {
   }
 };
 
-template <bool VALS>
-__global__ void __launch_bounds__(256)
+template <bool VALS, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 bfs_expand_warp(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
-                const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
+                const int32_t* __restrict__ tile_first, const int64_t* __restrict__ tile_base,
+                const int32_t* __restrict__ idx,
                 EdgeOn on, uint32_t* __restrict__ vbm) {
   const int64_t K = Kd.get();
   PushBits<VALS> f{idx, on, vbm};
-  warp_tiles(K, S, rowstart, tile_first, f);
+  warp_tiles(K, S, rowstart, tile_first, tile_base, f);
+}
+
+using ExpandKernel = void (*)(DevI64, const int64_t*, const int64_t*, const int32_t*,
+                              const int64_t*, const int32_t*, EdgeOn, uint32_t*);
+
+// Register budget of the push (GB_PUSH_MINB = minimum resident CTAs of 256
+// threads per SM: 1 leaves the allocation to ptxas, 3 allows 80, 4 caps at 64,
+// 5 (default, 40 warps per SM, measured best) at 48, 6 at 40).
+template <bool VALS>
+static ExpandKernel expand_kernel() {
+  static const int minb = getenv("GB_PUSH_MINB") ? atoi(getenv("GB_PUSH_MINB")) : 5;
+  switch (minb) {
+    case 1: return bfs_expand_warp<VALS, 1>;
+    case 4: return bfs_expand_warp<VALS, 4>;
+    case 5: return bfs_expand_warp<VALS, 5>;
+    case 6: return bfs_expand_warp<VALS, 6>;
+    case 3: return bfs_expand_warp<VALS, 3>;
+    default: return bfs_expand_warp<VALS, 5>;
+  }
 }
 
 // Push over a degree-ordered graph: the visited bits of the
@@ -113,9 +156,6 @@ struct PushBitsSmem {
   uint32_t* __restrict__ vbm;
   uint32_t* sbm;
   int32_t pbits;  // vertices [0, pbits) are tracked in shared memory
-  // Branch-free per item: every item reads a shared word (word 0 when its
-  // vertex is outside the prefix), only suffix items issue a global probe,
-  // and the marks are predicated atomics -- no divergent regions.
   template <int B>
   __device__ __forceinline__ void batch(const int64_t (&p)[B], const bool (&live)[B]) {
     int32_t v[B];
@@ -125,6 +165,28 @@ struct PushBitsSmem {
       if (live[r]) v[r] = ld_stream(idx + p[r]);
       if (VALS && v[r] >= 0 && !on(p[r])) v[r] = -1;
     }
+    probe_mark<B>(v);
+  }
+  template <int B>
+  __device__ __forceinline__ void batch2(int64_t b0, int64_t b1, int32_t st1, int32_t rel_end,
+                                         int32_t h) {
+    const int32_t lane = threadIdx.x & 31;
+    int32_t v[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      const int32_t er = h + r * 32 + lane;
+      const int64_t pos = (er >= st1 ? b1 : b0) + er;
+      v[r] = -1;
+      if (er < rel_end) v[r] = ld_stream(idx + pos);
+      if (VALS && v[r] >= 0 && !on(pos)) v[r] = -1;
+    }
+    probe_mark<B>(v);
+  }
+  // Branch-free per item: every item reads a shared word (word 0 when its
+  // vertex is outside the prefix), only suffix items issue a global probe,
+  // and the marks are predicated atomics -- no divergent regions.
+  template <int B>
+  __device__ __forceinline__ void probe_mark(const int32_t (&v)[B]) {
     uint32_t word[B];
 #pragma unroll
     for (int r = 0; r < B; ++r) {
@@ -156,7 +218,8 @@ struct PushBitsSmem {
 template <bool VALS>
 __global__ void __launch_bounds__(kSmemPushThreads, 1)
 bfs_expand_smem(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
-                const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
+                const int32_t* __restrict__ tile_first, const int64_t* __restrict__ tile_base,
+                const int32_t* __restrict__ idx,
                 EdgeOn on, uint32_t* __restrict__ vbm, const uint32_t* __restrict__ vprev,
                 int64_t W) {
   extern __shared__ uint32_t sbm[];
@@ -171,7 +234,7 @@ bfs_expand_smem(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restr
     __syncthreads();
   }
   PushBitsSmem<VALS> f{idx, on, vbm, sbm, use ? (int32_t)(P * 32) : 0};
-  warp_tiles(K, S, rowstart, tile_first, f);
+  warp_tiles(K, S, rowstart, tile_first, tile_base, f);
   if (use) {
     __syncthreads();
     for (int64_t w = threadIdx.x; w < P; w += blockDim.x) {
@@ -438,8 +501,9 @@ __global__ void bfs_unstamp(DevI64 Kd, const int32_t* __restrict__ F, int64_t* _
 template <bool VALS>
 static gb_status launch_push_t(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
                                EdgeOn on, uint32_t* vbm) {
-  bfs_expand_warp<VALS><<<resident_grid(ctx, bfs_expand_warp<VALS>, 256), 256, 0, stream_of(ctx)>>>(
-      dval(K), plan.S, plan.rowstart, plan.tile_first, a->indices, on, vbm);
+  const ExpandKernel k = expand_kernel<VALS>();
+  k<<<resident_grid(ctx, k, 256), 256, 0, stream_of(ctx)>>>(
+      dval(K), plan.S, plan.rowstart, plan.tile_first, plan.tile_base, a->indices, on, vbm);
   GB_LAUNCH_CHECK(ctx);
   return GB_OK;
 }
@@ -457,7 +521,7 @@ static gb_status launch_push_smem_t(gb_ctx* ctx, int64_t K, const LbsPlan& plan,
   size_t smem = 0;
   const int grid = smem_push_setup<VALS>(ctx, W, &smem);
   bfs_expand_smem<VALS><<<grid, kSmemPushThreads, smem, stream_of(ctx)>>>(
-      dval(K), plan.S, plan.rowstart, plan.tile_first, a->indices, on, vbm, vprev, W);
+      dval(K), plan.S, plan.rowstart, plan.tile_first, plan.tile_base, a->indices, on, vbm, vprev, W);
   GB_LAUNCH_CHECK(ctx);
   return GB_OK;
 }
@@ -538,7 +602,7 @@ __global__ void __launch_bounds__(kGScanThreads)
 g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
              const int64_t* __restrict__ off, const int64_t* __restrict__ part,
              int64_t* __restrict__ rowstart, int64_t* __restrict__ S,
-             int32_t* __restrict__ tile_first) {
+             int32_t* __restrict__ tile_first, int64_t* __restrict__ tile_base) {
   using BlockScan = cub::BlockScan<int64_t, kGScanThreads>;
   using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
   __shared__ union {
@@ -584,8 +648,11 @@ g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
       if (k < hi) {
         S[k] = acc;
         if (d[i] > 0) {
-          for (int64_t t = (acc + kWarpTile - 1) / kWarpTile; t * kWarpTile < acc + d[i]; ++t)
+          const int64_t b = rowstart[k] - acc;
+          for (int64_t t = (acc + kWarpTile - 1) / kWarpTile; t * kWarpTile < acc + d[i]; ++t) {
             tile_first[t] = (int32_t)k;
+            tile_base[t] = b;
+          }
         }
       }
       acc += d[i];
@@ -674,6 +741,7 @@ struct BfsGraph {
   uint32_t *vbm = nullptr, *vprev = nullptr, *fbm[2] = {nullptr, nullptr};
   int32_t* F = nullptr;
   int32_t* tile_first = nullptr;
+  int64_t* tile_base = nullptr;
   unsigned long long* cnt = nullptr;
   int64_t *rowstart = nullptr, *S = nullptr, *part = nullptr;
   int64_t* lv = nullptr;  // relabelled graph: levels by new id (never cleared)
@@ -719,8 +787,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   const bool pull_dead = !pull.values && pull.iso_i64 == 0 && pull.iso_f64 == 0.0;
   BfsState* st = G->st;
   const int grid_w = grid_for(ctx, W, 256, 8);
-  const int grid_expand = push.values ? resident_grid(ctx, bfs_expand_warp<true>, 256)
-                                      : resident_grid(ctx, bfs_expand_warp<false>, 256);
+  const ExpandKernel expand = push.values ? expand_kernel<true>() : expand_kernel<false>();
+  const int grid_expand = resident_grid(ctx, expand, 256);
   const bool ordered = G->rank != nullptr;
   const bool use_smem = ordered && push_smem_enabled();
   size_t smem = 0;
@@ -733,21 +801,18 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
     g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part);
     g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part,
-                                                        G->rowstart, G->S, G->tile_first);
+                                                        G->rowstart, G->S, G->tile_first,
+                                                        G->tile_base);
     if (!push_dead && use_smem) {
       if (push.values)
         bfs_expand_smem<true><<<grid_smem, kSmemPushThreads, smem, s>>>(
-            dptr(&st->K), G->S, G->rowstart, G->tile_first, push.indices, push_on, G->vbm, G->vprev, W);
+            dptr(&st->K), G->S, G->rowstart, G->tile_first, G->tile_base, push.indices, push_on, G->vbm, G->vprev, W);
       else
         bfs_expand_smem<false><<<grid_smem, kSmemPushThreads, smem, s>>>(
-            dptr(&st->K), G->S, G->rowstart, G->tile_first, push.indices, push_on, G->vbm, G->vprev, W);
+            dptr(&st->K), G->S, G->rowstart, G->tile_first, G->tile_base, push.indices, push_on, G->vbm, G->vprev, W);
     } else if (!push_dead) {
-      if (push.values)
-        bfs_expand_warp<true><<<grid_expand, 256, 0, s>>>(dptr(&st->K), G->S, G->rowstart,
-                                                          G->tile_first, push.indices, push_on, G->vbm);
-      else
-        bfs_expand_warp<false><<<grid_expand, 256, 0, s>>>(dptr(&st->K), G->S, G->rowstart,
-                                                           G->tile_first, push.indices, push_on, G->vbm);
+      expand<<<grid_expand, 256, 0, s>>>(dptr(&st->K), G->S, G->rowstart, G->tile_first,
+                                         G->tile_base, push.indices, push_on, G->vbm);
     }
     bfs_finalize<<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev, G->fbm[h ^ 1],
                                         pptr(&st->levels), G->F, G->cnt + h, G->cnt + (h ^ 1),
@@ -896,6 +961,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
     const size_t o_vbm = take(4 * W), o_vprev = take(4 * W), o_f0 = take(4 * W), o_f1 = take(4 * W);
     const size_t o_F = take(4 * (size_t)n), o_tf = take(4 * (size_t)(push->nnz / kWarpTile + 2));
+    const size_t o_tb = take(8 * (size_t)(push->nnz / kWarpTile + 2));
     const size_t o_cnt = take(16), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
     const size_t o_lv = rank ? take(8 * (size_t)n) : 0;
@@ -911,6 +977,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->fbm[1] = (uint32_t*)(m + o_f1);
     G->F = (int32_t*)(m + o_F);
     G->tile_first = (int32_t*)(m + o_tf);
+    G->tile_base = (int64_t*)(m + o_tb);
     G->cnt = (unsigned long long*)(m + o_cnt);
     G->rowstart = (int64_t*)(m + o_rs);
     G->S = (int64_t*)(m + o_S);

@@ -25,9 +25,11 @@ __global__ void lbs_degrees(int64_t K, const int32_t* __restrict__ ids,
                             int64_t* __restrict__ deg);
 
 // S = exclusive scan of deg (K+1 entries, S[K] = E); tile_first[t] = the
-// frontier entry whose range contains edge t*TE.
-__global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S, int64_t tile,
-                               int32_t* __restrict__ tile_first);
+// frontier entry whose range contains edge t*TE; tile_base[t] (optional) =
+// rowstart - S of that entry, so a slot e of the tile sits at tile_base + e.
+__global__ void lbs_tile_first(int64_t K, const int64_t* __restrict__ S,
+                               const int64_t* __restrict__ rowstart, int64_t tile,
+                               int32_t* __restrict__ tile_first, int64_t* __restrict__ tile_base);
 
 // Expansion kernel.  f(k, p, e) is called once per edge e of the expansion,
 // where k is the frontier position and p the position in the orientation's
@@ -89,6 +91,7 @@ struct LbsPlan {
   int64_t* rowstart = nullptr;
   int64_t* S = nullptr;
   int32_t* tile_first = nullptr;
+  int64_t* tile_base = nullptr;  // warp tiles only
   int grid = 0;
 };
 
@@ -102,9 +105,11 @@ gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
 // frontier entries of the tile, held one per lane and read with shuffles --
 // no shared memory and no block barriers.  Tiles that touch more than 32
 // frontier entries (many tiny adjacency lists) walk them one lane per entry.
-// f.visit(k, p) is called for every edge; F must provide
+// f.visit(p) is called for single edges; F must also provide
 //   template <int B> void batch(const int64_t (&p)[B], const bool (&live)[B])
-// for the batched fast path.
+//   template <int B> void batch2(b0, b1, st1, rel_end, h)
+// for the batched paths (batch2: slots h + r*32 + lane of a tile that lies in
+// at most two lists, slot e at b0 + e before st1 and at b1 + e from st1 on).
 // ---------------------------------------------------------------------------
 constexpr int kWarpItems = 16;
 constexpr int kWarpTile = 32 * kWarpItems;  // 512 slots
@@ -112,24 +117,38 @@ constexpr int kWarpTile = 32 * kWarpItems;  // 512 slots
 template <class F>
 __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* __restrict__ S,
                                            const int64_t* __restrict__ rowstart,
-                                           const int32_t* __restrict__ tile_first, F& f) {
+                                           const int32_t* __restrict__ tile_first,
+                                           const int64_t* __restrict__ tile_base, F& f) {
   const int lane = threadIdx.x & 31;
   const int64_t E = S[K];
   const int64_t ntiles = (E + kWarpTile - 1) / kWarpTile;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // the next tile's descriptor is loaded one tile ahead (three independent
+  // loads), so a tile inside one list starts without a dependent round trip
+  int32_t k0n = 0, k1n = 0;
+  int64_t bn = 0;
+  if (w0 < ntiles) {
+    k0n = tile_first[w0];
+    k1n = w0 + 1 < ntiles ? tile_first[w0 + 1] : (int32_t)(K - 1);
+    if (tile_base) bn = tile_base[w0];
+  }
   for (int64_t t = w0; t < ntiles; t += nw) {
     const int64_t e0 = t * kWarpTile;
     const int64_t e1 = e0 + kWarpTile < E ? e0 + kWarpTile : E;
-    const int64_t k0 = tile_first[t];
-    const int64_t k1 = t + 1 < ntiles ? tile_first[t + 1] : K - 1;
+    const int64_t k0 = k0n, k1 = k1n, tb = bn;
+    const int64_t tn = t + nw;
+    if (tn < ntiles) {
+      k0n = tile_first[tn];
+      k1n = tn + 1 < ntiles ? tile_first[tn + 1] : (int32_t)(K - 1);
+      if (tile_base) bn = tile_base[tn];
+    }
     const int64_t nk = k1 - k0 + 1;
     if (nk <= 2) {
       // Most tiles of a power-law push level lie inside one or two adjacency
       // lists (R-MAT s24 level 2: 69 % one, 22 % two): the owner is one
       // compare per item and the loads are warp-uniform broadcasts.
-      const int64_t s0 = S[k0];
-      const int64_t b0 = rowstart[k0] - s0 + e0;
+      const int64_t b0 = (tile_base ? tb : rowstart[k0] - S[k0]) + e0;
       int32_t st1 = INT32_MAX;
       int64_t b1 = b0;
       if (nk == 2) {
@@ -139,18 +158,8 @@ __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* __restrict_
       }
       const int32_t rel_end = (int32_t)(e1 - e0);
 #pragma unroll
-      for (int h = 0; h < kWarpItems; h += kWarpItems / 2) {
-        constexpr int B = kWarpItems / 2;
-        int64_t p[B];
-        bool live[B];
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-          const int32_t er = (h + r) * 32 + lane;
-          live[r] = er < rel_end;
-          p[r] = (er >= st1 ? b1 : b0) + er;
-        }
-        f.template batch<B>(p, live);
-      }
+      for (int h = 0; h < kWarpItems; h += kWarpItems / 2)
+        f.template batch2<kWarpItems / 2>(b0, b1, st1, rel_end, h * 32);
     } else if (nk <= 32) {
       // Entry j of the tile (lane j) starts at st_rel (relative to e0; the
       // first entry's start is clamped to 0).  Slot e_rel = r*32 + lane
@@ -178,8 +187,8 @@ __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* __restrict_
       int64_t base = __shfl_sync(GB_FULL, base_l, own) + e0;
       const int32_t rel_end = (int32_t)(e1 - e0);
 #pragma unroll
-      for (int h = 0; h < kWarpItems; h += kWarpItems / 2) {
-        constexpr int B = kWarpItems / 2;
+      for (int h = 0; h < kWarpItems; h += kWarpItems / 4) {
+        constexpr int B = kWarpItems / 4;  // small batches keep the kernel's register count low
         int64_t p[B];
         bool live[B];
 #pragma unroll
@@ -201,9 +210,9 @@ __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* __restrict_
         f.template batch<B>(p, live);
       }
     } else {
-      // many short lists: 8 entries per lane at a time, their bounds and first
-      // edges batched (one round trip for 256 entries), the rest walked
-      constexpr int B = 8;
+      // many short lists: 4 entries per lane at a time, their bounds and first
+      // edges batched (one round trip for 128 entries), the rest walked
+      constexpr int B = 4;
       for (int64_t i0 = 0; i0 < nk; i0 += 32 * B) {
         int32_t len[B];  // edges of the entry inside this tile
         int64_t p[B];    // position of its first edge in the tile

@@ -44,8 +44,8 @@ gb_status row_tiles_plan(gb_ctx* ctx, Arena& ar, int64_t n, const int64_t* off, 
                                                      plan->nz_off);
   GB_TRY(read_i64(ctx, pos + n, &plan->R));
   if (plan->R > 0)
-    lbs_tile_first<<<grid_for(ctx, nnz / kRowTile + 1, 256), 256, 0, s>>>(plan->R, plan->nz_off, kRowTile,
-                                                                plan->tile_first);
+    lbs_tile_first<<<grid_for(ctx, nnz / kRowTile + 1, 256), 256, 0, s>>>(
+        plan->R, plan->nz_off, nullptr, kRowTile, plan->tile_first, nullptr);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 5);
   return GB_OK;
