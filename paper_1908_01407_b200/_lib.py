@@ -16,7 +16,8 @@ import numpy as np
 from .errors import FormatError, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgraphblast_sm100a.so")
+# GB_LIB: load another build of the library (A/B of compile-time variants)
+LIB_PATH = os.environ.get("GB_LIB") or os.path.join(_HERE, "libgraphblast_sm100a.so")
 
 # gb_status codes (graphblast.h)
 GB_OK = 0

@@ -94,23 +94,34 @@ mv_pull_rows(int64_t nrows, const int64_t* __restrict__ off, const int32_t* __re
 }
 
 // ---------------------------------------------------------------------------
-// Edge-balanced masked pull (commutative folds, no early exit): the row-tile
-// layout of gb_rowtiles.cuh (512-entry warp tiles over the non-empty rows,
-// 16 consecutive column indices per lane via 16-byte loads) with the mask
-// applied per entry: a lane first walks its entries' rows in shared memory
-// to flag the allowed ones, then issues all their u gathers (and value loads)
-// at once, then folds row by row.  `out` holds the identity beforehand (rows
-// that are masked out, empty or without contributions keep it); whole rows
-// are stored, rows split across lanes are combined with an atomic fold.
-// Counters are exact: reads and multiplies are block-reduced; a row split
-// across lanes marks `hasmul` so that rows with >= 1 multiply are counted
-// once (adds = multiplies - such rows, kernels.py:185-189).
-// ---------------------------------------------------------------------------
+// Edge-balanced masked pull (commutative folds, no early exit): warp tiles of
+// 512 consecutive entries over the non-empty rows (gb_rowtiles.cuh layout).
+// Per tile the row starts and row-allowed flags are staged in shared memory;
+// each lane owns 16 consecutive entries:
+//   1. it walks its entries' rows and flags the allowed ones,
+//   2. loads the column indices of the 4-entry groups that hold an allowed
+//      entry (16-byte loads; masked-out rows cost no index traffic) and
+//      issues all u gathers at once,
+//   3. folds row segment by row segment.  A row wholly inside the lane is
+//      stored directly; a row that crosses lanes is combined by a warp
+//      segmented scan over the lanes' open segments and written once, by the
+//      lane where it ends -- a plain store when the row lies inside the tile,
+//      one atomic fold when it crosses a tile boundary.  Hub rows therefore
+//      cost one atomic per 512 entries instead of one per lane.
+// Rows with no contribution keep the identity `out` was filled with.
+// Counters are exact: reads and multiplies are block-reduced; rows with >= 1
+// multiply are counted where they are written (tile-crossing rows through
+// the `hasmul` bitmap, deduplicated by mv_pull_finish): adds = multiplies -
+// such rows (kernels.py:185-189).
 // ADD / MUL >= 0 fix the semiring at compile time (the builtin semirings,
 // algebra.py:161-179); -1 reads add_op / mult_op at run time.  VALS = false
 // for iso (structure-only) matrices.
+// ---------------------------------------------------------------------------
+#ifndef GB_MV_MINB
+#define GB_MV_MINB 3  // resident 256-thread CTAs per SM (3: 80 registers, no spills)
+#endif
 template <class T, int ADD, int MUL, bool VALS>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, GB_MV_MINB)
 mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
               const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
               const T* __restrict__ vals, T iso, const T* __restrict__ u,
@@ -134,26 +145,11 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
   unsigned long long c_reads = 0, c_muls = 0, c_rows = 0;
   for (int64_t t = w0; t < ntiles; t += nw) {
     const int64_t e0 = t * kRowTile;
-    const int64_t e1 = e0 + kRowTile < E ? e0 + kRowTile : E;
-    const int64_t my0 = e0 + (int64_t)lane * kRowItems;
-    const int64_t my1 = my0 + kRowItems < e1 ? my0 + kRowItems : e1;
-    int32_t cols[kRowItems];
-    if (my0 + kRowItems <= e1) {
-      const int4* p4 = reinterpret_cast<const int4*>(idx + my0);
-#pragma unroll
-      for (int q = 0; q < kRowItems / 4; ++q) {
-        int4 v;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
-        cols[4 * q] = v.x; cols[4 * q + 1] = v.y; cols[4 * q + 2] = v.z; cols[4 * q + 3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < kRowItems; ++q) cols[q] = my0 + q < e1 ? ld_stream(idx + my0 + q) : 0;
-    }
+    const int32_t rel_end = (int32_t)((e0 + kRowTile < E ? e0 + kRowTile : E) - e0);
     const int64_t r0 = tile_first[t];
     const int64_t r1 = t + 1 < ntiles ? tile_first[t + 1] : R_rows - 1;
     const int nr = (int)(r1 - r0 + 1);
+    // row starts relative to the tile, clamped to [0, kRowTile]; st[nr] ends the last row
     for (int i = lane; i <= nr; i += 32) {
       const int64_t o = nz_off[r0 + i] - e0;
       st[i] = (uint16_t)(o < 0 ? 0 : (o > kRowTile ? kRowTile : o));
@@ -162,82 +158,171 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
         okr[i] = !mask || ((__ldg(mask + (row >> 5)) >> (row & 31)) & 1u);
       }
     }
+    // does the tile's first row start before it / its last row end after it?
+    const bool head_out = nz_off[r0] < e0;
+    const bool tail_out = nz_off[r1 + 1] > e0 + rel_end;
     __syncwarp();
-    if (my0 < e1) {
-      const int rel0 = lane * kRowItems, rel1 = (int)(my1 - e0);
-      int lo = 0, hi = nr - 1;
+    const int rel0 = lane * kRowItems;
+    const int rel1 = rel0 + kRowItems < rel_end ? rel0 + kRowItems : rel_end;
+    int lo = 0;
+    if (rel0 < rel1) {
+      int hi = nr - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (st[mid] <= rel0) lo = mid; else hi = mid - 1;
       }
-      // pass 1: which of my entries belong to allowed rows
-      uint32_t allowed = 0;
-      {
-        int cur = lo, next = st[lo + 1];
-        bool ok = okr[cur];
+    }
+    // pass 1 (per row segment, not per entry): which of my entries belong to
+    // allowed rows
+    uint32_t allowed = 0;
+    if (rel0 < rel1) {
+      int a = rel0, c = lo;
+      do {
+        const int b = st[c + 1] < rel1 ? st[c + 1] : rel1;
+        if (okr[c]) allowed |= ((1u << (b - a)) - 1u) << (a - rel0);
+        a = b;
+        ++c;
+      } while (a < rel1);
+    }
+    // pass 2: column indices of the groups holding an allowed entry, then
+    // every gather at once
+    int32_t cols[kRowItems];
+    const int64_t my0 = e0 + rel0;
+    if (rel1 - rel0 == kRowItems) {
+      const int4* p4 = reinterpret_cast<const int4*>(idx + my0);
 #pragma unroll
-        for (int q = 0; q < kRowItems; ++q) {
-          const int e = rel0 + q;
-          if (e < rel1) {
-            while (e >= next) {
-              ++cur;
-              next = st[cur + 1];
-              ok = okr[cur];
-            }
-            if (ok) allowed |= 1u << q;
-          }
-        }
+      for (int g = 0; g < kRowItems / 4; ++g) {
+        int4 v = make_int4(0, 0, 0, 0);
+        if ((allowed >> (4 * g)) & 0xFu)
+          asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+              : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + g));
+        cols[4 * g] = v.x; cols[4 * g + 1] = v.y; cols[4 * g + 2] = v.z; cols[4 * g + 3] = v.w;
       }
-      // pass 2: gathers for the allowed entries, all issued before any use
-      T uv[kRowItems];
+    } else {
 #pragma unroll
-      for (int q = 0; q < kRowItems; ++q) uv[q] = (allowed >> q) & 1u ? __ldg(u + cols[q]) : ident;
-      // pass 3: fold row by row
-      int cur = lo;
-      int row_start = st[cur];
+      for (int q = 0; q < kRowItems; ++q) cols[q] = (allowed >> q) & 1u ? ld_stream(idx + my0 + q) : 0;
+    }
+    T uv[kRowItems];
+#pragma unroll
+    for (int q = 0; q < kRowItems; ++q) uv[q] = (allowed >> q) & 1u ? __ldg(u + cols[q]) : ident;
+    c_reads += __popc(allowed);
+    // pass 3: fold segment by segment.  Rows are non-empty, so one step
+    // always reaches the next segment.  A segment that ends inside the lane
+    // is either the lane's head (it continues a row from the previous lane:
+    // kept for the scan) or a whole row (stored: rows that end inside a lane
+    // and start inside it lie inside the tile).
+    T acc = ident;          // current segment
+    int cnt = 0;            // its multiplies
+    T h_acc = ident;        // head segment continuing a row from the previous lane
+    int h_cnt = 0;
+    int h_row = -1;         // its tile row index (-1: none, -2: a "through" lane)
+    int cur = lo;
+    if (rel0 < rel1) {
       int next = st[cur + 1];
-      T acc = ident;
-      long long incl = 0;
-      bool row_ok = false;
-      c_reads += __popc(allowed);
-      auto flush = [&](bool whole) {
-        const int32_t row = nz_rows[r0 + cur];
-        if (!row_ok) return;
-        c_muls += incl;
-        if (whole) {
-          out[row] = acc;
-          if (incl > 0) ++c_rows;
-        } else if (incl > 0) {
-          atomic_fold<T>(add_op, out + row, acc);
-          atomicOr(hasmul + (row >> 5), 1u << (row & 31));
-        }
-      };
+      // the lane's first segment continues a row from an earlier lane / tile
+      const bool cont = st[cur] < rel0 || (cur == 0 && head_out);
+      bool first = true;
 #pragma unroll
       for (int q = 0; q < kRowItems; ++q) {
         const int e = rel0 + q;
-        if (e < rel1) {
-          while (e >= next) {
-            flush(row_start >= rel0 && next <= rel1 && (cur > 0 || nz_off[r0] >= e0));
-            acc = ident;
-            incl = 0;
-            ++cur;
-            row_start = next;
-            next = st[cur + 1];
+        if (e < rel1 && e >= next) {
+          if (first && cont) {
+            h_acc = acc;
+            h_cnt = cnt;
+            h_row = cur;
+          } else if (cnt > 0) {
+            out[nz_rows[r0 + cur]] = acc;
+            c_muls += cnt;
+            ++c_rows;
           }
-          if ((allowed >> q) & 1u) {
-            row_ok = true;
-            if (uv[q] != ident) {
-              const T a = VALS ? __ldg(vals + my0 + q) : iso;
-              acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, a, uv[q]));
-              ++incl;
-            }
-          } else {
-            row_ok = false;
-          }
+          first = false;
+          acc = ident;
+          cnt = 0;
+          ++cur;
+          next = st[cur + 1];
+        }
+        if (((allowed >> q) & 1u) && uv[q] != ident) {
+          const T a = VALS ? __ldg(vals + my0 + q) : iso;
+          acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, a, uv[q]));
+          ++cnt;
         }
       }
-      flush(row_start >= rel0 && next <= rel1 && next < kRowTile + 1 &&
-            (cur > 0 || nz_off[r0] >= e0) && (cur < nr - 1 || nz_off[r1 + 1] <= e1));
+      // the last segment: closed when it ends at the lane end (and its row
+      // does not run past the tile)
+      if (next <= rel1 && !(cur == nr - 1 && tail_out)) {
+        if (first && cont) {
+          h_acc = acc;
+          h_cnt = cnt;
+          h_row = cur;
+        } else if (cnt > 0) {
+          const int32_t row = nz_rows[r0 + cur];
+          if (cur == 0 && head_out) {
+            atomic_fold<T>(add_op, out + row, acc);
+            atomicOr(hasmul + (row >> 5), 1u << (row & 31));
+          } else {
+            out[row] = acc;
+            ++c_rows;
+          }
+          c_muls += cnt;
+        }
+        acc = ident;
+        cnt = 0;
+        cur = -1;  // nothing open
+      } else if (first && cont) {
+        h_row = -2;  // one segment spanning the whole lane: it travels in the scan
+      }
+    } else {
+      cur = -1;
+    }
+    // warp segmented scan of the open tail segments (key = tile row index)
+    int key = cur;
+    T cv = acc;
+    int cc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int k2 = __shfl_up_sync(GB_FULL, key, o);
+      const T v2 = __shfl_up_sync(GB_FULL, cv, o);
+      const int c2 = __shfl_up_sync(GB_FULL, cc, o);
+      if (lane >= o && key >= 0 && k2 == key) {
+        cv = op_fold<T>(add_op, cv, v2);
+        cc += c2;
+      }
+    }
+    // the previous lane's scanned open segment completes my head segment
+    const int pk = __shfl_up_sync(GB_FULL, key, 1);
+    const T pv = __shfl_up_sync(GB_FULL, cv, 1);
+    const int pc = __shfl_up_sync(GB_FULL, cc, 1);
+    if (h_row >= 0) {
+      T v = h_acc;
+      int c = h_cnt;
+      if (lane > 0 && pk == h_row) {
+        v = op_fold<T>(add_op, v, pv);
+        c += pc;
+      }
+      if (c > 0) {
+        const int32_t row = nz_rows[r0 + h_row];
+        const bool in_tile = !(h_row == 0 && head_out) && !(h_row == nr - 1 && tail_out);
+        c_muls += c;
+        if (in_tile) {
+          out[row] = v;
+          ++c_rows;
+        } else {
+          atomic_fold<T>(add_op, out + row, v);
+          atomicOr(hasmul + (row >> 5), 1u << (row & 31));
+        }
+      }
+    }
+    // an open segment that no later lane closes (the row runs past the tile)
+    const int nk = __shfl_down_sync(GB_FULL, key, 1);
+    const int nh = __shfl_down_sync(GB_FULL, h_row, 1);
+    if (key >= 0) {
+      const bool continued = lane < 31 && (nk == key || nh == key);
+      if (!continued && cc > 0) {
+        const int32_t row = nz_rows[r0 + key];
+        c_muls += cc;
+        atomic_fold<T>(add_op, out + row, cv);
+        atomicOr(hasmul + (row >> 5), 1u << (row & 31));
+      }
     }
     __syncwarp();
   }
@@ -254,8 +339,8 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
     if (threadIdx.x == 0) {
       atomicAdd(counters + 0, s_cnt[0]);
       atomicAdd(counters + 1, s_cnt[1]);
-      // rows with a multiply so far (whole rows); split rows are added from
-      // `hasmul` by mv_pull_finish; adds = multiplies - rows
+      // rows with a multiply so far (whole rows); tile-crossing rows are
+      // added from `hasmul` by mv_pull_finish; adds = multiplies - rows
       atomicAdd(counters + 2, s_cnt[1] - s_cnt[2]);
     }
   }
