@@ -10,8 +10,10 @@
 // uint16; lane l then reads its 16 consecutive entries with four 16-byte
 // vector loads, finds the owner of its first entry with a 9-step search in
 // shared memory, and folds its entries row by row.  A row wholly inside one
-// lane's chunk is stored directly; partial rows are combined with an atomic
-// fold, so hub rows spread over as many warps as their length needs.
+// lane's chunk is stored directly; rows that cross lanes are combined by a
+// warp segmented scan and written once by the lane where they end; only rows
+// that cross a tile boundary use an atomic fold, so hub rows spread over as
+// many warps as their length needs at one atomic per 512 entries.
 //
 // tile_first[t] = compressed row containing entry t*kRowTile (lbs_tile_first
 // with S = nz_off).  Blocks must be 256 threads.
@@ -73,39 +75,76 @@ __device__ __forceinline__ void row_tiles(int64_t R_rows, const int32_t* __restr
 #pragma unroll
     for (int q = 0; q < kRowItems; ++q)
       vals[q] = my0 + q < e1 ? red.load(my0 + q, cols[q]) : red.identity();
+    // Fold row segment by row segment (rows are non-empty: one step reaches
+    // the next segment).  A segment closed inside the lane is a whole row
+    // (emitted with a plain store) unless it continues a row from the
+    // previous lane -- the lane's "head".  Open tail segments are combined
+    // across lanes by a warp segmented scan; the lane where a row ends emits
+    // it once, so only rows that cross a tile boundary use an atomic.
+    const bool head_out = nz_off[r0] < e0;
+    const bool tail_out = nz_off[r1 + 1] > e1;
+    const int rel0 = lane * kRowItems, rel1 = (int)(my1 - e0);
+    T acc = red.identity(), h_acc = red.identity();
+    int h_row = -1;  // tile row of the head segment (-1 none, -2 a lane inside one row)
+    int cur = -1;    // tile row of the open tail segment (-1 none)
     if (my0 < e1) {
-      const int rel0 = lane * kRowItems, rel1 = (int)(my1 - e0);
-      // owner of my first entry: last row whose start <= rel0
-      int lo = 0, hi = nr - 1;
+      int lo = 0, hi = nr - 1;  // owner of my first entry: last row whose start <= rel0
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (st[mid] <= rel0) lo = mid; else hi = mid - 1;
       }
-      int cur = lo;
-      int row_start = st[cur];
+      cur = lo;
       int next = st[cur + 1];
-      T acc = red.identity();
+      const bool cont = st[cur] < rel0 || (cur == 0 && head_out);
+      bool first = true;
 #pragma unroll
       for (int q = 0; q < kRowItems; ++q) {
         const int e = rel0 + q;
-        if (e < rel1) {
-          if (e >= next) {
-            red.emit(nz_rows[r0 + cur], acc, row_start >= rel0 && next <= rel1 &&
-                     (cur > 0 || nz_off[r0] >= e0));
-            acc = red.identity();
-            ++cur;
-            row_start = next;
-            next = st[cur + 1];
+        if (e < rel1 && e >= next) {
+          if (first && cont) {
+            h_acc = acc;
+            h_row = cur;
+          } else {
+            red.emit(nz_rows[r0 + cur], acc, true);
           }
-          acc = red.fold(acc, vals[q]);
+          first = false;
+          acc = red.identity();
+          ++cur;
+          next = st[cur + 1];
         }
+        if (e < rel1) acc = red.fold(acc, vals[q]);
       }
-      // the last row touched: whole only if it also ends inside my chunk
-      const bool whole = row_start >= rel0 && next <= rel1 && next < kRowTile + 1 &&
-                         (cur > 0 || nz_off[r0] >= e0) &&
-                         (cur < nr - 1 || nz_off[r1 + 1] <= e1);
-      red.emit(nz_rows[r0 + cur], acc, whole);
+      if (next <= rel1 && !(cur == nr - 1 && tail_out)) {
+        // the last segment ends with my chunk
+        if (first && cont) {
+          h_acc = acc;
+          h_row = cur;
+        } else {
+          red.emit(nz_rows[r0 + cur], acc, !(cur == 0 && head_out));
+        }
+        acc = red.identity();
+        cur = -1;
+      } else if (first && cont) {
+        h_row = -2;
+      }
     }
+    // segmented inclusive scan of the open tails (equal keys are adjacent lanes)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int k2 = __shfl_up_sync(GB_FULL, cur, o);
+      const T v2 = __shfl_up_sync(GB_FULL, acc, o);
+      if (lane >= o && cur >= 0 && k2 == cur) acc = red.fold(acc, v2);
+    }
+    const int pk = __shfl_up_sync(GB_FULL, cur, 1);
+    const T pv = __shfl_up_sync(GB_FULL, acc, 1);
+    if (h_row >= 0) {
+      const T v = lane > 0 && pk == h_row ? red.fold(h_acc, pv) : h_acc;
+      red.emit(nz_rows[r0 + h_row], v, !(h_row == 0 && head_out));
+    }
+    const int nk = __shfl_down_sync(GB_FULL, cur, 1);
+    const int nh = __shfl_down_sync(GB_FULL, h_row, 1);
+    if (cur >= 0 && !(lane < 31 && (nk == cur || nh == cur)))
+      red.emit(nz_rows[r0 + cur], acc, false);  // runs past the tile
     __syncwarp();
   }
 }
