@@ -426,6 +426,12 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                  int32_t* log_dir_host, int64_t* log_nvals_host, int64_t* log_est_host,
                  int64_t* iters_host);
 
+/* Engine of the fused bfs (no reference counterpart; a test / A-B knob):
+ * 0 = one CUDA graph with conditional nodes for the whole level loop
+ * (default), 1 = host-driven loop.  Negative values only query.  Returns the
+ * previous setting; process-wide. */
+int32_t gb_bfs_engine(int32_t engine);
+
 /* bfs (algorithms.py:48-77) over the degree-ordered relabelling of the
  * matrix (gb_csr_relabel_t): `push`/`pull`/`pull_nonempty` are the relabelled
  * orientations, rank[i] the new id of vertex i.  `source` and `levels` use

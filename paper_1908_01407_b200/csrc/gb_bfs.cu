@@ -283,17 +283,12 @@ __global__ void bfs_init(int64_t source, int64_t* levels, uint32_t* vbm, uint32_
 // Warp per 32 words (1024 vertices): lane l diffs word w0+l of the live
 // visited bitmap against the level-start snapshot, then the warp walks the
 // non-empty words so level stamps and frontier-list writes are coalesced.
-__global__ void __launch_bounds__(256)
-bfs_finalize(int64_t n, DevI64 depth_d, uint32_t* __restrict__ vbm,
-             uint32_t* __restrict__ vprev, uint32_t* __restrict__ fbm_next,
-             DevP64 levels_d, int32_t* __restrict__ F,
-             unsigned long long* __restrict__ count,
-             unsigned long long* __restrict__ count_clear, const uint32_t* __restrict__ xbm) {
+__device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t* vbm,
+                                              uint32_t* vprev, uint32_t* fbm_next,
+                                              int64_t* levels, int32_t* F,
+                                              unsigned long long* count, const uint32_t* xbm) {
   // xbm == NULL: new frontier = vbm & ~vprev (single GPU).  xbm != NULL: the
   // all-reduced new-frontier bitmap of a 1D-partitioned run is authoritative.
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
-  const int64_t depth = depth_d.get();
-  int64_t* __restrict__ levels = levels_d.get();
   const int lane = threadIdx.x & 31;
   const int64_t W = (n + 31) / 32;
   const int64_t G = (W + 31) / 32;
@@ -343,6 +338,16 @@ bfs_finalize(int64_t n, DevI64 depth_d, uint32_t* __restrict__ vbm,
   }
 }
 
+__global__ void __launch_bounds__(256)
+bfs_finalize(int64_t n, DevI64 depth_d, uint32_t* __restrict__ vbm,
+             uint32_t* __restrict__ vprev, uint32_t* __restrict__ fbm_next,
+             DevP64 levels_d, int32_t* __restrict__ F,
+             unsigned long long* __restrict__ count,
+             unsigned long long* __restrict__ count_clear, const uint32_t* __restrict__ xbm) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
+  finalize_body(n, depth_d.get(), vbm, vprev, fbm_next, levels_d.get(), F, count, xbm);
+}
+
 // ---------------------------------------------------------------------------
 // pull: warp per 32 words; candidate rows are compacted into a shared list
 // and processed 8 per lane with their first loads batched
@@ -351,21 +356,18 @@ constexpr int kPullBatch = 8;                // rows per lane per pass
 constexpr int kPullList = 32 * kPullBatch;   // rows per warp per pass
 constexpr int kPullSerial = 8;               // entries a lane scans alone before the warp helps
 
-__global__ void __launch_bounds__(256)
-bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
-         const int32_t* __restrict__ idx, EdgeOn on, const uint32_t* __restrict__ nonempty,
-         uint32_t* __restrict__ vbm, uint32_t* __restrict__ vprev, const uint32_t* __restrict__ fbm,
-         uint32_t* __restrict__ fbm_next, DevP64 levels_d,
-         int32_t* __restrict__ F, unsigned long long* __restrict__ count,
-         unsigned long long* __restrict__ count_clear, int64_t g_lo, int64_t g_hi) {
+// The frontier bitmap is probed through L1 (ld.global.ca).
+__device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_t* __restrict__ off,
+                                          const int32_t* __restrict__ idx, EdgeOn on,
+                                          const uint32_t* __restrict__ nonempty, uint32_t* vbm,
+                                          uint32_t* vprev, const uint32_t* fbm, uint32_t* fbm_next,
+                                          int64_t* levels, int32_t* F, unsigned long long* count,
+                                          int64_t g_lo, int64_t g_hi) {
   // [g_lo, g_hi): groups of 32 words (1024 vertices) this launch owns; a
   // 1D-partitioned rank passes its vertex block with `off`/`nonempty`
   // pointers rebased so global vertex ids index them directly.
   __shared__ int32_t s_list[8][kPullList];
   __shared__ uint32_t s_new[8][32];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
-  const int64_t depth = depth_d.get();
-  int64_t* __restrict__ levels = levels_d.get();
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int64_t W = (n + 31) / 32;
@@ -416,12 +418,12 @@ bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
       for (int r = 0; r < kPullBatch; ++r) {
         bool hit = false;
         if (lo[r] < hi[r]) {
-          hit = ((__ldg(fbm + (j0[r] >> 5)) >> (j0[r] & 31)) & 1u) && on(lo[r]);
+          hit = ((ld_probe(fbm + (j0[r] >> 5)) >> (j0[r] & 31)) & 1u) && on(lo[r]);
           int64_t p = lo[r] + 1;
           const int64_t stop = lo[r] + kPullSerial < hi[r] ? lo[r] + kPullSerial : hi[r];
           for (; !hit && p < stop; ++p) {
             const int32_t j = __ldg(idx + p);
-            hit = ((__ldg(fbm + (j >> 5)) >> (j & 31)) & 1u) && on(p);
+            hit = ((ld_probe(fbm + (j >> 5)) >> (j & 31)) & 1u) && on(p);
           }
           lo[r] = p;
           if (!hit && p < hi[r]) todo |= 1u << r;
@@ -446,7 +448,7 @@ bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
             bool mh = false;
             if (q < qhi) {
               const int32_t j = __ldg(idx + q);
-              mh = ((__ldg(fbm + (j >> 5)) >> (j & 31)) & 1u) && on(q);
+              mh = ((ld_probe(fbm + (j >> 5)) >> (j & 31)) & 1u) && on(q);
             }
             h = __ballot_sync(GB_FULL, mh) != 0;
           }
@@ -487,6 +489,18 @@ bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
     }
     __syncwarp();
   }
+}
+
+__global__ void __launch_bounds__(256)
+bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
+         const int32_t* __restrict__ idx, EdgeOn on, const uint32_t* __restrict__ nonempty,
+         uint32_t* __restrict__ vbm, uint32_t* __restrict__ vprev, const uint32_t* __restrict__ fbm,
+         uint32_t* __restrict__ fbm_next, DevP64 levels_d,
+         int32_t* __restrict__ F, unsigned long long* __restrict__ count,
+         unsigned long long* __restrict__ count_clear, int64_t g_lo, int64_t g_hi) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
+  pull_body(n, depth_d.get(), off, idx, on, nonempty, vbm, vprev, fbm, fbm_next, levels_d.get(), F,
+            count, g_lo, g_hi);
 }
 
 __global__ void bfs_unstamp(DevI64 Kd, const int32_t* __restrict__ F, int64_t* __restrict__ levels) {
@@ -571,19 +585,19 @@ constexpr int kGScanThreads = 256;
 constexpr int kGScanItems = 4;
 constexpr int64_t kGraphMaxCap = 1 << 20;  // longer loop caps use the host-driven path
 
+
 __device__ __forceinline__ void g_range(int64_t K, int64_t* lo, int64_t* hi) {
   const int64_t per = (K + gridDim.x - 1) / gridDim.x;
   *lo = blockIdx.x * per;
   *hi = *lo + per < K ? *lo + per : K;
 }
 
-__global__ void __launch_bounds__(kGScanThreads)
-g_scan_partials(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
-                const int64_t* __restrict__ off, int64_t* __restrict__ part) {
+__device__ __forceinline__ void scan_partials_body(int64_t K, const int32_t* F,
+                                                   const int64_t* __restrict__ off, int64_t* part) {
   using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
   __shared__ typename BlockReduce::TempStorage tmp;
   int64_t lo, hi;
-  g_range(*Kp, &lo, &hi);
+  g_range(K, &lo, &hi);
   int64_t sum = 0;
   for (int64_t k = lo + threadIdx.x; k < hi; k += kGScanThreads) {
     const int64_t v = F[k];
@@ -593,16 +607,21 @@ g_scan_partials(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
+__global__ void __launch_bounds__(kGScanThreads)
+g_scan_partials(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
+                const int64_t* __restrict__ off, int64_t* __restrict__ part) {
+  scan_partials_body(*Kp, F, off, part);
+}
+
 // rowstart[k] = off[F[k]], S = exclusive scan of the degrees, S[K] = E, and
 // tile_first[t] = the entry holding expansion slot t*kWarpTile.  Each block
 // derives its own carry-in from the partials (no separate top-level scan),
 // and every non-empty entry stamps the tiles that start inside its range, so
 // one launch replaces scan-top / scan-apply / tile-first.
-__global__ void __launch_bounds__(kGScanThreads)
-g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
-             const int64_t* __restrict__ off, const int64_t* __restrict__ part,
-             int64_t* __restrict__ rowstart, int64_t* __restrict__ S,
-             int32_t* __restrict__ tile_first, int64_t* __restrict__ tile_base) {
+__device__ __forceinline__ void scan_apply_body(int64_t K, const int32_t* F,
+                                                const int64_t* __restrict__ off, const int64_t* part,
+                                                int64_t* rowstart, int64_t* S, int32_t* tile_first,
+                                                int64_t* tile_base) {
   using BlockScan = cub::BlockScan<int64_t, kGScanThreads>;
   using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
   __shared__ union {
@@ -610,7 +629,6 @@ g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
     typename BlockReduce::TempStorage red;
   } tmp;
   __shared__ int64_t s_run;
-  const int64_t K = *Kp;
   int64_t lo, hi;
   g_range(K, &lo, &hi);
   {
@@ -642,17 +660,36 @@ g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
     int64_t pre, agg;
     BlockScan(tmp.scan).ExclusiveSum(sum, pre, agg);
     int64_t acc = run + pre;
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < kGScanItems; ++i) {
       const int64_t k = base + threadIdx.x * kGScanItems + i;
+      // tiles [t0, t1) start inside this entry's range; a few are stamped by
+      // the owning thread, long lists (a hub spans ~800 tiles) by its warp
+      int64_t t0 = 0, t1 = 0, b = 0;
       if (k < hi) {
         S[k] = acc;
         if (d[i] > 0) {
-          const int64_t b = rowstart[k] - acc;
-          for (int64_t t = (acc + kWarpTile - 1) / kWarpTile; t * kWarpTile < acc + d[i]; ++t) {
-            tile_first[t] = (int32_t)k;
-            tile_base[t] = b;
+          b = rowstart[k] - acc;
+          t0 = (acc + kWarpTile - 1) / kWarpTile;
+          t1 = (acc + d[i] + kWarpTile - 1) / kWarpTile;
+          if (t1 - t0 <= 4) {
+            for (int64_t t = t0; t < t1; ++t) {
+              tile_first[t] = (int32_t)k;
+              tile_base[t] = b;
+            }
           }
+        }
+      }
+      uint32_t big = __ballot_sync(GB_FULL, t1 - t0 > 4);
+      while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const int64_t u0 = __shfl_sync(GB_FULL, t0, src), u1 = __shfl_sync(GB_FULL, t1, src);
+        const int64_t ub = __shfl_sync(GB_FULL, b, src), uk = __shfl_sync(GB_FULL, k, src);
+        for (int64_t t = u0 + lane; t < u1; t += 32) {
+          tile_first[t] = (int32_t)uk;
+          tile_base[t] = ub;
         }
       }
       acc += d[i];
@@ -660,6 +697,14 @@ g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
     run += agg;
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(kGScanThreads)
+g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
+             const int64_t* __restrict__ off, const int64_t* __restrict__ part,
+             int64_t* __restrict__ rowstart, int64_t* __restrict__ S,
+             int32_t* __restrict__ tile_first, int64_t* __restrict__ tile_base) {
+  scan_apply_body(*Kp, F, off, part, rowstart, S, tile_first, tile_base);
 }
 
 __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
@@ -936,6 +981,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
 
 // Returns GB_OK after running the BFS, or GB_ERR_UNSUPPORTED when the graph
 // path cannot be used (the caller then runs the host-driven loop).
+
 static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                                const uint32_t* nonempty, const int32_t* rank, int64_t source, int64_t cap,
                                double ratio, int32_t policy, int64_t* levels, int32_t* log_dir,
@@ -962,7 +1008,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     const size_t o_vbm = take(4 * W), o_vprev = take(4 * W), o_f0 = take(4 * W), o_f1 = take(4 * W);
     const size_t o_F = take(4 * (size_t)n), o_tf = take(4 * (size_t)(push->nnz / kWarpTile + 2));
     const size_t o_tb = take(8 * (size_t)(push->nnz / kWarpTile + 2));
-    const size_t o_cnt = take(16), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
+    const size_t o_cnt = take(32), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
     const size_t o_lv = rank ? take(8 * (size_t)n) : 0;
     if (cudaMalloc(&G->mem, off) != cudaSuccess) {
@@ -994,6 +1040,16 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
       return set_error(ctx, GB_ERR_CUDA, "bfs graph build: %s", cudaGetErrorString(e));
     }
     *slot = G;
+  }
+  if (!G->exec) {
+    cudaStream_t cs[4];
+    for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    const cudaError_t e = bfs_graph_build(ctx, G, cs);
+    for (auto& x : cs) cudaStreamDestroy(x);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return set_error(ctx, GB_ERR_CUDA, "bfs graph build: %s", cudaGetErrorString(e));
+    }
   }
   cudaStream_t s = stream_of(ctx);
   Arena ar(ctx);
@@ -1063,17 +1119,32 @@ int32_t gb_decide_direction(int64_t nnz, int64_t nrows, int64_t nnz_u, double ra
 
 namespace gb {
 
+// A persistent cooperative kernel running every phase between grid barriers
+// was built and measured here (s24: 1.38 ms against 1.09 ms for the graph):
+// inside it the level-2 expansion took 0.84-0.90 ms instead of 0.55 ms -- the
+// kernel's register cap is the maximum over all phases (pull, scans) and its
+// static shared memory shrinks the L1 that holds the hot visited prefix.
+enum { kEngineGraph = 0, kEngineHost = 1 };
+static int g_bfs_engine = -1;  // -1: from the environment
+
+static int bfs_engine_current() {
+  if (g_bfs_engine < 0)
+    g_bfs_engine = getenv("GB_BFS_GRAPH") && atoi(getenv("GB_BFS_GRAPH")) == 0 ? kEngineHost
+                                                                               : kEngineGraph;
+  return g_bfs_engine;
+}
+
 static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                          const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
                          int64_t max_iters, double ratio, int32_t policy, int64_t* levels_out,
                          int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   const int64_t n = push->nrows;
   if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
-  // device-driven loop (one graph launch) unless profiling per kernel, the
+  // Device-driven loop (one graph launch) unless profiling per kernel, the
   // pull orientation is missing (the host loop reports that error when pull
-  // is chosen), or GB_BFS_GRAPH=0 asks for the host-driven loop
-  static const bool graph_off = getenv("GB_BFS_GRAPH") && atoi(getenv("GB_BFS_GRAPH")) == 0;
-  if (pull && !graph_off && !prof_enabled(ctx) && max_iters >= 1 && max_iters <= kGraphMaxCap) {
+  // is chosen), or the engine is pinned (gb_bfs_engine; GB_BFS_GRAPH=0).
+  if (pull && bfs_engine_current() == kEngineGraph && !prof_enabled(ctx) && max_iters >= 1 &&
+      max_iters <= kGraphMaxCap) {
     const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, source, max_iters,
                                        ratio, policy, levels_out, log_dir, log_nvals, log_est,
                                        iters_out);
@@ -1177,6 +1248,12 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
 }  // namespace gb
 
 extern "C" {
+
+int32_t gb_bfs_engine(int32_t engine) {
+  const int32_t prev = bfs_engine_current();
+  if (engine >= kEngineGraph && engine <= kEngineHost) g_bfs_engine = engine;
+  return prev;
+}
 
 gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                  const uint32_t* pull_nonempty, int64_t source, int64_t max_iters,

@@ -115,10 +115,9 @@ constexpr int kWarpItems = 16;
 constexpr int kWarpTile = 32 * kWarpItems;  // 512 slots
 
 template <class F>
-__device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* __restrict__ S,
-                                           const int64_t* __restrict__ rowstart,
-                                           const int32_t* __restrict__ tile_first,
-                                           const int64_t* __restrict__ tile_base, F& f) {
+__device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* S, const int64_t* rowstart,
+                                           const int32_t* tile_first, const int64_t* tile_base,
+                                           F& f) {
   const int lane = threadIdx.x & 31;
   const int64_t E = S[K];
   const int64_t ntiles = (E + kWarpTile - 1) / kWarpTile;

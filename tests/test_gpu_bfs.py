@@ -333,3 +333,59 @@ def test_bfs_ordered_smem_prefix_large_frontier(gb, monkeypatch):
             if want is not None:
                 assert np.array_equal(lv, want)
             _bfs_both_layouts(gb, A, src, monkeypatch, **kw)
+
+
+# ---------------------------------------------------------------------------
+# engines: the CUDA graph (default) vs the host-driven loop, both layouts
+# ---------------------------------------------------------------------------
+
+
+def _engines(gb, A, src, **kw):
+    from paper_1908_01407_b200 import _lib
+    lib = _lib.load()
+    out = []
+    prev = lib.gb_bfs_engine(-1)
+    try:
+        for eng in (0, 1):
+            lib.gb_bfs_engine(eng)
+            d = gb.Descriptor(**kw)
+            lv = gb.bfs(A, src, desc=d).values
+            out.append((lv, [(x.chosen, x.frontier_nvals, x.estimated_frontier_edges)
+                             for x in d.direction_log]))
+    finally:
+        lib.gb_bfs_engine(prev)
+    return out
+
+
+@pytest.mark.parametrize("s", [6, 12, 18, 22])
+def test_bfs_engines_agree(gb, s, monkeypatch):
+    from paper_1908_01407_b200 import algorithms
+    A = gb.io.rmat_matrix(s)
+    for ordered in (True, False):
+        monkeypatch.setattr(algorithms, "_ORDERED_BFS", ordered)
+        for src in (0, 7, A.nrows - 1):
+            for kw in ({}, {"max_niter": 1}, {"max_niter": 3}, {"direction": gb.Direction.FORCE_PUSH},
+                       {"direction": gb.Direction.FORCE_PULL}, {"switch_ratio": 0.0}):
+                (g, tg), (h, th) = _engines(gb, A, src, **kw)
+                assert np.array_equal(g, h), (ordered, src, kw)
+                assert tg == th, (ordered, src, kw)
+
+
+def test_bfs_engines_long_path_and_values(gb):
+    n = 300
+    r = np.r_[np.arange(n - 1), np.arange(1, n)]
+    c = np.r_[np.arange(1, n), np.arange(n - 1)]
+    A = gb.SparseMatrix.from_tuples(r, c, np.ones(r.size, np.int64), n, n)
+    for kw in ({}, {"max_niter": 21}, {"max_niter": 150}):
+        (g, tg), (h, th) = _engines(gb, A, 0, **kw)
+        assert np.array_equal(g, h) and tg == th
+    # stored zeros are not edges; a directed graph uses both orientations
+    rng = np.random.default_rng(3)
+    n = 3000
+    r = rng.integers(0, n, 40000)
+    c = (r + rng.integers(1, 50, 40000)) % n
+    v = rng.integers(0, 3, 40000)
+    A = gb.SparseMatrix.from_tuples(r, c, v, n, n)
+    for kw in ({}, {"direction": gb.Direction.FORCE_PULL}):
+        (g, tg), (h, th) = _engines(gb, A, 5, **kw)
+        assert np.array_equal(g, h) and tg == th
