@@ -74,7 +74,8 @@ def main():
     args = ap.parse_args()
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    old = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    traffic = {}  # kernels captured now replace their old entries
     lines = [f"# ncu --set full summaries ({args.tag}) {args.title}", "",
              "Per launch; `ncu --set full --clock-control none` (serialised, cold caches).", ""]
     for rep in args.rep:
@@ -135,6 +136,8 @@ def main():
         out.append("")
     with open(os.path.join(ROOT, "profiles", f"{args.tag}_launches.md"), "w") as fh:
         fh.write("\n".join(out) + "\n")
+    for k, v in old.items():
+        traffic.setdefault(k, v)
     with open(traffic_path, "w") as fh:
         json.dump(traffic, fh, indent=1, sort_keys=True)
 
