@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--source", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmv", action="store_true", help="skip the masked SpMV measurement")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config sweep (BASELINE configs C1-C5, GPU vs C oracle)")
     ap.add_argument("--cpu-cap-s", type=float, default=120.0,
                     help="wall-clock cap for CPU timing legs")
     return ap.parse_args()
@@ -195,6 +197,118 @@ def masked_spmv(gb, A, ctx, peak, peak_src, reps=10, density=0.5):
             "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4), "allowed_rows": R,
             "entries_read": int(e_read), "multiplies": int(d.counters.semiring_multiplies),
             "max_rel_err_vs_torch": rel, "tolerance": 1e-12, "parity": rel <= 1e-12}
+
+
+# ---------------------------------------------------------------------------
+# every BASELINE.json config: device time, parity against the C oracle on the
+# same CSR, and the C port timed on the host (the reported CPU baseline)
+# ---------------------------------------------------------------------------
+
+
+def _dev_ms(fn, reps):
+    import torch
+    r = fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        r = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, r
+
+
+def _cpu_s(fn):
+    t = time.perf_counter()
+    r = fn()
+    return time.perf_counter() - t, r
+
+
+def config_sweep(gb, scales=(16, 20, 22, 24, 26)):
+    """BASELINE.json configs C1-C5: one JSON object per config."""
+    import torch
+    from oracle import cgraph
+    from paper_1908_01407_b200.io import rmat_matrix
+    cgraph.lib()
+    out = {"cpu_threads": cgraph.threads(), "cpu_kind": "port (oracle/cgraph.c, OpenMP)"}
+
+    def host(A):
+        return A._csr.offsets.cpu().numpy(), A._csr.indices.cpu().numpy()
+
+    def cleanup():
+        gb._lib.context().trim()
+        torch.cuda.empty_cache()
+
+    # C1: BFS from 0 on s16
+    if 16 in scales:
+        A = rmat_matrix(16)
+        ms, lv = _dev_ms(lambda: gb.bfs(A, 0), 20)
+        rp, ci = host(A)
+        cs, (want, _tr) = _cpu_s(lambda: cgraph.bfs(rp, ci, 0))
+        out["C1_bfs_s16"] = {"gpu_ms": round(ms, 4), "cpu_ms": round(cs * 1e3, 3), "nnz": A.nnz,
+                             "gteps": round(A.nnz / ms / 1e6, 2),
+                             "parity": bool(np.array_equal(lv.values, want))}
+        A = None
+        cleanup()
+    # C2: SSSP (min-plus) on s20 with the reference integer weights as f64
+    if 20 in scales:
+        W = rmat_matrix(20, weighted=True)
+        ms, dist = _dev_ms(lambda: gb.sssp(W, 0), 5)
+        rp, ci = host(W)
+        w = W._csr.dense_values().cpu().numpy()
+        cs, (want, _tr) = _cpu_s(lambda: cgraph.sssp(rp, ci, w, 0))
+        got = dist.values
+        fin = np.isfinite(want)
+        rel = float(np.max(np.abs(got[fin] - want[fin]) / np.maximum(np.abs(want[fin]), 1e-300)))
+        out["C2_sssp_s20"] = {"gpu_ms": round(ms, 3), "cpu_ms": round(cs * 1e3, 1),
+                              "max_rel_err": rel, "tolerance": 1e-5,
+                              "parity": bool(rel <= 1e-5 and np.array_equal(np.isinf(got), ~fin))}
+        W = None
+        cleanup()
+        # C4: triangle counting via masked SpGEMM on s20 (golden 424,532,724)
+        A = rmat_matrix(20)
+        ms, cnt = _dev_ms(lambda: gb.triangle_count(A), 3)
+        rp, ci = host(A)
+        cs, want = _cpu_s(lambda: cgraph.tc(rp, ci))
+        out["C4_tc_s20"] = {"gpu_ms": round(ms, 3), "cpu_ms": round(cs * 1e3, 1), "triangles": int(cnt),
+                            "parity": bool(int(cnt) == want == 424_532_724)}
+        A = None
+        cleanup()
+    # C3: PageRank 20 iterations (plus-times, dense pull) on s22
+    if 22 in scales:
+        A = rmat_matrix(22)
+        ms, pr = _dev_ms(lambda: gb.pagerank(A, eps=1e-300, max_iters=20), 3)
+        rp, ci = host(A)
+        cs, (want, _e) = _cpu_s(lambda: cgraph.pagerank(rp, ci, eps=1e-300, max_iters=20))
+        l1 = float(np.abs(pr.values - want).sum())
+        out["C3_pagerank20_s22"] = {"gpu_ms": round(ms, 3), "cpu_ms": round(cs * 1e3, 1),
+                                    "l1_vs_oracle": l1, "tolerance": 1e-6, "parity": bool(l1 <= 1e-6)}
+        A = None
+        cleanup()
+    # C5: BFS + connected components on s24 and s26 (one GPU)
+    for sc in (24, 26):
+        if sc not in scales:
+            continue
+        try:
+            A = rmat_matrix(sc)
+            bms, lv = _dev_ms(lambda: gb.bfs(A, 0), 5)
+            cms, lab = _dev_ms(lambda: gb.connected_components(A), 2)
+            rp, ci = host(A)
+            bcs, (want, _tr) = _cpu_s(lambda: cgraph.bfs(rp, ci, 0))
+            ccs, (wlab, _t2) = _cpu_s(lambda: cgraph.cc(rp, ci))
+            out[f"C5_bfs_cc_s{sc}"] = {
+                "n": A.nrows, "nnz": A.nnz, "bfs_gpu_ms": round(bms, 3),
+                "bfs_gteps": round(A.nnz / bms / 1e6, 1), "bfs_cpu_ms": round(bcs * 1e3, 1),
+                "cc_gpu_ms": round(cms, 3), "cc_cpu_ms": round(ccs * 1e3, 1),
+                "parity": bool(np.array_equal(lv.values, want) and np.array_equal(lab.values, wlab))}
+            del rp, ci, want, wlab, lv, lab
+            A = None
+            cleanup()
+        except Exception as e:  # noqa: BLE001 -- report, never lose the bench line
+            out[f"C5_bfs_cc_s{sc}"] = {"error": f"{type(e).__name__}: {e}"[:200]}
+            gb._lib.context().trim()
+            torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -359,6 +473,13 @@ def run_ours(args):
                          f"oracle/cgraph.c og_bfs with {threads} OpenMP threads, mean of {len(times)} runs",
                "ms_per_bfs": round(cpu_s * 1e3, 2), "cpu": platform.processor() or platform.machine()}
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        del A
+        ctx.trim()
+        torch.cuda.empty_cache()
+        configs = config_sweep(gb)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
@@ -382,6 +503,7 @@ def run_ours(args):
             "masked_spmv": mspmv,
             "cpu_baseline": cpu,
             "parity_vs_oracle": parity,
+            "configs": configs,
         }
         print(json.dumps(line))
     if world > 1:
