@@ -115,6 +115,16 @@ bfs_expand_warp(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restr
                 EdgeOn on, uint32_t* __restrict__ vbm) {
   const int64_t K = Kd.get();
   PushBits<VALS> f{idx, on, vbm};
+  if (K > 0 && S[K] < 4 * K) {
+    // short lists (s24 level 4: 844 K entries, 1.04 M edges): one thread per
+    // frontier entry beats 512-slot tiles that each hold hundreds of entries
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t p0 = rowstart[k], d = S[k + 1] - S[k];
+      for (int64_t j = 0; j < d; ++j) f.visit(p0 + j);
+    }
+    return;
+  }
   warp_tiles(K, S, rowstart, tile_first, tile_base, f);
 }
 
