@@ -61,11 +61,12 @@ struct PushBits {
   const int32_t* __restrict__ idx;
   EdgeOn on;
   uint32_t* __restrict__ vbm;
+  int32_t xs = 0;  // vertices below xs are known visited: no probe (dense visited prefix)
   template <int B>
   __device__ __forceinline__ void probe_mark(const int32_t (&v)[B]) {
     uint32_t word[B];
 #pragma unroll
-    for (int r = 0; r < B; ++r) word[r] = v[r] >= 0 ? ld_probe(vbm + (v[r] >> 5)) : ~0u;
+    for (int r = 0; r < B; ++r) word[r] = v[r] >= xs && v[r] >= 0 ? ld_probe(vbm + (v[r] >> 5)) : ~0u;
 #pragma unroll
     for (int r = 0; r < B; ++r) mark(vbm, v[r] >= 0 ? v[r] : 0, word[r]);  // dead: word = ~0
   }
@@ -112,9 +113,9 @@ __global__ void __launch_bounds__(256, MINB)
 bfs_expand_warp(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restrict__ rowstart,
                 const int32_t* __restrict__ tile_first, const int64_t* __restrict__ tile_base,
                 const int32_t* __restrict__ idx,
-                EdgeOn on, uint32_t* __restrict__ vbm) {
+                EdgeOn on, uint32_t* __restrict__ vbm, DevI64 Xd) {
   const int64_t K = Kd.get();
-  PushBits<VALS> f{idx, on, vbm};
+  PushBits<VALS> f{idx, on, vbm, (int32_t)Xd.get()};
   if (K > 0 && S[K] < 4 * K) {
     // short lists (s24 level 4: 844 K entries, 1.04 M edges): one thread per
     // frontier entry beats 512-slot tiles that each hold hundreds of entries
@@ -129,7 +130,16 @@ bfs_expand_warp(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restr
 }
 
 using ExpandKernel = void (*)(DevI64, const int64_t*, const int64_t*, const int32_t*,
-                              const int64_t*, const int32_t*, EdgeOn, uint32_t*);
+                              const int64_t*, const int32_t*, EdgeOn, uint32_t*, DevI64);
+
+// How an ordered BFS uses the dense visited prefix X (every vertex below X is
+// visited): 1 = cut each sorted list at X in the degree scan (fewer index
+// loads, one lower-bound search per frontier entry), 2 = expand the whole
+// list but do not probe targets below X, 0 = ignore it.  GB_PREFIX_MODE.
+static int prefix_mode() {
+  static const int m = getenv("GB_PREFIX_MODE") ? atoi(getenv("GB_PREFIX_MODE")) : 1;
+  return m;
+}
 
 // Register budget of the push (GB_PUSH_MINB = minimum resident CTAs of 256
 // threads per SM: 1 leaves the allocation to ptxas, 3 allows 80, 4 caps at 64,
@@ -293,20 +303,40 @@ __global__ void bfs_init(int64_t source, int64_t* levels, uint32_t* vbm, uint32_
 // Warp per 32 words (1024 vertices): lane l diffs word w0+l of the live
 // visited bitmap against the level-start snapshot, then the warp walks the
 // non-empty words so level stamps and frontier-list writes are coalesced.
+// Dense visited prefix: xmin (when given) receives, via one atomicMin per
+// block, 32 x the index of the first visited-bitmap word that is not full
+// after this level -- every vertex below it is visited.  wmin is the calling
+// warp's candidate (groups are walked in increasing order per warp).
+__device__ __forceinline__ void prefix_note(int64_t* wmin, int64_t g, uint32_t visited_after,
+                                            bool valid) {
+  const uint32_t nf = __ballot_sync(GB_FULL, valid && visited_after != ~0u);
+  if (nf && *wmin == INT64_MAX) *wmin = (g * 32 + __ffs(nf) - 1) * 32;
+}
+__device__ __forceinline__ void prefix_flush(int64_t wmin, unsigned long long* xmin) {
+  __shared__ unsigned long long s_min;
+  if (threadIdx.x == 0) s_min = ~0ull;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && wmin != INT64_MAX) atomicMin(&s_min, (unsigned long long)wmin);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_min != ~0ull) atomicMin(xmin, s_min);
+}
+
 __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t* vbm,
                                               uint32_t* vprev, uint32_t* fbm_next,
                                               int64_t* levels, int32_t* F,
-                                              unsigned long long* count, const uint32_t* xbm) {
+                                              unsigned long long* count, const uint32_t* xbm,
+                                              unsigned long long* xmin = nullptr) {
   // xbm == NULL: new frontier = vbm & ~vprev (single GPU).  xbm != NULL: the
   // all-reduced new-frontier bitmap of a 1D-partitioned run is authoritative.
   const int lane = threadIdx.x & 31;
+  int64_t wmin = INT64_MAX;
   const int64_t W = (n + 31) / 32;
   const int64_t G = (W + 31) / 32;
   const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = g0; g < G; g += ng) {
     const int64_t w = g * 32 + lane;
-    uint32_t bits = 0;
+    uint32_t bits = 0, visited = ~0u;
     if (w < W) {
       if (xbm) {
         bits = xbm[w];
@@ -318,9 +348,11 @@ __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t
         const uint32_t cur = vbm[w], old = vprev[w];
         bits = cur & ~old;
         if (bits) vprev[w] = cur;
+        visited = cur;
       }
       fbm_next[w] = bits;
     }
+    if (xmin) prefix_note(&wmin, g, visited, w < W);
     // frontier list slots for the whole group, in word order
     const int c = __popc(bits);
     int incl = c;
@@ -346,6 +378,7 @@ __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t
       }
     }
   }
+  if (xmin) prefix_flush(wmin, xmin);
 }
 
 __global__ void __launch_bounds__(256)
@@ -353,9 +386,10 @@ bfs_finalize(int64_t n, DevI64 depth_d, uint32_t* __restrict__ vbm,
              uint32_t* __restrict__ vprev, uint32_t* __restrict__ fbm_next,
              DevP64 levels_d, int32_t* __restrict__ F,
              unsigned long long* __restrict__ count,
-             unsigned long long* __restrict__ count_clear, const uint32_t* __restrict__ xbm) {
+             unsigned long long* __restrict__ count_clear, const uint32_t* __restrict__ xbm,
+             unsigned long long* __restrict__ xmin) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
-  finalize_body(n, depth_d.get(), vbm, vprev, fbm_next, levels_d.get(), F, count, xbm);
+  finalize_body(n, depth_d.get(), vbm, vprev, fbm_next, levels_d.get(), F, count, xbm, xmin);
 }
 
 // ---------------------------------------------------------------------------
@@ -372,7 +406,8 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
                                           const uint32_t* __restrict__ nonempty, uint32_t* vbm,
                                           uint32_t* vprev, const uint32_t* fbm, uint32_t* fbm_next,
                                           int64_t* levels, int32_t* F, unsigned long long* count,
-                                          int64_t g_lo, int64_t g_hi) {
+                                          int64_t g_lo, int64_t g_hi,
+                                          unsigned long long* xmin = nullptr) {
   // [g_lo, g_hi): groups of 32 words (1024 vertices) this launch owns; a
   // 1D-partitioned rank passes its vertex block with `off`/`nonempty`
   // pointers rebased so global vertex ids index them directly.
@@ -385,9 +420,11 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int32_t* list = s_list[wid];
   uint32_t* nw = s_new[wid];
+  int64_t wmin = INT64_MAX;
   for (int64_t g = g_lo + g0; g < g_hi; g += ng) {
     const int64_t w = g * 32 + lane;
-    uint32_t rem = w < W ? (~vbm[w] & __ldg(nonempty + w)) : 0u;
+    const uint32_t vb0 = w < W ? vbm[w] : ~0u;
+    uint32_t rem = w < W ? (~vb0 & __ldg(nonempty + w)) : 0u;
     nw[lane] = 0;
     __syncwarp();
     while (true) {
@@ -479,6 +516,7 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
         vprev[w] |= bits;
       }
     }
+    if (xmin) prefix_note(&wmin, g, vb0 | bits, w < W);
     const int c = __popc(bits);
     int incl = c;
 #pragma unroll
@@ -499,6 +537,7 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
     }
     __syncwarp();
   }
+  if (xmin) prefix_flush(wmin, xmin);
 }
 
 __global__ void __launch_bounds__(256)
@@ -507,10 +546,11 @@ bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
          uint32_t* __restrict__ vbm, uint32_t* __restrict__ vprev, const uint32_t* __restrict__ fbm,
          uint32_t* __restrict__ fbm_next, DevP64 levels_d,
          int32_t* __restrict__ F, unsigned long long* __restrict__ count,
-         unsigned long long* __restrict__ count_clear, int64_t g_lo, int64_t g_hi) {
+         unsigned long long* __restrict__ count_clear, int64_t g_lo, int64_t g_hi,
+         unsigned long long* __restrict__ xmin) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_clear = 0;
   pull_body(n, depth_d.get(), off, idx, on, nonempty, vbm, vprev, fbm, fbm_next, levels_d.get(), F,
-            count, g_lo, g_hi);
+            count, g_lo, g_hi, xmin);
 }
 
 __global__ void bfs_unstamp(DevI64 Kd, const int32_t* __restrict__ F, int64_t* __restrict__ levels) {
@@ -524,18 +564,19 @@ __global__ void bfs_unstamp(DevI64 Kd, const int32_t* __restrict__ F, int64_t* _
 // bank conflicts and halved occupancy cost more than the saved L1 sectors.)
 template <bool VALS>
 static gb_status launch_push_t(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
-                               EdgeOn on, uint32_t* vbm) {
+                               EdgeOn on, uint32_t* vbm, int64_t xskip) {
   const ExpandKernel k = expand_kernel<VALS>();
   k<<<resident_grid(ctx, k, 256), 256, 0, stream_of(ctx)>>>(
-      dval(K), plan.S, plan.rowstart, plan.tile_first, plan.tile_base, a->indices, on, vbm);
+      dval(K), plan.S, plan.rowstart, plan.tile_first, plan.tile_base, a->indices, on, vbm,
+      dval(xskip));
   GB_LAUNCH_CHECK(ctx);
   return GB_OK;
 }
 
 static gb_status launch_push(gb_ctx* ctx, int64_t K, const LbsPlan& plan, const gb_csr* a,
-                             EdgeOn on, uint32_t* vbm) {
-  return a->values ? launch_push_t<true>(ctx, K, plan, a, on, vbm)
-                   : launch_push_t<false>(ctx, K, plan, a, on, vbm);
+                             EdgeOn on, uint32_t* vbm, int64_t xskip = 0) {
+  return a->values ? launch_push_t<true>(ctx, K, plan, a, on, vbm, xskip)
+                   : launch_push_t<false>(ctx, K, plan, a, on, vbm, xskip);
 }
 
 template <bool VALS>
@@ -588,9 +629,11 @@ struct BfsState {
   int32_t policy, pad_;
   int64_t* out;         // per call, relabelled graphs: levels by original id
   int64_t it, K, depth, dnext, unstamp;  // loop state
+  int64_t xcur;                 // dense visited prefix at the level start (ordered graphs)
+  unsigned long long xnext;     // ... after the level (atomicMin target)
 };
 
-constexpr int kGScanBlocks = 592;  // partial sums; each apply block folds its predecessors
+constexpr int kGScanBlocks = 2368;  // 16 per SM (the lower-bound searches want threads); each apply block folds its predecessors
 constexpr int kGScanThreads = 256;
 constexpr int kGScanItems = 4;
 constexpr int64_t kGraphMaxCap = 1 << 20;  // longer loop caps use the host-driven path
@@ -602,8 +645,17 @@ __device__ __forceinline__ void g_range(int64_t K, int64_t* lo, int64_t* hi) {
   *hi = *lo + per < K ? *lo + per : K;
 }
 
+// Per frontier entry k: the part of its (sorted) adjacency list the push must
+// expand -- rowstart[k] and its length (kept in S[k] until the apply pass
+// turns S into the exclusive scan) -- and the block's partial sum.  With
+// X > 0 every vertex below X is already visited (the dense visited prefix of
+// a degree-ordered graph: s24 level 2 has X = 13,043, and 24 % of the level's
+// edges point below it), so the neighbours below X are skipped: they could
+// only probe set bits.  A lower-bound search in the sorted row finds the cut.
 __device__ __forceinline__ void scan_partials_body(int64_t K, const int32_t* F,
-                                                   const int64_t* __restrict__ off, int64_t* part) {
+                                                   const int64_t* __restrict__ off,
+                                                   const int32_t* __restrict__ idx, int64_t X,
+                                                   int64_t* rowstart, int64_t* deg, int64_t* part) {
   using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
   __shared__ typename BlockReduce::TempStorage tmp;
   int64_t lo, hi;
@@ -611,16 +663,33 @@ __device__ __forceinline__ void scan_partials_body(int64_t K, const int32_t* F,
   int64_t sum = 0;
   for (int64_t k = lo + threadIdx.x; k < hi; k += kGScanThreads) {
     const int64_t v = F[k];
-    sum += __ldg(off + v + 1) - __ldg(off + v);
+    int64_t a = __ldg(off + v);
+    const int64_t b = __ldg(off + v + 1);
+    if (X > 0 && a < b && __ldg(idx + a) < X) {
+      if (__ldg(idx + b - 1) < X) {
+        a = b;
+      } else {  // first position in (a, b-1] holding a column >= X
+        int64_t l = a + 1, h = b - 1;
+        while (l < h) {
+          const int64_t m = (l + h) >> 1;
+          if (__ldg(idx + m) < X) l = m + 1; else h = m;
+        }
+        a = l;
+      }
+    }
+    rowstart[k] = a;
+    deg[k] = b - a;
+    sum += b - a;
   }
   const int64_t tot = BlockReduce(tmp).Sum(sum);
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
 __global__ void __launch_bounds__(kGScanThreads)
-g_scan_partials(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
-                const int64_t* __restrict__ off, int64_t* __restrict__ part) {
-  scan_partials_body(*Kp, F, off, part);
+g_scan_partials(DevI64 Kd, const int32_t* __restrict__ F, const int64_t* __restrict__ off,
+                const int32_t* __restrict__ idx, DevI64 Xd, int64_t* __restrict__ rowstart,
+                int64_t* __restrict__ deg, int64_t* __restrict__ part) {
+  scan_partials_body(Kd.get(), F, off, idx, Xd.get(), rowstart, deg, part);
 }
 
 // rowstart[k] = off[F[k]], S = exclusive scan of the degrees, S[K] = E, and
@@ -628,10 +697,9 @@ g_scan_partials(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
 // derives its own carry-in from the partials (no separate top-level scan),
 // and every non-empty entry stamps the tiles that start inside its range, so
 // one launch replaces scan-top / scan-apply / tile-first.
-__device__ __forceinline__ void scan_apply_body(int64_t K, const int32_t* F,
-                                                const int64_t* __restrict__ off, const int64_t* part,
-                                                int64_t* rowstart, int64_t* S, int32_t* tile_first,
-                                                int64_t* tile_base) {
+// rowstart[k] and the lengths (in S[k]) come from scan_partials_body.
+__device__ __forceinline__ void scan_apply_body(int64_t K, const int64_t* part, const int64_t* rowstart,
+                                                int64_t* S, int32_t* tile_first, int64_t* tile_base) {
   using BlockScan = cub::BlockScan<int64_t, kGScanThreads>;
   using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
   __shared__ union {
@@ -658,13 +726,7 @@ __device__ __forceinline__ void scan_apply_body(int64_t K, const int32_t* F,
 #pragma unroll
     for (int i = 0; i < kGScanItems; ++i) {
       const int64_t k = base + threadIdx.x * kGScanItems + i;
-      d[i] = 0;
-      if (k < hi) {
-        const int64_t v = F[k];
-        const int64_t a = __ldg(off + v);
-        d[i] = __ldg(off + v + 1) - a;
-        rowstart[k] = a;
-      }
+      d[i] = k < hi ? S[k] : 0;
       sum += d[i];
     }
     int64_t pre, agg;
@@ -710,11 +772,10 @@ __device__ __forceinline__ void scan_apply_body(int64_t K, const int32_t* F,
 }
 
 __global__ void __launch_bounds__(kGScanThreads)
-g_scan_apply(const int64_t* __restrict__ Kp, const int32_t* __restrict__ F,
-             const int64_t* __restrict__ off, const int64_t* __restrict__ part,
-             int64_t* __restrict__ rowstart, int64_t* __restrict__ S,
-             int32_t* __restrict__ tile_first, int64_t* __restrict__ tile_base) {
-  scan_apply_body(*Kp, F, off, part, rowstart, S, tile_first, tile_base);
+g_scan_apply(DevI64 Kd, const int64_t* __restrict__ part, const int64_t* __restrict__ rowstart,
+             int64_t* __restrict__ S, int32_t* __restrict__ tile_first,
+             int64_t* __restrict__ tile_base) {
+  scan_apply_body(Kd.get(), part, rowstart, S, tile_first, tile_base);
 }
 
 __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
@@ -736,6 +797,7 @@ __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32
   st->it = 0;
   st->K = 1;
   st->depth = 1;
+  st->xcur = 0;
   st->unstamp = 0;
   st->log[0] = 0;
   cudaGraphSetConditional(h_loop, st->cap > 0 ? 1u : 0u);
@@ -755,14 +817,16 @@ __global__ void g_decide(BfsState* st, int64_t nnz, int64_t nrows, unsigned long
   e[1] = K;
   e[2] = est;
   st->dnext = st->depth + 1;
+  st->xnext = ~0ull;
   *c = 0;
   cudaGraphSetConditional(h_push, dir == GB_DIR_PUSH ? 1u : 0u);
 }
 
 // after a level: new frontier size, loop continuation, cap handling
-__global__ void g_advance(BfsState* st, const unsigned long long* c,
+__global__ void g_advance(BfsState* st, const unsigned long long* c, int64_t n,
                           cudaGraphConditionalHandle h_a, cudaGraphConditionalHandle h_b) {
   const int64_t K = (int64_t)*c;
+  st->xcur = st->xnext < (unsigned long long)n ? (int64_t)st->xnext : n;
   const int64_t it = st->it;
   st->log[0] = it + 1;
   st->K = K;
@@ -854,10 +918,13 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   G->launches_fixed = 8;  // 4 memsets, zero (or unpermute), start, unstamp (+2 per level below)
 
   auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
-    g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part);
-    g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(&st->K, G->F, push.offsets, G->part,
-                                                        G->rowstart, G->S, G->tile_first,
-                                                        G->tile_base);
+    // ordered (sorted-row) graphs skip the dense visited prefix of each list
+    g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(
+        dptr(&st->K), G->F, push.offsets, push.indices,
+        ordered && prefix_mode() == 1 ? dptr(&st->xcur) : dval(0),
+        G->rowstart, G->S, G->part);
+    g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(dptr(&st->K), G->part, G->rowstart, G->S,
+                                                        G->tile_first, G->tile_base);
     if (!push_dead && use_smem) {
       if (push.values)
         bfs_expand_smem<true><<<grid_smem, kSmemPushThreads, smem, s>>>(
@@ -867,11 +934,12 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
             dptr(&st->K), G->S, G->rowstart, G->tile_first, G->tile_base, push.indices, push_on, G->vbm, G->vprev, W);
     } else if (!push_dead) {
       expand<<<grid_expand, 256, 0, s>>>(dptr(&st->K), G->S, G->rowstart, G->tile_first,
-                                         G->tile_base, push.indices, push_on, G->vbm);
+                                         G->tile_base, push.indices, push_on, G->vbm,
+                                         ordered && prefix_mode() == 2 ? dptr(&st->xcur) : dval(0));
     }
     bfs_finalize<<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev, G->fbm[h ^ 1],
                                         pptr(&st->levels), G->F, G->cnt + h, G->cnt + (h ^ 1),
-                                        nullptr);
+                                        nullptr, ordered ? &st->xnext : nullptr);
     return cudaGetLastError();
   };
   auto pull_body = [&](int h, cudaStream_t s) -> cudaError_t {
@@ -883,7 +951,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       bfs_pull<<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices, pull_on,
                                       G->nonempty, G->vbm, G->vprev, G->fbm[h], G->fbm[h ^ 1],
                                       pptr(&st->levels), G->F, G->cnt + h, G->cnt + (h ^ 1), 0,
-                                      (W + 31) / 32);
+                                      (W + 31) / 32, ordered ? &st->xnext : nullptr);
     }
     return cudaGetLastError();
   };
@@ -916,7 +984,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     }
     GB_GTRY(capture_into(br[0], s_inner, [&] { return push_body(h, s_inner); }));
     GB_GTRY(capture_into(br[1], s_inner, [&] { return pull_body(h, s_inner); }));
-    g_advance<<<1, 1, 0, s>>>(st, G->cnt + h, h_a, h_b);
+    g_advance<<<1, 1, 0, s>>>(st, G->cnt + h, n, h_a, h_b);
     return cudaGetLastError();
   };
 
@@ -1176,14 +1244,28 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
   uint32_t* fbm[2] = {ar.alloc<uint32_t>(W), ar.alloc<uint32_t>(W)};
   int32_t* F = ar.alloc<int32_t>(n);
   uint32_t* vprev = ar.alloc<uint32_t>(W);
-  unsigned long long* cnt = ar.alloc<unsigned long long>(2);
+  // cnt[0..1]: frontier counters (alternating); cnt[2]: dense visited prefix
+  unsigned long long* cnt = ar.alloc<unsigned long long>(3);
+  // push scratch of the ordered path (same kernels as the graph engine)
+  const bool ordered_push = rank && !push_smem_enabled();
+  int64_t *rowstart = nullptr, *Sx = nullptr, *part = nullptr, *tbase = nullptr;
+  int32_t* tfirst = nullptr;
+  if (ordered_push) {
+    rowstart = ar.alloc<int64_t>(n + 1);
+    Sx = ar.alloc<int64_t>(n + 1);
+    part = ar.alloc<int64_t>(kGScanBlocks + 1);
+    tfirst = ar.alloc<int32_t>(push->nnz / kWarpTile + 2);
+    tbase = ar.alloc<int64_t>(push->nnz / kWarpTile + 2);
+  }
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cudaMemsetAsync(levels, 0, sizeof(int64_t) * n, s));
   GB_CUDA(ctx, cudaMemsetAsync(vbm, 0, sizeof(uint32_t) * W, s));
   GB_CUDA(ctx, cudaMemsetAsync(fbm[0], 0, sizeof(uint32_t) * W, s));
   GB_CUDA(ctx, cudaMemsetAsync(vprev, 0, sizeof(uint32_t) * W, s));
-  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
+  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 24, s));
   bfs_init<<<1, 1, 0, s>>>(source, levels, vbm, vprev, fbm[0], F);
+  int64_t X = 0;  // every vertex below X is visited (ordered graphs)
+  unsigned long long* xmin = rank ? cnt + 2 : nullptr;
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 6);  // 5 memsets + init
 
@@ -1209,16 +1291,41 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
         GB_CUDA(ctx, cudaMemsetAsync(c, 0, 8, s));
         GB_CUDA(ctx, cudaMemsetAsync(c_next, 0, 8, s));
       } else {
+        if (xmin) GB_CUDA(ctx, cudaMemsetAsync(xmin, 0xff, 8, s));
         const int grid = grid_for(ctx, W, 256, 8);
         const int ps = prof_begin(ctx, PROF_BFS_PULL, K);
         bfs_pull<<<grid, 256, 0, s>>>(n, dval(depth + 1), pull->offsets, pull->indices, pull_on,
                                       pull_nonempty, vbm, vprev, fbm[cur], fbm[cur ^ 1], pval(levels), F,
-                                      c, c_next, 0, (W + 31) / 32);
+                                      c, c_next, 0, (W + 31) / 32, xmin);
         prof_end(ctx, ps);
         count_launch(ctx, 1);
       }
     } else {
-      if (!push_dead) {
+      if (!push_dead && ordered_push) {
+        // the graph engine's kernels: sorted rows skip the dense visited prefix
+        g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(dval(K), F, push->offsets,
+                                                               push->indices,
+                                                               dval(prefix_mode() == 1 ? X : 0),
+                                                               rowstart, Sx,
+                                                               part);
+        g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(dval(K), part, rowstart, Sx, tfirst,
+                                                            tbase);
+        if (prof_enabled(ctx)) {
+          int64_t E = 0;
+          GB_TRY(read_i64(ctx, Sx + K, &E));
+          prof_end(ctx, prof_begin(ctx, PROF_BFS_PUSH_EDGES, E));
+        }
+        const int ps = prof_begin(ctx, PROF_BFS_PUSH, K);
+        LbsPlan plan;
+        plan.K = K;
+        plan.rowstart = rowstart;
+        plan.S = Sx;
+        plan.tile_first = tfirst;
+        plan.tile_base = tbase;
+        GB_TRY(launch_push(ctx, K, plan, push, push_on, vbm, prefix_mode() == 2 ? X : 0));
+        prof_end(ctx, ps);
+        count_launch(ctx, 3);  // scan (2), expand
+      } else if (!push_dead) {
         LbsPlan plan;
         GB_TRY(lbs_prepare(ctx, ar, K, F, push->offsets, push->nnz, &plan, kWarpTile));
         const int ps = prof_begin(ctx, PROF_BFS_PUSH, K);
@@ -1227,14 +1334,20 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
         prof_end(ctx, ps);
         count_launch(ctx, 5);  // degrees, scan (2), tile_first, expand
       }
+      if (xmin) GB_CUDA(ctx, cudaMemsetAsync(xmin, 0xff, 8, s));
       const int pf = prof_begin(ctx, PROF_BFS_FINALIZE, K);
       bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, dval(depth + 1), vbm, vprev, fbm[cur ^ 1],
-                                                         pval(levels), F, c, c_next, nullptr);
+                                                         pval(levels), F, c, c_next, nullptr, xmin);
       prof_end(ctx, pf);
       count_launch(ctx, 1);
     }
     GB_LAUNCH_CHECK(ctx);
     GB_TRY(read_i64(ctx, (const int64_t*)c, &K));
+    if (xmin) {
+      int64_t x = 0;
+      GB_TRY(read_i64(ctx, (const int64_t*)xmin, &x));
+      X = (uint64_t)x < (uint64_t)n ? x : n;
+    }
     cur ^= 1;
     if (K == 0) break;
     ++depth;
@@ -1365,7 +1478,7 @@ gb_status gb_bfs_dist_pull(gb_ctx* ctx, const gb_csr* rowblock, int64_t lo, int6
     const int ps = prof_begin(ctx, PROF_BFS_PULL, 0);
     bfs_pull<<<grid_for(ctx, (g_hi - g_lo) * 32, 256, 8), 256, 0, s>>>(
         hi, dval(depth), off, rowblock->indices, on, ne, vbm, vprev, fbm, xbm, pval(levels), F, cnt, cnt + 1,
-        g_lo, g_hi);
+        g_lo, g_hi, nullptr);
     prof_end(ctx, ps);
   }
   GB_LAUNCH_CHECK(ctx);
@@ -1383,7 +1496,7 @@ gb_status gb_bfs_dist_apply(gb_ctx* ctx, int64_t n, int64_t depth, const uint32_
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
   bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, dval(depth), vbm, vprev, fbm, pval(levels), F,
-                                                        cnt, cnt + 1, xbm);
+                                                        cnt, cnt + 1, xbm, nullptr);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 2);
   return read_i64(ctx, (const int64_t*)cnt, K_host);
