@@ -114,6 +114,112 @@ gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
 constexpr int kWarpItems = 16;
 constexpr int kWarpTile = 32 * kWarpItems;  // 512 slots
 
+// One warp tile [e0, e1) whose slots start in frontier entries k0..k1 (tb:
+// the tile descriptor's base when has_tb).  Used by warp_tiles and by the
+// TMA-prefetching BFS push for the tiles it does not stage.
+template <class F>
+__device__ __forceinline__ void warp_tile_one(const int64_t* S, const int64_t* rowstart, bool has_tb,
+                                              int64_t e0, int64_t e1, int64_t k0, int64_t k1,
+                                              int64_t tb, F& f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nk = k1 - k0 + 1;
+  if (nk <= 2) {
+    // Most tiles of a power-law push level lie inside one or two adjacency
+    // lists (R-MAT s24 level 2: 69 % one, 22 % two): the owner is one
+    // compare per item and the loads are warp-uniform broadcasts.
+    const int64_t b0 = (has_tb ? tb : rowstart[k0] - S[k0]) + e0;
+    int32_t st1 = INT32_MAX;
+    int64_t b1 = b0;
+    if (nk == 2) {
+      const int64_t s1 = S[k0 + 1];
+      st1 = (int32_t)(s1 - e0);
+      b1 = rowstart[k0 + 1] - s1 + e0;
+    }
+    const int32_t rel_end = (int32_t)(e1 - e0);
+#pragma unroll
+    for (int h = 0; h < kWarpItems; h += kWarpItems / 2)
+      f.template batch2<kWarpItems / 2>(b0, b1, st1, rel_end, h * 32);
+  } else if (nk <= 32) {
+    // Entry j of the tile (lane j) starts at st_rel (relative to e0; the
+    // first entry's start is clamped to 0).  Slot e_rel = r*32 + lane
+    // grows with r, so each lane finds its first owner by a 5-step
+    // shuffle search and afterwards only advances when a row boundary
+    // passes (warp-uniform loop, usually zero or one step per item):
+    // ~2 ALU ops per edge instead of a 64-bit search per edge.
+    int32_t st_rel = INT32_MAX;
+    int64_t base_l = 0;
+    if (lane < nk) {
+      const int64_t sk = S[k0 + lane];
+      st_rel = sk > e0 ? (int32_t)(sk - e0) : 0;
+      base_l = rowstart[k0 + lane] - sk;
+    }
+    int own = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int32_t sv = __shfl_sync(GB_FULL, st_rel, (own + step) & 31);
+      if (own + step < 32 && sv <= lane) own += step;
+    }
+    // empty entries share their start with the next one: the search and
+    // the advance both land on the last entry whose start is <= e_rel
+    int32_t nxt = __shfl_sync(GB_FULL, st_rel, (own + 1) & 31);
+    if (own == 31) nxt = INT32_MAX;
+    int64_t base = __shfl_sync(GB_FULL, base_l, own) + e0;
+    const int32_t rel_end = (int32_t)(e1 - e0);
+#pragma unroll
+    for (int h = 0; h < kWarpItems; h += kWarpItems / 4) {
+      constexpr int B = kWarpItems / 4;  // small batches keep the kernel's register count low
+      int64_t p[B];
+      bool live[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int32_t er = (h + r) * 32 + lane;
+        live[r] = er < rel_end;
+        while (__any_sync(GB_FULL, er >= nxt)) {
+          const bool adv = er >= nxt;
+          own += adv;
+          const int32_t n2 = __shfl_sync(GB_FULL, st_rel, (own + 1) & 31);
+          const int64_t b2 = __shfl_sync(GB_FULL, base_l, own & 31);
+          if (adv) {
+            nxt = own == 31 ? INT32_MAX : n2;
+            base = b2 + e0;
+          }
+        }
+        p[r] = base + er;
+      }
+      f.template batch<B>(p, live);
+    }
+  } else {
+    // many short lists: 4 entries per lane at a time, their bounds and first
+    // edges batched (one round trip for 128 entries), the rest walked
+    constexpr int B = 4;
+    for (int64_t i0 = 0; i0 < nk; i0 += 32 * B) {
+      int32_t len[B];  // edges of the entry inside this tile
+      int64_t p[B];    // position of its first edge in the tile
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int64_t i = i0 + r * 32 + lane;
+        len[r] = 0;
+        p[r] = 0;
+        if (i < nk) {
+          const int64_t k = k0 + i;
+          const int64_t sk = S[k], sk1 = S[k + 1];
+          const int64_t lo = sk > e0 ? sk : e0;
+          const int64_t hi = sk1 < e1 ? sk1 : e1;
+          len[r] = hi > lo ? (int32_t)(hi - lo) : 0;
+          p[r] = rowstart[k] - sk + lo;
+        }
+      }
+      bool live[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) live[r] = len[r] > 0;
+      f.template batch<B>(p, live);
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+        for (int32_t j = 1; j < len[r]; ++j) f.visit(p[r] + j);
+    }
+  }
+}
+
 template <class F>
 __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* S, const int64_t* rowstart,
                                            const int32_t* tile_first, const int64_t* tile_base,
@@ -142,102 +248,7 @@ __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* S, const in
       k1n = tn + 1 < ntiles ? tile_first[tn + 1] : (int32_t)(K - 1);
       if (tile_base) bn = tile_base[tn];
     }
-    const int64_t nk = k1 - k0 + 1;
-    if (nk <= 2) {
-      // Most tiles of a power-law push level lie inside one or two adjacency
-      // lists (R-MAT s24 level 2: 69 % one, 22 % two): the owner is one
-      // compare per item and the loads are warp-uniform broadcasts.
-      const int64_t b0 = (tile_base ? tb : rowstart[k0] - S[k0]) + e0;
-      int32_t st1 = INT32_MAX;
-      int64_t b1 = b0;
-      if (nk == 2) {
-        const int64_t s1 = S[k0 + 1];
-        st1 = (int32_t)(s1 - e0);
-        b1 = rowstart[k0 + 1] - s1 + e0;
-      }
-      const int32_t rel_end = (int32_t)(e1 - e0);
-#pragma unroll
-      for (int h = 0; h < kWarpItems; h += kWarpItems / 2)
-        f.template batch2<kWarpItems / 2>(b0, b1, st1, rel_end, h * 32);
-    } else if (nk <= 32) {
-      // Entry j of the tile (lane j) starts at st_rel (relative to e0; the
-      // first entry's start is clamped to 0).  Slot e_rel = r*32 + lane
-      // grows with r, so each lane finds its first owner by a 5-step
-      // shuffle search and afterwards only advances when a row boundary
-      // passes (warp-uniform loop, usually zero or one step per item):
-      // ~2 ALU ops per edge instead of a 64-bit search per edge.
-      int32_t st_rel = INT32_MAX;
-      int64_t base_l = 0;
-      if (lane < nk) {
-        const int64_t sk = S[k0 + lane];
-        st_rel = sk > e0 ? (int32_t)(sk - e0) : 0;
-        base_l = rowstart[k0 + lane] - sk;
-      }
-      int own = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int32_t sv = __shfl_sync(GB_FULL, st_rel, (own + step) & 31);
-        if (own + step < 32 && sv <= lane) own += step;
-      }
-      // empty entries share their start with the next one: the search and
-      // the advance both land on the last entry whose start is <= e_rel
-      int32_t nxt = __shfl_sync(GB_FULL, st_rel, (own + 1) & 31);
-      if (own == 31) nxt = INT32_MAX;
-      int64_t base = __shfl_sync(GB_FULL, base_l, own) + e0;
-      const int32_t rel_end = (int32_t)(e1 - e0);
-#pragma unroll
-      for (int h = 0; h < kWarpItems; h += kWarpItems / 4) {
-        constexpr int B = kWarpItems / 4;  // small batches keep the kernel's register count low
-        int64_t p[B];
-        bool live[B];
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-          const int32_t er = (h + r) * 32 + lane;
-          live[r] = er < rel_end;
-          while (__any_sync(GB_FULL, er >= nxt)) {
-            const bool adv = er >= nxt;
-            own += adv;
-            const int32_t n2 = __shfl_sync(GB_FULL, st_rel, (own + 1) & 31);
-            const int64_t b2 = __shfl_sync(GB_FULL, base_l, own & 31);
-            if (adv) {
-              nxt = own == 31 ? INT32_MAX : n2;
-              base = b2 + e0;
-            }
-          }
-          p[r] = base + er;
-        }
-        f.template batch<B>(p, live);
-      }
-    } else {
-      // many short lists: 4 entries per lane at a time, their bounds and first
-      // edges batched (one round trip for 128 entries), the rest walked
-      constexpr int B = 4;
-      for (int64_t i0 = 0; i0 < nk; i0 += 32 * B) {
-        int32_t len[B];  // edges of the entry inside this tile
-        int64_t p[B];    // position of its first edge in the tile
-#pragma unroll
-        for (int r = 0; r < B; ++r) {
-          const int64_t i = i0 + r * 32 + lane;
-          len[r] = 0;
-          p[r] = 0;
-          if (i < nk) {
-            const int64_t k = k0 + i;
-            const int64_t sk = S[k], sk1 = S[k + 1];
-            const int64_t lo = sk > e0 ? sk : e0;
-            const int64_t hi = sk1 < e1 ? sk1 : e1;
-            len[r] = hi > lo ? (int32_t)(hi - lo) : 0;
-            p[r] = rowstart[k] - sk + lo;
-          }
-        }
-        bool live[B];
-#pragma unroll
-        for (int r = 0; r < B; ++r) live[r] = len[r] > 0;
-        f.template batch<B>(p, live);
-#pragma unroll
-        for (int r = 0; r < B; ++r)
-          for (int32_t j = 1; j < len[r]; ++j) f.visit(p[r] + j);
-      }
-    }
+    warp_tile_one(S, rowstart, tile_base != nullptr, e0, e1, k0, k1, tb, f);
   }
 }
 

@@ -120,9 +120,15 @@ mv_pull_rows(int64_t nrows, const int64_t* __restrict__ off, const int32_t* __re
 #ifndef GB_MV_MINB
 #define GB_MV_MINB 3  // resident 256-thread CTAs per SM (3: 80 registers, no spills)
 #endif
-template <class T, int ADD, int MUL, bool VALS>
+// COMPACT: the rows are only the ALLOWED non-empty rows (mv_mask_plan):
+// nz_off holds their offsets in the concatenation of just their entries and
+// row_pos their first position in the matrix, so masked-out rows cost
+// nothing.  Positions are contiguous only inside a row: a lane adds the
+// tile row's (row_pos - nz_off) to its slot position.
+template <class T, int ADD, int MUL, bool VALS, bool COMPACT>
 __global__ void __launch_bounds__(256, GB_MV_MINB)
-mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
+mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
+              const int64_t* __restrict__ row_pos,
               const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
               const T* __restrict__ vals, T iso, const T* __restrict__ u,
               const uint32_t* __restrict__ mask, int add_rt, int mult_rt, T* __restrict__ out,
@@ -130,14 +136,17 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
   const int add_op = ADD >= 0 ? ADD : add_rt;
   const int mult_op = MUL >= 0 ? MUL : mult_rt;
   __shared__ uint16_t s_st[8][kRowTile + 8];
-  __shared__ uint8_t s_ok[8][kRowTile + 8];  // mask bit of each tile row
+  __shared__ uint8_t s_ok[8][COMPACT ? 1 : kRowTile + 8];     // mask bit of each tile row
+  __shared__ int64_t s_sb[COMPACT ? 8 : 1][COMPACT ? kRowTile + 8 : 1];  // row_pos - nz_off
   __shared__ unsigned long long s_cnt[3];
   if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   uint16_t* st = s_st[threadIdx.x >> 5];
   uint8_t* okr = s_ok[threadIdx.x >> 5];
+  int64_t* sb = s_sb[COMPACT ? threadIdx.x >> 5 : 0];
   const T ident = op_identity<T>(add_op);
+  const int64_t R_rows = R_d.get();
   const int64_t E = nz_off[R_rows];
   const int64_t ntiles = (E + kRowTile - 1) / kRowTile;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -151,11 +160,16 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
     const int nr = (int)(r1 - r0 + 1);
     // row starts relative to the tile, clamped to [0, kRowTile]; st[nr] ends the last row
     for (int i = lane; i <= nr; i += 32) {
-      const int64_t o = nz_off[r0 + i] - e0;
+      const int64_t no = nz_off[r0 + i];
+      const int64_t o = no - e0;
       st[i] = (uint16_t)(o < 0 ? 0 : (o > kRowTile ? kRowTile : o));
       if (i < nr) {
-        const int32_t row = nz_rows[r0 + i];
-        okr[i] = !mask || ((__ldg(mask + (row >> 5)) >> (row & 31)) & 1u);
+        if (COMPACT) {
+          sb[i] = row_pos[r0 + i] - no;
+        } else {
+          const int32_t row = nz_rows[r0 + i];
+          okr[i] = !mask || ((__ldg(mask + (row >> 5)) >> (row & 31)) & 1u);
+        }
       }
     }
     // does the tile's first row start before it / its last row end after it?
@@ -175,7 +189,9 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
     // pass 1 (per row segment, not per entry): which of my entries belong to
     // allowed rows
     uint32_t allowed = 0;
-    if (rel0 < rel1) {
+    if (COMPACT) {
+      if (rel0 < rel1) allowed = rel1 - rel0 == 32 ? ~0u : (1u << (rel1 - rel0)) - 1u;
+    } else if (rel0 < rel1) {
       int a = rel0, c = lo;
       do {
         const int b = st[c + 1] < rel1 ? st[c + 1] : rel1;
@@ -188,7 +204,24 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
     // every gather at once
     int32_t cols[kRowItems];
     const int64_t my0 = e0 + rel0;
-    if (rel1 - rel0 == kRowItems) {
+    if (COMPACT) {
+      // positions are contiguous inside a row only: add the row's shift
+      int c = lo, next = rel0 < rel1 ? st[lo + 1] : 0;
+      int64_t sh = rel0 < rel1 ? sb[lo] : 0;
+#pragma unroll
+      for (int q = 0; q < kRowItems; ++q) {
+        const int e = rel0 + q;
+        cols[q] = 0;
+        if (e < rel1) {
+          if (e >= next) {
+            ++c;
+            next = st[c + 1];
+            sh = sb[c];
+          }
+          cols[q] = __ldg(idx + my0 + q + sh);  // L1-allocating: a lane's 16 loads share lines
+        }
+      }
+    } else if (rel1 - rel0 == kRowItems) {
       const int4* p4 = reinterpret_cast<const int4*>(idx + my0);
 #pragma unroll
       for (int g = 0; g < kRowItems / 4; ++g) {
@@ -219,6 +252,7 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
     int cur = lo;
     if (rel0 < rel1) {
       int next = st[cur + 1];
+      int64_t sh = COMPACT ? sb[cur] : 0;  // position shift of the current row (COMPACT)
       // the lane's first segment continues a row from an earlier lane / tile
       const bool cont = st[cur] < rel0 || (cur == 0 && head_out);
       bool first = true;
@@ -240,9 +274,10 @@ mv_pull_tiles(int64_t R_rows, const int32_t* __restrict__ nz_rows, const int64_t
           cnt = 0;
           ++cur;
           next = st[cur + 1];
+          if (COMPACT && VALS) sh = sb[cur];
         }
         if (((allowed >> q) & 1u) && uv[q] != ident) {
-          const T a = VALS ? __ldg(vals + my0 + q) : iso;
+          const T a = VALS ? __ldg(vals + my0 + q + sh) : iso;
           acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, a, uv[q]));
           ++cnt;
         }
@@ -509,20 +544,31 @@ static gb_status push_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a, i
   return GB_OK;
 }
 
+// Rows to reduce: the plan of all non-empty rows (mask tested per row), or,
+// with `compact`, only the allowed ones (R read on the device).
+struct MvRows {
+  DevI64 R;
+  const int32_t* rows;
+  const int64_t* off;
+  const int64_t* pos;  // compact: first matrix position of each row
+  const int32_t* tile_first;
+  bool compact;
+};
+
 template <class T, int ADD, int MUL, bool VALS>
-static gb_status launch_tiles_k(gb_ctx* ctx, int add_op, int mult_op, const RowTilesPlan& plan,
+static gb_status launch_tiles_k(gb_ctx* ctx, int add_op, int mult_op, const MvRows& plan,
                                 const gb_csr* a, T iso, const T* u, const uint32_t* mask, T* out,
                                 unsigned long long* counters, uint32_t* hasmul) {
-  auto k = mv_pull_tiles<T, ADD, MUL, VALS>;
+  auto k = plan.compact ? mv_pull_tiles<T, ADD, MUL, VALS, true> : mv_pull_tiles<T, ADD, MUL, VALS, false>;
   k<<<resident_grid(ctx, k, 256), 256, 0, stream_of(ctx)>>>(
-      plan.R, plan.nz_rows, plan.nz_off, plan.tile_first, a->indices, (const T*)a->values, iso, u,
-      mask, add_op, mult_op, out, counters, hasmul);
+      plan.R, plan.rows, plan.off, plan.pos, plan.tile_first, a->indices, (const T*)a->values, iso,
+      u, mask, add_op, mult_op, out, counters, hasmul);
   return GB_OK;
 }
 
 template <class T, int ADD, int MUL>
 static gb_status launch_tiles_v(gb_ctx* ctx, int add_op, int mult_op, bool vals,
-                                const RowTilesPlan& plan, const gb_csr* a, T iso, const T* u,
+                                const MvRows& plan, const gb_csr* a, T iso, const T* u,
                                 const uint32_t* mask, T* out, unsigned long long* counters,
                                 uint32_t* hasmul) {
   return vals ? launch_tiles_k<T, ADD, MUL, true>(ctx, add_op, mult_op, plan, a, iso, u, mask, out,
@@ -534,7 +580,7 @@ static gb_status launch_tiles_v(gb_ctx* ctx, int add_op, int mult_op, bool vals,
 // the builtin semirings get their own instantiation; anything else is generic
 template <class T>
 static gb_status launch_pull_tiles(gb_ctx* ctx, int add_op, int mult_op, bool vals,
-                                   const RowTilesPlan& plan, const gb_csr* a, T iso, const T* u,
+                                   const MvRows& plan, const gb_csr* a, T iso, const T* u,
                                    const uint32_t* mask, T* out, unsigned long long* counters,
                                    uint32_t* hasmul) {
 #define GB_SR(A_, M_)                                                                         \
@@ -552,6 +598,92 @@ static gb_status launch_pull_tiles(gb_ctx* ctx, int add_op, int mult_op, bool va
 #undef GB_SR
   return launch_tiles_v<T, -1, -1>(ctx, add_op, mult_op, vals, plan, a, iso, u, mask, out, counters,
                                    hasmul);
+}
+
+// ---------------------------------------------------------------------------
+// Compact plan of the allowed rows (per call: the mask changes).  One packed
+// scan counts allowed rows (low 28 bits) and their entries (high 36 bits).
+// ---------------------------------------------------------------------------
+constexpr int kPackBits = 28;
+constexpr uint64_t kPackMask = (1ull << kPackBits) - 1;
+
+__global__ void mask_pack(int64_t R, const int32_t* __restrict__ nz_rows,
+                          const int64_t* __restrict__ nz_off, const uint32_t* __restrict__ mask,
+                          uint64_t* __restrict__ pk) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= R;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t v = 0;
+    if (i < R) {
+      const int32_t row = nz_rows[i];
+      if ((__ldg(mask + (row >> 5)) >> (row & 31)) & 1u)
+        v = ((uint64_t)(nz_off[i + 1] - nz_off[i]) << kPackBits) | 1u;
+    }
+    pk[i] = v;
+  }
+}
+
+__global__ void mask_fill(int64_t R, const int32_t* __restrict__ nz_rows,
+                          const int64_t* __restrict__ nz_off, const uint64_t* __restrict__ sc,
+                          int32_t* __restrict__ a_rows, int64_t* __restrict__ a_off,
+                          int64_t* __restrict__ a_pos, int64_t* __restrict__ A_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= R;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = sc[i];
+    const int64_t p = (int64_t)(c & kPackMask);
+    if (i == R) {
+      *A_out = p;
+      a_off[p] = (int64_t)(c >> kPackBits);
+    } else if ((sc[i + 1] & kPackMask) != (uint64_t)p) {
+      a_rows[p] = nz_rows[i];
+      a_off[p] = (int64_t)(c >> kPackBits);
+      a_pos[p] = nz_off[i];
+    }
+  }
+}
+
+// tile_first over the compact offsets, counts read on the device
+__global__ void mask_tile_first(const int64_t* __restrict__ A_d, const int64_t* __restrict__ a_off,
+                                int32_t* __restrict__ tf) {
+  const int64_t A = *A_d;
+  const int64_t E = a_off[A];
+  const int64_t ntiles = (E + kRowTile - 1) / kRowTile;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t * kRowTile;
+    int64_t lo = 0, hi = A - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (a_off[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    tf[t] = (int32_t)lo;
+  }
+}
+
+static gb_status mv_mask_plan(gb_ctx* ctx, Arena& ar, const RowTilesPlan& plan, int64_t nnz,
+                              const uint32_t* mask, MvRows* out) {
+  cudaStream_t s = stream_of(ctx);
+  const int64_t R = plan.R;
+  uint64_t* pk = ar.alloc<uint64_t>(R + 1);
+  uint64_t* sc = ar.alloc<uint64_t>(R + 1);
+  int32_t* a_rows = ar.alloc<int32_t>(R > 0 ? R : 1);
+  int64_t* a_off = ar.alloc<int64_t>(R + 1);
+  int64_t* a_pos = ar.alloc<int64_t>(R > 0 ? R : 1);
+  int32_t* tf = ar.alloc<int32_t>(nnz / kRowTile + 2);
+  int64_t* A = ar.alloc<int64_t>(1);
+  GB_ARENA_CHECK(ctx, ar);
+  mask_pack<<<grid_for(ctx, R + 1, 256), 256, 0, s>>>(R, plan.nz_rows, plan.nz_off, mask, pk);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, pk, sc, R + 1, s);
+  void* tmp = ar.raw(tb);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, pk, sc, R + 1, s));
+  mask_fill<<<grid_for(ctx, R + 1, 256), 256, 0, s>>>(R, plan.nz_rows, plan.nz_off, sc, a_rows, a_off,
+                                                      a_pos, A);
+  mask_tile_first<<<grid_for(ctx, nnz / kRowTile + 1, 256), 256, 0, s>>>(A, a_off, tf);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 5);
+  *out = MvRows{dptr(A), a_rows, a_off, a_pos, tf, true};
+  return GB_OK;
 }
 
 template <class T>
@@ -578,9 +710,15 @@ static gb_status pull_tiles_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr
   if (hasmul) GB_CUDA(ctx, cudaMemsetAsync(hasmul, 0, sizeof(uint32_t) * W, s));
   fill_value<T><<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, ident, out);
   const int ps = prof_begin(ctx, PROF_MV, a->nnz);
-  if (plan.R > 0)
-    GB_TRY(launch_pull_tiles<T>(ctx, add_op, mult_op, a->values != nullptr, plan, a, iso, u, mask,
+  if (plan.R > 0) {
+    // a mask: reduce only the allowed rows (compact plan); otherwise every
+    // non-empty row
+    MvRows rows{dval(plan.R), plan.nz_rows, plan.nz_off, nullptr, plan.tile_first, false};
+    if (mask && plan.R < (int64_t)kPackMask && (a->nnz >> (64 - kPackBits)) == 0)
+      GB_TRY(mv_mask_plan(ctx, ar, plan, a->nnz, mask, &rows));
+    GB_TRY(launch_pull_tiles<T>(ctx, add_op, mult_op, a->values != nullptr, rows, a, iso, u, mask,
                                 out, (unsigned long long*)counters, hasmul));
+  }
   prof_end(ctx, ps);
   if (counters)
     mv_pull_finish<<<grid_for(ctx, W, 256, 4), 256, 0, s>>>(W, hasmul,
