@@ -6,6 +6,8 @@
 // These are the unfused operator-layer kernels behind mxv / vxm / spmv_pull /
 // spmspv_push.  They reproduce the reference exactly, including its work
 // counters; the algorithms use their own fused drivers instead.
+#include <stdlib.h>
+
 #include <type_traits>
 
 #include <cub/cub.cuh>
@@ -714,7 +716,12 @@ static gb_status pull_tiles_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr
     // a mask: reduce only the allowed rows (compact plan); otherwise every
     // non-empty row
     MvRows rows{dval(plan.R), plan.nz_rows, plan.nz_off, nullptr, plan.tile_first, false};
-    if (mask && plan.R < (int64_t)kPackMask && (a->nnz >> (64 - kPackBits)) == 0)
+    // The compact plan skips masked-out rows entirely but loses the 16-byte
+    // index loads; it measured slower at s24 with a 50 % mask (2.04 vs
+    // 1.80 ms: the x gathers, not the masked rows, bound the kernel), so it
+    // is opt-in (GB_MV_COMPACT=1) for sparse masks.
+    static const bool compact = getenv("GB_MV_COMPACT") && atoi(getenv("GB_MV_COMPACT")) == 1;
+    if (compact && mask && plan.R < (int64_t)kPackMask && (a->nnz >> (64 - kPackBits)) == 0)
       GB_TRY(mv_mask_plan(ctx, ar, plan, a->nnz, mask, &rows));
     GB_TRY(launch_pull_tiles<T>(ctx, add_op, mult_op, a->values != nullptr, rows, a, iso, u, mask,
                                 out, (unsigned long long*)counters, hasmul));
