@@ -1,0 +1,58 @@
+"""The command-line harness (cli.py:40-277 restated on the GPU): reports carry
+the reference's result digest and direction trace for the same inputs."""
+
+import contextlib
+import hashlib
+import io
+import json
+
+import pytest
+
+from golden_io import load_json
+
+pytestmark = pytest.mark.gpu
+
+
+def run_cli(*argv):
+    from paper_1908_01407_b200 import cli
+    out = io.StringIO()
+    with contextlib.redirect_stdout(out):
+        rc = cli.main(list(argv))
+    return rc, out.getvalue()
+
+
+@pytest.mark.parametrize("algo,scale", [("bfs", 16), ("bfs", 12), ("sssp", 12), ("cc", 12)])
+def test_cli_digest_and_trace_match_reference(algo, scale):
+    gold = load_json("algorithms.json")[f"{algo}_s{scale}"]
+    rc, out = run_cli(algo, "--rmat-scale", str(scale), "--runs", "2", "--json", "--verify")
+    assert rc == 0
+    rep = json.loads(out)
+    assert rep["result_digest"] == gold["digest"]
+    assert rep["verified"] is True
+    trace = [[r["direction"], r["frontier_nvals"], r["estimated_frontier_edges"], r["threshold_edges"]]
+             for r in rep["trace"]]
+    assert trace == gold["trace"]
+    assert rep["runs"] == 2 and rep["mteps"] > 0 and rep["nnz"] > 0
+
+
+def test_cli_triangle_count_and_pagerank():
+    gold = load_json("algorithms.json")["tc_s12"]["count"]
+    rc, out = run_cli("tc", "--rmat-scale", "12", "--runs", "1", "--json", "--verify")
+    rep = json.loads(out)
+    assert rc == 0 and rep["verified"] is True
+    assert rep["result_digest"] == hashlib.sha256(str(int(gold)).encode()).hexdigest()
+    rc, out = run_cli("pr", "--rmat-scale", "10", "--runs", "1", "--verify")
+    assert rc == 0 and "verification: ok" in out
+
+
+def test_cli_text_report_and_trace_table():
+    rc, out = run_cli("bfs", "--rmat-scale", "10", "--runs", "1", "--trace")
+    assert rc == 0
+    assert out.startswith("bfs on rmat-s10-e16: 1 runs")
+    assert "iter  frontier  est_edges  threshold  direction" in out
+
+
+def test_cli_bad_source():
+    from paper_1908_01407_b200 import cli
+    with pytest.raises(SystemExit):
+        cli.main(["bfs", "--rmat-scale", "6", "--source", "64"])

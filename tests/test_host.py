@@ -158,3 +158,20 @@ def test_splitmix_scalar_matches_stream():
     g = SplitMix64(1)
     want = port.splitmix_stream(1, 0, 5)
     assert [g.next_u64() for _ in range(5)] == [int(x) for x in want]
+
+
+def test_cli_parser_matches_reference_surface():
+    """cli.py:72-100: same positional algorithm and options."""
+    from paper_1908_01407_b200 import cli
+    p = cli.build_parser()
+    a = p.parse_args(["bfs", "--rmat-scale", "16", "--source", "3", "--runs", "4", "--json",
+                      "--trace", "--verify", "--direction", "force-pull", "--switch-ratio", "0.2",
+                      "--threads", "8", "--max-iters", "7", "--alpha", "0.9", "--eps", "1e-6"])
+    assert (a.algorithm, a.rmat_scale, a.source, a.runs, a.as_json, a.trace, a.verify) == \
+        ("bfs", 16, 3, 4, True, True, True)
+    assert (a.direction, a.switch_ratio, a.threads, a.max_iters, a.alpha, a.eps) == \
+        ("force-pull", 0.2, 8, 7, 0.9, 1e-6)
+    with pytest.raises(SystemExit):
+        p.parse_args(["dfs"])
+    d = cli._make_descriptor(a, fused=False)
+    assert d.direction.value == "force-pull" and d.max_niter == 7 and d.fused is False
