@@ -246,6 +246,20 @@ __device__ __forceinline__ long long warp_reserve(unsigned long long* counter, i
   return (long long)base + pre - want;
 }
 
+// 32 consecutive bytes of a column-index stream in one 256-bit load (sm_100),
+// L1-bypassing and marked evict-first in L2 (the matrix is read once per
+// pass, the gathered vectors and bitmaps should stay resident).  p must be
+// 32-byte aligned.  GB_STREAM_L2 selects the L2 policy (A/B builds).
+#ifndef GB_STREAM_L2
+#define GB_STREAM_L2 ".L2::evict_first"
+#endif
+__device__ __forceinline__ void ld_stream8(const int32_t* p, int32_t (&v)[8]) {
+  asm("ld.global.nc.L1::no_allocate" GB_STREAM_L2 ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "l"(p));
+}
+
 // streaming read-only load that does not allocate in L1 (column-index
 // streams).  Not volatile: the data is immutable during the kernel, so the
 // compiler may predicate, batch and schedule these loads freely.

@@ -202,7 +202,7 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
         ++c;
       } while (a < rel1);
     }
-    // pass 2: column indices of the groups holding an allowed entry, then
+    // pass 2: column indices of the 8-entry groups holding an allowed entry, then
     // every gather at once
     int32_t cols[kRowItems];
     const int64_t my0 = e0 + rel0;
@@ -224,14 +224,12 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
         }
       }
     } else if (rel1 - rel0 == kRowItems) {
-      const int4* p4 = reinterpret_cast<const int4*>(idx + my0);
 #pragma unroll
-      for (int g = 0; g < kRowItems / 4; ++g) {
-        int4 v = make_int4(0, 0, 0, 0);
-        if ((allowed >> (4 * g)) & 0xFu)
-          asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-              : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + g));
-        cols[4 * g] = v.x; cols[4 * g + 1] = v.y; cols[4 * g + 2] = v.z; cols[4 * g + 3] = v.w;
+      for (int g = 0; g < kRowItems / 8; ++g) {
+        int32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if ((allowed >> (8 * g)) & 0xFFu) ld_stream8(idx + my0 + 8 * g, v);  // 256-bit loads
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cols[8 * g + j] = v[j];
       }
     } else {
 #pragma unroll

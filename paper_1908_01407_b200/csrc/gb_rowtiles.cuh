@@ -50,13 +50,13 @@ __device__ __forceinline__ void row_tiles(int64_t R_rows, const int32_t* __restr
     // column loads first: they depend on nothing but the tile position
     int32_t cols[kRowItems];
     if (my0 + kRowItems <= e1) {
-      const int4* p4 = reinterpret_cast<const int4*>(idx + my0);  // e0 is 512-aligned
+      // e0 is 512-aligned: two 256-bit loads per lane
 #pragma unroll
-      for (int q = 0; q < kRowItems / 4; ++q) {
-        int4 v;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
-        cols[4 * q] = v.x; cols[4 * q + 1] = v.y; cols[4 * q + 2] = v.z; cols[4 * q + 3] = v.w;
+      for (int q = 0; q < kRowItems / 8; ++q) {
+        int32_t v[8];
+        ld_stream8(idx + my0 + 8 * q, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cols[8 * q + j] = v[j];
       }
     } else {
 #pragma unroll
