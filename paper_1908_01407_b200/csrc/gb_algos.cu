@@ -25,6 +25,10 @@
 #include "gb_lbs.cuh"
 #include "gb_rowtiles.cuh"
 
+#ifndef GB_ROW_MINB
+#define GB_ROW_MINB 5  // resident 256-thread CTAs per SM of the row-tile pulls (48 registers)
+#endif
+
 extern "C" int32_t gb_decide_direction(int64_t nnz, int64_t nrows, int64_t nnz_u, double ratio,
                                        int32_t policy, int64_t* estimate_out);
 
@@ -106,7 +110,7 @@ struct SsspMin {
   }
 };
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, GB_ROW_MINB)
 sssp_pull_tiles(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
                 const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
                 const void* vals, int dtype, double iso, const double* __restrict__ fvd,
@@ -220,7 +224,7 @@ struct PrSum {
   }
 };
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, GB_ROW_MINB)
 pr_spmv(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
         const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
         const double* __restrict__ y, double* __restrict__ spread) {
@@ -305,7 +309,7 @@ struct CcMin {
   }
 };
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, GB_ROW_MINB)
 cc_pull(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
         const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
         const int* __restrict__ gp, int* __restrict__ hook) {
@@ -656,7 +660,7 @@ struct CcMinBlock {
   }
 };
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, GB_ROW_MINB)
 cc_pull_block(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
               const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
               const int* __restrict__ gp, int* __restrict__ hook_rebased) {

@@ -120,7 +120,10 @@ mv_pull_rows(int64_t nrows, const int64_t* __restrict__ off, const int32_t* __re
 // for iso (structure-only) matrices.
 // ---------------------------------------------------------------------------
 #ifndef GB_MV_MINB
-#define GB_MV_MINB 3  // resident 256-thread CTAs per SM (3: 80 registers, no spills)
+#define GB_MV_MINB 4  // resident 256-thread CTAs per SM (4: 64 registers; measured best with 4 waves)
+#endif
+#ifndef GB_MV_SPLIT
+#define GB_MV_SPLIT 4  // u gathers in waves of 16/SPLIT per lane (s24: 1 wave 1.80 ms, 2: 1.51, 4: 1.39, 8: 1.44)
 #endif
 // COMPACT: the rows are only the ALLOWED non-empty rows (mv_mask_plan):
 // nz_off holds their offsets in the concatenation of just their entries and
@@ -235,9 +238,12 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
 #pragma unroll
       for (int q = 0; q < kRowItems; ++q) cols[q] = (allowed >> q) & 1u ? ld_stream(idx + my0 + q) : 0;
     }
-    T uv[kRowItems];
+    // the u gathers: all 16 at once, or (GB_MV_SPLIT=2) 8 now and 8 halfway
+    // through the fold -- fewer registers, more resident warps
+    constexpr int kGat = kRowItems / GB_MV_SPLIT;
+    T uv[kGat];
 #pragma unroll
-    for (int q = 0; q < kRowItems; ++q) uv[q] = (allowed >> q) & 1u ? __ldg(u + cols[q]) : ident;
+    for (int q = 0; q < kGat; ++q) uv[q] = (allowed >> q) & 1u ? __ldg(u + cols[q]) : ident;
     c_reads += __popc(allowed);
     // pass 3: fold segment by segment.  Rows are non-empty, so one step
     // always reaches the next segment.  A segment that ends inside the lane
@@ -258,6 +264,11 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
       bool first = true;
 #pragma unroll
       for (int q = 0; q < kRowItems; ++q) {
+        if (kGat < kRowItems && q > 0 && q % kGat == 0) {
+#pragma unroll
+          for (int j = 0; j < kGat; ++j)
+            uv[j] = (allowed >> (q + j)) & 1u ? __ldg(u + cols[q + j]) : ident;
+        }
         const int e = rel0 + q;
         if (e < rel1 && e >= next) {
           if (first && cont) {
@@ -276,9 +287,9 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
           next = st[cur + 1];
           if (COMPACT && VALS) sh = sb[cur];
         }
-        if (((allowed >> q) & 1u) && uv[q] != ident) {
+        if (((allowed >> q) & 1u) && uv[q % kGat] != ident) {
           const T a = VALS ? __ldg(vals + my0 + q + sh) : iso;
-          acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, a, uv[q]));
+          acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, a, uv[q % kGat]));
           ++cnt;
         }
       }

@@ -27,6 +27,10 @@
 
 namespace gb {
 
+#ifndef GB_ROW_SPLIT
+#define GB_ROW_SPLIT 4  // gather waves per lane and tile (PR s22 x20: 1 wave 11.7 ms, 4 waves + 48 regs 10.6 ms)
+#endif
+
 constexpr int kRowItems = 16;
 constexpr int kRowTile = 32 * kRowItems;  // 512 entries per warp tile
 
@@ -71,9 +75,11 @@ __device__ __forceinline__ void row_tiles(int64_t R_rows, const int32_t* __restr
       st[i] = (uint16_t)(o < 0 ? 0 : (o > kRowTile ? kRowTile : o));
     }
     __syncwarp();
-    T vals[kRowItems];
+    // gathers in GB_ROW_SPLIT waves (fewer registers, more resident warps)
+    constexpr int kGat = kRowItems / GB_ROW_SPLIT;
+    T vals[kGat];
 #pragma unroll
-    for (int q = 0; q < kRowItems; ++q)
+    for (int q = 0; q < kGat; ++q)
       vals[q] = my0 + q < e1 ? red.load(my0 + q, cols[q]) : red.identity();
     // Fold row segment by row segment (rows are non-empty: one step reaches
     // the next segment).  A segment closed inside the lane is a whole row
@@ -99,6 +105,11 @@ __device__ __forceinline__ void row_tiles(int64_t R_rows, const int32_t* __restr
       bool first = true;
 #pragma unroll
       for (int q = 0; q < kRowItems; ++q) {
+        if (kGat < kRowItems && q > 0 && q % kGat == 0) {
+#pragma unroll
+          for (int j = 0; j < kGat; ++j)
+            vals[j] = my0 + q + j < e1 ? red.load(my0 + q + j, cols[q + j]) : red.identity();
+        }
         const int e = rel0 + q;
         if (e < rel1 && e >= next) {
           if (first && cont) {
@@ -112,7 +123,7 @@ __device__ __forceinline__ void row_tiles(int64_t R_rows, const int32_t* __restr
           ++cur;
           next = st[cur + 1];
         }
-        if (e < rel1) acc = red.fold(acc, vals[q]);
+        if (e < rel1) acc = red.fold(acc, vals[q % kGat]);
       }
       if (next <= rel1 && !(cur == nr - 1 && tail_out)) {
         // the last segment ends with my chunk
