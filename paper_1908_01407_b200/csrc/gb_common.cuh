@@ -313,7 +313,8 @@ void count_launch(gb_ctx* ctx, int n = 1);
 // event-timed region around a driver's main kernel (no-op unless profiling)
 enum { PROF_BFS_PUSH = 1, PROF_BFS_PULL = 2, PROF_BFS_FINALIZE = 3, PROF_SSSP = 4, PROF_PR = 5,
        PROF_CC = 6, PROF_TC = 7, PROF_MV = 8,
-       PROF_BFS_PUSH_EDGES = 9 /* zero-length marker: arg = edges the next push expands */ };
+       PROF_BFS_PUSH_EDGES = 9 /* zero-length marker: arg = edges the next push expands */,
+       PROF_BFS_UNPERMUTE = 10 };
 int prof_begin(gb_ctx* ctx, int kind, int64_t arg);
 void prof_end(gb_ctx* ctx, int slot);
 int sm_count(gb_ctx* ctx);
