@@ -364,6 +364,7 @@ __global__ void cc_hook(int64_t n, const int* __restrict__ hook, int* __restrict
     int m = mn[k];
     const int h = hook[k];
     if (h < m) { m = h; mn[k] = m; }
+    if (m == kImax32) continue;  // nothing to propose (sparsified / isolated)
     // read first: most targets already hold a smaller label (the giant
     // component's root is the target of millions of k), so the atomic --
     // which serialises on one L2 slice per address -- is rarely issued
@@ -382,15 +383,30 @@ cc_shortcut(int64_t n, const int* __restrict__ parent, int* __restrict__ gp,
             unsigned long long* __restrict__ live) {
   __shared__ long long s_c[8], s_l[8];
   long long c = 0, l = 0;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int g = parent[parent[k]];
-    const bool ch = g != gpp[k];
-    gpp[k] = g;
-    const int out = (sparsify && !ch) ? kImax32 : g;
-    gp[k] = out;
-    c += ch;
-    l += out != kImax32;
+  // four independent pointer jumps in flight per thread (latency-bound)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k0 < n; k0 += 4 * stride) {
+    int p[4], g[4], q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = k0 + u * stride;
+      p[u] = k < n ? parent[k] : 0;
+      q[u] = k < n ? gpp[k] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) g[u] = __ldg(parent + p[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = k0 + u * stride;
+      if (k < n) {
+        const bool ch = g[u] != q[u];
+        gpp[k] = g[u];
+        const int out = (sparsify && !ch) ? kImax32 : g[u];
+        gp[k] = out;
+        c += ch;
+        l += out != kImax32;
+      }
+    }
   }
   c = warp_sum_ll(c);
   l = warp_sum_ll(l);
