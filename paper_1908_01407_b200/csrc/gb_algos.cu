@@ -98,7 +98,7 @@ struct SsspMin {
   long long* __restrict__ cand;
   __device__ __forceinline__ double identity() const { return INFINITY; }
   __device__ __forceinline__ double load(int64_t p, int32_t col) const {
-    const double u = __ldg(fvd + col);
+    const double u = ld_gather(fvd + col);
     return u == INFINITY ? INFINITY : ld_weight(vals, dtype, iso, p) + u;
   }
   __device__ __forceinline__ double fold(double a, double x) const { return fmin(a, x); }
@@ -216,7 +216,7 @@ struct PrSum {
   const double* __restrict__ y;
   double* __restrict__ spread;
   __device__ __forceinline__ double identity() const { return 0.0; }
-  __device__ __forceinline__ double load(int64_t, int32_t col) const { return __ldg(y + col); }
+  __device__ __forceinline__ double load(int64_t, int32_t col) const { return ld_gather(y + col); }
   __device__ __forceinline__ double fold(double a, double x) const { return a + x; }
   __device__ __forceinline__ void emit(int64_t row, double acc, bool whole) const {
     if (whole) spread[row] = acc;
@@ -300,7 +300,7 @@ struct CcMin {
   const int* __restrict__ gp;
   int* __restrict__ hook;
   __device__ __forceinline__ int identity() const { return kImax32; }
-  __device__ __forceinline__ int load(int64_t, int32_t col) const { return __ldg(gp + col); }
+  __device__ __forceinline__ int load(int64_t, int32_t col) const { return ld_gather(gp + col); }
   __device__ __forceinline__ int fold(int a, int x) const { return x < a ? x : a; }
   __device__ __forceinline__ void emit(int64_t row, int acc, bool whole) const {
     if (acc == kImax32) return;  // hook was reset to the identity
@@ -667,7 +667,7 @@ struct CcMinBlock {
   const int* __restrict__ gp;
   int* __restrict__ hook;  // rebased: local row r writes hook[lo + r]
   __device__ __forceinline__ int identity() const { return kImax32; }
-  __device__ __forceinline__ int load(int64_t, int32_t col) const { return __ldg(gp + col); }
+  __device__ __forceinline__ int load(int64_t, int32_t col) const { return ld_gather(gp + col); }
   __device__ __forceinline__ int fold(int a, int x) const { return x < a ? x : a; }
   __device__ __forceinline__ void emit(int64_t row, int acc, bool whole) const {
     if (acc == kImax32) return;

@@ -288,6 +288,29 @@ __device__ __forceinline__ void red_or_shared_if(bool pred, uint32_t* addr, uint
                :: "r"(a), "r"(bits), "r"((uint32_t)pred));
 }
 
+// Random gather of a vector the pull kernels index by column.  GB_GATHER_NA=1
+// bypasses L1 (the vectors are L2-sized; random 8-byte gathers rarely hit L1)
+// -- an A/B knob, off by default.
+#ifndef GB_GATHER_NA
+#define GB_GATHER_NA 0
+#endif
+template <class T>
+__device__ __forceinline__ T ld_gather(const T* p) {
+#if GB_GATHER_NA
+  if (sizeof(T) == 8) {
+    unsigned long long v;
+    asm("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
+    return *reinterpret_cast<T*>(&v);
+  } else {
+    unsigned v;
+    asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return *reinterpret_cast<T*>(&v);
+  }
+#else
+  return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ bool bit_test(const uint32_t* bm, int64_t i) {
   return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
 }

@@ -243,7 +243,7 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
     constexpr int kGat = kRowItems / GB_MV_SPLIT;
     T uv[kGat];
 #pragma unroll
-    for (int q = 0; q < kGat; ++q) uv[q] = (allowed >> q) & 1u ? __ldg(u + cols[q]) : ident;
+    for (int q = 0; q < kGat; ++q) uv[q] = (allowed >> q) & 1u ? ld_gather(u + cols[q]) : ident;
     c_reads += __popc(allowed);
     // pass 3: fold segment by segment.  Rows are non-empty, so one step
     // always reaches the next segment.  A segment that ends inside the lane
@@ -267,7 +267,7 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
         if (kGat < kRowItems && q > 0 && q % kGat == 0) {
 #pragma unroll
           for (int j = 0; j < kGat; ++j)
-            uv[j] = (allowed >> (q + j)) & 1u ? __ldg(u + cols[q + j]) : ident;
+            uv[j] = (allowed >> (q + j)) & 1u ? ld_gather(u + cols[q + j]) : ident;
         }
         const int e = rel0 + q;
         if (e < rel1 && e >= next) {
