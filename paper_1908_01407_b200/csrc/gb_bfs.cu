@@ -287,7 +287,7 @@ static int smem_push_setup(gb_ctx* ctx, int64_t W, size_t* smem) {
 // vertex i is new vertex rank[i]; unvisited vertices read 0 (the internal
 // level array is never cleared).
 __global__ void bfs_unpermute(int64_t n, const int32_t* __restrict__ rank,
-                              const uint32_t* __restrict__ vbm, const int64_t* __restrict__ lv,
+                              const uint32_t* __restrict__ vbm, const int32_t* __restrict__ lv,
                               DevP64 out_d) {
   int64_t* __restrict__ out = out_d.get();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -300,7 +300,8 @@ __global__ void bfs_unpermute(int64_t n, const int32_t* __restrict__ rank,
 // (Scattering instead -- new id r in order, out[order[r]] -- measured 3.7x
 // slower at s24: 16.8 M scattered 8-byte writes cost more than gathers.)
 
-__global__ void bfs_init(int64_t source, int64_t* levels, uint32_t* vbm, uint32_t* vprev,
+template <class LT>
+__global__ void bfs_init(int64_t source, LT* levels, uint32_t* vbm, uint32_t* vprev,
                          uint32_t* fbm, int32_t* F) {
   levels[source] = 1;
   vbm[source >> 5] |= 1u << (source & 31);
@@ -330,9 +331,12 @@ __device__ __forceinline__ void prefix_flush(int64_t wmin, unsigned long long* x
   if (threadIdx.x == 0 && s_min != ~0ull) atomicMin(xmin, s_min);
 }
 
+// LT: int64 levels (the API vector) or int32 (the internal levels of a
+// relabelled run: half the bytes for finalize and the final unpermute)
+template <class LT>
 __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t* vbm,
                                               uint32_t* vprev, uint32_t* fbm_next,
-                                              int64_t* levels, int32_t* F,
+                                              LT* levels, int32_t* F,
                                               unsigned long long* count, const uint32_t* xbm,
                                               unsigned long long* xmin = nullptr) {
   // xbm == NULL: new frontier = vbm & ~vprev (single GPU).  xbm != NULL: the
@@ -382,7 +386,7 @@ __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t
       const int start = __shfl_sync(GB_FULL, incl - c, j);
       if ((wb >> lane) & 1u) {
         const int64_t v = (g * 32 + j) * 32 + lane;
-        levels[v] = depth;
+        levels[v] = (LT)depth;
         F[base + start + __popc(wb & ((1u << lane) - 1u))] = (int32_t)v;
       }
     }
@@ -390,10 +394,11 @@ __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t
   if (xmin) prefix_flush(wmin, xmin);
 }
 
+template <class LT>
 __global__ void __launch_bounds__(256)
 bfs_finalize(int64_t n, DevI64 depth_d, uint32_t* __restrict__ vbm,
              uint32_t* __restrict__ vprev, uint32_t* __restrict__ fbm_next,
-             DevP64 levels_d, int32_t* __restrict__ F,
+             DevP<LT> levels_d, int32_t* __restrict__ F,
              unsigned long long* __restrict__ count,
              unsigned long long* __restrict__ count_clear, const uint32_t* __restrict__ xbm,
              unsigned long long* __restrict__ xmin) {
@@ -410,11 +415,12 @@ constexpr int kPullList = 32 * kPullBatch;   // rows per warp per pass
 constexpr int kPullSerial = 8;               // entries a lane scans alone before the warp helps
 
 // The frontier bitmap is probed through L1 (ld.global.ca).
+template <class LT>
 __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_t* __restrict__ off,
                                           const int32_t* __restrict__ idx, EdgeOn on,
                                           const uint32_t* __restrict__ nonempty, uint32_t* vbm,
                                           uint32_t* vprev, const uint32_t* fbm, uint32_t* fbm_next,
-                                          int64_t* levels, int32_t* F, unsigned long long* count,
+                                          LT* levels, int32_t* F, unsigned long long* count,
                                           int64_t g_lo, int64_t g_hi,
                                           unsigned long long* xmin = nullptr) {
   // [g_lo, g_hi): groups of 32 words (1024 vertices) this launch owns; a
@@ -486,7 +492,7 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
         }
         if (hit) {
           atomicOr(&nw[(v[r] >> 5) - g * 32], 1u << (v[r] & 31));
-          levels[v[r]] = depth;
+          levels[v[r]] = (LT)depth;
         }
       }
       // long rows still unresolved: the warp scans them together
@@ -510,7 +516,7 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
           }
           if (h && lane == src) {
             atomicOr(&nw[(vv >> 5) - g * 32], 1u << (vv & 31));
-            levels[vv] = depth;
+            levels[vv] = (LT)depth;
           }
         }
       }
@@ -549,11 +555,12 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
   if (xmin) prefix_flush(wmin, xmin);
 }
 
+template <class LT>
 __global__ void __launch_bounds__(256)
 bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
          const int32_t* __restrict__ idx, EdgeOn on, const uint32_t* __restrict__ nonempty,
          uint32_t* __restrict__ vbm, uint32_t* __restrict__ vprev, const uint32_t* __restrict__ fbm,
-         uint32_t* __restrict__ fbm_next, DevP64 levels_d,
+         uint32_t* __restrict__ fbm_next, DevP<LT> levels_d,
          int32_t* __restrict__ F, unsigned long long* __restrict__ count,
          unsigned long long* __restrict__ count_clear, int64_t g_lo, int64_t g_hi,
          unsigned long long* __restrict__ xmin) {
@@ -562,7 +569,8 @@ bfs_pull(int64_t n, DevI64 depth_d, const int64_t* __restrict__ off,
             count, g_lo, g_hi, xmin);
 }
 
-__global__ void bfs_unstamp(DevI64 Kd, const int32_t* __restrict__ F, int64_t* __restrict__ levels) {
+template <class LT>
+__global__ void bfs_unstamp(DevI64 Kd, const int32_t* __restrict__ F, LT* __restrict__ levels) {
   const int64_t K = Kd.get();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -637,6 +645,7 @@ struct BfsState {
   double ratio;         // per call
   int32_t policy, pad_;
   int64_t* out;         // per call, relabelled graphs: levels by original id
+  int32_t* lv32;        // relabelled graphs: internal levels by new id
   int64_t it, K, depth, dnext, unstamp;  // loop state
   int64_t xcur;                 // dense visited prefix at the level start (ordered graphs)
   unsigned long long xnext;     // ... after the level (atomicMin target)
@@ -797,7 +806,8 @@ __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
 __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32_t* vprev,
                         uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop) {
   const int64_t s = rank ? (int64_t)rank[st->source] : st->source;
-  st->levels[s] = 1;
+  if (rank) st->lv32[s] = 1;
+  else st->levels[s] = 1;
   const uint32_t bit = 1u << (s & 31);
   vbm[s >> 5] |= bit;
   vprev[s >> 5] |= bit;
@@ -854,9 +864,12 @@ __global__ void g_unstamp(const BfsState* __restrict__ st, const int32_t* __rest
   if (!st->unstamp) return;
   const int64_t K = st->K;
   int64_t* lv = st->levels;
+  int32_t* lv32 = st->lv32;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
-       i += (int64_t)gridDim.x * blockDim.x)
-    lv[F[i]] = 0;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (lv32) lv32[F[i]] = 0;
+    else lv[F[i]] = 0;
+  }
 }
 
 struct BfsGraph {
@@ -872,7 +885,7 @@ struct BfsGraph {
   int64_t* tile_base = nullptr;
   unsigned long long* cnt = nullptr;
   int64_t *rowstart = nullptr, *S = nullptr, *part = nullptr;
-  int64_t* lv = nullptr;  // relabelled graph: levels by new id (never cleared)
+  int32_t* lv = nullptr;  // relabelled graph: levels by new id (never cleared)
   BfsState* st = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches_push = 0, launches_pull = 0, launches_fixed = 0;
@@ -946,9 +959,14 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
                                          G->tile_base, push.indices, push_on, G->vbm,
                                          ordered && prefix_mode() == 2 ? dptr(&st->xcur) : dval(0));
     }
-    bfs_finalize<<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev, G->fbm[h ^ 1],
-                                        pptr(&st->levels), G->F, G->cnt + h, G->cnt + (h ^ 1),
-                                        nullptr, ordered ? &st->xnext : nullptr);
+    if (ordered)
+      bfs_finalize<int32_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev,
+                                                   G->fbm[h ^ 1], pptr(&st->lv32), G->F, G->cnt + h,
+                                                   G->cnt + (h ^ 1), nullptr, &st->xnext);
+    else
+      bfs_finalize<int64_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev,
+                                                   G->fbm[h ^ 1], pptr(&st->levels), G->F, G->cnt + h,
+                                                   G->cnt + (h ^ 1), nullptr, nullptr);
     return cudaGetLastError();
   };
   auto pull_body = [&](int h, cudaStream_t s) -> cudaError_t {
@@ -957,10 +975,16 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       GB_GTRY(cudaMemsetAsync(G->cnt + h, 0, 8, s));
       GB_GTRY(cudaMemsetAsync(G->cnt + (h ^ 1), 0, 8, s));
     } else {
-      bfs_pull<<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices, pull_on,
-                                      G->nonempty, G->vbm, G->vprev, G->fbm[h], G->fbm[h ^ 1],
-                                      pptr(&st->levels), G->F, G->cnt + h, G->cnt + (h ^ 1), 0,
-                                      (W + 31) / 32, ordered ? &st->xnext : nullptr);
+      if (ordered)
+        bfs_pull<int32_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices,
+                                                 pull_on, G->nonempty, G->vbm, G->vprev, G->fbm[h],
+                                                 G->fbm[h ^ 1], pptr(&st->lv32), G->F, G->cnt + h,
+                                                 G->cnt + (h ^ 1), 0, (W + 31) / 32, &st->xnext);
+      else
+        bfs_pull<int64_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices,
+                                                 pull_on, G->nonempty, G->vbm, G->vprev, G->fbm[h],
+                                                 G->fbm[h ^ 1], pptr(&st->levels), G->F, G->cnt + h,
+                                                 G->cnt + (h ^ 1), 0, (W + 31) / 32, nullptr);
     }
     return cudaGetLastError();
   };
@@ -1097,7 +1121,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     const size_t o_tb = take(8 * (size_t)(push->nnz / kWarpTile + 2));
     const size_t o_cnt = take(32), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
-    const size_t o_lv = rank ? take(8 * (size_t)n) : 0;
+    const size_t o_lv = rank ? take(4 * (size_t)n) : 0;
     if (cudaMalloc(&G->mem, off) != cudaSuccess) {
       cudaGetLastError();
       delete G;
@@ -1116,7 +1140,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->S = (int64_t*)(m + o_S);
     G->part = (int64_t*)(m + o_part);
     G->st = (BfsState*)(m + o_st);
-    G->lv = rank ? (int64_t*)(m + o_lv) : nullptr;
+    G->lv = rank ? (int32_t*)(m + o_lv) : nullptr;
     cudaStream_t cs[4];
     for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
     const cudaError_t e = bfs_graph_build(ctx, G, cs);
@@ -1143,7 +1167,8 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   int64_t* log = ar.alloc<int64_t>(1 + 3 * cap);
   GB_ARENA_CHECK(ctx, ar);
   BfsState h{};
-  h.levels = rank ? G->lv : levels;
+  h.levels = rank ? nullptr : levels;
+  h.lv32 = rank ? G->lv : nullptr;
   h.out = levels;
   h.log = log;
   h.source = source;
@@ -1221,33 +1246,25 @@ static int bfs_engine_current() {
   return g_bfs_engine;
 }
 
-static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
-                         const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
-                         int64_t max_iters, double ratio, int32_t policy, int64_t* levels_out,
-                         int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
+template <class LT>
+static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                               const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
+                               int64_t max_iters, double ratio, int32_t policy, int64_t* levels_out,
+                               int32_t* log_dir, int64_t* log_nvals, int64_t* log_est,
+                               int64_t* iters_out) {
   const int64_t n = push->nrows;
-  if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
-  // Device-driven loop (one graph launch) unless profiling per kernel, the
-  // pull orientation is missing (the host loop reports that error when pull
-  // is chosen), or the engine is pinned (gb_bfs_engine; GB_BFS_GRAPH=0).
-  if (pull && bfs_engine_current() == kEngineGraph && !prof_enabled(ctx) && max_iters >= 1 &&
-      max_iters <= kGraphMaxCap) {
-    const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, source, max_iters,
-                                       ratio, policy, levels_out, log_dir, log_nvals, log_est,
-                                       iters_out);
-    if (st != GB_ERR_UNSUPPORTED) return st;
-  }
   Arena ar(ctx);
   cudaStream_t s = stream_of(ctx);
   const int64_t W = (n + 31) / 32;
-  int64_t* levels = levels_out;
+  // relabelled runs keep int32 levels by new id and unpermute at the end
+  LT* levels = reinterpret_cast<LT*>(levels_out);
   if (rank) {
     // host-driven loop over the relabelled graph: internal levels by new id
     int32_t r = 0;
     GB_CUDA(ctx, cudaMemcpyAsync(&r, rank + source, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     GB_CUDA(ctx, cudaStreamSynchronize(s));
     source = r;
-    levels = ar.alloc<int64_t>(n);
+    levels = ar.alloc<LT>(n);
   }
   uint32_t* vbm = ar.alloc<uint32_t>(W);
   uint32_t* fbm[2] = {ar.alloc<uint32_t>(W), ar.alloc<uint32_t>(W)};
@@ -1267,7 +1284,7 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     tbase = ar.alloc<int64_t>(push->nnz / kWarpTile + 2);
   }
   GB_ARENA_CHECK(ctx, ar);
-  GB_CUDA(ctx, cudaMemsetAsync(levels, 0, sizeof(int64_t) * n, s));
+  GB_CUDA(ctx, cudaMemsetAsync(levels, 0, sizeof(LT) * n, s));
   GB_CUDA(ctx, cudaMemsetAsync(vbm, 0, sizeof(uint32_t) * W, s));
   GB_CUDA(ctx, cudaMemsetAsync(fbm[0], 0, sizeof(uint32_t) * W, s));
   GB_CUDA(ctx, cudaMemsetAsync(vprev, 0, sizeof(uint32_t) * W, s));
@@ -1369,14 +1386,40 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     }
   }
   *iters_out = iters;
-  if (rank) {
-    const int pu = prof_begin(ctx, PROF_BFS_UNPERMUTE, n);
-    bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rank, vbm, levels, pval(levels_out));
-    prof_end(ctx, pu);
-    GB_LAUNCH_CHECK(ctx);
-    count_launch(ctx, 1);
+  if constexpr (sizeof(LT) == 4) {
+    if (rank) {
+      const int pu = prof_begin(ctx, PROF_BFS_UNPERMUTE, n);
+      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rank, vbm, levels,
+                                                             pval(levels_out));
+      prof_end(ctx, pu);
+      GB_LAUNCH_CHECK(ctx);
+      count_launch(ctx, 1);
+    }
   }
   return GB_OK;
+}
+
+static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                         const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
+                         int64_t max_iters, double ratio, int32_t policy, int64_t* levels_out,
+                         int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
+  const int64_t n = push->nrows;
+  if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
+  // Device-driven loop (one graph launch) unless profiling per kernel, the
+  // pull orientation is missing (the host loop reports that error when pull
+  // is chosen), or the engine is pinned (gb_bfs_engine; GB_BFS_GRAPH=0).
+  if (pull && bfs_engine_current() == kEngineGraph && !prof_enabled(ctx) && max_iters >= 1 &&
+      max_iters <= kGraphMaxCap) {
+    const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, source, max_iters,
+                                       ratio, policy, levels_out, log_dir, log_nvals, log_est,
+                                       iters_out);
+    if (st != GB_ERR_UNSUPPORTED) return st;
+  }
+  if (rank)
+    return bfs_host_loop<int32_t>(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio,
+                                  policy, levels_out, log_dir, log_nvals, log_est, iters_out);
+  return bfs_host_loop<int64_t>(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio,
+                                policy, levels_out, log_dir, log_nvals, log_est, iters_out);
 }
 
 }  // namespace gb

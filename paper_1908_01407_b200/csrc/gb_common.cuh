@@ -372,13 +372,17 @@ struct DevI64 {
 inline DevI64 dval(int64_t v) { return DevI64{v, nullptr}; }
 inline DevI64 dptr(const int64_t* p) { return DevI64{0, p}; }
 // Same for an output array pointer.
-struct DevP64 {
-  int64_t* v;
-  int64_t* const* p;
-  __device__ __forceinline__ int64_t* get() const { return p ? *p : v; }
+template <class T>
+struct DevP {
+  T* v;
+  T* const* p;
+  __device__ __forceinline__ T* get() const { return p ? *p : v; }
 };
-inline DevP64 pval(int64_t* v) { return DevP64{v, nullptr}; }
-inline DevP64 pptr(int64_t* const* p) { return DevP64{nullptr, p}; }
+using DevP64 = DevP<int64_t>;
+template <class T>
+inline DevP<T> pval(T* v) { return DevP<T>{v, nullptr}; }
+template <class T>
+inline DevP<T> pptr(T* const* p) { return DevP<T>{nullptr, p}; }
 
 // grid for a grid-stride kernel over n items
 inline int grid_for(gb_ctx* ctx, int64_t n, int block, int per_sm = 8) {
