@@ -44,6 +44,9 @@ _INT_INF = np.iinfo(np.int64).max
 # bfs over the degree-ordered relabelling (SparseMatrix.traversal); GB_BFS_ORDER=0
 # keeps the original labels (A/B measurement, tests of both paths)
 _ORDERED_BFS = os.environ.get("GB_BFS_ORDER", "1") != "0"
+# pagerank iterates on the same layout (s22 x20: 10.9-11.2 ms vs 12.1-12.5 ms
+# on the stored labels); GB_PR_ORDER=0 keeps the stored labels
+_ORDERED_PR = os.environ.get("GB_PR_ORDER", "1") != "0"
 
 _POLICY = {Direction.AUTO: _lib.DIR_AUTO, Direction.FORCE_PUSH: _lib.DIR_PUSH,
            Direction.FORCE_PULL: _lib.DIR_PULL}
@@ -231,17 +234,29 @@ def pagerank(A: SparseMatrix, alpha=0.85, eps=1e-7, max_iters=10_000, desc=None)
         return _pagerank_composed(A, alpha, eps, max_iters, desc)
     n = A.nrows
     ranks = empty(n, np.float64)
-    pull_o = A.orient(True)
+    trav = A.traversal() if _ORDERED_PR else None
+    if trav is not None:
+        # iterate on the degree-ordered layout (hub ranks packed in L1/L2),
+        # unpermute once at the end
+        push_o, pull_o, rank = trav
+        out_off = push_o.offsets
+        work = empty(n, np.float64)
+    else:
+        pull_o, out_off, work = A.orient(True), A.orient(False).offsets, ranks
     pull, _k = pull_o.csr_struct()
     cap = max(max_iters, 1)
     dirs, nv, est = np.zeros(cap, np.int32), np.zeros(cap, np.int64), np.zeros(cap, np.int64)
     errs = np.zeros(cap, np.float64)
     done = C.c_int64(0)
-    _lib.context().call(
-        "gb_pagerank", C.byref(pull), _lib.ptr(A.orient(False).offsets), float(alpha), float(eps),
-        int(max_iters), float(desc.switch_ratio), _POLICY[desc.direction], _lib.ptr(ranks),
+    ctx = _lib.context()
+    ctx.call(
+        "gb_pagerank", C.byref(pull), _lib.ptr(out_off), float(alpha), float(eps),
+        int(max_iters), float(desc.switch_ratio), _POLICY[desc.direction], _lib.ptr(work),
         dirs.ctypes.data_as(C.c_void_p), nv.ctypes.data_as(C.c_void_p),
         est.ctypes.data_as(C.c_void_p), errs.ctypes.data_as(C.c_void_p), C.byref(done))
+    if trav is not None:
+        ctx.call("gb_gather", _lib.dtype_code(np.float64), n, _lib.ptr(A._rank64()), n,
+                 _lib.ptr(work), _lib.ptr(ranks))
     _log_decisions(desc, A, dirs, nv, est, int(done.value))
     return Vector._wrap(n, None, ranks, 0.0, np.float64)
 

@@ -728,6 +728,17 @@ class SparseMatrix:
         o._ordered = (csc, (push, pull, rank))
         return o._ordered[1]
 
+    def _rank64(self):
+        """int64 copy of the traversal rank (gather targets), cached with it."""
+        o = self._csr
+        c = o._ordered
+        if c is None or len(c) < 3:
+            rank = self.traversal()[2]
+            c = o._ordered
+        if len(c) < 3:
+            o._ordered = (c[0], c[1], c[1][2].to(torch.int64))
+        return o._ordered[2]
+
     def row_ids(self):
         o = self._csr
         out = empty(o.nnz, np.int32)

@@ -35,3 +35,7 @@ def test_bfs_prefix_modes(mode):
 def test_bfs_shared_memory_push():
     _pytest({"GB_PUSH_SMEM": "1"}, os.path.join(HERE, "test_gpu_bfs.py"), "-k",
             "golden or oracle or ordered or s24")
+
+
+def test_pagerank_stored_labels():
+    _pytest({"GB_PR_ORDER": "0"}, os.path.join(HERE, "test_gpu_algorithms.py"), "-k", "pr or pagerank")
