@@ -39,3 +39,7 @@ def test_bfs_shared_memory_push():
 
 def test_pagerank_stored_labels():
     _pytest({"GB_PR_ORDER": "0"}, os.path.join(HERE, "test_gpu_algorithms.py"), "-k", "pr or pagerank")
+
+
+def test_sssp_stored_labels():
+    _pytest({"GB_SSSP_ORDER": "0"}, os.path.join(HERE, "test_gpu_algorithms.py"), "-k", "sssp")
