@@ -326,9 +326,16 @@ def run_ours(args):
     from paper_1908_01407_b200.io import rmat_matrix
 
     rank, world, local = env_rank()
+    # one process per GPU; GB_DIST_BACKEND=gloo (test only) lets several ranks
+    # share one GPU to exercise the multi-rank path on a single-GPU box
+    backend = os.environ.get("GB_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     ctx = _lib.context()
 
@@ -343,12 +350,12 @@ def run_ours(args):
         # 1D vertex partition: this rank keeps its row block (pull) and column
         # block (push); one NCCL all-reduce of the n/8-byte frontier bitmap per level
         from paper_1908_01407_b200 import distributed as gbd
-        block = gbd.BlockGraph.from_matrix(A, rank, world)
-        steps = gbd.NativeSteps(block)
-        exchange = gbd.TorchExchange()
+        # the partition of the degree-ordered layout (as the 1-GPU bfs uses it);
+        # levels are gathered back to original ids inside the step
+        runner = gbd.OrderedPartitionedBfs(A, rank, world)
 
         def step():
-            return gbd.bfs_partitioned(block, args.source, steps=steps, exchange=exchange)
+            return runner(args.source)
     else:
         def step():
             return gb.bfs(A, args.source)

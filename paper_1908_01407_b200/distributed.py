@@ -284,13 +284,46 @@ def connected_components(A_or_block, desc=None, sparsify=True, group=None):
     return Vector._wrap(g.n, None, labels, np.iinfo(np.int64).max, np.int64)
 
 
-def bfs(A_or_block, source, desc=None, group=None):
-    """Public entry: bfs on this rank's block; returns the (replicated) level Vector."""
+class OrderedPartitionedBfs:
+    """The partitioned BFS over the degree-ordered layout of A (as the
+    single-GPU bfs uses it): vertices renumbered by descending degree
+    (SparseMatrix.traversal), edge-balanced blocks of NEW ids -- rank 0 owns
+    the hubs, and every rank's probes fall in its own slice of the bitmap --
+    the source mapped in, the replicated levels gathered back to the original
+    ids at the end (gb_gather).  Levels and the direction log equal bfs(A)."""
+
+    def __init__(self, A: SparseMatrix, rank: int, world: int, group=None, bounds=None):
+        push_o, pull_o, self.rank_t = A.traversal()
+        Ar = SparseMatrix._wrap(A.nrows, A.ncols, push_o, pull_o, A.dtype, A._sym)
+        self.block = BlockGraph.from_matrix(Ar, rank, world, bounds)
+        self.steps = NativeSteps(self.block)
+        self.exchange = TorchExchange(group)
+        self.rank64 = A._rank64()
+        self.out = torch.empty(A.nrows, dtype=torch.int64, device=push_o.offsets.device)
+
+    def __call__(self, source: int, desc=None):
+        if not 0 <= source < self.block.n:
+            raise IndexError(f"source {source} out of range")
+        src = int(self.rank_t[source].item())
+        lv = bfs_partitioned(self.block, src, desc, steps=self.steps, exchange=self.exchange)
+        n = self.block.n
+        _lib.context().call("gb_gather", _lib.dtype_code(np.int64), n, _lib.ptr(self.rank64), n,
+                            _lib.ptr(lv), _lib.ptr(self.out))
+        return self.out
+
+
+def bfs(A_or_block, source, desc=None, group=None, ordered=True):
+    """Public entry: bfs on this rank's block; returns the (replicated) level Vector.
+    A SparseMatrix with a column orientation is partitioned over its
+    degree-ordered layout unless ``ordered=False``."""
     g = A_or_block
     if isinstance(A_or_block, SparseMatrix):
         import torch.distributed as dist
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if ordered and A_or_block.traversal() is not None:
+            run = OrderedPartitionedBfs(A_or_block, rank, world, group)
+            return Vector._wrap(A_or_block.nrows, None, run(source, desc).clone(), 0, np.int64)
         g = BlockGraph.from_matrix(A_or_block, rank, world)
     levels = bfs_partitioned(g, source, desc, exchange=TorchExchange(group))
     return Vector._wrap(g.n, None, levels, 0, np.int64)

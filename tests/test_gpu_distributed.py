@@ -117,3 +117,31 @@ def test_partitioned_world1_entry_point():
     got = distributed.bfs(A, 0, desc=d).values
     want = gb.bfs(A, 0, desc=gb.Descriptor(max_niter=3)).values
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_partitioned_ordered_layout_equals_single(P):
+    """The partition of the degree-ordered layout (OrderedPartitionedBfs
+    blocks) in lock step: levels by original id equal the single-GPU BFS."""
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200.containers import SparseMatrix
+    A = gb.io.rmat_matrix(16)
+    push_o, pull_o, rank = A.traversal()
+    Ar = SparseMatrix._wrap(A.nrows, A.ncols, push_o, pull_o, A.dtype, A._sym)
+    rank = rank.long().cpu().numpy()
+    for src in (0, 5, 40000):
+        d1, d2 = gb.Descriptor(), gb.Descriptor()
+        want = gb.bfs(A, src, desc=d1).values
+        got_r = lockstep_bfs(Ar, P, int(rank[src]), d2)
+        assert np.array_equal(got_r[rank], want)
+        assert [(x.chosen, x.frontier_nvals) for x in d1.direction_log] == \
+            [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
+
+
+def test_ordered_partitioned_runner_single_rank():
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200.distributed import OrderedPartitionedBfs
+    A = gb.io.rmat_matrix(14)
+    run = OrderedPartitionedBfs(A, 0, 1)
+    for src in (0, 3, 9999):
+        assert np.array_equal(run(src).cpu().numpy(), gb.bfs(A, src).values)
