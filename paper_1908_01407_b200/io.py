@@ -305,3 +305,31 @@ def write_matrix_market(path, edges: EdgeList, comment=None):
         else:
             for s, t, x in zip(src, dst, w):
                 fh.write(f"{s + 1} {t + 1} {x:g}\n")
+
+
+# ---------------------------------------------------------------------------
+# Binary CSR cache (an extension): a preprocessed matrix
+# saved once and reloaded without re-running generation / preprocessing.
+# ---------------------------------------------------------------------------
+
+
+def save_matrix(path, A: SparseMatrix):
+    """Write A's CSR (and whether it is symmetric) to an .npz file."""
+    o = A._csr
+    vals = None if o.values is None else to_host(o.values)
+    np.savez(path, nrows=A.nrows, ncols=A.ncols, row_offsets=to_host(o.offsets),
+             col_indices=to_host(o.indices), values=vals if vals is not None else np.empty(0),
+             iso=np.asarray(o.iso if o.iso is not None else 0), has_values=vals is not None,
+             dtype=str(A.dtype), symmetric=bool(A.is_symmetric()) if A.nrows == A.ncols else False)
+
+
+def load_matrix(path, build_csc=True) -> SparseMatrix:
+    """Read a matrix written by save_matrix onto the current device."""
+    z = np.load(path, allow_pickle=False)
+    nrows, ncols = int(z["nrows"]), int(z["ncols"])
+    dt = np.dtype(str(z["dtype"]))
+    off, idx = z["row_offsets"], z["col_indices"]
+    vals = z["values"] if bool(z["has_values"]) else np.full(idx.size, z["iso"].item(), dtype=dt)
+    sym = bool(z["symmetric"])
+    return SparseMatrix.from_csr(nrows, ncols, off, idx, vals.astype(dt, copy=False),
+                                 build_csc=build_csc, symmetric=True if sym else None)

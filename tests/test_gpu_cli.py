@@ -56,3 +56,22 @@ def test_cli_bad_source():
     from paper_1908_01407_b200 import cli
     with pytest.raises(SystemExit):
         cli.main(["bfs", "--rmat-scale", "6", "--source", "64"])
+
+
+def test_binary_csr_cache_round_trip(tmp_path):
+    import numpy as np
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200.io import load_matrix, save_matrix
+    for weighted in (False, True):
+        A = gb.io.rmat_matrix(12, weighted=weighted)
+        p = str(tmp_path / f"g{int(weighted)}.npz")
+        save_matrix(p, A)
+        B = load_matrix(p)
+        assert B.nnz == A.nnz and B.is_symmetric()
+        assert np.array_equal(B.row_offsets, A.row_offsets)
+        assert np.array_equal(B.col_indices, A.col_indices)
+        assert np.array_equal(B.csr_values, A.csr_values)
+    gold = load_json("algorithms.json")["bfs_s12"]
+    save_matrix(str(tmp_path / "s12.npz"), gb.io.rmat_matrix(12))
+    rc, out = run_cli("bfs", "--graph", str(tmp_path / "s12.npz"), "--runs", "1", "--json")
+    assert rc == 0 and json.loads(out)["result_digest"] == gold["digest"]
