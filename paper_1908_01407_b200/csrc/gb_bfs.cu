@@ -146,6 +146,23 @@ static int prefix_mode() {
   static const int m = getenv("GB_PREFIX_MODE") ? atoi(getenv("GB_PREFIX_MODE")) : 1;
   return m;
 }
+// Degree window [lo, hi] of the lists that mode 1 cuts (GB_CUT_LO / GB_CUT_HI);
+// lists outside it are expanded whole.  Lists under 32 entries are not cut by
+// default: their search costs about what expanding the few prefix edges does
+// (s24: 0.885 vs 0.909 ms per BFS).
+// GB_CUT_SAMPLES=0: plain binary search for the cut (no column samples)
+static bool use_samples() {
+  static const bool v = !(getenv("GB_CUT_SAMPLES") && atoi(getenv("GB_CUT_SAMPLES")) == 0);
+  return v;
+}
+static int64_t cut_lo() {
+  static const int64_t v = getenv("GB_CUT_LO") ? atoll(getenv("GB_CUT_LO")) : 32;
+  return v > 1 ? v : 1;
+}
+static int64_t cut_hi() {
+  static const int64_t v = getenv("GB_CUT_HI") ? atoll(getenv("GB_CUT_HI")) : INT64_MAX;
+  return v;
+}
 
 // Register budget of the push (GB_PUSH_MINB = minimum resident CTAs of 256
 // threads per SM: 1 leaves the allocation to ptxas, 3 allows 80, 4 caps at 64,
@@ -654,12 +671,29 @@ struct BfsState {
 constexpr int kGScanBlocks = 2368;  // 16 per SM (the lower-bound searches want threads); each apply block folds its predecessors
 constexpr int kGScanThreads = 256;
 constexpr int kGScanItems = 4;
+constexpr int64_t kSampleStride = 32;  // column samples: samp[j] = idx[32 j]
+constexpr int kApplyRanges = 4;  // scan ranges per apply block
+constexpr int kApplyBlocks = kGScanBlocks / kApplyRanges;
+static_assert(kGScanBlocks % kApplyRanges == 0, "apply blocks cover the scan ranges");
 constexpr int64_t kGraphMaxCap = 1 << 20;  // longer loop caps use the host-driven path
 
 
-__device__ __forceinline__ void g_range(int64_t K, int64_t* lo, int64_t* hi) {
-  const int64_t per = (K + gridDim.x - 1) / gridDim.x;
-  *lo = blockIdx.x * per;
+// column samples of a sorted-row (ordered) push matrix: samp[j] = idx[32 j]
+__global__ void sample_columns(int64_t ns, const int32_t* __restrict__ idx,
+                               int32_t* __restrict__ samp) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ns;
+       j += (int64_t)gridDim.x * blockDim.x)
+    samp[j] = idx[j * kSampleStride];
+}
+
+// capacity of the stamp queue: a queued list spans > 4 tile starts, so it is
+// longer than 4 * kWarpTile edges
+static inline int64_t stamp_queue_cap(int64_t nnz) { return nnz / (4 * kWarpTile) + 2; }
+
+// entries [lo, hi) of scan range b out of kGScanBlocks
+__device__ __forceinline__ void g_range_of(int64_t K, int64_t b, int64_t* lo, int64_t* hi) {
+  const int64_t per = (K + kGScanBlocks - 1) / kGScanBlocks;
+  *lo = b * per < K ? b * per : K;
   *hi = *lo + per < K ? *lo + per : K;
 }
 
@@ -673,21 +707,42 @@ __device__ __forceinline__ void g_range(int64_t K, int64_t* lo, int64_t* hi) {
 __device__ __forceinline__ void scan_partials_body(int64_t K, const int32_t* F,
                                                    const int64_t* __restrict__ off,
                                                    const int32_t* __restrict__ idx, int64_t X,
+                                                   int64_t clo, int64_t chi,
+                                                   const int32_t* __restrict__ samp,
                                                    int64_t* rowstart, int64_t* deg, int64_t* part) {
   using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
   __shared__ typename BlockReduce::TempStorage tmp;
   int64_t lo, hi;
-  g_range(K, &lo, &hi);
+  g_range_of(K, blockIdx.x, &lo, &hi);
   int64_t sum = 0;
   for (int64_t k = lo + threadIdx.x; k < hi; k += kGScanThreads) {
     const int64_t v = F[k];
     int64_t a = __ldg(off + v);
     const int64_t b = __ldg(off + v + 1);
-    if (X > 0 && a < b && __ldg(idx + a) < X) {
+    if (X > 0 && b - a >= clo && b - a <= chi && __ldg(idx + a) < X) {
       if (__ldg(idx + b - 1) < X) {
         a = b;
       } else {  // first position in (a, b-1] holding a column >= X
         int64_t l = a + 1, h = b - 1;
+        if (samp) {
+          // narrow to one 32-entry line through the column samples
+          // (samp[j] = idx[32 j]): the samples of a 512-entry list share
+          // one line, so ~2 lines are touched instead of ~6
+          int64_t jl = (l + kSampleStride - 1) / kSampleStride, jh = h / kSampleStride;
+          if (jl <= jh) {
+            if (__ldg(samp + jh) < X) {
+              l = jh * kSampleStride + 1;  // the cut lies after the last sample
+            } else {
+              while (jl < jh) {  // first sample >= X
+                const int64_t m = (jl + jh) >> 1;
+                if (__ldg(samp + m) < X) jl = m + 1; else jh = m;
+              }
+              h = jh * kSampleStride;
+              const int64_t lp = h - kSampleStride + 1;
+              if (lp > l) l = lp;
+            }
+          }
+        }
         while (l < h) {
           const int64_t m = (l + h) >> 1;
           if (__ldg(idx + m) < X) l = m + 1; else h = m;
@@ -701,13 +756,15 @@ __device__ __forceinline__ void scan_partials_body(int64_t K, const int32_t* F,
   }
   const int64_t tot = BlockReduce(tmp).Sum(sum);
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
+  if (blockIdx.x == 0 && threadIdx.x == 0) part[kGScanBlocks] = 0;  // stamp queue length
 }
 
 __global__ void __launch_bounds__(kGScanThreads)
 g_scan_partials(DevI64 Kd, const int32_t* __restrict__ F, const int64_t* __restrict__ off,
-                const int32_t* __restrict__ idx, DevI64 Xd, int64_t* __restrict__ rowstart,
+                const int32_t* __restrict__ idx, DevI64 Xd, int64_t clo, int64_t chi,
+                const int32_t* __restrict__ samp, int64_t* __restrict__ rowstart,
                 int64_t* __restrict__ deg, int64_t* __restrict__ part) {
-  scan_partials_body(Kd.get(), F, off, idx, Xd.get(), rowstart, deg, part);
+  scan_partials_body(Kd.get(), F, off, idx, Xd.get(), clo, chi, samp, rowstart, deg, part);
 }
 
 // rowstart[k] = off[F[k]], S = exclusive scan of the degrees, S[K] = E, and
@@ -717,7 +774,8 @@ g_scan_partials(DevI64 Kd, const int32_t* __restrict__ F, const int64_t* __restr
 // one launch replaces scan-top / scan-apply / tile-first.
 // rowstart[k] and the lengths (in S[k]) come from scan_partials_body.
 __device__ __forceinline__ void scan_apply_body(int64_t K, const int64_t* part, const int64_t* rowstart,
-                                                int64_t* S, int32_t* tile_first, int64_t* tile_base) {
+                                                int64_t* S, int32_t* tile_first, int64_t* tile_base,
+                                                int64_t* qcount, int64_t* queue) {
   using BlockScan = cub::BlockScan<int64_t, kGScanThreads>;
   using BlockReduce = cub::BlockReduce<int64_t, kGScanThreads>;
   __shared__ union {
@@ -725,26 +783,46 @@ __device__ __forceinline__ void scan_apply_body(int64_t K, const int64_t* part, 
     typename BlockReduce::TempStorage red;
   } tmp;
   __shared__ int64_t s_run;
-  int64_t lo, hi;
-  g_range(K, &lo, &hi);
+  // block b applies scan ranges [b*kApplyRanges, (b+1)*kApplyRanges): one
+  // wave of blocks instead of four
+  const int r0 = blockIdx.x * kApplyRanges;
+  int64_t lo, hi, dummy;
+  g_range_of(K, r0, &lo, &dummy);
+  g_range_of(K, r0 + kApplyRanges - 1, &dummy, &hi);
+  // blocks past the end only matter for S[K] (the last block)
+  if (lo >= hi && blockIdx.x != gridDim.x - 1) return;
   {
     int64_t c = 0;
-    for (int i = threadIdx.x; i < (int)blockIdx.x; i += kGScanThreads) c += part[i];
+    // all predecessor partials in flight at once
+    constexpr int kCarry = (kGScanBlocks + kGScanThreads - 1) / kGScanThreads;
+    int64_t pv[kCarry];
+#pragma unroll
+    for (int j = 0; j < kCarry; ++j) {
+      const int i = threadIdx.x + j * kGScanThreads;
+      pv[j] = i < r0 ? part[i] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kCarry; ++j) c += pv[j];
     const int64_t run0 = BlockReduce(tmp.red).Sum(c);
     if (threadIdx.x == 0) {
       s_run = run0;
-      if (blockIdx.x == gridDim.x - 1) S[K] = run0 + part[blockIdx.x];
+      if (blockIdx.x == gridDim.x - 1) {
+        int64_t t = run0;
+        for (int i = r0; i < kGScanBlocks; ++i) t += part[i];
+        S[K] = t;
+      }
     }
     __syncthreads();
   }
   int64_t run = s_run;
   for (int64_t base = lo; base < hi; base += kGScanThreads * kGScanItems) {
-    int64_t d[kGScanItems];
+    int64_t d[kGScanItems], r[kGScanItems];
     int64_t sum = 0;
 #pragma unroll
     for (int i = 0; i < kGScanItems; ++i) {
       const int64_t k = base + threadIdx.x * kGScanItems + i;
       d[i] = k < hi ? S[k] : 0;
+      r[i] = k < hi ? rowstart[k] : 0;
       sum += d[i];
     }
     int64_t pre, agg;
@@ -754,13 +832,13 @@ __device__ __forceinline__ void scan_apply_body(int64_t K, const int64_t* part, 
 #pragma unroll
     for (int i = 0; i < kGScanItems; ++i) {
       const int64_t k = base + threadIdx.x * kGScanItems + i;
-      // tiles [t0, t1) start inside this entry's range; a few are stamped by
-      // the owning thread, long lists (a hub spans ~800 tiles) by its warp
+      // tiles [t0, t1) start inside this entry's range; up to 4 are stamped
+      // by the owning thread
       int64_t t0 = 0, t1 = 0, b = 0;
       if (k < hi) {
         S[k] = acc;
         if (d[i] > 0) {
-          b = rowstart[k] - acc;
+          b = r[i] - acc;
           t0 = (acc + kWarpTile - 1) / kWarpTile;
           t1 = (acc + d[i] + kWarpTile - 1) / kWarpTile;
           if (t1 - t0 <= 4) {
@@ -771,15 +849,23 @@ __device__ __forceinline__ void scan_apply_body(int64_t K, const int64_t* part, 
           }
         }
       }
-      uint32_t big = __ballot_sync(GB_FULL, t1 - t0 > 4);
-      while (big) {
-        const int src = __ffs(big) - 1;
-        big &= big - 1;
-        const int64_t u0 = __shfl_sync(GB_FULL, t0, src), u1 = __shfl_sync(GB_FULL, t1, src);
-        const int64_t ub = __shfl_sync(GB_FULL, b, src), uk = __shfl_sync(GB_FULL, k, src);
-        for (int64_t t = u0 + lane; t < u1; t += 32) {
-          tile_first[t] = (int32_t)uk;
-          tile_base[t] = ub;
+      // lists spanning more than 4 tiles go to the stamp queue (one warp
+      // each in g_scan_stamp): stamped here they serialise on the warps that
+      // hold the level's hubs
+      const bool qb = t1 - t0 > 4;
+      const uint32_t qm = __ballot_sync(GB_FULL, qb);
+      if (qm) {
+        const int leader = __ffs(qm) - 1;
+        unsigned long long qbase = 0;
+        if (lane == leader)
+          qbase = atomicAdd(reinterpret_cast<unsigned long long*>(qcount), (unsigned long long)__popc(qm));
+        qbase = __shfl_sync(GB_FULL, qbase, leader);
+        if (qb) {
+          int64_t* job = queue + 4 * (qbase + __popc(qm & ((1u << lane) - 1u)));
+          job[0] = t0;
+          job[1] = t1;
+          job[2] = b;
+          job[3] = k;
         }
       }
       acc += d[i];
@@ -789,11 +875,29 @@ __device__ __forceinline__ void scan_apply_body(int64_t K, const int64_t* part, 
   }
 }
 
-__global__ void __launch_bounds__(kGScanThreads)
-g_scan_apply(DevI64 Kd, const int64_t* __restrict__ part, const int64_t* __restrict__ rowstart,
+__global__ void __launch_bounds__(kGScanThreads, 4)
+g_scan_apply(DevI64 Kd, int64_t* __restrict__ part, const int64_t* __restrict__ rowstart,
              int64_t* __restrict__ S, int32_t* __restrict__ tile_first,
-             int64_t* __restrict__ tile_base) {
-  scan_apply_body(Kd.get(), part, rowstart, S, tile_first, tile_base);
+             int64_t* __restrict__ tile_base, int64_t* __restrict__ queue) {
+  scan_apply_body(Kd.get(), part, rowstart, S, tile_first, tile_base, part + kGScanBlocks, queue);
+}
+
+// Stamp the queued long lists' tiles, one warp per list.  The queue length
+// lives in part[kGScanBlocks] (reset by g_scan_partials).
+__global__ void __launch_bounds__(256)
+g_scan_stamp(const int64_t* __restrict__ part, const int64_t* __restrict__ queue,
+             int32_t* __restrict__ tile_first, int64_t* __restrict__ tile_base) {
+  const int64_t nq = part[kGScanBlocks];
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; e < nq;
+       e += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t t0 = queue[4 * e], t1 = queue[4 * e + 1], b = queue[4 * e + 2];
+    const int32_t k = (int32_t)queue[4 * e + 3];
+    for (int64_t t = t0 + lane; t < t1; t += 32) {
+      tile_first[t] = k;
+      tile_base[t] = b;
+    }
+  }
 }
 
 __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
@@ -886,6 +990,8 @@ struct BfsGraph {
   unsigned long long* cnt = nullptr;
   int64_t *rowstart = nullptr, *S = nullptr, *part = nullptr;
   int32_t* lv = nullptr;  // relabelled graph: levels by new id (never cleared)
+  int32_t* samp = nullptr;  // relabelled graph: column samples of the push matrix
+  int64_t* queue = nullptr;  // stamp queue of the long lists (4 x int64 per list)
   BfsState* st = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches_push = 0, launches_pull = 0, launches_fixed = 0;
@@ -935,7 +1041,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   size_t smem = 0;
   const int grid_smem = push.values ? smem_push_setup<true>(ctx, W, &smem)
                                     : smem_push_setup<false>(ctx, W, &smem);
-  G->launches_push = 3 + (push_dead ? 0 : 1);
+  G->launches_push = 4 + (push_dead ? 0 : 1);
+  const int grid_stamp = grid_for(ctx, (int64_t)1 << 40, 256, 8);
   G->launches_pull = pull_dead ? 3 : 1;
   G->launches_fixed = 8;  // 4 memsets, zero (or unpermute), start, unstamp (+2 per level below)
 
@@ -943,10 +1050,11 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     // ordered (sorted-row) graphs skip the dense visited prefix of each list
     g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(
         dptr(&st->K), G->F, push.offsets, push.indices,
-        ordered && prefix_mode() == 1 ? dptr(&st->xcur) : dval(0),
-        G->rowstart, G->S, G->part);
-    g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(dptr(&st->K), G->part, G->rowstart, G->S,
-                                                        G->tile_first, G->tile_base);
+        ordered && prefix_mode() == 1 ? dptr(&st->xcur) : dval(0), cut_lo(), cut_hi(),
+        use_samples() ? G->samp : nullptr, G->rowstart, G->S, G->part);
+    g_scan_apply<<<kApplyBlocks, kGScanThreads, 0, s>>>(dptr(&st->K), G->part, G->rowstart, G->S,
+                                                        G->tile_first, G->tile_base, G->queue);
+    g_scan_stamp<<<grid_stamp, 256, 0, s>>>(G->part, G->queue, G->tile_first, G->tile_base);
     if (!push_dead && use_smem) {
       if (push.values)
         bfs_expand_smem<true><<<grid_smem, kSmemPushThreads, smem, s>>>(
@@ -1121,7 +1229,10 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     const size_t o_tb = take(8 * (size_t)(push->nnz / kWarpTile + 2));
     const size_t o_cnt = take(32), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
+    const size_t o_q = take(32 * (size_t)stamp_queue_cap(push->nnz));
     const size_t o_lv = rank ? take(4 * (size_t)n) : 0;
+    const int64_t ns = (push->nnz + kSampleStride - 1) / kSampleStride;
+    const size_t o_samp = rank ? take(4 * (size_t)ns) : 0;
     if (cudaMalloc(&G->mem, off) != cudaSuccess) {
       cudaGetLastError();
       delete G;
@@ -1139,8 +1250,13 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->rowstart = (int64_t*)(m + o_rs);
     G->S = (int64_t*)(m + o_S);
     G->part = (int64_t*)(m + o_part);
+    G->queue = (int64_t*)(m + o_q);
     G->st = (BfsState*)(m + o_st);
     G->lv = rank ? (int32_t*)(m + o_lv) : nullptr;
+    G->samp = rank ? (int32_t*)(m + o_samp) : nullptr;
+    if (rank && ns > 0)
+      sample_columns<<<grid_for(ctx, ns, 256, 8), 256, 0, stream_of(ctx)>>>(ns, push->indices,
+                                                                          G->samp);
     cudaStream_t cs[4];
     for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
     const cudaError_t e = bfs_graph_build(ctx, G, cs);
@@ -1274,16 +1390,23 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   unsigned long long* cnt = ar.alloc<unsigned long long>(3);
   // push scratch of the ordered path (same kernels as the graph engine)
   const bool ordered_push = rank && !push_smem_enabled();
-  int64_t *rowstart = nullptr, *Sx = nullptr, *part = nullptr, *tbase = nullptr;
-  int32_t* tfirst = nullptr;
+  int64_t *rowstart = nullptr, *Sx = nullptr, *part = nullptr, *tbase = nullptr, *queue = nullptr;
+  int32_t *tfirst = nullptr, *samp = nullptr;
+  const int64_t ns = (push->nnz + kSampleStride - 1) / kSampleStride;
   if (ordered_push) {
+    if (use_samples() && ns > 0) samp = ar.alloc<int32_t>(ns);
     rowstart = ar.alloc<int64_t>(n + 1);
     Sx = ar.alloc<int64_t>(n + 1);
     part = ar.alloc<int64_t>(kGScanBlocks + 1);
+    queue = ar.alloc<int64_t>(4 * stamp_queue_cap(push->nnz));
     tfirst = ar.alloc<int32_t>(push->nnz / kWarpTile + 2);
     tbase = ar.alloc<int64_t>(push->nnz / kWarpTile + 2);
   }
   GB_ARENA_CHECK(ctx, ar);
+  if (samp) {  // rebuilt per call here; the graph engine keeps them with the graph
+    sample_columns<<<grid_for(ctx, ns, 256, 8), 256, 0, s>>>(ns, push->indices, samp);
+    count_launch(ctx, 1);
+  }
   GB_CUDA(ctx, cudaMemsetAsync(levels, 0, sizeof(LT) * n, s));
   GB_CUDA(ctx, cudaMemsetAsync(vbm, 0, sizeof(uint32_t) * W, s));
   GB_CUDA(ctx, cudaMemsetAsync(fbm[0], 0, sizeof(uint32_t) * W, s));
@@ -1332,10 +1455,13 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
         g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(dval(K), F, push->offsets,
                                                                push->indices,
                                                                dval(prefix_mode() == 1 ? X : 0),
+                                                               cut_lo(), cut_hi(), samp,
                                                                rowstart, Sx,
                                                                part);
-        g_scan_apply<<<kGScanBlocks, kGScanThreads, 0, s>>>(dval(K), part, rowstart, Sx, tfirst,
-                                                            tbase);
+        g_scan_apply<<<kApplyBlocks, kGScanThreads, 0, s>>>(dval(K), part, rowstart, Sx, tfirst,
+                                                            tbase, queue);
+        g_scan_stamp<<<grid_for(ctx, (int64_t)1 << 40, 256, 8), 256, 0, s>>>(part, queue, tfirst,
+                                                                              tbase);
         if (prof_enabled(ctx)) {
           int64_t E = 0;
           GB_TRY(read_i64(ctx, Sx + K, &E));
@@ -1350,7 +1476,7 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
         plan.tile_base = tbase;
         GB_TRY(launch_push(ctx, K, plan, push, push_on, vbm, prefix_mode() == 2 ? X : 0));
         prof_end(ctx, ps);
-        count_launch(ctx, 3);  // scan (2), expand
+        count_launch(ctx, 4);  // scan (3), expand
       } else if (!push_dead) {
         LbsPlan plan;
         GB_TRY(lbs_prepare(ctx, ar, K, F, push->offsets, push->nnz, &plan, kWarpTile));
