@@ -301,17 +301,45 @@ static int smem_push_setup(gb_ctx* ctx, int64_t W, size_t* smem) {
 }
 
 // levels of the original vertex ids from a run over the relabelled graph:
-// vertex i is new vertex rank[i]; unvisited vertices read 0 (the internal
-// level array is never cleared).
+// vertex i is new vertex rank[i]; the internal levels are cleared at the start
+// of each run, so unvisited vertices read 0 (one gather per vertex: the
+// random gathers, not HBM, bound this kernel).
+template <class LT>
 __global__ void bfs_unpermute(int64_t n, const int32_t* __restrict__ rank,
-                              const uint32_t* __restrict__ vbm, const int32_t* __restrict__ lv,
-                              DevP64 out_d) {
+                              const LT* __restrict__ lv, DevP64 out_d) {
   int64_t* __restrict__ out = out_d.get();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = rank[i];
-    out[i] = ((__ldg(vbm + (r >> 5)) >> (r & 31)) & 1u) ? lv[r] : 0;
+  // 8 vertices per thread, every load of the group in flight at once
+  // (one vertex at a time leaves the loop latency-bound at ~3.4 TB/s)
+  const bool aligned = ((reinterpret_cast<uintptr_t>(rank) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const int64_t n8 = aligned ? n / 8 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int4* r4 = reinterpret_cast<const int4*>(rank);
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int4 ra = make_int4(0, 0, 0, 0), rb = ra;
+  if (g < n8) {
+    ra = __ldcs(r4 + 2 * g);
+    rb = __ldcs(r4 + 2 * g + 1);
   }
+  for (; g < n8; g += stride) {
+    // the next group's ranks are in flight while this group gathers
+    int4 na = ra, nb = rb;
+    if (g + stride < n8) {
+      na = __ldcs(r4 + 2 * (g + stride));
+      nb = __ldcs(r4 + 2 * (g + stride) + 1);
+    }
+    const int32_t r[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+    ra = na;
+    rb = nb;
+    int64_t l[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) l[j] = (int64_t)lv[r[j]];
+    longlong2* o = reinterpret_cast<longlong2*>(out + 8 * g);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) __stcs(o + j, make_longlong2(l[2 * j], l[2 * j + 1]));
+  }
+  for (int64_t i = 8 * n8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)lv[rank[i]];
 }
 
 // (Scattering instead -- new id r in order, out[order[r]] -- measured 3.7x
@@ -347,6 +375,15 @@ __device__ __forceinline__ void prefix_flush(int64_t wmin, unsigned long long* x
   __syncthreads();
   if (threadIdx.x == 0 && s_min != ~0ull) atomicMin(xmin, s_min);
 }
+
+// The level stored for a vertex: byte levels (relabelled runs) saturate at
+// 255; a run that deep is redone with int32 levels (bfs_run).
+template <class LT>
+__device__ __forceinline__ LT level_of(int64_t depth) {
+  if constexpr (sizeof(LT) == 1) return (LT)(depth < 255 ? depth : 255);
+  else return (LT)depth;
+}
+constexpr int64_t kByteLevelIters = 250;  // deeper runs use int32 internal levels
 
 // LT: int64 levels (the API vector) or int32 (the internal levels of a
 // relabelled run: half the bytes for finalize and the final unpermute)
@@ -403,7 +440,7 @@ __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t
       const int start = __shfl_sync(GB_FULL, incl - c, j);
       if ((wb >> lane) & 1u) {
         const int64_t v = (g * 32 + j) * 32 + lane;
-        levels[v] = (LT)depth;
+        levels[v] = level_of<LT>(depth);
         F[base + start + __popc(wb & ((1u << lane) - 1u))] = (int32_t)v;
       }
     }
@@ -509,7 +546,7 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
         }
         if (hit) {
           atomicOr(&nw[(v[r] >> 5) - g * 32], 1u << (v[r] & 31));
-          levels[v[r]] = (LT)depth;
+          levels[v[r]] = level_of<LT>(depth);
         }
       }
       // long rows still unresolved: the warp scans them together
@@ -533,7 +570,7 @@ __device__ __forceinline__ void pull_body(int64_t n, int64_t depth, const int64_
           }
           if (h && lane == src) {
             atomicOr(&nw[(vv >> 5) - g * 32], 1u << (vv & 31));
-            levels[vv] = (LT)depth;
+            levels[vv] = level_of<LT>(depth);
           }
         }
       }
@@ -662,7 +699,7 @@ struct BfsState {
   double ratio;         // per call
   int32_t policy, pad_;
   int64_t* out;         // per call, relabelled graphs: levels by original id
-  int32_t* lv32;        // relabelled graphs: internal levels by new id
+  uint8_t* lv8;         // relabelled graphs: internal (byte) levels by new id
   int64_t it, K, depth, dnext, unstamp;  // loop state
   int64_t xcur;                 // dense visited prefix at the level start (ordered graphs)
   unsigned long long xnext;     // ... after the level (atomicMin target)
@@ -910,7 +947,7 @@ __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
 __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32_t* vprev,
                         uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop) {
   const int64_t s = rank ? (int64_t)rank[st->source] : st->source;
-  if (rank) st->lv32[s] = 1;
+  if (rank) st->lv8[s] = 1;
   else st->levels[s] = 1;
   const uint32_t bit = 1u << (s & 31);
   vbm[s >> 5] |= bit;
@@ -968,10 +1005,10 @@ __global__ void g_unstamp(const BfsState* __restrict__ st, const int32_t* __rest
   if (!st->unstamp) return;
   const int64_t K = st->K;
   int64_t* lv = st->levels;
-  int32_t* lv32 = st->lv32;
+  uint8_t* lv8 = st->lv8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (lv32) lv32[F[i]] = 0;
+    if (lv8) lv8[F[i]] = 0;
     else lv[F[i]] = 0;
   }
 }
@@ -989,7 +1026,7 @@ struct BfsGraph {
   int64_t* tile_base = nullptr;
   unsigned long long* cnt = nullptr;
   int64_t *rowstart = nullptr, *S = nullptr, *part = nullptr;
-  int32_t* lv = nullptr;  // relabelled graph: levels by new id (never cleared)
+  uint8_t* lv = nullptr;  // relabelled graph: byte levels by new id (never cleared)
   int32_t* samp = nullptr;  // relabelled graph: column samples of the push matrix
   int64_t* queue = nullptr;  // stamp queue of the long lists (4 x int64 per list)
   BfsState* st = nullptr;
@@ -1044,7 +1081,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   G->launches_push = 4 + (push_dead ? 0 : 1);
   const int grid_stamp = grid_for(ctx, (int64_t)1 << 40, 256, 8);
   G->launches_pull = pull_dead ? 3 : 1;
-  G->launches_fixed = 8;  // 4 memsets, zero (or unpermute), start, unstamp (+2 per level below)
+  // 4 memsets, zero levels (or clear byte levels + unpermute), start, unstamp
+  G->launches_fixed = ordered ? 9 : 8;
 
   auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
     // ordered (sorted-row) graphs skip the dense visited prefix of each list
@@ -1068,8 +1106,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
                                          ordered && prefix_mode() == 2 ? dptr(&st->xcur) : dval(0));
     }
     if (ordered)
-      bfs_finalize<int32_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev,
-                                                   G->fbm[h ^ 1], pptr(&st->lv32), G->F, G->cnt + h,
+      bfs_finalize<uint8_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev,
+                                                   G->fbm[h ^ 1], pptr(&st->lv8), G->F, G->cnt + h,
                                                    G->cnt + (h ^ 1), nullptr, &st->xnext);
     else
       bfs_finalize<int64_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev,
@@ -1084,9 +1122,9 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       GB_GTRY(cudaMemsetAsync(G->cnt + (h ^ 1), 0, 8, s));
     } else {
       if (ordered)
-        bfs_pull<int32_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices,
+        bfs_pull<uint8_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices,
                                                  pull_on, G->nonempty, G->vbm, G->vprev, G->fbm[h],
-                                                 G->fbm[h ^ 1], pptr(&st->lv32), G->F, G->cnt + h,
+                                                 G->fbm[h ^ 1], pptr(&st->lv8), G->F, G->cnt + h,
                                                  G->cnt + (h ^ 1), 0, (W + 31) / 32, &st->xnext);
       else
         bfs_pull<int64_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices,
@@ -1137,9 +1175,10 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     GB_GTRY(cudaMemsetAsync(G->vprev, 0, sizeof(uint32_t) * W, s));
     GB_GTRY(cudaMemsetAsync(G->fbm[0], 0, sizeof(uint32_t) * W, s));
     GB_GTRY(cudaMemsetAsync(G->cnt, 0, 16, s));
-    // a relabelled run never clears its internal levels: the final
-    // unpermute reads them only where the visited bit is set
+    // the API levels (int64) or the internal byte levels of a relabelled run
+    // start at 0: unvisited vertices read 0
     if (!ordered) g_zero_levels<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, st);
+    else GB_GTRY(cudaMemsetAsync(G->lv, 0, (size_t)n, s));  // unvisited read level 0
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
@@ -1189,7 +1228,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     }));
     g_unstamp<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(st, G->F);
     if (ordered)
-      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, G->rank, G->vbm, G->lv,
+      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, G->rank, G->lv,
                                                              pptr(&st->out));
     return cudaGetLastError();
   });
@@ -1230,7 +1269,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     const size_t o_cnt = take(32), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
     const size_t o_q = take(32 * (size_t)stamp_queue_cap(push->nnz));
-    const size_t o_lv = rank ? take(4 * (size_t)n) : 0;
+    const size_t o_lv = rank ? take((size_t)n) : 0;
     const int64_t ns = (push->nnz + kSampleStride - 1) / kSampleStride;
     const size_t o_samp = rank ? take(4 * (size_t)ns) : 0;
     if (cudaMalloc(&G->mem, off) != cudaSuccess) {
@@ -1252,7 +1291,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->part = (int64_t*)(m + o_part);
     G->queue = (int64_t*)(m + o_q);
     G->st = (BfsState*)(m + o_st);
-    G->lv = rank ? (int32_t*)(m + o_lv) : nullptr;
+    G->lv = rank ? (uint8_t*)(m + o_lv) : nullptr;
     G->samp = rank ? (int32_t*)(m + o_samp) : nullptr;
     if (rank && ns > 0)
       sample_columns<<<grid_for(ctx, ns, 256, 8), 256, 0, stream_of(ctx)>>>(ns, push->indices,
@@ -1284,7 +1323,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   GB_ARENA_CHECK(ctx, ar);
   BfsState h{};
   h.levels = rank ? nullptr : levels;
-  h.lv32 = rank ? G->lv : nullptr;
+  h.lv8 = rank ? G->lv : nullptr;
   h.out = levels;
   h.log = log;
   h.source = source;
@@ -1362,6 +1401,8 @@ static int bfs_engine_current() {
   return g_bfs_engine;
 }
 
+constexpr gb_status kTooDeep = -1000;  // internal: byte levels would saturate
+
 template <class LT>
 static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                                const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
@@ -1425,6 +1466,9 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   int64_t K = 1, depth = 1, iters = 0;
   int cur = 0;
   for (int64_t it = 0; it < max_iters; ++it) {
+    if constexpr (sizeof(LT) == 1) {
+      if (it >= kByteLevelIters) return kTooDeep;
+    }
     int64_t est = 0;
     const int32_t dir = gb_decide_direction(push->nnz, push->nrows, K, ratio, policy, &est);
     log_dir[it] = dir;
@@ -1512,10 +1556,10 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     }
   }
   *iters_out = iters;
-  if constexpr (sizeof(LT) == 4) {
+  if constexpr (sizeof(LT) <= 4) {
     if (rank) {
       const int pu = prof_begin(ctx, PROF_BFS_UNPERMUTE, n);
-      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rank, vbm, levels,
+      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rank, levels,
                                                              pval(levels_out));
       prof_end(ctx, pu);
       GB_LAUNCH_CHECK(ctx);
@@ -1539,11 +1583,22 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, source, max_iters,
                                        ratio, policy, levels_out, log_dir, log_nvals, log_est,
                                        iters_out);
+    // byte levels saturate: a relabelled run this deep is redone with int32
+    const bool deep = st == GB_OK && rank && *iters_out >= kByteLevelIters;
+    if (deep)
+      return bfs_host_loop<int32_t>(ctx, push, pull, pull_nonempty, rank, source, max_iters,
+                                    ratio, policy, levels_out, log_dir, log_nvals, log_est,
+                                    iters_out);
     if (st != GB_ERR_UNSUPPORTED) return st;
   }
-  if (rank)
+  if (rank) {
+    const gb_status st = bfs_host_loop<uint8_t>(ctx, push, pull, pull_nonempty, rank, source,
+                                                max_iters, ratio, policy, levels_out, log_dir,
+                                                log_nvals, log_est, iters_out);
+    if (st != kTooDeep) return st;
     return bfs_host_loop<int32_t>(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio,
                                   policy, levels_out, log_dir, log_nvals, log_est, iters_out);
+  }
   return bfs_host_loop<int64_t>(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio,
                                 policy, levels_out, log_dir, log_nvals, log_est, iters_out);
 }
