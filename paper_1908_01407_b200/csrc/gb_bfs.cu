@@ -385,8 +385,10 @@ __device__ __forceinline__ LT level_of(int64_t depth) {
 }
 constexpr int64_t kByteLevelIters = 250;  // deeper runs use int32 internal levels
 
-// LT: int64 levels (the API vector) or int32 (the internal levels of a
-// relabelled run: half the bytes for finalize and the final unpermute)
+constexpr int kFinalizeWarps = 8;  // finalize blocks are 256 threads
+
+// LT: int64 levels (the API vector) or byte levels (a relabelled run; int32
+// when it is deeper than 250 levels)
 template <class LT>
 __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t* vbm,
                                               uint32_t* vprev, uint32_t* fbm_next,
@@ -395,13 +397,19 @@ __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t
                                               unsigned long long* xmin = nullptr) {
   // xbm == NULL: new frontier = vbm & ~vprev (single GPU).  xbm != NULL: the
   // all-reduced new-frontier bitmap of a 1D-partitioned run is authoritative.
+  // The block walks 8 groups per step and reserves their frontier-list
+  // slots with ONE atomic (one per warp-group put ~16 K same-address atomics
+  // on the counter at s24 levels 1-2).
+  __shared__ unsigned long long s_base;
+  __shared__ int s_tot[kFinalizeWarps + 1];
   const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
   int64_t wmin = INT64_MAX;
   const int64_t W = (n + 31) / 32;
   const int64_t G = (W + 31) / 32;
-  const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t g = g0; g < G; g += ng) {
+  for (int64_t gb = (int64_t)blockIdx.x * kFinalizeWarps; gb < G;
+       gb += (int64_t)gridDim.x * kFinalizeWarps) {
+    const int64_t g = gb + wid;
     const int64_t w = g * 32 + lane;
     uint32_t bits = 0, visited = ~0u;
     if (w < W) {
@@ -429,9 +437,19 @@ __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t
       if (lane >= o) incl += y;
     }
     const int total = __shfl_sync(GB_FULL, incl, 31);
-    unsigned long long base = 0;
-    if (lane == 31 && total) base = atomicAdd(count, (unsigned long long)total);
-    base = __shfl_sync(GB_FULL, base, 31);
+    if (lane == 31) s_tot[wid] = total;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int i = 0; i < kFinalizeWarps; ++i) {
+        const int t = s_tot[i];
+        s_tot[i] = run;
+        run += t;
+      }
+      s_base = run ? atomicAdd(count, (unsigned long long)run) : 0ull;
+    }
+    __syncthreads();
+    const unsigned long long base = s_base + (unsigned long long)s_tot[wid];
     uint32_t nonzero = __ballot_sync(GB_FULL, bits != 0);
     while (nonzero) {
       const int j = __ffs(nonzero) - 1;
