@@ -302,12 +302,18 @@ static int smem_push_setup(gb_ctx* ctx, int64_t W, size_t* smem) {
 
 // levels of the original vertex ids from a run over the relabelled graph:
 // vertex i is new vertex rank[i]; the internal levels are cleared at the start
-// of each run, so unvisited vertices read 0 (one gather per vertex: the
-// random gathers, not HBM, bound this kernel).
+// of each run, so unvisited vertices read 0.  s24: ~50 us, the same with no
+// gathers at all -- the 67 MB rank read + 134 MB int64 write stream at
+// ~3.9 TB/s whatever the store flavour or grid (measured).
+// Vertices without in-edges are never reached (only the source is): in the
+// degree order they are the ids >= limit, read as 0 without a gather (47 %
+// of R-MAT vertices are isolated).
 template <class LT>
 __global__ void bfs_unpermute(int64_t n, const int32_t* __restrict__ rank,
-                              const LT* __restrict__ lv, DevP64 out_d) {
+                              const LT* __restrict__ lv, int64_t limit, DevI64 srank_d,
+                              DevP64 out_d) {
   int64_t* __restrict__ out = out_d.get();
+  const int64_t srank = srank_d.get();
   // 8 vertices per thread, every load of the group in flight at once
   // (one vertex at a time leaves the loop latency-bound at ~3.4 TB/s)
   const bool aligned = ((reinterpret_cast<uintptr_t>(rank) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
@@ -332,14 +338,29 @@ __global__ void bfs_unpermute(int64_t n, const int32_t* __restrict__ rank,
     rb = nb;
     int64_t l[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) l[j] = (int64_t)lv[r[j]];
+    for (int j = 0; j < 8; ++j)
+      l[j] = (r[j] < limit || r[j] == srank) ? (int64_t)lv[r[j]] : 0;
     longlong2* o = reinterpret_cast<longlong2*>(out + 8 * g);
 #pragma unroll
     for (int j = 0; j < 4; ++j) __stcs(o + j, make_longlong2(l[2 * j], l[2 * j + 1]));
   }
   for (int64_t i = 8 * n8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (int64_t)lv[rank[i]];
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rank[i];
+    out[i] = (r < limit || r == srank) ? (int64_t)lv[r] : 0;
+  }
+}
+
+// first vertex without in-edges of a degree-ordered graph (in-degrees are
+// non-increasing in the new ids): lower bound of nnz in the pull offsets
+__global__ void reach_limit(int64_t n, const int64_t* __restrict__ off, int64_t* out) {
+  int64_t lo = 0, hi = n;  // off[hi] == nnz
+  const int64_t nnz = off[n];
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (off[m] < nnz) lo = m + 1; else hi = m;
+  }
+  *out = lo;
 }
 
 // (Scattering instead -- new id r in order, out[order[r]] -- measured 3.7x
@@ -720,6 +741,7 @@ struct BfsState {
   uint8_t* lv8;         // relabelled graphs: internal (byte) levels by new id
   int64_t it, K, depth, dnext, unstamp;  // loop state
   int64_t xcur;                 // dense visited prefix at the level start (ordered graphs)
+  int64_t srank;                // relabelled graphs: the source's new id
   unsigned long long xnext;     // ... after the level (atomicMin target)
 };
 
@@ -965,6 +987,7 @@ __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
 __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32_t* vprev,
                         uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop) {
   const int64_t s = rank ? (int64_t)rank[st->source] : st->source;
+  st->srank = s;
   if (rank) st->lv8[s] = 1;
   else st->levels[s] = 1;
   const uint32_t bit = 1u << (s & 31);
@@ -1047,6 +1070,7 @@ struct BfsGraph {
   uint8_t* lv = nullptr;  // relabelled graph: byte levels by new id (never cleared)
   int32_t* samp = nullptr;  // relabelled graph: column samples of the push matrix
   int64_t* queue = nullptr;  // stamp queue of the long lists (4 x int64 per list)
+  int64_t reach = 0;         // relabelled graph: vertices >= reach have no in-edges
   BfsState* st = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches_push = 0, launches_pull = 0, launches_fixed = 0;
@@ -1246,8 +1270,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     }));
     g_unstamp<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(st, G->F);
     if (ordered)
-      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, G->rank, G->lv,
-                                                             pptr(&st->out));
+      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, G->rank, G->lv, G->reach,
+                                                             dptr(&st->srank), pptr(&st->out));
     return cudaGetLastError();
   });
   if (err == cudaSuccess) err = cudaGraphInstantiate(&G->exec, top, 0);
@@ -1314,6 +1338,14 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     if (rank && ns > 0)
       sample_columns<<<grid_for(ctx, ns, 256, 8), 256, 0, stream_of(ctx)>>>(ns, push->indices,
                                                                           G->samp);
+    G->reach = n;
+    if (rank) {
+      reach_limit<<<1, 1, 0, stream_of(ctx)>>>(n, pull->offsets, G->part);
+      if (read_i64(ctx, G->part, &G->reach) != GB_OK) {
+        bfs_graph_free(G);
+        return GB_ERR_CUDA;
+      }
+    }
     cudaStream_t cs[4];
     for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
     const cudaError_t e = bfs_graph_build(ctx, G, cs);
@@ -1440,6 +1472,13 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     GB_CUDA(ctx, cudaStreamSynchronize(s));
     source = r;
     levels = ar.alloc<LT>(n);
+  }
+  int64_t reach = n;
+  if (rank && pull) {
+    int64_t* tmp = ar.alloc<int64_t>(1);
+    GB_ARENA_CHECK(ctx, ar);
+    reach_limit<<<1, 1, 0, s>>>(n, pull->offsets, tmp);
+    GB_TRY(read_i64(ctx, tmp, &reach));
   }
   uint32_t* vbm = ar.alloc<uint32_t>(W);
   uint32_t* fbm[2] = {ar.alloc<uint32_t>(W), ar.alloc<uint32_t>(W)};
@@ -1577,8 +1616,8 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   if constexpr (sizeof(LT) <= 4) {
     if (rank) {
       const int pu = prof_begin(ctx, PROF_BFS_UNPERMUTE, n);
-      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rank, levels,
-                                                             pval(levels_out));
+      bfs_unpermute<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rank, levels, reach,
+                                                             dval(source), pval(levels_out));
       prof_end(ctx, pu);
       GB_LAUNCH_CHECK(ctx);
       count_launch(ctx, 1);
