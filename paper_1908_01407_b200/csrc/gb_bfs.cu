@@ -763,6 +763,67 @@ __global__ void sample_columns(int64_t ns, const int32_t* __restrict__ idx,
     samp[j] = idx[j * kSampleStride];
 }
 
+// Per-matrix data of a relabelled BFS, built once and cached in the context
+// (both engines use it): the push matrix's column samples and the reach limit.
+struct OrderedAux {
+  const int32_t* idx = nullptr;
+  int64_t nnz = 0;
+  const int64_t* pull_off = nullptr;
+  int32_t* samp = nullptr;
+  int64_t reach = 0;
+};
+
+static void ordered_aux_free(void* p) {
+  auto* a = static_cast<OrderedAux*>(p);
+  if (a->samp) cudaFree(a->samp);
+  delete a;
+}
+
+static gb_status ordered_aux(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                             const OrderedAux** out) {
+  void** slot = ctx_slot(ctx, SLOT_BFS_AUX, ordered_aux_free);
+  auto* a = static_cast<OrderedAux*>(*slot);
+  const int64_t* poff = pull ? pull->offsets : nullptr;
+  if (a && a->idx == push->indices && a->nnz == push->nnz && a->pull_off == poff) {
+    *out = a;
+    return GB_OK;
+  }
+  cudaStream_t s = stream_of(ctx);
+  if (a) {
+    cudaStreamSynchronize(s);
+    ordered_aux_free(a);
+    *slot = nullptr;
+  }
+  a = new OrderedAux();
+  a->idx = push->indices;
+  a->nnz = push->nnz;
+  a->pull_off = poff;
+  a->reach = push->nrows;
+  const int64_t ns = (push->nnz + kSampleStride - 1) / kSampleStride;
+  if (ns > 0) {
+    if (cudaMalloc(&a->samp, sizeof(int32_t) * ns) != cudaSuccess) {
+      cudaGetLastError();
+      delete a;
+      return set_error(ctx, GB_ERR_OOM, "bfs column samples (%lld)", (long long)ns);
+    }
+    sample_columns<<<grid_for(ctx, ns, 256, 8), 256, 0, s>>>(ns, push->indices, a->samp);
+  }
+  if (poff) {
+    Arena ar(ctx);
+    int64_t* tmp = ar.alloc<int64_t>(1);
+    GB_ARENA_CHECK(ctx, ar);
+    reach_limit<<<1, 1, 0, s>>>(push->nrows, poff, tmp);
+    const gb_status st = read_i64(ctx, tmp, &a->reach);
+    if (st != GB_OK) {
+      ordered_aux_free(a);
+      return st;
+    }
+  }
+  *slot = a;
+  *out = a;
+  return GB_OK;
+}
+
 // capacity of the stamp queue: a queued list spans > 4 tile starts, so it is
 // longer than 4 * kWarpTile edges
 static inline int64_t stamp_queue_cap(int64_t nnz) { return nnz / (4 * kWarpTile) + 2; }
@@ -1068,7 +1129,7 @@ struct BfsGraph {
   unsigned long long* cnt = nullptr;
   int64_t *rowstart = nullptr, *S = nullptr, *part = nullptr;
   uint8_t* lv = nullptr;  // relabelled graph: byte levels by new id (never cleared)
-  int32_t* samp = nullptr;  // relabelled graph: column samples of the push matrix
+  const int32_t* samp = nullptr;  // relabelled graph: column samples (OrderedAux)
   int64_t* queue = nullptr;  // stamp queue of the long lists (4 x int64 per list)
   int64_t reach = 0;         // relabelled graph: vertices >= reach have no in-edges
   BfsState* st = nullptr;
@@ -1283,7 +1344,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
 // path cannot be used (the caller then runs the host-driven loop).
 
 static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
-                               const uint32_t* nonempty, const int32_t* rank, int64_t source, int64_t cap,
+                               const uint32_t* nonempty, const int32_t* rank, const OrderedAux* aux, int64_t source, int64_t cap,
                                double ratio, int32_t policy, int64_t* levels, int32_t* log_dir,
                                int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   void** slot = ctx_slot(ctx, SLOT_BFS_GRAPH, bfs_graph_free);
@@ -1312,8 +1373,6 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
     const size_t o_q = take(32 * (size_t)stamp_queue_cap(push->nnz));
     const size_t o_lv = rank ? take((size_t)n) : 0;
-    const int64_t ns = (push->nnz + kSampleStride - 1) / kSampleStride;
-    const size_t o_samp = rank ? take(4 * (size_t)ns) : 0;
     if (cudaMalloc(&G->mem, off) != cudaSuccess) {
       cudaGetLastError();
       delete G;
@@ -1334,18 +1393,8 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->queue = (int64_t*)(m + o_q);
     G->st = (BfsState*)(m + o_st);
     G->lv = rank ? (uint8_t*)(m + o_lv) : nullptr;
-    G->samp = rank ? (int32_t*)(m + o_samp) : nullptr;
-    if (rank && ns > 0)
-      sample_columns<<<grid_for(ctx, ns, 256, 8), 256, 0, stream_of(ctx)>>>(ns, push->indices,
-                                                                          G->samp);
-    G->reach = n;
-    if (rank) {
-      reach_limit<<<1, 1, 0, stream_of(ctx)>>>(n, pull->offsets, G->part);
-      if (read_i64(ctx, G->part, &G->reach) != GB_OK) {
-        bfs_graph_free(G);
-        return GB_ERR_CUDA;
-      }
-    }
+    G->samp = aux ? aux->samp : nullptr;
+    G->reach = aux ? aux->reach : n;
     cudaStream_t cs[4];
     for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
     const cudaError_t e = bfs_graph_build(ctx, G, cs);
@@ -1455,7 +1504,7 @@ constexpr gb_status kTooDeep = -1000;  // internal: byte levels would saturate
 
 template <class LT>
 static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
-                               const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
+                               const uint32_t* pull_nonempty, const int32_t* rank, const OrderedAux* aux, int64_t source,
                                int64_t max_iters, double ratio, int32_t policy, int64_t* levels_out,
                                int32_t* log_dir, int64_t* log_nvals, int64_t* log_est,
                                int64_t* iters_out) {
@@ -1473,13 +1522,7 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     source = r;
     levels = ar.alloc<LT>(n);
   }
-  int64_t reach = n;
-  if (rank && pull) {
-    int64_t* tmp = ar.alloc<int64_t>(1);
-    GB_ARENA_CHECK(ctx, ar);
-    reach_limit<<<1, 1, 0, s>>>(n, pull->offsets, tmp);
-    GB_TRY(read_i64(ctx, tmp, &reach));
-  }
+  const int64_t reach = aux ? aux->reach : n;
   uint32_t* vbm = ar.alloc<uint32_t>(W);
   uint32_t* fbm[2] = {ar.alloc<uint32_t>(W), ar.alloc<uint32_t>(W)};
   int32_t* F = ar.alloc<int32_t>(n);
@@ -1489,10 +1532,9 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   // push scratch of the ordered path (same kernels as the graph engine)
   const bool ordered_push = rank && !push_smem_enabled();
   int64_t *rowstart = nullptr, *Sx = nullptr, *part = nullptr, *tbase = nullptr, *queue = nullptr;
-  int32_t *tfirst = nullptr, *samp = nullptr;
-  const int64_t ns = (push->nnz + kSampleStride - 1) / kSampleStride;
+  int32_t* tfirst = nullptr;
+  const int32_t* samp = aux && use_samples() ? aux->samp : nullptr;
   if (ordered_push) {
-    if (use_samples() && ns > 0) samp = ar.alloc<int32_t>(ns);
     rowstart = ar.alloc<int64_t>(n + 1);
     Sx = ar.alloc<int64_t>(n + 1);
     part = ar.alloc<int64_t>(kGScanBlocks + 1);
@@ -1501,10 +1543,6 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     tbase = ar.alloc<int64_t>(push->nnz / kWarpTile + 2);
   }
   GB_ARENA_CHECK(ctx, ar);
-  if (samp) {  // rebuilt per call here; the graph engine keeps them with the graph
-    sample_columns<<<grid_for(ctx, ns, 256, 8), 256, 0, s>>>(ns, push->indices, samp);
-    count_launch(ctx, 1);
-  }
   GB_CUDA(ctx, cudaMemsetAsync(levels, 0, sizeof(LT) * n, s));
   GB_CUDA(ctx, cudaMemsetAsync(vbm, 0, sizeof(uint32_t) * W, s));
   GB_CUDA(ctx, cudaMemsetAsync(fbm[0], 0, sizeof(uint32_t) * W, s));
@@ -1632,31 +1670,33 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                          int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   const int64_t n = push->nrows;
   if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
+  const OrderedAux* aux = nullptr;
+  if (rank) GB_TRY(ordered_aux(ctx, push, pull, &aux));
   // Device-driven loop (one graph launch) unless profiling per kernel, the
   // pull orientation is missing (the host loop reports that error when pull
   // is chosen), or the engine is pinned (gb_bfs_engine; GB_BFS_GRAPH=0).
   if (pull && bfs_engine_current() == kEngineGraph && !prof_enabled(ctx) && max_iters >= 1 &&
       max_iters <= kGraphMaxCap) {
-    const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, source, max_iters,
+    const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, aux, source, max_iters,
                                        ratio, policy, levels_out, log_dir, log_nvals, log_est,
                                        iters_out);
     // byte levels saturate: a relabelled run this deep is redone with int32
     const bool deep = st == GB_OK && rank && *iters_out >= kByteLevelIters;
     if (deep)
-      return bfs_host_loop<int32_t>(ctx, push, pull, pull_nonempty, rank, source, max_iters,
+      return bfs_host_loop<int32_t>(ctx, push, pull, pull_nonempty, rank, aux, source, max_iters,
                                     ratio, policy, levels_out, log_dir, log_nvals, log_est,
                                     iters_out);
     if (st != GB_ERR_UNSUPPORTED) return st;
   }
   if (rank) {
-    const gb_status st = bfs_host_loop<uint8_t>(ctx, push, pull, pull_nonempty, rank, source,
+    const gb_status st = bfs_host_loop<uint8_t>(ctx, push, pull, pull_nonempty, rank, aux, source,
                                                 max_iters, ratio, policy, levels_out, log_dir,
                                                 log_nvals, log_est, iters_out);
     if (st != kTooDeep) return st;
-    return bfs_host_loop<int32_t>(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio,
+    return bfs_host_loop<int32_t>(ctx, push, pull, pull_nonempty, rank, aux, source, max_iters, ratio,
                                   policy, levels_out, log_dir, log_nvals, log_est, iters_out);
   }
-  return bfs_host_loop<int64_t>(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio,
+  return bfs_host_loop<int64_t>(ctx, push, pull, pull_nonempty, rank, aux, source, max_iters, ratio,
                                 policy, levels_out, log_dir, log_nvals, log_est, iters_out);
 }
 
