@@ -13,7 +13,7 @@ GB_BFS_GRAPH=0 $NCU --metrics gpu__time_duration.sum --csv --log-file gpurun_out
 # one call of each algorithm inside a profiler window
 for spec in "bfs 24" "cc 24" "pr 22" "sssp 20" "tc 20" "mxvm 24"; do
   set -- $spec
-  GB_BFS_GRAPH=0 $NCU --profile-from-start off --metrics gpu__time_duration.sum --csv \
+  GB_BFS_GRAPH=0 $NCU $( [ $1 = bfs ] && echo --cache-control none ) --profile-from-start off --metrics gpu__time_duration.sum --csv \
     --log-file gpurun_out/launches_$1.csv python tools/prof_bfs.py --algo $1 --scale $2 > /dev/null 2>&1
 done
 # full captures of each algorithm's dominant kernel
