@@ -857,35 +857,40 @@ __device__ __forceinline__ void scan_partials_body(int64_t K, const int32_t* F,
     const int64_t v = F[k];
     int64_t a = __ldg(off + v);
     const int64_t b = __ldg(off + v + 1);
-    if (X > 0 && b - a >= clo && b - a <= chi && __ldg(idx + a) < X) {
-      if (__ldg(idx + b - 1) < X) {
-        a = b;
-      } else {  // first position in (a, b-1] holding a column >= X
-        int64_t l = a + 1, h = b - 1;
-        if (samp) {
-          // narrow to one 32-entry line through the column samples
-          // (samp[j] = idx[32 j]): the samples of a 512-entry list share
-          // one line, so ~2 lines are touched instead of ~6
-          int64_t jl = (l + kSampleStride - 1) / kSampleStride, jh = h / kSampleStride;
-          if (jl <= jh) {
-            if (__ldg(samp + jh) < X) {
-              l = jh * kSampleStride + 1;  // the cut lies after the last sample
-            } else {
-              while (jl < jh) {  // first sample >= X
-                const int64_t m = (jl + jh) >> 1;
-                if (__ldg(samp + m) < X) jl = m + 1; else jh = m;
-              }
-              h = jh * kSampleStride;
-              const int64_t lp = h - kSampleStride + 1;
-              if (lp > l) l = lp;
-            }
+    if (X > 0 && b - a >= clo && b - a <= chi) {
+      if (samp) {
+        // lower bound of X in [a, b) narrowed through the column samples
+        // (samp[j] = idx[32 j]): a search over the list's samples (one line
+        // for a 512-entry list), then one 32-entry line of the list -- ~3
+        // random lines per entry with the offsets, against ~6 for a plain
+        // binary search (this search is DRAM-bound)
+        int64_t l = a, h = b;
+        const int64_t jl = (a + kSampleStride - 1) / kSampleStride, jh = (b - 1) / kSampleStride;
+        if (jl <= jh) {
+          int64_t ql = jl, qh = jh + 1;  // first sample >= X, or jh + 1
+          while (ql < qh) {
+            const int64_t m = (ql + qh) >> 1;
+            if (__ldg(samp + m) < X) ql = m + 1; else qh = m;
           }
+          if (ql <= jh) h = ql * kSampleStride;
+          if (ql > jl) l = (ql - 1) * kSampleStride + 1;
         }
         while (l < h) {
           const int64_t m = (l + h) >> 1;
           if (__ldg(idx + m) < X) l = m + 1; else h = m;
         }
         a = l;
+      } else if (__ldg(idx + a) < X) {
+        if (__ldg(idx + b - 1) < X) {
+          a = b;
+        } else {  // first position in (a, b-1] holding a column >= X
+          int64_t l = a + 1, h = b - 1;
+          while (l < h) {
+            const int64_t m = (l + h) >> 1;
+            if (__ldg(idx + m) < X) l = m + 1; else h = m;
+          }
+          a = l;
+        }
       }
     }
     rowstart[k] = a;
