@@ -397,18 +397,20 @@ __device__ __forceinline__ void prefix_flush(int64_t wmin, unsigned long long* x
   if (threadIdx.x == 0 && s_min != ~0ull) atomicMin(xmin, s_min);
 }
 
-// The level stored for a vertex: byte levels (relabelled runs) saturate at
-// 255; a run that deep is redone with int32 levels (bfs_run).
+// The level stored for a vertex: 16-bit levels (relabelled runs) saturate at
+// 65535; a run that deep is redone with int32 levels (bfs_run).
 template <class LT>
 __device__ __forceinline__ LT level_of(int64_t depth) {
-  if constexpr (sizeof(LT) == 1) return (LT)(depth < 255 ? depth : 255);
+  if constexpr (sizeof(LT) == 2) return (LT)(depth < 65535 ? depth : 65535);
   else return (LT)depth;
 }
-constexpr int64_t kByteLevelIters = 250;  // deeper runs use int32 internal levels
+// a relabelled run of this many levels is redone with int32 internal levels;
+// loop caps up to it cannot saturate (the asynchronous entry relies on that)
+constexpr int64_t kNarrowLevelIters = 65000;
 
 constexpr int kFinalizeWarps = 8;  // finalize blocks are 256 threads
 
-// LT: int64 levels (the API vector) or byte levels (a relabelled run; int32
+// LT: int64 levels (the API vector) or 16-bit levels (a relabelled run; int32
 // when it is deeper than 250 levels)
 template <class LT>
 __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t* vbm,
@@ -738,7 +740,7 @@ struct BfsState {
   double ratio;         // per call
   int32_t policy, pad_;
   int64_t* out;         // per call, relabelled graphs: levels by original id
-  uint8_t* lv8;         // relabelled graphs: internal (byte) levels by new id
+  uint16_t* lv16;       // relabelled graphs: internal (16-bit) levels by new id
   int64_t it, K, depth, dnext, unstamp;  // loop state
   int64_t xcur;                 // dense visited prefix at the level start (ordered graphs)
   int64_t srank;                // relabelled graphs: the source's new id
@@ -1054,7 +1056,7 @@ __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32
                         uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop) {
   const int64_t s = rank ? (int64_t)rank[st->source] : st->source;
   st->srank = s;
-  if (rank) st->lv8[s] = 1;
+  if (rank) st->lv16[s] = 1;
   else st->levels[s] = 1;
   const uint32_t bit = 1u << (s & 31);
   vbm[s >> 5] |= bit;
@@ -1112,10 +1114,10 @@ __global__ void g_unstamp(const BfsState* __restrict__ st, const int32_t* __rest
   if (!st->unstamp) return;
   const int64_t K = st->K;
   int64_t* lv = st->levels;
-  uint8_t* lv8 = st->lv8;
+  uint16_t* lv16 = st->lv16;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (lv8) lv8[F[i]] = 0;
+    if (lv16) lv16[F[i]] = 0;
     else lv[F[i]] = 0;
   }
 }
@@ -1133,7 +1135,7 @@ struct BfsGraph {
   int64_t* tile_base = nullptr;
   unsigned long long* cnt = nullptr;
   int64_t *rowstart = nullptr, *S = nullptr, *part = nullptr;
-  uint8_t* lv = nullptr;  // relabelled graph: byte levels by new id (never cleared)
+  uint16_t* lv = nullptr;  // relabelled graph: 16-bit levels by new id
   const int32_t* samp = nullptr;  // relabelled graph: column samples (OrderedAux)
   int64_t* queue = nullptr;  // stamp queue of the long lists (4 x int64 per list)
   int64_t reach = 0;         // relabelled graph: vertices >= reach have no in-edges
@@ -1189,7 +1191,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   G->launches_push = 4 + (push_dead ? 0 : 1);
   const int grid_stamp = grid_for(ctx, (int64_t)1 << 40, 256, 8);
   G->launches_pull = pull_dead ? 3 : 1;
-  // 4 memsets, zero levels (or clear byte levels + unpermute), start, unstamp
+  // 4 memsets, zero levels (or clear 16-bit levels + unpermute), start, unstamp
   G->launches_fixed = ordered ? 9 : 8;
 
   auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
@@ -1214,8 +1216,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
                                          ordered && prefix_mode() == 2 ? dptr(&st->xcur) : dval(0));
     }
     if (ordered)
-      bfs_finalize<uint8_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev,
-                                                   G->fbm[h ^ 1], pptr(&st->lv8), G->F, G->cnt + h,
+      bfs_finalize<uint16_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev,
+                                                   G->fbm[h ^ 1], pptr(&st->lv16), G->F, G->cnt + h,
                                                    G->cnt + (h ^ 1), nullptr, &st->xnext);
     else
       bfs_finalize<int64_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), G->vbm, G->vprev,
@@ -1230,9 +1232,9 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       GB_GTRY(cudaMemsetAsync(G->cnt + (h ^ 1), 0, 8, s));
     } else {
       if (ordered)
-        bfs_pull<uint8_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices,
+        bfs_pull<uint16_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices,
                                                  pull_on, G->nonempty, G->vbm, G->vprev, G->fbm[h],
-                                                 G->fbm[h ^ 1], pptr(&st->lv8), G->F, G->cnt + h,
+                                                 G->fbm[h ^ 1], pptr(&st->lv16), G->F, G->cnt + h,
                                                  G->cnt + (h ^ 1), 0, (W + 31) / 32, &st->xnext);
       else
         bfs_pull<int64_t><<<grid_w, 256, 0, s>>>(n, dptr(&st->dnext), pull.offsets, pull.indices,
@@ -1283,10 +1285,10 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     GB_GTRY(cudaMemsetAsync(G->vprev, 0, sizeof(uint32_t) * W, s));
     GB_GTRY(cudaMemsetAsync(G->fbm[0], 0, sizeof(uint32_t) * W, s));
     GB_GTRY(cudaMemsetAsync(G->cnt, 0, 16, s));
-    // the API levels (int64) or the internal byte levels of a relabelled run
+    // the API levels (int64) or the internal 16-bit levels of a relabelled run
     // start at 0: unvisited vertices read 0
     if (!ordered) g_zero_levels<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, st);
-    else GB_GTRY(cudaMemsetAsync(G->lv, 0, (size_t)n, s));  // unvisited read level 0
+    else GB_GTRY(cudaMemsetAsync(G->lv, 0, 2 * (size_t)n, s));  // unvisited read level 0
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
@@ -1377,7 +1379,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     const size_t o_cnt = take(32), o_rs = take(8 * (size_t)(n + 1)), o_S = take(8 * (size_t)(n + 1));
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
     const size_t o_q = take(32 * (size_t)stamp_queue_cap(push->nnz));
-    const size_t o_lv = rank ? take((size_t)n) : 0;
+    const size_t o_lv = rank ? take(2 * (size_t)n) : 0;
     if (cudaMalloc(&G->mem, off) != cudaSuccess) {
       cudaGetLastError();
       delete G;
@@ -1397,7 +1399,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->part = (int64_t*)(m + o_part);
     G->queue = (int64_t*)(m + o_q);
     G->st = (BfsState*)(m + o_st);
-    G->lv = rank ? (uint8_t*)(m + o_lv) : nullptr;
+    G->lv = rank ? (uint16_t*)(m + o_lv) : nullptr;
     G->samp = aux ? aux->samp : nullptr;
     G->reach = aux ? aux->reach : n;
     cudaStream_t cs[4];
@@ -1427,7 +1429,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   GB_ARENA_CHECK(ctx, ar);
   BfsState h{};
   h.levels = rank ? nullptr : levels;
-  h.lv8 = rank ? G->lv : nullptr;
+  h.lv16 = rank ? G->lv : nullptr;
   h.out = levels;
   h.log = log;
   h.source = source;
@@ -1505,7 +1507,7 @@ static int bfs_engine_current() {
   return g_bfs_engine;
 }
 
-constexpr gb_status kTooDeep = -1000;  // internal: byte levels would saturate
+constexpr gb_status kTooDeep = -1000;  // internal: 16-bit levels would saturate
 
 template <class LT>
 static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
@@ -1566,8 +1568,8 @@ static gb_status bfs_host_loop(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   int64_t K = 1, depth = 1, iters = 0;
   int cur = 0;
   for (int64_t it = 0; it < max_iters; ++it) {
-    if constexpr (sizeof(LT) == 1) {
-      if (it >= kByteLevelIters) return kTooDeep;
+    if constexpr (sizeof(LT) == 2) {
+      if (it >= kNarrowLevelIters) return kTooDeep;
     }
     int64_t est = 0;
     const int32_t dir = gb_decide_direction(push->nnz, push->nrows, K, ratio, policy, &est);
@@ -1685,8 +1687,8 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, aux, source, max_iters,
                                        ratio, policy, levels_out, log_dir, log_nvals, log_est,
                                        iters_out);
-    // byte levels saturate: a relabelled run this deep is redone with int32
-    const bool deep = st == GB_OK && rank && *iters_out >= kByteLevelIters;
+    // 16-bit levels saturate: a relabelled run this deep is redone with int32
+    const bool deep = st == GB_OK && rank && *iters_out >= kNarrowLevelIters;
     if (deep)
       return bfs_host_loop<int32_t>(ctx, push, pull, pull_nonempty, rank, aux, source, max_iters,
                                     ratio, policy, levels_out, log_dir, log_nvals, log_est,
@@ -1694,7 +1696,7 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
     if (st != GB_ERR_UNSUPPORTED) return st;
   }
   if (rank) {
-    const gb_status st = bfs_host_loop<uint8_t>(ctx, push, pull, pull_nonempty, rank, aux, source,
+    const gb_status st = bfs_host_loop<uint16_t>(ctx, push, pull, pull_nonempty, rank, aux, source,
                                                 max_iters, ratio, policy, levels_out, log_dir,
                                                 log_nvals, log_est, iters_out);
     if (st != kTooDeep) return st;

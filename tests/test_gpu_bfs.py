@@ -175,21 +175,32 @@ def test_bfs_graph_long_path(gb):
         assert np.array_equal(g, h) and t1 == t2 and len(t1) == cap
 
 
-def test_bfs_deep_levels_past_byte_range(gb):
-    """Relabelled runs keep byte levels and redo runs of >= 250 levels with
-    int32 levels: both engines, around the switch and the 255 saturation."""
+def test_bfs_deep_levels_past_narrow_range(gb):
+    """Relabelled runs keep 16-bit levels and redo runs of >= 65,000 levels
+    with int32 levels: both engines, around the switch and the saturation."""
+    n = 65600
+    r = np.r_[np.arange(n - 1), np.arange(1, n)]
+    c = np.r_[np.arange(1, n), np.arange(n - 1)]
+    A = gb.SparseMatrix.from_tuples(r, c, np.ones(r.size, np.int64), n, n)
+    for cap in (70000, 65001):
+        g, h, t1, t2 = _run_both(gb, A, 0, max_niter=cap)
+        want = np.arange(1, n + 1)
+        want[cap:] = 0
+        assert np.array_equal(g, want), cap
+        assert np.array_equal(g, h) and t1 == t2, cap
+
+
+def test_bfs_deep_levels_with_a_shortcut(gb):
     from oracle import port
     n = 700
     r = np.r_[np.arange(n - 1), np.arange(1, n), [0, 5]]
     c = np.r_[np.arange(1, n), np.arange(n - 1), [5, 0]]
     A = gb.SparseMatrix.from_tuples(r, c, np.ones(r.size, np.int64), n, n)
     P = port.mat_from_tuples(r, c, np.ones(r.size, np.int64), n, n)
-    for src, cap in ((0, None), (350, None), (0, 249), (0, 250), (0, 251), (0, 254),
-                     (0, 255), (0, 256), (0, 400)):
+    for src, cap in ((0, None), (350, None), (0, 249), (0, 256), (0, 400)):
         kw = {} if cap is None else {"max_niter": cap}
         g, h, t1, t2 = _run_both(gb, A, src, **kw)
         want = port.bfs(P, src, port.Desc(**kw)).vals
-        assert g.max() > 255 or cap is not None
         assert np.array_equal(g, want), (src, cap)
         assert np.array_equal(g, h) and t1 == t2, (src, cap)
 
