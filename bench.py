@@ -357,8 +357,14 @@ def run_ours(args):
         def step():
             return runner(args.source)
     else:
+        # bfs() enqueues without a host sync; each call's decision log is read
+        # after the timed region (it books the call's kernel launches)
+        descs = []
+
         def step():
-            return gb.bfs(A, args.source)
+            d = gb.Descriptor()
+            descs.append(d)
+            return gb.bfs(A, args.source, desc=d)
 
     for _ in range(max(args.warmup, 3)):
         lv = step()
@@ -379,6 +385,10 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+    if world == 1:
+        for d in descs[-args.steps:]:
+            assert len(d.direction_log) > 0
+        descs.clear()
     launches = (ctx.launches() - launches0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:

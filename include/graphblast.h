@@ -444,6 +444,26 @@ gb_status gb_bfs_ordered(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                          int64_t* levels, int32_t* log_dir_host, int64_t* log_nvals_host,
                          int64_t* log_est_host, int64_t* iters_host);
 
+/* Asynchronous gb_bfs_ordered (same algorithm and results): enqueues the run
+ * on the context stream and returns without synchronising when the device
+ * loop can run it (otherwise it runs synchronously).  log_dev: device buffer
+ * of 1 + 3*max_iters int64 receiving [iters, (dir, frontier, estimate) x
+ * iters]; log_host: pinned host buffer of 1 + 3*21 int64 that receives the
+ * first 1 + 3*min(iters, 21) entries in stream order -- synchronise the
+ * stream before reading it, and read entries past 21 decisions from log_dev.  launch_info[3] = launches of the
+ * fixed part, of one push level and of one pull level (0 on the synchronous
+ * path); pass the total to gb_count_launches once the log is read.  Replaces
+ * the synchronous return of algorithms.py:48-77 + the direction_log appends
+ * of kernels.py:303-304, resolved lazily by the host. */
+gb_status gb_bfs_ordered_async(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                               const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
+                               int64_t max_iters, double switch_ratio, int32_t policy,
+                               int64_t* levels, int64_t* log_dev, int64_t* log_host,
+                               int64_t* launch_info);
+
+/* Adds n to the context's launch counter (asynchronous entries). */
+void gb_count_launches(gb_ctx* ctx, int64_t n);
+
 /* ----------------------------------------------------------------------------
  * measurement support (bench.py)
  * --------------------------------------------------------------------------*/

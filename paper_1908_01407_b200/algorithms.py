@@ -16,13 +16,14 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import weakref
 
 import numpy as np
 import torch
 
 from . import _lib
 from .algebra import LESS, MINUS, TIMES, builtin_monoid, builtin_semiring
-from .containers import INDEX_DTYPE, Descriptor, Direction, SparseMatrix, Vector, empty
+from .containers import INDEX_DTYPE, DecisionLog, Descriptor, Direction, SparseMatrix, Vector, empty
 from .errors import ShapeError
 from .kernels import (
     DirectionDecision,
@@ -65,6 +66,101 @@ def _require_symmetric(A):
         raise ValueError("adjacency matrix must be symmetric (undirected graph)")
 
 
+_ASYNC_CAP = 65000   # loop caps the asynchronous entry accepts (16-bit device levels)
+# GB_BFS_ASYNC=0: every bfs() call synchronises and fills the log eagerly
+_ASYNC_BFS = os.environ.get("GB_BFS_ASYNC", "1") != "0"
+_LOG_PREFIX = 21     # decisions gb_bfs_ordered_async copies to the pinned log
+
+
+class _PendingBfs:
+    """Resolver of one asynchronous bfs: waits for it, then returns its
+    DirectionDecision list (and books its kernel launches).  Its log lives in
+    a slot of the context's ring (pinned prefix + device buffer); the slot is
+    settled -- copied out -- before the ring reuses it."""
+
+    def __init__(self, ctx, A, switch_ratio, info):
+        self.ctx = ctx
+        self.total = A.nnz
+        self.thr = A.nnz * switch_ratio
+        self.info = info
+        self.row = None
+        self.dev = None
+        self.event = None
+        self.raw = None
+
+    def settle(self):
+        if self.raw is None:
+            self.event.synchronize()
+            raw = self.row.numpy().copy()
+            iters = int(raw[0])
+            if iters > _LOG_PREFIX:
+                tail = self.dev[1 + 3 * _LOG_PREFIX:1 + 3 * iters].cpu().numpy()
+                raw = np.concatenate([raw, tail])
+            self.raw = raw
+            self.row = self.dev = None
+
+    def __call__(self):
+        self.settle()
+        raw = self.raw
+        iters = int(raw[0])
+        dirs = raw[1:1 + 3 * iters:3]
+        info = self.info
+        if info[0]:
+            npush = int(np.count_nonzero(dirs == _lib.DIR_PUSH))
+            self.ctx.lib.gb_count_launches(self.ctx.ptr, int(info[0] + npush * info[1] +
+                                                            (iters - npush) * info[2]))
+        return [DirectionDecision("pull" if dirs[i] == _lib.DIR_PULL else "push",
+                                  int(raw[2 + 3 * i]), int(raw[3 + 3 * i]), self.total, self.thr)
+                for i in range(iters)]
+
+
+class _LogRing:
+    """Log buffers of asynchronous bfs calls, allocated once per context and
+    reused round robin: a pinned prefix row and a device log per slot (pinning
+    or allocating per call costs milliseconds and can synchronise)."""
+
+    SLOTS = 256
+
+    def __init__(self, device):
+        self.pin = torch.empty((self.SLOTS, 1 + 3 * _LOG_PREFIX), dtype=torch.int64,
+                               pin_memory=True)
+        self.dev = None
+        self.device = device
+        self.owner = [None] * self.SLOTS
+        self.next = 0
+
+    def _settle(self, i):
+        prev = self.owner[i]() if self.owner[i] is not None else None
+        if prev is not None:
+            prev.settle()
+        self.owner[i] = None
+
+    def take(self, pending, cap):
+        need = 1 + 3 * cap
+        if self.dev is None or self.dev.shape[1] < need:
+            for i in range(self.SLOTS):  # a longer loop cap: grow every slot once
+                self._settle(i)
+            self.dev = torch.empty((self.SLOTS, max(need, 1 + 3 * 10_000)), dtype=torch.int64,
+                                   device=self.device)
+        i = self.next
+        self.next = (i + 1) % self.SLOTS
+        self._settle(i)
+        self.owner[i] = weakref.ref(pending)
+        pending.row = self.pin[i]
+        pending.dev = self.dev[i]
+        return self.pin[i], self.dev[i]
+
+
+_rings = {}
+
+
+def _log_ring(ctx, device):
+    ring = _rings.get(id(ctx))
+    if ring is None:
+        ring = _rings[id(ctx)] = _LogRing(device)
+    return ring
+
+
 def _log_decisions(desc, A, dirs, nvals, ests, count):
     total = A.nnz
     thr = total * desc.switch_ratio
@@ -97,6 +193,24 @@ def bfs(A: SparseMatrix, source: int, desc=None, early_exit=True) -> Vector:
     est = np.zeros(cap, np.int64)
     done = C.c_int64(0)
     trav = A.traversal() if _ORDERED_BFS else None
+    if (trav is not None and _ASYNC_BFS and isinstance(desc.direction_log, DecisionLog)
+            and cap < _ASYNC_CAP):
+        # degree-ordered relabelling, enqueued without a host
+        # synchronisation: the decision log is read when first used
+        push_o, pull_o, rank = trav
+        (push, _k1), (pull, _k2) = push_o.csr_struct(), pull_o.csr_struct()
+        ctx = _lib.context()
+        info = np.zeros(3, np.int64)
+        pending = _PendingBfs(ctx, A, desc.switch_ratio, info)
+        log_pin, log_dev = _log_ring(ctx, levels.device).take(pending, cap)
+        ctx.call("gb_bfs_ordered_async", C.byref(push), C.byref(pull), _lib.ptr(pull_o.nonempty()),
+                 _lib.ptr(rank), int(source), int(iters), float(desc.switch_ratio),
+                 _POLICY[desc.direction], _lib.ptr(levels), _lib.ptr(log_dev),
+                 C.c_void_p(log_pin.data_ptr()), info.ctypes.data_as(C.c_void_p))
+        pending.event = torch.cuda.Event()
+        pending.event.record()
+        desc.direction_log._defer(pending)
+        return Vector._wrap(n, None, levels, 0, np.int64)
     if trav is not None:
         # degree-ordered relabelling: same levels and log
         push_o, pull_o, rank = trav

@@ -75,6 +75,55 @@ class Counters:
         self.semiring_adds += other.semiring_adds
 
 
+class DecisionLog(list):
+    """The direction log (a list of DirectionDecision, kernels.py:303-304).
+
+    An asynchronous device call (``bfs``) appends a pending resolver instead
+    of its decisions; any read or further append first waits for the pending
+    calls in order and materialises their decisions, so the log always reads
+    exactly like the reference's eagerly filled list.
+    """
+
+    __slots__ = ("_pending",)
+
+    def __init__(self, *args):
+        super().__init__(*args)
+        self._pending = []
+
+    def _defer(self, resolve):
+        self._pending.append(resolve)
+
+    def _flush(self):
+        if self._pending:
+            pending, self._pending = self._pending, []
+            for resolve in pending:
+                list.extend(self, resolve())
+
+    def __reduce_ex__(self, protocol):
+        self._flush()
+        return (DecisionLog, (list(self),))
+
+
+def _flushing(name):
+    base = getattr(list, name)
+
+    def method(self, *args, **kwargs):
+        self._flush()
+        return base(self, *args, **kwargs)
+
+    method.__name__ = name
+    return method
+
+
+for _name in ("__len__", "__iter__", "__getitem__", "__setitem__", "__delitem__", "__contains__",
+              "__reversed__", "__eq__", "__ne__", "__lt__", "__le__", "__gt__", "__ge__",
+              "__repr__", "__add__", "__iadd__", "__mul__", "__rmul__", "__imul__", "append",
+              "extend", "insert", "pop", "remove", "clear", "index", "count", "copy", "sort",
+              "reverse"):
+    setattr(DecisionLog, _name, _flushing(_name))
+DecisionLog.__hash__ = None
+
+
 @dataclass
 class Descriptor:
     """Per-call modifiers (containers.py:74-113).
@@ -96,7 +145,7 @@ class Descriptor:
     partition: Partition = Partition.NONZERO_SPLIT
     early_exit: bool = False
     counters: Counters = field(default_factory=Counters)
-    direction_log: list = field(default_factory=list)
+    direction_log: list = field(default_factory=DecisionLog)
     fused: bool = True
 
     _TOGGLES = {"mask": "mask_mode", "inp0": "transpose_inp0", "inp1": "transpose_inp1"}

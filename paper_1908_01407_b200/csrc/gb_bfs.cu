@@ -1350,10 +1350,18 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
 // Returns GB_OK after running the BFS, or GB_ERR_UNSUPPORTED when the graph
 // path cannot be used (the caller then runs the host-driven loop).
 
+// Asynchronous form (log_ext != NULL): the device writes the raw log
+// [iters, (dir, K, est) x iters] to log_ext, its first kLogPrefix decisions
+// are copied to the pinned log_pin behind the graph on the stream, and the
+// call returns without synchronising; launch_info receives the launches of
+// the fixed part and of one push / pull level.
+constexpr int64_t kLogPrefix = 21;
 static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                                const uint32_t* nonempty, const int32_t* rank, const OrderedAux* aux, int64_t source, int64_t cap,
                                double ratio, int32_t policy, int64_t* levels, int32_t* log_dir,
-                               int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
+                               int64_t* log_nvals, int64_t* log_est, int64_t* iters_out,
+                               int64_t* log_ext = nullptr, int64_t* log_pin = nullptr,
+                               int64_t* launch_info = nullptr) {
   void** slot = ctx_slot(ctx, SLOT_BFS_GRAPH, bfs_graph_free);
   BfsGraph* G = static_cast<BfsGraph*>(*slot);
   if (G && !(same_csr(G->push, *push) && same_csr(G->pull, *pull) && G->nonempty == nonempty &&
@@ -1425,7 +1433,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   }
   cudaStream_t s = stream_of(ctx);
   Arena ar(ctx);
-  int64_t* log = ar.alloc<int64_t>(1 + 3 * cap);
+  int64_t* log = log_ext ? log_ext : ar.alloc<int64_t>(1 + 3 * cap);
   GB_ARENA_CHECK(ctx, ar);
   BfsState h{};
   h.levels = rank ? nullptr : levels;
@@ -1439,9 +1447,17 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   // the state block's per-call head (everything before the loop state)
   GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(BfsState, it), cudaMemcpyHostToDevice, s));
   GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
+  const int64_t first = cap < kLogPrefix ? cap : kLogPrefix;
+  if (log_ext) {
+    GB_CUDA(ctx, cudaMemcpyAsync(log_pin, log, sizeof(int64_t) * (1 + 3 * first),
+                                 cudaMemcpyDeviceToHost, s));
+    launch_info[0] = G->launches_fixed;
+    launch_info[1] = 2 + G->launches_push;
+    launch_info[2] = 2 + G->launches_pull;
+    return GB_OK;
+  }
   // one readback: iteration count and up to 21 decisions
   int64_t* pin = pinned_slots(ctx);
-  const int64_t first = cap < 21 ? cap : 21;
   GB_CUDA(ctx, cudaMemcpyAsync(pin, log, sizeof(int64_t) * (1 + 3 * first), cudaMemcpyDeviceToHost, s));
   GB_CUDA(ctx, cudaStreamSynchronize(s));
   const int64_t iters = pin[0];
@@ -1734,6 +1750,53 @@ gb_status gb_bfs_ordered(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
   return bfs_run(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio, policy, levels,
                  log_dir, log_nvals, log_est, iters_out);
 }
+
+gb_status gb_bfs_ordered_async(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                               const uint32_t* pull_nonempty, const int32_t* rank, int64_t source,
+                               int64_t max_iters, double ratio, int32_t policy, int64_t* levels,
+                               int64_t* log_dev, int64_t* log_host, int64_t* launch_info) {
+  if (!rank) return set_error(ctx, GB_ERR_ARG, "gb_bfs_ordered_async needs the vertex rank array");
+  const int64_t n = push->nrows;
+  if (source < 0 || source >= n)
+    return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
+  if (max_iters < 1) return set_error(ctx, GB_ERR_ARG, "max_iters must be >= 1");
+  // the graph engine, with a loop cap its 16-bit levels cannot exceed
+  if (pull && bfs_engine_current() == kEngineGraph && !prof_enabled(ctx) &&
+      max_iters <= kGraphMaxCap && max_iters < kNarrowLevelIters) {
+    const OrderedAux* aux = nullptr;
+    GB_TRY(ordered_aux(ctx, push, pull, &aux));
+    int64_t iters = 0;
+    const gb_status st = bfs_graph_run(ctx, push, pull, pull_nonempty, rank, aux, source,
+                                       max_iters, ratio, policy, levels, nullptr, nullptr,
+                                       nullptr, &iters, log_dev, log_host, launch_info);
+    if (st != GB_ERR_UNSUPPORTED) return st;
+  }
+  // otherwise synchronously: the raw log to log_dev, its prefix to log_host
+  std::vector<int32_t> dir(max_iters);
+  std::vector<int64_t> nv(max_iters), est(max_iters);
+  int64_t iters = 0;
+  GB_TRY(bfs_run(ctx, push, pull, pull_nonempty, rank, source, max_iters, ratio, policy, levels,
+                 dir.data(), nv.data(), est.data(), &iters));
+  std::vector<int64_t> raw(1 + 3 * iters);
+  raw[0] = iters;
+  for (int64_t i = 0; i < iters; ++i) {
+    raw[1 + 3 * i] = dir[i];
+    raw[2 + 3 * i] = nv[i];
+    raw[3 + 3 * i] = est[i];
+  }
+  const int64_t first = iters < kLogPrefix ? iters : kLogPrefix;
+  for (int64_t i = 0; i < 1 + 3 * first; ++i) log_host[i] = raw[i];
+  GB_CUDA(ctx, cudaMemcpyAsync(log_dev, raw.data(), sizeof(int64_t) * raw.size(),
+                               cudaMemcpyHostToDevice, stream_of(ctx)));
+  GB_CUDA(ctx, cudaStreamSynchronize(stream_of(ctx)));
+  // the synchronous path counted its own launches
+  launch_info[0] = 0;
+  launch_info[1] = 0;
+  launch_info[2] = 0;
+  return GB_OK;
+}
+
+void gb_count_launches(gb_ctx* ctx, int64_t n) { count_launch(ctx, (int)n); }
 
 // ---------------------------------------------------------------------------
 // 1D-partitioned BFS steps (one rank of P; the host loop and the NCCL
