@@ -419,3 +419,22 @@ def test_bfs_engines_long_path_and_values(gb):
     for kw in ({}, {"direction": gb.Direction.FORCE_PULL}):
         (g, tg), (h, th) = _engines(gb, A, 5, **kw)
         assert np.array_equal(g, h) and tg == th
+
+
+def test_bfs_async_logs_survive_the_ring(gb, monkeypatch):
+    """bfs() returns before the device finishes; 300 calls (more than the 256
+    ring slots) keep their own levels and decision logs, equal to the
+    synchronous entry's, whatever order the logs are read in."""
+    from paper_1908_01407_b200 import algorithms
+    A = gb.io.rmat_matrix(12)
+    n = A.nrows
+    srcs = [(7 * i) % n for i in range(300)]
+    pending = [(s, gb.Descriptor()) for s in srcs]
+    outs = [gb.bfs(A, s, desc=d) for s, d in pending]
+    monkeypatch.setattr(algorithms, "_ASYNC_BFS", False)
+    for k in list(range(299, -1, -37)) + list(range(300)):
+        s, d = pending[k]
+        d2 = gb.Descriptor()
+        want = gb.bfs(A, s, desc=d2).values
+        assert np.array_equal(outs[k].values, want), k
+        assert list(d.direction_log) == list(d2.direction_log), k
