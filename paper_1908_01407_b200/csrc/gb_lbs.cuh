@@ -224,7 +224,6 @@ template <class F>
 __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* S, const int64_t* rowstart,
                                            const int32_t* tile_first, const int64_t* tile_base,
                                            F& f) {
-  const int lane = threadIdx.x & 31;
   const int64_t E = S[K];
   const int64_t ntiles = (E + kWarpTile - 1) / kWarpTile;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;

@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "gb_common.cuh"
 
@@ -124,7 +125,7 @@ static gb_status compact_t(gb_ctx* ctx, int64_t n, int64_t k, const int32_t* idx
   int64_t* pos = ar.alloc<int64_t>(len);
   int64_t* cnt = ar.alloc<int64_t>(1);
   GB_ARENA_CHECK(ctx, ar);
-  cub::CountingInputIterator<int64_t> it(0);
+  thrust::counting_iterator<int64_t> it(0);
   NotZeroAt<T> pred{vals, zero};
   size_t tb = 0;
   cub::DeviceSelect::If(nullptr, tb, it, pos, cnt, len, pred, s);
