@@ -411,7 +411,7 @@ constexpr int64_t kNarrowLevelIters = 65000;
 constexpr int kFinalizeWarps = 8;  // finalize blocks are 256 threads
 
 // LT: int64 levels (the API vector) or 16-bit levels (a relabelled run; int32
-// when it is deeper than 250 levels)
+// when it is deeper than kNarrowLevelIters levels)
 template <class LT>
 __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t* vbm,
                                               uint32_t* vprev, uint32_t* fbm_next,
