@@ -1052,8 +1052,13 @@ __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
     lv[i] = 0;
 }
 
+__device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned long long* c,
+                            cudaGraphConditionalHandle h_push);
+
 __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32_t* vprev,
-                        uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop) {
+                        uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop,
+                        int64_t nnz, int64_t nrows, unsigned long long* c0,
+                        cudaGraphConditionalHandle h_push0) {
   const int64_t s = rank ? (int64_t)rank[st->source] : st->source;
   st->srank = s;
   if (rank) st->lv16[s] = 1;
@@ -1070,10 +1075,13 @@ __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32
   st->unstamp = 0;
   st->log[0] = 0;
   cudaGraphSetConditional(h_loop, st->cap > 0 ? 1u : 0u);
+  if (st->cap > 0) decide_body(st, nnz, nrows, c0, h_push0);
 }
 
-__global__ void g_decide(BfsState* st, int64_t nnz, int64_t nrows, unsigned long long* c,
-                         cudaGraphConditionalHandle h_push) {
+// the reference rule (kernels.py:108-126) for iteration st->it; c: the
+// counter that iteration's finalize / pull accumulates into
+__device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned long long* c,
+                            cudaGraphConditionalHandle h_push) {
   const int64_t K = st->K, it = st->it;
   const double d = nrows ? (double)nnz / (double)nrows : 0.0;
   const int64_t est = (int64_t)rint(d * (double)K);
@@ -1091,9 +1099,12 @@ __global__ void g_decide(BfsState* st, int64_t nnz, int64_t nrows, unsigned long
   cudaGraphSetConditional(h_push, dir == GB_DIR_PUSH ? 1u : 0u);
 }
 
-// after a level: new frontier size, loop continuation, cap handling
-__global__ void g_advance(BfsState* st, const unsigned long long* c, int64_t n,
-                          cudaGraphConditionalHandle h_a, cudaGraphConditionalHandle h_b) {
+// after a level: new frontier size, loop continuation, cap handling; when the
+// loop continues, the next iteration's decision (one node instead of two)
+__global__ void g_step(BfsState* st, const unsigned long long* c, int64_t n,
+                       cudaGraphConditionalHandle h_a, cudaGraphConditionalHandle h_b,
+                       int64_t nnz, int64_t nrows, unsigned long long* c_next,
+                       cudaGraphConditionalHandle h_push_next) {
   const int64_t K = (int64_t)*c;
   st->xcur = st->xnext < (unsigned long long)n ? (int64_t)st->xnext : n;
   const int64_t it = st->it;
@@ -1108,6 +1119,7 @@ __global__ void g_advance(BfsState* st, const unsigned long long* c, int64_t n,
   st->it = it + 1;
   cudaGraphSetConditional(h_a, cont);
   cudaGraphSetConditional(h_b, cont);
+  if (cont) decide_body(st, nnz, nrows, c_next, h_push_next);
 }
 
 __global__ void g_unstamp(const BfsState* __restrict__ st, const int32_t* __restrict__ F) {
@@ -1191,8 +1203,9 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   G->launches_push = 4 + (push_dead ? 0 : 1);
   const int grid_stamp = grid_for(ctx, (int64_t)1 << 40, 256, 8);
   G->launches_pull = pull_dead ? 3 : 1;
-  // 4 memsets, zero levels (or clear 16-bit levels + unpermute), start, unstamp
-  G->launches_fixed = ordered ? 9 : 8;
+  // 4 memsets, zero levels (or clear 16-bit levels + unpermute), start (with
+  // the first decision), unstamp; each level adds its body and one g_step
+  G->launches_fixed = ordered ? 8 : 7;
 
   auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
     // ordered (sorted-row) graphs skip the dense visited prefix of each list
@@ -1246,16 +1259,14 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   };
   // one iteration on stream s (capturing into the graph that should hold it)
   auto iteration = [&](int h, cudaStream_t s, cudaStream_t s_inner,
-                       cudaGraphConditionalHandle h_a, cudaGraphConditionalHandle h_b) -> cudaError_t {
-    cudaGraphConditionalHandle h_push;
+                       cudaGraphConditionalHandle h_push, cudaGraphConditionalHandle h_a,
+                       cudaGraphConditionalHandle h_b,
+                       cudaGraphConditionalHandle h_push_next) -> cudaError_t {
+    // h_push was set by the previous node that decided this iteration
+    // (g_start or the previous g_step); the handles live in the top graph
     cudaGraph_t br[2];
-    // decide sets h_push before the IF node reads it: create the handle first
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
-    GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
-    GB_GTRY(cudaGraphConditionalHandleCreate(&h_push, g, 0, cudaGraphCondAssignDefault));
-    g_decide<<<1, 1, 0, s>>>(st, push.nnz, push.nrows, G->cnt + h, h_push);
-    GB_GTRY(cudaGetLastError());
     {
       const cudaGraphNode_t* deps = nullptr;
       size_t nd = 0;
@@ -1273,7 +1284,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     }
     GB_GTRY(capture_into(br[0], s_inner, [&] { return push_body(h, s_inner); }));
     GB_GTRY(capture_into(br[1], s_inner, [&] { return pull_body(h, s_inner); }));
-    g_advance<<<1, 1, 0, s>>>(st, G->cnt + h, n, h_a, h_b);
+    g_step<<<1, 1, 0, s>>>(st, G->cnt + h, n, h_a, h_b, push.nnz, push.nrows, G->cnt + (h ^ 1),
+                           h_push_next);
     return cudaGetLastError();
   };
 
@@ -1292,9 +1304,12 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
-    cudaGraphConditionalHandle h_loop;
+    cudaGraphConditionalHandle h_loop, h_push_e, h_push_o;
     GB_GTRY(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
-    g_start<<<1, 1, 0, s>>>(st, G->rank, G->vbm, G->vprev, G->fbm[0], G->F, h_loop);
+    GB_GTRY(cudaGraphConditionalHandleCreate(&h_push_e, g, 0, cudaGraphCondAssignDefault));
+    GB_GTRY(cudaGraphConditionalHandleCreate(&h_push_o, g, 0, cudaGraphCondAssignDefault));
+    g_start<<<1, 1, 0, s>>>(st, G->rank, G->vbm, G->vprev, G->fbm[0], G->F, h_loop, push.nnz,
+                            push.nrows, G->cnt, h_push_e);
     GB_GTRY(cudaGetLastError());
     cudaGraph_t body;
     {
@@ -1318,7 +1333,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       cudaGraph_t gb;
       GB_GTRY(cudaStreamGetCaptureInfo(cs[1], &st2, nullptr, &gb, nullptr, nullptr));
       GB_GTRY(cudaGraphConditionalHandleCreate(&h_odd, gb, 0, cudaGraphCondAssignDefault));
-      GB_GTRY(iteration(0, cs[1], cs[2], h_odd, h_loop));
+      GB_GTRY(iteration(0, cs[1], cs[2], h_push_e, h_odd, h_loop, h_push_o));
       cudaGraph_t odd;
       {
         const cudaGraphNode_t* deps = nullptr;
@@ -1334,7 +1349,9 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
         odd = p.conditional.phGraph_out[0];
         GB_GTRY(cudaStreamUpdateCaptureDependencies(cs[1], &node, 1, cudaStreamSetCaptureDependencies));
       }
-      return capture_into(odd, cs[3], [&] { return iteration(1, cs[3], cs[2], h_loop, h_loop); });
+      return capture_into(odd, cs[3], [&] {
+        return iteration(1, cs[3], cs[2], h_push_o, h_loop, h_loop, h_push_e);
+      });
     }));
     g_unstamp<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(st, G->F);
     if (ordered)
@@ -1452,8 +1469,8 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     GB_CUDA(ctx, cudaMemcpyAsync(log_pin, log, sizeof(int64_t) * (1 + 3 * first),
                                  cudaMemcpyDeviceToHost, s));
     launch_info[0] = G->launches_fixed;
-    launch_info[1] = 2 + G->launches_push;
-    launch_info[2] = 2 + G->launches_pull;
+    launch_info[1] = 1 + G->launches_push;  // + g_step
+    launch_info[2] = 1 + G->launches_pull;
     return GB_OK;
   }
   // one readback: iteration count and up to 21 decisions
@@ -1480,7 +1497,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   *iters_out = iters;
   int64_t nl = G->launches_fixed;
   for (int64_t i = 0; i < iters; ++i)
-    nl += 2 + (log_dir[i] == GB_DIR_PUSH ? G->launches_push : G->launches_pull);
+    nl += 1 + (log_dir[i] == GB_DIR_PUSH ? G->launches_push : G->launches_pull);
   count_launch(ctx, (int)nl);
   return GB_OK;
 }
