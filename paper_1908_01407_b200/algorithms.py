@@ -107,8 +107,10 @@ class _PendingBfs:
         info = self.info
         if info[0]:
             npush = int(np.count_nonzero(dirs == _lib.DIR_PUSH))
+            # + the no-op g_step that follows a loop ending on an even level
             self.ctx.lib.gb_count_launches(self.ctx.ptr, int(info[0] + npush * info[1] +
-                                                            (iters - npush) * info[2]))
+                                                            (iters - npush) * info[2] +
+                                                            (iters & 1)))
         return [DirectionDecision("pull" if dirs[i] == _lib.DIR_PULL else "push",
                                   int(raw[2 + 3 * i]), int(raw[3 + 3 * i]), self.total, self.thr)
                 for i in range(iters)]

@@ -742,6 +742,7 @@ struct BfsState {
   int64_t* out;         // per call, relabelled graphs: levels by original id
   uint16_t* lv16;       // relabelled graphs: internal (16-bit) levels by new id
   int64_t it, K, depth, dnext, unstamp;  // loop state
+  int64_t stopped;                        // the loop ended inside a body pass
   int64_t xcur;                 // dense visited prefix at the level start (ordered graphs)
   int64_t srank;                // relabelled graphs: the source's new id
   unsigned long long xnext;     // ... after the level (atomicMin target)
@@ -1054,6 +1055,8 @@ __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
 
 __device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned long long* c,
                             cudaGraphConditionalHandle h_push);
+// SWITCH values of a level node: its push body, its pull body, or nothing
+constexpr unsigned kSwPush = 0, kSwPull = 1, kSwSkip = 2;
 
 __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32_t* vprev,
                         uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop,
@@ -1073,6 +1076,7 @@ __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32
   st->depth = 1;
   st->xcur = 0;
   st->unstamp = 0;
+  st->stopped = 0;
   st->log[0] = 0;
   cudaGraphSetConditional(h_loop, st->cap > 0 ? 1u : 0u);
   if (st->cap > 0) decide_body(st, nnz, nrows, c0, h_push0);
@@ -1096,7 +1100,7 @@ __device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned l
   st->dnext = st->depth + 1;
   st->xnext = ~0ull;
   *c = 0;
-  cudaGraphSetConditional(h_push, dir == GB_DIR_PUSH ? 1u : 0u);
+  cudaGraphSetConditional(h_push, dir == GB_DIR_PUSH ? kSwPush : kSwPull);
 }
 
 // after a level: new frontier size, loop continuation, cap handling; when the
@@ -1105,6 +1109,11 @@ __global__ void g_step(BfsState* st, const unsigned long long* c, int64_t n,
                        cudaGraphConditionalHandle h_a, cudaGraphConditionalHandle h_b,
                        int64_t nnz, int64_t nrows, unsigned long long* c_next,
                        cudaGraphConditionalHandle h_push_next) {
+  if (st->stopped) {  // the body's earlier level ended the loop
+    cudaGraphSetConditional(h_a, 0);
+    cudaGraphSetConditional(h_b, 0);
+    return;
+  }
   const int64_t K = (int64_t)*c;
   st->xcur = st->xnext < (unsigned long long)n ? (int64_t)st->xnext : n;
   const int64_t it = st->it;
@@ -1119,7 +1128,12 @@ __global__ void g_step(BfsState* st, const unsigned long long* c, int64_t n,
   st->it = it + 1;
   cudaGraphSetConditional(h_a, cont);
   cudaGraphSetConditional(h_b, cont);
-  if (cont) decide_body(st, nnz, nrows, c_next, h_push_next);
+  if (cont) {
+    decide_body(st, nnz, nrows, c_next, h_push_next);
+  } else {
+    st->stopped = 1;
+    cudaGraphSetConditional(h_push_next, kSwSkip);
+  }
 }
 
 __global__ void g_unstamp(const BfsState* __restrict__ st, const int32_t* __restrict__ F) {
@@ -1274,8 +1288,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       cudaGraphNodeParams p = {};
       p.type = cudaGraphNodeTypeConditional;
       p.conditional.handle = h_push;
-      p.conditional.type = cudaGraphCondTypeIf;
-      p.conditional.size = 2;
+      p.conditional.type = cudaGraphCondTypeSwitch;
+      p.conditional.size = 2;  // kSwPush, kSwPull; kSwSkip runs neither
       cudaGraphNode_t node;
       GB_GTRY(cudaGraphAddNode(&node, g, deps, nd, &p));
       br[0] = p.conditional.phGraph_out[0];
@@ -1327,31 +1341,10 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       GB_GTRY(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
     }
     GB_GTRY(capture_into(body, cs[1], [&]() -> cudaError_t {
-      // even iteration; its advance gates the odd one (and the loop)
-      cudaGraphConditionalHandle h_odd;
-      cudaStreamCaptureStatus st2;
-      cudaGraph_t gb;
-      GB_GTRY(cudaStreamGetCaptureInfo(cs[1], &st2, nullptr, &gb, nullptr, nullptr));
-      GB_GTRY(cudaGraphConditionalHandleCreate(&h_odd, gb, 0, cudaGraphCondAssignDefault));
-      GB_GTRY(iteration(0, cs[1], cs[2], h_push_e, h_odd, h_loop, h_push_o));
-      cudaGraph_t odd;
-      {
-        const cudaGraphNode_t* deps = nullptr;
-        size_t nd = 0;
-        GB_GTRY(cudaStreamGetCaptureInfo(cs[1], &st2, nullptr, &gb, &deps, &nd));
-        cudaGraphNodeParams p = {};
-        p.type = cudaGraphNodeTypeConditional;
-        p.conditional.handle = h_odd;
-        p.conditional.type = cudaGraphCondTypeIf;
-        p.conditional.size = 1;
-        cudaGraphNode_t node;
-        GB_GTRY(cudaGraphAddNode(&node, gb, deps, nd, &p));
-        odd = p.conditional.phGraph_out[0];
-        GB_GTRY(cudaStreamUpdateCaptureDependencies(cs[1], &node, 1, cudaStreamSetCaptureDependencies));
-      }
-      return capture_into(odd, cs[3], [&] {
-        return iteration(1, cs[3], cs[2], h_push_o, h_loop, h_loop, h_push_e);
-      });
+      // two levels per pass; a level after the one that ended the loop is a
+      // skipped SWITCH and a no-op g_step
+      GB_GTRY(iteration(0, cs[1], cs[2], h_push_e, h_loop, h_loop, h_push_o));
+      return iteration(1, cs[1], cs[2], h_push_o, h_loop, h_loop, h_push_e);
     }));
     g_unstamp<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(st, G->F);
     if (ordered)
@@ -1498,6 +1491,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   int64_t nl = G->launches_fixed;
   for (int64_t i = 0; i < iters; ++i)
     nl += 1 + (log_dir[i] == GB_DIR_PUSH ? G->launches_push : G->launches_pull);
+  nl += iters & 1;  // the no-op g_step after a loop that ends on an even level
   count_launch(ctx, (int)nl);
   return GB_OK;
 }
