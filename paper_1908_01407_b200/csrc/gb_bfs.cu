@@ -1112,6 +1112,7 @@ __global__ void g_step(BfsState* st, const unsigned long long* c, int64_t n,
   if (st->stopped) {  // the body's earlier level ended the loop
     cudaGraphSetConditional(h_a, 0);
     cudaGraphSetConditional(h_b, 0);
+    cudaGraphSetConditional(h_push_next, kSwSkip);
     return;
   }
   const int64_t K = (int64_t)*c;
@@ -1168,6 +1169,7 @@ struct BfsGraph {
   BfsState* st = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches_push = 0, launches_pull = 0, launches_fixed = 0;
+  int unroll = 2;  // levels per WHILE pass (even)
 };
 
 static void bfs_graph_free(void* p) {
@@ -1220,6 +1222,11 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   // 4 memsets, zero levels (or clear 16-bit levels + unpermute), start (with
   // the first decision), unstamp; each level adds its body and one g_step
   G->launches_fixed = ordered ? 8 : 7;
+  {
+    // 2 measured best (s24: 0.765 ms; 4: 0.797, 6: 0.774, 8: 0.805)
+    const int u = getenv("GB_BFS_UNROLL") ? atoi(getenv("GB_BFS_UNROLL")) : 2;
+    G->unroll = u >= 2 && u % 2 == 0 && u <= 16 ? u : 2;
+  }
 
   auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
     // ordered (sorted-row) graphs skip the dense visited prefix of each list
@@ -1318,12 +1325,14 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     GB_GTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
-    cudaGraphConditionalHandle h_loop, h_push_e, h_push_o;
+    // one SWITCH handle per level slot of a pass (a handle drives exactly one
+    // conditional node); slot j's g_step decides slot j+1
+    cudaGraphConditionalHandle h_loop, h_push[16];
     GB_GTRY(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
-    GB_GTRY(cudaGraphConditionalHandleCreate(&h_push_e, g, 0, cudaGraphCondAssignDefault));
-    GB_GTRY(cudaGraphConditionalHandleCreate(&h_push_o, g, 0, cudaGraphCondAssignDefault));
+    for (int j = 0; j < G->unroll; ++j)
+      GB_GTRY(cudaGraphConditionalHandleCreate(&h_push[j], g, 0, cudaGraphCondAssignDefault));
     g_start<<<1, 1, 0, s>>>(st, G->rank, G->vbm, G->vprev, G->fbm[0], G->F, h_loop, push.nnz,
-                            push.nrows, G->cnt, h_push_e);
+                            push.nrows, G->cnt, h_push[0]);
     GB_GTRY(cudaGetLastError());
     cudaGraph_t body;
     {
@@ -1341,10 +1350,12 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       GB_GTRY(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
     }
     GB_GTRY(capture_into(body, cs[1], [&]() -> cudaError_t {
-      // two levels per pass; a level after the one that ended the loop is a
-      // skipped SWITCH and a no-op g_step
-      GB_GTRY(iteration(0, cs[1], cs[2], h_push_e, h_loop, h_loop, h_push_o));
-      return iteration(1, cs[1], cs[2], h_push_o, h_loop, h_loop, h_push_e);
+      // G->unroll (even) levels per pass; a level after the one that ended
+      // the loop is a skipped SWITCH and a no-op g_step
+      for (int j = 0; j < G->unroll; ++j)
+        GB_GTRY(iteration(j & 1, cs[1], cs[2], h_push[j], h_loop, h_loop,
+                          h_push[(j + 1) % G->unroll]));
+      return cudaSuccess;
     }));
     g_unstamp<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(st, G->F);
     if (ordered)
@@ -1462,6 +1473,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     GB_CUDA(ctx, cudaMemcpyAsync(log_pin, log, sizeof(int64_t) * (1 + 3 * first),
                                  cudaMemcpyDeviceToHost, s));
     launch_info[0] = G->launches_fixed;
+    launch_info[3] = G->unroll;
     launch_info[1] = 1 + G->launches_push;  // + g_step
     launch_info[2] = 1 + G->launches_pull;
     return GB_OK;
@@ -1491,7 +1503,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   int64_t nl = G->launches_fixed;
   for (int64_t i = 0; i < iters; ++i)
     nl += 1 + (log_dir[i] == GB_DIR_PUSH ? G->launches_push : G->launches_pull);
-  nl += iters & 1;  // the no-op g_step after a loop that ends on an even level
+  nl += (G->unroll - iters % G->unroll) % G->unroll;  // no-op g_steps of the last pass
   count_launch(ctx, (int)nl);
   return GB_OK;
 }
@@ -1804,6 +1816,7 @@ gb_status gb_bfs_ordered_async(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   launch_info[0] = 0;
   launch_info[1] = 0;
   launch_info[2] = 0;
+  launch_info[3] = 2;
   return GB_OK;
 }
 
