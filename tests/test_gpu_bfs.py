@@ -438,3 +438,24 @@ def test_bfs_async_logs_survive_the_ring(gb, monkeypatch):
         want = gb.bfs(A, s, desc=d2).values
         assert np.array_equal(outs[k].values, want), k
         assert list(d.direction_log) == list(d2.direction_log), k
+
+
+@pytest.mark.parametrize("src", [0, 5])
+def test_bfs_async_launch_accounting_matches_sync(gb, src, monkeypatch):
+    """The launches an asynchronous bfs books when its log is read equal the
+    synchronous graph entry's count for the same run (bench gpu_launches)."""
+    from paper_1908_01407_b200 import _lib, algorithms
+    ctx = _lib.context()
+    A = gb.io.rmat_matrix(14)
+    gb.bfs(A, src).values  # build the graph and the log ring
+    monkeypatch.setattr(algorithms, "_ASYNC_BFS", False)
+    l0 = ctx.launches()
+    d1 = gb.Descriptor()
+    gb.bfs(A, src, desc=d1).values
+    sync_n = ctx.launches() - l0
+    monkeypatch.setattr(algorithms, "_ASYNC_BFS", True)
+    l0 = ctx.launches()
+    d2 = gb.Descriptor()
+    gb.bfs(A, src, desc=d2).values
+    assert len(d2.direction_log) == len(d1.direction_log)
+    assert ctx.launches() - l0 == sync_n > 0
