@@ -119,10 +119,35 @@ bfs_expand_warp(DevI64 Kd, const int64_t* __restrict__ S, const int64_t* __restr
   if (K > 0 && S[K] < 4 * K) {
     // short lists (s24 level 4: 844 K entries, 1.04 M edges): one thread per
     // frontier entry beats 512-slot tiles that each hold hundreds of entries
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
-         k += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t p0 = rowstart[k], d = S[k + 1] - S[k];
-      for (int64_t j = 0; j < d; ++j) f.visit(p0 + j);
+    // four entries per thread per pass: their bounds, first edges and probes
+    // are each one batched round trip
+    constexpr int B = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += B * stride) {
+      int64_t p0[B], d[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int64_t kk = k + j * stride;
+        p0[j] = 0;
+        d[j] = 0;
+        if (kk < K) {
+          p0[j] = rowstart[kk];
+          d[j] = S[kk + 1] - S[kk];
+        }
+      }
+      int32_t v[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        v[j] = -1;
+        if (d[j] > 0) {
+          const int32_t c = ld_stream(idx + p0[j]);
+          v[j] = (!VALS || on(p0[j])) ? c : -1;
+        }
+      }
+      f.template probe_mark<B>(v);
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+        for (int64_t e = 1; e < d[j]; ++e) f.visit(p0[j] + e);
     }
     return;
   }
