@@ -450,10 +450,11 @@ gb_status gb_bfs_ordered(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
  * of 1 + 3*max_iters int64 receiving [iters, (dir, frontier, estimate) x
  * iters]; log_host: pinned host buffer of 1 + 3*21 int64 that receives the
  * first 1 + 3*min(iters, 21) entries in stream order -- synchronise the
- * stream before reading it, and read entries past 21 decisions from log_dev.  launch_info[4] = launches of the
+ * stream before reading it, and read entries past 21 decisions from log_dev.  launch_info[5] = launches of the
  * fixed part, of one push level, of one pull level (0 on the synchronous
- * path) and the levels per device-loop pass u; pass fixed + per-level
- * launches + (u - iters % u) % u (no-op steps of the last pass) to
+ * path), the levels per device-loop pass u, and of one push level whose
+ * frontier is a single vertex (it skips the degree scan); pass fixed +
+ * per-level launches + (u - iters % u) % u (no-op steps of the last pass) to
  * gb_count_launches once the log is read.  Replaces
  * the synchronous return of algorithms.py:48-77 + the direction_log appends
  * of kernels.py:303-304, resolved lazily by the host. */

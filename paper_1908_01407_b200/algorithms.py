@@ -106,11 +106,15 @@ class _PendingBfs:
         dirs = raw[1:1 + 3 * iters:3]
         info = self.info
         if info[0]:
-            npush = int(np.count_nonzero(dirs == _lib.DIR_PUSH))
-            # + the no-op g_steps of the device loop's last pass
+            push = dirs == _lib.DIR_PUSH
+            npush1 = int(np.count_nonzero(push & (raw[2:2 + 3 * iters:3] == 1)))
+            npush = int(np.count_nonzero(push)) - npush1
+            # single-entry push levels skip the degree scan; + the no-op
+            # g_steps of the device loop's last pass
             u = int(info[3])
             self.ctx.lib.gb_count_launches(self.ctx.ptr, int(info[0] + npush * info[1] +
-                                                            (iters - npush) * info[2] +
+                                                            npush1 * info[4] +
+                                                            (iters - npush - npush1) * info[2] +
                                                             (u - iters % u) % u))
         return [DirectionDecision("pull" if dirs[i] == _lib.DIR_PULL else "push",
                                   int(raw[2 + 3 * i]), int(raw[3 + 3 * i]), self.total, self.thr)
@@ -203,7 +207,7 @@ def bfs(A: SparseMatrix, source: int, desc=None, early_exit=True) -> Vector:
         push_o, pull_o, rank = trav
         (push, _k1), (pull, _k2) = push_o.csr_struct(), pull_o.csr_struct()
         ctx = _lib.context()
-        info = np.zeros(4, np.int64)
+        info = np.zeros(5, np.int64)
         pending = _PendingBfs(ctx, A, desc.switch_ratio, info)
         log_pin, log_dev = _log_ring(ctx, levels.device).take(pending, cap)
         ctx.call("gb_bfs_ordered_async", C.byref(push), C.byref(pull), _lib.ptr(pull_o.nonempty()),

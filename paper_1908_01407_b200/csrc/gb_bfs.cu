@@ -766,6 +766,12 @@ struct BfsState {
   int32_t policy, pad_;
   int64_t* out;         // per call, relabelled graphs: levels by original id
   uint16_t* lv16;       // relabelled graphs: internal (16-bit) levels by new id
+  // single-entry push levels (K == 1) skip the degree scan: the decision
+  // writes that entry's bounds itself (k1 == 0: disabled)
+  const int64_t* off;
+  const int32_t* F1;
+  int64_t *rowstart1, *S1;
+  int64_t k1;
   int64_t it, K, depth, dnext, unstamp;  // loop state
   int64_t stopped;                        // the loop ended inside a body pass
   int64_t xcur;                 // dense visited prefix at the level start (ordered graphs)
@@ -1081,7 +1087,7 @@ __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
 __device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned long long* c,
                             cudaGraphConditionalHandle h_push);
 // SWITCH values of a level node: its push body, its pull body, or nothing
-constexpr unsigned kSwPush = 0, kSwPull = 1, kSwSkip = 2;
+constexpr unsigned kSwPush = 0, kSwPull = 1, kSwPush1 = 2, kSwSkip = 3;
 
 __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32_t* vprev,
                         uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop,
@@ -1125,7 +1131,17 @@ __device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned l
   st->dnext = st->depth + 1;
   st->xnext = ~0ull;
   *c = 0;
-  cudaGraphSetConditional(h_push, dir == GB_DIR_PUSH ? kSwPush : kSwPull);
+  unsigned sw = dir == GB_DIR_PUSH ? kSwPush : kSwPull;
+  if (dir == GB_DIR_PUSH && K == 1 && st->k1) {
+    // one frontier entry: its whole list (no prefix cut) as the expansion space
+    const int64_t v = st->F1[0];
+    const int64_t a = st->off[v], b = st->off[v + 1];
+    st->rowstart1[0] = a;
+    st->S1[0] = 0;
+    st->S1[1] = b - a;
+    sw = kSwPush1;
+  }
+  cudaGraphSetConditional(h_push, sw);
 }
 
 // after a level: new frontier size, loop continuation, cap handling; when the
@@ -1195,6 +1211,8 @@ struct BfsGraph {
   cudaGraphExec_t exec = nullptr;
   int launches_push = 0, launches_pull = 0, launches_fixed = 0;
   int unroll = 2;  // levels per WHILE pass (even)
+  int launches_push1 = 0;  // a single-entry push level (expansion + finalize)
+  int64_t k1 = 0;          // single-entry push levels skip the degree scan
 };
 
 static void bfs_graph_free(void* p) {
@@ -1242,6 +1260,8 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
   const int grid_smem = push.values ? smem_push_setup<true>(ctx, W, &smem)
                                     : smem_push_setup<false>(ctx, W, &smem);
   G->launches_push = 4 + (push_dead ? 0 : 1);
+  G->launches_push1 = 1 + (push_dead ? 0 : 1);
+  G->k1 = !use_smem && !(getenv("GB_BFS_K1") && atoi(getenv("GB_BFS_K1")) == 0);
   const int grid_stamp = grid_for(ctx, (int64_t)1 << 40, 256, 8);
   G->launches_pull = pull_dead ? 3 : 1;
   // 4 memsets, zero levels (or clear 16-bit levels + unpermute), start (with
@@ -1253,7 +1273,9 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     G->unroll = u >= 2 && u % 2 == 0 && u <= 16 ? u : 2;
   }
 
-  auto push_body = [&](int h, cudaStream_t s) -> cudaError_t {
+  auto push_body = [&](int h, cudaStream_t s, bool single) -> cudaError_t {
+    // single: one frontier entry whose bounds g_step / g_start wrote (no scan)
+    if (!single) {
     // ordered (sorted-row) graphs skip the dense visited prefix of each list
     g_scan_partials<<<kGScanBlocks, kGScanThreads, 0, s>>>(
         dptr(&st->K), G->F, push.offsets, push.indices,
@@ -1262,6 +1284,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
     g_scan_apply<<<kApplyBlocks, kGScanThreads, 0, s>>>(dptr(&st->K), G->part, G->rowstart, G->S,
                                                         G->tile_first, G->tile_base, G->queue);
     g_scan_stamp<<<grid_stamp, 256, 0, s>>>(G->part, G->queue, G->tile_first, G->tile_base);
+    }
     if (!push_dead && use_smem) {
       if (push.values)
         bfs_expand_smem<true><<<grid_smem, kSmemPushThreads, smem, s>>>(
@@ -1310,7 +1333,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
                        cudaGraphConditionalHandle h_push_next) -> cudaError_t {
     // h_push was set by the previous node that decided this iteration
     // (g_start or the previous g_step); the handles live in the top graph
-    cudaGraph_t br[2];
+    cudaGraph_t br[3];
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     {
@@ -1321,15 +1344,17 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       p.type = cudaGraphNodeTypeConditional;
       p.conditional.handle = h_push;
       p.conditional.type = cudaGraphCondTypeSwitch;
-      p.conditional.size = 2;  // kSwPush, kSwPull; kSwSkip runs neither
+      p.conditional.size = 3;  // kSwPush, kSwPull, kSwPush1; kSwSkip runs none
       cudaGraphNode_t node;
       GB_GTRY(cudaGraphAddNode(&node, g, deps, nd, &p));
       br[0] = p.conditional.phGraph_out[0];
       br[1] = p.conditional.phGraph_out[1];
+      br[2] = p.conditional.phGraph_out[2];
       GB_GTRY(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
     }
-    GB_GTRY(capture_into(br[0], s_inner, [&] { return push_body(h, s_inner); }));
+    GB_GTRY(capture_into(br[0], s_inner, [&] { return push_body(h, s_inner, false); }));
     GB_GTRY(capture_into(br[1], s_inner, [&] { return pull_body(h, s_inner); }));
+    GB_GTRY(capture_into(br[2], s_inner, [&] { return push_body(h, s_inner, true); }));
     g_step<<<1, 1, 0, s>>>(st, G->cnt + h, n, h_a, h_b, push.nnz, push.nrows, G->cnt + (h ^ 1),
                            h_push_next);
     return cudaGetLastError();
@@ -1483,6 +1508,11 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   GB_ARENA_CHECK(ctx, ar);
   BfsState h{};
   h.levels = rank ? nullptr : levels;
+  h.off = push->offsets;
+  h.F1 = G->F;
+  h.rowstart1 = G->rowstart;
+  h.S1 = G->S;
+  h.k1 = G->k1;
   h.lv16 = rank ? G->lv : nullptr;
   h.out = levels;
   h.log = log;
@@ -1501,6 +1531,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     launch_info[3] = G->unroll;
     launch_info[1] = 1 + G->launches_push;  // + g_step
     launch_info[2] = 1 + G->launches_pull;
+    launch_info[4] = G->k1 ? 1 + G->launches_push1 : launch_info[1];
     return GB_OK;
   }
   // one readback: iteration count and up to 21 decisions
@@ -1527,7 +1558,8 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   *iters_out = iters;
   int64_t nl = G->launches_fixed;
   for (int64_t i = 0; i < iters; ++i)
-    nl += 1 + (log_dir[i] == GB_DIR_PUSH ? G->launches_push : G->launches_pull);
+    nl += 1 + (log_dir[i] != GB_DIR_PUSH ? G->launches_pull
+               : (G->k1 && log_nvals[i] == 1) ? G->launches_push1 : G->launches_push);
   nl += (G->unroll - iters % G->unroll) % G->unroll;  // no-op g_steps of the last pass
   count_launch(ctx, (int)nl);
   return GB_OK;
@@ -1842,6 +1874,7 @@ gb_status gb_bfs_ordered_async(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   launch_info[1] = 0;
   launch_info[2] = 0;
   launch_info[3] = 2;
+  launch_info[4] = 0;
   return GB_OK;
 }
 
