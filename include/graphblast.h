@@ -81,6 +81,12 @@ typedef struct gb_csr {
   int32_t pad_;
   int64_t iso_i64;
   double iso_f64;
+  /* Identity of the arrays' CONTENTS, assigned by the owner (the Python
+   * package stamps every orientation with a fresh id).  Per-matrix device
+   * caches (BFS column samples, the instantiated BFS graph) are reused only
+   * for an equal non-zero gen -- never on equal pointers alone, which the
+   * caching allocator recycles.  0 = never cached. */
+  uint64_t gen;
 } gb_csr;
 
 /* ----------------------------------------------------------------------------

@@ -11,9 +11,14 @@ graphalg``) on the CPU so the CUDA product path can be checked against it:
   PageRank, degree-ordered triangle count) used at RMAT scales the numpy port
   cannot reach, and as the ``cpu_baseline`` / ``--impl reference`` timing arm.
 
-Parity is PINNED: ``tests/test_oracle.py`` checks both against the golden
-fixtures in ``tests/golden/`` that ``tests/golden/make_golden.py`` produced by
-running the real reference package in the build container.
+Parity is PINNED against outputs of the real reference package, produced in
+the build container by ``tests/golden/make_golden.py`` (``tests/golden/``):
+``tests/test_oracle.py`` checks the numpy port (operator cases, generator,
+algorithms at s8-s12); ``tests/test_oracle_pins.py`` checks the C oracle --
+BFS (two sources) s8-s20, SSSP / CC / TC / PageRank s8-s20, the reference
+weights at s16/s18/s20, the non-integral SSSP variant and all 20 PageRank
+iterates at s16/s20, the uniform family at s14/s16 and the reference's s22
+BFS / CC / PageRank digests.
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
 leg may import this package.  The product package (``paper_1908_01407_b200``)

@@ -147,6 +147,56 @@ int64_t og_rmat_csr(int scale, int64_t m, uint64_t seed, double a, double tab, d
   return nnz;
 }
 
+/* assign_weights(edges, low, high, seed) (io.py:252-272) on the symmetric,
+ * sorted CSR that preprocess + edges_to_matrix produce: the k-th upper entry
+ * (i < j, row-major -- the first appearance of (min, max) in the sorted edge
+ * list) draws low + mix_k mod (high-low+1); its mirror (j, i) takes the same
+ * value (found by binary search in the sorted row j).  Returns 0, or -1 when
+ * a mirror is missing (the CSR is not symmetric). */
+int64_t og_upper_weights(int64_t n, const int64_t* rp, const int32_t* ci, uint64_t seed,
+                         int64_t low, int64_t high, double* w) {
+  int64_t* ufirst = malloc(sizeof(int64_t) * (size_t)(n + 1));
+  /* rank of a row's first upper entry = upper entries of all earlier rows */
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t lo = rp[i], hi = rp[i + 1];
+    while (lo < hi) { /* first column > i */
+      int64_t mid = lo + (hi - lo) / 2;
+      if (ci[mid] <= i) lo = mid + 1; else hi = mid;
+    }
+    ufirst[i + 1] = rp[i + 1] - lo;
+  }
+  ufirst[0] = 0;
+  for (int64_t i = 0; i < n; ++i) ufirst[i + 1] += ufirst[i];
+  uint64_t span = (uint64_t)(high - low + 1);
+  int64_t bad = 0;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : bad)
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t base = rp[i + 1] - (ufirst[i + 1] - ufirst[i]); /* first upper slot of row i */
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+      int64_t j = ci[e], k;
+      if (j > i) {
+        k = ufirst[i] + (e - base);
+      } else if (j < i) {
+        int64_t lo = rp[j], hi = rp[j + 1];
+        while (lo < hi) {
+          int64_t mid = lo + (hi - lo) / 2;
+          if (ci[mid] < i) lo = mid + 1; else hi = mid;
+        }
+        if (lo == rp[j + 1] || ci[lo] != i) { ++bad; continue; }
+        int64_t bj = rp[j + 1] - (ufirst[j + 1] - ufirst[j]);
+        k = ufirst[j] + (lo - bj);
+      } else {
+        ++bad; /* preprocess drops self loops */
+        continue;
+      }
+      w[e] = (double)(low + (int64_t)(mix(seed + ((uint64_t)k + 1) * GAMMA) % span));
+    }
+  }
+  free(ufirst);
+  return bad ? -1 : 0;
+}
+
 /* kernels.py:108-126 */
 static int decide(int64_t nnz, int64_t nrows, int64_t nnz_u, double ratio, int policy,
                   int64_t* est_out) {

@@ -42,6 +42,8 @@ def lib():
         L.og_pagerank.argtypes = [i64, vp, vp, vp, f64, f64, i64, vp, vp]
         L.og_cc.restype = i64
         L.og_cc.argtypes = [i64, vp, vp, vp, vp, i64, f64, C.c_int, C.c_int, vp, vp, vp, vp]
+        L.og_upper_weights.restype = i64
+        L.og_upper_weights.argtypes = [i64, vp, vp, u64, i64, i64, vp]
         L.og_tc.restype = i64
         L.og_tc.argtypes = [i64, vp, vp]
         _lib = L
@@ -82,6 +84,15 @@ def rmat_csr(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1):
     tab = a + b
     nnz = lib().og_rmat_csr(scale, m, seed, a, tab, tab + c, _p(rp), _p(ci))
     return rp, ci[:nnz].copy()
+
+
+def upper_weights(rp, ci, seed=1, low=1, high=64):
+    """io.py:252-272 on a symmetric sorted CSR: float64 weights per stored entry."""
+    rp, ci = _csr(rp, ci)
+    w = np.empty(ci.size, np.float64)
+    if lib().og_upper_weights(rp.size - 1, _p(rp), _p(ci), seed, low, high, _p(w)) != 0:
+        raise ValueError("CSR is not symmetric / has self loops")
+    return w
 
 
 def _log(cap):

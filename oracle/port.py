@@ -833,6 +833,8 @@ def upper_weights(rp, ci, seed=1, low=1, high=64):
     """io.py:252-272 restated for a symmetric sorted CSR: the k-th upper entry
     (row-major) gets 1 + mix_k mod 64; its mirror gets the same value."""
     n = rp.size - 1
+    rp = np.asarray(rp, dtype=I64)
+    ci = np.asarray(ci, dtype=I64)  # int32 columns would overflow rows*n + col from n = 2^16
     rows = np.repeat(np.arange(n, dtype=I64), np.diff(rp))
     up = rows < ci
     k = np.cumsum(up) - 1

@@ -50,11 +50,15 @@ pi32 = C.POINTER(C.c_int32)
 pf64 = C.POINTER(C.c_double)
 
 
+# gb_abi_version() of the library these bindings describe (include/graphblast.h)
+ABI_VERSION = 2
+
+
 class gb_csr(C.Structure):
     _fields_ = [
         ("nrows", i64), ("ncols", i64), ("nnz", i64),
         ("offsets", vp), ("indices", vp), ("values", vp),
-        ("dtype", i32), ("pad_", i32), ("iso_i64", i64), ("iso_f64", f64),
+        ("dtype", i32), ("pad_", i32), ("iso_i64", i64), ("iso_f64", f64), ("gen", C.c_uint64),
     ]
 
 
@@ -167,6 +171,10 @@ def load(path: str = LIB_PATH):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = [ITER_CB if a == "ITER_CB" else a for a in args]
+        got = lib.gb_abi_version()
+        if got != ABI_VERSION:
+            _lib_err = f"{path} has ABI {got}, this package binds ABI {ABI_VERSION}"
+            raise RuntimeError(_lib_err + " (rebuild with __graft_entry__.build())")
         _lib = lib
         return lib
 
@@ -207,6 +215,7 @@ class Context:
         self.ptr = ptr
         self.lib = lib
         self._stream = None
+        self._trim_hooks = []
 
     def launches(self) -> int:
         return int(self.lib.gb_launch_count(self.ptr))
@@ -222,7 +231,13 @@ class Context:
                                   ms.ctypes.data_as(vp))
         return [(int(kind[i]), int(arg[i]), float(ms[i])) for i in range(k)]
 
+    def on_trim(self, fn):
+        """Run fn() before the scratch pool is released (Python-side caches)."""
+        self._trim_hooks.append(fn)
+
     def trim(self):
+        for fn in self._trim_hooks:
+            fn()
         self.lib.gb_ctx_trim(self.ptr)
 
     def call(self, name, *args):

@@ -23,7 +23,8 @@ import torch
 
 from . import _lib
 from .algebra import LESS, MINUS, TIMES, builtin_monoid, builtin_semiring
-from .containers import INDEX_DTYPE, DecisionLog, Descriptor, Direction, SparseMatrix, Vector, empty
+from .containers import (INDEX_DTYPE, DecisionLog, Descriptor, Direction, SparseMatrix, Vector,
+                         empty, full)
 from .errors import ShapeError
 from .kernels import (
     DirectionDecision,
@@ -131,7 +132,8 @@ class _LogRing:
     def __init__(self, device):
         self.pin = torch.empty((self.SLOTS, 1 + 3 * _LOG_PREFIX), dtype=torch.int64,
                                pin_memory=True)
-        self.dev = None
+        # device logs are sized per slot from the call's loop cap, on first use
+        self.dev = [None] * self.SLOTS
         self.device = device
         self.owner = [None] * self.SLOTS
         self.next = 0
@@ -144,18 +146,21 @@ class _LogRing:
 
     def take(self, pending, cap):
         need = 1 + 3 * cap
-        if self.dev is None or self.dev.shape[1] < need:
-            for i in range(self.SLOTS):  # a longer loop cap: grow every slot once
-                self._settle(i)
-            self.dev = torch.empty((self.SLOTS, max(need, 1 + 3 * 10_000)), dtype=torch.int64,
-                                   device=self.device)
         i = self.next
         self.next = (i + 1) % self.SLOTS
-        self._settle(i)
+        self._settle(i)  # the slot's previous call has finished with both buffers
+        if self.dev[i] is None or self.dev[i].numel() < need:
+            self.dev[i] = torch.empty(max(need, 1 + 3 * 64), dtype=torch.int64, device=self.device)
         self.owner[i] = weakref.ref(pending)
         pending.row = self.pin[i]
         pending.dev = self.dev[i]
         return self.pin[i], self.dev[i]
+
+    def release(self):
+        """Settle every outstanding call and drop the device logs (ctx.trim())."""
+        for i in range(self.SLOTS):
+            self._settle(i)
+        self.dev = [None] * self.SLOTS
 
 
 _rings = {}
@@ -165,6 +170,7 @@ def _log_ring(ctx, device):
     ring = _rings.get(id(ctx))
     if ring is None:
         ring = _rings[id(ctx)] = _LogRing(device)
+        ctx.on_trim(ring.release)
     return ring
 
 
@@ -193,6 +199,9 @@ def bfs(A: SparseMatrix, source: int, desc=None, early_exit=True) -> Vector:
         return _bfs_composed(A, source, desc)
     n = A.nrows
     iters = min(desc.max_niter, n + 1)
+    if iters <= 0:
+        # the reference loop runs zero times: an all-zero level vector, no log
+        return Vector._wrap(n, None, full(n, 0, np.int64), 0, np.int64)
     levels = empty(n, np.int64)
     cap = max(iters, 1)
     dirs = np.zeros(cap, np.int32)

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import itertools
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -457,11 +458,14 @@ def scatter_dense(idx_t, vals_t, dt, zero, size):
 # ---------------------------------------------------------------------------
 
 
+_ORIENT_GEN = itertools.count(1)
+
+
 class _Orient:
     """One orientation on the device: rows of A (CSR) or of A^T (CSC)."""
 
     __slots__ = ("nrows", "ncols", "offsets", "indices", "values", "iso", "dt", "_nonempty",
-                 "_plan", "_ordered", "__weakref__")
+                 "_plan", "_ordered", "gen", "__weakref__")
 
     def __init__(self, nrows, ncols, offsets, indices, values, iso, dt):
         self.nrows, self.ncols = int(nrows), int(ncols)
@@ -471,6 +475,9 @@ class _Orient:
         self._nonempty = None
         self._plan = None
         self._ordered = None
+        # contents identity for the native per-matrix caches (gb_csr.gen);
+        # orientations are immutable, so one id per object
+        self.gen = next(_ORIENT_GEN)
 
     @property
     def nnz(self):
@@ -517,6 +524,7 @@ class _Orient:
             keep = self.values_as(dt)
             s.values = keep.data_ptr() if self.nnz else 0
         s.dtype = _lib.dtype_code(dt)
+        s.gen = self.gen
         return s, keep
 
     def values_as(self, dt):

@@ -805,6 +805,7 @@ struct OrderedAux {
   const int64_t* pull_off = nullptr;
   int32_t* samp = nullptr;
   int64_t reach = 0;
+  uint64_t gen = 0, pull_gen = 0;  // gb_csr.gen of the matrices (0: rebuilt every call)
 };
 
 static void ordered_aux_free(void* p) {
@@ -818,7 +819,9 @@ static gb_status ordered_aux(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull
   void** slot = ctx_slot(ctx, SLOT_BFS_AUX, ordered_aux_free);
   auto* a = static_cast<OrderedAux*>(*slot);
   const int64_t* poff = pull ? pull->offsets : nullptr;
-  if (a && a->idx == push->indices && a->nnz == push->nnz && a->pull_off == poff) {
+  const uint64_t pgen = pull ? pull->gen : 0;
+  if (a && push->gen != 0 && a->gen == push->gen && a->pull_gen == pgen && a->idx == push->indices &&
+      a->nnz == push->nnz && a->pull_off == poff) {
     *out = a;
     return GB_OK;
   }
@@ -831,6 +834,8 @@ static gb_status ordered_aux(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull
   a = new OrderedAux();
   a->idx = push->indices;
   a->nnz = push->nnz;
+  a->gen = push->gen;
+  a->pull_gen = pgen;
   a->pull_off = poff;
   a->reach = push->nrows;
   const int64_t ns = (push->nnz + kSampleStride - 1) / kSampleStride;
@@ -1223,7 +1228,7 @@ static void bfs_graph_free(void* p) {
 }
 
 static bool same_csr(const gb_csr& a, const gb_csr& b) {
-  return a.nrows == b.nrows && a.ncols == b.ncols && a.nnz == b.nnz && a.offsets == b.offsets &&
+  return a.gen != 0 && a.gen == b.gen && a.nrows == b.nrows && a.ncols == b.ncols && a.nnz == b.nnz && a.offsets == b.offsets &&
          a.indices == b.indices && a.values == b.values && a.dtype == b.dtype &&
          a.iso_i64 == b.iso_i64 && a.iso_f64 == b.iso_f64;
 }

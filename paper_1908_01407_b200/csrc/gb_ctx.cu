@@ -14,6 +14,7 @@ struct gb_ctx {
   int device = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
+  cudaEvent_t handoff = nullptr;  // orders a new stream after the previous one
   // scratch pool: blocks reused across calls; arena marks index into `blocks`
   struct Block {
     void* ptr;
@@ -130,7 +131,7 @@ using namespace gb;
 
 extern "C" {
 
-int32_t gb_abi_version(void) { return 1; }
+int32_t gb_abi_version(void) { return 2; }
 
 gb_status gb_ctx_create(int device, gb_ctx** out) {
   if (!out) return GB_ERR_ARG;
@@ -162,13 +163,24 @@ gb_status gb_ctx_destroy(gb_ctx* ctx) {
   for (auto& b : ctx->blocks) cudaFree(b.ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->dev_err) cudaFree(ctx->dev_err);
+  if (ctx->handoff) cudaEventDestroy(ctx->handoff);
   delete ctx;
   return GB_OK;
 }
 
+// Everything the context owns (scratch arena, cached BFS graph state, the
+// pinned log slots) is ordered by its stream.  A switch to another stream
+// therefore makes the new stream wait for all work already enqueued on the old
+// one, so two calls issued under different torch streams never overlap on the
+// shared state.
 gb_status gb_ctx_set_stream(gb_ctx* ctx, void* s) {
   if (!ctx) return GB_ERR_ARG;
-  ctx->stream = (cudaStream_t)s;
+  cudaStream_t ns = (cudaStream_t)s;
+  if (ns == ctx->stream) return GB_OK;
+  if (!ctx->handoff) GB_CUDA(ctx, cudaEventCreateWithFlags(&ctx->handoff, cudaEventDisableTiming));
+  GB_CUDA(ctx, cudaEventRecord(ctx->handoff, ctx->stream));
+  GB_CUDA(ctx, cudaStreamWaitEvent(ns, ctx->handoff, 0));
+  ctx->stream = ns;
   return GB_OK;
 }
 

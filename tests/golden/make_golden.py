@@ -399,6 +399,96 @@ def kernel_cases(seed=20240917):
     return cases
 
 
+# ---------------------------------------------------------------------------
+# round-2 pins: weights, non-integral SSSP and per-iteration PageRank at the
+# BASELINE scales, the uniform family at s16 (written to pins.json)
+# ---------------------------------------------------------------------------
+
+PIN_SAMPLES = 256
+
+
+def sample_ids(n, seed=7):
+    """Vertex 0 (the R-MAT hub) plus PIN_SAMPLES-1 seeded vertex ids."""
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([[0], rng.integers(0, n, PIN_SAMPLES - 1)])).astype(np.int64)
+
+
+def pr_replay(A, alpha=0.85, iters=20):
+    """algorithms.py:153-161 replayed with the reference's own kernels, one
+    record per iteration (the reference's pagerank(max_iters=k) returns the
+    k-th of these)."""
+    from graphalg.algorithms import _scale_rows
+    from graphalg.algebra import MINUS, TIMES
+    pt = ref.builtin_semiring("PlusMultiplies")
+    plus = ref.builtin_monoid("Plus")
+    n = A.nrows
+    scaled = _scale_rows(A, alpha)
+    teleport = (1.0 - alpha) / n
+    ranks = ref.Vector.filled(n, 1.0 / n)
+    ids = sample_ids(n)
+    out = []
+    for _ in range(iters):
+        previous = ranks
+        spread = ref.vxm(pt, previous, scaled, desc=ref.Descriptor())
+        ranks = ref.ewise_add(pt, spread, teleport, desc=ref.Descriptor())
+        delta = ref.ewise_mult(MINUS, ranks, previous, desc=ref.Descriptor())
+        squared = ref.ewise_add(TIMES, delta, delta, desc=ref.Descriptor())
+        err = float(np.sqrt(float(ref.reduce(plus, squared))))
+        v = np.asarray(ranks.values, dtype=np.float64)
+        out.append(dict(sum=float(v.sum()), sumsq=float(np.dot(v, v)), error=err,
+                        digest9=ref_cli._digest(ranks), samples=[float(x) for x in v[ids]]))
+    final = ref.pagerank(A, alpha=alpha, eps=1e-300, max_iters=iters)
+    assert np.array_equal(np.asarray(final.values), v), "replay differs from pagerank()"
+    return dict(sample_ids=ids.tolist(), iterations=out)
+
+
+def make_pins(scales_w=(16, 18, 20), scales_pr=(16, 20)):
+    res = dict(note="reference outputs (graphalg 0.1.0, /root/reference/pkg) computed in the "
+                    "build container by tests/golden/make_golden.py --only pins")
+    for s in scales_w:
+        t = time.time()
+        W = build(s, weighted=True)
+        res[f"weights_rmat_s{s}"] = dict(digest=values_digest(W.csr_values), nnz=int(W.nnz),
+                                         sum=float(W.csr_values.sum()))
+        if s in (16, 20):
+            # the non-integral variant of C2 (SURVEY §8(d)): sqrt of the reference weights,
+            # fed as the same CSR to both sides
+            Wn = ref.SparseMatrix.from_csr(W.nrows, W.ncols, W.row_offsets.copy(),
+                                           W.col_indices.copy(), np.sqrt(W.csr_values))
+            desc = ref.Descriptor()
+            dist = ref.sssp(Wn, 0, desc=desc)
+            v = np.asarray(dist.values)
+            ids = sample_ids(W.nrows)
+            fin = np.isfinite(v)
+            res[f"sssp_sqrt_s{s}"] = dict(digest=ref_cli._digest(dist), trace=trace_of(desc),
+                                          finite=int(fin.sum()), sum_finite=float(v[fin].sum()),
+                                          sample_ids=ids.tolist(),
+                                          samples=[float(x) if np.isfinite(x) else None for x in v[ids]])
+        del W
+        print(f"pins weights s{s} {time.time()-t:.1f}s", flush=True)
+    for s in scales_pr:
+        t = time.time()
+        res[f"pr_iter_s{s}"] = pr_replay(build(s))
+        print(f"pins pr s{s} {time.time()-t:.1f}s", flush=True)
+    uni = dict(a=0.25, b=0.25, c=0.25, d=0.25)
+    for s in (14, 16):
+        t = time.time()
+        A = build(s, **uni)
+        W = build(s, weighted=True, **uni)
+        desc = ref.Descriptor()
+        lv = ref.bfs(A, 0, desc=desc)
+        dd = ref.Descriptor()
+        cc = ref.connected_components(A, desc=dd)
+        res[f"uniform_s{s}"] = dict(nnz=int(A.nnz), csr=csr_digest(A),
+                                    weights=values_digest(W.csr_values),
+                                    bfs=dict(digest=ref_cli._digest(lv), trace=trace_of(desc)),
+                                    cc=dict(digest=ref_cli._digest(cc), trace=trace_of(dd)),
+                                    sssp=dict(digest=ref_cli._digest(ref.sssp(W, 0))),
+                                    tc=int(ref.triangle_count(A)))
+        print(f"pins uniform s{s} {time.time()-t:.1f}s", flush=True)
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -414,6 +504,11 @@ def main():
         make_graphs(out, [8, 10, 12, 14, 16] + ([18, 20] if args.big else []))
         with open(os.path.join(HERE, "rmat_graphs.json"), "w") as fh:
             json.dump(out, fh, indent=1)
+    if args.only == "pins":
+        res = make_pins()
+        with open(os.path.join(HERE, "pins.json"), "w") as fh:
+            json.dump(res, fh, indent=1)
+        return
     if args.only in ("all", "algorithms"):
         res = run_algorithms([8, 10, 12, 14, 16] + ([18, 20] if args.big else []),
                              [8, 10, 12, 14] + ([16, 20] if args.big else []), args.big)

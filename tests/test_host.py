@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     # double without one)
     unbound = [s for s in syms if s not in _lib.SIGNATURES]
     assert not unbound, unbound
-    assert lib.gb_abi_version() == 1
+    assert lib.gb_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_native_direction_rule_matches_reference_cases():

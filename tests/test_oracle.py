@@ -1,8 +1,9 @@
-"""Pin the CPU oracle (oracle/port.py, oracle/cgraph.c) to the reference goldens.
+"""Pin the numpy oracle (oracle/port.py) to the reference goldens.
 
 CPU only.  The goldens were produced by the real reference package
-(tests/golden/make_golden.py); the oracle must reproduce every one of them
-before any GPU result is compared against it.
+(tests/golden/make_golden.py); the port must reproduce every one of them
+before any GPU result is compared against it.  The C oracle (oracle/cgraph.c,
+the checker at s16 and above) is pinned by tests/test_oracle_pins.py.
 """
 
 import hashlib
