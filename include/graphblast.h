@@ -248,6 +248,51 @@ gb_status gb_mxv_pull(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr
                       const gb_row_plan* plan, const void* u, const uint32_t* mask,
                       int32_t early_exit, int32_t partition, void* out, int64_t* counters);
 
+/* Row bins of an orientation (gb_mv_binned.cu), built once per matrix:
+ * short rows (1..16 entries), medium rows (17..512) and the 512-entry tiles
+ * of the long rows, cut at absolute multiples of 512.  The row split of
+ * kernels.py:133-150 (Partition.ROW_SPLIT) made row-granular so the mask is
+ * tested per row before any entry is read. */
+typedef struct gb_bin_plan {
+  int64_t n_short, n_mid, n_long_tiles;
+  const int32_t* short_rows;  /* [n_short] */
+  const int32_t* mid_rows;    /* [n_mid] */
+  const int32_t* tile_row;    /* [n_long_tiles] */
+  const int64_t* tile_beg;    /* [n_long_tiles] first entry */
+  const int64_t* tile_end;    /* [n_long_tiles] one past the last entry */
+} gb_bin_plan;
+
+/* counts_host[3] = {n_short, n_mid, n_long_tiles}.  Synchronizes. */
+gb_status gb_bin_plan_counts(gb_ctx* ctx, const gb_csr* a, int64_t* counts_host);
+
+/* fill the caller's arrays of `plan` (sizes from gb_bin_plan_counts).  Sync. */
+gb_status gb_bin_plan_fill(gb_ctx* ctx, const gb_csr* a, gb_bin_plan* plan);
+
+/* Pull SpMV over the row bins (same contract as gb_mxv_pull without early
+ * exit; commutative folds).  Rows are mask-tested before their entries are
+ * read.  Asynchronous. */
+gb_status gb_mxv_pull_binned(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                             const gb_bin_plan* plan, const void* u, const uint32_t* mask,
+                             void* out, int64_t* counters);
+
+/* gb_mxv_pull on the degree-ordered layout of the same matrix (same results,
+ * kernels.py:153-229; commutative folds without early exit).  `a` is the
+ * relabelled orientation P A P^T (gb_csr_relabel_t), `plan` its row plan with
+ * nz_rows mapped back to ORIGINAL row ids (gb_row_plan_remap), order[r] the
+ * original id of new id r, reach = 1 + the largest column id of `a`.  u, mask
+ * and out use the original ids.  Asynchronous. */
+gb_status gb_mxv_pull_ordered(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                              const gb_row_plan* plan, const int32_t* order, int64_t reach,
+                              const void* u, const uint32_t* mask, void* out, int64_t* counters);
+
+/* out[i] = map[ids[i]] for i < count (row plans of a relabelled matrix in the
+ * original ids).  Asynchronous. */
+gb_status gb_row_plan_remap(gb_ctx* ctx, int64_t count, const int32_t* ids, const int32_t* map,
+                            int32_t* out);
+
+/* largest entry of idx[count] (-1 when empty).  Synchronizes. */
+gb_status gb_index_max(gb_ctx* ctx, int64_t count, const int32_t* idx, int64_t* max_host);
+
 /* Push SpMSpV (kernels.py:242-280): expand the columns named by the sparse u
  * (k entries), multiply, fold per output row, drop identity results, apply
  * the mask.  `a` is the column orientation (rows of `a` = the columns walked).
@@ -481,6 +526,12 @@ void gb_count_launches(gb_ctx* ctx, int64_t n);
  * `words`-word bitmap (>= min_probes of them) at full occupancy; writes
  * probes per second.  Synchronizes. */
 gb_status gb_probe_rate(gb_ctx* ctx, int64_t words, int64_t min_probes, double* probes_per_s_host);
+
+/* Gather ceiling of a pull SpMV on `a`: gathers/s of a kernel that only
+ * streams a's column indices and gathers x[col] (f64, n entries) for every
+ * stored entry.  Measurement support for bench.py.  Synchronizes. */
+gb_status gb_gather_replay_rate(gb_ctx* ctx, const gb_csr* a, const double* x,
+                                double* gathers_per_s_host);
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,8 @@ GB_F64 = 1
 # operator ids
 OP_PLUS, OP_PLUS_WRAP, OP_MINUS, OP_TIMES, OP_MIN, OP_MAX, OP_LOR, OP_LAND, OP_LESS, OP_NE, \
     OP_SECOND, OP_FIRST = range(12)
+# folds whose result does not depend on the order (gb_mv.cu fold_is_commutative)
+COMMUTATIVE_FOLD_IDS = (OP_PLUS, OP_PLUS_WRAP, OP_TIMES, OP_MIN, OP_MAX, OP_LOR, OP_LAND)
 
 DIR_AUTO, DIR_PUSH, DIR_PULL = 0, 1, 2
 PART_NONZERO, PART_ROW = 0, 1
@@ -64,6 +66,11 @@ class gb_csr(C.Structure):
 
 class gb_row_plan(C.Structure):
     _fields_ = [("nrows_nz", i64), ("nz_rows", vp), ("nz_off", vp), ("tile_first", vp)]
+
+
+class gb_bin_plan(C.Structure):
+    _fields_ = [("n_short", i64), ("n_mid", i64), ("n_long_tiles", i64), ("short_rows", vp),
+                ("mid_rows", vp), ("tile_row", vp), ("tile_beg", vp), ("tile_end", vp)]
 
 
 # name -> (restype, argtypes)
@@ -107,7 +114,16 @@ SIGNATURES = {
     "gb_mxv_pull": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_row_plan), vp, vp, i32,
                           i32, vp, vp]),
     "gb_row_plan_build": (i32, [vp, C.POINTER(gb_csr), vp, vp, vp, pi64]),
+    "gb_mxv_pull_ordered": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_row_plan), vp,
+                                  i64, vp, vp, vp, vp]),
+    "gb_row_plan_remap": (i32, [vp, i64, vp, vp, vp]),
+    "gb_bin_plan_counts": (i32, [vp, C.POINTER(gb_csr), vp]),
+    "gb_bin_plan_fill": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_bin_plan)]),
+    "gb_mxv_pull_binned": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_bin_plan), vp, vp,
+                                 vp, vp]),
+    "gb_index_max": (i32, [vp, i64, vp, pi64]),
     "gb_probe_rate": (i32, [vp, i64, i64, C.POINTER(f64)]),
+    "gb_gather_replay_rate": (i32, [vp, C.POINTER(gb_csr), vp, C.POINTER(f64)]),
     "gb_mxv_push": (i32, [vp, i32, i32, C.POINTER(gb_csr), i64, i64, vp, vp, vp, vp, vp, pi64,
                           vp]),
     "gb_mxm_masked": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_csr),

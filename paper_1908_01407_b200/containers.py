@@ -465,7 +465,7 @@ class _Orient:
     """One orientation on the device: rows of A (CSR) or of A^T (CSC)."""
 
     __slots__ = ("nrows", "ncols", "offsets", "indices", "values", "iso", "dt", "_nonempty",
-                 "_plan", "_ordered", "gen", "__weakref__")
+                 "_plan", "_bins", "_ordered", "_order", "_mv_ordered", "gen", "__weakref__")
 
     def __init__(self, nrows, ncols, offsets, indices, values, iso, dt):
         self.nrows, self.ncols = int(nrows), int(ncols)
@@ -474,7 +474,10 @@ class _Orient:
         self.dt = np.dtype(dt)
         self._nonempty = None
         self._plan = None
+        self._bins = None
         self._ordered = None
+        self._order = None       # new -> original id of the traversal layout
+        self._mv_ordered = {}    # transpose -> ordered masked-pull view (SparseMatrix.ordered_pull)
         # contents identity for the native per-matrix caches (gb_csr.gen);
         # orientations are immutable, so one id per object
         self.gen = next(_ORIENT_GEN)
@@ -482,6 +485,27 @@ class _Orient:
     @property
     def nnz(self):
         return int(self.indices.numel())
+
+    def bin_plan(self):
+        """Row bins of this orientation (gb_bin_plan_counts / _fill): short
+        rows, medium rows and the 512-entry tiles of long rows, built once.
+        Returns (gb_bin_plan, keepalive)."""
+        if self._bins is None:
+            s, _keep = self.csr_struct()
+            ctx = _lib.context()
+            cnt = (C.c_int64 * 3)()
+            ctx.call("gb_bin_plan_counts", C.byref(s), cnt)
+            ns, nm, nl = int(cnt[0]), int(cnt[1]), int(cnt[2])
+            bufs = (empty(max(ns, 1), np.int32), empty(max(nm, 1), np.int32),
+                    empty(max(nl, 1), np.int32), empty(max(nl, 1), np.int64),
+                    empty(max(nl, 1), np.int64))
+            p = _lib.gb_bin_plan()
+            p.n_short, p.n_mid, p.n_long_tiles = ns, nm, nl
+            (p.short_rows, p.mid_rows, p.tile_row, p.tile_beg,
+             p.tile_end) = (b.data_ptr() for b in bufs)
+            ctx.call("gb_bin_plan_fill", C.byref(s), C.byref(p))
+            self._bins = (p, bufs)
+        return self._bins
 
     def row_plan(self):
         """Edge-balanced work plan of this orientation (gb_row_plan_build):
@@ -783,7 +807,39 @@ class SparseMatrix:
             pull = relabel_t(o)    # rows of P A^T P^T: in-edges
             push = relabel_t(csc)  # rows of P A P^T: out-edges
         o._ordered = (csc, (push, pull, rank))
+        o._order = order
+        o._mv_ordered = {}
         return o._ordered[1]
+
+    def ordered_pull(self, transpose):
+        """The masked pull SpMV's view of the degree-ordered layout
+        (gb_mxv_pull_ordered): the relabelled orientation whose rows the pull
+        walks (P A P^T, or P A^T P^T when transposed), its row plan with the
+        non-empty rows named by their ORIGINAL ids, the new -> original
+        order and the column reach.  Built once per matrix and orientation;
+        None when the matrix has no traversal layout."""
+        t = self.traversal()
+        if t is None:
+            return None
+        o = self._csr
+        v = o._mv_ordered.get(bool(transpose))
+        if v is not None:
+            return v
+        push, pull, _rank = t
+        ov = pull if transpose else push
+        plan, keep = ov.row_plan()
+        ctx = _lib.context()
+        rows_old = empty(max(int(plan.nrows_nz), 1), np.int32)
+        ctx.call("gb_row_plan_remap", int(plan.nrows_nz), C.c_void_p(plan.nz_rows),
+                 _lib.ptr(o._order), _lib.ptr(rows_old))
+        p = _lib.gb_row_plan()
+        p.nrows_nz = plan.nrows_nz
+        p.nz_rows, p.nz_off, p.tile_first = rows_old.data_ptr(), plan.nz_off, plan.tile_first
+        mx = C.c_int64(0)
+        ctx.call("gb_index_max", ov.nnz, _lib.ptr(ov.indices), C.byref(mx))
+        v = (ov, p, (rows_old, keep), o._order, int(mx.value) + 1)
+        o._mv_ordered[bool(transpose)] = v
+        return v
 
     def _rank64(self):
         """int64 copy of the traversal rank (gather targets), cached with it."""

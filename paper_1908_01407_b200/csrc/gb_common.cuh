@@ -117,6 +117,12 @@ __host__ __device__ __forceinline__ T op_fold(int op, T acc, T x) {
   }
 }
 
+// folds whose result does not depend on the order of the operands
+__host__ __device__ __forceinline__ bool fold_commutes(int op) {
+  return op == GB_OP_PLUS || op == GB_OP_PLUS_WRAP || op == GB_OP_TIMES || op == GB_OP_MIN ||
+         op == GB_OP_MAX || op == GB_OP_LOR || op == GB_OP_LAND;
+}
+
 // value of a one-element fold (reduceat on a length-1 segment)
 template <class T>
 __host__ __device__ __forceinline__ T op_fold1(int op, T x) {
@@ -294,9 +300,24 @@ __device__ __forceinline__ void red_or_shared_if(bool pred, uint32_t* addr, uint
 #ifndef GB_GATHER_NA
 #define GB_GATHER_NA 0
 #endif
+#ifndef GB_GATHER_EL
+#define GB_GATHER_EL 0  // 1: gathers carry an L2 evict_last policy (A/B knob)
+#endif
 template <class T>
 __device__ __forceinline__ T ld_gather(const T* p) {
-#if GB_GATHER_NA
+#if GB_GATHER_EL
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  if (sizeof(T) == 8) {
+    unsigned long long v;
+    asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return *reinterpret_cast<T*>(&v);
+  } else {
+    unsigned v;
+    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return *reinterpret_cast<T*>(&v);
+  }
+#elif GB_GATHER_NA
   if (sizeof(T) == 8) {
     unsigned long long v;
     asm("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -361,6 +382,12 @@ inline int resident_grid(gb_ctx* ctx, Kernel kernel, int block, size_t smem = 0)
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// gb_mv.cu: out[0..n) = v; counters[2] -= rows folded across tiles (hasmul bits)
+template <class T>
+void fill_identity(gb_ctx* ctx, int64_t n, T v, T* out);
+void mv_pull_finish_counts(gb_ctx* ctx, int64_t W, const uint32_t* hasmul,
+                           unsigned long long* counters);
 
 // A scalar kernel argument that is either a value known at launch or a device
 // location read when the kernel starts (graph-driven loops).

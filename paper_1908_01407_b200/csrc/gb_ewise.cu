@@ -296,11 +296,6 @@ reduce_rows_kernel(int64_t nrows, const int64_t* __restrict__ off, const T* __re
   }
 }
 
-static bool fold_commutes(int op) {
-  return op == GB_OP_PLUS || op == GB_OP_PLUS_WRAP || op == GB_OP_TIMES || op == GB_OP_MIN ||
-         op == GB_OP_MAX || op == GB_OP_LOR || op == GB_OP_LAND;
-}
-
 template <class T>
 static T host_val(const void* p) {
   T v;

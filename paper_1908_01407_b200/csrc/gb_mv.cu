@@ -18,10 +18,7 @@
 
 namespace gb {
 
-__host__ __device__ __forceinline__ bool fold_is_commutative(int op) {
-  return op == GB_OP_PLUS || op == GB_OP_PLUS_WRAP || op == GB_OP_TIMES || op == GB_OP_MIN ||
-         op == GB_OP_MAX || op == GB_OP_LOR || op == GB_OP_LAND;
-}
+__host__ __device__ __forceinline__ bool fold_is_commutative(int op) { return fold_commutes(op); }
 
 template <class T>
 __device__ __forceinline__ T aval(const T* vals, T iso, int64_t p) {
@@ -130,25 +127,48 @@ mv_pull_rows(int64_t nrows, const int64_t* __restrict__ off, const int32_t* __re
 // row_pos their first position in the matrix, so masked-out rows cost
 // nothing.  Positions are contiguous only inside a row: a lane adds the
 // tile row's (row_pos - nz_off) to its slot position.
-template <class T, int ADD, int MUL, bool VALS, bool COMPACT>
-__global__ void __launch_bounds__(256, GB_MV_MINB)
+// HOT (ordered layout, gb_mxv_pull_ordered): u is the degree-ordered copy of
+// the input vector, whose first hot_n entries -- the highest-degree columns,
+// ~31 % of all gathers at R-MAT s24 -- are staged once per CTA in dynamic
+// shared memory; gathers of those columns never reach L2.  One 1024-thread
+// CTA per SM (WPB = 32) shares the largest possible copy.
+template <class T, int ADD, int MUL, bool VALS, bool COMPACT, int WPB, bool HOT>
+__global__ void __launch_bounds__(WPB * 32, WPB == 8 ? GB_MV_MINB : 1)
 mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
               const int64_t* __restrict__ row_pos,
               const int32_t* __restrict__ tile_first, const int32_t* __restrict__ idx,
               const T* __restrict__ vals, T iso, const T* __restrict__ u,
               const uint32_t* __restrict__ mask, int add_rt, int mult_rt, T* __restrict__ out,
-              unsigned long long* __restrict__ counters, uint32_t* __restrict__ hasmul) {
+              unsigned long long* __restrict__ counters, uint32_t* __restrict__ hasmul,
+              int32_t hot_n) {
   const int add_op = ADD >= 0 ? ADD : add_rt;
   const int mult_op = MUL >= 0 ? MUL : mult_rt;
-  __shared__ uint16_t s_st[8][kRowTile + 8];
-  __shared__ uint8_t s_ok[8][COMPACT ? 1 : kRowTile + 8];     // mask bit of each tile row
-  __shared__ int64_t s_sb[COMPACT ? 8 : 1][COMPACT ? kRowTile + 8 : 1];  // row_pos - nz_off
+  __shared__ uint16_t s_st[WPB][kRowTile + 8];
+  __shared__ uint32_t s_ok[WPB][COMPACT ? 1 : kRowTile / 32 + 1];  // mask bit of each tile row
+  __shared__ int64_t s_sb[COMPACT ? WPB : 1][COMPACT ? kRowTile + 8 : 1];  // row_pos - nz_off
   __shared__ unsigned long long s_cnt[3];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  T* s_hot = reinterpret_cast<T*>(s_dyn);
   if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  if (HOT) {
+    // the hot prefix of u (L2-resident: written by the permutation just before)
+    for (int i = 2 * threadIdx.x; i < hot_n; i += 2 * blockDim.x) {
+      if (i + 1 < hot_n) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(u + i));
+        *reinterpret_cast<double2*>(s_hot + i) = v;
+      } else {
+        s_hot[i] = __ldg(u + i);
+      }
+    }
+  }
   __syncthreads();
+  auto gather = [&](int32_t c) -> T {
+    if (HOT) return c < hot_n ? s_hot[c] : ld_gather(u + c);
+    return ld_gather(u + c);
+  };
   const int lane = threadIdx.x & 31;
   uint16_t* st = s_st[threadIdx.x >> 5];
-  uint8_t* okr = s_ok[threadIdx.x >> 5];
+  uint32_t* okw = s_ok[threadIdx.x >> 5];
   int64_t* sb = s_sb[COMPACT ? threadIdx.x >> 5 : 0];
   const T ident = op_identity<T>(add_op);
   const int64_t R_rows = R_d.get();
@@ -164,17 +184,25 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
     const int64_t r1 = t + 1 < ntiles ? tile_first[t + 1] : R_rows - 1;
     const int nr = (int)(r1 - r0 + 1);
     // row starts relative to the tile, clamped to [0, kRowTile]; st[nr] ends the last row
-    for (int i = lane; i <= nr; i += 32) {
-      const int64_t no = nz_off[r0 + i];
-      const int64_t o = no - e0;
-      st[i] = (uint16_t)(o < 0 ? 0 : (o > kRowTile ? kRowTile : o));
-      if (i < nr) {
-        if (COMPACT) {
-          sb[i] = row_pos[r0 + i] - no;
-        } else {
-          const int32_t row = nz_rows[r0 + i];
-          okr[i] = !mask || ((__ldg(mask + (row >> 5)) >> (row & 31)) & 1u);
+    for (int i0 = 0; i0 <= nr; i0 += 32) {
+      const int i = i0 + lane;
+      bool ok = false;
+      if (i <= nr) {
+        const int64_t no = nz_off[r0 + i];
+        const int64_t o = no - e0;
+        st[i] = (uint16_t)(o < 0 ? 0 : (o > kRowTile ? kRowTile : o));
+        if (i < nr) {
+          if (COMPACT) {
+            sb[i] = row_pos[r0 + i] - no;
+          } else {
+            const int32_t row = nz_rows[r0 + i];
+            ok = !mask || ((__ldg(mask + (row >> 5)) >> (row & 31)) & 1u);
+          }
         }
+      }
+      if (!COMPACT) {
+        const uint32_t b = __ballot_sync(GB_FULL, ok);
+        if (lane == 0) okw[i0 >> 5] = b;
       }
     }
     // does the tile's first row start before it / its last row end after it?
@@ -200,7 +228,7 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
       int a = rel0, c = lo;
       do {
         const int b = st[c + 1] < rel1 ? st[c + 1] : rel1;
-        if (okr[c]) allowed |= ((1u << (b - a)) - 1u) << (a - rel0);
+        if ((okw[c >> 5] >> (c & 31)) & 1u) allowed |= ((1u << (b - a)) - 1u) << (a - rel0);
         a = b;
         ++c;
       } while (a < rel1);
@@ -243,7 +271,7 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
     constexpr int kGat = kRowItems / GB_MV_SPLIT;
     T uv[kGat];
 #pragma unroll
-    for (int q = 0; q < kGat; ++q) uv[q] = (allowed >> q) & 1u ? ld_gather(u + cols[q]) : ident;
+    for (int q = 0; q < kGat; ++q) uv[q] = (allowed >> q) & 1u ? gather(cols[q]) : ident;
     c_reads += __popc(allowed);
     // pass 3: fold segment by segment.  Rows are non-empty, so one step
     // always reaches the next segment.  A segment that ends inside the lane
@@ -267,7 +295,7 @@ mv_pull_tiles(DevI64 R_d, const int32_t* __restrict__ nz_rows, const int64_t* __
         if (kGat < kRowItems && q > 0 && q % kGat == 0) {
 #pragma unroll
           for (int j = 0; j < kGat; ++j)
-            uv[j] = (allowed >> (q + j)) & 1u ? ld_gather(u + cols[q + j]) : ident;
+            uv[j] = (allowed >> (q + j)) & 1u ? gather(cols[q + j]) : ident;
         }
         const int e = rel0 + q;
         if (e < rel1 && e >= next) {
@@ -566,14 +594,26 @@ struct MvRows {
   bool compact;
 };
 
+// hot == 0: the original-layout kernel (4 x 256-thread CTAs per SM); hot > 0:
+// the ordered-layout kernel with `hot` entries of u in shared memory
 template <class T, int ADD, int MUL, bool VALS>
 static gb_status launch_tiles_k(gb_ctx* ctx, int add_op, int mult_op, const MvRows& plan,
                                 const gb_csr* a, T iso, const T* u, const uint32_t* mask, T* out,
-                                unsigned long long* counters, uint32_t* hasmul) {
-  auto k = plan.compact ? mv_pull_tiles<T, ADD, MUL, VALS, true> : mv_pull_tiles<T, ADD, MUL, VALS, false>;
+                                unsigned long long* counters, uint32_t* hasmul, int32_t hot) {
+  if (hot > 0) {
+    auto k = mv_pull_tiles<T, ADD, MUL, VALS, false, 32, true>;
+    const size_t smem = (size_t)hot * sizeof(T);
+    GB_CUDA(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<resident_grid(ctx, k, 1024, smem), 1024, smem, stream_of(ctx)>>>(
+        plan.R, plan.rows, plan.off, plan.pos, plan.tile_first, a->indices, (const T*)a->values,
+        iso, u, mask, add_op, mult_op, out, counters, hasmul, hot);
+    return GB_OK;
+  }
+  auto k = plan.compact ? mv_pull_tiles<T, ADD, MUL, VALS, true, 8, false>
+                        : mv_pull_tiles<T, ADD, MUL, VALS, false, 8, false>;
   k<<<resident_grid(ctx, k, 256), 256, 0, stream_of(ctx)>>>(
       plan.R, plan.rows, plan.off, plan.pos, plan.tile_first, a->indices, (const T*)a->values, iso,
-      u, mask, add_op, mult_op, out, counters, hasmul);
+      u, mask, add_op, mult_op, out, counters, hasmul, 0);
   return GB_OK;
 }
 
@@ -581,11 +621,11 @@ template <class T, int ADD, int MUL>
 static gb_status launch_tiles_v(gb_ctx* ctx, int add_op, int mult_op, bool vals,
                                 const MvRows& plan, const gb_csr* a, T iso, const T* u,
                                 const uint32_t* mask, T* out, unsigned long long* counters,
-                                uint32_t* hasmul) {
+                                uint32_t* hasmul, int32_t hot) {
   return vals ? launch_tiles_k<T, ADD, MUL, true>(ctx, add_op, mult_op, plan, a, iso, u, mask, out,
-                                                  counters, hasmul)
+                                                  counters, hasmul, hot)
               : launch_tiles_k<T, ADD, MUL, false>(ctx, add_op, mult_op, plan, a, iso, u, mask, out,
-                                                   counters, hasmul);
+                                                   counters, hasmul, hot);
 }
 
 // the builtin semirings get their own instantiation; anything else is generic
@@ -593,11 +633,11 @@ template <class T>
 static gb_status launch_pull_tiles(gb_ctx* ctx, int add_op, int mult_op, bool vals,
                                    const MvRows& plan, const gb_csr* a, T iso, const T* u,
                                    const uint32_t* mask, T* out, unsigned long long* counters,
-                                   uint32_t* hasmul) {
+                                   uint32_t* hasmul, int32_t hot = 0) {
 #define GB_SR(A_, M_)                                                                         \
   if (add_op == A_ && mult_op == M_)                                                          \
     return launch_tiles_v<T, A_, M_>(ctx, add_op, mult_op, vals, plan, a, iso, u, mask, out, \
-                                     counters, hasmul);
+                                     counters, hasmul, hot);
   GB_SR(GB_OP_PLUS, GB_OP_TIMES)    // PlusMultiplies
   GB_SR(GB_OP_LOR, GB_OP_LAND)      // LogicalOrAnd
   GB_SR(GB_OP_MIN, GB_OP_PLUS)      // MinPlus
@@ -608,7 +648,7 @@ static gb_status launch_pull_tiles(gb_ctx* ctx, int add_op, int mult_op, bool va
   GB_SR(GB_OP_MIN, GB_OP_NE)        // MinimumNotEqualTo
 #undef GB_SR
   return launch_tiles_v<T, -1, -1>(ctx, add_op, mult_op, vals, plan, a, iso, u, mask, out, counters,
-                                   hasmul);
+                                   hasmul, hot);
 }
 
 // ---------------------------------------------------------------------------
@@ -744,6 +784,110 @@ static gb_status pull_tiles_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr
   return GB_OK;
 }
 
+template <class T>
+void fill_identity(gb_ctx* ctx, int64_t n, T v, T* out) {
+  fill_value<T><<<grid_for(ctx, n, 256, 8), 256, 0, stream_of(ctx)>>>(n, v, out);
+}
+template void fill_identity<int64_t>(gb_ctx*, int64_t, int64_t, int64_t*);
+template void fill_identity<double>(gb_ctx*, int64_t, double, double*);
+
+void mv_pull_finish_counts(gb_ctx* ctx, int64_t W, const uint32_t* hasmul,
+                           unsigned long long* counters) {
+  mv_pull_finish<<<grid_for(ctx, W, 256, 4), 256, 0, stream_of(ctx)>>>(W, hasmul, counters);
+}
+
+// ---------------------------------------------------------------------------
+// Masked pull on the degree-ordered layout (SparseMatrix.traversal()).  The
+// matrix is P A P^T; the plan's rows are the ORIGINAL row ids of its
+// non-empty rows, so the mask is probed and `out` written in the caller's
+// labels, and only the column gathers use new ids -- on uo = u permuted into
+// the new order (one pass over the `reach` columns that have entries).  In
+// the new order the gathered part of u is a dense prefix (71 MB at R-MAT s24
+// against 134 MB for u, so it stays in L2) and its highest-degree head sits
+// in shared memory (HOT kernel above).
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void perm_gather(int64_t m, const int32_t* __restrict__ order, const T* __restrict__ u,
+                            T* __restrict__ uo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    uo[i] = __ldg(u + __ldg(order + i));
+}
+
+__global__ void remap_ids(int64_t m, const int32_t* __restrict__ ids, const int32_t* __restrict__ map,
+                          int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = map[ids[i]];
+}
+
+__global__ void index_max(int64_t m, const int32_t* __restrict__ idx, int* __restrict__ out) {
+  int v = -1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v = max(v, ld_stream(idx + i));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(GB_FULL, v, o));
+  if ((threadIdx.x & 31) == 0 && v >= 0) atomicMax(out, v);
+}
+
+#ifndef GB_MV_HOT_MAX
+#define GB_MV_HOT_MAX (1 << 30)  // cap on the shared-memory head (A/B knob)
+#endif
+
+template <class T>
+static int32_t hot_entries(gb_ctx* ctx, int64_t reach) {
+  static int cap = -1;
+  if (cap < 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, mv_pull_tiles<T, GB_OP_PLUS, GB_OP_TIMES, false, false, 32, true>);
+    cap = (int)((optin - (int)fa.sharedSizeBytes - 1024) / sizeof(T)) & ~1;
+    if (cap < 0) cap = 0;
+    const char* e = getenv("GB_MV_HOT");
+    if (e) cap = cap < atoi(e) ? cap : atoi(e);
+    if (cap > GB_MV_HOT_MAX) cap = GB_MV_HOT_MAX;
+  }
+  (void)ctx;
+  return (int32_t)(reach < cap ? reach : cap);
+}
+
+template <class T>
+static gb_status pull_ordered_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a,
+                                const gb_row_plan* given, const int32_t* order, int64_t reach,
+                                const T* u, const uint32_t* mask, T* out, int64_t* counters) {
+  cudaStream_t s = stream_of(ctx);
+  const int64_t n = a->nrows;
+  const int64_t W = (n + 31) / 32;
+  Arena ar(ctx);
+  T* uo = ar.alloc<T>(reach > 0 ? reach : 1);
+  uint32_t* hasmul = counters ? ar.alloc<uint32_t>(W) : nullptr;
+  GB_ARENA_CHECK(ctx, ar);
+  const T ident = op_identity<T>(add_op);
+  const T iso = std::is_same<T, double>::value ? (T)a->iso_f64 : (T)a->iso_i64;
+  if (hasmul) GB_CUDA(ctx, cudaMemsetAsync(hasmul, 0, sizeof(uint32_t) * W, s));
+  fill_value<T><<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, ident, out);
+  if (reach > 0)
+    perm_gather<T><<<grid_for(ctx, reach, 256, 8), 256, 0, s>>>(reach, order, u, uo);
+  const int ps = prof_begin(ctx, PROF_MV, a->nnz);
+  if (given->nrows_nz > 0) {
+    MvRows rows{dval(given->nrows_nz), given->nz_rows, given->nz_off, nullptr, given->tile_first,
+                false};
+    const int32_t hot = hot_entries<T>(ctx, reach);
+    GB_TRY(launch_pull_tiles<T>(ctx, add_op, mult_op, a->values != nullptr, rows, a, iso, uo, mask,
+                                out, (unsigned long long*)counters, hasmul, hot > 0 ? hot : 0));
+  }
+  prof_end(ctx, ps);
+  if (counters)
+    mv_pull_finish<<<grid_for(ctx, W, 256, 4), 256, 0, s>>>(W, hasmul,
+                                                             (unsigned long long*)counters);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 3 + (counters ? 2 : 0));
+  return GB_OK;
+}
+
 }  // namespace gb
 
 using namespace gb;
@@ -779,6 +923,48 @@ gb_status gb_mxv_pull(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr
   prof_end(ctx, ps);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 1);
+  return GB_OK;
+}
+
+gb_status gb_mxv_pull_ordered(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                              const gb_row_plan* plan, const int32_t* order, int64_t reach,
+                              const void* u, const uint32_t* mask, void* out, int64_t* counters) {
+  if (a->nrows == 0) return GB_OK;
+  if (!plan || !order || !fold_is_commutative(add_op))
+    return set_error(ctx, GB_ERR_VALUE, "gb_mxv_pull_ordered: needs a plan, the order and a "
+                     "commutative fold");
+  if (a->dtype == GB_I64)
+    return pull_ordered_t<int64_t>(ctx, add_op, mult_op, a, plan, order, reach, (const int64_t*)u,
+                                   mask, (int64_t*)out, counters);
+  return pull_ordered_t<double>(ctx, add_op, mult_op, a, plan, order, reach, (const double*)u,
+                                mask, (double*)out, counters);
+}
+
+gb_status gb_row_plan_remap(gb_ctx* ctx, int64_t count, const int32_t* ids, const int32_t* map,
+                            int32_t* out) {
+  if (count > 0) {
+    remap_ids<<<grid_for(ctx, count, 256, 8), 256, 0, stream_of(ctx)>>>(count, ids, map, out);
+    GB_LAUNCH_CHECK(ctx);
+    count_launch(ctx, 1);
+  }
+  return GB_OK;
+}
+
+gb_status gb_index_max(gb_ctx* ctx, int64_t count, const int32_t* idx, int64_t* max_host) {
+  *max_host = -1;
+  if (count == 0) return GB_OK;
+  Arena ar(ctx);
+  int* d = ar.alloc<int>(1);
+  GB_ARENA_CHECK(ctx, ar);
+  cudaStream_t s = stream_of(ctx);
+  GB_CUDA(ctx, cudaMemsetAsync(d, 0xff, sizeof(int), s));
+  index_max<<<grid_for(ctx, count, 256, 8), 256, 0, s>>>(count, idx, d);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  int h = -1;
+  GB_CUDA(ctx, cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GB_CUDA(ctx, cudaStreamSynchronize(s));
+  *max_host = h;
   return GB_OK;
 }
 

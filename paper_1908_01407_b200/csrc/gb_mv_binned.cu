@@ -1,0 +1,423 @@
+// Row-binned pull SpMV: the masked pull (kernels.py:153-229) and the
+// reference's row split (Partition.ROW_SPLIT, kernels.py:142-143) as
+// row-granular work.
+//
+// The edge-balanced row tiles (gb_rowtiles.cuh) walk every stored entry of
+// the matrix: a masked-out row still costs its share of tile staging, owner
+// search, fold slots and warp scan.  At R-MAT s24 with a 50 % mask that is
+// half of 520 M slots for nothing, and with a 90 % mask the kernel spends
+// 1.06 ms on 52 M entries.  Here the rows are binned ONCE per matrix by
+// length and every bin tests the mask per row before touching an entry:
+//
+//   short  (1..16 entries, 6.4 M rows / 4.6 % of the entries at s24): one
+//          lane per row, its entries loaded through L1 (a row is <= 2 sectors);
+//   medium (17..512, 2.3 M rows / 31 %): a half-warp per row, two rows at a
+//          time, 128 entries (8 loads + 8 gathers per lane) per pass; the 32
+//          rows of a group are mask-tested with one ballot so only allowed
+//          rows are walked;
+//   long   (> 512, 190 K rows / 64 %): 512-entry tiles at absolute multiples of
+//          512 (a full tile is two 256-bit loads per lane, gathers in two waves
+//          of 8), 32 tile descriptors loaded and mask-tested per warp batch,
+//          warp fold, one atomic fold per tile (out is prefilled with the
+//          identity).
+//
+// Each warp runs its stride of the long tiles, then of the medium groups,
+// then of the short groups, so no bin waits for another.  Commutative folds
+// only (the products of a row are combined in tree order).  Work counters
+// are exact: reads = entries of allowed rows, multiplies = those with
+// u(j) != identity, adds = multiplies - rows with >= 1 multiply (long rows
+// through the `hasmul` bitmap, deduplicated by mv_pull_finish).
+#include <type_traits>
+
+#include <cub/cub.cuh>
+
+#include "gb_common.cuh"
+
+namespace gb {
+
+constexpr int kBinShort = 16;
+constexpr int kBinLong = 512;
+
+#ifndef GB_MVB_MINB
+#define GB_MVB_MINB 4
+#endif
+
+template <class T>
+__device__ __forceinline__ T bin_aval(const T* vals, T iso, int64_t p) {
+  return vals ? __ldg(vals + p) : iso;
+}
+
+template <class T, int ADD, int MUL, bool VALS>
+__global__ void __launch_bounds__(256, GB_MVB_MINB)
+mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __restrict__ L_beg,
+               const int64_t* __restrict__ L_end, int64_t nM, const int32_t* __restrict__ M_rows,
+               int64_t nS, const int32_t* __restrict__ S_rows, const int64_t* __restrict__ off,
+               const int32_t* __restrict__ idx, const T* __restrict__ vals, T iso,
+               const T* __restrict__ u, const uint32_t* __restrict__ mask, int add_rt,
+               int mult_rt, T* __restrict__ out, unsigned long long* __restrict__ counters,
+               uint32_t* __restrict__ hasmul) {
+  const int add_op = ADD >= 0 ? ADD : add_rt;
+  const int mult_op = MUL >= 0 ? MUL : mult_rt;
+  const T ident = op_identity<T>(add_op);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long c_reads = 0, c_muls = 0, c_rows = 0;  // warp-wide work (lanes 0 / 16)
+  unsigned long long s_reads = 0, s_muls = 0, s_rows = 0;  // per lane (short rows)
+  auto fold_one = [&](T& acc, int& cnt, bool live, int64_t p, int32_t c) {
+    if (live) {
+      const T x = ld_gather(u + c);
+      if (x != ident) {
+        acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, VALS ? bin_aval(vals, iso, p) : iso, x));
+        ++cnt;
+      }
+    }
+  };
+  // fold a gathered value (identity values are skipped, kernels.py:167)
+  auto fold_one_v = [&](T& acc, int& cnt, T x, int64_t p) {
+    if (x != ident) {
+      acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, VALS ? bin_aval(vals, iso, p) : iso, x));
+      ++cnt;
+    }
+  };
+
+  // ---- long rows: 512-entry tiles, 32 tile descriptors per warp batch -----
+  // Lane l loads descriptor g*32+l (coalesced) and tests its row's mask bit;
+  // the warp then walks the allowed tiles of the batch.  Consecutive tiles
+  // mostly belong to one hub row, so a batch is usually all-in or all-out.
+  for (int64_t g = w0; g * 32 < nL; g += nw) {
+    const int64_t ti = g * 32 + lane;
+    int32_t row = -1;
+    int64_t tb = 0, te = 0;
+    if (ti < nL) {
+      row = __ldg(L_row + ti);
+      tb = __ldg(L_beg + ti);
+      te = __ldg(L_end + ti);
+    }
+    uint32_t bal = __ballot_sync(GB_FULL, row >= 0 && (!mask || bit_test(mask, row)));
+    while (bal) {
+      const int j = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const int32_t rr = __shfl_sync(GB_FULL, row, j);
+      const int64_t beg = __shfl_sync(GB_FULL, tb, j), end = __shfl_sync(GB_FULL, te, j);
+      T acc = ident;
+      int cnt = 0;
+      if (end - beg == kBinLong) {
+        // absolute 512-aligned: lane l takes entries 16l .. 16l+15 (2 x 256-bit),
+        // gathers in two waves of 8
+        int32_t cols[16];
+        ld_stream8(idx + beg + 16 * lane, *reinterpret_cast<int32_t(*)[8]>(cols));
+        ld_stream8(idx + beg + 16 * lane + 8, *reinterpret_cast<int32_t(*)[8]>(cols + 8));
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          T x[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x[k] = ld_gather(u + cols[8 * w + k]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) fold_one_v(acc, cnt, x[k], beg + 16 * lane + 8 * w + k);
+        }
+      } else {
+        // a partial tile (the row's first or last): lane-strided, coalesced
+        for (int64_t base = beg; base < end; base += 256) {
+          int32_t cols[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int64_t p = base + 32 * k + lane;
+            cols[k] = p < end ? ld_stream(idx + p) : 0;
+          }
+          T x[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x[k] = base + 32 * k + lane < end ? ld_gather(u + cols[k]) : ident;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) fold_one_v(acc, cnt, x[k], base + 32 * k + lane);
+        }
+      }
+      acc = warp_fold<T>(add_op, acc);
+      cnt = (int)warp_sum_ll(cnt);
+      if (lane == 0) {
+        c_reads += (unsigned long long)(end - beg);
+        if (cnt > 0) {
+          atomic_fold<T>(add_op, out + rr, acc);
+          c_muls += cnt;
+          if (hasmul) atomicOr(hasmul + (rr >> 5), 1u << (rr & 31));
+        }
+      }
+    }
+  }
+
+  // ---- medium rows: a half-warp per allowed row, two rows at a time --------
+  const int half = lane >> 4, hl = lane & 15;
+  for (int64_t g = w0; g * 32 < nM; g += nw) {
+    const int64_t i = g * 32 + lane;
+    const int32_t r = i < nM ? __ldg(M_rows + i) : -1;
+    const bool ok = r >= 0 && (!mask || bit_test(mask, r));
+    int64_t lo = 0, hi = 0;
+    if (ok) {
+      lo = __ldg(off + r);
+      hi = __ldg(off + r + 1);
+    }
+    uint32_t bal = __ballot_sync(GB_FULL, ok);
+    while (bal) {
+      const int j0 = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const int j1 = bal ? __ffs(bal) - 1 : -1;
+      if (bal) bal &= bal - 1;
+      const int src = half ? (j1 >= 0 ? j1 : j0) : j0;
+      const int32_t rr = __shfl_sync(GB_FULL, r, src);
+      int64_t l = __shfl_sync(GB_FULL, lo, src), h = __shfl_sync(GB_FULL, hi, src);
+      if (half && j1 < 0) h = l;  // no second row: the upper half idles
+      T acc = ident;
+      int cnt = 0;
+      for (int64_t base = l; base < h; base += 128) {
+        int32_t cols[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int64_t p = base + 16 * k + hl;
+          cols[k] = p < h ? ld_stream(idx + p) : 0;
+        }
+        T x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = base + 16 * k + hl < h ? ld_gather(u + cols[k]) : ident;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fold_one_v(acc, cnt, x[k], base + 16 * k + hl);
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        acc = op_fold<T>(add_op, acc, __shfl_xor_sync(GB_FULL, acc, o));
+        cnt += __shfl_xor_sync(GB_FULL, cnt, o);
+      }
+      if (hl == 0 && h > l) {
+        c_reads += (unsigned long long)(h - l);
+        if (cnt > 0) {
+          out[rr] = acc;
+          c_muls += cnt;
+          ++c_rows;
+        }
+      }
+    }
+  }
+
+  // ---- short rows: a lane per row ------------------------------------------
+  for (int64_t g = w0; g * 32 < nS; g += nw) {
+    const int64_t i = g * 32 + lane;
+    const int32_t r = i < nS ? __ldg(S_rows + i) : -1;
+    if (r >= 0 && (!mask || bit_test(mask, r))) {
+      const int64_t lo = __ldg(off + r);
+      const int len = (int)(__ldg(off + r + 1) - lo);
+      int32_t cols[kBinShort];
+#pragma unroll
+      for (int q = 0; q < kBinShort; ++q) cols[q] = q < len ? __ldg(idx + lo + q) : 0;
+      T acc = ident;
+      int cnt = 0;
+#pragma unroll
+      for (int q = 0; q < kBinShort; ++q) fold_one(acc, cnt, q < len, lo + q, cols[q]);
+      s_reads += (unsigned long long)len;
+      if (cnt > 0) {
+        out[r] = acc;
+        s_muls += cnt;
+        ++s_rows;
+      }
+    }
+  }
+
+  if (counters) {
+    __shared__ unsigned long long s_cnt[3];
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const long long r_ = warp_sum_ll((long long)(s_reads + c_reads));
+    const long long m_ = warp_sum_ll((long long)(s_muls + c_muls));
+    const long long w_ = warp_sum_ll((long long)(s_rows + c_rows));
+    if (lane == 0) {
+      atomicAdd(&s_cnt[0], (unsigned long long)r_);
+      atomicAdd(&s_cnt[1], (unsigned long long)m_);
+      atomicAdd(&s_cnt[2], (unsigned long long)w_);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(counters + 0, s_cnt[0]);
+      atomicAdd(counters + 1, s_cnt[1]);
+      atomicAdd(counters + 2, s_cnt[1] - s_cnt[2]);  // long rows: mv_pull_finish
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plan: per row, (short, medium) flags packed in one u64 (two 32-bit
+// counters, n < 2^32) and the long tiles it spans in a second scan
+// ---------------------------------------------------------------------------
+__global__ void bin_count(int64_t n, const int64_t* __restrict__ off, uint64_t* __restrict__ sm,
+                          int64_t* __restrict__ lt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t a = 0;
+    int64_t t = 0;
+    if (r < n) {
+      const int64_t lo = off[r], hi = off[r + 1], len = hi - lo;
+      if (len >= 1 && len <= kBinShort) a = 1;
+      else if (len > kBinShort && len <= kBinLong) a = 1ull << 32;
+      else if (len > kBinLong) t = (hi - 1) / kBinLong - lo / kBinLong + 1;
+    }
+    sm[r] = a;
+    lt[r] = t;
+  }
+}
+
+__global__ void bin_fill(int64_t n, const int64_t* __restrict__ off, const uint64_t* __restrict__ sm,
+                         const int64_t* __restrict__ lt, int32_t* __restrict__ S_rows,
+                         int32_t* __restrict__ M_rows, int32_t* __restrict__ L_row,
+                         int64_t* __restrict__ L_beg, int64_t* __restrict__ L_end) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = off[r], hi = off[r + 1], len = hi - lo;
+    if (len >= 1 && len <= kBinShort) {
+      S_rows[sm[r] & 0xffffffffull] = (int32_t)r;
+    } else if (len > kBinShort && len <= kBinLong) {
+      M_rows[sm[r] >> 32] = (int32_t)r;
+    } else if (len > kBinLong) {
+      int64_t p = lt[r];
+      for (int64_t b = lo / kBinLong * kBinLong; b < hi; b += kBinLong, ++p) {
+        L_row[p] = (int32_t)r;
+        L_beg[p] = b > lo ? b : lo;
+        L_end[p] = b + kBinLong < hi ? b + kBinLong : hi;
+      }
+    }
+  }
+}
+
+// exclusive scans of the flags; returns the three totals on the host
+static gb_status bin_scan(gb_ctx* ctx, Arena& ar, const gb_csr* a, uint64_t** sm_out,
+                          int64_t** lt_out, int64_t* counts) {
+  cudaStream_t s = stream_of(ctx);
+  const int64_t n = a->nrows;
+  uint64_t* sm = ar.alloc<uint64_t>(n + 1);
+  uint64_t* smx = ar.alloc<uint64_t>(n + 1);
+  int64_t* lt = ar.alloc<int64_t>(n + 1);
+  int64_t* ltx = ar.alloc<int64_t>(n + 1);
+  GB_ARENA_CHECK(ctx, ar);
+  bin_count<<<grid_for(ctx, n + 1, 256), 256, 0, s>>>(n, a->offsets, sm, lt);
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t1, sm, smx, n + 1, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, lt, ltx, n + 1, s);
+  void* tmp = ar.raw(t1 > t2 ? t1 : t2);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, t1, sm, smx, n + 1, s));
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, t2, lt, ltx, n + 1, s));
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 3);
+  int64_t h[2];
+  GB_CUDA(ctx, cudaMemcpyAsync(h, smx + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  GB_CUDA(ctx, cudaMemcpyAsync(h + 1, ltx + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  GB_CUDA(ctx, cudaStreamSynchronize(s));
+  counts[0] = (int64_t)((uint64_t)h[0] & 0xffffffffull);  // short rows
+  counts[1] = (int64_t)((uint64_t)h[0] >> 32);           // medium rows
+  counts[2] = h[1];                                      // long tiles
+  *sm_out = smx;
+  *lt_out = ltx;
+  return GB_OK;
+}
+
+template <class T, int ADD, int MUL, bool VALS>
+static void launch_binned_k(gb_ctx* ctx, int add_op, int mult_op, const gb_bin_plan* p,
+                            const gb_csr* a, T iso, const T* u, const uint32_t* mask, T* out,
+                            unsigned long long* counters, uint32_t* hasmul) {
+  auto k = mv_pull_binned<T, ADD, MUL, VALS>;
+  k<<<resident_grid(ctx, k, 256), 256, 0, stream_of(ctx)>>>(
+      p->n_long_tiles, p->tile_row, p->tile_beg, p->tile_end, p->n_mid, p->mid_rows, p->n_short,
+      p->short_rows, a->offsets, a->indices, (const T*)a->values, iso, u, mask, add_op, mult_op,
+      out, counters, hasmul);
+}
+
+template <class T, int ADD, int MUL>
+static void launch_binned_v(gb_ctx* ctx, int add_op, int mult_op, const gb_bin_plan* p,
+                            const gb_csr* a, T iso, const T* u, const uint32_t* mask, T* out,
+                            unsigned long long* counters, uint32_t* hasmul) {
+  if (a->values)
+    launch_binned_k<T, ADD, MUL, true>(ctx, add_op, mult_op, p, a, iso, u, mask, out, counters, hasmul);
+  else
+    launch_binned_k<T, ADD, MUL, false>(ctx, add_op, mult_op, p, a, iso, u, mask, out, counters, hasmul);
+}
+
+template <class T>
+static gb_status pull_binned_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a,
+                               const gb_bin_plan* p, const T* u, const uint32_t* mask, T* out,
+                               int64_t* counters) {
+  cudaStream_t s = stream_of(ctx);
+  const int64_t n = a->nrows;
+  const int64_t W = (n + 31) / 32;
+  Arena ar(ctx);
+  uint32_t* hasmul = counters ? ar.alloc<uint32_t>(W) : nullptr;
+  GB_ARENA_CHECK(ctx, ar);
+  const T iso = std::is_same<T, double>::value ? (T)a->iso_f64 : (T)a->iso_i64;
+  if (hasmul) GB_CUDA(ctx, cudaMemsetAsync(hasmul, 0, sizeof(uint32_t) * W, s));
+  fill_identity<T>(ctx, n, op_identity<T>(add_op), out);
+  const int ps = prof_begin(ctx, PROF_MV, a->nnz);
+  unsigned long long* c = (unsigned long long*)counters;
+#define GB_SR(A_, M_)                                                                     \
+  if (add_op == A_ && mult_op == M_) {                                                    \
+    launch_binned_v<T, A_, M_>(ctx, add_op, mult_op, p, a, iso, u, mask, out, c, hasmul); \
+  } else
+  GB_SR(GB_OP_PLUS, GB_OP_TIMES)
+  GB_SR(GB_OP_LOR, GB_OP_LAND)
+  GB_SR(GB_OP_MIN, GB_OP_PLUS)
+  GB_SR(GB_OP_MAX, GB_OP_PLUS)
+  GB_SR(GB_OP_MIN, GB_OP_TIMES)
+  GB_SR(GB_OP_MIN, GB_OP_SECOND)
+  GB_SR(GB_OP_PLUS, GB_OP_LESS)
+  GB_SR(GB_OP_MIN, GB_OP_NE)
+  launch_binned_v<T, -1, -1>(ctx, add_op, mult_op, p, a, iso, u, mask, out, c, hasmul);
+#undef GB_SR
+  prof_end(ctx, ps);
+  if (counters) mv_pull_finish_counts(ctx, W, hasmul, c);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2);
+  return GB_OK;
+}
+
+}  // namespace gb
+
+using namespace gb;
+
+extern "C" {
+
+gb_status gb_bin_plan_counts(gb_ctx* ctx, const gb_csr* a, int64_t* counts_host) {
+  counts_host[0] = counts_host[1] = counts_host[2] = 0;
+  if (a->nrows == 0) return GB_OK;
+  Arena ar(ctx);
+  uint64_t* sm;
+  int64_t* lt;
+  return bin_scan(ctx, ar, a, &sm, &lt, counts_host);
+}
+
+gb_status gb_bin_plan_fill(gb_ctx* ctx, const gb_csr* a, gb_bin_plan* plan) {
+  if (a->nrows == 0) return GB_OK;
+  Arena ar(ctx);
+  uint64_t* sm;
+  int64_t* lt;
+  int64_t c[3];
+  GB_TRY(bin_scan(ctx, ar, a, &sm, &lt, c));
+  if (c[0] != plan->n_short || c[1] != plan->n_mid || c[2] != plan->n_long_tiles)
+    return set_error(ctx, GB_ERR_VALUE, "gb_bin_plan_fill: plan sizes differ from the matrix");
+  bin_fill<<<grid_for(ctx, a->nrows, 256), 256, 0, stream_of(ctx)>>>(
+      a->nrows, a->offsets, sm, lt, const_cast<int32_t*>(plan->short_rows),
+      const_cast<int32_t*>(plan->mid_rows), const_cast<int32_t*>(plan->tile_row),
+      const_cast<int64_t*>(plan->tile_beg), const_cast<int64_t*>(plan->tile_end));
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  GB_CUDA(ctx, cudaStreamSynchronize(stream_of(ctx)));
+  return GB_OK;
+}
+
+gb_status gb_mxv_pull_binned(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const gb_csr* a,
+                             const gb_bin_plan* plan, const void* u, const uint32_t* mask,
+                             void* out, int64_t* counters) {
+  if (a->nrows == 0) return GB_OK;
+  if (!plan || !fold_commutes(add_op))
+    return set_error(ctx, GB_ERR_VALUE, "gb_mxv_pull_binned: needs a plan and a commutative fold");
+  if (a->dtype == GB_I64)
+    return pull_binned_t<int64_t>(ctx, add_op, mult_op, a, plan, (const int64_t*)u, mask,
+                                  (int64_t*)out, counters);
+  return pull_binned_t<double>(ctx, add_op, mult_op, a, plan, (const double*)u, mask,
+                               (double*)out, counters);
+}
+
+}  // extern "C"

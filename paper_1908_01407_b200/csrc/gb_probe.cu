@@ -30,9 +30,57 @@ probe_kernel(const uint32_t* __restrict__ bm, uint32_t nbits, int iters, uint32_
   if (acc == 0x9e3779b9u) sink[0] = acc;
 }
 
+// The gather ceiling of a pull SpMV on a given matrix: stream the column
+// indices (256-bit loads, as the pull kernels do) and gather x[col] for every
+// stored entry with nothing else -- no rows, mask, fold or output.  Its rate
+// (gathers/s) is what a pull kernel over the same column sequence can at
+// best reach when the random 8-byte gathers, not HBM bandwidth, bound it.
+__global__ void __launch_bounds__(256)
+gather_replay_kernel(int64_t nnz, const int32_t* __restrict__ idx, const double* __restrict__ x,
+                     double* sink) {
+  double acc = 0.0;
+  const int64_t groups = nnz / 8;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int32_t c[8];
+    ld_stream8(idx + 8 * g, c);
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = ld_gather(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += v[k];
+  }
+  if (acc == -1.2345) sink[0] = acc;
+}
+
 }  // namespace gb
 
 using namespace gb;
+
+extern "C" gb_status gb_gather_replay_rate(gb_ctx* ctx, const gb_csr* a, const double* x,
+                                           double* gathers_per_s_host) {
+  cudaStream_t s = stream_of(ctx);
+  Arena ar(ctx);
+  double* sink = ar.alloc<double>(1);
+  GB_ARENA_CHECK(ctx, ar);
+  const int grid = resident_grid(ctx, gather_replay_kernel, 256);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  gather_replay_kernel<<<grid, 256, 0, s>>>(a->nnz, a->indices, x, sink);  // warm-up
+  cudaEventRecord(e0, s);
+  gather_replay_kernel<<<grid, 256, 0, s>>>(a->nnz, a->indices, x, sink);
+  cudaEventRecord(e1, s);
+  GB_LAUNCH_CHECK(ctx);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  count_launch(ctx, 2);
+  *gathers_per_s_host = (double)(a->nnz / 8 * 8) / (ms * 1e-3);
+  return GB_OK;
+}
 
 extern "C" gb_status gb_probe_rate(gb_ctx* ctx, int64_t words, int64_t min_probes,
                                    double* probes_per_s_host) {

@@ -11,6 +11,7 @@ direction log; the algorithms call fused drivers instead (algorithms.py).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -180,11 +181,54 @@ def _spmv_pull(semiring, A, u, mask, desc, transpose):
     out = empty(o.nrows, dtype)
     cnt = _counters_tensor()
     part = _lib.PART_ROW if desc.partition is Partition.ROW_SPLIT else _lib.PART_NONZERO
-    plan, _pk = o.row_plan()
-    _ctx().call("gb_mxv_pull", add, mult, C.byref(s), C.byref(plan), _lib.ptr(uv), _lib.ptr(bm),
-                early, part, _lib.ptr(out), _lib.ptr(cnt))
+    view = None
+    if _use_bins(bm, add, early, part):
+        bins, _bk = o.bin_plan()
+        _ctx().call("gb_mxv_pull_binned", add, mult, C.byref(s), C.byref(bins), _lib.ptr(uv),
+                    _lib.ptr(bm), _lib.ptr(out), _lib.ptr(cnt))
+    elif (view := _ordered_view(A, o, transpose, add, early, part)) is not None:
+        ov, oplan, _keep, order, reach = view
+        so, _ko = ov.csr_struct(dtype)
+        _ctx().call("gb_mxv_pull_ordered", add, mult, C.byref(so), C.byref(oplan), _lib.ptr(order),
+                    reach, _lib.ptr(uv), _lib.ptr(bm), _lib.ptr(out), _lib.ptr(cnt))
+    else:
+        plan, _pk = o.row_plan()
+        _ctx().call("gb_mxv_pull", add, mult, C.byref(s), C.byref(plan), _lib.ptr(uv),
+                    _lib.ptr(bm), early, part, _lib.ptr(out), _lib.ptr(cnt))
     _merge_counters(desc, cnt)
     return Vector._wrap(o.nrows, None, out, identity, dtype)
+
+
+# The masked pull runs on the degree-ordered layout (gb_mxv_pull_ordered) for
+# large power-law matrices: the layout is built once per matrix (~0.2 s and
+# one relabelled copy of the structure at s24, shared with bfs) and makes the
+# gathered part of u a dense, L2-resident prefix whose head sits in shared
+# memory.  Measured at s24 with a 50 % mask it gains 5 % in the kernel and
+# loses it to the per-call permutation (1.32 + 0.08 vs 1.40 ms), and the
+# shared-memory head made it slower (2.2 ms: the L1 it displaces held more
+# hits), so it is opt-in: GB_MV_ORDERED=1.
+_MV_ORDERED = os.environ.get("GB_MV_ORDERED", "")
+
+
+# Row bins (gb_mxv_pull_binned) for masked pulls and Partition.ROW_SPLIT:
+# rows are mask-tested before their entries are read, so masked-out rows cost
+# one bit probe instead of their share of the edge-balanced tiles.
+# GB_MV_BINS=0 disables, =1 also takes unmasked pulls.
+_MV_BINS = os.environ.get("GB_MV_BINS", "")
+
+
+def _use_bins(bm, add, early, part):
+    if _MV_BINS == "0" or early or add not in _lib.COMMUTATIVE_FOLD_IDS:
+        return False
+    return bm is not None or part == _lib.PART_ROW or _MV_BINS == "1"
+
+
+def _ordered_view(A, o, transpose, add, early, part):
+    if _MV_ORDERED != "1" or early or part == _lib.PART_ROW:
+        return None
+    if add not in _lib.COMMUTATIVE_FOLD_IDS or A.nrows != A.ncols or A._csc is None:
+        return None
+    return A.ordered_pull(transpose)
 
 
 def spmv_pull(semiring: Semiring, A: SparseMatrix, u: Vector, mask=None, desc=None) -> Vector:

@@ -65,6 +65,10 @@ got = w._vals
 err = float((got - ref).abs().max())
 rel = float(((got - ref).abs() / ref.abs().clamp_min(1e-300)).max())
 
+import ctypes  # noqa: E402
+rate = ctypes.c_double(0)
+st, _k = A._csr.csr_struct(np.float64)
+ctx.call("gb_gather_replay_rate", ctypes.byref(st), _lib.ptr(x), ctypes.byref(rate))
 c = d.counters
 R = int(((torch.diff(off) > 0) & allowed).sum())
 E_read = c.matrix_entries_read
@@ -75,4 +79,6 @@ print(json.dumps({
     "multiplies": c.semiring_multiplies, "adds": c.semiring_adds,
     "kernel_ms": round(kernel_ms, 4), "call_ms": round(call_ms, 4),
     "bytes_alg": int(bytes_alg), "GBps": round(bytes_alg / (kernel_ms * 1e-3) / 1e9, 1),
+    "gather_ceiling_G_s": round(rate.value / 1e9, 1),
+    "gathers_G_s": round(E_read / (kernel_ms * 1e-3) / 1e9, 1),
     "max_abs_err": err, "max_rel_err": rel}))
