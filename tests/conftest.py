@@ -13,6 +13,7 @@ for p in (ROOT, HERE):
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built library")
     config.addinivalue_line("markers", "slow: long-running parity case")
+    config.addinivalue_line("markers", "reference_suite: the reference's own tests, run unchanged")
 
 
 def cuda_available():
