@@ -121,6 +121,25 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
+def bench_config(args, n, m):
+    """The config object, identical in both arms (same workload, same graph)."""
+    return {"workload": f"bfs(A, {args.source}) on rmat-s{args.scale}-e16 symmetrised",
+            "n": n, "nnz": m,
+            "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB)" % ((m * 4 + (n + 1) * 8) / 1e9)}
+
+
+def cpu_model():
+    """lscpu's model name (the host the CPU baseline ran on)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or platform.machine()
+
+
 def measured_peaks():
     p = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -152,7 +171,7 @@ def ctx_ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def masked_spmv(gb, A, ctx, peak, peak_src, reps=10, density=0.5):
+def masked_spmv(gb, A, ctx, peak, peak_src, reps=10, density=0.5, graph="rmat"):
     """The second half of the BASELINE metric: masked pull SpMV at the bench
     scale through the public API, w<!m> = A (+.*) x (x dense f64, m a seeded
     50 % mask, complemented; forced pull), timed per kernel with events.
@@ -210,8 +229,27 @@ def masked_spmv(gb, A, ctx, peak, peak_src, reps=10, density=0.5):
     rel = float(((w._vals - ref).abs() / ref.abs().clamp_min(1e-300)).max())
     del rows, keep, ref
     achieved = bytes_alg / (t_ms * 1e-3) / 1e9
-    return {"workload": "mxv(PlusMultiplies f64, A, x dense, mask=~m, m 50 % seeded), forced pull",
+    # A/B: the same call through the edge-balanced row tiles (the reference's
+    # nonzero split) instead of the row bins (its row split)
+    from paper_1908_01407_b200 import kernels as _k
+    saved = _k._MV_BINS
+    _k._MV_BINS = "0"
+    try:
+        run()
+        torch.cuda.synchronize()
+        ctx.profiling(True)
+        for _ in range(reps):
+            run()
+        torch.cuda.synchronize()
+        tiles_ms = float(np.median([t for (kind, _a, t) in ctx.prof_read() if kind == 8]))
+        ctx.profiling(False)
+    finally:
+        _k._MV_BINS = saved
+    return {"workload": f"mxv(PlusMultiplies f64, A={graph}, x dense, mask=~m, m {density:.0%} "
+                        "seeded), forced pull",
             "kernel": "mv_pull_binned (row bins, mask tested per row)",
+            "ab_ms": {"row_bins (default; Partition.ROW_SPLIT)": round(t_ms, 4),
+                      "row_tiles (edge-balanced)": round(tiles_ms, 4)},
             "achieved": round(achieved, 1), "peak": peak,
             "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
             "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4),
@@ -339,6 +377,38 @@ def config_sweep(gb, scales=(16, 20, 22, 24, 26)):
     return out
 
 
+def uniform_sweep(gb, ctx, peak, peak_src, scale=24):
+    """SURVEY §8(d) "uniform" row: the same generator with a=b=c=d=.25 at the
+    benchmark scale -- BFS and CC against the C oracle on the same CSR, and
+    the masked pull SpMV (row bins vs row tiles) against torch."""
+    import torch
+    from oracle import cgraph
+    from paper_1908_01407_b200.io import rmat_matrix
+    A = rmat_matrix(scale, a=0.25, b=0.25, c=0.25, d=0.25)
+    n, m = A.nrows, A.nnz
+    bms, lv = _dev_ms(lambda: gb.bfs(A, 0), 10)
+    cms, lab = _dev_ms(lambda: gb.connected_components(A), 2)
+    rp, ci = A._csr.offsets.cpu().numpy(), A._csr.indices.cpu().numpy()
+    bcs, (want, trace) = _cpu_s(lambda: cgraph.bfs(rp, ci, 0))
+    ccs, (wlab, _t) = _cpu_s(lambda: cgraph.cc(rp, ci))
+    d = gb.Descriptor()
+    gb.bfs(A, 0, desc=d)
+    out = {"graph": f"uniform-s{scale}-e16 (a=b=c=d=.25) symmetrised", "n": n, "nnz": m,
+           "bfs_gpu_ms": round(bms, 3), "bfs_gteps": round(m / bms / 1e6, 1),
+           "bfs_cpu_ms": round(bcs * 1e3, 1), "bfs_trace": [(x.chosen, x.frontier_nvals)
+                                                           for x in d.direction_log],
+           "cc_gpu_ms": round(cms, 3), "cc_cpu_ms": round(ccs * 1e3, 1),
+           "parity": bool(np.array_equal(lv.values, want) and np.array_equal(lab.values, wlab)
+                          and [t[:2] for t in trace] == [(x.chosen, x.frontier_nvals)
+                                                         for x in d.direction_log])}
+    del rp, ci, want, wlab, lv, lab
+    out["masked_spmv"] = masked_spmv(gb, A, ctx, peak, peak_src, graph=f"uniform-s{scale}")
+    A = None
+    ctx.trim()
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -433,6 +503,9 @@ def run_ours(args):
     ctx.profiling(False)
     trace = [(d.chosen, d.frontier_nvals) for d in desc.direction_log]
     levels_host = lv.values
+    deg_all = np.diff(A._csr.offsets.cpu().numpy())
+    g500_edges = int(deg_all[levels_host > 0].sum()) // 2
+    del deg_all
     counts = np.bincount(levels_host, minlength=len(trace) + 2)
     roof = None
     peak, peak_src = measured_peaks()
@@ -475,6 +548,20 @@ def run_ours(args):
             "frac": round(probes_s / rate.value, 3)}
 
     mspmv = masked_spmv(gb, A, ctx, peak, peak_src) if world == 1 and not args.no_spmv else None
+
+    # ---- BFS tree (north star "levels/parents-validity"): min-id parents
+    # derived on the device, Graph500-style validation of (levels, parents)
+    tree = None
+    if world == 1:
+        pms, (tl, tp) = _dev_ms(lambda: gb.bfs_parents(A, args.source), 5)
+        val = gb.validate_bfs(A, args.source, tl, tp)
+        tree = {"bfs_plus_parents_ms": round(pms, 4),
+                "parents_only_ms": round(pms - ms, 4),
+                "validate": val,
+                "rule": "parent[v] = smallest neighbour one level up (deterministic); "
+                        "validated: source, tree edges exist one level up, unreached -> -1, "
+                        "every edge spans <= 1 level"}
+        del tl, tp
 
     # ---- end-to-end through the public API (host result every step) --------
     # warm-up: the first calls allocate the pinned staging blocks (~57 ms each
@@ -549,14 +636,37 @@ def run_ours(args):
                "kind": "port",
                "sample": f"full BFS from vertex {args.source} on the same s{args.scale} CSR, "
                          f"oracle/cgraph.c og_bfs with {threads} OpenMP threads, mean of {len(times)} runs",
-               "ms_per_bfs": round(cpu_s * 1e3, 2), "cpu": platform.processor() or platform.machine()}
+               "ms_per_bfs": round(cpu_s * 1e3, 2), "cpu": cpu_model(),
+               "os_cpu_count": os.cpu_count()}
 
+    if cpu is not None:
+        # the same BFS with ONE host thread (the reference's pull pool often
+        # does not help); one run
+        from oracle import cgraph
+        rp = A._csr.offsets.cpu().numpy()
+        ci = A._csr.indices.cpu().numpy()
+        prev = cgraph.threads()
+        cgraph.set_threads(1)
+        try:
+            t1 = time.perf_counter()
+            cgraph.bfs(rp, ci, args.source)
+            one = time.perf_counter() - t1
+        finally:
+            cgraph.set_threads(prev)
+        cpu["one_thread"] = {"value": round(m / one / 1e9, 4), "unit": "GTEPS", "cores": 1,
+                             "ms_per_bfs": round(one * 1e3, 1)}
+        del rp, ci
     configs = None
+    uniform = None
     if rank == 0 and world == 1 and not args.no_configs:
         del A
         ctx.trim()
         torch.cuda.empty_cache()
         configs = config_sweep(gb)
+        try:
+            uniform = uniform_sweep(gb, ctx, peak, peak_src, args.scale)
+        except Exception as e:  # noqa: BLE001 -- report, never lose the bench line
+            uniform = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     if rank == 0:
         line = {
@@ -565,11 +675,13 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32/i64 (bitmaps, int32 indices, int64 levels)",
             "data": "synthetic R-MAT (reference SplitMix64 generator, seed 1), generated on GPU",
-            "config": {"workload": f"bfs(A, {args.source}) on rmat-s{args.scale}-e16 symmetrised",
-                       "n": n, "nnz": m, "global_batch": 1, "seq_len": None,
-                       "parallelism": f"1d-vertex-partition x{world}" if world > 1 else "single-gpu",
-                       "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB)" % ((m * 4 + (n + 1) * 8) / 1e9),
-                       "build_s": round(build_s, 2), "trace": trace},
+            "config": bench_config(args, n, m),
+            "parallelism": f"1d-vertex-partition x{world}" if world > 1 else "single-gpu",
+            "build_s": round(build_s, 2), "trace": trace,
+            "graph500_gteps": round(g500_edges / (ms * 1e-3) / 1e9, 3),
+            "graph500_what": "Graph500-style TEPS: undirected edges with both endpoints in the "
+                             "source's component (stored entries of reached vertices / 2) per "
+                             "second, same device time as `value`",
             "clocks": clocks.summary(),
             "e2e": {"value": round(m / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GTEPS",
                     "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": 8,
@@ -584,9 +696,11 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": roof,
             "masked_spmv": mspmv,
+            "bfs_tree": tree,
             "cpu_baseline": cpu,
             "parity_vs_oracle": parity,
             "configs": configs,
+            "uniform": uniform,
         }
         print(json.dumps(line))
     if world > 1:
@@ -631,10 +745,10 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8/i64", "data": "synthetic R-MAT (reference generator, seed 1)",
             "impl": "reference",
-            "config": {"workload": f"bfs(A, {args.source}) on rmat-s{args.scale}-e16 symmetrised",
-                       "n": n, "nnz": m, "build_s": round(build_s, 2)},
+            "config": bench_config(args, n, m), "build_s": round(build_s, 2),
             "cpu_baseline": {"value": round(value, 4), "unit": "GTEPS", "cores": threads,
-                             "kind": "port", "sample": sample},
+                             "kind": "port", "sample": sample, "cpu": cpu_model(),
+                             "os_cpu_count": os.cpu_count()},
             "e2e": {"value": round(value, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

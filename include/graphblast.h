@@ -483,6 +483,23 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
  * previous setting; process-wide. */
 int32_t gb_bfs_engine(int32_t engine);
 
+/* BFS parents (extension; the reference returns levels only,
+ * algorithms.py:66-77): parent[v] = the smallest u with (u, v) stored in A and
+ * level[u] = level[v] - 1; parent[source] = source; -1 when unreached.
+ * `in_edges` = rows of A^T (the CSR itself for a symmetric matrix), `levels`
+ * a bfs result (1-based, 0 = unreached).  Asynchronous. */
+gb_status gb_bfs_parents(gb_ctx* ctx, const gb_csr* in_edges, const int64_t* levels,
+                         int64_t source, int64_t* parents);
+
+/* Graph500-style validation of a BFS tree: errors_host[4] counts violations of
+ * {source is its own parent at level 1; every reached v != source has a
+ * reached parent one level up with (parent, v) stored; unreached vertices
+ * have parent -1; every stored (u, v) with u reached has v reached and
+ * level[v] <= level[u] + 1 (for a symmetric matrix: both ends reached or
+ * neither, at most one level apart)}.  Synchronizes. */
+gb_status gb_bfs_validate(gb_ctx* ctx, const gb_csr* a, const gb_csr* in_edges, int64_t source,
+                          const int64_t* levels, const int64_t* parents, int64_t* errors_host);
+
 /* bfs (algorithms.py:48-77) over the degree-ordered relabelling of the
  * matrix (gb_csr_relabel_t): `push`/`pull`/`pull_nonempty` are the relabelled
  * orientations, rank[i] the new id of vertex i.  `source` and `levels` use

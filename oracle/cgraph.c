@@ -531,3 +531,33 @@ int64_t og_tc(int64_t n, const int64_t* rp, const int32_t* ci) {
   free(byrank);
   return total;
 }
+
+/* ------------------------------------------------------------------------ */
+/* BFS parents (the north star's "levels/parents" extension; the reference   */
+/* returns levels only, algorithms.py:66-77): parent[v] = the smallest u in  */
+/* v's in-edge row (cp/ri, ascending) with level[u] = level[v] - 1;          */
+/* parent[source] = source; -1 when unreached.  Returns the number of        */
+/* reached vertices without such a u (0 for a consistent level vector).      */
+/* ------------------------------------------------------------------------ */
+int64_t og_bfs_parents(int64_t n, const int64_t* cp, const int32_t* ri, const int64_t* lv,
+                       int64_t source, int64_t* parent) {
+  int64_t bad = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : bad)
+  for (int64_t v = 0; v < n; ++v) {
+    if (lv[v] == 0) {
+      parent[v] = -1;
+    } else if (v == source) {
+      parent[v] = source;
+    } else {
+      int64_t p = -1;
+      for (int64_t k = cp[v]; k < cp[v + 1]; ++k)
+        if (lv[ri[k]] == lv[v] - 1) {
+          p = ri[k];
+          break;
+        }
+      parent[v] = p;
+      bad += p < 0;
+    }
+  }
+  return bad;
+}

@@ -44,6 +44,8 @@ def lib():
         L.og_cc.argtypes = [i64, vp, vp, vp, vp, i64, f64, C.c_int, C.c_int, vp, vp, vp, vp]
         L.og_upper_weights.restype = i64
         L.og_upper_weights.argtypes = [i64, vp, vp, u64, i64, i64, vp]
+        L.og_bfs_parents.restype = i64
+        L.og_bfs_parents.argtypes = [i64, vp, vp, vp, i64, vp]
         L.og_tc.restype = i64
         L.og_tc.argtypes = [i64, vp, vp]
         _lib = L
@@ -114,6 +116,17 @@ def bfs(rp, ci, source=0, cp=None, ri=None, max_iters=None, ratio=0.1, policy=0)
     k = lib().og_bfs(n, _p(rp), _p(ci), _p(cp), _p(ri), source, iters, ratio, policy, _p(lv),
                      _p(d), _p(nv), _p(est))
     return lv, _trace(d, nv, est, k)
+
+
+def bfs_parents(rp, ci, levels, source=0, cp=None, ri=None):
+    """Min-id BFS parents derived from a level vector (og_bfs_parents)."""
+    rp, ci = _csr(rp, ci)
+    cp, ri = (rp, ci) if cp is None else _csr(cp, ri)
+    lv = np.ascontiguousarray(levels, np.int64)
+    par = np.empty(lv.size, np.int64)
+    bad = lib().og_bfs_parents(lv.size, _p(cp), _p(ri), _p(lv), int(source), _p(par))
+    assert bad == 0, "level vector is not a BFS layering"
+    return par
 
 
 def sssp(rp, ci, w, source=0, cp=None, ri=None, wt=None, ratio=0.1, policy=0):

@@ -108,6 +108,8 @@ SIGNATURES = {
     "gb_bfs_ordered_async": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), vp, vp, i64, i64,
                                    f64, i32, vp, vp, vp, vp]),
     "gb_count_launches": (None, [vp, i64]),
+    "gb_bfs_parents": (i32, [vp, C.POINTER(gb_csr), vp, i64, vp]),
+    "gb_bfs_validate": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, vp, vp, vp]),
     "gb_bfs_engine": (i32, [i32]),
     "gb_degree_order": (i32, [vp, i64, vp, vp, vp]),
     "gb_csr_relabel_t": (i32, [vp, C.POINTER(gb_csr), vp, vp, vp, vp, vp]),

@@ -251,6 +251,41 @@ def bfs(A: SparseMatrix, source: int, desc=None, early_exit=True) -> Vector:
     return Vector._wrap(n, None, levels, 0, np.int64)
 
 
+def bfs_parents(A: SparseMatrix, source: int, desc=None):
+    """Extension beyond the reference (which returns levels only,
+    algorithms.py:66-77; BASELINE.json north star "BFS levels/parents"):
+    ``(levels, parents)`` where ``levels`` is exactly ``bfs(A, source)`` and
+    ``parents`` a BFS tree derived from it on the device (gb_bfs_parents):
+    parent[v] = the smallest u with (u, v) stored in A and level[u] =
+    level[v] - 1, parent[source] = source, -1 when unreached."""
+    levels = bfs(A, source, desc)
+    n = A.nrows
+    parents = empty(n, np.int64)
+    s, _k = A.orient(True).csr_struct()   # in-edges: rows of A^T (FormatError without CSC)
+    _lib.context().call("gb_bfs_parents", C.byref(s), _lib.ptr(levels._vals), int(source),
+                        _lib.ptr(parents))
+    return levels, Vector._wrap(n, None, parents, -1, np.int64)
+
+
+def validate_bfs(A: SparseMatrix, source: int, levels, parents) -> dict:
+    """Graph500-style validation of a BFS tree on the device
+    (gb_bfs_validate): violation counts of the four checks; ``ok`` when all
+    are zero.  ``levels``/``parents`` are Vectors from bfs_parents (or any
+    int64 vectors of the same meaning)."""
+    _require_square(A)
+    s, _k1 = A.orient(False).csr_struct()
+    t, _k2 = A.orient(True).csr_struct()
+    lv = levels.to_dense(0)._vals if isinstance(levels, Vector) else levels
+    pa = parents.to_dense(-1)._vals if isinstance(parents, Vector) else parents
+    err = np.zeros(4, np.int64)
+    _lib.context().call("gb_bfs_validate", C.byref(s), C.byref(t), int(source), _lib.ptr(lv),
+                        _lib.ptr(pa), err.ctypes.data_as(C.c_void_p))
+    names = ("source", "tree_edges", "unreached", "graph_edges")
+    out = {k: int(v) for k, v in zip(names, err)}
+    out["ok"] = not err.any()
+    return out
+
+
 def _bfs_composed(A, source, desc):
     boolean = builtin_semiring("LogicalOrAnd")
     plus = builtin_monoid("Plus")
