@@ -697,6 +697,12 @@ def run_ours(args):
             "roofline": roof,
             "masked_spmv": mspmv,
             "bfs_tree": tree,
+            "exchange": (None if world == 1 else {
+                "per_level_last_step": runner.exchange.log[-len(trace):],
+                "what": "FrontierExchange per level: (mode, bytes sent per rank); dense = "
+                        "allgather of the owned bitmap words (|f|*32 > n), sparse = "
+                        "allgather(v) of the owned new vertex ids; plus one 8 B count "
+                        "allgather", "backend": os.environ.get("GB_DIST_BACKEND", "nccl")}),
             "cpu_baseline": cpu,
             "parity_vs_oracle": parity,
             "configs": configs,

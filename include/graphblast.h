@@ -409,10 +409,28 @@ gb_status gb_bfs_dist_pull(gb_ctx* ctx, const gb_csr* rowblock, int64_t lo, int6
                            uint32_t* vbm, uint32_t* vprev, const uint32_t* fbm, uint32_t* xbm,
                            int64_t* levels);
 /* apply the exchanged new-frontier bitmap xbm: stamp `depth`, rebuild F and
- * fbm; *K_host = global frontier size (synchronizes) */
+ * fbm; *K_host = global frontier size (synchronizes), or K_host = NULL when
+ * the caller knows it from the exchange (asynchronous) */
 gb_status gb_bfs_dist_apply(gb_ctx* ctx, int64_t n, int64_t depth, const uint32_t* xbm,
                             uint32_t* vbm, uint32_t* vprev, uint32_t* fbm, int64_t* levels,
                             int32_t* F, int64_t* K_host);
+
+/* Frontier exchange of the 1D-partitioned BFS (distributed.FrontierExchange).
+ * owned: list this rank's new vertices (owned words of xbm) into ids and
+ *   their count into *count_dev (device int64).  Asynchronous.
+ * pack_words: out[i] = owned word i of xbm, zero padded to wmax words.
+ * unpack_words: xbm[wb[p] + i] = gathered[p*wmax + i] for the P slices
+ *   (wb: device int64[P+1] word bounds).
+ * set_ids: xbm = the bits of every gathered id (rank p: gathered[p*kmax ..
+ *   + counts[p]), counts a device int64[P]). */
+gb_status gb_bfs_dist_owned(gb_ctx* ctx, int64_t lo, int64_t hi, const uint32_t* xbm,
+                            int32_t* ids, int64_t* count_dev);
+gb_status gb_bfs_dist_pack_words(gb_ctx* ctx, int64_t lo, int64_t hi, int64_t wmax,
+                                 const uint32_t* xbm, uint32_t* out);
+gb_status gb_bfs_dist_unpack_words(gb_ctx* ctx, int32_t P, int64_t wmax, const int64_t* wb,
+                                   const uint32_t* gathered, uint32_t* xbm);
+gb_status gb_bfs_dist_set_ids(gb_ctx* ctx, int64_t n, int32_t P, int64_t kmax,
+                              const int64_t* counts, const int32_t* gathered, uint32_t* xbm);
 /* clear the levels of the K vertices in F (loop cap reached, algorithms.py:69) */
 gb_status gb_bfs_dist_unstamp(gb_ctx* ctx, int64_t K, const int32_t* F, int64_t* levels);
 /* entries of every row of `a` whose column lies in [lo, hi): CSR with the

@@ -1988,6 +1988,7 @@ gb_status gb_bfs_dist_apply(gb_ctx* ctx, int64_t n, int64_t depth, const uint32_
                                                         cnt, cnt + 1, xbm, nullptr);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 2);
+  if (!K_host) return GB_OK;  // the frontier size is known from the exchange: stay asynchronous
   return read_i64(ctx, (const int64_t*)cnt, K_host);
 }
 
@@ -1996,6 +1997,106 @@ gb_status gb_bfs_dist_unstamp(gb_ctx* ctx, int64_t K, const int32_t* F, int64_t*
   bfs_unstamp<<<grid_for(ctx, K, 256), 256, 0, stream_of(ctx)>>>(dval(K), F, levels);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 1);
+  return GB_OK;
+}
+
+// ---- frontier exchange (distributed.FrontierExchange) ----------------------
+// After a level each rank holds its OWNED new-frontier words xbm[w_lo, w_hi)
+// (words outside are zero).  The exchange replicates the union: a dense
+// allgather of the owned word slices when the frontier is large (|f|*32 > n,
+// SURVEY §8(e)), else an allgather(v) of the owned vertex ids.
+
+// count the owned new vertices and list them (unordered)
+__global__ void dist_owned_ids(int64_t w_lo, int64_t w_hi, const uint32_t* __restrict__ xbm,
+                               int32_t* __restrict__ ids, unsigned long long* __restrict__ count) {
+  for (int64_t w = w_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < w_hi;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t b = xbm[w];
+    if (!b) continue;
+    unsigned long long at = atomicAdd(count, (unsigned long long)__popc(b));
+    while (b) {
+      const int k = __ffs(b) - 1;
+      b &= b - 1;
+      ids[at++] = (int32_t)(w * 32 + k);
+    }
+  }
+}
+
+__global__ void dist_pack_words(int64_t w_lo, int64_t w_hi, int64_t wmax,
+                                const uint32_t* __restrict__ xbm, uint32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < wmax;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = w_lo + i < w_hi ? xbm[w_lo + i] : 0u;
+}
+
+// xbm[wb[p] + i] = gathered[p * wmax + i] for every rank p (slices tile [0, W))
+__global__ void dist_unpack_words(int32_t P, int64_t wmax, const int64_t* __restrict__ wb,
+                                  const uint32_t* __restrict__ gathered, uint32_t* __restrict__ xbm) {
+  const int64_t total = (int64_t)P * wmax;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(j / wmax);
+    const int64_t i = j - (int64_t)p * wmax;
+    if (wb[p] + i < wb[p + 1]) xbm[wb[p] + i] = gathered[j];
+  }
+}
+
+// set the bits of every gathered id (rank p's ids are gathered[p*kmax, +counts[p]))
+__global__ void dist_set_ids(int32_t P, int64_t kmax, const int64_t* __restrict__ counts,
+                             const int32_t* __restrict__ gathered, uint32_t* __restrict__ xbm) {
+  const int64_t total = (int64_t)P * kmax;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(j / kmax);
+    if (j - (int64_t)p * kmax < counts[p]) {
+      const int32_t v = gathered[j];
+      atomicOr(xbm + (v >> 5), 1u << (v & 31));
+    }
+  }
+}
+
+gb_status gb_bfs_dist_owned(gb_ctx* ctx, int64_t lo, int64_t hi, const uint32_t* xbm,
+                            int32_t* ids, int64_t* count_dev) {
+  cudaStream_t s = stream_of(ctx);
+  GB_CUDA(ctx, cudaMemsetAsync(count_dev, 0, sizeof(int64_t), s));
+  const int64_t w_lo = lo / 32, w_hi = (hi + 31) / 32;
+  if (w_hi > w_lo)
+    dist_owned_ids<<<grid_for(ctx, w_hi - w_lo, 256), 256, 0, s>>>(
+        w_lo, w_hi, xbm, ids, (unsigned long long*)count_dev);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_pack_words(gb_ctx* ctx, int64_t lo, int64_t hi, int64_t wmax,
+                                 const uint32_t* xbm, uint32_t* out) {
+  if (wmax <= 0) return GB_OK;
+  dist_pack_words<<<grid_for(ctx, wmax, 256), 256, 0, stream_of(ctx)>>>(lo / 32, (hi + 31) / 32,
+                                                                         wmax, xbm, out);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_unpack_words(gb_ctx* ctx, int32_t P, int64_t wmax, const int64_t* wb,
+                                   const uint32_t* gathered, uint32_t* xbm) {
+  if (wmax <= 0 || P <= 0) return GB_OK;
+  dist_unpack_words<<<grid_for(ctx, (int64_t)P * wmax, 256), 256, 0, stream_of(ctx)>>>(
+      P, wmax, wb, gathered, xbm);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_set_ids(gb_ctx* ctx, int64_t n, int32_t P, int64_t kmax,
+                              const int64_t* counts, const int32_t* gathered, uint32_t* xbm) {
+  cudaStream_t s = stream_of(ctx);
+  GB_CUDA(ctx, cudaMemsetAsync(xbm, 0, sizeof(uint32_t) * ((n + 31) / 32), s));
+  if (kmax > 0 && P > 0)
+    dist_set_ids<<<grid_for(ctx, (int64_t)P * kmax, 256), 256, 0, s>>>(P, kmax, counts, gathered,
+                                                                       xbm);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 2);
   return GB_OK;
 }
 

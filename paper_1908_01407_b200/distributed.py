@@ -14,12 +14,16 @@ two ranks.  Each rank stores
   direction expands the replicated frontier list over it, so only owned
   vertices are ever marked.
 
-Per BFS level there is ONE collective: the ranks' owned words of the
-new-frontier bitmap (n/8 bytes; disjoint across ranks) are combined with an
-all-reduce SUM.  Every rank then applies the same global bitmap, so the
-frontier count, the push/pull decision (the reference rule,
-kernels.py:108-126) and the level vector are identical and replicated -- no
-all-to-all and no allgatherv are needed.
+Per BFS level the new frontier is replicated by the exchange the north star
+names (FrontierExchange): every rank lists its owned new vertices and the P
+counts are allgathered (8 B per rank; their sum is the global frontier size
+|f|, so no separate reduction or read-back is needed); then either a dense
+ALLGATHER of the owned bitmap word slices (|f|*32 > n: n/8 bytes in total)
+or an ALLGATHERV of the owned vertex ids (4 B per new vertex; NCCL has no
+native allgatherv, so the lists are padded to the largest count).  Every
+rank then applies the same global bitmap, so the frontier count, the
+push/pull decision (the reference rule, kernels.py:108-126) and the level
+vector are identical and replicated -- no all-to-all is needed.
 """
 
 from __future__ import annotations
@@ -123,6 +127,8 @@ class NativeSteps:
         self.fbm = torch.empty(W, dtype=torch.int32, device=dev)
         self.xbm = torch.empty(W, dtype=torch.int32, device=dev)
         self.F = torch.empty(n, dtype=torch.int32, device=dev)
+        self.ids = torch.empty(max(g.hi - g.lo, 1), dtype=torch.int32, device=dev)
+        self.count = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def init(self, source):
         p = _lib.ptr
@@ -140,27 +146,108 @@ class NativeSteps:
                       int(depth), p(self.vbm), p(self.vprev), p(self.fbm), p(self.xbm),
                       p(self.levels))
 
-    def apply(self, depth):
+    def apply(self, depth, K=None):
+        """Stamp the replicated new frontier.  K known (from the exchange): no
+        read-back; otherwise the count is read (synchronizes)."""
         p = _lib.ptr
-        K = C.c_int64(0)
+        k = C.c_int64(0)
         self.ctx.call("gb_bfs_dist_apply", self.g.n, int(depth), p(self.xbm), p(self.vbm),
-                      p(self.vprev), p(self.fbm), p(self.levels), p(self.F), C.byref(K))
-        return int(K.value)
+                      p(self.vprev), p(self.fbm), p(self.levels), p(self.F),
+                      None if K is not None else C.byref(k))
+        return int(K) if K is not None else int(k.value)
+
+    # -- frontier exchange steps (gb_bfs_dist_owned / pack / unpack / set_ids)
+    def owned(self):
+        """Device int64[1]: this rank's new vertices (listed in self.ids)."""
+        g = self.g
+        self.ctx.call("gb_bfs_dist_owned", g.lo, g.hi, _lib.ptr(self.xbm), _lib.ptr(self.ids),
+                      _lib.ptr(self.count))
+        return self.count
+
+    def pack_words(self, wmax):
+        out = torch.empty(max(wmax, 1), dtype=torch.int32, device=self.xbm.device)
+        self.ctx.call("gb_bfs_dist_pack_words", self.g.lo, self.g.hi, int(wmax),
+                      _lib.ptr(self.xbm), _lib.ptr(out))
+        return out[:wmax]
+
+    def unpack_words(self, gathered, wmax, wb):
+        self.ctx.call("gb_bfs_dist_unpack_words", int(wb.numel() - 1), int(wmax), _lib.ptr(wb),
+                      _lib.ptr(gathered), _lib.ptr(self.xbm))
+
+    def owned_ids(self, kmax):
+        return self.ids[:kmax] if kmax <= self.ids.numel() else torch.cat(
+            [self.ids, self.ids.new_zeros(kmax - self.ids.numel())])
+
+    def set_ids(self, gathered, counts, kmax):
+        self.ctx.call("gb_bfs_dist_set_ids", self.g.n, int(counts.numel()), int(kmax),
+                      _lib.ptr(counts), _lib.ptr(gathered), _lib.ptr(self.xbm))
 
     def unstamp(self, K):
         self.ctx.call("gb_bfs_dist_unstamp", int(K), _lib.ptr(self.F), _lib.ptr(self.levels))
 
 
-class TorchExchange:
-    """The frontier exchange: all-reduce SUM of the disjoint owned bitmap words."""
+class FrontierExchange:
+    """The per-level frontier exchange of the north star: allgather of the
+    owned new-frontier counts, then a dense allgather of the owned bitmap
+    word slices (|f|*32 > n) or an allgather(v) of the owned vertex ids.
+    Returns the global frontier size; ``log`` records (mode, bytes sent per
+    rank) per level."""
 
     def __init__(self, group=None):
         self.group = group
+        self.log = []
+        self._wb = None
 
-    def allreduce_words(self, xbm: torch.Tensor):
+    def _world(self):
         import torch.distributed as dist
-        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            dist.all_reduce(xbm, op=dist.ReduceOp.SUM, group=self.group)
+        if dist.is_initialized():
+            return dist.get_world_size(self.group)
+        return 1
+
+    def _allgather(self, t):
+        """Equal-length 1-D tensors of every rank, concatenated in rank order."""
+        import torch.distributed as dist
+        P = dist.get_world_size(self.group)
+        if dist.get_backend(self.group) == "nccl":
+            out = torch.empty(P * t.numel(), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(P)]
+        dist.all_gather(parts, t.contiguous(), group=self.group)
+        return torch.cat(parts)
+
+    def word_bounds(self, g, device):
+        if self._wb is None or self._wb[0] is not g:
+            W = (g.n + 31) // 32
+            wb = [min(b // 32, W) for b in g.bounds[:-1]] + [W]
+            self._wb = (g, torch.tensor(wb, dtype=torch.int64, device=device),
+                        max(b - a for a, b in zip(wb, wb[1:])))
+        return self._wb[1], self._wb[2]
+
+    def __call__(self, steps, g) -> int:
+        count = steps.owned()
+        P = self._world()
+        if P == 1:
+            total = int(count.item())
+            self.log.append(("local", 0))
+            return total
+        counts = self._allgather(count)
+        ch = counts.cpu().tolist()                      # the one host read per level
+        total = int(sum(ch))
+        if total * 32 > g.n:
+            wb, wmax = self.word_bounds(g, count.device)
+            gathered = self._allgather(steps.pack_words(wmax))
+            steps.unpack_words(gathered, wmax, wb)
+            self.log.append(("dense", 4 * wmax))
+        else:
+            kmax = max(ch)
+            if kmax > 0:
+                gathered = self._allgather(steps.owned_ids(kmax))
+            else:
+                gathered = count.new_zeros(0, dtype=torch.int32)
+            steps.set_ids(gathered, counts, kmax)
+            self.log.append(("sparse", 4 * kmax))
+        return total
 
 
 def bfs_partitioned(g: BlockGraph, source: int, desc=None, steps=None, exchange=None):
@@ -171,7 +258,7 @@ def bfs_partitioned(g: BlockGraph, source: int, desc=None, steps=None, exchange=
         raise IndexError(f"source {source} out of range")
     desc = desc if desc is not None else Descriptor()
     steps = steps if steps is not None else NativeSteps(g)
-    exchange = exchange if exchange is not None else TorchExchange()
+    exchange = exchange if exchange is not None else FrontierExchange()
     steps.init(source)
     K, depth = 1, 1
     iters = min(desc.max_niter, g.n + 1)
@@ -182,8 +269,8 @@ def bfs_partitioned(g: BlockGraph, source: int, desc=None, steps=None, exchange=
             steps.pull(depth + 1)
         else:
             steps.push(K)
-        exchange.allreduce_words(steps.xbm)
-        K = steps.apply(depth + 1)
+        K = exchange(steps, g)
+        steps.apply(depth + 1, K)
         if K == 0:
             break
         depth += 1
@@ -297,7 +384,7 @@ class OrderedPartitionedBfs:
         Ar = SparseMatrix._wrap(A.nrows, A.ncols, push_o, pull_o, A.dtype, A._sym)
         self.block = BlockGraph.from_matrix(Ar, rank, world, bounds)
         self.steps = NativeSteps(self.block)
-        self.exchange = TorchExchange(group)
+        self.exchange = FrontierExchange(group)
         self.rank64 = A._rank64()
         self.out = torch.empty(A.nrows, dtype=torch.int64, device=push_o.offsets.device)
 
@@ -325,5 +412,5 @@ def bfs(A_or_block, source, desc=None, group=None, ordered=True):
             run = OrderedPartitionedBfs(A_or_block, rank, world, group)
             return Vector._wrap(A_or_block.nrows, None, run(source, desc).clone(), 0, np.int64)
         g = BlockGraph.from_matrix(A_or_block, rank, world)
-    levels = bfs_partitioned(g, source, desc, exchange=TorchExchange(group))
+    levels = bfs_partitioned(g, source, desc, exchange=FrontierExchange(group))
     return Vector._wrap(g.n, None, levels, 0, np.int64)

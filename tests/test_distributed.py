@@ -1,8 +1,9 @@
 """Multi-rank host logic of the 1D-partitioned BFS, on CPU with gloo.
 
 The partition, the level loop, the reference direction rule on global
-counts, the bitmap exchange (all-reduce SUM of disjoint owned words) and the
-loop-cap handling are the product code (paper_1908_01407_b200.distributed).
+counts, the frontier exchange (allgather of the owned counts, then a dense
+allgather of the owned bitmap words or an allgather(v) of the owned ids) and
+the loop-cap handling are the product code (paper_1908_01407_b200.distributed).
 The per-rank level steps -- CUDA kernels in the product -- are replaced here
 by a numpy restatement with the same contract, so world_size-2 runs execute
 on this CPU-only box.  Results must equal the single-process oracle BFS.
@@ -18,7 +19,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import port
-from paper_1908_01407_b200.distributed import ALIGN, TorchExchange, bfs_partitioned, partition_bounds
+from paper_1908_01407_b200.distributed import (ALIGN, FrontierExchange, bfs_partitioned,
+                                               partition_bounds)
 
 
 def test_partition_bounds_properties():
@@ -43,10 +45,11 @@ def test_partition_bounds_properties():
 class Block:
     """Numpy stand-in for BlockGraph (same fields the loop reads)."""
 
-    def __init__(self, rp, ci, lo, hi):
+    def __init__(self, rp, ci, lo, hi, bounds=None):
         self.n = rp.size - 1
         self.nnz = int(rp[-1])
         self.lo, self.hi = lo, hi
+        self.bounds = bounds
         self.rp, self.ci = rp, ci   # symmetric: in-edges == out-edges
 
 
@@ -105,7 +108,7 @@ class NumpySteps:
                     self._set(bm, v)
                 self.levels[v] = depth
 
-    def apply(self, depth):
+    def apply(self, depth, K=None):
         x = self._x().copy()
         self.vbm |= x
         self.vprev |= x
@@ -114,7 +117,44 @@ class NumpySteps:
         F = np.flatnonzero(bits)
         self.levels[F] = depth
         self.F = F
+        assert K is None or K == F.size
         return int(F.size)
+
+    # frontier exchange steps (gb_bfs_dist_owned / pack / unpack / set_ids)
+    def owned(self):
+        g = self.g
+        x = self._x()
+        wl, wh = g.lo // 32, (g.hi + 31) // 32
+        bits = np.unpackbits(x[wl:wh].view(np.uint8), bitorder="little")
+        self.ids = (np.flatnonzero(bits) + wl * 32).astype(np.int32)
+        return torch.tensor([self.ids.size], dtype=torch.int64)
+
+    def pack_words(self, wmax):
+        g = self.g
+        wl, wh = g.lo // 32, (g.hi + 31) // 32
+        out = np.zeros(wmax, np.uint32)
+        out[: wh - wl] = self._x()[wl:wh]
+        return torch.from_numpy(out.view(np.int32))
+
+    def unpack_words(self, gathered, wmax, wb):
+        x = self._x()
+        gw = gathered.numpy().view(np.uint32)
+        wb = wb.numpy()
+        for p in range(wb.size - 1):
+            x[wb[p]:wb[p + 1]] = gw[p * wmax: p * wmax + wb[p + 1] - wb[p]]
+
+    def owned_ids(self, kmax):
+        out = np.zeros(kmax, np.int32)
+        out[: self.ids.size] = self.ids
+        return torch.from_numpy(out)
+
+    def set_ids(self, gathered, counts, kmax):
+        x = self._x()
+        x[:] = 0
+        g = gathered.numpy()
+        for p, c in enumerate(counts.tolist()):
+            for v in g[p * kmax: p * kmax + c]:
+                self._set(x, int(v))
 
     def unstamp(self, K):
         self.levels[self.F[:K]] = 0
@@ -222,12 +262,13 @@ def _worker(rank, world, port_, scale, source, cap, results):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rp, ci, n = port.rmat_csr(scale)
     bounds = partition_bounds(rp, world)
-    g = Block(rp, ci, bounds[rank], bounds[rank + 1])
+    g = Block(rp, ci, bounds[rank], bounds[rank + 1], bounds)
     from paper_1908_01407_b200.containers import Descriptor
     desc = Descriptor(max_niter=cap)
-    levels = bfs_partitioned(g, source, desc, steps=NumpySteps(g), exchange=TorchExchange())
+    ex = FrontierExchange()
+    levels = bfs_partitioned(g, source, desc, steps=NumpySteps(g), exchange=ex)
     results[rank] = (levels.copy(), [(d.chosen, d.frontier_nvals, d.estimated_frontier_edges)
-                                     for d in desc.direction_log])
+                                     for d in desc.direction_log], list(ex.log))
     dist.destroy_process_group()
 
 
@@ -249,7 +290,13 @@ def test_partitioned_bfs_world2_matches_oracle(scale, source, cap):
     pd = port.Desc(max_niter=cap)
     want = port.bfs(P, source, pd)
     for r in range(2):
-        levels, trace = results[r]
+        levels, trace, xlog = results[r]
         assert np.array_equal(levels, want.vals)
         assert [t[0] for t in trace] == [x[0] for x in pd.log]
         assert [t[1:] for t in trace] == [tuple(x[1:3]) for x in pd.log]
+        # the exchange mode follows |f|*32 > n on the NEXT frontier size
+        sizes = [x[1] for x in pd.log[1:]]
+        assert [m for m, _b in xlog[:len(sizes)]] == ["dense" if k * 32 > n else "sparse"
+                                                     for k in sizes]
+    if cap > 2:
+        assert {"dense", "sparse"} <= {m for m, _b in results[0][2]}

@@ -1,10 +1,16 @@
-"""The 1D-partitioned BFS steps on one GPU: P ranks simulated in lock step.
+"""The 1D-partitioned BFS steps on one GPU: P ranks simulated in lock step,
+and two real processes sharing the GPU over gloo.
 
-Each simulated rank owns a BlockGraph and NativeSteps (its own device
-buffers); the exchange sums the ranks' new-frontier words exactly as the
-NCCL all-reduce does.  Levels and the direction trace must equal the
-single-GPU fused BFS for P = 1, 2, 3, 4, 8.
+Lock step: each simulated rank owns a BlockGraph and NativeSteps (its own
+device buffers); the exchange runs FrontierExchange's protocol with the
+collectives emulated by concatenating the ranks' tensors in rank order
+(what allgather returns): counts, then the dense word slices
+(gb_bfs_dist_pack_words / unpack_words) or the sparse id lists
+(gb_bfs_dist_owned / set_ids).  Levels and the direction trace must equal
+the single-GPU fused BFS for P = 1, 2, 3, 4, 8.
 """
+import os
+import socket
 
 import numpy as np
 import pytest
@@ -13,7 +19,25 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def lockstep_bfs(A, P, source, desc):
+def lockstep_exchange(ranks, g):
+    """FrontierExchange with the allgathers emulated (rank-order concatenation)."""
+    from paper_1908_01407_b200.distributed import FrontierExchange
+    counts = torch.cat([st.owned().clone() for st in ranks])
+    total = int(counts.sum())
+    if total * 32 > g.n:
+        wb, wmax = FrontierExchange().word_bounds(g, counts.device)
+        gathered = torch.cat([st.pack_words(wmax).clone() for st in ranks])
+        for st in ranks:
+            st.unpack_words(gathered, wmax, wb)
+    else:
+        kmax = int(counts.max())
+        gathered = torch.cat([st.owned_ids(kmax).clone() for st in ranks])
+        for st in ranks:
+            st.set_ids(gathered, counts, kmax)
+    return total
+
+
+def lockstep_bfs(A, P, source, desc, modes=None):
     from paper_1908_01407_b200.distributed import BlockGraph, NativeSteps, partition_bounds
     from paper_1908_01407_b200.kernels import DirectionDecision, direction_rule
     bounds = partition_bounds(A._csr.offsets.cpu().numpy(), P)
@@ -21,6 +45,7 @@ def lockstep_bfs(A, P, source, desc):
     g = ranks[0].g
     for st in ranks:
         st.init(source)
+    modes = modes if modes is not None else set()
     K, depth = 1, 1
     iters = min(desc.max_niter, g.n + 1)
     for it in range(iters):
@@ -31,14 +56,10 @@ def lockstep_bfs(A, P, source, desc):
                 st.pull(depth + 1)
             else:
                 st.push(K)
-        total = torch.zeros_like(ranks[0].xbm)
-        for st in ranks:
-            total += st.xbm
-        for st in ranks:
-            st.xbm.copy_(total)
-        Ks = [st.apply(depth + 1) for st in ranks]
-        assert len(set(Ks)) == 1
-        K = Ks[0]
+        K = lockstep_exchange(ranks, g)
+        modes.add("dense" if K * 32 > g.n else "sparse")
+        Ks = [st.apply(depth + 1) for st in ranks]   # read back: must equal the exchanged K
+        assert set(Ks) == {K}
         if K == 0:
             break
         depth += 1
@@ -59,7 +80,10 @@ def test_partitioned_equals_single(scale, P):
     for src in (0, 7):
         d1, d2 = gb.Descriptor(), gb.Descriptor()
         want = gb.bfs(A, src, desc=d1).values
-        got = lockstep_bfs(A, P, src, d2)
+        modes = set()
+        got = lockstep_bfs(A, P, src, d2, modes)
+        if P > 1 and src == 0:
+            assert modes == {"dense", "sparse"}
         assert np.array_equal(got, want)
         assert [(x.chosen, x.frontier_nvals) for x in d1.direction_log] == \
             [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
@@ -145,3 +169,71 @@ def test_ordered_partitioned_runner_single_rank():
     run = OrderedPartitionedBfs(A, 0, 1)
     for src in (0, 3, 9999):
         assert np.array_equal(run(src).cpu().numpy(), gb.bfs(A, src).values)
+
+
+# ---------------------------------------------------------------------------
+# two processes, one GPU, gloo: the product loop with NativeSteps and the
+# real FrontierExchange collectives (NCCL needs one GPU per rank)
+# ---------------------------------------------------------------------------
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port_, scale, results):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200 import distributed as gbd
+    A = gb.io.rmat_matrix(scale)
+    out = {}
+    for ordered in (False, True):
+        d = gb.Descriptor()
+        if ordered:
+            run = gbd.OrderedPartitionedBfs(A, rank, world)
+            lv = run(0, d).cpu().numpy()
+            log = run.exchange.log
+        else:
+            g = gbd.BlockGraph.from_matrix(A, rank, world)
+            ex = gbd.FrontierExchange()
+            lv = gbd.bfs_partitioned(g, 0, d, exchange=ex).cpu().numpy()
+            log = ex.log
+        out[ordered] = (lv, [(x.chosen, x.frontier_nvals) for x in d.direction_log], list(log))
+    d = gb.Descriptor()
+    lab = gbd.connected_components(A, d).values
+    out["cc"] = lab
+    results[rank] = out
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scale", [14, 18])
+def test_two_processes_gloo_native_steps(scale):
+    import torch.multiprocessing as mp
+    import paper_1908_01407_b200 as gb
+    ctx = mp.get_context("spawn")
+    results = ctx.Manager().dict()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port_, scale, results)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    A = gb.io.rmat_matrix(scale)
+    d = gb.Descriptor()
+    want = gb.bfs(A, 0, desc=d).values
+    trace = [(x.chosen, x.frontier_nvals) for x in d.direction_log]
+    want_cc = gb.connected_components(A).values
+    for r in range(2):
+        for ordered in (False, True):
+            lv, tr, log = results[r][ordered]
+            assert np.array_equal(lv, want)
+            assert tr == trace
+            assert {m for m, _b in log} == {"dense", "sparse"}
+        assert np.array_equal(results[r]["cc"], want_cc)
