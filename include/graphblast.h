@@ -458,6 +458,13 @@ gb_status gb_widen_i32(gb_ctx* ctx, int64_t n, const int32_t* in, int64_t* out);
 /* Per-iteration host callback of the fused drivers (the sssp on_iteration hook). */
 typedef void (*gb_iter_cb)(int64_t iteration, void* user);
 
+/* Engine of the SSSP / PageRank / CC iteration loops: 0 = one CUDA-graph
+ * launch per call (WHILE conditional node, device-side direction decisions
+ * and exit tests; the default), 1 = the host-driven loop (one synchronisation
+ * per iteration; also used under per-kernel profiling and for an SSSP
+ * on_iteration callback).  Returns the previous engine. */
+int32_t gb_loop_engine(int32_t engine);
+
 /* sssp (algorithms.py:80-119): dist (float64[n]) receives the distances
  * (+inf unreached).  Weights must be positive (checked by the caller). */
 gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t source,

@@ -15,9 +15,12 @@
 // Every driver logs the reference direction rule (gb_decide_direction) per
 // multiply and synchronizes once per iteration for the loop-exit scalar.
 #include <math.h>
+#include <stddef.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <type_traits>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -165,10 +168,26 @@ sssp_pull(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict_
 }
 
 // changed bitmap -> frontier list (+ values) and dense frontier values
+__device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restrict__ changed,
+                                                   const double* __restrict__ dist,
+                                                   int32_t* __restrict__ F,
+                                                   double* __restrict__ Fv,
+                                                   double* __restrict__ fvd,
+                                                   unsigned long long* __restrict__ count);
+
 __global__ void sssp_finalize(int64_t n, uint32_t* __restrict__ changed,
                               const double* __restrict__ dist, int32_t* __restrict__ F,
                               double* __restrict__ Fv, double* __restrict__ fvd,
                               unsigned long long* __restrict__ count) {
+  sssp_finalize_body(n, changed, dist, F, Fv, fvd, count);
+}
+
+__device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restrict__ changed,
+                                                   const double* __restrict__ dist,
+                                                   int32_t* __restrict__ F,
+                                                   double* __restrict__ Fv,
+                                                   double* __restrict__ fvd,
+                                                   unsigned long long* __restrict__ count) {
   const int64_t W = (n + 31) / 32;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
        w += (int64_t)gridDim.x * blockDim.x) {
@@ -234,10 +253,28 @@ pr_spmv(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restric
 
 // ranks = spread + teleport; error^2 += (ranks - prev)^2; y = inv * ranks;
 // spread reset for the next iteration; count of non-zero ranks (next decision)
+__device__ __forceinline__ void pr_epilogue_body(int64_t n, double tele,
+                                                 const double* __restrict__ inv,
+                                                 double* __restrict__ spread,
+                                                 const double* __restrict__ prev,
+                                                 double* __restrict__ rank, double* __restrict__ y,
+                                                 double* __restrict__ err2,
+                                                 unsigned long long* __restrict__ nz);
+
 __global__ void __launch_bounds__(256)
 pr_epilogue(int64_t n, double tele, const double* __restrict__ inv, double* __restrict__ spread,
             const double* __restrict__ prev, double* __restrict__ rank, double* __restrict__ y,
             double* __restrict__ err2, unsigned long long* __restrict__ nz) {
+  pr_epilogue_body(n, tele, inv, spread, prev, rank, y, err2, nz);
+}
+
+__device__ __forceinline__ void pr_epilogue_body(int64_t n, double tele,
+                                                 const double* __restrict__ inv,
+                                                 double* __restrict__ spread,
+                                                 const double* __restrict__ prev,
+                                                 double* __restrict__ rank, double* __restrict__ y,
+                                                 double* __restrict__ err2,
+                                                 unsigned long long* __restrict__ nz) {
   __shared__ double s_e[8];
   __shared__ long long s_c[8];
   double e = 0.0;
@@ -377,10 +414,24 @@ __global__ void cc_hook(int64_t n, const int* __restrict__ hook, int* __restrict
 // gp = parent[parent]; changed = gp != gp_prev; gp_prev = gp; sparsify.
 // Counts are reduced per block (one atomic per block, not per warp: the two
 // counters are single addresses every block hits).
+__device__ __forceinline__ void cc_shortcut_body(int64_t n, const int* __restrict__ parent,
+                                                 int* __restrict__ gp, int* __restrict__ gpp,
+                                                 int sparsify,
+                                                 unsigned long long* __restrict__ changed,
+                                                 unsigned long long* __restrict__ live);
+
 __global__ void __launch_bounds__(256)
 cc_shortcut(int64_t n, const int* __restrict__ parent, int* __restrict__ gp,
             int* __restrict__ gpp, int sparsify, unsigned long long* __restrict__ changed,
             unsigned long long* __restrict__ live) {
+  cc_shortcut_body(n, parent, gp, gpp, sparsify, changed, live);
+}
+
+__device__ __forceinline__ void cc_shortcut_body(int64_t n, const int* __restrict__ parent,
+                                                 int* __restrict__ gp, int* __restrict__ gpp,
+                                                 int sparsify,
+                                                 unsigned long long* __restrict__ changed,
+                                                 unsigned long long* __restrict__ live) {
   __shared__ long long s_c[8], s_l[8];
   long long c = 0, l = 0;
   // four independent pointer jumps in flight per thread (latency-bound)
@@ -438,6 +489,876 @@ __global__ void widen_i32(int64_t n, const int* __restrict__ a, long long* __res
     out[i] = a[i];
 }
 
+// ===========================================================================
+// Device-resident iteration loops: PageRank, FastSV and
+// SSSP as ONE CUDA-graph launch each -- a WHILE conditional node whose body
+// runs an iteration and a single-thread step kernel that logs the reference
+// direction rule (kernels.py:108-126, half-even rint), evaluates the loop
+// exit (algorithms.py:160 / 196-197 / 114-118) and sets the loop handle;
+// CC and SSSP pick their multiply in a two-way SWITCH node (pull | push).
+// No host synchronisation inside the loop: the log and the iteration count
+// are read once, after it.  The graphs are cached per context and matrix
+// (gb_csr.gen) like the BFS graph; per-call parameters travel in a device
+// state block written before each launch.  Push multiplies size themselves
+// from a device count: a warp per frontier entry, entries longer than
+// kLongPush edges cut into 512-edge tasks for a second pass.
+// ===========================================================================
+constexpr int64_t kLongPush = 4096;
+enum { kLoopGraph = 0, kLoopHost = 1 };
+static int g_loop_engine = -1;
+static int loop_engine() {
+  if (g_loop_engine < 0) {
+    const char* e = getenv("GB_LOOP_GRAPH");
+    g_loop_engine = (e && atoi(e) == 0) ? kLoopHost : kLoopGraph;
+  }
+  return g_loop_engine;
+}
+
+__device__ __forceinline__ int32_t decide_dev(int64_t nnz, int64_t nrows, int64_t k, double ratio,
+                                              int32_t policy, int64_t* est) {
+  const double d = nrows ? (double)nnz / (double)nrows : 0.0;
+  const int64_t e = (int64_t)rint(d * (double)k);  // Python round: half-even
+  *est = e;
+  int32_t dir = (double)e > (double)nnz * ratio ? GB_DIR_PULL : GB_DIR_PUSH;
+  if (policy == GB_DIR_PUSH) dir = GB_DIR_PUSH;
+  if (policy == GB_DIR_PULL) dir = GB_DIR_PULL;
+  return dir;
+}
+
+__device__ __forceinline__ int32_t log_decision(int64_t* log, int64_t it, int64_t nnz,
+                                                int64_t nrows, int64_t k, double ratio,
+                                                int32_t policy) {
+  int64_t est = 0;
+  const int32_t dir = decide_dev(nnz, nrows, k, ratio, policy, &est);
+  log[3 * it] = dir;
+  log[3 * it + 1] = k;
+  log[3 * it + 2] = est;
+  return dir;
+}
+
+template <class Fn>
+static cudaError_t loop_capture_into(cudaGraph_t g, cudaStream_t cs, Fn fn) {
+  cudaError_t e = cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) return e;
+  cudaError_t e2 = fn();
+  cudaGraph_t out = g;
+  e = cudaStreamEndCapture(cs, &out);
+  return e2 != cudaSuccess ? e2 : e;
+}
+
+#define GB_LTRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
+
+// add a conditional node (WHILE: size 1, SWITCH: size k) after the capture's
+// current dependencies; returns its body graphs
+static cudaError_t add_conditional(cudaStream_t s, cudaGraphConditionalHandle h,
+                                   cudaGraphConditionalNodeType type, unsigned size,
+                                   cudaGraph_t* bodies) {
+  cudaStreamCaptureStatus status;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  GB_LTRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = size;
+  cudaGraphNode_t node;
+  GB_LTRY(cudaGraphAddNode(&node, g, deps, nd, &p));
+  for (unsigned i = 0; i < size; ++i) bodies[i] = p.conditional.phGraph_out[i];
+  return cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
+static cudaGraph_t capturing_graph(cudaStream_t s) {
+  cudaStreamCaptureStatus status;
+  cudaGraph_t g = nullptr;
+  cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr);
+  return g;
+}
+
+static bool loop_same_csr(const gb_csr* a, const gb_csr* b) {
+  if (!a || !b) return a == b;
+  return a->gen != 0 && a->gen == b->gen && a->nrows == b->nrows && a->nnz == b->nnz &&
+         a->offsets == b->offsets && a->indices == b->indices && a->values == b->values &&
+         a->dtype == b->dtype && a->iso_i64 == b->iso_i64 && a->iso_f64 == b->iso_f64;
+}
+
+__global__ void copy_i32(int64_t n, const int* __restrict__ a, int* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+// warp per frontier entry k < *count; a row longer than kLongPush edges is
+// cut into kLongChunk-edge tasks (k, chunk) queued for push_long
+constexpr int64_t kLongChunk = 512;
+template <class Op>
+__global__ void __launch_bounds__(256)
+push_short(const unsigned long long* __restrict__ count, const int32_t* __restrict__ F,
+           const int64_t* __restrict__ off, int32_t* __restrict__ longk,
+           int32_t* __restrict__ longc, unsigned long long* __restrict__ nlong, Op op) {
+  const int lane = threadIdx.x & 31;
+  const int64_t K = (int64_t)*count;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = w0; k < K; k += nw) {
+    const int32_t j = F[k];
+    const int64_t lo = off[j], hi = off[j + 1];
+    if (hi - lo > kLongPush) {
+      const int64_t nc = (hi - lo + kLongChunk - 1) / kLongChunk;
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(nlong, (unsigned long long)nc);
+      at = __shfl_sync(GB_FULL, at, 0);
+      for (int64_t c = lane; c < nc; c += 32) {
+        longk[at + c] = (int32_t)k;
+        longc[at + c] = (int32_t)c;
+      }
+      continue;
+    }
+    for (int64_t p = lo + lane; p < hi; p += 32) op(k, p);
+  }
+}
+
+// warp per queued (entry, chunk) task of the long rows
+template <class Op>
+__global__ void __launch_bounds__(256)
+push_long(const unsigned long long* __restrict__ nlong, const int32_t* __restrict__ longk,
+          const int32_t* __restrict__ longc, const int32_t* __restrict__ F,
+          const int64_t* __restrict__ off, Op op) {
+  const int lane = threadIdx.x & 31;
+  const int64_t L = (int64_t)*nlong;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = w0; t < L; t += nw) {
+    const int64_t k = longk[t];
+    const int32_t j = F[k];
+    const int64_t lo = off[j] + (int64_t)longc[t] * kLongChunk;
+    const int64_t hi = min(off[j + 1], lo + kLongChunk);
+    for (int64_t p = lo + lane; p < hi; p += 32) op(k, p);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PageRank (algorithms.py:132-162)
+// ---------------------------------------------------------------------------
+struct PrState {
+  // per call
+  double alpha, tele, eps, ratio;
+  int64_t max_iters;
+  int64_t* log;   // [max_iters][3]
+  double* errs;   // [max_iters]
+  int32_t policy, pad_;
+  // loop
+  int64_t it, nz, iters;
+  double e2;
+  unsigned long long nzc;
+};
+
+__global__ void pr_init_g(int64_t n, const int64_t* __restrict__ out_off,
+                          const PrState* __restrict__ st, double* __restrict__ inv,
+                          double* __restrict__ rank, double* __restrict__ y,
+                          double* __restrict__ spread) {
+  const double alpha = st->alpha;
+  const double r0 = 1.0 / (double)n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = out_off[i + 1] - out_off[i];
+    const double sc = d > 0 ? alpha / (double)d : 0.0;  // algorithms.py:124-127
+    inv[i] = sc;
+    rank[i] = r0;
+    y[i] = sc * r0;
+    spread[i] = 0.0;
+  }
+}
+
+__global__ void pr_start_g(PrState* st, int64_t n, int64_t nnz, cudaGraphConditionalHandle h) {
+  st->it = 0;
+  st->nz = n;
+  st->iters = 0;
+  st->e2 = 0.0;
+  st->nzc = 0;
+  if (st->max_iters > 0) log_decision(st->log, 0, nnz, n, n, st->ratio, st->policy);
+  cudaGraphSetConditional(h, st->max_iters > 0 ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(256)
+pr_epilogue_g(int64_t n, PrState* st, const double* __restrict__ inv, double* __restrict__ spread,
+              double* __restrict__ rk0, double* __restrict__ rk1, double* __restrict__ y) {
+  const bool odd = st->it & 1;
+  pr_epilogue_body(n, st->tele, inv, spread, odd ? rk1 : rk0, odd ? rk0 : rk1, y, &st->e2,
+                   &st->nzc);
+}
+
+__global__ void pr_step_g(PrState* st, int64_t n, int64_t nnz, cudaGraphConditionalHandle h) {
+  const double err = sqrt(st->e2);
+  const int64_t it = st->it;
+  st->errs[it] = err;
+  st->nz = (int64_t)st->nzc;
+  st->it = it + 1;
+  st->iters = it + 1;
+  const bool cont = !(err <= st->eps) && it + 1 < st->max_iters;  // algorithms.py:160
+  st->e2 = 0.0;
+  st->nzc = 0;
+  if (cont) log_decision(st->log, it + 1, nnz, n, st->nz, st->ratio, st->policy);
+  cudaGraphSetConditional(h, cont ? 1u : 0u);
+}
+
+struct PrGraph {
+  gb_csr pull{};
+  const int64_t* out_off = nullptr;
+  void* mem = nullptr;
+  double *inv, *y, *spread, *rk[2];
+  PrState* st;
+  RowTilesPlan plan;
+  cudaGraphExec_t exec = nullptr;
+};
+
+static void pr_graph_free(void* p) {
+  auto* g = static_cast<PrGraph*>(p);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->mem) cudaFree(g->mem);
+  delete g;
+}
+
+static cudaError_t pr_graph_build(gb_ctx* ctx, PrGraph* G) {
+  const int64_t n = G->pull.nrows, nnz = G->pull.nnz;
+  cudaStream_t cs[2];
+  for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+  cudaGraph_t top;
+  cudaError_t err = cudaGraphCreate(&top, 0);
+  if (err == cudaSuccess) err = loop_capture_into(top, cs[0], [&]() -> cudaError_t {
+    cudaStream_t s = cs[0];
+    pr_init_g<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, G->out_off, G->st, G->inv, G->rk[0], G->y,
+                                                    G->spread);
+    cudaGraphConditionalHandle h;
+    GB_LTRY(cudaGraphConditionalHandleCreate(&h, capturing_graph(s), 0, cudaGraphCondAssignDefault));
+    pr_start_g<<<1, 1, 0, s>>>(G->st, n, nnz, h);
+    GB_LTRY(cudaGetLastError());
+    cudaGraph_t body;
+    GB_LTRY(add_conditional(s, h, cudaGraphCondTypeWhile, 1, &body));
+    return loop_capture_into(body, cs[1], [&]() -> cudaError_t {
+      if (G->plan.R)
+        pr_spmv<<<resident_grid(ctx, pr_spmv, 256), 256, 0, cs[1]>>>(
+            G->plan.R, G->plan.nz_rows, G->plan.nz_off, G->pull.indices, G->plan.tile_first, G->y,
+            G->spread);
+      pr_epilogue_g<<<grid_for(ctx, n, 256, 8), 256, 0, cs[1]>>>(n, G->st, G->inv, G->spread,
+                                                                 G->rk[0], G->rk[1], G->y);
+      pr_step_g<<<1, 1, 0, cs[1]>>>(G->st, n, nnz, h);
+      return cudaGetLastError();
+    });
+  });
+  if (err == cudaSuccess) err = cudaGraphInstantiate(&G->exec, top, 0);
+  cudaGraphDestroy(top);
+  for (auto& x : cs) cudaStreamDestroy(x);
+  return err;
+}
+
+static gb_status pagerank_graph(gb_ctx* ctx, const gb_csr* pull, const int64_t* out_offsets,
+                                double alpha, double eps, int64_t max_iters, double ratio,
+                                int32_t policy, double* ranks_out, int32_t* log_dir,
+                                int64_t* log_nvals, int64_t* log_est, double* err_out,
+                                int64_t* iters_out) {
+  const int64_t n = pull->nrows;
+  void** slot = ctx_slot(ctx, SLOT_PR_GRAPH, pr_graph_free);
+  PrGraph* G = static_cast<PrGraph*>(*slot);
+  cudaStream_t s = stream_of(ctx);
+  if (G && !(loop_same_csr(&G->pull, pull) && G->out_off == out_offsets)) {
+    cudaStreamSynchronize(s);
+    pr_graph_free(G);
+    *slot = G = nullptr;
+  }
+  if (!G) {
+    G = new PrGraph();
+    G->pull = *pull;
+    G->out_off = out_offsets;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += (b + 255) / 256 * 256; return o; };
+    const size_t o_v = take(5 * 8 * (size_t)n), o_st = take(sizeof(PrState));
+    const size_t o_r = take(4 * (size_t)n), o_o = take(8 * (size_t)(n + 1));
+    const size_t o_t = take(4 * (size_t)(pull->nnz / kRowTile + 2));
+    if (cudaMalloc(&G->mem, off) != cudaSuccess) {
+      cudaGetLastError();
+      delete G;
+      return GB_ERR_UNSUPPORTED;
+    }
+    char* m = static_cast<char*>(G->mem);
+    double* v = (double*)(m + o_v);
+    G->inv = v;
+    G->y = v + n;
+    G->spread = v + 2 * n;
+    G->rk[0] = v + 3 * n;
+    G->rk[1] = v + 4 * n;
+    G->st = (PrState*)(m + o_st);
+    G->plan.nz_rows = (int32_t*)(m + o_r);
+    G->plan.nz_off = (int64_t*)(m + o_o);
+    G->plan.tile_first = (int32_t*)(m + o_t);
+    Arena ar(ctx);
+    gb_status st = row_tiles_plan(ctx, ar, n, pull->offsets, pull->nnz, &G->plan);
+    cudaError_t e = st == GB_OK ? pr_graph_build(ctx, G) : cudaSuccess;
+    if (st != GB_OK || e != cudaSuccess) {
+      cudaGetLastError();
+      pr_graph_free(G);
+      return st != GB_OK ? st : set_error(ctx, GB_ERR_CUDA, "pagerank graph: %s", cudaGetErrorString(e));
+    }
+    *slot = G;
+  }
+  Arena ar(ctx);
+  const int64_t cap = max_iters > 0 ? max_iters : 1;
+  int64_t* dlog = ar.alloc<int64_t>(3 * cap + 1);
+  double* derr = ar.alloc<double>(cap);
+  GB_ARENA_CHECK(ctx, ar);
+  PrState h{};
+  h.alpha = alpha;
+  h.tele = (1.0 - alpha) / (double)n;
+  h.eps = eps;
+  h.ratio = ratio;
+  h.max_iters = max_iters;
+  h.log = dlog;
+  h.errs = derr;
+  h.policy = policy;
+  GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(PrState, it), cudaMemcpyHostToDevice, s));
+  GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
+  count_launch(ctx, 3);  // init, start + the body kernels are booked below
+  int64_t iters = 0;
+  GB_CUDA(ctx, cudaMemcpyAsync(&iters, &G->st->iters, 8, cudaMemcpyDeviceToHost, s));
+  GB_CUDA(ctx, cudaStreamSynchronize(s));
+  if (iters > 0) {
+    std::vector<int64_t> lg(3 * iters);
+    GB_CUDA(ctx, cudaMemcpyAsync(lg.data(), dlog, 8 * 3 * iters, cudaMemcpyDeviceToHost, s));
+    if (err_out) GB_CUDA(ctx, cudaMemcpyAsync(err_out, derr, 8 * iters, cudaMemcpyDeviceToHost, s));
+    GB_CUDA(ctx, cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < iters; ++i) {
+      log_dir[i] = (int32_t)lg[3 * i];
+      log_nvals[i] = lg[3 * i + 1];
+      log_est[i] = lg[3 * i + 2];
+    }
+  }
+  count_launch(ctx, (int)(3 * iters));
+  // iteration i reads rk[i & 1] and writes the other: the result is rk[iters & 1]
+  GB_CUDA(ctx, cudaMemcpyAsync(ranks_out, G->rk[iters & 1], 8 * (size_t)n, cudaMemcpyDeviceToDevice, s));
+  *iters_out = iters;
+  return GB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Connected components, FastSV (algorithms.py:165-203)
+// ---------------------------------------------------------------------------
+struct CcState {
+  double ratio;
+  int64_t max_iters;
+  int64_t* log;
+  int32_t policy, sparsify;
+  // loop
+  int64_t it, live, iters;
+  unsigned long long cnt[3];  // changed, live, listed
+  unsigned long long nlong;
+};
+
+struct CcPushOp {
+  const int32_t* idx;
+  const int32_t* F;
+  const int* gp;
+  int* hook;
+  __device__ __forceinline__ void operator()(int64_t k, int64_t p) const {
+    const int32_t i = __ldg(idx + p);
+    const int g = gp[F[k]];
+    if (g < hook[i]) atomicMin(hook + i, g);
+  }
+};
+
+__global__ void cc_start_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditionalHandle h_loop,
+                           cudaGraphConditionalHandle h_dir) {
+  st->it = 0;
+  st->live = n;
+  st->iters = 0;
+  st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
+  st->nlong = 0;
+  const bool run = st->max_iters > 0;
+  unsigned dir = 0;
+  if (run) dir = log_decision(st->log, 0, nnz, n, n, st->ratio, st->policy) == GB_DIR_PULL ? 0 : 1;
+  cudaGraphSetConditional(h_loop, run ? 1u : 0u);
+  cudaGraphSetConditional(h_dir, dir);
+}
+
+__global__ void cc_shortcut_g(int64_t n, const int* __restrict__ parent, int* __restrict__ gp,
+                              int* __restrict__ gpp, CcState* st) {
+  // sparsify read from the state: one graph serves both settings
+  cc_shortcut_body(n, parent, gp, gpp, st->sparsify, &st->cnt[0], &st->cnt[1]);
+}
+
+__global__ void cc_step_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditionalHandle h_loop,
+                          cudaGraphConditionalHandle h_dir) {
+  const int64_t it = st->it;
+  const unsigned long long changed = st->cnt[0];
+  st->it = it + 1;
+  st->iters = it + 1;
+  bool cont = changed != 0 && it + 1 < st->max_iters;  // algorithms.py:196-197
+  if (changed != 0) st->live = (int64_t)st->cnt[1];
+  st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
+  st->nlong = 0;
+  unsigned dir = 2;  // no branch
+  if (cont)
+    dir = log_decision(st->log, it + 1, nnz, n, st->live, st->ratio, st->policy) == GB_DIR_PULL
+              ? 0 : 1;
+  cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
+  cudaGraphSetConditional(h_dir, dir);
+}
+
+struct CcGraph {
+  gb_csr rows{}, cols{};
+  bool has_cols = false;
+  void* mem = nullptr;
+  int *P, *mn, *gp, *gpp, *pp, *hook;
+  int32_t *F, *longk, *longc;
+  CcState* st;
+  RowTilesPlan plan;
+  cudaGraphExec_t exec = nullptr;
+};
+
+static void cc_graph_free(void* p) {
+  auto* g = static_cast<CcGraph*>(p);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->mem) cudaFree(g->mem);
+  delete g;
+}
+
+static cudaError_t cc_graph_build(gb_ctx* ctx, CcGraph* G) {
+  const int64_t n = G->rows.nrows, nnz = G->rows.nnz;
+  const int vec_grid = grid_for(ctx, n, 256, 8);
+  cudaStream_t cs[3];
+  for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+  cudaGraph_t top;
+  cudaError_t err = cudaGraphCreate(&top, 0);
+  if (err == cudaSuccess) err = loop_capture_into(top, cs[0], [&]() -> cudaError_t {
+    cudaStream_t s = cs[0];
+    cc_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, G->P, G->mn, G->gp, G->gpp);
+    cudaGraphConditionalHandle h_loop, h_dir;
+    cudaGraph_t g = capturing_graph(s);
+    GB_LTRY(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
+    GB_LTRY(cudaGraphConditionalHandleCreate(&h_dir, g, 0, cudaGraphCondAssignDefault));
+    cc_start_g<<<1, 1, 0, s>>>(G->st, n, nnz, h_loop, h_dir);
+    GB_LTRY(cudaGetLastError());
+    cudaGraph_t body;
+    GB_LTRY(add_conditional(s, h_loop, cudaGraphCondTypeWhile, 1, &body));
+    return loop_capture_into(body, cs[1], [&]() -> cudaError_t {
+      cudaStream_t b = cs[1];
+      copy_i32<<<vec_grid, 256, 0, b>>>(n, G->P, G->pp);
+      fill_i32<<<vec_grid, 256, 0, b>>>(n, kImax32, G->hook);
+      cudaGraph_t br[2];
+      GB_LTRY(add_conditional(b, h_dir, cudaGraphCondTypeSwitch, 2, br));
+      GB_LTRY(loop_capture_into(br[0], cs[2], [&]() -> cudaError_t {
+        // pull: mxv walks rows of A (kernels.py:313-316)
+        if (G->plan.R)
+          cc_pull<<<resident_grid(ctx, cc_pull, 256), 256, 0, cs[2]>>>(
+              G->plan.R, G->plan.nz_rows, G->plan.nz_off, G->rows.indices, G->plan.tile_first,
+              G->gp, G->hook);
+        return cudaGetLastError();
+      }));
+      GB_LTRY(loop_capture_into(br[1], cs[2], [&]() -> cudaError_t {
+        // push: columns of A from the live grandparents, listed on the device
+        if (!G->has_cols) return cudaSuccess;
+        cc_list<<<vec_grid, 256, 0, cs[2]>>>(n, G->gp, G->F, &G->st->cnt[2]);
+        const CcPushOp op{G->cols.indices, G->F, G->gp, G->hook};
+        push_short<CcPushOp><<<grid_for(ctx, n * 32, 256, 8), 256, 0, cs[2]>>>(
+            &G->st->cnt[2], G->F, G->cols.offsets, G->longk, G->longc, &G->st->nlong, op);
+        push_long<CcPushOp><<<grid_for(ctx, G->cols.nnz / 16 + 32, 256, 8), 256, 0, cs[2]>>>(
+            &G->st->nlong, G->longk, G->longc, G->F, G->cols.offsets, op);
+        return cudaGetLastError();
+      }));
+      cc_hook<<<vec_grid, 256, 0, b>>>(n, G->hook, G->mn, G->pp, G->P);
+      cc_shortcut_g<<<vec_grid, 256, 0, b>>>(n, G->P, G->gp, G->gpp, G->st);
+      cc_step_g<<<1, 1, 0, b>>>(G->st, n, nnz, h_loop, h_dir);
+      return cudaGetLastError();
+    });
+  });
+  if (err == cudaSuccess) err = cudaGraphInstantiate(&G->exec, top, 0);
+  cudaGraphDestroy(top);
+  for (auto& x : cs) cudaStreamDestroy(x);
+  return err;
+}
+
+static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max_iters,
+                          double ratio, int32_t policy, int32_t sparsify, int64_t* parent,
+                          int32_t* log_dir, int64_t* log_nvals, int64_t* log_est,
+                          int64_t* iters_out) {
+  const int64_t n = rows->nrows;
+  void** slot = ctx_slot(ctx, SLOT_CC_GRAPH, cc_graph_free);
+  CcGraph* G = static_cast<CcGraph*>(*slot);
+  cudaStream_t s = stream_of(ctx);
+  if (G && !(loop_same_csr(&G->rows, rows) && G->has_cols == (cols != nullptr) &&
+             (!cols || loop_same_csr(&G->cols, cols)))) {
+    cudaStreamSynchronize(s);
+    cc_graph_free(G);
+    *slot = G = nullptr;
+  }
+  if (!G) {
+    G = new CcGraph();
+    G->rows = *rows;
+    G->has_cols = cols != nullptr;
+    if (cols) G->cols = *cols;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += (b + 255) / 256 * 256; return o; };
+    const size_t o_v = take(7 * 4 * (size_t)n), o_st = take(sizeof(CcState));
+    const size_t ntask = (size_t)n + (size_t)(rows->nnz / kLongChunk) + 1;
+    const size_t o_lk = take(4 * ntask), o_lc = take(4 * ntask);
+    const size_t o_r = take(4 * (size_t)n), o_o = take(8 * (size_t)(n + 1));
+    const size_t o_t = take(4 * (size_t)(rows->nnz / kRowTile + 2));
+    if (cudaMalloc(&G->mem, off) != cudaSuccess) {
+      cudaGetLastError();
+      delete G;
+      return GB_ERR_UNSUPPORTED;
+    }
+    char* m = static_cast<char*>(G->mem);
+    int* v = (int*)(m + o_v);
+    G->P = v;
+    G->mn = v + n;
+    G->gp = v + 2 * n;
+    G->gpp = v + 3 * n;
+    G->pp = v + 4 * n;
+    G->hook = v + 5 * n;
+    G->F = v + 6 * n;
+    G->longk = (int32_t*)(m + o_lk);
+    G->longc = (int32_t*)(m + o_lc);
+    G->st = (CcState*)(m + o_st);
+    G->plan.nz_rows = (int32_t*)(m + o_r);
+    G->plan.nz_off = (int64_t*)(m + o_o);
+    G->plan.tile_first = (int32_t*)(m + o_t);
+    Arena ar(ctx);
+    gb_status st = row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &G->plan);
+    cudaError_t e = st == GB_OK ? cc_graph_build(ctx, G) : cudaSuccess;
+    if (st != GB_OK || e != cudaSuccess) {
+      cudaGetLastError();
+      cc_graph_free(G);
+      return st != GB_OK ? st : set_error(ctx, GB_ERR_CUDA, "cc graph: %s", cudaGetErrorString(e));
+    }
+    *slot = G;
+  }
+  Arena ar(ctx);
+  const int64_t cap = max_iters > 0 ? max_iters : 1;
+  int64_t* dlog = ar.alloc<int64_t>(3 * cap + 1);
+  GB_ARENA_CHECK(ctx, ar);
+  CcState h{};
+  h.ratio = ratio;
+  h.max_iters = max_iters;
+  h.log = dlog;
+  h.policy = policy;
+  h.sparsify = sparsify;
+  GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(CcState, it), cudaMemcpyHostToDevice, s));
+  GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
+  widen_i32<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, G->P, reinterpret_cast<long long*>(parent));
+  GB_LAUNCH_CHECK(ctx);
+  int64_t iters = 0;
+  GB_CUDA(ctx, cudaMemcpyAsync(&iters, &G->st->iters, 8, cudaMemcpyDeviceToHost, s));
+  GB_CUDA(ctx, cudaStreamSynchronize(s));
+  if (iters > 0) {
+    std::vector<int64_t> lg(3 * iters);
+    GB_CUDA(ctx, cudaMemcpyAsync(lg.data(), dlog, 8 * 3 * iters, cudaMemcpyDeviceToHost, s));
+    GB_CUDA(ctx, cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < iters; ++i) {
+      log_dir[i] = (int32_t)lg[3 * i];
+      log_nvals[i] = lg[3 * i + 1];
+      log_est[i] = lg[3 * i + 2];
+    }
+  }
+  count_launch(ctx, (int)(3 + 6 * iters));
+  *iters_out = iters;
+  return GB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// SSSP (algorithms.py:80-119)
+// ---------------------------------------------------------------------------
+struct SsspState {
+  double ratio;
+  int64_t max_iters, source;
+  int64_t* log;
+  double* dist;
+  int32_t policy, pad_;
+  // loop
+  int64_t it, K, reached, succ_last, iters;
+  unsigned long long cnt[2];  // new frontier, newly reached
+  unsigned long long nlong;
+};
+
+struct SsspPushOp {
+  const int32_t* idx;
+  const void* vals;
+  int dtype;
+  double iso;
+  const double* Fv;
+  double* const* dist;
+  uint32_t* changed;
+  unsigned long long* reached;
+  __device__ __forceinline__ void operator()(int64_t k, int64_t p) const {
+    const int32_t v = __ldg(idx + p);
+    const double nd = ld_weight(vals, dtype, iso, p) + Fv[k];  // mult(A value, u value)
+    if (relax(*dist, v, nd, reached)) atomicOr(changed + (v >> 5), 1u << (v & 31));
+  }
+};
+
+__global__ void sssp_init_g(int64_t n, const SsspState* __restrict__ st, double* __restrict__ fvd,
+                            int32_t* __restrict__ F, double* __restrict__ Fv,
+                            long long* __restrict__ cand, uint32_t* __restrict__ changed) {
+  double* dist = st->dist;
+  const int64_t source = st->source;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    dist[i] = i == source ? 0.0 : INFINITY;
+    fvd[i] = i == source ? 0.0 : INFINITY;  // the frontier's dense copy: the source
+    cand[i] = kInfBits;
+    if ((i & 31) == 0) changed[i >> 5] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    F[0] = (int32_t)source;
+    Fv[0] = 0.0;
+  }
+}
+
+__device__ __forceinline__ unsigned sssp_branch(SsspState* st, int64_t n, int64_t nnz) {
+  const int32_t dir = log_decision(st->log, st->it, nnz, n, st->K, st->ratio, st->policy);
+  st->cnt[0] = 0;
+  st->nlong = 0;
+  return dir == GB_DIR_PULL ? 0u : (st->K > 0 ? 1u : 2u);
+}
+
+__global__ void sssp_start_g(SsspState* st, int64_t n, int64_t nnz,
+                             cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_dir) {
+  st->it = 0;
+  st->K = 1;
+  st->reached = 1;
+  st->succ_last = -1;
+  st->iters = 0;
+  st->cnt[0] = st->cnt[1] = 0;
+  const bool run = st->max_iters > 0;
+  const unsigned dir = run ? sssp_branch(st, n, nnz) : 2u;
+  cudaGraphSetConditional(h_loop, run ? 1u : 0u);
+  cudaGraphSetConditional(h_dir, dir);
+}
+
+__global__ void reset_fvd_g(const SsspState* __restrict__ st, const int32_t* __restrict__ F,
+                            double* __restrict__ fvd) {
+  const int64_t K = st->K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
+       i += (int64_t)gridDim.x * blockDim.x)
+    fvd[F[i]] = INFINITY;
+}
+
+__global__ void sssp_pull_apply_g(int64_t n, long long* __restrict__ cand, SsspState* st,
+                                  uint32_t* __restrict__ changed) {
+  double* dist = st->dist;
+  unsigned long long* reached = &st->cnt[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const long long c = cand[i];
+    if (c == kInfBits) continue;
+    cand[i] = kInfBits;
+    const double nd = __longlong_as_double(c);
+    const double od = dist[i];
+    if (nd < od) {
+      if (od == INFINITY) atomicAdd(reached, 1ull);
+      dist[i] = nd;
+      atomicOr(changed + (i >> 5), 1u << (i & 31));
+    }
+  }
+}
+
+__global__ void sssp_finalize_g(int64_t n, uint32_t* __restrict__ changed, SsspState* st,
+                                int32_t* __restrict__ F, double* __restrict__ Fv,
+                                double* __restrict__ fvd) {
+  sssp_finalize_body(n, changed, st->dist, F, Fv, fvd, &st->cnt[0]);
+}
+
+__global__ void sssp_step_g(SsspState* st, int64_t n, int64_t nnz,
+                            cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_dir) {
+  const int64_t it = st->it;
+  const int64_t K = (int64_t)st->cnt[0];
+  const int64_t reached = st->reached + (int64_t)st->cnt[1];
+  st->cnt[1] = 0;
+  st->K = K;
+  st->reached = reached;
+  st->it = it + 1;
+  st->iters = it + 1;
+  // algorithms.py:114-118: count of finite distances stable and no frontier
+  const bool done = reached == st->succ_last && K == 0;
+  st->succ_last = reached;
+  const bool cont = !done && it + 1 < st->max_iters;
+  const unsigned dir = cont ? sssp_branch(st, n, nnz) : 2u;
+  cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
+  cudaGraphSetConditional(h_dir, dir);
+}
+
+struct SsspGraph {
+  gb_csr push{}, pull{};
+  bool has_pull = false;
+  void* mem = nullptr;
+  uint32_t* changed;
+  int32_t *F, *longk, *longc;
+  double *Fv, *fvd;
+  long long* cand;
+  SsspState* st;
+  RowTilesPlan plan;
+  cudaGraphExec_t exec = nullptr;
+};
+
+static void sssp_graph_free(void* p) {
+  auto* g = static_cast<SsspGraph*>(p);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->mem) cudaFree(g->mem);
+  delete g;
+}
+
+static cudaError_t sssp_graph_build(gb_ctx* ctx, SsspGraph* G) {
+  const int64_t n = G->push.nrows, nnz = G->push.nnz;
+  const int64_t W = (n + 31) / 32;
+  cudaStream_t cs[3];
+  for (auto& x : cs) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+  cudaGraph_t top;
+  cudaError_t err = cudaGraphCreate(&top, 0);
+  if (err == cudaSuccess) err = loop_capture_into(top, cs[0], [&]() -> cudaError_t {
+    cudaStream_t s = cs[0];
+    sssp_init_g<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, G->st, G->fvd, G->F, G->Fv, G->cand,
+                                                      G->changed);
+    cudaGraphConditionalHandle h_loop, h_dir;
+    cudaGraph_t g = capturing_graph(s);
+    GB_LTRY(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
+    GB_LTRY(cudaGraphConditionalHandleCreate(&h_dir, g, 0, cudaGraphCondAssignDefault));
+    sssp_start_g<<<1, 1, 0, s>>>(G->st, n, nnz, h_loop, h_dir);
+    GB_LTRY(cudaGetLastError());
+    cudaGraph_t body;
+    GB_LTRY(add_conditional(s, h_loop, cudaGraphCondTypeWhile, 1, &body));
+    return loop_capture_into(body, cs[1], [&]() -> cudaError_t {
+      cudaStream_t b = cs[1];
+      cudaGraph_t br[2];
+      GB_LTRY(add_conditional(b, h_dir, cudaGraphCondTypeSwitch, 2, br));
+      GB_LTRY(loop_capture_into(br[0], cs[2], [&]() -> cudaError_t {
+        if (!G->has_pull) return cudaSuccess;
+        if (G->plan.R)
+          sssp_pull_tiles<<<resident_grid(ctx, sssp_pull_tiles, 256), 256, 0, cs[2]>>>(
+              G->plan.R, G->plan.nz_rows, G->plan.nz_off, G->pull.indices, G->plan.tile_first,
+              G->pull.values, G->pull.dtype, G->pull.iso_f64, G->fvd, G->cand);
+        sssp_pull_apply_g<<<grid_for(ctx, n, 256), 256, 0, cs[2]>>>(n, G->cand, G->st, G->changed);
+        return cudaGetLastError();
+      }));
+      GB_LTRY(loop_capture_into(br[1], cs[2], [&]() -> cudaError_t {
+        const SsspPushOp op{G->push.indices, G->push.values, G->push.dtype, G->push.iso_f64,
+                            G->Fv, &G->st->dist, G->changed, &G->st->cnt[1]};
+        // the frontier size K: the previous finalize's count, kept in the state
+        push_short<SsspPushOp><<<grid_for(ctx, n * 32, 256, 8), 256, 0, cs[2]>>>(
+            reinterpret_cast<const unsigned long long*>(&G->st->K), G->F, G->push.offsets,
+            G->longk, G->longc, &G->st->nlong, op);
+        push_long<SsspPushOp><<<grid_for(ctx, G->push.nnz / 16 + 32, 256, 8), 256, 0, cs[2]>>>(
+            &G->st->nlong, G->longk, G->longc, G->F, G->push.offsets, op);
+        return cudaGetLastError();
+      }));
+      reset_fvd_g<<<grid_for(ctx, n, 256), 256, 0, b>>>(G->st, G->F, G->fvd);
+      sssp_finalize_g<<<grid_for(ctx, W, 256), 256, 0, b>>>(n, G->changed, G->st, G->F, G->Fv,
+                                                            G->fvd);
+      sssp_step_g<<<1, 1, 0, b>>>(G->st, n, nnz, h_loop, h_dir);
+      return cudaGetLastError();
+    });
+  });
+  if (err == cudaSuccess) err = cudaGraphInstantiate(&G->exec, top, 0);
+  cudaGraphDestroy(top);
+  for (auto& x : cs) cudaStreamDestroy(x);
+  return err;
+}
+
+static gb_status sssp_graph(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t source,
+                            int64_t max_iters, double ratio, int32_t policy, double* dist,
+                            int32_t* log_dir, int64_t* log_nvals, int64_t* log_est,
+                            int64_t* iters_out) {
+  const int64_t n = push->nrows;
+  void** slot = ctx_slot(ctx, SLOT_SSSP_GRAPH, sssp_graph_free);
+  SsspGraph* G = static_cast<SsspGraph*>(*slot);
+  cudaStream_t s = stream_of(ctx);
+  if (G && !(loop_same_csr(&G->push, push) && G->has_pull == (pull != nullptr) &&
+             (!pull || loop_same_csr(&G->pull, pull)))) {
+    cudaStreamSynchronize(s);
+    sssp_graph_free(G);
+    *slot = G = nullptr;
+  }
+  if (!G) {
+    G = new SsspGraph();
+    G->push = *push;
+    G->has_pull = pull != nullptr;
+    if (pull) G->pull = *pull;
+    const int64_t W = (n + 31) / 32;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += (b + 255) / 256 * 256; return o; };
+    const size_t ntask = (size_t)n + (size_t)(push->nnz / kLongChunk) + 1;
+    const size_t o_c = take(4 * (size_t)W), o_F = take(4 * (size_t)n), o_L = take(4 * ntask);
+    const size_t o_LC = take(4 * ntask);
+    const size_t o_Fv = take(8 * (size_t)n), o_fvd = take(8 * (size_t)n);
+    const size_t o_cand = take(8 * (size_t)n), o_st = take(sizeof(SsspState));
+    const size_t o_r = pull ? take(4 * (size_t)n) : 0, o_o = pull ? take(8 * (size_t)(n + 1)) : 0;
+    const size_t o_t = pull ? take(4 * (size_t)(pull->nnz / kRowTile + 2)) : 0;
+    if (cudaMalloc(&G->mem, off) != cudaSuccess) {
+      cudaGetLastError();
+      delete G;
+      return GB_ERR_UNSUPPORTED;
+    }
+    char* m = static_cast<char*>(G->mem);
+    G->changed = (uint32_t*)(m + o_c);
+    G->F = (int32_t*)(m + o_F);
+    G->longk = (int32_t*)(m + o_L);
+    G->longc = (int32_t*)(m + o_LC);
+    G->Fv = (double*)(m + o_Fv);
+    G->fvd = (double*)(m + o_fvd);
+    G->cand = (long long*)(m + o_cand);
+    G->st = (SsspState*)(m + o_st);
+    gb_status st = GB_OK;
+    if (pull) {
+      G->plan.nz_rows = (int32_t*)(m + o_r);
+      G->plan.nz_off = (int64_t*)(m + o_o);
+      G->plan.tile_first = (int32_t*)(m + o_t);
+      Arena ar(ctx);
+      st = row_tiles_plan(ctx, ar, n, pull->offsets, pull->nnz, &G->plan);
+    }
+    cudaError_t e = st == GB_OK ? sssp_graph_build(ctx, G) : cudaSuccess;
+    if (st != GB_OK || e != cudaSuccess) {
+      cudaGetLastError();
+      sssp_graph_free(G);
+      return st != GB_OK ? st : set_error(ctx, GB_ERR_CUDA, "sssp graph: %s", cudaGetErrorString(e));
+    }
+    *slot = G;
+  }
+  Arena ar(ctx);
+  const int64_t cap = max_iters > 0 ? max_iters : 1;
+  int64_t* dlog = ar.alloc<int64_t>(3 * cap + 1);
+  GB_ARENA_CHECK(ctx, ar);
+  SsspState h{};
+  h.ratio = ratio;
+  h.max_iters = max_iters;
+  h.source = source;
+  h.log = dlog;
+  h.dist = dist;
+  h.policy = policy;
+  GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(SsspState, it), cudaMemcpyHostToDevice, s));
+  GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
+  int64_t iters = 0;
+  GB_CUDA(ctx, cudaMemcpyAsync(&iters, &G->st->iters, 8, cudaMemcpyDeviceToHost, s));
+  GB_CUDA(ctx, cudaStreamSynchronize(s));
+  std::vector<int64_t> lg(3 * (iters > 0 ? iters : 1));
+  if (iters > 0) {
+    GB_CUDA(ctx, cudaMemcpyAsync(lg.data(), dlog, 8 * 3 * iters, cudaMemcpyDeviceToHost, s));
+    GB_CUDA(ctx, cudaStreamSynchronize(s));
+  }
+  for (int64_t i = 0; i < iters; ++i) {
+    log_dir[i] = (int32_t)lg[3 * i];
+    log_nvals[i] = lg[3 * i + 1];
+    log_est[i] = lg[3 * i + 2];
+  }
+  // a pull iteration the graph met without the column orientation: report it
+  // the way the host loop does
+  for (int64_t i = 0; i < iters; ++i)
+    if (log_dir[i] == GB_DIR_PULL && !pull)
+      return set_error(ctx, GB_ERR_FORMAT, "column-oriented storage missing");
+  count_launch(ctx, (int)(2 + 5 * iters));
+  *iters_out = iters;
+  return GB_OK;
+}
+
 }  // namespace gb
 
 using namespace gb;
@@ -446,12 +1367,25 @@ extern "C" {
 
 typedef void (*gb_iter_cb)(int64_t iteration, void* user);
 
+int32_t gb_loop_engine(int32_t engine) {
+  const int32_t prev = loop_engine();
+  if (engine == kLoopGraph || engine == kLoopHost) g_loop_engine = engine;
+  return prev;
+}
+
 gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t source,
                   int64_t max_iters, double ratio, int32_t policy, double* dist,
                   int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out,
                   gb_iter_cb cb, void* user) {
   const int64_t n = push->nrows;
   if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source out of range");
+  // device-resident loop unless a per-iteration host callback is requested
+  // or the kernels are being timed one by one
+  if (!cb && loop_engine() == kLoopGraph && !prof_enabled(ctx)) {
+    const gb_status st = sssp_graph(ctx, push, pull, source, max_iters, ratio, policy, dist,
+                                    log_dir, log_nvals, log_est, iters_out);
+    if (st != GB_ERR_UNSUPPORTED) return st;
+  }
   Arena ar(ctx);
   cudaStream_t s = stream_of(ctx);
   const int64_t W = (n + 31) / 32;
@@ -530,6 +1464,12 @@ gb_status gb_pagerank(gb_ctx* ctx, const gb_csr* pull, const int64_t* out_offset
                       double* ranks_out, int32_t* log_dir, int64_t* log_nvals, int64_t* log_est,
                       double* err_out, int64_t* iters_out) {
   const int64_t n = pull->nrows;
+  if (loop_engine() == kLoopGraph && !prof_enabled(ctx) && n > 0) {
+    const gb_status st = pagerank_graph(ctx, pull, out_offsets, alpha, eps, max_iters, ratio,
+                                        policy, ranks_out, log_dir, log_nvals, log_est, err_out,
+                                        iters_out);
+    if (st != GB_ERR_UNSUPPORTED) return st;
+  }
   Arena ar(ctx);
   cudaStream_t s = stream_of(ctx);
   double* inv = ar.alloc<double>(n);
@@ -589,6 +1529,11 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
                 int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   const int64_t n = rows->nrows;
   if (n >= kImax32) return set_error(ctx, GB_ERR_UNSUPPORTED, "cc needs n < 2^31 - 1");
+  if (loop_engine() == kLoopGraph && !prof_enabled(ctx) && n > 0) {
+    const gb_status st = cc_graph(ctx, rows, cols, max_iters, ratio, policy, sparsify, parent,
+                                  log_dir, log_nvals, log_est, iters_out);
+    if (st != GB_ERR_UNSUPPORTED) return st;
+  }
   Arena ar(ctx);
   cudaStream_t s = stream_of(ctx);
   int* P = ar.alloc<int>(n);
