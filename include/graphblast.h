@@ -508,6 +508,17 @@ gb_status gb_bfs(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
  * previous setting; process-wide. */
 int32_t gb_bfs_engine(int32_t engine);
 
+/* Result certificates (the CLI's --verify; independent of the kernels that
+ * computed the result).  gb_sssp_certify: errors_host[3] = {dist[source] != 0,
+ * stored edges (u, v, w) with dist[u] + w < dist[v], reached v != source
+ * without a tight in-edge}; `in_edges` = rows of A^T with A's weights.
+ * gb_cc_certify: errors_host[2] = {vertices with label > v or label[label] !=
+ * label, stored edges joining different labels}.  Both synchronize. */
+gb_status gb_sssp_certify(gb_ctx* ctx, const gb_csr* in_edges, int64_t source, const double* dist,
+                          int64_t* errors_host);
+gb_status gb_cc_certify(gb_ctx* ctx, const gb_csr* a, const int64_t* labels,
+                        int64_t* errors_host);
+
 /* BFS parents (extension; the reference returns levels only,
  * algorithms.py:66-77): parent[v] = the smallest u with (u, v) stored in A and
  * level[u] = level[v] - 1; parent[source] = source; -1 when unreached.

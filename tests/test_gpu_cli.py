@@ -75,3 +75,32 @@ def test_binary_csr_cache_round_trip(tmp_path):
     save_matrix(str(tmp_path / "s12.npz"), gb.io.rmat_matrix(12))
     rc, out = run_cli("bfs", "--graph", str(tmp_path / "s12.npz"), "--runs", "1", "--json")
     assert rc == 0 and json.loads(out)["result_digest"] == gold["digest"]
+
+
+def test_cli_certificates_reject_corrupted_results():
+    """--verify's SSSP / CC certificates (gb_sssp_certify, gb_cc_certify) fail
+    on a perturbed result and pass on the computed one."""
+    import numpy as np
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200 import cli
+    from paper_1908_01407_b200.containers import Vector
+    args = cli.build_parser().parse_args(["sssp", "--rmat-scale", "10"])
+    h = cli.Harness(args)
+    W = gb.io.rmat_matrix(10, weighted=True)
+    d = gb.sssp(W, 0)
+    assert h._certify_sssp(W, d)
+    bad = d.to_dense(np.inf)._vals.clone()
+    v = int(np.flatnonzero(np.isfinite(d.values) & (d.values > 0))[3])
+    bad[v] += 1.0
+    assert not h._certify_sssp(W, Vector._wrap(W.nrows, None, bad, np.inf, np.float64))
+    bad = d.to_dense(np.inf)._vals.clone()
+    bad[v] -= 0.5
+    assert not h._certify_sssp(W, Vector._wrap(W.nrows, None, bad, np.inf, np.float64))
+    A = gb.io.rmat_matrix(10)
+    lab = gb.connected_components(A)
+    args = cli.build_parser().parse_args(["cc", "--rmat-scale", "10"])
+    h = cli.Harness(args)
+    assert h._certify_cc(A, lab)
+    t = lab.to_dense(0)._vals.clone()
+    t[5] = 5 if int(t[5]) != 5 else 4     # a label that is not the class minimum
+    assert not h._certify_cc(A, Vector._wrap(A.nrows, None, t, 0, np.int64))
