@@ -527,6 +527,16 @@ gb_status gb_cc_certify(gb_ctx* ctx, const gb_csr* a, const int64_t* labels,
 gb_status gb_bfs_parents(gb_ctx* ctx, const gb_csr* in_edges, const int64_t* levels,
                          int64_t source, int64_t* parents);
 
+/* Work counters of a BFS run as the reference tallies them over its vxm
+ * calls (kernels.py:153-191, 242-280), recomputed from the final levels and
+ * the direction log (dirs_host[iters], GB_DIR_*): totals_host[3] = {entries
+ * read, multiplies, adds}.  out_edges = rows of A (push), in_edges = rows of
+ * A^T (pull); pattern matrices with <= 64 iterations, <= 4 of them pull
+ * (else GB_ERR_UNSUPPORTED).  Synchronizes. */
+gb_status gb_bfs_counters(gb_ctx* ctx, const gb_csr* out_edges, const gb_csr* in_edges,
+                          const int64_t* levels, int64_t iters, const int32_t* dirs_host,
+                          int32_t early_exit, int64_t* totals_host);
+
 /* Graph500-style validation of a BFS tree: errors_host[4] counts violations of
  * {source is its own parent at level 1; every reached v != source has a
  * reached parent one level up with (parent, v) stored; unreached vertices

@@ -109,6 +109,7 @@ SIGNATURES = {
                                    f64, i32, vp, vp, vp, vp]),
     "gb_count_launches": (None, [vp, i64]),
     "gb_bfs_parents": (i32, [vp, C.POINTER(gb_csr), vp, i64, vp]),
+    "gb_bfs_counters": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), vp, i64, vp, i32, vp]),
     "gb_sssp_certify": (i32, [vp, C.POINTER(gb_csr), i64, vp, vp]),
     "gb_cc_certify": (i32, [vp, C.POINTER(gb_csr), vp, vp]),
     "gb_bfs_validate": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, vp, vp, vp]),

@@ -197,6 +197,42 @@ def bfs(A: SparseMatrix, source: int, desc=None, early_exit=True) -> Vector:
     desc.early_exit = early_exit
     if not desc.fused:
         return _bfs_composed(A, source, desc)
+    if desc.count_work:
+        first = len(desc.direction_log)
+        levels = _bfs_fused(A, source, desc)
+        _bfs_count_work(A, source, desc, levels, desc.direction_log[first:])
+        return levels
+    return _bfs_fused(A, source, desc)
+
+
+def _bfs_count_work(A, source, desc, levels, decisions):
+    """desc.counters += the reference's tallies of this BFS (gb_bfs_counters:
+    recomputed from the levels and the direction log); beyond its limits
+    (valued matrices, > 64 levels, > 4 pull levels) the composition is
+    replayed for the counts."""
+    dirs = np.array([_lib.DIR_PULL if d.chosen == "pull" else _lib.DIR_PUSH for d in decisions],
+                    np.int32)
+    tot = np.zeros(3, np.int64)
+    try:
+        if not A.has_csc:
+            raise NotImplementedError
+        s, _k1 = A.orient(False).csr_struct()
+        t, _k2 = A.orient(True).csr_struct()
+        _lib.context().call("gb_bfs_counters", C.byref(s), C.byref(t), _lib.ptr(levels._vals),
+                            int(dirs.size), dirs.ctypes.data_as(C.c_void_p),
+                            1 if desc.early_exit else 0, tot.ctypes.data_as(C.c_void_p))
+    except NotImplementedError:
+        d = Descriptor(direction=desc.direction, switch_ratio=desc.switch_ratio,
+                       max_niter=desc.max_niter, fused=False, early_exit=desc.early_exit)
+        _bfs_composed(A, source, d)
+        tot[:] = (d.counters.matrix_entries_read, d.counters.semiring_multiplies,
+                  d.counters.semiring_adds)
+    desc.counters.matrix_entries_read += int(tot[0])
+    desc.counters.semiring_multiplies += int(tot[1])
+    desc.counters.semiring_adds += int(tot[2])
+
+
+def _bfs_fused(A, source, desc):
     n = A.nrows
     iters = min(desc.max_niter, n + 1)
     if iters <= 0:
@@ -286,6 +322,16 @@ def validate_bfs(A: SparseMatrix, source: int, levels, parents) -> dict:
     return out
 
 
+def _replay_counts(desc, run):
+    """count_work for SSSP / CC / TC: the reference's tallies come from
+    replaying the operator composition (run(d) with a fused=False copy of the
+    descriptor's settings); results still come from the fused driver."""
+    d = Descriptor(direction=desc.direction, switch_ratio=desc.switch_ratio,
+                   max_niter=desc.max_niter, fused=False)
+    run(d)
+    desc.counters.merge(d.counters)
+
+
 def _bfs_composed(A, source, desc):
     boolean = builtin_semiring("LogicalOrAnd")
     plus = builtin_monoid("Plus")
@@ -321,6 +367,8 @@ def sssp(A: SparseMatrix, source: int, desc=None, on_iteration=None) -> Vector:
     desc = desc if desc is not None else Descriptor()
     if not desc.fused:
         return _sssp_composed(A, source, desc, on_iteration)
+    if desc.count_work:
+        _replay_counts(desc, lambda d: _sssp_composed(A, source, d, None))
     n = A.nrows
     iters = min(desc.max_niter, n)
     dist = empty(n, np.float64)
@@ -412,6 +460,27 @@ def pagerank(A: SparseMatrix, alpha=0.85, eps=1e-7, max_iters=10_000, desc=None)
     desc = desc if desc is not None else Descriptor()
     if not desc.fused or desc.direction is Direction.FORCE_PUSH or A.nnz == 0:
         return _pagerank_composed(A, alpha, eps, max_iters, desc)
+    first = len(desc.direction_log) if desc.count_work else 0
+    out = _pagerank_fused(A, alpha, eps, max_iters, desc)
+    if desc.count_work:
+        log = desc.direction_log[first:]
+        if all(d.chosen == "pull" and d.frontier_nvals == A.nrows for d in log):
+            # every iterate positive (teleport > 0): each pull reads and
+            # multiplies every stored entry, one segment per non-empty row
+            # (kernels.py:153-191)
+            nnz = A.nnz
+            rows = int(A.orient(True).row_plan()[0].nrows_nz)
+            desc.counters.matrix_entries_read += nnz * len(log)
+            desc.counters.semiring_multiplies += nnz * len(log)
+            desc.counters.semiring_adds += (nnz - rows) * len(log)
+        else:
+            d = Descriptor(direction=desc.direction, switch_ratio=desc.switch_ratio, fused=False)
+            _pagerank_composed(A, alpha, eps, max_iters, d)
+            desc.counters.merge(d.counters)
+    return out
+
+
+def _pagerank_fused(A, alpha, eps, max_iters, desc):
     n = A.nrows
     ranks = empty(n, np.float64)
     trav = A.traversal() if _ORDERED_PR else None
@@ -483,6 +552,8 @@ def connected_components(A: SparseMatrix, desc=None, sparsify=True) -> Vector:
     desc = desc if desc is not None else Descriptor()
     if not desc.fused:
         return _cc_composed(A, desc, sparsify)
+    if desc.count_work:
+        _replay_counts(desc, lambda d: _cc_composed(A, d, sparsify))
     n = A.nrows
     parent = empty(n, np.int64)
     rows, _k1 = A.orient(False).csr_struct()
@@ -556,6 +627,8 @@ def triangle_count(A: SparseMatrix, desc=None) -> int:
     desc = desc if desc is not None else Descriptor()
     if not desc.fused:
         return _tc_composed(A, desc)
+    if desc.count_work:
+        _replay_counts(desc, lambda d: _tc_composed(A, d))
     o = A.orient(False)
     if o.values is not None or (o.iso is not None and o.iso != 1):
         # weighted entries: the product sums value products, not a count

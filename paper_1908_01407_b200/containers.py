@@ -132,6 +132,10 @@ class Descriptor:
     Extensions (not in the reference): ``fused`` -- algorithms run their
     fused device loops (default); ``False`` replays the reference's exact
     operator composition so ``counters`` carry the reference's tallies.
+    ``count_work`` -- the fused algorithms also fill ``counters`` with the
+    reference's exact tallies (BFS: recomputed on the device from the levels
+    and the direction log, gb_bfs_counters; PageRank: from the direction log;
+    SSSP / CC / TC: by running the operator composition), at extra cost.
     ``num_workers`` is accepted and ignored (the GPU grid replaces the
     thread pool).
     """
@@ -148,6 +152,7 @@ class Descriptor:
     counters: Counters = field(default_factory=Counters)
     direction_log: list = field(default_factory=DecisionLog)
     fused: bool = True
+    count_work: bool = False
 
     _TOGGLES = {"mask": "mask_mode", "inp0": "transpose_inp0", "inp1": "transpose_inp1"}
 
