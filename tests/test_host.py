@@ -173,5 +173,6 @@ def test_cli_parser_matches_reference_surface():
         ("force-pull", 0.2, 8, 7, 0.9, 1e-6)
     with pytest.raises(SystemExit):
         p.parse_args(["dfs"])
-    d = cli._make_descriptor(a, fused=False)
+    d = cli.Harness(a).descriptor(fused=False)
     assert d.direction.value == "force-pull" and d.max_niter == 7 and d.fused is False
+    assert d.switch_ratio == 0.2
