@@ -275,6 +275,16 @@ gb_status gb_mxv_pull_binned(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const
                              const gb_bin_plan* plan, const void* u, const uint32_t* mask,
                              void* out, int64_t* counters);
 
+/* The binned pull over COLUMN STRIPES of a matrix (stripes[k]: the same rows,
+ * the entries with columns in stripe k -- gb_csr_column_block -- and
+ * plans[k] its row bins): the stripes are multiplied one after the other and
+ * folded into `out`, so each stripe's slice of u stays L2-resident while it
+ * is gathered.  Same contract and counters as gb_mxv_pull_binned.
+ * Asynchronous. */
+gb_status gb_mxv_pull_striped(gb_ctx* ctx, int32_t add_op, int32_t mult_op, int32_t nstripes,
+                              const gb_csr* stripes, const gb_bin_plan* plans, const void* u,
+                              const uint32_t* mask, void* out, int64_t* counters);
+
 /* gb_mxv_pull on the degree-ordered layout of the same matrix (same results,
  * kernels.py:153-229; commutative folds without early exit).  `a` is the
  * relabelled orientation P A P^T (gb_csr_relabel_t), `plan` its row plan with

@@ -127,6 +127,7 @@ SIGNATURES = {
     "gb_bin_plan_fill": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_bin_plan)]),
     "gb_mxv_pull_binned": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_bin_plan), vp, vp,
                                  vp, vp]),
+    "gb_mxv_pull_striped": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "gb_index_max": (i32, [vp, i64, vp, pi64]),
     "gb_probe_rate": (i32, [vp, i64, i64, C.POINTER(f64)]),
     "gb_gather_replay_rate": (i32, [vp, C.POINTER(gb_csr), vp, C.POINTER(f64)]),

@@ -470,7 +470,7 @@ class _Orient:
     """One orientation on the device: rows of A (CSR) or of A^T (CSC)."""
 
     __slots__ = ("nrows", "ncols", "offsets", "indices", "values", "iso", "dt", "_nonempty",
-                 "_plan", "_bins", "_ordered", "_order", "_mv_ordered", "gen", "__weakref__")
+                 "_plan", "_bins", "_stripes", "_ordered", "_order", "_mv_ordered", "gen", "__weakref__")
 
     def __init__(self, nrows, ncols, offsets, indices, values, iso, dt):
         self.nrows, self.ncols = int(nrows), int(ncols)
@@ -480,6 +480,7 @@ class _Orient:
         self._nonempty = None
         self._plan = None
         self._bins = None
+        self._stripes = None
         self._ordered = None
         self._order = None       # new -> original id of the traversal layout
         self._mv_ordered = {}    # transpose -> ordered masked-pull view (SparseMatrix.ordered_pull)
@@ -511,6 +512,43 @@ class _Orient:
             ctx.call("gb_bin_plan_fill", C.byref(s), C.byref(p))
             self._bins = (p, bufs)
         return self._bins
+
+    def stripes(self, count):
+        """Column stripes of this (structure-only) orientation for the striped
+        pull (gb_mxv_pull_striped): `count` CSRs over the same rows, stripe k
+        holding the entries with columns in [k*w, (k+1)*w), w =
+        ceil(ncols/count) rounded up to 1024, each with its row bins.  Built
+        once per count.  Returns (gb_csr array, gb_bin_plan array, keepalive)."""
+        if self._stripes is not None and self._stripes[0] == count:
+            return self._stripes[1]
+        if self.values is not None:
+            raise NotImplementedError("column stripes take a structure-only matrix")
+        n, nc = self.nrows, self.ncols
+        w = -(-nc // count)
+        w = -(-w // 1024) * 1024
+        ctx = _lib.context()
+        s, _keep = self.csr_struct()
+        subs = []
+        for k in range(count):
+            lo, hi = min(k * w, nc), min((k + 1) * w, nc)
+            off = empty(n + 1, np.int64)
+            cnt = C.c_int64(0)
+            ctx.call("gb_csr_column_block", C.byref(s), lo, hi, _lib.ptr(off), None, C.byref(cnt))
+            idx = empty(max(int(cnt.value), 1), np.int32)
+            ctx.call("gb_csr_column_block", C.byref(s), lo, hi, _lib.ptr(off), _lib.ptr(idx),
+                     C.byref(cnt))
+            subs.append(_Orient(n, nc, off, idx[:int(cnt.value)], None, self.iso, self.dt))
+        csrs = (_lib.gb_csr * count)()
+        plans = (_lib.gb_bin_plan * count)()
+        keep = []
+        for k, sub in enumerate(subs):
+            st, kk = sub.csr_struct()
+            csrs[k] = st
+            plan, pk = sub.bin_plan()
+            plans[k] = plan
+            keep += [kk, pk]
+        self._stripes = (count, (csrs, plans, (subs, keep)))
+        return self._stripes[1]
 
     def row_plan(self):
         """Edge-balanced work plan of this orientation (gb_row_plan_build):

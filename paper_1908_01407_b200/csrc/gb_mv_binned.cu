@@ -55,7 +55,7 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
                const int32_t* __restrict__ idx, const T* __restrict__ vals, T iso,
                const T* __restrict__ u, const uint32_t* __restrict__ mask, int add_rt,
                int mult_rt, T* __restrict__ out, unsigned long long* __restrict__ counters,
-               uint32_t* __restrict__ hasmul) {
+               uint32_t* __restrict__ hasmul, int accumulate) {
   const int add_op = ADD >= 0 ? ADD : add_rt;
   const int mult_op = MUL >= 0 ? MUL : mult_rt;
   const T ident = op_identity<T>(add_op);
@@ -64,15 +64,6 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long c_reads = 0, c_muls = 0, c_rows = 0;  // warp-wide work (lanes 0 / 16)
   unsigned long long s_reads = 0, s_muls = 0, s_rows = 0;  // per lane (short rows)
-  auto fold_one = [&](T& acc, int& cnt, bool live, int64_t p, int32_t c) {
-    if (live) {
-      const T x = ld_gather(u + c);
-      if (x != ident) {
-        acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, VALS ? bin_aval(vals, iso, p) : iso, x));
-        ++cnt;
-      }
-    }
-  };
   // fold a gathered value (identity values are skipped, kernels.py:167)
   auto fold_one_v = [&](T& acc, int& cnt, T x, int64_t p) {
     if (x != ident) {
@@ -189,9 +180,14 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
       if (hl == 0 && h > l) {
         c_reads += (unsigned long long)(h - l);
         if (cnt > 0) {
-          out[rr] = acc;
           c_muls += cnt;
-          ++c_rows;
+          if (accumulate) {  // a column stripe: fold into the earlier stripes' value
+            out[rr] = op_fold<T>(add_op, out[rr], acc);
+            if (hasmul) atomicOr(hasmul + (rr >> 5), 1u << (rr & 31));
+          } else {
+            out[rr] = acc;
+            ++c_rows;
+          }
         }
       }
     }
@@ -209,13 +205,25 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
       for (int q = 0; q < kBinShort; ++q) cols[q] = q < len ? __ldg(idx + lo + q) : 0;
       T acc = ident;
       int cnt = 0;
+      // gathers in two waves of 8, every load of a wave in flight together
 #pragma unroll
-      for (int q = 0; q < kBinShort; ++q) fold_one(acc, cnt, q < len, lo + q, cols[q]);
+      for (int w = 0; w < kBinShort / 8; ++w) {
+        T x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = 8 * w + k < len ? ld_gather(u + cols[8 * w + k]) : ident;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fold_one_v(acc, cnt, x[k], lo + 8 * w + k);
+      }
       s_reads += (unsigned long long)len;
       if (cnt > 0) {
-        out[r] = acc;
         s_muls += cnt;
-        ++s_rows;
+        if (accumulate) {
+          out[r] = op_fold<T>(add_op, out[r], acc);
+          if (hasmul) atomicOr(hasmul + (r >> 5), 1u << (r & 31));
+        } else {
+          out[r] = acc;
+          ++s_rows;
+        }
       }
     }
   }
@@ -319,57 +327,71 @@ static gb_status bin_scan(gb_ctx* ctx, Arena& ar, const gb_csr* a, uint64_t** sm
 template <class T, int ADD, int MUL, bool VALS>
 static void launch_binned_k(gb_ctx* ctx, int add_op, int mult_op, const gb_bin_plan* p,
                             const gb_csr* a, T iso, const T* u, const uint32_t* mask, T* out,
-                            unsigned long long* counters, uint32_t* hasmul) {
+                            unsigned long long* counters, uint32_t* hasmul, int accumulate) {
   auto k = mv_pull_binned<T, ADD, MUL, VALS>;
   k<<<resident_grid(ctx, k, 256), 256, 0, stream_of(ctx)>>>(
       p->n_long_tiles, p->tile_row, p->tile_beg, p->tile_end, p->n_mid, p->mid_rows, p->n_short,
       p->short_rows, a->offsets, a->indices, (const T*)a->values, iso, u, mask, add_op, mult_op,
-      out, counters, hasmul);
+      out, counters, hasmul, accumulate);
 }
 
 template <class T, int ADD, int MUL>
 static void launch_binned_v(gb_ctx* ctx, int add_op, int mult_op, const gb_bin_plan* p,
                             const gb_csr* a, T iso, const T* u, const uint32_t* mask, T* out,
-                            unsigned long long* counters, uint32_t* hasmul) {
+                            unsigned long long* counters, uint32_t* hasmul, int accumulate) {
   if (a->values)
-    launch_binned_k<T, ADD, MUL, true>(ctx, add_op, mult_op, p, a, iso, u, mask, out, counters, hasmul);
+    launch_binned_k<T, ADD, MUL, true>(ctx, add_op, mult_op, p, a, iso, u, mask, out, counters,
+                                       hasmul, accumulate);
   else
-    launch_binned_k<T, ADD, MUL, false>(ctx, add_op, mult_op, p, a, iso, u, mask, out, counters, hasmul);
+    launch_binned_k<T, ADD, MUL, false>(ctx, add_op, mult_op, p, a, iso, u, mask, out, counters,
+                                        hasmul, accumulate);
 }
 
+// nstripes == 1: the whole matrix; > 1: column stripes of it (each a CSR
+// over the same rows), folded into `out` one after the other so every
+// stripe's slice of u stays L2-resident while it is gathered
 template <class T>
-static gb_status pull_binned_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a,
-                               const gb_bin_plan* p, const T* u, const uint32_t* mask, T* out,
-                               int64_t* counters) {
+static gb_status pull_binned_t(gb_ctx* ctx, int add_op, int mult_op, int nstripes,
+                               const gb_csr* as, const gb_bin_plan* ps, const T* u,
+                               const uint32_t* mask, T* out, int64_t* counters) {
   cudaStream_t s = stream_of(ctx);
-  const int64_t n = a->nrows;
+  const int64_t n = as[0].nrows;
   const int64_t W = (n + 31) / 32;
   Arena ar(ctx);
   uint32_t* hasmul = counters ? ar.alloc<uint32_t>(W) : nullptr;
   GB_ARENA_CHECK(ctx, ar);
-  const T iso = std::is_same<T, double>::value ? (T)a->iso_f64 : (T)a->iso_i64;
   if (hasmul) GB_CUDA(ctx, cudaMemsetAsync(hasmul, 0, sizeof(uint32_t) * W, s));
   fill_identity<T>(ctx, n, op_identity<T>(add_op), out);
-  const int ps = prof_begin(ctx, PROF_MV, a->nnz);
+  int64_t nnz = 0;
+  for (int k = 0; k < nstripes; ++k) nnz += as[k].nnz;
+  const int prof = prof_begin(ctx, PROF_MV, nnz);
   unsigned long long* c = (unsigned long long*)counters;
-#define GB_SR(A_, M_)                                                                     \
-  if (add_op == A_ && mult_op == M_) {                                                    \
-    launch_binned_v<T, A_, M_>(ctx, add_op, mult_op, p, a, iso, u, mask, out, c, hasmul); \
-  } else
-  GB_SR(GB_OP_PLUS, GB_OP_TIMES)
-  GB_SR(GB_OP_LOR, GB_OP_LAND)
-  GB_SR(GB_OP_MIN, GB_OP_PLUS)
-  GB_SR(GB_OP_MAX, GB_OP_PLUS)
-  GB_SR(GB_OP_MIN, GB_OP_TIMES)
-  GB_SR(GB_OP_MIN, GB_OP_SECOND)
-  GB_SR(GB_OP_PLUS, GB_OP_LESS)
-  GB_SR(GB_OP_MIN, GB_OP_NE)
-  launch_binned_v<T, -1, -1>(ctx, add_op, mult_op, p, a, iso, u, mask, out, c, hasmul);
+  const int accumulate = nstripes > 1;
+  for (int k = 0; k < nstripes; ++k) {
+    const gb_csr* a = as + k;
+    const gb_bin_plan* p = ps + k;
+    const T iso = std::is_same<T, double>::value ? (T)a->iso_f64 : (T)a->iso_i64;
+#define GB_SR(A_, M_)                                                                  \
+    if (add_op == A_ && mult_op == M_) {                                               \
+      launch_binned_v<T, A_, M_>(ctx, add_op, mult_op, p, a, iso, u, mask, out, c, hasmul, \
+                                 accumulate);                                          \
+    } else
+    GB_SR(GB_OP_PLUS, GB_OP_TIMES)
+    GB_SR(GB_OP_LOR, GB_OP_LAND)
+    GB_SR(GB_OP_MIN, GB_OP_PLUS)
+    GB_SR(GB_OP_MAX, GB_OP_PLUS)
+    GB_SR(GB_OP_MIN, GB_OP_TIMES)
+    GB_SR(GB_OP_MIN, GB_OP_SECOND)
+    GB_SR(GB_OP_PLUS, GB_OP_LESS)
+    GB_SR(GB_OP_MIN, GB_OP_NE)
+    launch_binned_v<T, -1, -1>(ctx, add_op, mult_op, p, a, iso, u, mask, out, c, hasmul,
+                               accumulate);
 #undef GB_SR
-  prof_end(ctx, ps);
+  }
+  prof_end(ctx, prof);
   if (counters) mv_pull_finish_counts(ctx, W, hasmul, c);
   GB_LAUNCH_CHECK(ctx);
-  count_launch(ctx, 2);
+  count_launch(ctx, 1 + nstripes + (counters ? 1 : 0));
   return GB_OK;
 }
 
@@ -414,10 +436,28 @@ gb_status gb_mxv_pull_binned(gb_ctx* ctx, int32_t add_op, int32_t mult_op, const
   if (!plan || !fold_commutes(add_op))
     return set_error(ctx, GB_ERR_VALUE, "gb_mxv_pull_binned: needs a plan and a commutative fold");
   if (a->dtype == GB_I64)
-    return pull_binned_t<int64_t>(ctx, add_op, mult_op, a, plan, (const int64_t*)u, mask,
+    return pull_binned_t<int64_t>(ctx, add_op, mult_op, 1, a, plan, (const int64_t*)u, mask,
                                   (int64_t*)out, counters);
-  return pull_binned_t<double>(ctx, add_op, mult_op, a, plan, (const double*)u, mask,
+  return pull_binned_t<double>(ctx, add_op, mult_op, 1, a, plan, (const double*)u, mask,
                                (double*)out, counters);
+}
+
+gb_status gb_mxv_pull_striped(gb_ctx* ctx, int32_t add_op, int32_t mult_op, int32_t nstripes,
+                              const gb_csr* stripes, const gb_bin_plan* plans, const void* u,
+                              const uint32_t* mask, void* out, int64_t* counters) {
+  if (nstripes < 1 || !stripes || !plans)
+    return set_error(ctx, GB_ERR_ARG, "gb_mxv_pull_striped: needs >= 1 stripe and its plan");
+  if (stripes[0].nrows == 0) return GB_OK;
+  if (!fold_commutes(add_op))
+    return set_error(ctx, GB_ERR_VALUE, "gb_mxv_pull_striped: needs a commutative fold");
+  for (int k = 1; k < nstripes; ++k)
+    if (stripes[k].nrows != stripes[0].nrows || stripes[k].dtype != stripes[0].dtype)
+      return set_error(ctx, GB_ERR_SHAPE, "gb_mxv_pull_striped: stripes differ in rows or dtype");
+  if (stripes[0].dtype == GB_I64)
+    return pull_binned_t<int64_t>(ctx, add_op, mult_op, nstripes, stripes, plans,
+                                  (const int64_t*)u, mask, (int64_t*)out, counters);
+  return pull_binned_t<double>(ctx, add_op, mult_op, nstripes, stripes, plans, (const double*)u,
+                               mask, (double*)out, counters);
 }
 
 }  // extern "C"

@@ -36,14 +36,23 @@ def graphs(gb):
     return {"sym_f64": sym, "directed_f64": directed, "pattern_i64": pattern}
 
 
-IMPLS = {"tiles": ("0", "0"), "ordered": ("1", "0"), "bins": ("0", "1")}
+# (GB_MV_ORDERED, GB_MV_BINS, GB_MV_STRIPE_BYTES): "stripes" cuts a
+# structure-only matrix into 8 KB-of-vector column stripes (many stripes)
+IMPLS = {"tiles": ("0", "0", 0), "ordered": ("1", "0", 0), "bins": ("0", "1", 0),
+         "stripes": ("0", "1", 8192)}
+
+
+def _use(monkeypatch, impl):
+    from paper_1908_01407_b200 import kernels
+    ordered, bins, stripe = IMPLS[impl]
+    monkeypatch.setattr(kernels, "_MV_ORDERED", ordered)
+    monkeypatch.setattr(kernels, "_MV_BINS", bins)
+    monkeypatch.setattr(kernels, "_MV_STRIPE_BYTES", stripe)
+    monkeypatch.setattr(kernels, "_MV_STRIPE_SKEW", 1.0)   # stripe skewed graphs too
 
 
 def _run(gb, monkeypatch, impl, sr, A, u, mask, desc_kw, vxm):
-    from paper_1908_01407_b200 import kernels
-    ordered, bins = IMPLS[impl]
-    monkeypatch.setattr(kernels, "_MV_ORDERED", ordered)
-    monkeypatch.setattr(kernels, "_MV_BINS", bins)
+    _use(monkeypatch, impl)
     d = gb.Descriptor(direction=gb.Direction.FORCE_PULL, **desc_kw)
     w = gb.vxm(sr, u, A, mask=mask, desc=d) if vxm else gb.mxv(sr, A, u, mask=mask, desc=d)
     c = d.counters
@@ -54,7 +63,7 @@ def _run(gb, monkeypatch, impl, sr, A, u, mask, desc_kw, vxm):
 @pytest.mark.parametrize("name", SEMIRINGS)
 @pytest.mark.parametrize("gname", ["sym_f64", "directed_f64", "pattern_i64"])
 @pytest.mark.parametrize("vxm", [False, True])
-@pytest.mark.parametrize("impl", ["ordered", "bins"])
+@pytest.mark.parametrize("impl", ["ordered", "bins", "stripes"])
 def test_pull_variants_equal_row_tiles(gb, graphs, monkeypatch, name, gname, vxm, impl):
     A = graphs[gname]
     n = A.nrows
@@ -75,15 +84,15 @@ def test_pull_variants_equal_row_tiles(gb, graphs, monkeypatch, name, gname, vxm
             assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("impl", ["ordered", "bins"])
+@pytest.mark.parametrize("impl", ["ordered", "bins", "stripes"])
 def test_pull_variants_s20_against_torch(gb, monkeypatch, impl):
     """Size-independent check at s20: torch index_add reference and exact
     counters."""
-    from paper_1908_01407_b200 import kernels
     from paper_1908_01407_b200.containers import Vector
-    ordered, bins = IMPLS[impl]
-    monkeypatch.setattr(kernels, "_MV_ORDERED", ordered)
-    monkeypatch.setattr(kernels, "_MV_BINS", bins)
+    _use(monkeypatch, impl)
+    if impl == "stripes":
+        from paper_1908_01407_b200 import kernels
+        monkeypatch.setattr(kernels, "_MV_STRIPE_BYTES", 2 << 20)   # 4 stripes at s20
     A = gb.io.rmat_matrix(20)
     assert A.nnz >= 1 << 24
     n = A.nrows
@@ -95,6 +104,8 @@ def test_pull_variants_s20_against_torch(gb, monkeypatch, impl):
                mask=Vector._wrap(n, None, mb, 0, np.int64), desc=d)
     if impl == "ordered":
         assert A._csr._mv_ordered, "the s20 call did not take the ordered layout"
+    elif impl == "stripes":
+        assert A._csr._stripes is not None and A._csr._stripes[0] == 4
     else:
         assert A._csr._bins is not None, "the s20 call did not take the row bins"
     deg = torch.diff(A._csr.offsets)
@@ -141,3 +152,25 @@ def test_row_split_partition_and_ragged_rows(gb, monkeypatch, impl):
     assert d.counters.semiring_adds == int(keep.sum()) - int(((lens > 0) & (m == 0)).sum())
     if impl == "bins":
         assert A._csr._bins is not None
+
+
+def test_stripes_chosen_for_regular_graphs_only(gb, monkeypatch):
+    """The default dispatch stripes a uniform graph whose vector exceeds the
+    stripe budget and leaves a skewed R-MAT graph unstriped."""
+    from paper_1908_01407_b200 import kernels
+    monkeypatch.setattr(kernels, "_MV_STRIPE_BYTES", 64 << 10)   # 8 K entries per stripe
+    U = gb.io.rmat_matrix(14, a=.25, b=.25, c=.25, d=.25)
+    R = gb.io.rmat_matrix(14)
+    assert kernels._stripe_count(U._csr) == 2 and kernels._stripe_count(R._csr) == 1
+    n = U.nrows
+    x = np.random.default_rng(1).random(n)
+    m = gb.Vector.dense_of((np.arange(n) % 3 == 0).astype(np.int64), 0)
+    d = gb.Descriptor(direction=gb.Direction.FORCE_PULL, mask_mode=gb.MaskMode.COMPLEMENT)
+    w = gb.mxv(gb.builtin_semiring("PlusMultiplies"), U, gb.Vector.dense_of(x, 0.0), mask=m, desc=d)
+    assert U._csr._stripes is not None
+    rp, ci = U.row_offsets, U.col_indices
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    keep = (np.arange(n) % 3 != 0)[rows]
+    ref = np.zeros(n)
+    np.add.at(ref, rows[keep], x[ci[keep]])
+    np.testing.assert_allclose(w.to_dense(0.0).values, ref, rtol=1e-12, atol=0)

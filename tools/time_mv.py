@@ -20,9 +20,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=24)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--density", type=float, default=0.5)
+ap.add_argument("--uniform", action="store_true", help="a=b=c=d=.25 instead of R-MAT")
 args = ap.parse_args()
 
-A = gb.io.rmat_matrix(args.scale)
+A = (gb.io.rmat_matrix(args.scale, a=.25, b=.25, c=.25, d=.25) if args.uniform
+     else gb.io.rmat_matrix(args.scale))
 n = A.nrows
 g = torch.Generator(device="cuda").manual_seed(1)
 x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) + 0.5
@@ -74,7 +76,8 @@ R = int(((torch.diff(off) > 0) & allowed).sum())
 E_read = c.matrix_entries_read
 bytes_alg = n / 8 + min(2 * R, n + 1) * 8 + E_read * 4 + n * 8 + n * 8
 print(json.dumps({
-    "workload": f"mxv(PlusMultiplies f64, rmat-s{args.scale}, x dense, mask=~m {args.density:.0%}), pull",
+    "workload": f"mxv(PlusMultiplies f64, {'uniform' if args.uniform else 'rmat'}-s{args.scale}, "
+                f"x dense, mask=~m {args.density:.0%}), pull",
     "n": n, "nnz": A.nnz, "allowed_rows": R, "entries_read": E_read,
     "multiplies": c.semiring_multiplies, "adds": c.semiring_adds,
     "kernel_ms": round(kernel_ms, 4), "call_ms": round(call_ms, 4),
