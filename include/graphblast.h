@@ -112,6 +112,41 @@ int32_t gb_prof_read(gb_ctx* ctx, int32_t max, int32_t* kind_host, int64_t* arg_
                      float* ms_host);
 
 /* ----------------------------------------------------------------------------
+ * element-wise utilities of the operator layer (gb_util.cu); dtype codes
+ * GB_I64 = 0, GB_F64 = 1 and GB_I32 = 2 (index vectors).  Asynchronous unless
+ * they return a host count.
+ * --------------------------------------------------------------------------*/
+enum { GB_I32 = 2 };
+/* out[i] = i */
+gb_status gb_iota(gb_ctx* ctx, int32_t code, int64_t n, void* out);
+/* numpy astype between int32 / int64 / float64 (float -> int truncates) */
+gb_status gb_cast(gb_ctx* ctx, int64_t n, int32_t in_code, const void* in, int32_t out_code,
+                  void* out);
+/* keep entries i with flags[i] != 0, in order: out_idx (idx[i], or i when idx
+ * is NULL; NULL = not wanted) and out_vals (vals of dtype; NULL = not wanted);
+ * *count_host = kept.  Synchronizes. */
+gb_status gb_select_flags(gb_ctx* ctx, int64_t k, const int32_t* flags, const int32_t* idx,
+                          const void* vals, int32_t dtype, int32_t* out_idx, void* out_vals,
+                          int64_t* count_host);
+/* out[i] = src[tgt[i]] with int32 targets (dtype GB_I64 / GB_F64 / GB_I32) */
+gb_status gb_gather_i32(gb_ctx* ctx, int32_t dtype, int64_t k, const int32_t* tgt,
+                        const void* src, void* out);
+/* preprocess of weighted edges (io.py:220-249 before the dedup): drop
+ * src == dst, append the mirror when `mirror`; int64 outputs sized 2m;
+ * *count_host = edges written.  Synchronizes. */
+gb_status gb_edges_clean(gb_ctx* ctx, int64_t m, const int32_t* src, const int32_t* dst,
+                         const double* w, int32_t mirror, int64_t* out_src, int64_t* out_dst,
+                         double* out_w, int64_t* count_host);
+/* vals[p] = alpha / (row length) for every entry of row r (algorithms.py:122-129) */
+gb_status gb_scale_rows(gb_ctx* ctx, int64_t n, const int64_t* offsets, double alpha,
+                        double* vals);
+/* algorithms.py:206-218: vertices ranked by a stable ascending sort of their
+ * row length; the entries (rank[i], rank[j], a_ij) with rank[i] > rank[j]
+ * (outputs sized nnz; *count_host = kept).  Synchronizes. */
+gb_status gb_lower_by_rank(gb_ctx* ctx, const gb_csr* a, int64_t* out_rows, int64_t* out_cols,
+                           void* out_vals, int64_t* count_host);
+
+/* ----------------------------------------------------------------------------
  * matrix construction   (containers.py:307-364, io.py:220-315)
  * --------------------------------------------------------------------------*/
 

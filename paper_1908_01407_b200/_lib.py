@@ -32,6 +32,7 @@ GB_ERR_ARG = -8
 
 GB_I64 = 0
 GB_F64 = 1
+GB_I32 = 2
 
 # operator ids
 OP_PLUS, OP_PLUS_WRAP, OP_MINUS, OP_TIMES, OP_MIN, OP_MAX, OP_LOR, OP_LAND, OP_LESS, OP_NE, \
@@ -83,6 +84,13 @@ SIGNATURES = {
     "gb_last_error": (C.c_char_p, [vp]),
     "gb_scratch_bytes": (i64, [vp]),
     "gb_ctx_trim": (i32, [vp]),
+    "gb_iota": (i32, [vp, i32, i64, vp]),
+    "gb_cast": (i32, [vp, i64, i32, vp, i32, vp]),
+    "gb_select_flags": (i32, [vp, i64, vp, vp, vp, i32, vp, vp, pi64]),
+    "gb_gather_i32": (i32, [vp, i32, i64, vp, vp, vp]),
+    "gb_edges_clean": (i32, [vp, i64, vp, vp, vp, i32, vp, vp, vp, pi64]),
+    "gb_scale_rows": (i32, [vp, i64, vp, f64, vp]),
+    "gb_lower_by_rank": (i32, [vp, C.POINTER(gb_csr), vp, vp, vp, pi64]),
     "gb_launch_count": (i64, [vp]),
     "gb_ctx_set_profiling": (i32, [vp, i32]),
     "gb_prof_read": (i32, [vp, i32, vp, vp, vp]),

@@ -24,7 +24,7 @@ import torch
 from . import _lib
 from .algebra import LESS, MINUS, TIMES, builtin_monoid, builtin_semiring
 from .containers import (INDEX_DTYPE, DecisionLog, Descriptor, Direction, SparseMatrix, Vector,
-                         empty, full)
+                         empty, full, iota)
 from .errors import ShapeError
 from .kernels import (
     DirectionDecision,
@@ -513,11 +513,9 @@ def _pagerank_fused(A, alpha, eps, max_iters, desc):
 def _scale_rows(A, alpha):
     """algorithms.py:122-129: Â(i, j) = alpha / outdegree(i), as a device matrix."""
     o = A.orient(False)
-    deg = torch.diff(o.offsets)
-    inv = torch.zeros(A.nrows, dtype=torch.float64, device=deg.device)
-    nz = deg > 0
-    inv[nz] = alpha / deg[nz].to(torch.float64)
-    vals = torch.repeat_interleave(inv, deg)
+    vals = empty(o.nnz, np.float64)
+    _lib.context().call("gb_scale_rows", A.nrows, _lib.ptr(o.offsets), float(alpha),
+                        _lib.ptr(vals))
     return SparseMatrix.from_csr(A.nrows, A.ncols, o.offsets, o.indices, vals)
 
 
@@ -562,7 +560,7 @@ def connected_components(A: SparseMatrix, desc=None, sparsify=True) -> Vector:
     dirs, nv, est = np.zeros(cap, np.int32), np.zeros(cap, np.int64), np.zeros(cap, np.int64)
     done = C.c_int64(0)
     if desc.max_niter <= 0:
-        return Vector._wrap(n, None, torch.arange(n, dtype=torch.int64, device=parent.device), 0,
+        return Vector._wrap(n, None, iota(n, np.int64), 0,
                             np.int64)
     _lib.context().call(
         "gb_cc", C.byref(rows), C.byref(cols), int(desc.max_niter), float(desc.switch_ratio),
@@ -642,16 +640,14 @@ def triangle_count(A: SparseMatrix, desc=None) -> int:
 def _degree_sorted_lower_triangle(A):
     """algorithms.py:206-218 on the device."""
     o = A.orient(False)
-    deg = torch.diff(o.offsets)
-    order = torch.sort(deg, stable=True).indices
-    position = torch.empty_like(order)
-    position[order] = torch.arange(A.nrows, device=order.device)
-    rows = A.row_ids().to(torch.int64)
-    cols = o.indices.to(torch.int64)
-    pr, pc = position[rows], position[cols]
-    keep = pr > pc
-    vals = o.dense_values()
-    return SparseMatrix.from_tuples(pr[keep], pc[keep], vals[keep], A.nrows, A.ncols)
+    s, _k = o.csr_struct()
+    rows, cols = empty(max(o.nnz, 1), np.int64), empty(max(o.nnz, 1), np.int64)
+    vals = empty(max(o.nnz, 1), o.dt)
+    c = C.c_int64(0)
+    _lib.context().call("gb_lower_by_rank", C.byref(s), _lib.ptr(rows), _lib.ptr(cols),
+                        _lib.ptr(vals), C.byref(c))
+    k = int(c.value)
+    return SparseMatrix.from_tuples(rows[:k], cols[:k], vals[:k], A.nrows, A.ncols)
 
 
 def _tc_composed(A, desc):

@@ -227,6 +227,39 @@ def full(n, value, np_dtype) -> torch.Tensor:
     return torch.full((int(n),), value, dtype=_TORCH[np.dtype(np_dtype)], device=_device())
 
 
+_CODE_OF_TORCH = {torch.int64: 0, torch.float64: 1, torch.int32: 2}   # GB_I64 / GB_F64 / GB_I32
+
+
+def cast(t: torch.Tensor, np_dtype) -> torch.Tensor:
+    """numpy astype on a device array (gb_cast); t itself when already of dtype."""
+    want = _TORCH[np.dtype(np_dtype)]
+    if t.dtype == want:
+        return t
+    out = torch.empty(t.numel(), dtype=want, device=t.device)
+    if t.numel():
+        _lib.context().call("gb_cast", int(t.numel()), _CODE_OF_TORCH[t.dtype], _lib.ptr(t),
+                            _CODE_OF_TORCH[want], _lib.ptr(out))
+    return out
+
+
+def iota(n, np_dtype=np.int32) -> torch.Tensor:
+    """0, 1, ..., n-1 on the device (gb_iota)."""
+    out = empty(n, np_dtype)
+    if n:
+        _lib.context().call("gb_iota", _CODE_OF_TORCH[out.dtype], int(n), _lib.ptr(out))
+    return out
+
+
+def gather32(src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """src[idx] with int32 device indices (gb_gather_i32)."""
+    k = int(idx.numel())
+    out = torch.empty(k, dtype=src.dtype, device=src.device)
+    if k:
+        _lib.context().call("gb_gather_i32", _CODE_OF_TORCH[src.dtype], k,
+                            _lib.ptr(cast(idx, np.int32)), _lib.ptr(src), _lib.ptr(out))
+    return out
+
+
 def _zero_buf(zero, dt):
     return _lib.scalar_buf(zero, dt)
 
@@ -272,7 +305,7 @@ class Vector:
         if idx.size == 0:
             return cls._wrap(size, empty(0, np.int32), empty(0, dt), 0, dt)
         # sort + validate on the device through the CSR builder (one row)
-        rows = torch.zeros(idx.size, dtype=torch.int64, device=_device())
+        rows = full(idx.size, 0, np.int64)
         A = SparseMatrix.from_tuples(rows, idx, vals, 1, int(size), build_csc=False,
                                      _check_unique=True)
         o = A._csr
@@ -600,7 +633,7 @@ class _Orient:
             return None
         if dt == self.dt:
             return self.values
-        return self.values.to(_TORCH[dt])
+        return cast(self.values, dt)
 
     def nonempty(self):
         if self._nonempty is None:
@@ -892,7 +925,7 @@ class SparseMatrix:
             rank = self.traversal()[2]
             c = o._ordered
         if len(c) < 3:
-            o._ordered = (c[0], c[1], c[1][2].to(torch.int64))
+            o._ordered = (c[0], c[1], cast(c[1][2], np.int64))
         return o._ordered[2]
 
     def row_ids(self):

@@ -22,7 +22,7 @@ import torch
 
 from . import _lib
 from .algebra import builtin_monoid
-from .containers import INDEX_DTYPE, SparseMatrix, _Orient, empty, to_dev, to_host
+from .containers import INDEX_DTYPE, SparseMatrix, _Orient, cast, empty, full, to_dev, to_host
 from .errors import ParseError
 
 
@@ -155,13 +155,15 @@ def preprocess(edges: EdgeList, make_undirected=True) -> EdgeList:
 
 def _preprocess_weighted(edges, make_undirected):
     """Weighted edges: duplicates keep the minimum weight (io.py:245-247)."""
-    src, dst, w = edges._src, edges._dst, edges._w
-    keep = src != dst
-    src, dst, w = src[keep], dst[keep], w[keep]
-    if make_undirected:
-        src, dst = torch.cat([src, dst]), torch.cat([dst, src])
-        w = torch.cat([w, w])
-    A = SparseMatrix.from_tuples(src.to(torch.int64), dst.to(torch.int64), w, edges.n, edges.n,
+    m = edges.nedges
+    cap = max(2 * m if make_undirected else m, 1)
+    src, dst, w = empty(cap, np.int64), empty(cap, np.int64), empty(cap, np.float64)
+    c = C.c_int64(0)
+    _lib.context().call("gb_edges_clean", m, _lib.ptr(edges._src), _lib.ptr(edges._dst),
+                        _lib.ptr(edges._w), 1 if make_undirected else 0, _lib.ptr(src),
+                        _lib.ptr(dst), _lib.ptr(w), C.byref(c))
+    k = int(c.value)
+    A = SparseMatrix.from_tuples(src[:k], dst[:k], w[:k], edges.n, edges.n,
                                  dedup=builtin_monoid("Minimum"), build_csc=False)
     rows = A.row_ids()
     o = A._csr
@@ -198,7 +200,7 @@ def edges_to_matrix(edges: EdgeList, weighted=False, build_csc=True) -> SparseMa
             elif build_csc:
                 m._build_csc()
             return m
-        return SparseMatrix.from_tuples(edges._src.to(torch.int64), edges._dst.to(torch.int64),
+        return SparseMatrix.from_tuples(cast(edges._src, np.int64), cast(edges._dst, np.int64),
                                         edges._w, n, n, dedup=builtin_monoid("Minimum"),
                                         build_csc=build_csc)
     if edges._csr is not None:
@@ -210,8 +212,8 @@ def edges_to_matrix(edges: EdgeList, weighted=False, build_csc=True) -> SparseMa
         elif build_csc:
             m._build_csc()
         return m
-    ones = torch.ones(edges.nedges, dtype=torch.int64, device=edges._src.device)
-    return SparseMatrix.from_tuples(edges._src.to(torch.int64), edges._dst.to(torch.int64), ones,
+    ones = full(edges.nedges, 1, np.int64)
+    return SparseMatrix.from_tuples(cast(edges._src, np.int64), cast(edges._dst, np.int64), ones,
                                     n, n, dedup=builtin_monoid("Plus"), build_csc=build_csc)
 
 

@@ -29,10 +29,13 @@ from .containers import (
     Vector,
     _Orient,
     _TORCH,
+    cast,
     compact,
     device_dtype,
     empty,
     full,
+    gather32,
+    iota,
     to_dev,
 )
 from .errors import FormatError, ShapeError
@@ -66,8 +69,7 @@ def _buf(value, dt):
 
 
 def _as(t, dt):
-    dt = np.dtype(dt)
-    return t if t.dtype == _TORCH[dt] else t.to(_TORCH[dt])
+    return cast(t, dt)
 
 
 def _counters_tensor():
@@ -493,8 +495,7 @@ def ewise_mult(op: OpLike, u: Vector, v: Vector, mask=None, desc=None) -> Vector
     bm = _mask_bitmap(mask, u.size, desc.mask_mode)
     out = _dense_pair(opid, dtype, u._vals, v._vals, None, False, None, 0, u.size)
     if bm is not None:
-        idx = torch.arange(u.size, dtype=torch.int32, device=out.device)
-        i, vals = _filter(idx, out, dtype, bm)
+        i, vals = _filter(iota(u.size), out, dtype, bm)
         return Vector._wrap(u.size, i, vals, 0, dtype)
     return Vector._wrap(u.size, None, out, 0, dtype)
 
@@ -517,8 +518,7 @@ def assign(w: Vector, value, mask=None, desc=None, indices=None) -> Vector:
     if indices is not None:
         sel = to_dev(np.asarray(indices, dtype=INDEX_DTYPE), np.int32)
         if bm is not None:
-            sel, _ = _filter(sel, torch.zeros(int(sel.numel()), dtype=torch.int64,
-                                              device=sel.device), np.int64, bm)
+            sel, _ = _filter(sel, empty(int(sel.numel()), np.int64), np.int64, bm)
         bm = _bitmap_of_indices(sel, w.size)
     if w.size == 0:
         return w
@@ -557,13 +557,13 @@ def _targets_and_values(values, indices):
         tgt = out_t[:n]
         # values at the common positions: gather from the dense image of `values`
         vd = values.to_dense(values.zero)._vals
-        val = vd[common.long()] if n else empty(0, values._dt)
+        val = gather32(vd, common) if n else empty(0, values._dt)
         return tgt, val
     if indices.is_sparse:
         k = indices._idx
-        return indices._vals, values._vals[k.long()]
+        return indices._vals, gather32(values._vals, k)
     k = values._idx
-    return indices._vals[k.long()], values._vals
+    return gather32(indices._vals, k), values._vals
 
 
 def assign_scatter(w: Vector, values: Vector, indices: Vector, mask=None, desc=None) -> Vector:
@@ -572,7 +572,7 @@ def assign_scatter(w: Vector, values: Vector, indices: Vector, mask=None, desc=N
     if values.size != indices.size:
         raise ShapeError("values and indices must have equal size")
     tgt, val = _targets_and_values(values, indices)
-    tgt = tgt.to(torch.int64)
+    tgt = _as(tgt, np.int64)
     k = int(tgt.numel())
     if k:
         bad = C.c_int32(0)
@@ -581,8 +581,8 @@ def assign_scatter(w: Vector, values: Vector, indices: Vector, mask=None, desc=N
             raise IndexError("scatter target index out of range")
     bm = _mask_bitmap(mask, w.size, desc.mask_mode)
     if bm is not None and k:
-        t32, v2 = _filter(tgt.to(torch.int32), val, values._dt, bm)
-        tgt, val = t32.to(torch.int64), v2
+        t32, v2 = _filter(_as(tgt, np.int32), val, values._dt, bm)
+        tgt, val = _as(t32, np.int64), v2
         k = int(tgt.numel())
     if k == 0:
         return w
@@ -598,10 +598,9 @@ def extract_gather(w: Vector, u: Vector, indices: Vector, mask=None, desc=None) 
     dev = u._vals.device
     if indices.is_sparse:
         k = indices._idx
-        gather = indices._vals.to(torch.int64)
     else:
-        k = torch.arange(indices.size, dtype=torch.int32, device=dev)
-        gather = indices._vals.to(torch.int64)
+        k = iota(indices.size)
+    gather = _as(indices._vals, np.int64)
     n = int(gather.numel())
     dt = u._dt
     if u.is_sparse:
@@ -611,8 +610,12 @@ def extract_gather(w: Vector, u: Vector, indices: Vector, mask=None, desc=None) 
             _ctx().call("gb_gather_sparse", _code(dt), n, _lib.ptr(gather), int(u.size),
                         int(u._idx.numel()), _lib.ptr(u._idx), _lib.ptr(u._vals),
                         _lib.ptr(present), _lib.ptr(vals))
-            keep = present[:n].to(torch.bool)
-            k, vals = k[keep], vals[:n][keep]
+            ko = empty(n, np.int32)
+            vo = empty(n, dt)
+            c = C.c_int64(0)
+            _ctx().call("gb_select_flags", n, _lib.ptr(present), _lib.ptr(k), _lib.ptr(vals),
+                        _code(dt), _lib.ptr(ko), _lib.ptr(vo), C.byref(c))
+            k, vals = ko[:c.value], vo[:c.value]
         else:
             vals = vals[:0]
         sparse_out = True
@@ -624,9 +627,9 @@ def extract_gather(w: Vector, u: Vector, indices: Vector, mask=None, desc=None) 
         sparse_out = indices.is_sparse
     bm = _mask_bitmap(mask, w.size, desc.mask_mode)
     if bm is not None:
-        k, vals = _filter(k.to(torch.int32), vals, dt, bm)
+        k, vals = _filter(_as(k, np.int32), vals, dt, bm)
         sparse_out = True
-    w._idx = k.to(torch.int32).clone() if sparse_out else None
+    w._idx = _as(k, np.int32).clone() if sparse_out else None
     w._vals = vals.clone()
     w._dt = dt
     w.zero = dt.type(w.zero)
@@ -663,8 +666,7 @@ def apply(fn, u: Vector, mask=None, desc=None) -> Vector:
     elif u.is_sparse:
         idx, vals = _filter(u._idx, u._vals, u._dt, bm)
     else:
-        ar = torch.arange(u.size, dtype=torch.int32, device=u._vals.device)
-        idx, vals = _filter(ar, u._vals, u._dt, bm)
+        idx, vals = _filter(iota(u.size), u._vals, u._dt, bm)
     out = _apply_values(fn, vals, u._dt)
     odt = device_dtype(np.dtype(str(out.dtype).replace("torch.", "")))
     if bm is None and not u.is_sparse:
