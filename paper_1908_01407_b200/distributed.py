@@ -259,9 +259,13 @@ def bfs_partitioned(g: BlockGraph, source: int, desc=None, steps=None, exchange=
     desc = desc if desc is not None else Descriptor()
     steps = steps if steps is not None else NativeSteps(g)
     exchange = exchange if exchange is not None else FrontierExchange()
-    steps.init(source)
-    K, depth = 1, 1
     iters = min(desc.max_niter, g.n + 1)
+    steps.init(source)
+    if iters <= 0:
+        # the reference loop runs zero times: nothing is stamped, not even the source
+        steps.unstamp(1)
+        return steps.levels
+    K, depth = 1, 1
     for it in range(iters):
         chosen, est, thr = direction_rule(g.nnz, g.n, K, desc.switch_ratio, desc.direction)
         desc.direction_log.append(DirectionDecision(chosen, K, est, g.nnz, thr))

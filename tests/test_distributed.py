@@ -272,7 +272,7 @@ def _worker(rank, world, port_, scale, source, cap, results):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scale,source,cap", [(10, 0, 10_000), (11, 5, 10_000), (10, 0, 2)])
+@pytest.mark.parametrize("scale,source,cap", [(10, 0, 10_000), (11, 5, 10_000), (10, 0, 2), (10, 0, 0)])
 def test_partitioned_bfs_world2_matches_oracle(scale, source, cap):
     ctx = mp.get_context("spawn")
     manager = ctx.Manager()
