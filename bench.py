@@ -255,12 +255,14 @@ def masked_spmv(gb, A, ctx, peak, peak_src, reps=10, density=0.5, graph="rmat"):
             "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
             "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4),
             "call_ms": round(call_ms, 4),
-            "gather_ceiling": {
+            "gather_replay": {
                 "what": "gb_gather_replay_rate: stream A's column indices and gather x[col] "
-                        "for every stored entry, nothing else (measured in this run)",
-                "ceiling_Ggather_s": round(rate.value / 1e9, 1),
+                        "for every stored entry in one pass, nothing else (measured in this "
+                        "run) -- the rate the random 8 B gathers allow a one-pass pull; a "
+                        "column-striped pull (regular graphs) can exceed it",
+                "replay_Ggather_s": round(rate.value / 1e9, 1),
                 "achieved_Ggather_s": round(e_read / (t_ms * 1e-3) / 1e9, 1),
-                "frac": round(e_read / (t_ms * 1e-3) / rate.value, 4)},
+                "ratio": round(e_read / (t_ms * 1e-3) / rate.value, 4)},
             "allowed_rows": R,
             "entries_read": int(e_read), "multiplies": int(d.counters.semiring_multiplies),
             "max_rel_err_vs_torch": rel, "tolerance": 1e-12, "parity": rel <= 1e-12}
@@ -525,28 +527,43 @@ def run_ours(args):
         flops = int(deg[front].sum())
         edges = int(expanded[j]) if len(expanded) == len(push_times) else flops
         k_next = int(counts[lvl + 2]) if lvl + 2 < counts.size else 0
-        bytes_alg = push_level_bytes(n, k, edges, k_next)
+        # SURVEY §8(d)'s push rule: the level's multiplies (flops = sum of the
+        # frontier's degrees, the reference's semiring_multiplies) at 4 B each
+        bytes_alg = push_level_bytes(n, k, flops, k_next)
         achieved = bytes_alg / (t_ms * 1e-3) / 1e9
+        # the conservative variant: only the edges the kernel reads (the
+        # degree-ordered prefix cut skips the neighbours below the dense
+        # visited prefix)
+        bytes_read = push_level_bytes(n, k, edges, k_next)
+        read_gbs = bytes_read / (t_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": "bfs_expand_warp (push SpMSpV, level %d)" % (lvl + 1),
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "traffic": committed_traffic("bfs_expand_warp"),
                 "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4),
                 "frontier": int(k), "flops": flops, "edges_expanded": edges,
-                "bytes_rule": "K*(4+2*8) + edges_expanded*4 + n/8 (visited) + n/8 (new bits) "
-                              "+ K_next*(4+8); edges below the dense visited prefix are not read",
+                "bytes_rule": "SURVEY §8(d) push: K*(4+2*8) + flops*4 + n/8 (mask) + n/8 "
+                              "(out bitmap) + K_next*(4+8), flops = sum of the frontier's "
+                              "degrees",
+                "conservative": {
+                    "what": "the same rule over the edges actually read (edges below the dense "
+                            "visited prefix are skipped, never loaded)",
+                    "bytes": int(bytes_read), "achieved": round(read_gbs, 1),
+                    "frac": round(read_gbs / peak, 4)},
                 "level_ms": [(kind, a, round(t, 4)) for (kind, a, t) in prof]}
         # the push is bound by scattered 4 B probes of the visited bitmap, not
         # by HBM: report it against the random-probe rate of this GPU too
         rate = ctypes.c_double(0.0)
         ctx.call("gb_probe_rate", (n + 31) // 32, 1 << 30, ctypes.byref(rate))
         probes_s = edges / (t_ms * 1e-3)
-        roof["probe_ceiling"] = {
+        roof["probe_rate"] = {
             "what": "uniformly random 4 B ld.global.ca probes of an n-bit bitmap on all SMs "
-                    "(gb_probe_rate, measured in this run); the push does one probe per edge",
-            "ceiling_Gprobe_s": round(rate.value / 1e9, 1),
+                    "(gb_probe_rate, measured in this run) beside the push's probes per second "
+                    "(one per edge read); the push beats it because the degree-ordered layout "
+                    "concentrates its probes on an L1-resident prefix",
+            "uniform_random_Gprobe_s": round(rate.value / 1e9, 1),
             "achieved_Gprobe_s": round(probes_s / 1e9, 1),
-            "frac": round(probes_s / rate.value, 3)}
+            "ratio": round(probes_s / rate.value, 3)}
 
     mspmv = masked_spmv(gb, A, ctx, peak, peak_src) if world == 1 and not args.no_spmv else None
 

@@ -32,10 +32,13 @@ __global__ void bfs_parents_kernel(int64_t n, const int64_t* __restrict__ off,
                                    const int64_t* __restrict__ levels, int64_t source,
                                    int64_t* __restrict__ parents) {
   const int lane = threadIdx.x & 31;
+  const int grp = lane >> 3, gl = lane & 7;  // four 8-lane groups per warp
+  const unsigned gmask = 0xffu << (8 * grp);
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // 32 vertices per warp step: lanes test their vertex, then the warp walks
-  // each reached one
+  // 32 vertices per warp step: lanes test their vertex, then each 8-lane
+  // group walks one reached vertex's row 8 entries at a time (a parent is
+  // usually among the first few in-neighbours: the lowest ids are the hubs)
   for (int64_t base = w0 * 32; base < n; base += nw * 32) {
     const int64_t v = base + lane;
     const int64_t lv = v < n ? levels[v] : 0;
@@ -43,20 +46,28 @@ __global__ void bfs_parents_kernel(int64_t n, const int64_t* __restrict__ off,
     if (v == source) parents[v] = source;
     uint32_t todo = __ballot_sync(GB_FULL, v < n && lv > 1 && v != source);
     while (todo) {
-      const int j = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int64_t vv = base + j;
-      const int64_t want = __shfl_sync(GB_FULL, lv, j) - 1;
-      const int64_t lo = off[vv], hi = off[vv + 1];
-      int64_t found = -1;
-      for (int64_t p0 = lo; p0 < hi && found < 0; p0 += 32) {
-        const int64_t p = p0 + lane;
-        const int32_t u = p < hi ? idx[p] : -1;
-        const bool hit = u >= 0 && levels[u] == want;
-        const uint32_t b = __ballot_sync(GB_FULL, hit);
-        if (b) found = __shfl_sync(GB_FULL, u, __ffs(b) - 1);  // rows ascend: min id
+      // group g takes the g-th remaining vertex (if any)
+      uint32_t t = todo;
+      for (int g = 0; g < grp && t; ++g) t &= t - 1;
+      const int j = t ? __ffs(t) - 1 : -1;
+      for (int g = 0; g < 4 && todo; ++g) todo &= todo - 1;
+      const int64_t want = __shfl_sync(GB_FULL, lv, j < 0 ? 0 : j) - 1;
+      if (j >= 0) {
+        const int64_t vv = base + j;
+        const int64_t lo = off[vv], hi = off[vv + 1];
+        int64_t found = -1;
+        for (int64_t p0 = lo; p0 < hi; p0 += 8) {
+          const int64_t p = p0 + gl;
+          const int32_t u = p < hi ? idx[p] : -1;
+          const bool hit = u >= 0 && levels[u] == want;
+          const uint32_t b = __ballot_sync(gmask, hit) & gmask;
+          if (b) {
+            found = __shfl_sync(gmask, u, __ffs(b) - 1);  // rows ascend: the min id
+            break;
+          }
+        }
+        if (gl == 0) parents[vv] = found;  // -1 only for an inconsistent level vector
       }
-      if (lane == 0) parents[vv] = found;  // -1 only for an inconsistent level vector
     }
   }
 }
