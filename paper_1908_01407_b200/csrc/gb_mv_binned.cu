@@ -124,7 +124,7 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
         }
       }
       acc = warp_fold<T>(add_op, acc);
-      cnt = (int)warp_sum_ll(cnt);
+      cnt = (int)__reduce_add_sync(GB_FULL, (unsigned)cnt);
       if (lane == 0) {
         c_reads += (unsigned long long)(end - beg);
         if (cnt > 0) {
@@ -173,10 +173,8 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
         for (int k = 0; k < 8; ++k) fold_one_v(acc, cnt, x[k], base + 16 * k + hl);
       }
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        acc = op_fold<T>(add_op, acc, __shfl_xor_sync(GB_FULL, acc, o));
-        cnt += __shfl_xor_sync(GB_FULL, cnt, o);
-      }
+      for (int o = 8; o > 0; o >>= 1) acc = op_fold<T>(add_op, acc, __shfl_xor_sync(GB_FULL, acc, o));
+      cnt = (int)__reduce_add_sync(0xffffu << (16 * half), (unsigned)cnt);
       if (hl == 0 && h > l) {
         c_reads += (unsigned long long)(h - l);
         if (cnt > 0) {
@@ -229,22 +227,15 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
   }
 
   if (counters) {
-    __shared__ unsigned long long s_cnt[3];
-    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
-    __syncthreads();
+    // warp-level totals straight to global: no block barrier, so a warp
+    // that finishes its stride leaves at once
     const long long r_ = warp_sum_ll((long long)(s_reads + c_reads));
     const long long m_ = warp_sum_ll((long long)(s_muls + c_muls));
     const long long w_ = warp_sum_ll((long long)(s_rows + c_rows));
     if (lane == 0) {
-      atomicAdd(&s_cnt[0], (unsigned long long)r_);
-      atomicAdd(&s_cnt[1], (unsigned long long)m_);
-      atomicAdd(&s_cnt[2], (unsigned long long)w_);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      atomicAdd(counters + 0, s_cnt[0]);
-      atomicAdd(counters + 1, s_cnt[1]);
-      atomicAdd(counters + 2, s_cnt[1] - s_cnt[2]);  // long rows: mv_pull_finish
+      if (r_) atomicAdd(counters + 0, (unsigned long long)r_);
+      if (m_) atomicAdd(counters + 1, (unsigned long long)m_);
+      if (m_ - w_) atomicAdd(counters + 2, (unsigned long long)(m_ - w_));  // long rows: mv_pull_finish
     }
   }
 }
