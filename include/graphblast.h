@@ -609,10 +609,12 @@ gb_status gb_bfs_ordered(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
  * of 1 + 3*max_iters int64 receiving [iters, (dir, frontier, estimate) x
  * iters]; log_host: pinned host buffer of 1 + 3*21 int64 that receives the
  * first 1 + 3*min(iters, 21) entries in stream order -- synchronise the
- * stream before reading it, and read entries past 21 decisions from log_dev.  launch_info[5] = launches of the
- * fixed part, of one push level, of one pull level (0 on the synchronous
- * path), the levels per device-loop pass u, and of one push level whose
- * frontier is a single vertex (it skips the degree scan); pass fixed +
+ * stream before reading it, and read entries past 21 decisions from log_dev.
+ * launch_info[6] = launches of the fixed part, of one push level, of one
+ * pull level (0 on the synchronous path), the levels per device-loop pass u,
+ * of one push level whose frontier is a single vertex (it skips the degree
+ * scan) and of one tiny push level (2..4096 entries: one expansion kernel
+ * that appends its discoveries, no scan or bitmap finalize); pass fixed +
  * per-level launches + (u - iters % u) % u (no-op steps of the last pass) to
  * gb_count_launches once the log is read.  Replaces
  * the synchronous return of algorithms.py:48-77 + the direction_log appends

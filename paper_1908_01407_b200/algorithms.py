@@ -70,6 +70,7 @@ def _require_symmetric(A):
 _ASYNC_CAP = 65000   # loop caps the asynchronous entry accepts (16-bit device levels)
 # GB_BFS_ASYNC=0: every bfs() call synchronises and fills the log eagerly
 _ASYNC_BFS = os.environ.get("GB_BFS_ASYNC", "1") != "0"
+_TINY_K = 4096   # gb_bfs.cu kTinyK: push levels up to this many entries take the one-kernel path
 _LOG_PREFIX = 21     # decisions gb_bfs_ordered_async copies to the pinned log
 
 
@@ -108,14 +109,18 @@ class _PendingBfs:
         info = self.info
         if info[0]:
             push = dirs == _lib.DIR_PUSH
-            npush1 = int(np.count_nonzero(push & (raw[2:2 + 3 * iters:3] == 1)))
-            npush = int(np.count_nonzero(push)) - npush1
-            # single-entry push levels skip the degree scan; + the no-op
-            # g_steps of the device loop's last pass
+            kk = raw[2:2 + 3 * iters:3]
+            npush1 = int(np.count_nonzero(push & (kk == 1)))
+            ntiny = int(np.count_nonzero(push & (kk > 1) & (kk <= _TINY_K)))
+            npush = int(np.count_nonzero(push)) - npush1 - ntiny
+            # single-entry push levels skip the degree scan, tiny ones take the
+            # one-kernel path; + the no-op g_steps of the device loop's last pass
             u = int(info[3])
             self.ctx.lib.gb_count_launches(self.ctx.ptr, int(info[0] + npush * info[1] +
                                                             npush1 * info[4] +
-                                                            (iters - npush - npush1) * info[2] +
+                                                            ntiny * info[5] +
+                                                            (iters - npush - npush1 - ntiny) *
+                                                            info[2] +
                                                             (u - iters % u) % u))
         return [DirectionDecision("pull" if dirs[i] == _lib.DIR_PULL else "push",
                                   int(raw[2 + 3 * i]), int(raw[3 + 3 * i]), self.total, self.thr)
@@ -252,7 +257,7 @@ def _bfs_fused(A, source, desc):
         push_o, pull_o, rank = trav
         (push, _k1), (pull, _k2) = push_o.csr_struct(), pull_o.csr_struct()
         ctx = _lib.context()
-        info = np.zeros(5, np.int64)
+        info = np.zeros(6, np.int64)
         pending = _PendingBfs(ctx, A, desc.switch_ratio, info)
         log_pin, log_dev = _log_ring(ctx, levels.device).take(pending, cap)
         ctx.call("gb_bfs_ordered_async", C.byref(push), C.byref(pull), _lib.ptr(pull_o.nonempty()),

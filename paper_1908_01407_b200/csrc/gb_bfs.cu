@@ -772,6 +772,8 @@ struct BfsState {
   const int32_t* F1;
   int64_t *rowstart1, *S1;
   int64_t k1;
+  int64_t tiny;         // tiny push levels enabled (GB_BFS_TINY=0 disables)
+  int32_t* Ft;          // tiny levels: the new frontier before it is committed to F
   int64_t it, K, depth, dnext, unstamp;  // loop state
   int64_t stopped;                        // the loop ended inside a body pass
   int64_t xcur;                 // dense visited prefix at the level start (ordered graphs)
@@ -1092,7 +1094,11 @@ __global__ void g_zero_levels(int64_t n, const BfsState* __restrict__ st) {
 __device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned long long* c,
                             cudaGraphConditionalHandle h_push);
 // SWITCH values of a level node: its push body, its pull body, or nothing
-constexpr unsigned kSwPush = 0, kSwPull = 1, kSwPush1 = 2, kSwSkip = 3;
+constexpr unsigned kSwPush = 0, kSwPull = 1, kSwPush1 = 2, kSwTiny = 3, kSwSkip = 4;
+// a push level with at most this many frontier entries takes the tiny path:
+// one expansion kernel that appends each discovered vertex itself (no degree
+// scan, no full-bitmap finalize) -- the s24 tail levels (3,034 and 9 entries)
+constexpr int64_t kTinyK = 4096;
 
 __global__ void g_start(BfsState* st, const int32_t* rank, uint32_t* vbm, uint32_t* vprev,
                         uint32_t* fbm0, int32_t* F, cudaGraphConditionalHandle h_loop,
@@ -1137,6 +1143,7 @@ __device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned l
   st->xnext = ~0ull;
   *c = 0;
   unsigned sw = dir == GB_DIR_PUSH ? kSwPush : kSwPull;
+  if (dir == GB_DIR_PUSH && K > 1 && K <= kTinyK && st->tiny) sw = kSwTiny;
   if (dir == GB_DIR_PUSH && K == 1 && st->k1) {
     // one frontier entry: its whole list (no prefix cut) as the expansion space
     const int64_t v = st->F1[0];
@@ -1195,6 +1202,60 @@ __global__ void g_unstamp(const BfsState* __restrict__ st, const int32_t* __rest
   }
 }
 
+static bool tiny_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GB_BFS_TINY");
+    v = !(e && atoi(e) == 0);
+  }
+  return v != 0;
+}
+
+// ---- tiny push levels (K <= kTinyK): a block per frontier entry expands its
+// list; the thread that sets a vertex's visited bit owns the discovery and
+// stamps its level, frontier bit and visited-at-level-start bit and appends
+// it to Ft.  bfs_tiny_commit then moves Ft to F.  fbm_next was cleared
+// before; the dense visited prefix is kept as it was (still valid).
+template <class LT>
+__global__ void __launch_bounds__(256)
+bfs_tiny_expand(BfsState* st, const int32_t* __restrict__ F, const int64_t* __restrict__ off,
+                const int32_t* __restrict__ idx, EdgeOn on, uint32_t* vbm, uint32_t* vprev,
+                uint32_t* fbm_next, DevP<LT> levels_d, unsigned long long* count) {
+  const int64_t K = st->K;
+  const int64_t depth = st->dnext;
+  LT* levels = levels_d.get();
+  int32_t* Ft = st->Ft;
+  for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
+    const int32_t u = F[k];
+    const int64_t lo = off[u], hi = off[u + 1];
+    for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+      if (!on(p)) continue;
+      const int32_t v = idx[p];
+      const uint32_t bit = 1u << (v & 31);
+      if (ld_probe(vbm + (v >> 5)) & bit) continue;
+      if (atomicOr(vbm + (v >> 5), bit) & bit) continue;
+      atomicOr(vprev + (v >> 5), bit);
+      atomicOr(fbm_next + (v >> 5), bit);
+      levels[v] = level_of<LT>(depth);
+      Ft[atomicAdd(count, 1ull)] = v;
+    }
+  }
+}
+
+__global__ void bfs_tiny_commit(BfsState* st, int32_t* __restrict__ F,
+                                const unsigned long long* __restrict__ count,
+                                unsigned long long* __restrict__ count_clear) {
+  const int64_t c = (int64_t)*count;
+  const int32_t* Ft = st->Ft;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c;
+       i += (int64_t)gridDim.x * blockDim.x)
+    F[i] = Ft[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *count_clear = 0;
+    st->xnext = (unsigned long long)st->xcur;  // the prefix is unchanged (still a lower bound)
+  }
+}
+
 struct BfsGraph {
   // key: the matrix orientations the graph was built for
   gb_csr push{}, pull{};
@@ -1211,12 +1272,14 @@ struct BfsGraph {
   uint16_t* lv = nullptr;  // relabelled graph: 16-bit levels by new id
   const int32_t* samp = nullptr;  // relabelled graph: column samples (OrderedAux)
   int64_t* queue = nullptr;  // stamp queue of the long lists (4 x int64 per list)
+  int32_t* Ft = nullptr;     // tiny levels' new frontier
   int64_t reach = 0;         // relabelled graph: vertices >= reach have no in-edges
   BfsState* st = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches_push = 0, launches_pull = 0, launches_fixed = 0;
   int unroll = 2;  // levels per WHILE pass (even)
   int launches_push1 = 0;  // a single-entry push level (expansion + finalize)
+  int launches_tiny = 0;   // a tiny push level (memset, expansion, commit)
   int64_t k1 = 0;          // single-entry push levels skip the degree scan
 };
 
@@ -1266,6 +1329,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
                                     : smem_push_setup<false>(ctx, W, &smem);
   G->launches_push = 4 + (push_dead ? 0 : 1);
   G->launches_push1 = 1 + (push_dead ? 0 : 1);
+  G->launches_tiny = 2 + (push_dead ? 0 : 1);
   G->k1 = !use_smem && !(getenv("GB_BFS_K1") && atoi(getenv("GB_BFS_K1")) == 0);
   const int grid_stamp = grid_for(ctx, (int64_t)1 << 40, 256, 8);
   G->launches_pull = pull_dead ? 3 : 1;
@@ -1312,6 +1376,21 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
                                                    G->cnt + (h ^ 1), nullptr, nullptr);
     return cudaGetLastError();
   };
+  auto tiny_body = [&](int h, cudaStream_t s) -> cudaError_t {
+    GB_GTRY(cudaMemsetAsync(G->fbm[h ^ 1], 0, sizeof(uint32_t) * W, s));
+    if (!push_dead) {
+      if (ordered)
+        bfs_tiny_expand<uint16_t><<<grid_for(ctx, kTinyK, 1, 4), 256, 0, s>>>(
+            st, G->F, push.offsets, push.indices, push_on, G->vbm, G->vprev, G->fbm[h ^ 1],
+            pptr(&st->lv16), G->cnt + h);
+      else
+        bfs_tiny_expand<int64_t><<<grid_for(ctx, kTinyK, 1, 4), 256, 0, s>>>(
+            st, G->F, push.offsets, push.indices, push_on, G->vbm, G->vprev, G->fbm[h ^ 1],
+            pptr(&st->levels), G->cnt + h);
+    }
+    bfs_tiny_commit<<<4, 256, 0, s>>>(st, G->F, G->cnt + h, G->cnt + (h ^ 1));
+    return cudaGetLastError();
+  };
   auto pull_body = [&](int h, cudaStream_t s) -> cudaError_t {
     if (pull_dead) {
       GB_GTRY(cudaMemsetAsync(G->fbm[h ^ 1], 0, sizeof(uint32_t) * W, s));
@@ -1338,7 +1417,7 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
                        cudaGraphConditionalHandle h_push_next) -> cudaError_t {
     // h_push was set by the previous node that decided this iteration
     // (g_start or the previous g_step); the handles live in the top graph
-    cudaGraph_t br[3];
+    cudaGraph_t br[4];
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     {
@@ -1349,17 +1428,16 @@ static cudaError_t bfs_graph_build(gb_ctx* ctx, BfsGraph* G, const cudaStream_t*
       p.type = cudaGraphNodeTypeConditional;
       p.conditional.handle = h_push;
       p.conditional.type = cudaGraphCondTypeSwitch;
-      p.conditional.size = 3;  // kSwPush, kSwPull, kSwPush1; kSwSkip runs none
+      p.conditional.size = 4;  // kSwPush, kSwPull, kSwPush1, kSwTiny; kSwSkip runs none
       cudaGraphNode_t node;
       GB_GTRY(cudaGraphAddNode(&node, g, deps, nd, &p));
-      br[0] = p.conditional.phGraph_out[0];
-      br[1] = p.conditional.phGraph_out[1];
-      br[2] = p.conditional.phGraph_out[2];
+      for (int b = 0; b < 4; ++b) br[b] = p.conditional.phGraph_out[b];
       GB_GTRY(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
     }
     GB_GTRY(capture_into(br[0], s_inner, [&] { return push_body(h, s_inner, false); }));
     GB_GTRY(capture_into(br[1], s_inner, [&] { return pull_body(h, s_inner); }));
     GB_GTRY(capture_into(br[2], s_inner, [&] { return push_body(h, s_inner, true); }));
+    GB_GTRY(capture_into(br[3], s_inner, [&] { return tiny_body(h, s_inner); }));
     g_step<<<1, 1, 0, s>>>(st, G->cnt + h, n, h_a, h_b, push.nnz, push.nrows, G->cnt + (h ^ 1),
                            h_push_next);
     return cudaGetLastError();
@@ -1464,6 +1542,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     const size_t o_part = take(8 * (kGScanBlocks + 1)), o_st = take(sizeof(BfsState));
     const size_t o_q = take(32 * (size_t)stamp_queue_cap(push->nnz));
     const size_t o_lv = rank ? take(2 * (size_t)n) : 0;
+    const size_t o_Ft = take(4 * (size_t)n);
     if (cudaMalloc(&G->mem, off) != cudaSuccess) {
       cudaGetLastError();
       delete G;
@@ -1484,6 +1563,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     G->queue = (int64_t*)(m + o_q);
     G->st = (BfsState*)(m + o_st);
     G->lv = rank ? (uint16_t*)(m + o_lv) : nullptr;
+    G->Ft = (int32_t*)(m + o_Ft);
     G->samp = aux ? aux->samp : nullptr;
     G->reach = aux ? aux->reach : n;
     cudaStream_t cs[4];
@@ -1518,6 +1598,8 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   h.rowstart1 = G->rowstart;
   h.S1 = G->S;
   h.k1 = G->k1;
+  h.tiny = tiny_enabled() ? 1 : 0;
+  h.Ft = G->Ft;
   h.lv16 = rank ? G->lv : nullptr;
   h.out = levels;
   h.log = log;
@@ -1537,6 +1619,7 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
     launch_info[1] = 1 + G->launches_push;  // + g_step
     launch_info[2] = 1 + G->launches_pull;
     launch_info[4] = G->k1 ? 1 + G->launches_push1 : launch_info[1];
+    launch_info[5] = h.tiny ? 1 + G->launches_tiny : launch_info[1];
     return GB_OK;
   }
   // one readback: iteration count and up to 21 decisions
@@ -1564,7 +1647,8 @@ static gb_status bfs_graph_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   int64_t nl = G->launches_fixed;
   for (int64_t i = 0; i < iters; ++i)
     nl += 1 + (log_dir[i] != GB_DIR_PUSH ? G->launches_pull
-               : (G->k1 && log_nvals[i] == 1) ? G->launches_push1 : G->launches_push);
+               : (G->k1 && log_nvals[i] == 1) ? G->launches_push1
+               : (h.tiny && log_nvals[i] <= kTinyK) ? G->launches_tiny : G->launches_push);
   nl += (G->unroll - iters % G->unroll) % G->unroll;  // no-op g_steps of the last pass
   count_launch(ctx, (int)nl);
   return GB_OK;
@@ -1880,6 +1964,7 @@ gb_status gb_bfs_ordered_async(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   launch_info[2] = 0;
   launch_info[3] = 2;
   launch_info[4] = 0;
+  launch_info[5] = 0;
   return GB_OK;
 }
 
