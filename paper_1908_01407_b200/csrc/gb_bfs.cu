@@ -1143,6 +1143,8 @@ __device__ void decide_body(BfsState* st, int64_t nnz, int64_t nrows, unsigned l
   st->xnext = ~0ull;
   *c = 0;
   unsigned sw = dir == GB_DIR_PUSH ? kSwPush : kSwPull;
+  // (the single-entry level keeps push1 + finalize: finalize finds the dense
+  // visited prefix the next push cuts at -- measured 0.79 vs 1.06 ms at s24)
   if (dir == GB_DIR_PUSH && K > 1 && K <= kTinyK && st->tiny) sw = kSwTiny;
   if (dir == GB_DIR_PUSH && K == 1 && st->k1) {
     // one frontier entry: its whole list (no prefix cut) as the expansion space
@@ -1225,19 +1227,37 @@ bfs_tiny_expand(BfsState* st, const int32_t* __restrict__ F, const int64_t* __re
   const int64_t depth = st->dnext;
   LT* levels = levels_d.get();
   int32_t* Ft = st->Ft;
-  for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
+  // fewer entries than blocks (the source level: K = 1): several blocks share
+  // an entry's list
+  const int64_t bpe = K < gridDim.x ? gridDim.x / K : 1;
+  for (int64_t b = blockIdx.x; b < K * bpe; b += gridDim.x) {
+    const int64_t k = b / bpe, part = b % bpe;
     const int32_t u = F[k];
     const int64_t lo = off[u], hi = off[u + 1];
-    for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-      if (!on(p)) continue;
-      const int32_t v = idx[p];
-      const uint32_t bit = 1u << (v & 31);
-      if (ld_probe(vbm + (v >> 5)) & bit) continue;
-      if (atomicOr(vbm + (v >> 5), bit) & bit) continue;
-      atomicOr(vprev + (v >> 5), bit);
-      atomicOr(fbm_next + (v >> 5), bit);
-      levels[v] = level_of<LT>(depth);
-      Ft[atomicAdd(count, 1ull)] = v;
+    for (int64_t p0 = lo + part * blockDim.x; p0 < hi; p0 += bpe * blockDim.x) {
+      const int64_t p = p0 + threadIdx.x;
+      bool disc = false;
+      int32_t v = 0;
+      if (p < hi && on(p)) {
+        v = idx[p];
+        const uint32_t bit = 1u << (v & 31);
+        if (!(ld_probe(vbm + (v >> 5)) & bit) && !(atomicOr(vbm + (v >> 5), bit) & bit)) {
+          disc = true;  // this thread set the bit: it owns the discovery
+          atomicOr(vprev + (v >> 5), bit);
+          atomicOr(fbm_next + (v >> 5), bit);
+          levels[v] = level_of<LT>(depth);
+        }
+      }
+      const uint32_t bal = __ballot_sync(__activemask(), disc);
+      if (bal) {
+        // one reservation per warp for its discoveries
+        unsigned long long at = 0;
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(bal) - 1;
+        if (lane == leader) at = atomicAdd(count, (unsigned long long)__popc(bal));
+        at = __shfl_sync(__activemask(), at, leader);
+        if (disc) Ft[at + __popc(bal & ((1u << lane) - 1u))] = v;
+      }
     }
   }
 }
