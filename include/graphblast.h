@@ -625,6 +625,11 @@ gb_status gb_bfs_ordered_async(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
                                int64_t* levels, int64_t* log_dev, int64_t* log_host,
                                int64_t* launch_info);
 
+/* Largest graph (vertices) a default-layout BFS runs as ONE cooperative
+ * kernel (gb_bfs_coop.cu) instead of the device-graph loop; n >= 0 sets it
+ * (0 = never), n < 0 only reads.  Returns the previous value. */
+int64_t gb_bfs_coop_max_n(int64_t n);
+
 /* Adds n to the context's launch counter (asynchronous entries). */
 void gb_count_launches(gb_ctx* ctx, int64_t n);
 

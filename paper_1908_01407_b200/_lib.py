@@ -123,6 +123,7 @@ SIGNATURES = {
     "gb_bfs_validate": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, vp, vp, vp]),
     "gb_bfs_engine": (i32, [i32]),
     "gb_loop_engine": (i32, [i32]),
+    "gb_bfs_coop_max_n": (i64, [i64]),
     "gb_degree_order": (i32, [vp, i64, vp, vp, vp]),
     "gb_csr_relabel_t": (i32, [vp, C.POINTER(gb_csr), vp, vp, vp, vp, vp]),
     "gb_mxv_pull": (i32, [vp, i32, i32, C.POINTER(gb_csr), C.POINTER(gb_row_plan), vp, vp, i32,

@@ -1882,6 +1882,33 @@ static gb_status bfs_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
                          int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out) {
   const int64_t n = push->nrows;
   if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
+  if (rank && pull && bfs_engine_current() == kEngineGraph && !prof_enabled(ctx) && max_iters >= 1 &&
+      n <= bfs_coop_max_n()) {
+    // a small relabelled graph: the whole traversal in one cooperative kernel
+    Arena ar(ctx);
+    int64_t* log = ar.alloc<int64_t>(1 + 3 * max_iters);
+    GB_ARENA_CHECK(ctx, ar);
+    const gb_status st = bfs_coop_run(ctx, push, pull, pull_nonempty, rank, source, max_iters,
+                                      ratio, policy, levels_out, log);
+    if (st == GB_OK) {
+      int64_t iters = 0;
+      GB_TRY(read_i64(ctx, log, &iters));
+      std::vector<int64_t> raw(3 * (iters > 0 ? iters : 1));
+      if (iters > 0) {
+        GB_CUDA(ctx, cudaMemcpyAsync(raw.data(), log + 1, sizeof(int64_t) * 3 * iters,
+                                     cudaMemcpyDeviceToHost, stream_of(ctx)));
+        GB_CUDA(ctx, cudaStreamSynchronize(stream_of(ctx)));
+      }
+      for (int64_t i = 0; i < iters; ++i) {
+        log_dir[i] = (int32_t)raw[3 * i];
+        log_nvals[i] = raw[3 * i + 1];
+        log_est[i] = raw[3 * i + 2];
+      }
+      *iters_out = iters;
+      return GB_OK;
+    }
+    if (st != GB_ERR_UNSUPPORTED) return st;
+  }
   const OrderedAux* aux = nullptr;
   if (rank) GB_TRY(ordered_aux(ctx, push, pull, &aux));
   // Device-driven loop (one graph launch) unless profiling per kernel, the
@@ -1949,6 +1976,21 @@ gb_status gb_bfs_ordered_async(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
   if (source < 0 || source >= n)
     return set_error(ctx, GB_ERR_INDEX, "source %lld out of range", (long long)source);
   if (max_iters < 1) return set_error(ctx, GB_ERR_ARG, "max_iters must be >= 1");
+  // a small graph: the whole traversal in one cooperative kernel
+  if (pull && bfs_engine_current() == kEngineGraph && !prof_enabled(ctx) && n <= bfs_coop_max_n()) {
+    const gb_status st = bfs_coop_run(ctx, push, pull, pull_nonempty, rank, source, max_iters,
+                                      ratio, policy, levels, log_dev);
+    if (st == GB_OK) {
+      const int64_t first = max_iters < kLogPrefix ? max_iters : kLogPrefix;
+      GB_CUDA(ctx, cudaMemcpyAsync(log_host, log_dev, sizeof(int64_t) * (1 + 3 * first),
+                                   cudaMemcpyDeviceToHost, stream_of(ctx)));
+      // its one launch is counted already: nothing to book when the log is read
+      for (int i = 0; i < 6; ++i) launch_info[i] = 0;
+      launch_info[3] = 1;
+      return GB_OK;
+    }
+    if (st != GB_ERR_UNSUPPORTED) return st;
+  }
   // the graph engine, with a loop cap its 16-bit levels cannot exceed
   if (pull && bfs_engine_current() == kEngineGraph && !prof_enabled(ctx) &&
       max_iters <= kGraphMaxCap && max_iters < kNarrowLevelIters) {

@@ -366,7 +366,7 @@ bool prof_enabled(gb_ctx* ctx);
 // Per-context cached objects (e.g. instantiated CUDA graphs) that live until
 // the context is destroyed: slot i holds a pointer and its destructor.
 enum { SLOT_BFS_GRAPH = 0, SLOT_BFS_AUX = 1, SLOT_PR_GRAPH = 2, SLOT_CC_GRAPH = 3,
-       SLOT_SSSP_GRAPH = 4, kCtxSlots = 8 };
+       SLOT_SSSP_GRAPH = 4, SLOT_BFS_COOP = 5, kCtxSlots = 8 };
 void** ctx_slot(gb_ctx* ctx, int i, void (*destroy)(void*));
 // pinned host scratch for small device->host reads (>= 64 int64 slots)
 int64_t* pinned_slots(gb_ctx* ctx);
@@ -383,6 +383,14 @@ inline int resident_grid(gb_ctx* ctx, Kernel kernel, int block, size_t smem = 0)
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// gb_bfs_coop.cu: small-graph BFS in one cooperative kernel (degree-ordered
+// layout; levels by original id, raw log [iters, (dir, K, est) x iters])
+int64_t bfs_coop_max_n();
+gb_status bfs_coop_run(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
+                       const uint32_t* nonempty, const int32_t* rank, int64_t source,
+                       int64_t cap, double ratio, int32_t policy, int64_t* levels,
+                       int64_t* log_dev);
 
 // gb_mv.cu: out[0..n) = v; counters[2] -= rows folded across tiles (hasmul bits)
 template <class T>

@@ -459,3 +459,24 @@ def test_bfs_async_launch_accounting_matches_sync(gb, src, monkeypatch):
     gb.bfs(A, src, desc=d2).values
     assert len(d2.direction_log) == len(d1.direction_log)
     assert ctx.launches() - l0 == sync_n > 0
+
+
+@pytest.mark.parametrize("scale,src,cap", [(10, 0, 10_000), (13, 3, 10_000), (12, 0, 2),
+                                           (12, 0, 1)])
+def test_cooperative_small_graph_bfs_equals_graph_loop(gb, scale, src, cap):
+    """The one-kernel cooperative BFS (gb_bfs_coop.cu, the default for small
+    graphs) against the device-graph loop: levels, trace and loop caps."""
+    lib = gb._lib.load()
+    A = gb.io.rmat_matrix(scale)
+    out = {}
+    for name, lim in (("coop", 1 << 30), ("graph", 0)):
+        prev = lib.gb_bfs_coop_max_n(lim)
+        try:
+            d = gb.Descriptor(max_niter=cap)
+            out[name] = (gb.bfs(A, src, desc=d).values,
+                         [(x.chosen, x.frontier_nvals, x.estimated_frontier_edges)
+                          for x in d.direction_log])
+        finally:
+            lib.gb_bfs_coop_max_n(prev)
+    assert np.array_equal(out["coop"][0], out["graph"][0])
+    assert out["coop"][1] == out["graph"][1]
