@@ -205,14 +205,38 @@ tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict_
       for (int64_t q = lane; q < len; q += 32) s_row[wid][q] = uidx[lo + q];
       __syncwarp();
     }
-    for (int64_t a = 0; a < len; ++a) {
-      const int32_t j = row[a];
-      const int64_t jlo = uoff[j], jhi = uoff[j + 1];
+    const int ilen = (int)len;
+    const int32_t rmax = row[ilen - 1];
+    int64_t mylo = 0, myhi = 0;  // bounds of U(row[a]) for a = (chunk of 32) + lane
+    for (int a = 0; a < ilen; ++a) {
+      if ((a & 31) == 0) {
+        // the next 32 lists' bounds in one round of loads
+        const int aa = a + lane;
+        mylo = myhi = 0;
+        if (aa < ilen) {
+          const int32_t jj = row[aa];
+          mylo = uoff[jj];
+          myhi = uoff[jj + 1];
+        }
+      }
+      const int64_t jlo = __shfl_sync(GB_FULL, mylo, a & 31);
+      const int64_t jhi = __shfl_sync(GB_FULL, myhi, a & 31);
       // elements of U(j) are > j > r; search them in U(r) after position a
+      // (branchless 32-bit lower bound: the kernel is issue-bound)
+      const int32_t* base0 = row + a + 1;
+      const int m = ilen - a - 1;
+      if (m == 0) continue;
       for (int64_t q = jlo + lane; q < jhi; q += 32) {
         const int32_t key = uidx[q];
-        const int64_t p = lb32(row + a + 1, len - a - 1, key);
-        c += (p < len - a - 1 && row[a + 1 + p] == key);
+        if (key > rmax) break;  // sorted lists: no later key of U(j) is in U(r) either
+        const int32_t* b = base0;
+        int l = m;
+        while (l > 1) {
+          const int h = l >> 1;
+          b = b[h - 1] < key ? b + h : b;
+          l -= h;
+        }
+        c += *b == key;
       }
     }
     __syncwarp();
