@@ -22,13 +22,17 @@
 
 namespace gb {
 
+// first position with a[p] >= key (branchless halving: a select per step)
 __device__ __forceinline__ int64_t lb32(const int32_t* a, int64_t n, int32_t key) {
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  if (n <= 0) return 0;
+  const int32_t* b = a;
+  int64_t l = n;
+  while (l > 1) {
+    const int64_t h = l >> 1;
+    b = b[h - 1] < key ? b + h : b;
+    l -= h;
   }
-  return lo;
+  return (b - a) + (*b < key);
 }
 
 // One warp per mask row.  out_flag[e] = 1 when mask entry e produces an
