@@ -630,6 +630,13 @@ gb_status gb_bfs_ordered_async(gb_ctx* ctx, const gb_csr* push, const gb_csr* pu
  * (0 = never), n < 0 only reads.  Returns the previous value. */
 int64_t gb_bfs_coop_max_n(int64_t n);
 
+/* Completion events on a context's stream (host-side waits for asynchronous
+ * calls): create, record on ctx's stream, wait, destroy. */
+gb_status gb_event_create(void** ev);
+gb_status gb_event_record(gb_ctx* ctx, void* ev);
+gb_status gb_event_sync(void* ev);
+gb_status gb_event_destroy(void* ev);
+
 /* Adds n to the context's launch counter (asynchronous entries). */
 void gb_count_launches(gb_ctx* ctx, int64_t n);
 

@@ -84,6 +84,10 @@ SIGNATURES = {
     "gb_last_error": (C.c_char_p, [vp]),
     "gb_scratch_bytes": (i64, [vp]),
     "gb_ctx_trim": (i32, [vp]),
+    "gb_event_create": (i32, [C.POINTER(vp)]),
+    "gb_event_record": (i32, [vp, vp]),
+    "gb_event_sync": (i32, [vp]),
+    "gb_event_destroy": (i32, [vp]),
     "gb_iota": (i32, [vp, i32, i64, vp]),
     "gb_cast": (i32, [vp, i64, i32, vp, i32, vp]),
     "gb_select_flags": (i32, [vp, i64, vp, vp, vp, i32, vp, vp, pi64]),
@@ -277,8 +281,7 @@ class Context:
         self.lib.gb_ctx_trim(self.ptr)
 
     def call(self, name, *args):
-        import torch
-        s = torch.cuda.current_stream(self.device_index).cuda_stream
+        s = _raw_stream(self.device_index)
         if s != self._stream:
             self.lib.gb_ctx_set_stream(self.ptr, vp(s))
             self._stream = s
@@ -288,14 +291,58 @@ class Context:
         return st
 
 
+def _raw_stream(device_index):
+    """cudaStream_t of torch's current stream on the device (the raw getter
+    skips building a Stream object: ~10 us per call on the host)."""
+    import torch
+    get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if get is not None:
+        return get(device_index)
+    return torch.cuda.current_stream(device_index).cuda_stream
+
+
+class DeviceEvent:
+    """A cudaEvent recorded on the context's stream through the library (no
+    torch Stream object per record); sync() waits for it."""
+
+    __slots__ = ("lib", "ev")
+
+    def __init__(self, ctx):
+        self.lib = ctx.lib
+        self.ev = vp()
+        st = self.lib.gb_event_create(C.byref(self.ev))
+        if st != GB_OK:
+            raise RuntimeError("gb_event_create failed")
+
+    def record(self, ctx):
+        ctx.call("gb_event_record", self.ev)
+
+    def sync(self):
+        self.lib.gb_event_sync(self.ev)
+
+    def __del__(self):
+        try:
+            if self.ev:
+                self.lib.gb_event_destroy(self.ev)
+        except Exception:
+            pass
+
+
 _contexts = {}
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
+    global _CUDA_OK
+    if _CUDA_OK:
+        return
     import torch
     if not torch.cuda.is_available():
         raise RuntimeError(
             "paper_1908_01407_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    _CUDA_OK = True
 
 
 def context(device=None) -> Context:

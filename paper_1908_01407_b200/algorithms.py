@@ -92,7 +92,7 @@ class _PendingBfs:
 
     def settle(self):
         if self.raw is None:
-            self.event.synchronize()
+            self.event.sync()
             raw = self.row.numpy().copy()
             iters = int(raw[0])
             if iters > _LOG_PREFIX:
@@ -141,6 +141,7 @@ class _LogRing:
         self.dev = [None] * self.SLOTS
         self.device = device
         self.owner = [None] * self.SLOTS
+        self.events = [None] * self.SLOTS  # completion event per slot (reused)
         self.next = 0
 
     def _settle(self, i):
@@ -157,6 +158,9 @@ class _LogRing:
         if self.dev[i] is None or self.dev[i].numel() < need:
             self.dev[i] = torch.empty(max(need, 1 + 3 * 64), dtype=torch.int64, device=self.device)
         self.owner[i] = weakref.ref(pending)
+        if self.events[i] is None:
+            self.events[i] = _lib.DeviceEvent(pending.ctx)
+        pending.event = self.events[i]
         pending.row = self.pin[i]
         pending.dev = self.dev[i]
         return self.pin[i], self.dev[i]
@@ -264,8 +268,7 @@ def _bfs_fused(A, source, desc):
                  _lib.ptr(rank), int(source), int(iters), float(desc.switch_ratio),
                  _POLICY[desc.direction], _lib.ptr(levels), _lib.ptr(log_dev),
                  C.c_void_p(log_pin.data_ptr()), info.ctypes.data_as(C.c_void_p))
-        pending.event = torch.cuda.Event()
-        pending.event.record()
+        pending.event.record(ctx)
         desc.direction_log._defer(pending)
         return Vector._wrap(n, None, levels, 0, np.int64)
     if trav is not None:

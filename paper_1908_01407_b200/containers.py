@@ -503,7 +503,8 @@ class _Orient:
     """One orientation on the device: rows of A (CSR) or of A^T (CSC)."""
 
     __slots__ = ("nrows", "ncols", "offsets", "indices", "values", "iso", "dt", "_nonempty",
-                 "_plan", "_bins", "_stripes", "_ordered", "_order", "_mv_ordered", "gen", "__weakref__")
+                 "_plan", "_bins", "_stripes", "_ordered", "_order", "_mv_ordered", "_struct", "gen",
+                 "__weakref__")
 
     def __init__(self, nrows, ncols, offsets, indices, values, iso, dt):
         self.nrows, self.ncols = int(nrows), int(ncols)
@@ -514,6 +515,7 @@ class _Orient:
         self._plan = None
         self._bins = None
         self._stripes = None
+        self._struct = None      # cached csr_struct() of the stored dtype (immutable)
         self._ordered = None
         self._order = None       # new -> original id of the traversal layout
         self._mv_ordered = {}    # transpose -> ordered masked-pull view (SparseMatrix.ordered_pull)
@@ -608,6 +610,8 @@ class _Orient:
 
         Keep the second element alive for as long as the struct is used: it
         owns the converted value array the struct points at."""
+        if (as_dtype is None or np.dtype(as_dtype) == self.dt) and self._struct is not None:
+            return self._struct
         s = _lib.gb_csr()
         s.nrows, s.ncols, s.nnz = self.nrows, self.ncols, self.nnz
         s.offsets = self.offsets.data_ptr()
@@ -625,6 +629,8 @@ class _Orient:
             s.values = keep.data_ptr() if self.nnz else 0
         s.dtype = _lib.dtype_code(dt)
         s.gen = self.gen
+        if dt == self.dt:
+            self._struct = (s, keep)
         return s, keep
 
     def values_as(self, dt):

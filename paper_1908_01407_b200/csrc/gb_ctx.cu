@@ -228,3 +228,23 @@ int64_t gb_scratch_bytes(gb_ctx* ctx) {
 }
 
 }  // extern "C"
+
+// Events recorded on a context's stream (the asynchronous bfs's completion
+// marks): no per-record object on the Python side.
+extern "C" gb_status gb_event_create(void** ev) {
+  cudaEvent_t e;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return GB_ERR_CUDA;
+  *ev = (void*)e;
+  return GB_OK;
+}
+extern "C" gb_status gb_event_record(gb_ctx* ctx, void* ev) {
+  GB_CUDA(ctx, cudaEventRecord((cudaEvent_t)ev, ctx->stream));
+  return GB_OK;
+}
+extern "C" gb_status gb_event_sync(void* ev) {
+  return cudaEventSynchronize((cudaEvent_t)ev) == cudaSuccess ? GB_OK : GB_ERR_CUDA;
+}
+extern "C" gb_status gb_event_destroy(void* ev) {
+  cudaEventDestroy((cudaEvent_t)ev);
+  return GB_OK;
+}
