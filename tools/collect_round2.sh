@@ -23,7 +23,7 @@ cap bfs_push "bfs_expand_warp" bfs 24 2
 cap bfs_pull "bfs_pull" bfs 24 1
 cap mxvm "mv_pull_binned" mxvm 24 1
 cap pr "pr_spmv|pr_epilogue" pr 22 2
-cap cc "cc_pull|cc_hook|cc_shortcut" cc 24 3
+cap cc "cc_pull|cc_hook|cc_shortcut" cc 24 5
 cap sssp "sssp_pull_tiles|lbs_expand" sssp 20 3
 cap tc "tc_count" tc 20 1
 ls -la gpurun_out/r2
