@@ -149,99 +149,301 @@ __global__ void tc_rank(int64_t n, const int32_t* __restrict__ order, int32_t* _
     rank[order[r]] = (int32_t)r;
 }
 
-// upper degree of vertex order[r] -> ucnt[r]
+// Upper row of rank r (vertex v = order[r]): the ranks of v's higher-ranked
+// neighbours, left in adjacency order -- tc_count tests membership, it does
+// not merge.  Warp per row in rank order for rows up to kTcLong entries; the
+// longer rows (the top of the degree order) are cut into kTcLong-entry tiles
+// shared out over all warps, so a hub is not one warp's serial loop.
+#ifndef GB_TC_LONG
+#define GB_TC_LONG 2048
+#endif
+constexpr int kTcLong = GB_TC_LONG;
+
+// Tile plan of the long rows: tstart[i] = first tile of rank first + i,
+// meta = {first, tiles}; zeroes the long rows' counters and fill cursors.
+// One block; the degrees arrive sorted ascending.
+__global__ void __launch_bounds__(1024)
+tc_long_plan(int64_t n, const uint32_t* __restrict__ deg_sorted, int64_t* __restrict__ tstart,
+             int64_t* __restrict__ meta, unsigned long long* __restrict__ cursor,
+             int64_t* __restrict__ ucnt) {
+  typedef cub::BlockScan<int64_t, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t s_first, s_carry;
+  if (threadIdx.x == 0) {
+    int64_t lo = 0, hi = n;  // first degree > kTcLong
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (deg_sorted[mid] > (uint32_t)kTcLong) hi = mid; else lo = mid + 1;
+    }
+    s_first = lo;
+    s_carry = 0;
+  }
+  __syncthreads();
+  const int64_t first = s_first, nlong = n - first;
+  for (int64_t b = 0; b < nlong; b += 1024) {
+    const int64_t i = b + threadIdx.x;
+    const int64_t t = i < nlong ? (deg_sorted[first + i] + kTcLong - 1) / kTcLong : 0;
+    int64_t x;
+    Scan(tmp).ExclusiveSum(t, x);
+    if (i < nlong) {
+      tstart[i] = s_carry + x;
+      cursor[i] = 0;
+      ucnt[first + i] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry += x + t;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tstart[nlong] = s_carry;
+    meta[0] = first;
+    meta[1] = s_carry;
+    ucnt[n] = 0;
+  }
+}
+
+// long-row tile g -> (long row i, entries [p0, p1) of vertex order[first + i])
+__device__ __forceinline__ int64_t tc_tile(int64_t g, const int64_t* __restrict__ tstart,
+                                           int64_t nlong) {
+  int64_t lo = 0, hi = nlong;  // last i with tstart[i] <= g
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (tstart[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 __global__ void tc_upper_count(int64_t n, const int64_t* __restrict__ off,
                                const int32_t* __restrict__ idx, const int32_t* __restrict__ order,
-                               const int32_t* __restrict__ rank, int64_t* __restrict__ ucnt) {
+                               const int32_t* __restrict__ rank, const int64_t* __restrict__ tstart,
+                               const int64_t* __restrict__ meta, int64_t* __restrict__ ucnt) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = w0; r < n; r += nw) {
+  const int64_t first = meta[0], ntiles = meta[1], nlong = n - first;
+  for (int64_t r = w0; r < first; r += nw) {
     const int32_t v = order[r];
     long long c = 0;
     for (int64_t p = off[v] + lane; p < off[v + 1]; p += 32) c += rank[idx[p]] > r;
     c = warp_sum_ll(c);
     if (lane == 0) ucnt[r] = c;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ucnt[n] = 0;
+  // long rows: tile partial counts onto the zeros tc_long_plan wrote
+  for (int64_t g = w0; g < ntiles; g += nw) {
+    const int64_t i = tc_tile(g, tstart, nlong);
+    const int64_t r = first + i;
+    const int32_t v = order[r];
+    const int64_t p0 = off[v] + (g - tstart[i]) * kTcLong;
+    const int64_t p1 = min(p0 + kTcLong, off[v + 1]);
+    long long c = 0;
+    for (int64_t p = p0 + lane; p < p1; p += 32) c += rank[idx[p]] > r;
+    c = warp_sum_ll(c);
+    if (lane == 0 && c) atomicAdd((unsigned long long*)&ucnt[r], (unsigned long long)c);
+  }
+}
+
+__device__ __forceinline__ void tc_fill_range(int64_t p0, int64_t p1, int32_t r,
+                                              const int32_t* __restrict__ idx,
+                                              const int32_t* __restrict__ rank,
+                                              int32_t* __restrict__ out_row, int lane) {
+  int64_t out = 0;
+  for (int64_t base = p0; base < p1; base += 32) {
+    const int64_t p = base + lane;
+    int32_t rj = -1;
+    if (p < p1) rj = rank[idx[p]];
+    const bool keep = rj > r;
+    const uint32_t bal = __ballot_sync(GB_FULL, keep);
+    if (keep) out_row[out + __popc(bal & ((1u << lane) - 1u))] = rj;
+    out += __popc(bal);
+  }
 }
 
 __global__ void tc_upper_fill(int64_t n, const int64_t* __restrict__ off,
                               const int32_t* __restrict__ idx, const int32_t* __restrict__ order,
-                              const int32_t* __restrict__ rank, const int64_t* __restrict__ uoff,
+                              const int32_t* __restrict__ rank, const int64_t* __restrict__ tstart,
+                              const int64_t* __restrict__ meta, const int64_t* __restrict__ uoff,
+                              unsigned long long* __restrict__ cursor,
                               int32_t* __restrict__ uidx) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = w0; r < n; r += nw) {
+  const int64_t first = meta[0], ntiles = meta[1], nlong = n - first;
+  for (int64_t r = w0; r < first; r += nw) {
     const int32_t v = order[r];
-    int64_t out = uoff[r];
-    for (int64_t base = off[v]; base < off[v + 1]; base += 32) {
-      const int64_t p = base + lane;
-      int32_t rj = -1;
-      if (p < off[v + 1]) rj = rank[idx[p]];
-      const bool keep = rj > r;
-      const uint32_t bal = __ballot_sync(GB_FULL, keep);
-      if (keep) uidx[out + __popc(bal & ((1u << lane) - 1u))] = rj;
-      out += __popc(bal);
+    tc_fill_range(off[v], off[v + 1], (int32_t)r, idx, rank, uidx + uoff[r], lane);
+  }
+  for (int64_t g = w0; g < ntiles; g += nw) {
+    const int64_t i = tc_tile(g, tstart, nlong);
+    const int64_t r = first + i;
+    const int32_t v = order[r];
+    const int64_t p0 = off[v] + (g - tstart[i]) * kTcLong;
+    const int64_t p1 = min(p0 + kTcLong, off[v + 1]);
+    long long c = 0;  // the tile's count reserves its slice of the row
+    for (int64_t p = p0 + lane; p < p1; p += 32) c += rank[idx[p]] > r;
+    c = warp_sum_ll(c);
+    unsigned long long at = 0;
+    if (lane == 0 && c) at = atomicAdd(&cursor[i], (unsigned long long)c);
+    at = __shfl_sync(GB_FULL, at, 0);
+    if (c) tc_fill_range(p0, p1, (int32_t)r, idx, rank, uidx + uoff[r] + at, lane);
+  }
+}
+
+// Top ranks held in a per-warp bitmap.  With the degree ordering the keys of
+// the searched lists concentrate on the highest ranks (the hubs): on R-MAT s20
+// 99.8 % of them fall in the top 32768, so membership in U(r) is one shared
+// load and a bit test; the rest binary-search r's (sorted) adjacency for the
+// key's vertex.  No list needs sorting and no search touches U(r) itself.
+#ifndef GB_TC_TOP
+#define GB_TC_TOP 32768
+#endif
+constexpr int kTcTopBits = GB_TC_TOP;
+constexpr int kTcWords = kTcTopBits / 32;
+
+// The top kTcDense ranks also get a dense adjacency bitmap (8 MB, L2-resident):
+// row j holds U(j), whose keys all lie above j.  For a pair (r, j) with j in
+// that range, |U(r) & U(j)| is the popcount of the AND of j's row with r's
+// bitmap over the words above j -- fewer loads than walking U(j) whenever
+// U(j) is denser than one key per 32 ranks (the hub-hub part of R-MAT: 3x
+// fewer loads over the whole count at s20).
+#ifndef GB_TC_DENSE
+#define GB_TC_DENSE 8192
+#endif
+constexpr int kTcDense = GB_TC_DENSE;
+#ifndef GB_TC_KEYS
+#define GB_TC_KEYS 4
+#endif
+constexpr int kTcKeys = GB_TC_KEYS;
+
+__global__ void tc_dense_rows(int64_t n, int32_t dbase, int32_t W, const int64_t* __restrict__ uoff,
+                              const int32_t* __restrict__ uidx, uint32_t* __restrict__ dense) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = dbase + w0; j < n; j += nw) {
+    uint32_t* row = dense + (j - dbase) * W;
+    for (int64_t q = uoff[j] + lane; q < uoff[j + 1]; q += 32) {
+      const int32_t k = uidx[q] - dbase;
+      atomicOr(&row[k >> 5], 1u << (k & 31));
     }
   }
 }
 
-constexpr int kTcSmem = 1024;  // per-warp staged row capacity
+// branchless 32-bit lower bound of vertex u in the sorted list nb[0, len)
+__device__ __forceinline__ int tc_in_adjacency(const int32_t* __restrict__ nb, int len, int32_t u) {
+  const int32_t* b = nb;
+  while (len > 1) {
+    const int h = len >> 1;
+    b = b[h - 1] < u ? b + h : b;
+    len -= h;
+  }
+  return *b == u;
+}
 
 // warp per upper row r: count |U(r) & U(j)| for every j in U(r)
 __global__ void __launch_bounds__(256)
 tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict__ uidx,
-         unsigned long long* __restrict__ total) {
-  __shared__ int32_t s_row[8][kTcSmem];
+         const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+         const int32_t* __restrict__ order, int32_t dbase, int32_t W,
+         const uint32_t* __restrict__ dense, unsigned long long* __restrict__ total) {
+  __shared__ uint32_t s_bm[8][kTcWords];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t base = n > kTcTopBits ? (int32_t)(n - kTcTopBits) : 0;
+  const int boff = (dbase - base) >> 5;  // word of rank dbase in the row bitmap
+  uint32_t* bm = s_bm[wid];
+  for (int q = lane; q < kTcWords; q += 32) bm[q] = 0;
+  __syncwarp();
   long long c = 0;
   for (int64_t r = w0; r < n; r += nw) {
     const int64_t lo = uoff[r], hi = uoff[r + 1];
     const int64_t len = hi - lo;
     if (len < 2) continue;
-    const bool staged = len <= kTcSmem;
-    const int32_t* row = staged ? s_row[wid] : uidx + lo;
-    if (staged) {
-      for (int64_t q = lane; q < len; q += 32) s_row[wid][q] = uidx[lo + q];
-      __syncwarp();
+    const int32_t* row = uidx + lo;
+    for (int64_t q = lane; q < len; q += 32) {
+      const int32_t v = row[q] - base;
+      if (v >= 0) atomicOr(&bm[v >> 5], 1u << (v & 31));
     }
+    __syncwarp();
     const int ilen = (int)len;
-    const int32_t rmax = row[ilen - 1];
-    int64_t mylo = 0, myhi = 0;  // bounds of U(row[a]) for a = (chunk of 32) + lane
-    for (int a = 0; a < ilen; ++a) {
-      if ((a & 31) == 0) {
-        // the next 32 lists' bounds in one round of loads
-        const int aa = a + lane;
-        mylo = myhi = 0;
-        if (aa < ilen) {
-          const int32_t jj = row[aa];
-          mylo = uoff[jj];
-          myhi = uoff[jj + 1];
+    const int32_t vr = order[r];  // for keys below the bitmap: search r's sorted adjacency
+    const int32_t* nb = idx + off[vr];
+    const int nlen = (int)(off[vr + 1] - off[vr]);
+    // r's bitmap words of the 32-word window at the top of the dense range
+    const int wt = (W > 32 ? W - 32 : 0) + lane;
+    const uint32_t bmtop = wt < W ? bm[wt + boff] : 0u;
+    uint32_t cr = 0;  // this lane's count for row r
+    for (int c0 = 0; c0 < ilen; c0 += 32) {
+      // lane = one pair (r, j) of the next 32; classify it
+      const int a = c0 + lane;
+      int32_t j = -1;
+      int64_t jlo = 0, jhi = 0;
+      if (a < ilen) {
+        j = row[a];
+        jlo = uoff[j];
+        jhi = uoff[j + 1];
+      }
+      int wj = W;  // first dense word holding ranks above j
+      bool dn = false;
+      if (j >= dbase) {
+        wj = (j + 1 - dbase) >> 5;
+        dn = W - wj < jhi - jlo;  // fewer words than keys: AND the dense row
+      }
+      uint32_t top = __ballot_sync(GB_FULL, dn && W - wj <= 32);
+      const uint32_t wide = __ballot_sync(GB_FULL, dn && W - wj > 32);
+      const uint32_t keyed = __ballot_sync(GB_FULL, !dn && jhi > jlo);
+      // dense rows inside the top window: one coalesced word per lane, four
+      // pairs' loads in flight
+      while (top) {
+        uint32_t word[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          word[u] = 0;
+          if (top) {
+            const int p = __ffs(top) - 1;
+            top &= top - 1;
+            const int32_t jp = __shfl_sync(GB_FULL, j, p);
+            if (wt < W) word[u] = dense[(int64_t)(jp - dbase) * W + wt];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cr += __popc(word[u] & bmtop);
+      }
+      for (uint32_t m = wide; m; m &= m - 1) {
+        const int p = __ffs(m) - 1;
+        const int32_t jp = __shfl_sync(GB_FULL, j, p);
+        const int wp = __shfl_sync(GB_FULL, wj, p);
+        const uint32_t* arow = dense + (int64_t)(jp - dbase) * W;
+        for (int w = wp + lane; w < W; w += 32) cr += __popc(arow[w] & bm[w + boff]);
+      }
+      // every key k of U(j) has rank k > j > r, so k is in U(r) iff it is a
+      // neighbour of r: |U(r) & U(j)| is the count of those memberships
+      for (uint32_t m = keyed; m; m &= m - 1) {
+        const int p = __ffs(m) - 1;
+        const int64_t klo = __shfl_sync(GB_FULL, jlo, p);
+        const int64_t khi = __shfl_sync(GB_FULL, jhi, p);
+        // kTcKeys keys in flight per lane: the loop is bound by L2 latency
+        for (int64_t q = klo + lane; q < khi; q += 32 * kTcKeys) {
+          int32_t key[kTcKeys];
+#pragma unroll
+          for (int u = 0; u < kTcKeys; ++u) key[u] = q + 32 * u < khi ? uidx[q + 32 * u] : -1;
+#pragma unroll
+          for (int u = 0; u < kTcKeys; ++u) {
+            if (key[u] < 0) continue;
+            const int32_t v = key[u] - base;
+            if (v >= 0)
+              cr += (bm[v >> 5] >> (v & 31)) & 1u;
+            else
+              cr += tc_in_adjacency(nb, nlen, order[key[u]]);
+          }
         }
       }
-      const int64_t jlo = __shfl_sync(GB_FULL, mylo, a & 31);
-      const int64_t jhi = __shfl_sync(GB_FULL, myhi, a & 31);
-      // elements of U(j) are > j > r; search them in U(r) after position a
-      // (branchless 32-bit lower bound: the kernel is issue-bound)
-      const int32_t* base0 = row + a + 1;
-      const int m = ilen - a - 1;
-      if (m == 0) continue;
-      for (int64_t q = jlo + lane; q < jhi; q += 32) {
-        const int32_t key = uidx[q];
-        if (key > rmax) break;  // sorted lists: no later key of U(j) is in U(r) either
-        const int32_t* b = base0;
-        int l = m;
-        while (l > 1) {
-          const int h = l >> 1;
-          b = b[h - 1] < key ? b + h : b;
-          l -= h;
-        }
-        c += *b == key;
-      }
+    }
+    c += cr;
+    __syncwarp();
+    for (int64_t q = lane; q < len; q += 32) {
+      const int32_t v = row[q] - base;
+      if (v >= 0) bm[v >> 5] = 0;
     }
     __syncwarp();
   }
@@ -358,6 +560,10 @@ gb_status gb_tc(gb_ctx* ctx, const gb_csr* a, int64_t* count_host) {
   int64_t* ucnt = ar.alloc<int64_t>(n + 1);
   int64_t* uoff = ar.alloc<int64_t>(n + 1);
   unsigned long long* total = ar.alloc<unsigned long long>(1);
+  const int64_t maxlong = a->nnz / kTcLong + 1;  // rows longer than kTcLong
+  int64_t* tstart = ar.alloc<int64_t>(maxlong + 1);
+  int64_t* meta = ar.alloc<int64_t>(2);
+  unsigned long long* cursor = ar.alloc<unsigned long long>(maxlong);
   GB_ARENA_CHECK(ctx, ar);
   tc_degree_keys<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, a->offsets, deg, ids);
   // stable: ties keep ascending vertex id (algorithms.py:209-212)
@@ -367,8 +573,9 @@ gb_status gb_tc(gb_ctx* ctx, const gb_csr* a, int64_t* count_host) {
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp, tb, deg, deg2, ids, order, n, 0, 32, s));
   tc_rank<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, order, rank);
+  tc_long_plan<<<1, 1024, 0, s>>>(n, deg2, tstart, meta, cursor, ucnt);
   tc_upper_count<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(n, a->offsets, a->indices, order,
-                                                                rank, ucnt);
+                                                                rank, tstart, meta, ucnt);
   size_t tb2 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb2, ucnt, uoff, n + 1, s);
   void* tmp2 = ar.raw(tb2);
@@ -377,22 +584,28 @@ gb_status gb_tc(gb_ctx* ctx, const gb_csr* a, int64_t* count_host) {
   int64_t m = 0;
   GB_TRY(read_i64(ctx, uoff + n, &m));
   int32_t* uidx = ar.alloc<int32_t>(m + 1);
-  int32_t* uidx2 = ar.alloc<int32_t>(m + 1);
   GB_ARENA_CHECK(ctx, ar);
   tc_upper_fill<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(n, a->offsets, a->indices, order,
-                                                               rank, uoff, uidx);
-  // sort each upper row ascending (rank order)
-  size_t tb3 = 0;
-  cub::DeviceSegmentedSort::SortKeys(nullptr, tb3, uidx, uidx2, m, n, uoff, uoff + 1, s);
-  void* tmp3 = ar.raw(tb3);
+                                                               rank, tstart, meta, uoff, cursor,
+                                                               uidx);
+  // dense rows of the top ranks, word-aligned with tc_count's row bitmap
+  const int64_t tbase = n > kTcTopBits ? n - kTcTopBits : 0;
+  const int64_t lowest = n > kTcDense ? n - kTcDense : 0;
+  const int32_t dbase = (int32_t)(tbase + ((lowest - tbase) >> 5 << 5));
+  const int32_t W = (int32_t)((n - dbase + 31) / 32);
+  uint32_t* dense = ar.alloc<uint32_t>((size_t)W * (n - dbase));
   GB_ARENA_CHECK(ctx, ar);
-  GB_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(tmp3, tb3, uidx, uidx2, m, n, uoff, uoff + 1, s));
+  GB_CUDA(ctx, cudaMemsetAsync(dense, 0, sizeof(uint32_t) * (size_t)W * (n - dbase), s));
+  tc_dense_rows<<<grid_for(ctx, (n - dbase) * 32, 256, 16), 256, 0, s>>>(n, dbase, W, uoff, uidx,
+                                                                         dense);
   GB_CUDA(ctx, cudaMemsetAsync(total, 0, 8, s));
   const int ps = prof_begin(ctx, PROF_TC, m);
-  tc_count<<<resident_grid(ctx, tc_count, 256), 256, 0, s>>>(n, uoff, uidx2, total);
+  tc_count<<<resident_grid(ctx, tc_count, 256), 256, 0, s>>>(n, uoff, uidx, a->offsets,
+                                                               a->indices, order, dbase, W, dense,
+                                                               total);
   prof_end(ctx, ps);
   GB_LAUNCH_CHECK(ctx);
-  count_launch(ctx, 12);
+  count_launch(ctx, 11);
   return read_i64(ctx, (const int64_t*)total, count_host);
 }
 
