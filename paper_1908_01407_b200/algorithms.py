@@ -130,14 +130,20 @@ class _PendingBfs:
 class _LogRing:
     """Log buffers of asynchronous bfs calls, allocated once per context and
     reused round robin: a pinned prefix row and a device log per slot (pinning
-    or allocating per call costs milliseconds and can synchronise)."""
+    or allocating per call costs milliseconds and can synchronise).  The
+    device logs of calls up to the default loop cap share one slab allocated
+    on first use: per-slot allocations came from the caching allocator's small
+    pool, whose every eighth request mapped a new 2 MB segment with a
+    synchronising cudaMalloc -- that drained the queue of asynchronous calls."""
 
     SLOTS = 256
+    STRIDE = 1 + 3 * 10_000   # Descriptor().max_niter
 
     def __init__(self, device):
         self.pin = torch.empty((self.SLOTS, 1 + 3 * _LOG_PREFIX), dtype=torch.int64,
                                pin_memory=True)
-        # device logs are sized per slot from the call's loop cap, on first use
+        self.slab = None
+        # device logs of larger caps are sized per slot, on first use
         self.dev = [None] * self.SLOTS
         self.device = device
         self.owner = [None] * self.SLOTS
@@ -155,20 +161,28 @@ class _LogRing:
         i = self.next
         self.next = (i + 1) % self.SLOTS
         self._settle(i)  # the slot's previous call has finished with both buffers
-        if self.dev[i] is None or self.dev[i].numel() < need:
-            self.dev[i] = torch.empty(max(need, 1 + 3 * 64), dtype=torch.int64, device=self.device)
+        if need <= self.STRIDE:
+            if self.slab is None:
+                self.slab = torch.empty((self.SLOTS, self.STRIDE), dtype=torch.int64,
+                                        device=self.device)
+            dev = self.slab[i]
+        else:
+            if self.dev[i] is None or self.dev[i].numel() < need:
+                self.dev[i] = torch.empty(need, dtype=torch.int64, device=self.device)
+            dev = self.dev[i]
         self.owner[i] = weakref.ref(pending)
         if self.events[i] is None:
             self.events[i] = _lib.DeviceEvent(pending.ctx)
         pending.event = self.events[i]
         pending.row = self.pin[i]
-        pending.dev = self.dev[i]
-        return self.pin[i], self.dev[i]
+        pending.dev = dev
+        return self.pin[i], dev
 
     def release(self):
         """Settle every outstanding call and drop the device logs (ctx.trim())."""
         for i in range(self.SLOTS):
             self._settle(i)
+        self.slab = None
         self.dev = [None] * self.SLOTS
 
 
