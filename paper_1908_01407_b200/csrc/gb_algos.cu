@@ -383,6 +383,51 @@ cc_pull_live(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __re
   row_tiles<int>(R, nz_rows, nz_off, idx, tile_first, red);
 }
 
+// The first iteration's pull: every grandparent is still its own id
+// (cc_init), so min over neighbours of gp[j] is the smallest column id of the
+// row -- the same hook values from the index stream alone, no gathers (s24:
+// one full pull of 520 M random 4-byte gathers becomes a streaming read).
+struct CcMinId {
+  int* __restrict__ hook;
+  __device__ __forceinline__ int identity() const { return kImax32; }
+  __device__ __forceinline__ int load(int64_t, int32_t col) const { return col; }
+  __device__ __forceinline__ int fold(int a, int x) const { return x < a ? x : a; }
+  __device__ __forceinline__ void emit(int64_t row, int acc, bool whole) const {
+    if (acc == kImax32) return;
+    if (whole) hook[row] = acc;
+    else atomicMin(hook + row, acc);
+  }
+};
+
+__global__ void __launch_bounds__(256, GB_ROW_MINB)
+cc_pull_first(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __restrict__ nz_off,
+              const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_first,
+              int* __restrict__ hook) {
+  CcMinId red{hook};
+  row_tiles<int>(R, nz_rows, nz_off, idx, tile_first, red);
+}
+
+// With rows that start at their minimum (any sorted CSR) the first pull is
+// one load per row.
+__global__ void cc_hook_first(int64_t n, const int64_t* __restrict__ off,
+                              const int32_t* __restrict__ idx, int* __restrict__ hook) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = off[r];
+    hook[r] = p < off[r + 1] ? idx[p] : kImax32;
+  }
+}
+
+__global__ void cc_first_is_min(int64_t n, const int64_t* __restrict__ off,
+                                const int32_t* __restrict__ idx, const int* __restrict__ rmin,
+                                int* __restrict__ bad) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = off[r];
+    if (p < off[r + 1] && idx[p] != rmin[r]) *bad = 1;
+  }
+}
+
 // a pull iteration probes the live bitmap first when fewer than this share
 // of the grandparents are live (GB_CC_LIVE_SHARE)
 static double cc_live_share() {
@@ -390,6 +435,21 @@ static double cc_live_share() {
   if (v < 0) {
     const char* e = getenv("GB_CC_LIVE_SHARE");
     v = e ? atof(e) : 0.3;
+  }
+  return v;
+}
+
+// A pull iteration (the reference rule's decision, logged as such) whose
+// live grandparents are fewer than this share of n runs as the transposed
+// traversal: for each live j, min-fold gp[j] into hook[i] over column j of A.
+// Column j lists exactly the rows i with A(i, j), so the hook values are the
+// pull's, bit for bit, from sum(deg(live)) edges instead of a pass over all
+// of A (GB_CC_PUSH_SHARE).
+static double cc_push_share() {
+  static double v = -1.0;
+  if (v < 0) {
+    const char* e = getenv("GB_CC_PUSH_SHARE");
+    v = e ? atof(e) : 0.2;
   }
   return v;
 }
@@ -444,10 +504,13 @@ __global__ void cc_hook(int64_t n, const int* __restrict__ hook, int* __restrict
     if (m == kImax32) continue;  // nothing to propose (sparsified / isolated)
     // read first: most targets already hold a smaller label (the giant
     // component's root is the target of millions of k), so the atomic --
-    // which serialises on one L2 slice per address -- is rarely issued
-    if (m < *reinterpret_cast<volatile int*>(parent + k)) atomicMin(parent + k, m);
+    // which serialises on one L2 slice per address -- is rarely issued.  The
+    // read goes through L1: parent only decreases inside the kernel, so a
+    // stale cached value is never below the true one and at worst issues an
+    // unneeded atomic (a volatile read sent every k to the root's L2 slice)
+    if (m < __ldca(parent + k)) atomicMin(parent + k, m);
     const int t = pp[k];
-    if (m < *reinterpret_cast<volatile int*>(parent + t)) atomicMin(parent + t, m);
+    if (m < __ldca(parent + t)) atomicMin(parent + t, m);
   }
 }
 
@@ -527,14 +590,31 @@ __device__ __forceinline__ void cc_shortcut_body(int64_t n, const int* __restric
   }
 }
 
-// frontier list of live grandparents (gp != sentinel) for a push iteration
+// frontier list of live grandparents (gp != sentinel) for a push iteration.
+// The order is free (the push folds with min), so a warp reserves once per
+// 1024-vertex chunk: one counter atomic per warp and iteration measured
+// 0.31-0.42 ms at s24, serialised on the single address.
 __global__ void cc_list(int64_t n, const int* __restrict__ gp, int32_t* __restrict__ F,
                         unsigned long long* __restrict__ count) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const bool l = gp[k] != kImax32;
-    const long long slot = warp_reserve(count, l ? 1 : 0);
-    if (l) F[slot] = (int32_t)k;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w0 * 1024; c < n; c += nw * 1024) {
+    const int64_t end = c + 1024 < n ? c + 1024 : n;
+    int cnt = 0;
+    for (int64_t k = c + lane; k < end; k += 32) cnt += gp[k] != kImax32;
+    cnt = __reduce_add_sync(GB_FULL, cnt);
+    if (cnt == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)cnt);
+    base = __shfl_sync(GB_FULL, base, 0);
+    for (int64_t k0 = c; k0 < end; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const bool l = k < end && gp[k] != kImax32;
+      const uint32_t bal = __ballot_sync(GB_FULL, l);
+      if (l) F[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)k;
+      base += __popc(bal);
+    }
   }
 }
 
@@ -902,6 +982,8 @@ static gb_status pagerank_graph(gb_ctx* ctx, const gb_csr* pull, const int64_t* 
 struct CcState {
   double ratio;
   double live_share;  // pull with the live bitmap below this share of live grandparents
+  double push_share;  // below this share a pull runs as the transposed push
+  int32_t has_cols, pad_;
   int64_t max_iters;
   int64_t* log;
   int32_t policy, sparsify;
@@ -909,6 +991,7 @@ struct CcState {
   int64_t it, live, iters;
   unsigned long long cnt[3];  // changed, live, listed
   unsigned long long nlong;
+  int64_t npush;  // iterations that ran the push branch (launch accounting)
 };
 
 struct CcPushOp {
@@ -930,9 +1013,12 @@ __global__ void cc_start_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditi
   st->iters = 0;
   st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
   st->nlong = 0;
+  st->npush = 0;
   const bool run = st->max_iters > 0;
   unsigned dir = 0;
-  if (run) dir = log_decision(st->log, 0, nnz, n, n, st->ratio, st->policy) == GB_DIR_PULL ? 0 : 1;
+  // branch 3: the first pull (grandparents are the identity)
+  if (run) dir = log_decision(st->log, 0, nnz, n, n, st->ratio, st->policy) == GB_DIR_PULL ? 3 : 1;
+  st->npush = dir == 1;
   cudaGraphSetConditional(h_loop, run ? 1u : 0u);
   cudaGraphSetConditional(h_dir, dir);
 }
@@ -953,11 +1039,15 @@ __global__ void cc_step_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditio
   if (changed != 0) st->live = (int64_t)st->cnt[1];
   st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
   st->nlong = 0;
-  unsigned dir = 3;  // no branch
+  unsigned dir = 4;  // no branch
   if (cont) {
     // branch 0: pull, 1: push, 2: pull probing the live bitmap first
     const int32_t d = log_decision(st->log, it + 1, nnz, n, st->live, st->ratio, st->policy);
-    dir = d == GB_DIR_PULL ? ((double)st->live < st->live_share * (double)n ? 2u : 0u) : 1u;
+    const double live = (double)st->live;
+    dir = d != GB_DIR_PULL || (st->has_cols && live < st->push_share * (double)n)
+              ? 1u
+              : (live < st->live_share * (double)n ? 2u : 0u);
+    st->npush += dir == 1;
   }
   cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
   cudaGraphSetConditional(h_dir, dir);
@@ -968,6 +1058,7 @@ struct CcGraph {
   bool has_cols = false;
   void* mem = nullptr;
   int *P, *mn, *gp, *gpp, *pp, *hook;
+  bool first_min = false;  // every row's first stored column is its smallest (format check)
   int32_t *F, *longk, *longc;
   uint32_t* livebm;  // live grandparents (written by the shortcut pass)
   CcState* st;
@@ -1004,8 +1095,19 @@ static cudaError_t cc_graph_build(gb_ctx* ctx, CcGraph* G) {
       cudaStream_t b = cs[1];
       copy_i32<<<vec_grid, 256, 0, b>>>(n, G->P, G->pp);
       fill_i32<<<vec_grid, 256, 0, b>>>(n, kImax32, G->hook);
-      cudaGraph_t br[3];
-      GB_LTRY(add_conditional(b, h_dir, cudaGraphCondTypeSwitch, 3, br));
+      cudaGraph_t br[4];
+      GB_LTRY(add_conditional(b, h_dir, cudaGraphCondTypeSwitch, 4, br));
+      GB_LTRY(loop_capture_into(br[3], cs[2], [&]() -> cudaError_t {
+        // first pull (grandparents are the identity): each row's smallest
+        // column id -- its first entry when the rows start at their minimum
+        if (G->first_min)
+          cc_hook_first<<<vec_grid, 256, 0, cs[2]>>>(n, G->rows.offsets, G->rows.indices, G->hook);
+        else if (G->plan.R)
+          cc_pull_first<<<resident_grid(ctx, cc_pull_first, 256), 256, 0, cs[2]>>>(
+              G->plan.R, G->plan.nz_rows, G->plan.nz_off, G->rows.indices, G->plan.tile_first,
+              G->hook);
+        return cudaGetLastError();
+      }));
       GB_LTRY(loop_capture_into(br[0], cs[2], [&]() -> cudaError_t {
         // pull: mxv walks rows of A (kernels.py:313-316)
         if (G->plan.R)
@@ -1094,6 +1196,26 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
     G->plan.tile_first = (int32_t*)(m + o_t);
     Arena ar(ctx);
     gb_status st = row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &G->plan);
+    if (st == GB_OK) {
+      // format check, once per matrix: is each row's first stored column its
+      // smallest?  (true for every sorted CSR; from_csr may wrap unsorted rows)
+      int* rmin = ar.alloc<int>(n);
+      int* bad = ar.alloc<int>(2);
+      if (ar.failed) st = GB_ERR_OOM;
+      if (st == GB_OK) {
+        fill_i32<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, kImax32, rmin);
+        cudaMemsetAsync(bad, 0, 8, s);
+        if (G->plan.R)
+          cc_pull_first<<<resident_grid(ctx, cc_pull_first, 256), 256, 0, s>>>(
+              G->plan.R, G->plan.nz_rows, G->plan.nz_off, rows->indices, G->plan.tile_first, rmin);
+        cc_first_is_min<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rows->offsets, rows->indices,
+                                                                   rmin, bad);
+        int64_t h = 1;
+        st = read_i64(ctx, (const int64_t*)bad, &h);
+        G->first_min = (h & 0xffffffff) == 0;
+        count_launch(ctx, 4);
+      }
+    }
     cudaError_t e = st == GB_OK ? cc_graph_build(ctx, G) : cudaSuccess;
     if (st != GB_OK || e != cudaSuccess) {
       cudaGetLastError();
@@ -1113,12 +1235,15 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
   h.policy = policy;
   h.sparsify = sparsify;
   h.live_share = cc_live_share();
+  h.push_share = cc_push_share();
+  h.has_cols = cols != nullptr;
   GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(CcState, it), cudaMemcpyHostToDevice, s));
   GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
   widen_i32<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, G->P, reinterpret_cast<long long*>(parent));
   GB_LAUNCH_CHECK(ctx);
-  int64_t iters = 0;
+  int64_t iters = 0, npush = 0;
   GB_CUDA(ctx, cudaMemcpyAsync(&iters, &G->st->iters, 8, cudaMemcpyDeviceToHost, s));
+  GB_CUDA(ctx, cudaMemcpyAsync(&npush, &G->st->npush, 8, cudaMemcpyDeviceToHost, s));
   GB_CUDA(ctx, cudaStreamSynchronize(s));
   if (iters > 0) {
     std::vector<int64_t> lg(3 * iters);
@@ -1130,7 +1255,8 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
       log_est[i] = lg[3 * i + 2];
     }
   }
-  count_launch(ctx, (int)(3 + 6 * iters));
+  // per iteration: copy, fill, the branch (1 kernel; push 3), hook, shortcut, step
+  count_launch(ctx, (int)(3 + 6 * iters + 2 * npush));
   *iters_out = iters;
   return GB_OK;
 }
@@ -1633,9 +1759,14 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
     GB_CUDA(ctx, cudaMemcpyAsync(pp, P, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
     fill_i32<<<vec_grid, 256, 0, s>>>(n, kImax32, hook);
     const int ps = prof_begin(ctx, PROF_CC, live);
-    if (dir == GB_DIR_PULL) {
+    // a pull over few live grandparents runs as the transposed push (same hooks)
+    const bool as_push = dir != GB_DIR_PULL || (it > 0 && cols && (double)live < cc_push_share() * (double)n);
+    if (!as_push) {
       // mxv pull walks rows of A (kernels.py:313-316, row_view(False))
-      if (plan.R && it > 0 && (double)live < cc_live_share() * (double)n)
+      if (plan.R && it == 0)  // grandparents are the identity: column ids suffice
+        cc_pull_first<<<resident_grid(ctx, cc_pull_first, 256), 256, 0, s>>>(
+            plan.R, plan.nz_rows, plan.nz_off, rows->indices, plan.tile_first, hook);
+      else if (plan.R && (double)live < cc_live_share() * (double)n)
         cc_pull_live<<<resident_grid(ctx, cc_pull_live, 256), 256, 0, s>>>(
             plan.R, plan.nz_rows, plan.nz_off, rows->indices, plan.tile_first, gp, livebm, hook);
       else if (plan.R) cc_pull<<<pull_grid, 256, 0, s>>>(plan.R, plan.nz_rows, plan.nz_off, rows->indices,

@@ -2,7 +2,7 @@
 calls of one algorithm inside a cudaProfilerStart/Stop window (use with
 `ncu --profile-from-start off`).
 
-    python tools/prof_bfs.py --algo bfs|sssp|pr|cc|tc|mxv --scale 24 --reps 1
+    python tools/prof_bfs.py --algo bfs|sssp|pr|cc|ccpush|tc|mxv --scale 24 --reps 1
 """
 import argparse
 import os
@@ -22,7 +22,9 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--algo", default="bfs")
 args = ap.parse_args()
 
-A = rmat_matrix(args.scale, weighted=args.algo == "sssp")
+A = (rmat_matrix(args.scale, a=.25, b=.25, c=.25, d=.25) if args.algo.endswith("_u")
+     else rmat_matrix(args.scale, weighted=args.algo == "sssp"))
+args.algo = args.algo[:-2] if args.algo.endswith("_u") else args.algo   # *_u: uniform graph
 gb._lib.context().trim()
 if args.algo == "mxvm":
     from paper_1908_01407_b200.containers import Vector
@@ -42,6 +44,8 @@ def run():
         gb.pagerank(A, eps=1e-300, max_iters=3)
     elif args.algo == "cc":
         gb.connected_components(A)
+    elif args.algo == "ccpush":   # same labels and iterations, every iteration pushed
+        gb.connected_components(A, desc=gb.Descriptor(direction=gb.Direction.FORCE_PUSH))
     elif args.algo == "tc":
         gb.triangle_count(A)
     elif args.algo == "mxvm":

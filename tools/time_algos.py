@@ -29,12 +29,14 @@ CASES = [
     ("tc", 20, lambda A: gb.triangle_count(A)),
     ("bfs", 20, lambda A: gb.bfs(A, 0)),
     ("cc", 20, lambda A: gb.connected_components(A)),
+    ("ccu", 24, lambda A: gb.connected_components(A)),   # uniform a=b=c=d=.25
 ]
 for name, scale, fn in CASES:
     if args.only and name not in args.only.split(","):
         continue
     t0 = time.perf_counter()
-    A = rmat_matrix(scale, weighted=name == "sssp")
+    A = (rmat_matrix(scale, a=.25, b=.25, c=.25, d=.25) if name == "ccu"
+         else rmat_matrix(scale, weighted=name == "sssp"))
     torch.cuda.synchronize()
     build = time.perf_counter() - t0
     gb._lib.context().trim()
