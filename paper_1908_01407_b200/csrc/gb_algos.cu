@@ -484,6 +484,53 @@ __global__ void fill_i32(int64_t n, int v, int* __restrict__ a) {
     a[i] = v;
 }
 
+// Format check behind the gather-free first pull: does every row start at
+// its smallest column (any sorted CSR; from_csr may wrap unsorted rows)?
+// Computed once per matrix (the csr's content id `gen`) and shared by both
+// loop engines.
+struct CcFirstMin {
+  uint64_t gen = 0;
+  int64_t n = 0, nnz = 0;
+  bool first_min = false;
+};
+
+static void cc_first_min_free(void* p) { delete static_cast<CcFirstMin*>(p); }
+
+static gb_status cc_rows_start_at_min(gb_ctx* ctx, const gb_csr* rows, const RowTilesPlan& plan,
+                                      bool* out) {
+  void** slot = ctx_slot(ctx, SLOT_CC_FIRSTMIN, cc_first_min_free);
+  auto* c = static_cast<CcFirstMin*>(*slot);
+  if (c && rows->gen != 0 && c->gen == rows->gen && c->n == rows->nrows && c->nnz == rows->nnz) {
+    *out = c->first_min;
+    return GB_OK;
+  }
+  const int64_t n = rows->nrows;
+  cudaStream_t s = stream_of(ctx);
+  Arena ar(ctx);
+  int* rmin = ar.alloc<int>(n);
+  int* bad = ar.alloc<int>(2);
+  GB_ARENA_CHECK(ctx, ar);
+  fill_i32<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, kImax32, rmin);
+  GB_CUDA(ctx, cudaMemsetAsync(bad, 0, 8, s));
+  if (plan.R)
+    cc_pull_first<<<resident_grid(ctx, cc_pull_first, 256), 256, 0, s>>>(
+        plan.R, plan.nz_rows, plan.nz_off, rows->indices, plan.tile_first, rmin);
+  cc_first_is_min<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rows->offsets, rows->indices, rmin,
+                                                             bad);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 4);
+  int64_t h = 1;
+  GB_TRY(read_i64(ctx, (const int64_t*)bad, &h));
+  if (!c) *slot = c = new CcFirstMin();
+  c->gen = rows->gen;
+  c->n = n;
+  c->nnz = rows->nnz;
+  c->first_min = (h & 0xffffffff) == 0;
+  *out = c->first_min;
+  return GB_OK;
+}
+
+
 __global__ void cc_init(int64_t n, int* __restrict__ parent, int* __restrict__ mn,
                         int* __restrict__ gp, int* __restrict__ gpp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -1196,26 +1243,7 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
     G->plan.tile_first = (int32_t*)(m + o_t);
     Arena ar(ctx);
     gb_status st = row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &G->plan);
-    if (st == GB_OK) {
-      // format check, once per matrix: is each row's first stored column its
-      // smallest?  (true for every sorted CSR; from_csr may wrap unsorted rows)
-      int* rmin = ar.alloc<int>(n);
-      int* bad = ar.alloc<int>(2);
-      if (ar.failed) st = GB_ERR_OOM;
-      if (st == GB_OK) {
-        fill_i32<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, kImax32, rmin);
-        cudaMemsetAsync(bad, 0, 8, s);
-        if (G->plan.R)
-          cc_pull_first<<<resident_grid(ctx, cc_pull_first, 256), 256, 0, s>>>(
-              G->plan.R, G->plan.nz_rows, G->plan.nz_off, rows->indices, G->plan.tile_first, rmin);
-        cc_first_is_min<<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, rows->offsets, rows->indices,
-                                                                   rmin, bad);
-        int64_t h = 1;
-        st = read_i64(ctx, (const int64_t*)bad, &h);
-        G->first_min = (h & 0xffffffff) == 0;
-        count_launch(ctx, 4);
-      }
-    }
+    if (st == GB_OK) st = cc_rows_start_at_min(ctx, rows, G->plan, &G->first_min);
     cudaError_t e = st == GB_OK ? cc_graph_build(ctx, G) : cudaSuccess;
     if (st != GB_OK || e != cudaSuccess) {
       cudaGetLastError();
@@ -1743,6 +1771,8 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   GB_ARENA_CHECK(ctx, ar);
   RowTilesPlan plan;
   GB_TRY(row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &plan));
+  bool first_min = false;
+  GB_TRY(cc_rows_start_at_min(ctx, rows, plan, &first_min));
   cc_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, P, mn, gp, gpp);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 1);
@@ -1763,7 +1793,9 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
     const bool as_push = dir != GB_DIR_PULL || (it > 0 && cols && (double)live < cc_push_share() * (double)n);
     if (!as_push) {
       // mxv pull walks rows of A (kernels.py:313-316, row_view(False))
-      if (plan.R && it == 0)  // grandparents are the identity: column ids suffice
+      if (it == 0 && first_min)  // grandparents are the identity: each row's first column
+        cc_hook_first<<<vec_grid, 256, 0, s>>>(n, rows->offsets, rows->indices, hook);
+      else if (plan.R && it == 0)  // ... or its streaming minimum
         cc_pull_first<<<resident_grid(ctx, cc_pull_first, 256), 256, 0, s>>>(
             plan.R, plan.nz_rows, plan.nz_off, rows->indices, plan.tile_first, hook);
       else if (plan.R && (double)live < cc_live_share() * (double)n)

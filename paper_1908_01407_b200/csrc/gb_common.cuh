@@ -366,7 +366,7 @@ bool prof_enabled(gb_ctx* ctx);
 // Per-context cached objects (e.g. instantiated CUDA graphs) that live until
 // the context is destroyed: slot i holds a pointer and its destructor.
 enum { SLOT_BFS_GRAPH = 0, SLOT_BFS_AUX = 1, SLOT_PR_GRAPH = 2, SLOT_CC_GRAPH = 3,
-       SLOT_SSSP_GRAPH = 4, SLOT_BFS_COOP = 5, kCtxSlots = 8 };
+       SLOT_SSSP_GRAPH = 4, SLOT_BFS_COOP = 5, SLOT_CC_FIRSTMIN = 6, kCtxSlots = 8 };
 void** ctx_slot(gb_ctx* ctx, int i, void (*destroy)(void*));
 // pinned host scratch for small device->host reads (>= 64 int64 slots)
 int64_t* pinned_slots(gb_ctx* ctx);
