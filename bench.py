@@ -740,11 +740,15 @@ def run_ours(args):
             "bfs_tree": tree,
             "bfs_switch_ratio_001": dopt,
             "exchange": (None if world == 1 else {
-                "per_level_last_step": runner.exchange.log[-len(trace):],
-                "what": "FrontierExchange per level: (mode, bytes sent per rank); dense = "
-                        "allgather of the owned bitmap words (|f|*32 > n), sparse = "
-                        "allgather(v) of the owned new vertex ids; plus one 8 B count "
-                        "allgather", "backend": os.environ.get("GB_DIST_BACKEND", "nccl")}),
+                "per_level_last_step": runner.exchange.log[-(len(trace) + 1):],
+                "loop": runner.loop,
+                "what": "FrontierExchange per level: (mode, bytes sent per rank).  The "
+                        "device-resident loop (default) exchanges dense = allgather of the "
+                        "owned bitmap words every level, plus one no-op level past the end "
+                        "(the host watches the done flag one level behind); the host loop "
+                        "picks dense (|f|*32 > n) or sparse = allgather(v) of the owned new "
+                        "vertex ids after an 8 B count allgather",
+                "backend": os.environ.get("GB_DIST_BACKEND", "nccl")}),
             "cpu_baseline": cpu,
             "parity_vs_oracle": parity,
             "configs": configs,

@@ -478,6 +478,33 @@ gb_status gb_bfs_dist_set_ids(gb_ctx* ctx, int64_t n, int32_t P, int64_t kmax,
                               const int64_t* counts, const int32_t* gathered, uint32_t* xbm);
 /* clear the levels of the K vertices in F (loop cap reached, algorithms.py:69) */
 gb_status gb_bfs_dist_unstamp(gb_ctx* ctx, int64_t K, const int32_t* F, int64_t* levels);
+/* Device-resident partitioned levels (distributed.bfs_partitioned_device):
+ * the host never reads K.  `state` is an int64[16] device block (frontier
+ * size, depth, iteration, mode, done, the loop cap), `log` the raw decision
+ * log int64[1 + 3*max_iters] (count, then (dir, K, estimate) per iteration,
+ * like gb_bfs_ordered_async).  Per level: gb_bfs_dist_dev_level (the
+ * reference rule on the device -- kernels.py:108-126 -- then the push over
+ * the column block or the pull over the row block, whichever the state's mode
+ * says, each returning at once otherwise), the dense word exchange
+ * (gb_bfs_dist_pack_words / allgather / gb_bfs_dist_unpack_words), then
+ * gb_bfs_dist_dev_apply (stamp, new K, loop exit and cap).  Levels enqueued
+ * after `done` are no-ops.  prefix_cut (rows sorted by column, e.g. the
+ * degree-ordered layout): the push skips each list's entries below the dense
+ * visited prefix, as the single-GPU push does.  Replaces the per-level host loop of
+ * algorithms.py:48-77 on a 1D partition. */
+gb_status gb_bfs_dist_dev_init(gb_ctx* ctx, int64_t* state, int64_t* log, int64_t n, int64_t nnz,
+                               int64_t source, int64_t max_iters, double ratio, int32_t policy,
+                               int64_t* levels, uint32_t* vbm, uint32_t* vprev, uint32_t* fbm,
+                               int32_t* F);
+gb_status gb_bfs_dist_dev_level(gb_ctx* ctx, int64_t* state, int64_t* log,
+                                const gb_csr* rowblock, const gb_csr* colblock, int64_t lo,
+                                int64_t hi, const uint32_t* nonempty_block, int64_t n,
+                                uint32_t* vbm, uint32_t* vprev, const uint32_t* fbm,
+                                uint32_t* xbm, int64_t* levels, const int32_t* F,
+                                int32_t prefix_cut);
+gb_status gb_bfs_dist_dev_apply(gb_ctx* ctx, int64_t* state, int64_t n, const uint32_t* xbm,
+                                uint32_t* vbm, uint32_t* vprev, uint32_t* fbm, int64_t* levels,
+                                int32_t* F);
 /* entries of every row of `a` whose column lies in [lo, hi): CSR with the
  * same row count (out_offsets: nrows+1); pass out_indices = NULL to size. */
 gb_status gb_csr_column_block(gb_ctx* ctx, const gb_csr* a, int64_t lo, int64_t hi,

@@ -180,6 +180,10 @@ SIGNATURES = {
     "gb_bfs_dist_pack_words": (i32, [vp, i64, i64, i64, vp, vp]),
     "gb_bfs_dist_unpack_words": (i32, [vp, i32, i64, vp, vp, vp]),
     "gb_bfs_dist_set_ids": (i32, [vp, i64, i32, i64, vp, vp, vp]),
+    "gb_bfs_dist_dev_init": (i32, [vp, vp, vp, i64, i64, i64, i64, f64, i32, vp, vp, vp, vp, vp]),
+    "gb_bfs_dist_dev_level": (i32, [vp, vp, vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, i64, vp,
+                                    i64, vp, vp, vp, vp, vp, vp, i32]),
+    "gb_bfs_dist_dev_apply": (i32, [vp, vp, i64, vp, vp, vp, vp, vp, vp]),
     "gb_csr_column_block": (i32, [vp, C.POINTER(gb_csr), i64, i64, vp, vp, pi64]),
     "gb_cc_dist_init": (i32, [vp, i64, vp, vp, vp, vp]),
     "gb_cc_dist_hook": (i32, [vp, i32, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, i64, i64, vp,

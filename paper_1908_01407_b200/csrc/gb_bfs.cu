@@ -463,10 +463,12 @@ __device__ __forceinline__ void finalize_body(int64_t n, int64_t depth, uint32_t
     if (w < W) {
       if (xbm) {
         bits = xbm[w];
+        const uint32_t cur = vbm[w] | bits;
         if (bits) {
-          vbm[w] |= bits;
+          vbm[w] = cur;
           vprev[w] |= bits;
         }
+        visited = cur;
       } else {
         const uint32_t cur = vbm[w], old = vprev[w];
         bits = cur & ~old;
@@ -2244,6 +2246,278 @@ gb_status gb_bfs_dist_set_ids(gb_ctx* ctx, int64_t n, int32_t P, int64_t kmax,
                                                                        xbm);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 2);
+  return GB_OK;
+}
+
+// ---- device-resident levels (distributed.bfs_partitioned_device) ---------
+// The same level steps with every scalar the host used to hold -- the
+// frontier size K, the depth, the iteration, the direction -- kept in a
+// per-rank device state: the reference rule is evaluated on the device, the
+// push / pull kernels run or return by the state's mode, and the exchange is
+// the dense allgather of owned word slices (fixed size, so no count has to
+// reach the host).  The host enqueues level after level and only watches a
+// pinned copy of `done` a few levels behind.
+struct DistBfsState {
+  int64_t K;        // frontier size (replicated)
+  int64_t Kpush;    // K when this level pushes, else 0
+  int64_t mode;     // 0 none (finished), 1 push, 2 pull
+  int64_t dnext;    // level stamped on this level's new vertices
+  int64_t it, max_iters, done, Kun, iters;
+  int64_t n, nnz, policy;
+  double ratio;
+  unsigned long long cnt[2];
+  unsigned long long nlong;
+  int64_t xcur;                // dense visited prefix: every vertex below it is visited
+  unsigned long long xnext;    // ... after the level (finalize's atomicMin target)
+};
+static_assert(sizeof(DistBfsState) <= 24 * sizeof(int64_t), "state fits int64[24]");
+
+__global__ void dist_state_init(DistBfsState* st, int64_t n, int64_t nnz, int64_t max_iters,
+                                double ratio, int64_t policy, int64_t* log) {
+  st->K = 1;
+  st->Kpush = 0;
+  st->mode = 0;
+  st->dnext = 2;
+  st->it = 0;
+  st->max_iters = max_iters;
+  st->done = max_iters <= 0;
+  st->Kun = 0;
+  st->iters = 0;
+  st->n = n;
+  st->nnz = nnz;
+  st->policy = policy;
+  st->ratio = ratio;
+  st->cnt[0] = st->cnt[1] = 0;
+  st->nlong = 0;
+  st->xcur = 0;
+  st->xnext = ~0ull;
+  log[0] = 0;
+}
+
+// the reference rule (kernels.py:108-126) on the replicated K; raw log
+// entries (dir, K, estimate) after the count, like gb_bfs_ordered_async's
+__global__ void dist_decide(DistBfsState* st, int64_t* log) {
+  st->nlong = 0;
+  if (st->done) {
+    st->mode = 0;
+    st->Kpush = 0;
+    return;
+  }
+  const double d = st->n ? (double)st->nnz / (double)st->n : 0.0;
+  const int64_t est = (int64_t)rint(d * (double)st->K);  // Python round: half-even
+  int32_t dir = (double)est > (double)st->nnz * st->ratio ? GB_DIR_PULL : GB_DIR_PUSH;
+  if (st->policy == GB_DIR_PUSH) dir = GB_DIR_PUSH;
+  if (st->policy == GB_DIR_PULL) dir = GB_DIR_PULL;
+  const int64_t it = st->it;
+  log[1 + 3 * it] = dir;
+  log[2 + 3 * it] = st->K;
+  log[3 + 3 * it] = est;
+  log[0] = it + 1;
+  st->mode = dir == GB_DIR_PULL ? 2 : 1;
+  st->Kpush = dir == GB_DIR_PULL ? 0 : st->K;
+}
+
+// push over the column block: warp per frontier entry (K from the state),
+// lists longer than kDistLong edges cut into kDistChunk-edge tasks
+constexpr int64_t kDistLong = 4096, kDistChunk = 512;
+struct DistMark {
+  const int32_t* idx;
+  EdgeOn on;
+  uint32_t* vbm;
+  __device__ __forceinline__ void operator()(int64_t p) const {
+    if (!on(p)) return;
+    const int32_t v = __ldg(idx + p);
+    const uint32_t bit = 1u << (v & 31);
+    if (!(ld_probe(vbm + (v >> 5)) & bit)) atomicOr(vbm + (v >> 5), bit);
+  }
+};
+
+// first position of idx[lo, hi) (sorted) holding a column >= key: 32-ary
+// warp search, one coalesced round of probes per factor of 32
+__device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t lo,
+                                                    int64_t hi, int32_t key, int lane) {
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + lane * step;
+    const uint32_t m = __ballot_sync(GB_FULL, p < hi && __ldg(idx + p) < key);
+    if (!m) return lo;
+    const int64_t last = lo + (int64_t)(__popc(m) - 1) * step;  // the last probe below key
+    hi = min(hi, last + step);
+    lo = last + 1;
+  }
+  const int64_t p = lo + lane;
+  return lo + __popc(__ballot_sync(GB_FULL, p < hi && __ldg(idx + p) < key));
+}
+
+// cut: the rows are sorted -- skip each list's entries below the dense
+// visited prefix (the single-GPU push's prefix cut, on the column block)
+__global__ void __launch_bounds__(256)
+dist_push_short(DistBfsState* st, const int32_t* __restrict__ F, const int64_t* __restrict__ off,
+                int32_t* __restrict__ longk, int32_t* __restrict__ longc, DistMark op, int cut) {
+  const int lane = threadIdx.x & 31;
+  const int64_t K = st->Kpush;
+  const int32_t xc = cut ? (int32_t)st->xcur : 0;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = w0; k < K; k += nw) {
+    const int32_t j = F[k];
+    int64_t lo = off[j];
+    const int64_t hi = off[j + 1];
+    if (xc > 0 && lo < hi && __ldg(op.idx + lo) < xc) lo = warp_lower_bound(op.idx, lo, hi, xc, lane);
+    if (hi - lo > kDistLong) {
+      const int64_t nc = (hi - lo + kDistChunk - 1) / kDistChunk;
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(&st->nlong, (unsigned long long)nc);
+      at = __shfl_sync(GB_FULL, at, 0);
+      for (int64_t c = lane; c < nc; c += 32) {
+        longk[at + c] = (int32_t)k;
+        longc[at + c] = (int32_t)c;
+      }
+      continue;
+    }
+    for (int64_t p = lo + lane; p < hi; p += 32) op(p);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+dist_push_long(const DistBfsState* st, const int32_t* __restrict__ longk,
+               const int32_t* __restrict__ longc, const int32_t* __restrict__ F,
+               const int64_t* __restrict__ off, DistMark op, int cut) {
+  const int lane = threadIdx.x & 31;
+  const int64_t L = (int64_t)st->nlong;
+  const int32_t xc = cut ? (int32_t)st->xcur : 0;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = w0; t < L; t += nw) {
+    const int32_t j = F[longk[t]];
+    int64_t base = off[j];
+    const int64_t end = off[j + 1];
+    // the same cut push_short chunked from
+    if (xc > 0 && base < end && __ldg(op.idx + base) < xc)
+      base = warp_lower_bound(op.idx, base, end, xc, lane);
+    const int64_t lo = base + (int64_t)longc[t] * kDistChunk;
+    const int64_t hi = min(end, lo + kDistChunk);
+    for (int64_t p = lo + lane; p < hi; p += 32) op(p);
+  }
+}
+
+__global__ void dist_collect_if(const DistBfsState* st, int64_t w_lo, int64_t w_hi,
+                                const uint32_t* __restrict__ vbm,
+                                const uint32_t* __restrict__ vprev, uint32_t* __restrict__ xbm) {
+  if (st->mode != 1) return;
+  for (int64_t w = w_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < w_hi;
+       w += (int64_t)gridDim.x * blockDim.x)
+    xbm[w] = vbm[w] & ~vprev[w];
+}
+
+__global__ void __launch_bounds__(256)
+dist_pull_if(const DistBfsState* st, int64_t n, const int64_t* __restrict__ off,
+             const int32_t* __restrict__ idx, EdgeOn on, const uint32_t* __restrict__ nonempty,
+             uint32_t* __restrict__ vbm, uint32_t* __restrict__ vprev,
+             const uint32_t* __restrict__ fbm, uint32_t* __restrict__ xbm,
+             int64_t* __restrict__ levels, int32_t* __restrict__ F,
+             unsigned long long* __restrict__ count, int64_t g_lo, int64_t g_hi) {
+  if (st->mode != 2) return;
+  pull_body(n, st->dnext, off, idx, on, nonempty, vbm, vprev, fbm, xbm, levels, F, count, g_lo,
+            g_hi, nullptr);
+}
+
+// after finalize: the new K; the loop cap (the reference stamps the last
+// frontier at the next iteration, which never runs: unstamp it)
+__global__ void dist_advance(DistBfsState* st) {
+  st->Kun = 0;
+  const int64_t K = (int64_t)st->cnt[0];
+  st->cnt[0] = st->cnt[1] = 0;
+  // the dense visited prefix after this level (replicated: finalize scanned
+  // the whole replicated bitmap)
+  if (st->xnext < (unsigned long long)st->n) st->xcur = (int64_t)st->xnext;
+  st->xnext = ~0ull;
+  if (st->done) return;
+  st->K = K;
+  st->it += 1;
+  st->iters = st->it;
+  if (K == 0) {
+    st->done = 1;
+    return;
+  }
+  st->dnext += 1;
+  if (st->it == st->max_iters) {
+    st->Kun = K;
+    st->done = 1;
+  }
+}
+
+
+// ---- device-resident levels: entry points ----------------------------------
+gb_status gb_bfs_dist_dev_init(gb_ctx* ctx, int64_t* state, int64_t* log, int64_t n, int64_t nnz,
+                               int64_t source, int64_t max_iters, double ratio, int32_t policy,
+                               int64_t* levels, uint32_t* vbm, uint32_t* vprev, uint32_t* fbm,
+                               int32_t* F) {
+  GB_TRY(gb_bfs_dist_init(ctx, n, source, levels, vbm, vprev, fbm, F));
+  dist_state_init<<<1, 1, 0, stream_of(ctx)>>>(reinterpret_cast<DistBfsState*>(state), n, nnz,
+                                                max_iters, ratio, policy, log);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 1);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_dev_level(gb_ctx* ctx, int64_t* state, int64_t* log,
+                                const gb_csr* rowblock, const gb_csr* colblock, int64_t lo,
+                                int64_t hi, const uint32_t* nonempty_block, int64_t n,
+                                uint32_t* vbm, uint32_t* vprev, const uint32_t* fbm,
+                                uint32_t* xbm, int64_t* levels, const int32_t* F,
+                                int32_t prefix_cut) {
+  if (lo % 1024) return set_error(ctx, GB_ERR_ARG, "partition start must be a multiple of 1024");
+  auto* st = reinterpret_cast<DistBfsState*>(state);
+  Arena ar(ctx);
+  cudaStream_t s = stream_of(ctx);
+  const int64_t W = (n + 31) / 32;
+  const int64_t ntask = n + colblock->nnz / kDistChunk + 1;
+  int32_t* longk = ar.alloc<int32_t>(ntask);
+  int32_t* longc = ar.alloc<int32_t>(ntask);
+  int32_t* Fp = ar.alloc<int32_t>(hi - lo + 1);  // the pull's own list (unused)
+  unsigned long long* pc = ar.alloc<unsigned long long>(1);
+  GB_ARENA_CHECK(ctx, ar);
+  dist_decide<<<1, 1, 0, s>>>(st, log);
+  GB_CUDA(ctx, cudaMemsetAsync(xbm, 0, sizeof(uint32_t) * W, s));
+  GB_CUDA(ctx, cudaMemsetAsync(pc, 0, sizeof(unsigned long long), s));
+  if (colblock->nnz) {
+    const DistMark op{colblock->indices, EdgeOn{colblock->values, colblock->dtype}, vbm};
+    dist_push_short<<<grid_for(ctx, n * 32, 256, 8), 256, 0, s>>>(st, F, colblock->offsets,
+                                                                 longk, longc, op, prefix_cut);
+    dist_push_long<<<grid_for(ctx, colblock->nnz / 16 + 32, 256, 8), 256, 0, s>>>(
+        st, longk, longc, F, colblock->offsets, op, prefix_cut);
+  }
+  const int64_t w_lo = lo / 32, w_hi = (hi + 31) / 32;
+  if (w_hi > w_lo)
+    dist_collect_if<<<grid_for(ctx, w_hi - w_lo, 256), 256, 0, s>>>(st, w_lo, w_hi, vbm, vprev,
+                                                                    xbm);
+  if (hi > lo && rowblock->nnz) {
+    const EdgeOn on{rowblock->values, rowblock->dtype};
+    const int64_t* off = rowblock->offsets - lo;
+    const uint32_t* ne = nonempty_block - lo / 32;
+    const int64_t g_lo = lo / 1024, g_hi = (hi + 1023) / 1024;
+    dist_pull_if<<<grid_for(ctx, (g_hi - g_lo) * 32, 256, 8), 256, 0, s>>>(
+        st, hi, off, rowblock->indices, on, ne, vbm, vprev, fbm, xbm, levels, Fp, pc, g_lo, g_hi);
+  }
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 7);
+  return GB_OK;
+}
+
+gb_status gb_bfs_dist_dev_apply(gb_ctx* ctx, int64_t* state, int64_t n, const uint32_t* xbm,
+                                uint32_t* vbm, uint32_t* vprev, uint32_t* fbm, int64_t* levels,
+                                int32_t* F) {
+  auto* st = reinterpret_cast<DistBfsState*>(state);
+  cudaStream_t s = stream_of(ctx);
+  const int64_t W = (n + 31) / 32;
+  bfs_finalize<<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, dptr(&st->dnext), vbm, vprev, fbm,
+                                                        pval(levels), F, &st->cnt[0], &st->cnt[1],
+                                                        xbm, &st->xnext);
+  dist_advance<<<1, 1, 0, s>>>(st);
+  bfs_unstamp<<<grid_for(ctx, n, 256, 4), 256, 0, s>>>(dptr(&st->Kun), F, levels);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 3);
   return GB_OK;
 }
 

@@ -129,6 +129,9 @@ class NativeSteps:
         self.F = torch.empty(n, dtype=torch.int32, device=dev)
         self.ids = torch.empty(max(g.hi - g.lo, 1), dtype=torch.int32, device=dev)
         self.count = torch.zeros(1, dtype=torch.int64, device=dev)
+        # rows sorted by column (the degree-ordered layout guarantees it):
+        # the device-resident push may skip the dense visited prefix
+        self.prefix_cut = False
 
     def init(self, source):
         p = _lib.ptr
@@ -184,6 +187,30 @@ class NativeSteps:
 
     def unstamp(self, K):
         self.ctx.call("gb_bfs_dist_unstamp", int(K), _lib.ptr(self.F), _lib.ptr(self.levels))
+
+    # -- device-resident levels (gb_bfs_dist_dev_*): no scalar reaches the host
+    STATE_DONE, STATE_ITERS = 6, 8   # DistBfsState fields read back (int64 slots)
+
+    def dev_init(self, source, max_iters, switch_ratio, policy):
+        g, p = self.g, _lib.ptr
+        self.state = torch.zeros(24, dtype=torch.int64, device=self.levels.device)
+        self.log = torch.zeros(1 + 3 * max(int(max_iters), 1), dtype=torch.int64,
+                               device=self.levels.device)
+        self.ctx.call("gb_bfs_dist_dev_init", p(self.state), p(self.log), g.n, g.nnz, int(source),
+                      int(max_iters), float(switch_ratio), int(policy), p(self.levels), p(self.vbm),
+                      p(self.vprev), p(self.fbm), p(self.F))
+
+    def dev_level(self):
+        g, p = self.g, _lib.ptr
+        self.ctx.call("gb_bfs_dist_dev_level", p(self.state), p(self.log), C.byref(self.rows),
+                      C.byref(self.cols), g.lo, g.hi, p(g.row_nonempty), g.n, p(self.vbm),
+                      p(self.vprev), p(self.fbm), p(self.xbm), p(self.levels), p(self.F),
+                      1 if self.prefix_cut else 0)
+
+    def dev_apply(self):
+        p = _lib.ptr
+        self.ctx.call("gb_bfs_dist_dev_apply", p(self.state), self.g.n, p(self.xbm), p(self.vbm),
+                      p(self.vprev), p(self.fbm), p(self.levels), p(self.F))
 
 
 class FrontierExchange:
@@ -248,6 +275,76 @@ class FrontierExchange:
             steps.set_ids(gathered, counts, kmax)
             self.log.append(("sparse", 4 * kmax))
         return total
+
+
+    def dense(self, steps, g):
+        """The dense exchange alone (fixed size, nothing read back): the
+        device-resident loop's per-level step."""
+        if self._world() == 1:
+            return
+        wb, wmax = self.word_bounds(g, steps.xbm.device)
+        gathered = self._allgather(steps.pack_words(wmax))
+        steps.unpack_words(gathered, wmax, wb)
+        self.log.append(("dense", 4 * wmax))
+
+
+def bfs_partitioned_device(g: BlockGraph, source: int, desc=None, steps=None, exchange=None,
+                           lookahead: int = 1):
+    """bfs_partitioned with the level loop's scalars on the device
+    (gb_bfs_dist_dev_*): the direction rule runs on the device, the push or
+    pull kernel returns at once when the level took the other direction, and
+    the frontier is exchanged as the dense allgather of owned word slices
+    (2 MB over all ranks at s24 -- on NVSwitch a few microseconds, against a
+    host round trip per level for the count-dependent sparse mode).  The host
+    enqueues levels back to back and learns that the traversal ended from a
+    pinned copy of the state's `done` flag, waiting only on the level
+    `lookahead` behind (so every rank stops after the same number of
+    collectives, `lookahead` no-op levels past the end).  Levels and the
+    direction log equal bfs_partitioned's."""
+    if not 0 <= source < g.n:
+        raise IndexError(f"source {source} out of range")
+    desc = desc if desc is not None else Descriptor()
+    steps = steps if steps is not None else NativeSteps(g)
+    exchange = exchange if exchange is not None else FrontierExchange()
+    iters = min(desc.max_niter, g.n + 1)
+    if iters <= 0:
+        # the reference loop runs zero times: nothing is stamped, not even the source
+        steps.init(source)
+        steps.unstamp(1)
+        return steps.levels
+    policy = {Direction.AUTO: _lib.DIR_AUTO, Direction.FORCE_PUSH: _lib.DIR_PUSH,
+              Direction.FORCE_PULL: _lib.DIR_PULL}[desc.direction]
+    steps.dev_init(source, iters, desc.switch_ratio, policy)
+    slots = max(lookahead, 1) + 1
+    flags = torch.zeros((slots, 1), dtype=torch.int64, pin_memory=True)
+    pending = []   # (slot, event) of enqueued levels, oldest first
+    stream = torch.cuda.current_stream(steps.levels.device)
+    for it in range(iters):
+        steps.dev_level()
+        exchange.dense(steps, g)
+        steps.dev_apply()
+        slot = it % slots
+        flags[slot].copy_(steps.state[NativeSteps.STATE_DONE:NativeSteps.STATE_DONE + 1],
+                          non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        pending.append((slot, ev))
+        # deterministic: every rank waits on the same level, so all ranks stop
+        # after the same number of collectives (an event query would let
+        # them diverge)
+        if len(pending) > lookahead:
+            s0, e0 = pending.pop(0)
+            e0.synchronize()
+            if int(flags[s0, 0]):
+                break
+    torch.cuda.current_stream(steps.levels.device).synchronize()
+    n_it = int(steps.state[NativeSteps.STATE_ITERS].item())
+    raw = steps.log[:1 + 3 * n_it].cpu().numpy()
+    for i in range(n_it):
+        d, k, est = int(raw[1 + 3 * i]), int(raw[2 + 3 * i]), int(raw[3 + 3 * i])
+        desc.direction_log.append(DirectionDecision("pull" if d == _lib.DIR_PULL else "push", k,
+                                                    est, g.nnz, g.nnz * desc.switch_ratio))
+    return steps.levels
 
 
 def bfs_partitioned(g: BlockGraph, source: int, desc=None, steps=None, exchange=None):
@@ -383,11 +480,16 @@ class OrderedPartitionedBfs:
     the source mapped in, the replicated levels gathered back to the original
     ids at the end (gb_gather).  Levels and the direction log equal bfs(A)."""
 
-    def __init__(self, A: SparseMatrix, rank: int, world: int, group=None, bounds=None):
+    def __init__(self, A: SparseMatrix, rank: int, world: int, group=None, bounds=None,
+                 loop: str = "device"):
+        if loop not in ("device", "host"):
+            raise ValueError("loop is 'device' (bfs_partitioned_device) or 'host' (bfs_partitioned)")
+        self.loop = loop
         push_o, pull_o, self.rank_t = A.traversal()
         Ar = SparseMatrix._wrap(A.nrows, A.ncols, push_o, pull_o, A.dtype, A._sym)
         self.block = BlockGraph.from_matrix(Ar, rank, world, bounds)
         self.steps = NativeSteps(self.block)
+        self.steps.prefix_cut = True   # traversal() relabels with sorted rows
         self.exchange = FrontierExchange(group)
         self.rank64 = A._rank64()
         self.out = torch.empty(A.nrows, dtype=torch.int64, device=push_o.offsets.device)
@@ -396,25 +498,30 @@ class OrderedPartitionedBfs:
         if not 0 <= source < self.block.n:
             raise IndexError(f"source {source} out of range")
         src = int(self.rank_t[source].item())
-        lv = bfs_partitioned(self.block, src, desc, steps=self.steps, exchange=self.exchange)
+        run = bfs_partitioned_device if self.loop == "device" else bfs_partitioned
+        lv = run(self.block, src, desc, steps=self.steps, exchange=self.exchange)
         n = self.block.n
         _lib.context().call("gb_gather", _lib.dtype_code(np.int64), n, _lib.ptr(self.rank64), n,
                             _lib.ptr(lv), _lib.ptr(self.out))
         return self.out
 
 
-def bfs(A_or_block, source, desc=None, group=None, ordered=True):
+def bfs(A_or_block, source, desc=None, group=None, ordered=True, loop="device"):
     """Public entry: bfs on this rank's block; returns the (replicated) level Vector.
     A SparseMatrix with a column orientation is partitioned over its
-    degree-ordered layout unless ``ordered=False``."""
+    degree-ordered layout unless ``ordered=False``.  ``loop="device"`` keeps
+    the level loop's scalars on the device (dense exchange every level, no
+    host read per level); ``loop="host"`` is the count-driven loop with the
+    dense / sparse exchange."""
     g = A_or_block
     if isinstance(A_or_block, SparseMatrix):
         import torch.distributed as dist
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         if ordered and A_or_block.traversal() is not None:
-            run = OrderedPartitionedBfs(A_or_block, rank, world, group)
+            run = OrderedPartitionedBfs(A_or_block, rank, world, group, loop=loop)
             return Vector._wrap(A_or_block.nrows, None, run(source, desc).clone(), 0, np.int64)
         g = BlockGraph.from_matrix(A_or_block, rank, world)
-    levels = bfs_partitioned(g, source, desc, exchange=FrontierExchange(group))
+    run = bfs_partitioned_device if loop == "device" else bfs_partitioned
+    levels = run(g, source, desc, exchange=FrontierExchange(group))
     return Vector._wrap(g.n, None, levels, 0, np.int64)

@@ -89,6 +89,134 @@ def test_partitioned_equals_single(scale, P):
             [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
 
 
+def lockstep_bfs_device(A, P, source, desc, extra=1, cut=False):
+    """bfs_partitioned_device's protocol for P simulated ranks: every level
+    the device-resident step, the dense word exchange (rank-order
+    concatenation), the device-resident apply; `extra` no-op levels past the
+    end, as the product loop enqueues them."""
+    from paper_1908_01407_b200 import _lib
+    from paper_1908_01407_b200.distributed import (BlockGraph, FrontierExchange, NativeSteps,
+                                                   partition_bounds)
+    from paper_1908_01407_b200.kernels import DirectionDecision
+    bounds = partition_bounds(A._csr.offsets.cpu().numpy(), P)
+    ranks = [NativeSteps(BlockGraph.from_matrix(A, r, P, bounds)) for r in range(P)]
+    for st in ranks:
+        st.prefix_cut = cut
+    g = ranks[0].g
+    iters = min(desc.max_niter, g.n + 1)
+    policy = {"auto": _lib.DIR_AUTO, "force-push": _lib.DIR_PUSH,
+              "force-pull": _lib.DIR_PULL}[desc.direction.value]
+    for st in ranks:
+        st.dev_init(source, iters, desc.switch_ratio, policy)
+    wb, wmax = FrontierExchange().word_bounds(g, ranks[0].levels.device)
+    left = None
+    for it in range(iters):
+        for st in ranks:
+            st.dev_level()
+        gathered = torch.cat([st.pack_words(wmax).clone() for st in ranks])
+        for st in ranks:
+            st.unpack_words(gathered, wmax, wb)
+            st.dev_apply()
+        done = {int(st.state[NativeSteps.STATE_DONE]) for st in ranks}
+        assert len(done) == 1
+        if left is None and done == {1}:
+            left = extra
+        if left is not None:
+            if left == 0:
+                break
+            left -= 1
+    states = [st.state.cpu().numpy() for st in ranks]
+    logs = [st.log.cpu().numpy() for st in ranks]
+    for a, b in zip(states[1:], logs[1:]):
+        assert np.array_equal(a, states[0]) and np.array_equal(b, logs[0])
+    n_it = int(states[0][NativeSteps.STATE_ITERS])
+    raw = logs[0]
+    for i in range(n_it):
+        desc.direction_log.append(DirectionDecision(
+            "pull" if raw[1 + 3 * i] == _lib.DIR_PULL else "push", int(raw[2 + 3 * i]),
+            int(raw[3 + 3 * i]), g.nnz, g.nnz * desc.switch_ratio))
+    out = [st.levels.cpu().numpy() for st in ranks]
+    for o in out[1:]:
+        assert np.array_equal(o, out[0])
+    return out[0]
+
+
+@pytest.mark.parametrize("scale", [12, 16, 20])
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_device_resident_partitioned_equals_single(scale, P):
+    """The device-resident level loop (direction rule, K, depth and exit on
+    the device; dense exchange only): levels, decisions and estimates equal
+    the single-GPU fused BFS, with no-op levels past the end."""
+    import paper_1908_01407_b200 as gb
+    A = gb.io.rmat_matrix(scale)
+    for src, extra, cut in ((0, 1, False), (7, 3, False), (0, 1, True), (7, 2, True)):
+        if True:
+            d1, d2 = gb.Descriptor(), gb.Descriptor()
+            want = gb.bfs(A, src, desc=d1).values
+            got = lockstep_bfs_device(A, P, src, d2, extra, cut)
+            assert np.array_equal(got, want)
+            assert [(x.chosen, x.frontier_nvals, x.estimated_frontier_edges)
+                    for x in d1.direction_log] == \
+                [(x.chosen, x.frontier_nvals, x.estimated_frontier_edges)
+                 for x in d2.direction_log]
+
+
+@pytest.mark.parametrize("cap", [0, 1, 2, 3])
+@pytest.mark.parametrize("direction", ["auto", "force-push", "force-pull"])
+def test_device_resident_partitioned_caps_and_policies(cap, direction):
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200 import distributed
+    A = gb.io.rmat_matrix(14)
+    dir_ = gb.Direction(direction)
+    for P in (1, 3):
+        d1 = gb.Descriptor(max_niter=cap, direction=dir_)
+        d2 = gb.Descriptor(max_niter=cap, direction=dir_)
+        want = gb.bfs(A, 5, desc=d1).values
+        if cap == 0:
+            g = distributed.BlockGraph.from_matrix(A, 0, 1)
+            got = distributed.bfs_partitioned_device(g, 5, d2).cpu().numpy()
+        else:
+            got = lockstep_bfs_device(A, P, 5, d2)
+        assert np.array_equal(got, want)
+        assert [(x.chosen, x.frontier_nvals) for x in d1.direction_log] == \
+            [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_device_resident_ordered_layout_prefix_cut(P):
+    """The degree-ordered partition (rank 0 owns the hubs) with the push's
+    prefix cut: levels by original id and the trace equal the single GPU's."""
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200.containers import SparseMatrix
+    A = gb.io.rmat_matrix(18)
+    push_o, pull_o, rank = A.traversal()
+    Ar = SparseMatrix._wrap(A.nrows, A.ncols, push_o, pull_o, A.dtype, A._sym)
+    rank = rank.long().cpu().numpy()
+    for src in (0, 5, 100000):
+        d1, d2 = gb.Descriptor(), gb.Descriptor()
+        want = gb.bfs(A, src, desc=d1).values
+        got_r = lockstep_bfs_device(Ar, P, int(rank[src]), d2, cut=True)
+        assert np.array_equal(got_r[rank], want)
+        assert [(x.chosen, x.frontier_nvals) for x in d1.direction_log] == \
+            [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
+
+
+def test_device_resident_entry_single_rank():
+    """The product loop itself at world size 1 (the exchange is local)."""
+    import paper_1908_01407_b200 as gb
+    from paper_1908_01407_b200 import distributed
+    A = gb.io.rmat_matrix(16)
+    g = distributed.BlockGraph.from_matrix(A, 0, 1)
+    for src in (0, 3, 60000):
+        for look in (1, 2, 4):
+            d1, d2 = gb.Descriptor(), gb.Descriptor()
+            want = gb.bfs(A, src, desc=d1).values
+            got = distributed.bfs_partitioned_device(g, src, d2, lookahead=look).cpu().numpy()
+            assert np.array_equal(got, want)
+            assert [(x.chosen, x.frontier_nvals) for x in d1.direction_log] == \
+                [(x.chosen, x.frontier_nvals) for x in d2.direction_log]
+
+
 def lockstep_cc(A, P, desc, sparsify=True):
     from paper_1908_01407_b200.distributed import BlockGraph, NativeCCSteps, partition_bounds
     from paper_1908_01407_b200.kernels import DirectionDecision, direction_rule
@@ -196,7 +324,7 @@ def _gloo_worker(rank, world, port_, scale, results):
     for ordered in (False, True):
         d = gb.Descriptor()
         if ordered:
-            run = gbd.OrderedPartitionedBfs(A, rank, world)
+            run = gbd.OrderedPartitionedBfs(A, rank, world, loop="host")
             lv = run(0, d).cpu().numpy()
             log = run.exchange.log
         else:
@@ -205,6 +333,14 @@ def _gloo_worker(rank, world, port_, scale, results):
             lv = gbd.bfs_partitioned(g, 0, d, exchange=ex).cpu().numpy()
             log = ex.log
         out[ordered] = (lv, [(x.chosen, x.frontier_nvals) for x in d.direction_log], list(log))
+    d = gb.Descriptor()
+    g = gbd.BlockGraph.from_matrix(A, rank, world)
+    ex = gbd.FrontierExchange()
+    lv = gbd.bfs_partitioned_device(g, 0, d, exchange=ex).cpu().numpy()
+    out["device"] = (lv, [(x.chosen, x.frontier_nvals) for x in d.direction_log], list(ex.log))
+    d = gb.Descriptor()
+    lv = gbd.OrderedPartitionedBfs(A, rank, world)(0, d).cpu().numpy()   # default: device loop
+    out["device_ordered"] = (lv, [(x.chosen, x.frontier_nvals) for x in d.direction_log])
     d = gb.Descriptor()
     lab = gbd.connected_components(A, d).values
     out["cc"] = lab
@@ -236,4 +372,9 @@ def test_two_processes_gloo_native_steps(scale):
             assert np.array_equal(lv, want)
             assert tr == trace
             assert {m for m, _b in log} == {"dense", "sparse"}
+        lv, tr, log = results[r]["device"]
+        assert np.array_equal(lv, want) and tr == trace
+        assert {m for m, _b in log} == {"dense"} and len(log) == len(trace) + 1
+        lv, tr = results[r]["device_ordered"]
+        assert np.array_equal(lv, want) and tr == trace
         assert np.array_equal(results[r]["cc"], want_cc)
