@@ -2319,7 +2319,10 @@ __global__ void dist_decide(DistBfsState* st, int64_t* log) {
 
 // push over the column block: warp per frontier entry (K from the state),
 // lists longer than kDistLong edges cut into kDistChunk-edge tasks
-constexpr int64_t kDistLong = 4096, kDistChunk = 512;
+#ifndef GB_DIST_LONG
+#define GB_DIST_LONG 4096
+#endif
+constexpr int64_t kDistLong = GB_DIST_LONG, kDistChunk = 512;
 struct DistMark {
   const int32_t* idx;
   EdgeOn on;
