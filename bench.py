@@ -31,6 +31,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 METRIC = "BFS GTEPS on RMAT scale-24"
+# B200 nominal HBM3e bandwidth (SURVEY §8(d) asks for the fraction of it too)
+NOMINAL_HBM_GBS = 8000.0
 
 
 def parse():
@@ -253,6 +255,7 @@ def masked_spmv(gb, A, ctx, peak, peak_src, reps=10, density=0.5, graph="rmat"):
                       "row_tiles (edge-balanced)": round(tiles_ms, 4)},
             "achieved": round(achieved, 1), "peak": peak,
             "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
+            "frac_vs_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
             "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4),
             "call_ms": round(call_ms, 4),
             "gather_replay": {
@@ -542,6 +545,7 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": "bfs_expand_warp (push SpMSpV, level %d)" % (lvl + 1),
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                "frac_vs_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
                 "traffic": committed_traffic("bfs_expand_warp"),
                 "bytes_alg": int(bytes_alg), "launch_ms": round(t_ms, 4),
                 "frontier": int(k), "flops": flops, "edges_expanded": edges,
