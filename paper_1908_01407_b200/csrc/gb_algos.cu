@@ -685,7 +685,10 @@ __global__ void widen_i32(int64_t n, const int* __restrict__ a, long long* __res
 // from a device count: a warp per frontier entry, entries longer than
 // kLongPush edges cut into 512-edge tasks for a second pass.
 // ===========================================================================
-constexpr int64_t kLongPush = 4096;
+#ifndef GB_LONG_PUSH
+#define GB_LONG_PUSH 1024  // A/B: 4096 / 1024 / 512 / 256 -> SSSP s20 1.63 / 1.56 / 1.57 / 1.60 ms, CC equal
+#endif
+constexpr int64_t kLongPush = GB_LONG_PUSH;
 enum { kLoopGraph = 0, kLoopHost = 1 };
 static int g_loop_engine = -1;
 static int loop_engine() {
