@@ -173,13 +173,17 @@ __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restri
                                                    int32_t* __restrict__ F,
                                                    double* __restrict__ Fv,
                                                    double* __restrict__ fvd,
-                                                   unsigned long long* __restrict__ count);
+                                                   unsigned long long* __restrict__ count,
+                                                   const int64_t* __restrict__ off,
+                                                   unsigned long long* __restrict__ sumdeg);
 
 __global__ void sssp_finalize(int64_t n, uint32_t* __restrict__ changed,
                               const double* __restrict__ dist, int32_t* __restrict__ F,
                               double* __restrict__ Fv, double* __restrict__ fvd,
-                              unsigned long long* __restrict__ count) {
-  sssp_finalize_body(n, changed, dist, F, Fv, fvd, count);
+                              unsigned long long* __restrict__ count,
+                              const int64_t* __restrict__ off,
+                              unsigned long long* __restrict__ sumdeg) {
+  sssp_finalize_body(n, changed, dist, F, Fv, fvd, count, off, sumdeg);
 }
 
 __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restrict__ changed,
@@ -187,14 +191,23 @@ __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restri
                                                    int32_t* __restrict__ F,
                                                    double* __restrict__ Fv,
                                                    double* __restrict__ fvd,
-                                                   unsigned long long* __restrict__ count) {
+                                                   unsigned long long* __restrict__ count,
+                                                   const int64_t* __restrict__ off,
+                                                   unsigned long long* __restrict__ sumdeg) {
+  // off / sumdeg: also total the new frontier's out-degrees (the edges a
+  // push of it would relax)
   const int64_t W = (n + 31) / 32;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t bits = changed[w];
-    if (bits) changed[w] = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t wb = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); wb < W; wb += stride) {
+    const int64_t w = wb + (threadIdx.x & 31);
+    uint32_t bits = 0;
+    if (w < W) {
+      bits = changed[w];
+      if (bits) changed[w] = 0;
+    }
     const int c = __popc(bits);
     long long slot = warp_reserve(count, c);
+    unsigned long long deg = 0;
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
@@ -202,7 +215,12 @@ __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restri
       F[slot] = (int32_t)v;
       Fv[slot] = dist[v];
       fvd[v] = dist[v];
+      if (off) deg += (unsigned long long)(off[v + 1] - off[v]);
       ++slot;
+    }
+    if (sumdeg) {
+      deg = warp_sum_ll((long long)deg);
+      if ((threadIdx.x & 31) == 0 && deg) atomicAdd(sumdeg, deg);
     }
   }
 }
@@ -1300,12 +1318,27 @@ struct SsspState {
   int64_t max_iters, source;
   int64_t* log;
   double* dist;
-  int32_t policy, pad_;
+  int32_t policy, has_pull;
+  double pull_share;  // a push level relaxing more than this share of nnz runs as the pull
   // loop
   int64_t it, K, reached, succ_last, iters;
   unsigned long long cnt[2];  // new frontier, newly reached
   unsigned long long nlong;
+  unsigned long long sumdeg;  // out-degrees of the frontier (finalize)
+  int64_t npull;              // levels run by the pull branch (launch accounting)
 };
+
+// A push level whose frontier's out-degrees exceed this share of the stored
+// edges runs as the pull (GB_SSSP_PULL_SHARE; s20: the level after the
+// source's pushes 64,602 vertices with 22 M out-edges, 70 % of nnz)
+static double sssp_pull_share() {
+  static double v = -1.0;
+  if (v < 0) {
+    const char* e = getenv("GB_SSSP_PULL_SHARE");
+    v = e ? atof(e) : 0.3;
+  }
+  return v;
+}
 
 struct SsspPushOp {
   const int32_t* idx;
@@ -1341,11 +1374,18 @@ __global__ void sssp_init_g(int64_t n, const SsspState* __restrict__ st, double*
   }
 }
 
+// The logged decision is the reference rule's; a push whose frontier would
+// relax more than pull_share of all stored edges runs as the pull -- the same
+// min over the same candidates w + d(u), so the same distances.
 __device__ __forceinline__ unsigned sssp_branch(SsspState* st, int64_t n, int64_t nnz) {
   const int32_t dir = log_decision(st->log, st->it, nnz, n, st->K, st->ratio, st->policy);
   st->cnt[0] = 0;
   st->nlong = 0;
-  return dir == GB_DIR_PULL ? 0u : (st->K > 0 ? 1u : 2u);
+  const bool heavy = st->has_pull && (double)st->sumdeg > st->pull_share * (double)nnz;
+  st->sumdeg = 0;
+  const unsigned b = dir == GB_DIR_PULL || (st->K > 0 && heavy) ? 0u : (st->K > 0 ? 1u : 2u);
+  st->npull += b == 0;
+  return b;
 }
 
 __global__ void sssp_start_g(SsspState* st, int64_t n, int64_t nnz,
@@ -1356,6 +1396,8 @@ __global__ void sssp_start_g(SsspState* st, int64_t n, int64_t nnz,
   st->succ_last = -1;
   st->iters = 0;
   st->cnt[0] = st->cnt[1] = 0;
+  st->sumdeg = 0;
+  st->npull = 0;
   const bool run = st->max_iters > 0;
   const unsigned dir = run ? sssp_branch(st, n, nnz) : 2u;
   cudaGraphSetConditional(h_loop, run ? 1u : 0u);
@@ -1391,8 +1433,8 @@ __global__ void sssp_pull_apply_g(int64_t n, long long* __restrict__ cand, SsspS
 
 __global__ void sssp_finalize_g(int64_t n, uint32_t* __restrict__ changed, SsspState* st,
                                 int32_t* __restrict__ F, double* __restrict__ Fv,
-                                double* __restrict__ fvd) {
-  sssp_finalize_body(n, changed, st->dist, F, Fv, fvd, &st->cnt[0]);
+                                double* __restrict__ fvd, const int64_t* __restrict__ off) {
+  sssp_finalize_body(n, changed, st->dist, F, Fv, fvd, &st->cnt[0], off, &st->sumdeg);
 }
 
 __global__ void sssp_step_g(SsspState* st, int64_t n, int64_t nnz,
@@ -1479,7 +1521,7 @@ static cudaError_t sssp_graph_build(gb_ctx* ctx, SsspGraph* G) {
       }));
       reset_fvd_g<<<grid_for(ctx, n, 256), 256, 0, b>>>(G->st, G->F, G->fvd);
       sssp_finalize_g<<<grid_for(ctx, W, 256), 256, 0, b>>>(n, G->changed, G->st, G->F, G->Fv,
-                                                            G->fvd);
+                                                            G->fvd, G->push.offsets);
       sssp_step_g<<<1, 1, 0, b>>>(G->st, n, nnz, h_loop, h_dir);
       return cudaGetLastError();
     });
@@ -1560,6 +1602,8 @@ static gb_status sssp_graph(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
   h.log = dlog;
   h.dist = dist;
   h.policy = policy;
+  h.has_pull = pull != nullptr;
+  h.pull_share = sssp_pull_share();
   GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(SsspState, it), cudaMemcpyHostToDevice, s));
   GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
   int64_t iters = 0;
@@ -1619,10 +1663,10 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
   int32_t* F = ar.alloc<int32_t>(n);
   double* Fv = ar.alloc<double>(n);
   double* fvd = ar.alloc<double>(n);
-  unsigned long long* cnt = ar.alloc<unsigned long long>(2);  // [frontier, reached]
+  unsigned long long* cnt = ar.alloc<unsigned long long>(3);  // [frontier, reached, out-degrees]
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cudaMemsetAsync(changed, 0, sizeof(uint32_t) * W, s));
-  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
+  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 24, s));
   sssp_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, dist, fvd, source, F, Fv);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 3);
@@ -1631,7 +1675,7 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
   GB_CUDA(ctx, cudaMemcpyAsync(fvd + source, &zero, 8, cudaMemcpyHostToDevice, s));
   RowTilesPlan pull_plan;    // built on the first pull iteration
   long long* cand = nullptr;  // pull candidates (+inf bits between iterations)
-  int64_t K = 1, reached = 1, succ_last = -1, iters = 0;
+  int64_t K = 1, reached = 1, succ_last = -1, iters = 0, sumdeg = 0;
   const double push_iso = push->iso_f64, pull_iso = pull ? pull->iso_f64 : 0.0;
   for (int64_t it = 0; it < max_iters; ++it) {
     int64_t est = 0;
@@ -1641,7 +1685,9 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
     log_est[it] = est;
     iters = it + 1;
     GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 8, s));
-    if (dir == GB_DIR_PULL) {
+    // a heavy push runs as the pull (same candidates, same minima)
+    const bool heavy = pull && K > 0 && (double)sumdeg > sssp_pull_share() * (double)push->nnz;
+    if (dir == GB_DIR_PULL || heavy) {
       if (!pull) return set_error(ctx, GB_ERR_FORMAT, "column-oriented storage missing");
       const int ps = prof_begin(ctx, PROF_SSSP, K);
       if (!pull_plan.nz_rows) {
@@ -1668,14 +1714,16 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
       count_launch(ctx, 5);
     }
     reset_fvd<<<grid_for(ctx, K > 0 ? K : 1, 256), 256, 0, s>>>(K, F, fvd);
-    sssp_finalize<<<grid_for(ctx, W, 256), 256, 0, s>>>(n, changed, dist, F, Fv, fvd, cnt);
+    sssp_finalize<<<grid_for(ctx, W, 256), 256, 0, s>>>(n, changed, dist, F, Fv, fvd, cnt,
+                                                         push->offsets, cnt + 2);
     GB_LAUNCH_CHECK(ctx);
     count_launch(ctx, 2);
-    int64_t h[2];
-    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 2));
+    int64_t h[3];
+    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 3));
     K = h[0];
     reached += h[1];
-    GB_CUDA(ctx, cudaMemsetAsync(cnt + 1, 0, 8, s));
+    sumdeg = h[2];
+    GB_CUDA(ctx, cudaMemsetAsync(cnt + 1, 0, 16, s));
     if (cb) cb(it, user);
     // algorithms.py:114-118: count of finite distances stable and no frontier
     if (reached == succ_last && K == 0) break;
