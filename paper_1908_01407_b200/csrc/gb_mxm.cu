@@ -328,6 +328,15 @@ __global__ void tc_dense_rows(int64_t n, int32_t dbase, int32_t W, const int64_t
   }
 }
 
+// U(r)'s entries below the bitmap (low ranks) go to a per-warp open-address
+// hash set when there are at most kTcLoSlots / 2 of them; the keys that miss
+// the bitmap then probe it in shared memory instead of binary-searching r's
+// adjacency in global memory (a divergent chain of dependent loads).
+constexpr int kTcLoSlots = 128;
+__device__ __forceinline__ uint32_t tc_hash(int32_t v) {
+  return ((uint32_t)v * 2654435761u) >> 25;  // 7 bits: kTcLoSlots
+}
+
 // branchless 32-bit lower bound of vertex u in the sorted list nb[0, len)
 __device__ __forceinline__ int tc_in_adjacency(const int32_t* __restrict__ nb, int len, int32_t u) {
   const int32_t* b = nb;
@@ -346,13 +355,16 @@ tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict_
          const int32_t* __restrict__ order, int32_t dbase, int32_t W,
          const uint32_t* __restrict__ dense, unsigned long long* __restrict__ total) {
   __shared__ uint32_t s_bm[8][kTcWords];
+  __shared__ int32_t s_lo[8][kTcLoSlots];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int32_t base = n > kTcTopBits ? (int32_t)(n - kTcTopBits) : 0;
   const int boff = (dbase - base) >> 5;  // word of rank dbase in the row bitmap
   uint32_t* bm = s_bm[wid];
+  int32_t* lo_set = s_lo[wid];
   for (int q = lane; q < kTcWords; q += 32) bm[q] = 0;
+  for (int q = lane; q < kTcLoSlots; q += 32) lo_set[q] = -1;
   __syncwarp();
   long long c = 0;
   for (int64_t r = w0; r < n; r += nw) {
@@ -360,9 +372,22 @@ tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict_
     const int64_t len = hi - lo;
     if (len < 2) continue;
     const int32_t* row = uidx + lo;
-    for (int64_t q = lane; q < len; q += 32) {
-      const int32_t v = row[q] - base;
-      if (v >= 0) atomicOr(&bm[v >> 5], 1u << (v & 31));
+    int nlow = 0;  // entries of U(r) below the bitmap (warp-uniform count)
+    for (int64_t q0 = 0; q0 < len; q0 += 32) {
+      const int64_t q = q0 + lane;
+      const int32_t v = q < len ? row[q] - base : 0;
+      if (q < len && v >= 0) atomicOr(&bm[v >> 5], 1u << (v & 31));
+      nlow += __popc(__ballot_sync(GB_FULL, q < len && v < 0));
+    }
+    // few of them: a shared hash set answers the keys below the bitmap
+    const bool lo_hashed = nlow > 0 && nlow <= kTcLoSlots / 2;
+    if (lo_hashed) {
+      for (int64_t q = lane; q < len; q += 32) {
+        const int32_t v = row[q];
+        if (v >= base) continue;
+        uint32_t h = tc_hash(v);
+        while (atomicCAS(&lo_set[h], -1, v) != -1) h = (h + 1) & (kTcLoSlots - 1);
+      }
     }
     __syncwarp();
     const int ilen = (int)len;
@@ -431,10 +456,16 @@ tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict_
           for (int u = 0; u < kTcKeys; ++u) {
             if (key[u] < 0) continue;
             const int32_t v = key[u] - base;
-            if (v >= 0)
+            if (v >= 0) {
               cr += (bm[v >> 5] >> (v & 31)) & 1u;
-            else
+            } else if (lo_hashed) {
+              uint32_t h = tc_hash(key[u]);
+              int32_t e;
+              while ((e = lo_set[h]) != -1 && e != key[u]) h = (h + 1) & (kTcLoSlots - 1);
+              cr += e == key[u];
+            } else if (nlow > 0) {
               cr += tc_in_adjacency(nb, nlen, order[key[u]]);
+            }
           }
         }
       }
@@ -445,6 +476,8 @@ tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict_
       const int32_t v = row[q] - base;
       if (v >= 0) bm[v >> 5] = 0;
     }
+    if (lo_hashed)
+      for (int q = lane; q < kTcLoSlots; q += 32) lo_set[q] = -1;
     __syncwarp();
   }
   c = warp_sum_ll(c);
