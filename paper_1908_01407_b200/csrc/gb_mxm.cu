@@ -160,12 +160,11 @@ __global__ void tc_rank(int64_t n, const int32_t* __restrict__ order, int32_t* _
 constexpr int kTcLong = GB_TC_LONG;
 
 // Tile plan of the long rows: tstart[i] = first tile of rank first + i,
-// meta = {first, tiles}; zeroes the long rows' counters and fill cursors.
+// meta = {first, tiles}; zeroes the long rows' lengths.
 // One block; the degrees arrive sorted ascending.
 __global__ void __launch_bounds__(1024)
 tc_long_plan(int64_t n, const uint32_t* __restrict__ deg_sorted, int64_t* __restrict__ tstart,
-             int64_t* __restrict__ meta, unsigned long long* __restrict__ cursor,
-             int64_t* __restrict__ ucnt) {
+             int64_t* __restrict__ meta, int64_t* __restrict__ ulen) {
   typedef cub::BlockScan<int64_t, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int64_t s_first, s_carry;
@@ -187,8 +186,7 @@ tc_long_plan(int64_t n, const uint32_t* __restrict__ deg_sorted, int64_t* __rest
     Scan(tmp).ExclusiveSum(t, x);
     if (i < nlong) {
       tstart[i] = s_carry + x;
-      cursor[i] = 0;
-      ucnt[first + i] = 0;
+      ulen[first + i] = 0;  // the long rows' tiles reserve their slices on it
     }
     __syncthreads();
     if (threadIdx.x == 1023) s_carry += x + t;
@@ -198,7 +196,6 @@ tc_long_plan(int64_t n, const uint32_t* __restrict__ deg_sorted, int64_t* __rest
     tstart[nlong] = s_carry;
     meta[0] = first;
     meta[1] = s_carry;
-    ucnt[n] = 0;
   }
 }
 
@@ -213,39 +210,10 @@ __device__ __forceinline__ int64_t tc_tile(int64_t g, const int64_t* __restrict_
   return lo;
 }
 
-__global__ void tc_upper_count(int64_t n, const int64_t* __restrict__ off,
-                               const int32_t* __restrict__ idx, const int32_t* __restrict__ order,
-                               const int32_t* __restrict__ rank, const int64_t* __restrict__ tstart,
-                               const int64_t* __restrict__ meta, int64_t* __restrict__ ucnt) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t first = meta[0], ntiles = meta[1], nlong = n - first;
-  for (int64_t r = w0; r < first; r += nw) {
-    const int32_t v = order[r];
-    long long c = 0;
-    for (int64_t p = off[v] + lane; p < off[v + 1]; p += 32) c += rank[idx[p]] > r;
-    c = warp_sum_ll(c);
-    if (lane == 0) ucnt[r] = c;
-  }
-  // long rows: tile partial counts onto the zeros tc_long_plan wrote
-  for (int64_t g = w0; g < ntiles; g += nw) {
-    const int64_t i = tc_tile(g, tstart, nlong);
-    const int64_t r = first + i;
-    const int32_t v = order[r];
-    const int64_t p0 = off[v] + (g - tstart[i]) * kTcLong;
-    const int64_t p1 = min(p0 + kTcLong, off[v + 1]);
-    long long c = 0;
-    for (int64_t p = p0 + lane; p < p1; p += 32) c += rank[idx[p]] > r;
-    c = warp_sum_ll(c);
-    if (lane == 0 && c) atomicAdd((unsigned long long*)&ucnt[r], (unsigned long long)c);
-  }
-}
-
-__device__ __forceinline__ void tc_fill_range(int64_t p0, int64_t p1, int32_t r,
-                                              const int32_t* __restrict__ idx,
-                                              const int32_t* __restrict__ rank,
-                                              int32_t* __restrict__ out_row, int lane) {
+__device__ __forceinline__ int64_t tc_fill_range(int64_t p0, int64_t p1, int32_t r,
+                                                 const int32_t* __restrict__ idx,
+                                                 const int32_t* __restrict__ rank,
+                                                 int32_t* __restrict__ out_row, int lane) {
   int64_t out = 0;
   for (int64_t base = p0; base < p1; base += 32) {
     const int64_t p = base + lane;
@@ -256,21 +224,29 @@ __device__ __forceinline__ void tc_fill_range(int64_t p0, int64_t p1, int32_t r,
     if (keep) out_row[out + __popc(bal & ((1u << lane) - 1u))] = rj;
     out += __popc(bal);
   }
+  return out;
 }
 
-__global__ void tc_upper_fill(int64_t n, const int64_t* __restrict__ off,
-                              const int32_t* __restrict__ idx, const int32_t* __restrict__ order,
-                              const int32_t* __restrict__ rank, const int64_t* __restrict__ tstart,
-                              const int64_t* __restrict__ meta, const int64_t* __restrict__ uoff,
-                              unsigned long long* __restrict__ cursor,
-                              int32_t* __restrict__ uidx) {
+// One pass: U(r) is written where vertex order[r]'s adjacency starts in the
+// matrix (it holds at most deg entries), so no count pass, scan or read-back
+// of the total is needed; ustart / ulen locate each row.
+__global__ void tc_upper_build(int64_t n, const int64_t* __restrict__ off,
+                               const int32_t* __restrict__ idx, const int32_t* __restrict__ order,
+                               const int32_t* __restrict__ rank, const int64_t* __restrict__ tstart,
+                               const int64_t* __restrict__ meta, int64_t* __restrict__ ustart,
+                               int64_t* __restrict__ ulen, int32_t* __restrict__ uidx) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t first = meta[0], ntiles = meta[1], nlong = n - first;
   for (int64_t r = w0; r < first; r += nw) {
     const int32_t v = order[r];
-    tc_fill_range(off[v], off[v + 1], (int32_t)r, idx, rank, uidx + uoff[r], lane);
+    const int64_t p0 = off[v];
+    const int64_t c = tc_fill_range(p0, off[v + 1], (int32_t)r, idx, rank, uidx + p0, lane);
+    if (lane == 0) {
+      ustart[r] = p0;
+      ulen[r] = c;
+    }
   }
   for (int64_t g = w0; g < ntiles; g += nw) {
     const int64_t i = tc_tile(g, tstart, nlong);
@@ -282,9 +258,13 @@ __global__ void tc_upper_fill(int64_t n, const int64_t* __restrict__ off,
     for (int64_t p = p0 + lane; p < p1; p += 32) c += rank[idx[p]] > r;
     c = warp_sum_ll(c);
     unsigned long long at = 0;
-    if (lane == 0 && c) at = atomicAdd(&cursor[i], (unsigned long long)c);
+    if (lane == 0) {
+      if (g == tstart[i]) ustart[r] = off[v];
+      if (c) at = atomicAdd(reinterpret_cast<unsigned long long*>(ulen + r),
+                            (unsigned long long)c);
+    }
     at = __shfl_sync(GB_FULL, at, 0);
-    if (c) tc_fill_range(p0, p1, (int32_t)r, idx, rank, uidx + uoff[r] + at, lane);
+    if (c) tc_fill_range(p0, p1, (int32_t)r, idx, rank, uidx + off[v] + at, lane);
   }
 }
 
@@ -314,14 +294,15 @@ constexpr int kTcDense = GB_TC_DENSE;
 #endif
 constexpr int kTcKeys = GB_TC_KEYS;
 
-__global__ void tc_dense_rows(int64_t n, int32_t dbase, int32_t W, const int64_t* __restrict__ uoff,
-                              const int32_t* __restrict__ uidx, uint32_t* __restrict__ dense) {
+__global__ void tc_dense_rows(int64_t n, int32_t dbase, int32_t W, const int64_t* __restrict__ ustart,
+                              const int64_t* __restrict__ ulen, const int32_t* __restrict__ uidx,
+                              uint32_t* __restrict__ dense) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t j = dbase + w0; j < n; j += nw) {
     uint32_t* row = dense + (j - dbase) * W;
-    for (int64_t q = uoff[j] + lane; q < uoff[j + 1]; q += 32) {
+    for (int64_t q = ustart[j] + lane; q < ustart[j] + ulen[j]; q += 32) {
       const int32_t k = uidx[q] - dbase;
       atomicOr(&row[k >> 5], 1u << (k & 31));
     }
@@ -350,7 +331,8 @@ __device__ __forceinline__ int tc_in_adjacency(const int32_t* __restrict__ nb, i
 
 // warp per upper row r: count |U(r) & U(j)| for every j in U(r)
 __global__ void __launch_bounds__(256)
-tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict__ uidx,
+tc_count(int64_t n, const int64_t* __restrict__ ustart, const int64_t* __restrict__ ulen,
+         const int32_t* __restrict__ uidx,
          const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
          const int32_t* __restrict__ order, int32_t dbase, int32_t W,
          const uint32_t* __restrict__ dense, unsigned long long* __restrict__ total) {
@@ -368,8 +350,8 @@ tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict_
   __syncwarp();
   long long c = 0;
   for (int64_t r = w0; r < n; r += nw) {
-    const int64_t lo = uoff[r], hi = uoff[r + 1];
-    const int64_t len = hi - lo;
+    const int64_t lo = ustart[r];
+    const int64_t len = ulen[r];
     if (len < 2) continue;
     const int32_t* row = uidx + lo;
     int nlow = 0;  // entries of U(r) below the bitmap (warp-uniform count)
@@ -405,8 +387,8 @@ tc_count(int64_t n, const int64_t* __restrict__ uoff, const int32_t* __restrict_
       int64_t jlo = 0, jhi = 0;
       if (a < ilen) {
         j = row[a];
-        jlo = uoff[j];
-        jhi = uoff[j + 1];
+        jlo = ustart[j];
+        jhi = jlo + ulen[j];
       }
       int wj = W;  // first dense word holding ranks above j
       bool dn = false;
@@ -590,13 +572,13 @@ gb_status gb_tc(gb_ctx* ctx, const gb_csr* a, int64_t* count_host) {
   int32_t* ids = ar.alloc<int32_t>(n);
   int32_t* order = ar.alloc<int32_t>(n);
   int32_t* rank = ar.alloc<int32_t>(n);
-  int64_t* ucnt = ar.alloc<int64_t>(n + 1);
-  int64_t* uoff = ar.alloc<int64_t>(n + 1);
+  int64_t* ustart = ar.alloc<int64_t>(n);
+  int64_t* ulen = ar.alloc<int64_t>(n);
+  int32_t* uidx = ar.alloc<int32_t>(a->nnz);  // U(r) at its vertex's adjacency start
   unsigned long long* total = ar.alloc<unsigned long long>(1);
   const int64_t maxlong = a->nnz / kTcLong + 1;  // rows longer than kTcLong
   int64_t* tstart = ar.alloc<int64_t>(maxlong + 1);
   int64_t* meta = ar.alloc<int64_t>(2);
-  unsigned long long* cursor = ar.alloc<unsigned long long>(maxlong);
   GB_ARENA_CHECK(ctx, ar);
   tc_degree_keys<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, a->offsets, deg, ids);
   // stable: ties keep ascending vertex id (algorithms.py:209-212)
@@ -606,21 +588,10 @@ gb_status gb_tc(gb_ctx* ctx, const gb_csr* a, int64_t* count_host) {
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp, tb, deg, deg2, ids, order, n, 0, 32, s));
   tc_rank<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, order, rank);
-  tc_long_plan<<<1, 1024, 0, s>>>(n, deg2, tstart, meta, cursor, ucnt);
-  tc_upper_count<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(n, a->offsets, a->indices, order,
-                                                                rank, tstart, meta, ucnt);
-  size_t tb2 = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb2, ucnt, uoff, n + 1, s);
-  void* tmp2 = ar.raw(tb2);
-  GB_ARENA_CHECK(ctx, ar);
-  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp2, tb2, ucnt, uoff, n + 1, s));
-  int64_t m = 0;
-  GB_TRY(read_i64(ctx, uoff + n, &m));
-  int32_t* uidx = ar.alloc<int32_t>(m + 1);
-  GB_ARENA_CHECK(ctx, ar);
-  tc_upper_fill<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(n, a->offsets, a->indices, order,
-                                                               rank, tstart, meta, uoff, cursor,
-                                                               uidx);
+  tc_long_plan<<<1, 1024, 0, s>>>(n, deg2, tstart, meta, ulen);
+  tc_upper_build<<<grid_for(ctx, n * 32, 256, 16), 256, 0, s>>>(n, a->offsets, a->indices, order,
+                                                                rank, tstart, meta, ustart, ulen,
+                                                                uidx);
   // dense rows of the top ranks, word-aligned with tc_count's row bitmap
   const int64_t tbase = n > kTcTopBits ? n - kTcTopBits : 0;
   const int64_t lowest = n > kTcDense ? n - kTcDense : 0;
@@ -629,16 +600,16 @@ gb_status gb_tc(gb_ctx* ctx, const gb_csr* a, int64_t* count_host) {
   uint32_t* dense = ar.alloc<uint32_t>((size_t)W * (n - dbase));
   GB_ARENA_CHECK(ctx, ar);
   GB_CUDA(ctx, cudaMemsetAsync(dense, 0, sizeof(uint32_t) * (size_t)W * (n - dbase), s));
-  tc_dense_rows<<<grid_for(ctx, (n - dbase) * 32, 256, 16), 256, 0, s>>>(n, dbase, W, uoff, uidx,
-                                                                         dense);
+  tc_dense_rows<<<grid_for(ctx, (n - dbase) * 32, 256, 16), 256, 0, s>>>(n, dbase, W, ustart,
+                                                                         ulen, uidx, dense);
   GB_CUDA(ctx, cudaMemsetAsync(total, 0, 8, s));
-  const int ps = prof_begin(ctx, PROF_TC, m);
-  tc_count<<<resident_grid(ctx, tc_count, 256), 256, 0, s>>>(n, uoff, uidx, a->offsets,
+  const int ps = prof_begin(ctx, PROF_TC, a->nnz / 2);
+  tc_count<<<resident_grid(ctx, tc_count, 256), 256, 0, s>>>(n, ustart, ulen, uidx, a->offsets,
                                                                a->indices, order, dbase, W, dense,
                                                                total);
   prof_end(ctx, ps);
   GB_LAUNCH_CHECK(ctx);
-  count_launch(ctx, 11);
+  count_launch(ctx, 9);
   return read_i64(ctx, (const int64_t*)total, count_host);
 }
 
