@@ -35,8 +35,11 @@ __device__ __forceinline__ int64_t lb32(const int32_t* a, int64_t n, int32_t key
   return (b - a) + (*b < key);
 }
 
-// One warp per mask row.  out_flag[e] = 1 when mask entry e produces an
-// output entry (matches > 0, or the identity is non-zero), out_val[e] its value.
+// Warp per task of kMxmTask consecutive mask entries (rows cut across
+// tasks): a hub row's thousands of entries no longer serialise on one warp.
+// out_flag[e] = 1 when mask entry e produces an output entry (matches > 0, or
+// the identity is non-zero), out_val[e] its value.
+constexpr int64_t kMxmTask = 32;
 template <class T>
 __global__ void __launch_bounds__(256)
 mxm_masked_kernel(int64_t nrows, const int64_t* __restrict__ moff, const int32_t* __restrict__ midx,
@@ -51,11 +54,30 @@ mxm_masked_kernel(int64_t nrows, const int64_t* __restrict__ moff, const int32_t
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const T ident = op_identity<T>(add_op);
-  for (int64_t i = w0; i < nrows; i += nw) {
-    const int64_t alo = aoff[i], ahi = aoff[i + 1];
-    const int64_t la = ahi - alo;
+  const int64_t nnz_m = moff[nrows];
+  const int64_t ntasks = (nnz_m + kMxmTask - 1) / kMxmTask;
+  for (int64_t t = w0; t < ntasks; t += nw) {
+    const int64_t e0 = t * kMxmTask, e1 = min(e0 + kMxmTask, nnz_m);
+    // the row holding e0: last i with moff[i] <= e0
+    int64_t i;
+    {
+      int64_t lo = 0, hi = nrows;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (moff[mid] <= e0) lo = mid; else hi = mid;
+      }
+      i = lo;
+    }
     long long mults = 0, adds = 0;
-    for (int64_t e = moff[i]; e < moff[i + 1]; ++e) {
+    int64_t rend = moff[i + 1];
+    int64_t alo = aoff[i], la = aoff[i + 1] - alo;
+    for (int64_t e = e0; e < e1; ++e) {
+      while (e >= rend) {  // the task crossed into the next row(s)
+        ++i;
+        rend = moff[i + 1];
+        alo = aoff[i];
+        la = aoff[i + 1] - alo;
+      }
       const bool live = !mval ? miso_live != 0
                               : (mdtype == GB_I64 ? ((const int64_t*)mval)[e] != 0
                                                   : ((const double*)mval)[e] != 0.0);
