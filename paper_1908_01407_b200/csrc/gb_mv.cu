@@ -500,6 +500,177 @@ __global__ void select_kept(int64_t nseg, const int32_t* __restrict__ keep,
     }
 }
 
+// ---- push with an order-independent fold: a dense accumulator ------------
+// When the add monoid gives the same result in any order (integer plus /
+// times wrap, min, max, logical or / and -- fold_commutes on the stored
+// type), the products fold straight into a dense accumulator with atomics;
+// no expansion buffer, sort or segment scan.  The rows that received a
+// product are marked in a bitmap (read before the atomicOr) for the adds
+// counter; the output keeps, in index order, the rows whose fold is not the
+// identity and that the mask allows -- exactly the sorted path's result.
+__device__ __forceinline__ void acc_fold(int add_op, int64_t* a, int64_t x) {
+  switch (add_op) {
+    case GB_OP_PLUS:
+    case GB_OP_PLUS_WRAP:
+      atomicAdd(reinterpret_cast<unsigned long long*>(a), (unsigned long long)x);
+      return;
+    case GB_OP_MIN:
+      if (x < *reinterpret_cast<volatile long long*>(a)) atomicMin(reinterpret_cast<long long*>(a), x);
+      return;
+    case GB_OP_MAX:
+      if (x > *reinterpret_cast<volatile long long*>(a)) atomicMax(reinterpret_cast<long long*>(a), x);
+      return;
+    case GB_OP_LOR:
+      if (x != 0 && *reinterpret_cast<volatile long long*>(a) == 0)
+        atomicExch(reinterpret_cast<unsigned long long*>(a), 1ull);
+      return;
+    case GB_OP_LAND:
+      if (x == 0 && *reinterpret_cast<volatile long long*>(a) != 0)
+        atomicExch(reinterpret_cast<unsigned long long*>(a), 0ull);
+      return;
+    default: {  // TIMES (wrapping)
+      unsigned long long* u = reinterpret_cast<unsigned long long*>(a);
+      unsigned long long old = *u, assumed;
+      do {
+        assumed = old;
+        old = atomicCAS(u, assumed, (unsigned long long)wrap_mul((int64_t)assumed, x));
+      } while (old != assumed);
+    }
+  }
+}
+
+__device__ __forceinline__ void acc_fold(int add_op, double* a, double x) {
+  unsigned long long* u = reinterpret_cast<unsigned long long*>(a);
+  switch (add_op) {
+    case GB_OP_LOR:
+      if (x != 0.0) *reinterpret_cast<volatile double*>(a) = 1.0;  // idempotent store
+      return;
+    case GB_OP_LAND:
+      if (x == 0.0) *reinterpret_cast<volatile double*>(a) = 0.0;
+      return;
+    default: {  // MIN / MAX: compare-and-swap on the value
+      const bool mn = add_op == GB_OP_MIN;
+      double cur = *reinterpret_cast<volatile double*>(a);
+      while (mn ? x < cur : x > cur) {
+        const unsigned long long old =
+            atomicCAS(u, __double_as_longlong(cur), __double_as_longlong(x));
+        if (old == (unsigned long long)__double_as_longlong(cur)) break;
+        cur = __longlong_as_double(old);
+      }
+    }
+  }
+}
+
+template <class T>
+struct PushAccum {
+  const int32_t* __restrict__ idx;
+  const T* __restrict__ vals;
+  T iso;
+  const T* __restrict__ u_vals;
+  int add_op, mult_op;
+  T* acc;
+  uint32_t* touched;
+  __device__ __forceinline__ void operator()(int64_t k, int64_t p, int64_t) const {
+    const int32_t r = __ldg(idx + p);
+    acc_fold(add_op, acc + r, op_pair<T>(mult_op, aval(vals, iso, p), u_vals[k]));
+    const uint32_t bit = 1u << (r & 31);
+    if (!(ld_probe(touched + (r >> 5)) & bit)) atomicOr(touched + (r >> 5), bit);
+  }
+};
+
+// kept bits per word (fold != identity, mask allows) and the word's count;
+// the touched rows' count for the adds counter
+template <class T>
+__global__ void accum_keep(int64_t n, const T* __restrict__ acc, T ident,
+                           const uint32_t* __restrict__ mask, const uint32_t* __restrict__ touched,
+                           uint32_t* __restrict__ keep, int64_t* __restrict__ wcnt,
+                           unsigned long long* __restrict__ ntouched) {
+  const int64_t W = (n + 31) / 32;
+  long long t = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t tw = touched[w];
+    uint32_t kb = 0;
+    for (uint32_t b = tw; b; b &= b - 1) {
+      const int j = __ffs(b) - 1;
+      const int64_t r = w * 32 + j;
+      if (acc[r] != ident && (!mask || ((mask[w] >> j) & 1u))) kb |= 1u << j;
+    }
+    keep[w] = kb;
+    wcnt[w] = __popc(kb);
+    t += __popc(tw);
+  }
+  t = warp_sum_ll(t);
+  if ((threadIdx.x & 31) == 0 && t) atomicAdd(ntouched, (unsigned long long)t);
+}
+
+template <class T>
+__global__ void accum_emit(int64_t n, const T* __restrict__ acc, const uint32_t* __restrict__ keep,
+                           const int64_t* __restrict__ wpos, int32_t* __restrict__ out_idx,
+                           T* __restrict__ out_vals) {
+  const int64_t W = (n + 31) / 32;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t at = wpos[w];
+    for (uint32_t b = keep[w]; b; b &= b - 1) {
+      const int64_t r = w * 32 + (__ffs(b) - 1);
+      out_idx[at] = (int32_t)r;
+      out_vals[at] = acc[r];
+      ++at;
+    }
+  }
+}
+
+template <class T>
+static bool accum_fold_ok(int add_op) {
+  if (std::is_same<T, int64_t>::value) return fold_commutes(add_op);
+  return add_op == GB_OP_MIN || add_op == GB_OP_MAX || add_op == GB_OP_LOR || add_op == GB_OP_LAND;
+}
+
+template <class T>
+static gb_status push_accum_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a,
+                              int64_t out_size, int64_t k, const int32_t* u_idx, const T* u_vals,
+                              const uint32_t* mask, int32_t* out_idx, T* out_vals, int64_t* count,
+                              int64_t* counters, const LbsPlan& plan, Arena& ar, int64_t E) {
+  cudaStream_t s = stream_of(ctx);
+  const int64_t n = out_size, W = (n + 31) / 32;
+  T* acc = ar.alloc<T>(n);
+  uint32_t* touched = ar.alloc<uint32_t>(W);
+  uint32_t* keep = ar.alloc<uint32_t>(W);
+  int64_t* wcnt = ar.alloc<int64_t>(W + 1);
+  int64_t* wpos = ar.alloc<int64_t>(W + 1);
+  unsigned long long* nt = ar.alloc<unsigned long long>(1);
+  GB_ARENA_CHECK(ctx, ar);
+  const T ident = op_identity<T>(add_op);
+  fill_value<T><<<grid_for(ctx, n, 256, 8), 256, 0, s>>>(n, ident, acc);
+  GB_CUDA(ctx, cudaMemsetAsync(touched, 0, sizeof(uint32_t) * W, s));
+  GB_CUDA(ctx, cudaMemsetAsync(nt, 0, 8, s));
+  GB_CUDA(ctx, cudaMemsetAsync(wcnt + W, 0, 8, s));
+  const T iso = std::is_same<T, double>::value ? (T)a->iso_f64 : (T)a->iso_i64;
+  PushAccum<T> f{a->indices, (const T*)a->values, iso, u_vals, add_op, mult_op, acc, touched};
+  lbs_expand<PushAccum<T>><<<plan.grid, kLbsThreads, 0, s>>>(k, plan.S, plan.rowstart,
+                                                             plan.tile_first, f);
+  accum_keep<T><<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, acc, ident, mask, touched, keep, wcnt,
+                                                          nt);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, wcnt, wpos, W + 1, s);
+  void* tmp = ar.raw(tb);
+  GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, wcnt, wpos, W + 1, s));
+  accum_emit<T><<<grid_for(ctx, W, 256, 8), 256, 0, s>>>(n, acc, keep, wpos, out_idx, out_vals);
+  GB_LAUNCH_CHECK(ctx);
+  count_launch(ctx, 9);
+  if (counters) {
+    int64_t ntouched = 0;
+    GB_TRY(read_i64(ctx, (const int64_t*)nt, &ntouched));
+    int64_t c[3];
+    GB_TRY(read_i64(ctx, counters, c, 3));
+    c[2] += E - ntouched;
+    GB_CUDA(ctx, cudaMemcpyAsync(counters, c, 24, cudaMemcpyHostToDevice, s));
+  }
+  return read_i64(ctx, wpos + W, count);
+}
+
 static int bits_for(int64_t n) {
   int b = 1;
   while (((int64_t)1 << b) < n) ++b;
@@ -525,6 +696,9 @@ static gb_status push_t(gb_ctx* ctx, int add_op, int mult_op, const gb_csr* a, i
     GB_CUDA(ctx, cudaMemcpyAsync(counters, c, 24, cudaMemcpyHostToDevice, s));
   }
   if (E == 0) return GB_OK;
+  if (accum_fold_ok<T>(add_op) && !getenv("GB_PUSH_SORTED"))
+    return push_accum_t<T>(ctx, add_op, mult_op, a, out_size, k, u_idx, u_vals, mask, out_idx,
+                           out_vals, count, counters, plan, ar, E);
   int32_t* ka = ar.alloc<int32_t>(E);
   int32_t* kb = ar.alloc<int32_t>(E);
   T* va = ar.alloc<T>(E);
