@@ -9,7 +9,7 @@ mkdir -p gpurun_out/r2
 NCU="ncu --clock-control none"
 export GB_BFS_GRAPH=0 GB_LOOP_GRAPH=0
 # launch list of one BFS (bench workload) and of each algorithm
-for spec in "bfs 24" "mxvm 24" "pr 22" "cc 24" "sssp 20" "tc 20"; do
+for spec in "bfs 24" "mxvm 24" "pr 22" "cc 24" "sssp 20" "tc 20" "push 24" "mxm 20"; do
   set -- $spec
   $NCU --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
     --log-file gpurun_out/r2/launches_$1.csv python tools/prof_bfs.py --algo $1 --scale $2 > /dev/null 2>&1
@@ -26,4 +26,6 @@ cap pr "pr_spmv|pr_epilogue" pr 22 2
 cap cc "cc_pull|cc_hook|cc_shortcut" cc 24 5
 cap sssp "sssp_pull_tiles|lbs_expand" sssp 20 3
 cap tc "tc_count" tc 20 1
+cap push "lbs_expand" push 24 1
+cap mxm "mxm_masked_kernel" mxm 20 1
 ls -la gpurun_out/r2

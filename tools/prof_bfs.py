@@ -35,6 +35,14 @@ if args.algo == "mxvm":
                       .to(torch.int64), 0, np.int64)
 
 
+if args.algo == "push":
+    _o = A.orient(False)
+    _nb = _o.indices[int(_o.offsets[0]):int(_o.offsets[1])].cpu().numpy()
+    _U = gb.Vector.from_entries(_nb, np.ones(_nb.size, np.int64), A.nrows)
+if args.algo == "mxm":
+    _L = gb.algorithms._degree_sorted_lower_triangle(A)
+
+
 def run():
     if args.algo == "bfs":
         gb.bfs(A, 0)
@@ -56,6 +64,13 @@ def run():
     elif args.algo == "mxv":
         u = gb.vector_fill(A.nrows, 1.0)
         gb.mxv(gb.builtin_semiring("PlusMultiplies"), A, u)
+    elif args.algo == "push":   # operator-level push SpMSpV from the hub's neighbours
+        gb.vxm(gb.builtin_semiring("PlusMultiplies"), _U, A,
+               desc=gb.Descriptor(direction=gb.Direction.FORCE_PUSH))
+    elif args.algo == "mxm":    # the reference's L.L^T .* L masked SpGEMM
+        d = gb.Descriptor()
+        d.toggle("inp1")
+        gb.mxm_masked(gb.builtin_semiring("PlusMultiplies"), _L, _L, mask=_L, desc=d)
 
 
 for _ in range(2):
