@@ -35,6 +35,19 @@ __device__ __forceinline__ int64_t lb32(const int32_t* a, int64_t n, int32_t key
   return (b - a) + (*b < key);
 }
 
+// 32-bit form of lb32 for one row's list (the issue-bound inner search)
+__device__ __forceinline__ int lb32i(const int32_t* a, int n, int32_t key) {
+  if (n <= 0) return 0;
+  const int32_t* b = a;
+  int l = n;
+  while (l > 1) {
+    const int h = l >> 1;
+    b = b[h - 1] < key ? b + h : b;
+    l -= h;
+  }
+  return (int)(b - a) + (*b < key);
+}
+
 // Warp per task of kMxmTask consecutive mask entries (rows cut across
 // tasks): a hub row's thousands of entries no longer serialise on one warp.
 // out_flag[e] = 1 when mask entry e produces an output entry (matches > 0, or
@@ -95,10 +108,11 @@ mxm_masked_kernel(int64_t nrows, const int64_t* __restrict__ moff, const int32_t
       const int64_t ls = a_short ? la : lb, ll = a_short ? lb : la;
       T acc = ident;
       long long m = 0;
+      const int ll32 = (int)ll;  // a row's length fits 32 bits: the search stays 32-bit
       for (int64_t q = lane; q < ls; q += 32) {
         const int32_t key = sidx[q];
-        const int64_t p = lb32(lidx, ll, key);
-        if (p < ll && lidx[p] == key) {
+        const int p = lb32i(lidx, ll32, key);
+        if (p < ll32 && lidx[p] == key) {
           const T x = a_short ? (aval ? aval[alo + q] : aiso) : (aval ? aval[alo + p] : aiso);
           const T y = a_short ? (bval ? bval[blo + p] : biso) : (bval ? bval[blo + q] : biso);
           acc = op_fold<T>(add_op, acc, op_pair<T>(mult_op, x, y));
