@@ -184,7 +184,7 @@ def _spmv_pull(semiring, A, u, mask, desc, transpose):
     cnt = _counters_tensor()
     part = _lib.PART_ROW if desc.partition is Partition.ROW_SPLIT else _lib.PART_NONZERO
     view = None
-    if _use_bins(bm, add, early, part):
+    if _use_bins(bm, add, early, part, o):
         nst = _stripe_count(o)
         if nst > 1:
             csrs, plans, _sk = o.stripes(nst)
@@ -261,10 +261,12 @@ def _retag(csrs, dtype):
     return out
 
 
-def _use_bins(bm, add, early, part):
+def _use_bins(bm, add, early, part, o):
     if _MV_BINS == "0" or early or add not in _lib.COMMUTATIVE_FOLD_IDS:
         return False
-    return bm is not None or part == _lib.PART_ROW or _MV_BINS == "1"
+    # unmasked too when the matrix takes column stripes (large gathered
+    # vector, degrees not skewed): uniform s24 min-pull 5.18 -> 3.04 ms
+    return bm is not None or part == _lib.PART_ROW or _MV_BINS == "1" or _stripe_count(o) > 1
 
 
 def _ordered_view(A, o, transpose, add, early, part):
