@@ -8,6 +8,8 @@
 // of a `words`-word bitmap per step (the same load the push uses), grid = all
 // SMs at full occupancy.  bench.py reports the push against it next to the
 // HBM roofline.
+#include <cstdlib>
+
 #include "gb_common.cuh"
 
 namespace gb {
@@ -53,6 +55,30 @@ gather_replay_kernel(int64_t nnz, const int32_t* __restrict__ idx, const double*
   if (acc == -1.2345) sink[0] = acc;
 }
 
+// The same replay with lane-consecutive entries (lane l of a warp gathers
+// entries 32k + l of the warp's 256-entry chunk): sorted neighbours of one
+// row that share a 128-byte line of x coalesce into one L1 wavefront.
+__global__ void __launch_bounds__(256)
+gather_replay_consec(int64_t nnz, const int32_t* __restrict__ idx, const double* __restrict__ x,
+                     double* sink) {
+  double acc = 0.0;
+  const int lane = threadIdx.x & 31;
+  const int64_t chunks = nnz / 256;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = w0; g < chunks; g += nw) {
+    int32_t c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = ld_stream(idx + 256 * g + 32 * k + lane);
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = ld_gather(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += v[k];
+  }
+  if (acc == -1.2345) sink[0] = acc;
+}
+
 }  // namespace gb
 
 using namespace gb;
@@ -63,13 +89,17 @@ extern "C" gb_status gb_gather_replay_rate(gb_ctx* ctx, const gb_csr* a, const d
   Arena ar(ctx);
   double* sink = ar.alloc<double>(1);
   GB_ARENA_CHECK(ctx, ar);
-  const int grid = resident_grid(ctx, gather_replay_kernel, 256);
+  // lane-consecutive by default (the higher of the two rates, and the
+  // mapping of the row-bin pull's long tiles); GB_REPLAY_CONSEC=0: strided
+  const char* cm = getenv("GB_REPLAY_CONSEC");
+  auto k = (cm && cm[0] == '0') ? gather_replay_kernel : gather_replay_consec;
+  const int grid = resident_grid(ctx, k, 256);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  gather_replay_kernel<<<grid, 256, 0, s>>>(a->nnz, a->indices, x, sink);  // warm-up
+  k<<<grid, 256, 0, s>>>(a->nnz, a->indices, x, sink);  // warm-up
   cudaEventRecord(e0, s);
-  gather_replay_kernel<<<grid, 256, 0, s>>>(a->nnz, a->indices, x, sink);
+  k<<<grid, 256, 0, s>>>(a->nnz, a->indices, x, sink);
   cudaEventRecord(e1, s);
   GB_LAUNCH_CHECK(ctx);
   cudaEventSynchronize(e1);
