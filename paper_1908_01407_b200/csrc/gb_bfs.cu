@@ -58,6 +58,10 @@ __device__ __forceinline__ void mark(uint32_t* vbm, int32_t v, uint32_t word) {
 // column loads is issued before any visited probe.
 template <bool VALS>
 struct PushBits {
+  // 4 items per round trip in one/two-list tiles: 0.4-1.6 % less per s24
+  // BFS than 8 on two boxes (0.783 -> 0.780, 0.785 -> 0.772 ms), 2: 0.85 ms
+  // (tools/ab_push_batch2.sh, same box, alternating)
+  static constexpr int kTileBatch = 4;
   const int32_t* __restrict__ idx;
   EdgeOn on;
   uint32_t* __restrict__ vbm;

@@ -10,6 +10,8 @@
 // costs one LDS for its owner plus a coalesced load of its column index.
 #pragma once
 
+#include <type_traits>
+
 #include "gb_common.cuh"
 
 namespace gb {
@@ -114,6 +116,17 @@ gb_status lbs_prepare(gb_ctx* ctx, Arena& ar, int64_t K, const int32_t* ids,
 constexpr int kWarpItems = 16;
 constexpr int kWarpTile = 32 * kWarpItems;  // 512 slots
 
+// Items per batch2 round trip in the one/two-list tiles: F::kTileBatch when
+// the functor names one (the BFS push: 4), else half a lane's 16 items.
+template <class F, class = void>
+struct tile_batch {
+  static constexpr int value = kWarpItems / 2;
+};
+template <class F>
+struct tile_batch<F, std::void_t<decltype(F::kTileBatch)>> {
+  static constexpr int value = F::kTileBatch;
+};
+
 // One warp tile [e0, e1) whose slots start in frontier entries k0..k1 (tb:
 // the tile descriptor's base when has_tb).  Used by warp_tiles and by the
 // TMA-prefetching BFS push for the tiles it does not stage.
@@ -136,9 +149,9 @@ __device__ __forceinline__ void warp_tile_one(const int64_t* S, const int64_t* r
       b1 = rowstart[k0 + 1] - s1 + e0;
     }
     const int32_t rel_end = (int32_t)(e1 - e0);
+    constexpr int B = tile_batch<F>::value;
 #pragma unroll
-    for (int h = 0; h < kWarpItems; h += kWarpItems / 2)
-      f.template batch2<kWarpItems / 2>(b0, b1, st1, rel_end, h * 32);
+    for (int h = 0; h < kWarpItems; h += B) f.template batch2<B>(b0, b1, st1, rel_end, h * 32);
   } else if (nk <= 32) {
     // Entry j of the tile (lane j) starts at st_rel (relative to e0; the
     // first entry's start is clamped to 0).  Slot e_rel = r*32 + lane
