@@ -245,11 +245,23 @@ __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* S, const in
   // loads), so a tile inside one list starts without a dependent round trip
   int32_t k0n = 0, k1n = 0;
   int64_t bn = 0;
-  // a single frontier entry owns every tile: no descriptors are read (the
+  // a single frontier entry owns every slot: no descriptors are read (the
   // BFS device loop does not stamp them for such levels)
   const bool single = K == 1;
-  if (single) bn = rowstart[0] - S[0];
-  if (w0 < ntiles && !single) {
+  if (single) {
+    // one list (a BFS's first level: the source's 406 K edges at R-MAT s24)
+    // in 128-slot tiles, one batch per lane: 4x the warps of 512-slot tiles
+    // on a level too small to fill the GPU with those
+    constexpr int kT = 128;
+    const int64_t b = rowstart[0] - S[0];
+    for (int64_t t = w0; t * kT < E; t += nw) {
+      const int64_t e0 = t * kT;
+      const int32_t rel_end = (int32_t)(E - e0 < kT ? E - e0 : kT);
+      f.template batch2<kT / 32>(b + e0, b + e0, INT32_MAX, rel_end, 0);
+    }
+    return;
+  }
+  if (w0 < ntiles) {
     k0n = tile_first[w0];
     k1n = w0 + 1 < ntiles ? tile_first[w0 + 1] : (int32_t)(K - 1);
     if (tile_base) bn = tile_base[w0];
@@ -259,12 +271,12 @@ __device__ __forceinline__ void warp_tiles(int64_t K, const int64_t* S, const in
     const int64_t e1 = e0 + kWarpTile < E ? e0 + kWarpTile : E;
     const int64_t k0 = k0n, k1 = k1n, tb = bn;
     const int64_t tn = t + nw;
-    if (tn < ntiles && !single) {
+    if (tn < ntiles) {
       k0n = tile_first[tn];
       k1n = tn + 1 < ntiles ? tile_first[tn + 1] : (int32_t)(K - 1);
       if (tile_base) bn = tile_base[tn];
     }
-    warp_tile_one(S, rowstart, tile_base != nullptr || single, e0, e1, k0, k1, tb, f);
+    warp_tile_one(S, rowstart, tile_base != nullptr, e0, e1, k0, k1, tb, f);
   }
 }
 
