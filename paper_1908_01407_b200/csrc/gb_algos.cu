@@ -425,6 +425,185 @@ cc_pull_first(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __r
   row_tiles<int>(R, nz_rows, nz_off, idx, tile_first, red);
 }
 
+// A pull over the row bins (gb_mv_binned.cu's plan: short rows a lane each,
+// medium rows a half-warp each, long rows in 512-entry tiles, 32 tiles per
+// warp batch) that reads only what can change a proposal.  hook[u] matters
+// only through min(mn[u], hook[u]) (cc_hook), and no gathered grandparent is
+// below `low`, the smallest live grandparent (the previous shortcut pass
+// records it; 0, the smallest label, is always a valid bound).  So a row
+// with mn[u] <= low is skipped and a row stops reading once its running
+// minimum reaches low -- the proposals are exactly the full pull's.  In the
+// first gathering pull of an R-MAT graph most grandparents are already the
+// giant component's label 0: hub lists, which start at the hubs, stop within
+// their first tile, and most rows after one pass.
+__global__ void __launch_bounds__(256, 4)
+cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __restrict__ L_beg,
+             const int64_t* __restrict__ L_end, int64_t nM, const int32_t* __restrict__ M_rows,
+             int64_t nS, const int32_t* __restrict__ S_rows, const int64_t* __restrict__ off,
+             const int32_t* __restrict__ idx, const int* __restrict__ gp,
+             const int* __restrict__ mn, const int* __restrict__ lowp, int* __restrict__ hook) {
+  const int low = *lowp;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  // ---- long rows: 512-entry tiles; a row that reached `low` in an earlier
+  // tile of the batch skips the rest of its tiles
+  for (int64_t g = w0; g * 32 < nL; g += nw) {
+    const int64_t ti = g * 32 + lane;
+    int32_t row = -1;
+    int64_t tb = 0, te = 0;
+    if (ti < nL) {
+      row = __ldg(L_row + ti);
+      tb = __ldg(L_beg + ti);
+      te = __ldg(L_end + ti);
+    }
+    uint32_t bal = __ballot_sync(GB_FULL, row >= 0 && __ldg(mn + row) > low);
+    int32_t done = -1;
+    while (bal) {
+      const int j = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const int32_t rr = __shfl_sync(GB_FULL, row, j);
+      const int64_t beg = __shfl_sync(GB_FULL, tb, j), end = __shfl_sync(GB_FULL, te, j);
+      if (rr == done) continue;
+      int acc = kImax32;
+      for (int64_t base = beg; base < end; base += 256) {
+        int32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int64_t p = base + 32 * k + lane;
+          c[k] = p < end ? ld_stream(idx + p) : -1;
+        }
+        int x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = c[k] >= 0 ? ld_gather(gp + c[k]) : kImax32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = x[k] < acc ? x[k] : acc;
+        acc = __reduce_min_sync(GB_FULL, acc);
+        if (acc <= low) break;
+      }
+      if (lane == 0 && acc != kImax32) atomicMin(hook + rr, acc);
+      if (acc <= low) done = rr;
+    }
+  }
+
+  // ---- medium rows: a half-warp per row, two rows at a time, 128 entries a pass
+  const int half = lane >> 4, hl = lane & 15;
+  const unsigned hmask = 0xffffu << (16 * half);
+  for (int64_t g = w0; g * 32 < nM; g += nw) {
+    const int64_t i = g * 32 + lane;
+    const int32_t r = i < nM ? __ldg(M_rows + i) : -1;
+    const bool ok = r >= 0 && __ldg(mn + r) > low;
+    int64_t lo = 0, hi = 0;
+    if (ok) {
+      lo = __ldg(off + r);
+      hi = __ldg(off + r + 1);
+    }
+    uint32_t bal = __ballot_sync(GB_FULL, ok);
+    while (bal) {
+      const int j0 = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const int j1 = bal ? __ffs(bal) - 1 : -1;
+      if (bal) bal &= bal - 1;
+      const int src = half ? (j1 >= 0 ? j1 : j0) : j0;
+      const int32_t rr = __shfl_sync(GB_FULL, r, src);
+      const int64_t l = __shfl_sync(GB_FULL, lo, src);
+      int64_t h = __shfl_sync(GB_FULL, hi, src);
+      if (half && j1 < 0) h = l;  // no second row: the upper half idles
+      int acc = kImax32;
+      for (int64_t base = l; base < h; base += 128) {
+        int32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int64_t p = base + 16 * k + hl;
+          c[k] = p < h ? ld_stream(idx + p) : -1;
+        }
+        int x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = c[k] >= 0 ? ld_gather(gp + c[k]) : kImax32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = x[k] < acc ? x[k] : acc;
+        acc = __reduce_min_sync(hmask, acc);
+        if (acc <= low) break;
+      }
+      if (hl == 0 && acc != kImax32) hook[rr] = acc;
+    }
+  }
+
+  // ---- short rows: a lane per row
+  for (int64_t g = w0; g * 32 < nS; g += nw) {
+    const int64_t i = g * 32 + lane;
+    const int32_t r = i < nS ? __ldg(S_rows + i) : -1;
+    if (r >= 0 && __ldg(mn + r) > low) {
+      const int64_t lo = __ldg(off + r);
+      const int len = (int)(__ldg(off + r + 1) - lo);
+      int32_t c[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) c[q] = q < len ? __ldg(idx + lo + q) : -1;
+      int acc = kImax32;
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        int x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = c[8 * w + k] >= 0 ? ld_gather(gp + c[8 * w + k]) : kImax32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = x[k] < acc ? x[k] : acc;
+      }
+      if (acc != kImax32) hook[r] = acc;
+    }
+  }
+}
+
+// the row bins of the CC rows orientation in one cudaMalloc block (*mem, the
+// caller frees it); synchronises.  Leaves *mem null -- full pulls keep the
+// edge-balanced tiles -- when the degrees are not skewed (rows over 512
+// entries hold under 10 % of the entries: the hubs whose lists stop early are
+// what the bounded pull saves; uniform s24 ran 9.23 vs 8.02 ms with it, R-MAT
+// s24 2.15 vs 3.62 ms), when the rows are empty, or with GB_CC_EXIT=0
+// (GB_CC_EXIT=2: always).
+static int cc_exit_mode() {
+  static const int m = getenv("GB_CC_EXIT") ? atoi(getenv("GB_CC_EXIT")) : 1;
+  return m;
+}
+static gb_status cc_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem) {
+  *mem = nullptr;
+  *b = gb_bin_plan{};
+  if (cc_exit_mode() == 0 || rows->nrows == 0) return GB_OK;
+  int64_t c[3];
+  GB_TRY(gb_bin_plan_counts(ctx, rows, c));
+  if (cc_exit_mode() != 2 && (double)c[2] * 512.0 < 0.1 * (double)rows->nnz) return GB_OK;
+  const size_t bytes = 4 * (size_t)(c[0] + c[1] + c[2]) + 16 * (size_t)c[2] + 64;
+  if (cudaMalloc(mem, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    *mem = nullptr;
+    return set_error(ctx, GB_ERR_OOM, "cc bins: cudaMalloc of %zu bytes", bytes);
+  }
+  char* m = static_cast<char*>(*mem);
+  b->n_short = c[0];
+  b->n_mid = c[1];
+  b->n_long_tiles = c[2];
+  b->tile_beg = (const int64_t*)m;
+  b->tile_end = (const int64_t*)(m + 8 * c[2]);
+  int32_t* r = (int32_t*)(m + 16 * c[2]);
+  b->tile_row = r;
+  b->mid_rows = r + c[2];
+  b->short_rows = r + c[2] + c[1];
+  const gb_status st = gb_bin_plan_fill(ctx, rows, b);
+  if (st != GB_OK) {
+    cudaFree(*mem);
+    *mem = nullptr;
+  }
+  return st;
+}
+
+static void cc_pull_exit_launch(gb_ctx* ctx, cudaStream_t s, const gb_bin_plan& b,
+                                const gb_csr* rows, const int* gp, const int* mn, const int* low,
+                                int* hook) {
+  cc_pull_exit<<<resident_grid(ctx, cc_pull_exit, 256), 256, 0, s>>>(
+      b.n_long_tiles, b.tile_row, b.tile_beg, b.tile_end, b.n_mid, b.mid_rows, b.n_short,
+      b.short_rows, rows->offsets, rows->indices, gp, mn, low, hook);
+}
+
 // With rows that start at their minimum (any sorted CSR) the first pull is
 // one load per row.
 __global__ void cc_hook_first(int64_t n, const int64_t* __restrict__ off,
@@ -560,7 +739,10 @@ __global__ void cc_init(int64_t n, int* __restrict__ parent, int* __restrict__ m
 // (the scatter-min overwrite of kernels.py:538-583 followed by the two Min
 // folds of algorithms.py:192-193 equals this atomic min)
 __global__ void cc_hook(int64_t n, const int* __restrict__ hook, int* __restrict__ mn,
-                        const int* __restrict__ pp, int* __restrict__ parent) {
+                        const int* __restrict__ pp, int* __restrict__ parent,
+                        int* __restrict__ low_reset) {
+  // the pull has read the bound; the shortcut pass after this recomputes it
+  if (low_reset && blockIdx.x == 0 && threadIdx.x == 0) *low_reset = kImax32;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     int m = mn[k];
@@ -587,13 +769,15 @@ __device__ __forceinline__ void cc_shortcut_body(int64_t n, const int* __restric
                                                  int sparsify,
                                                  unsigned long long* __restrict__ changed,
                                                  unsigned long long* __restrict__ live,
-                                                 uint32_t* __restrict__ livebm);
+                                                 uint32_t* __restrict__ livebm,
+                                                 int* __restrict__ low);
 
 __global__ void __launch_bounds__(256)
 cc_shortcut(int64_t n, const int* __restrict__ parent, int* __restrict__ gp,
             int* __restrict__ gpp, int sparsify, unsigned long long* __restrict__ changed,
-            unsigned long long* __restrict__ live, uint32_t* __restrict__ livebm) {
-  cc_shortcut_body(n, parent, gp, gpp, sparsify, changed, live, livebm);
+            unsigned long long* __restrict__ live, uint32_t* __restrict__ livebm,
+            int* __restrict__ low) {
+  cc_shortcut_body(n, parent, gp, gpp, sparsify, changed, live, livebm, low);
 }
 
 __device__ __forceinline__ void cc_shortcut_body(int64_t n, const int* __restrict__ parent,
@@ -601,9 +785,13 @@ __device__ __forceinline__ void cc_shortcut_body(int64_t n, const int* __restric
                                                  int sparsify,
                                                  unsigned long long* __restrict__ changed,
                                                  unsigned long long* __restrict__ live,
-                                                 uint32_t* __restrict__ livebm) {
+                                                 uint32_t* __restrict__ livebm,
+                                                 int* __restrict__ low) {
+  // low (nullable): atomic min of the live grandparents (reset by cc_hook)
   __shared__ long long s_c[8], s_l[8];
+  __shared__ int s_m[8];
   long long c = 0, l = 0;
+  int lmin = kImax32;
   // four independent pointer jumps in flight per thread (latency-bound); the
   // loop bound is warp-uniform (the live-bitmap ballot needs every lane)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -632,6 +820,7 @@ __device__ __forceinline__ void cc_shortcut_body(int64_t n, const int* __restric
         c += ch;
         is_live = out != kImax32;
         l += is_live;
+        lmin = out < lmin ? out : lmin;
       }
       if (livebm) {
         // the 32 lanes hold 32 consecutive vertices (block and grid strides
@@ -644,14 +833,22 @@ __device__ __forceinline__ void cc_shortcut_body(int64_t n, const int* __restric
   }
   c = warp_sum_ll(c);
   l = warp_sum_ll(l);
+  lmin = __reduce_min_sync(GB_FULL, lmin);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) { s_c[wid] = c; s_l[wid] = l; }
+  if (lane == 0) { s_c[wid] = c; s_l[wid] = l; s_m[wid] = lmin; }
   __syncthreads();
   if (threadIdx.x == 0) {
     long long tc = 0, tl = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { tc += s_c[i]; tl += s_l[i]; }
+    int tm = kImax32;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      tc += s_c[i];
+      tl += s_l[i];
+      tm = s_m[i] < tm ? s_m[i] : tm;
+    }
     if (tc) atomicAdd(changed, (unsigned long long)tc);
     if (tl) atomicAdd(live, (unsigned long long)tl);
+    // read first: after the first blocks the bound is usually settled (0)
+    if (low && tm < *(volatile int*)low) atomicMin(low, tm);
   }
 }
 
@@ -1060,6 +1257,8 @@ struct CcState {
   unsigned long long cnt[3];  // changed, live, listed
   unsigned long long nlong;
   int64_t npush;  // iterations that ran the push branch (launch accounting)
+  int32_t low;    // smallest live grandparent (cc_pull_exit's bound)
+  int32_t pad2_;
 };
 
 struct CcPushOp {
@@ -1082,6 +1281,7 @@ __global__ void cc_start_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditi
   st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
   st->nlong = 0;
   st->npush = 0;
+  st->low = 0;  // a valid bound until the first shortcut pass sets it
   const bool run = st->max_iters > 0;
   unsigned dir = 0;
   // branch 3: the first pull (grandparents are the identity)
@@ -1094,7 +1294,7 @@ __global__ void cc_start_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditi
 __global__ void cc_shortcut_g(int64_t n, const int* __restrict__ parent, int* __restrict__ gp,
                               int* __restrict__ gpp, CcState* st, uint32_t* __restrict__ livebm) {
   // sparsify read from the state: one graph serves both settings
-  cc_shortcut_body(n, parent, gp, gpp, st->sparsify, &st->cnt[0], &st->cnt[1], livebm);
+  cc_shortcut_body(n, parent, gp, gpp, st->sparsify, &st->cnt[0], &st->cnt[1], livebm, &st->low);
 }
 
 __global__ void cc_step_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditionalHandle h_loop,
@@ -1131,6 +1331,8 @@ struct CcGraph {
   uint32_t* livebm;  // live grandparents (written by the shortcut pass)
   CcState* st;
   RowTilesPlan plan;
+  gb_bin_plan bins{};      // row bins of `rows` for cc_pull_exit
+  void* binmem = nullptr;  // their storage (null: full pulls run cc_pull)
   cudaGraphExec_t exec = nullptr;
 };
 
@@ -1138,6 +1340,7 @@ static void cc_graph_free(void* p) {
   auto* g = static_cast<CcGraph*>(p);
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->mem) cudaFree(g->mem);
+  if (g->binmem) cudaFree(g->binmem);
   delete g;
 }
 
@@ -1178,7 +1381,9 @@ static cudaError_t cc_graph_build(gb_ctx* ctx, CcGraph* G) {
       }));
       GB_LTRY(loop_capture_into(br[0], cs[2], [&]() -> cudaError_t {
         // pull: mxv walks rows of A (kernels.py:313-316)
-        if (G->plan.R)
+        if (G->binmem)
+          cc_pull_exit_launch(ctx, cs[2], G->bins, &G->rows, G->gp, G->mn, &G->st->low, G->hook);
+        else if (G->plan.R)
           cc_pull<<<resident_grid(ctx, cc_pull, 256), 256, 0, cs[2]>>>(
               G->plan.R, G->plan.nz_rows, G->plan.nz_off, G->rows.indices, G->plan.tile_first,
               G->gp, G->hook);
@@ -1202,7 +1407,7 @@ static cudaError_t cc_graph_build(gb_ctx* ctx, CcGraph* G) {
             &G->st->nlong, G->longk, G->longc, G->F, G->cols.offsets, op);
         return cudaGetLastError();
       }));
-      cc_hook<<<vec_grid, 256, 0, b>>>(n, G->hook, G->mn, G->pp, G->P);
+      cc_hook<<<vec_grid, 256, 0, b>>>(n, G->hook, G->mn, G->pp, G->P, &G->st->low);
       cc_shortcut_g<<<vec_grid, 256, 0, b>>>(n, G->P, G->gp, G->gpp, G->st, G->livebm);
       cc_step_g<<<1, 1, 0, b>>>(G->st, n, nnz, h_loop, h_dir);
       return cudaGetLastError();
@@ -1265,6 +1470,7 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
     Arena ar(ctx);
     gb_status st = row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &G->plan);
     if (st == GB_OK) st = cc_rows_start_at_min(ctx, rows, G->plan, &G->first_min);
+    if (st == GB_OK) st = cc_bins_build(ctx, rows, &G->bins, &G->binmem);
     cudaError_t e = st == GB_OK ? cc_graph_build(ctx, G) : cudaSuccess;
     if (st != GB_OK || e != cudaSuccess) {
       cudaGetLastError();
@@ -1820,10 +2026,20 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   int32_t* F = ar.alloc<int32_t>(n);
   unsigned long long* cnt = ar.alloc<unsigned long long>(3);  // [changed, live, listed]
   GB_ARENA_CHECK(ctx, ar);
+  int* low = ar.alloc<int>(1);
+  GB_ARENA_CHECK(ctx, ar);
   RowTilesPlan plan;
   GB_TRY(row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &plan));
   bool first_min = false;
   GB_TRY(cc_rows_start_at_min(ctx, rows, plan, &first_min));
+  gb_bin_plan bins;
+  void* binmem = nullptr;
+  GB_TRY(cc_bins_build(ctx, rows, &bins, &binmem));
+  struct BinFree {  // cudaFree waits for the work that reads the bins
+    void* p;
+    ~BinFree() { if (p) cudaFree(p); }
+  } bin_free{binmem};
+  GB_CUDA(ctx, cudaMemsetAsync(low, 0, sizeof(int), s));
   cc_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, P, mn, gp, gpp);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 1);
@@ -1852,6 +2068,7 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
       else if (plan.R && (double)live < cc_live_share() * (double)n)
         cc_pull_live<<<resident_grid(ctx, cc_pull_live, 256), 256, 0, s>>>(
             plan.R, plan.nz_rows, plan.nz_off, rows->indices, plan.tile_first, gp, livebm, hook);
+      else if (binmem) cc_pull_exit_launch(ctx, s, bins, rows, gp, mn, low, hook);
       else if (plan.R) cc_pull<<<pull_grid, 256, 0, s>>>(plan.R, plan.nz_rows, plan.nz_off, rows->indices,
                                                     plan.tile_first, gp, hook);
       count_launch(ctx, 1);
@@ -1868,9 +2085,9 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
       count_launch(ctx, 7);
     }
     prof_end(ctx, ps);
-    cc_hook<<<vec_grid, 256, 0, s>>>(n, hook, mn, pp, P);
+    cc_hook<<<vec_grid, 256, 0, s>>>(n, hook, mn, pp, P, low);
     GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
-    cc_shortcut<<<vec_grid, 256, 0, s>>>(n, P, gp, gpp, sparsify, cnt, cnt + 1, livebm);
+    cc_shortcut<<<vec_grid, 256, 0, s>>>(n, P, gp, gpp, sparsify, cnt, cnt + 1, livebm, low);
     GB_LAUNCH_CHECK(ctx);
     count_launch(ctx, 5);
     int64_t h[2];
@@ -2015,7 +2232,7 @@ gb_status gb_cc_dist_shortcut(gb_ctx* ctx, int64_t n, const int32_t* pp, const i
   const int vg = grid_for(ctx, n, 256, 8);
   cc_merge<<<vg, 256, 0, s>>>(n, pp, prop, parent);
   GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
-  cc_shortcut<<<vg, 256, 0, s>>>(n, parent, gp, gpp, sparsify, cnt, cnt + 1, nullptr);
+  cc_shortcut<<<vg, 256, 0, s>>>(n, parent, gp, gpp, sparsify, cnt, cnt + 1, nullptr, nullptr);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 3);
   int64_t h[2];

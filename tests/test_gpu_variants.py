@@ -43,3 +43,13 @@ def test_pagerank_stored_labels():
 
 def test_sssp_stored_labels():
     _pytest({"GB_SSSP_ORDER": "0"}, os.path.join(HERE, "test_gpu_algorithms.py"), "-k", "sssp")
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_cc_pull_variants(mode):
+    # full CC pulls: 0 = edge-balanced tiles everywhere, 2 = the bounded
+    # row-bin pull (cc_pull_exit) on every graph, skewed or not (1, the
+    # default, takes it on skewed graphs only)
+    _pytest({"GB_CC_EXIT": mode}, os.path.join(HERE, "test_gpu_algorithms.py"),
+            os.path.join(HERE, "test_gpu_loops.py"), os.path.join(HERE, "test_gpu_pins.py"),
+            "-k", "cc")
