@@ -250,7 +250,7 @@ def masked_spmv(gb, A, ctx, peak, peak_src, reps=10, density=0.5, graph="rmat"):
     return {"workload": f"mxv(PlusMultiplies f64, A={graph}, x dense, mask=~m, m {density:.0%} "
                         "seeded), forced pull",
             "kernel": "mv_pull_binned (row bins, mask tested per row)",
-            "traffic": committed_traffic("mv_pull_binned") if graph == "rmat" else None,
+            "traffic": committed_traffic("mv_pull_binned" if graph == "rmat" else "mv_pull_binned_uniform_striped"),
             "ab_ms": {"row_bins (default; Partition.ROW_SPLIT)": round(t_ms, 4),
                       "row_tiles (edge-balanced)": round(tiles_ms, 4)},
             "achieved": round(achieved, 1), "peak": peak,

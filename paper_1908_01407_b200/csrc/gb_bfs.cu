@@ -61,7 +61,10 @@ struct PushBits {
   // 4 items per round trip in one/two-list tiles: 0.4-1.6 % less per s24
   // BFS than 8 on two boxes (0.783 -> 0.780, 0.785 -> 0.772 ms), 2: 0.85 ms
   // (tools/ab_push_batch2.sh, same box, alternating)
-  static constexpr int kTileBatch = 4;
+#ifndef GB_PUSH_TILE_BATCH
+#define GB_PUSH_TILE_BATCH 4
+#endif
+  static constexpr int kTileBatch = GB_PUSH_TILE_BATCH;
   const int32_t* __restrict__ idx;
   EdgeOn on;
   uint32_t* __restrict__ vbm;
