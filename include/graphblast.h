@@ -538,9 +538,13 @@ typedef void (*gb_iter_cb)(int64_t iteration, void* user);
 int32_t gb_loop_engine(int32_t engine);
 
 /* sssp (algorithms.py:80-119): dist (float64[n]) receives the distances
- * (+inf unreached).  Weights must be positive (checked by the caller). */
+ * (+inf unreached).  Weights must be positive (checked by the caller);
+ * min_weight is a lower bound on them (their minimum, which the caller's
+ * check computes; 0 is always valid) -- the pull skips rows no candidate can
+ * improve. */
 gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t source,
-                  int64_t max_iters, double switch_ratio, int32_t policy, double* dist,
+                  int64_t max_iters, double switch_ratio, int32_t policy, double min_weight,
+                  double* dist,
                   int32_t* log_dir_host, int64_t* log_nvals_host, int64_t* log_est_host,
                   int64_t* iters_host, gb_iter_cb cb, void* user);
 

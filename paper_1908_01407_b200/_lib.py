@@ -162,8 +162,8 @@ SIGNATURES = {
     "gb_apply_affine": (i32, [vp, i32, i64, vp, vp, vp, vp]),
     "gb_reduce": (i32, [vp, i32, i32, i64, vp, vp, vp, pi64]),
     "gb_reduce_rows": (i32, [vp, i32, C.POINTER(gb_csr), vp]),
-    "gb_sssp": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, i64, f64, i32, vp, vp, vp,
-                      vp, pi64, "ITER_CB", vp]),
+    "gb_sssp": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, i64, f64, i32, f64, vp, vp,
+                      vp, vp, pi64, "ITER_CB", vp]),
     "gb_pagerank": (i32, [vp, C.POINTER(gb_csr), vp, f64, f64, i64, f64, i32, vp, vp, vp, vp,
                           vp, pi64]),
     "gb_cc": (i32, [vp, C.POINTER(gb_csr), C.POINTER(gb_csr), i64, f64, i32, i32, vp, vp, vp,

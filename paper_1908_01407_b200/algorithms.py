@@ -384,7 +384,8 @@ def sssp(A: SparseMatrix, source: int, desc=None, on_iteration=None) -> Vector:
     _require_square(A)
     if not 0 <= source < A.nrows:
         raise IndexError(f"source {source} out of range")
-    if A.nnz and _min_value(A) <= 0:
+    wmin = _min_value(A) if A.nnz else 0.0
+    if A.nnz and wmin <= 0:
         raise ValueError("edge weights must be positive")
     desc = desc if desc is not None else Descriptor()
     if not desc.fused:
@@ -417,7 +418,7 @@ def sssp(A: SparseMatrix, source: int, desc=None, on_iteration=None) -> Vector:
     ctx = _lib.context()
     ctx.call(
         "gb_sssp", C.byref(push), C.byref(pull) if pull is not None else None, int(src_run),
-        int(iters), float(desc.switch_ratio), _POLICY[desc.direction], _lib.ptr(work),
+        int(iters), float(desc.switch_ratio), _POLICY[desc.direction], float(wmin), _lib.ptr(work),
         dirs.ctypes.data_as(C.c_void_p), nv.ctypes.data_as(C.c_void_p),
         est.ctypes.data_as(C.c_void_p), C.byref(done), cb, None)
     if trav is not None:

@@ -124,22 +124,56 @@ sssp_pull_tiles(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* _
 
 constexpr long long kInfBits = 0x7ff0000000000000ll;
 
-__global__ void sssp_pull_apply(int64_t n, long long* __restrict__ cand, double* __restrict__ dist,
-                                uint32_t* __restrict__ changed,
-                                unsigned long long* __restrict__ reached) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+// Folds the pull's candidates into dist.  With `settled` (nullable): also
+// totals the stored in-edges (pull offsets `off`) of the rows whose distance
+// is now <= low -- the share of the matrix a bounded pull (sssp_pull_exit)
+// with this bound would skip.  The next pull takes the bounded kernel when
+// that share is large (the share only grows as distances settle).
+__device__ __forceinline__ void sssp_apply_body(int64_t n, long long* __restrict__ cand,
+                                                double* __restrict__ dist,
+                                                uint32_t* __restrict__ changed,
+                                                unsigned long long* __restrict__ reached,
+                                                const int64_t* __restrict__ off, double low,
+                                                unsigned long long* __restrict__ settled) {
+  unsigned long long sd = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t ib = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); ib < n; ib += stride) {
+    const int64_t i = ib + (threadIdx.x & 31);
+    if (i >= n) continue;
     const long long c = cand[i];
-    if (c == kInfBits) continue;
-    cand[i] = kInfBits;
-    const double nd = __longlong_as_double(c);
-    const double od = dist[i];
-    if (nd < od) {
-      if (od == INFINITY) atomicAdd(reached, 1ull);
-      dist[i] = nd;
-      atomicOr(changed + (i >> 5), 1u << (i & 31));
+    double d = dist[i];
+    if (c != kInfBits) {
+      cand[i] = kInfBits;
+      const double nd = __longlong_as_double(c);
+      if (nd < d) {
+        if (d == INFINITY) atomicAdd(reached, 1ull);
+        dist[i] = nd;
+        d = nd;
+        atomicOr(changed + (i >> 5), 1u << (i & 31));
+      }
+    }
+    if (settled && d <= low) sd += (unsigned long long)(off[i + 1] - off[i]);
+  }
+  if (settled) {
+    __shared__ unsigned long long s_sd[8];
+    sd = (unsigned long long)warp_sum_ll((long long)sd);
+    if ((threadIdx.x & 31) == 0) s_sd[threadIdx.x >> 5] = sd;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_sd[w];
+      if (t) atomicAdd(settled, t);
     }
   }
+}
+
+__global__ void __launch_bounds__(256)
+sssp_pull_apply(int64_t n, long long* __restrict__ cand, double* __restrict__ dist,
+                uint32_t* __restrict__ changed, unsigned long long* __restrict__ reached,
+                const int64_t* __restrict__ off, const long long* __restrict__ fmin,
+                const double* __restrict__ wmin, unsigned long long* __restrict__ settled) {
+  const double low = settled ? __longlong_as_double(*fmin) + *wmin : 0.0;
+  sssp_apply_body(n, cand, dist, changed, reached, off, low, settled);
 }
 
 // warp per row over in-edges; contributions only from frontier vertices
@@ -175,15 +209,17 @@ __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restri
                                                    double* __restrict__ fvd,
                                                    unsigned long long* __restrict__ count,
                                                    const int64_t* __restrict__ off,
-                                                   unsigned long long* __restrict__ sumdeg);
+                                                   unsigned long long* __restrict__ sumdeg,
+                                                   long long* __restrict__ fmin);
 
 __global__ void sssp_finalize(int64_t n, uint32_t* __restrict__ changed,
                               const double* __restrict__ dist, int32_t* __restrict__ F,
                               double* __restrict__ Fv, double* __restrict__ fvd,
                               unsigned long long* __restrict__ count,
                               const int64_t* __restrict__ off,
-                              unsigned long long* __restrict__ sumdeg) {
-  sssp_finalize_body(n, changed, dist, F, Fv, fvd, count, off, sumdeg);
+                              unsigned long long* __restrict__ sumdeg,
+                              long long* __restrict__ fmin) {
+  sssp_finalize_body(n, changed, dist, F, Fv, fvd, count, off, sumdeg, fmin);
 }
 
 __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restrict__ changed,
@@ -193,9 +229,12 @@ __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restri
                                                    double* __restrict__ fvd,
                                                    unsigned long long* __restrict__ count,
                                                    const int64_t* __restrict__ off,
-                                                   unsigned long long* __restrict__ sumdeg) {
+                                                   unsigned long long* __restrict__ sumdeg,
+                                                   long long* __restrict__ fmin) {
   // off / sumdeg: also total the new frontier's out-degrees (the edges a
-  // push of it would relax)
+  // push of it would relax).  fmin (nullable, reset to +inf bits before the
+  // launch): the smallest listed distance, as bits (distances are >= 0)
+  long long dmin = kInfBits;
   const int64_t W = (n + 31) / 32;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t wb = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); wb < W; wb += stride) {
@@ -212,9 +251,12 @@ __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restri
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
       const int64_t v = w * 32 + b;
+      const double dv = dist[v];
       F[slot] = (int32_t)v;
-      Fv[slot] = dist[v];
-      fvd[v] = dist[v];
+      Fv[slot] = dv;
+      fvd[v] = dv;
+      const long long db = __double_as_longlong(dv);
+      dmin = db < dmin ? db : dmin;
       if (off) deg += (unsigned long long)(off[v + 1] - off[v]);
       ++slot;
     }
@@ -223,9 +265,21 @@ __device__ __forceinline__ void sssp_finalize_body(int64_t n, uint32_t* __restri
       if ((threadIdx.x & 31) == 0 && deg) atomicAdd(sumdeg, deg);
     }
   }
+  if (fmin) {
+    // the wb loop is warp-uniform: every lane gets here
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long x = __shfl_xor_sync(GB_FULL, dmin, o);
+      dmin = x < dmin ? x : dmin;
+    }
+    if ((threadIdx.x & 31) == 0 && dmin < *(volatile long long*)fmin) atomicMin(fmin, dmin);
+  }
 }
 
-__global__ void reset_fvd(int64_t K, const int32_t* __restrict__ F, double* __restrict__ fvd) {
+__global__ void reset_fvd(int64_t K, const int32_t* __restrict__ F, double* __restrict__ fvd,
+                          long long* __restrict__ fmin_reset) {
+  // the next finalize records the new frontier's smallest distance
+  if (fmin_reset && blockIdx.x == 0 && threadIdx.x == 0) *fmin_reset = kInfBits;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
        i += (int64_t)gridDim.x * blockDim.x)
     fvd[F[i]] = INFINITY;
@@ -425,40 +479,60 @@ cc_pull_first(int64_t R, const int32_t* __restrict__ nz_rows, const int64_t* __r
   row_tiles<int>(R, nz_rows, nz_off, idx, tile_first, red);
 }
 
-// A pull over the row bins (gb_mv_binned.cu's plan: short rows a lane each,
-// medium rows a half-warp each, long rows in 512-entry tiles, 32 tiles per
-// warp batch) that reads only what can change a proposal.  hook[u] matters
-// only through min(mn[u], hook[u]) (cc_hook), and no gathered grandparent is
-// below `low`, the smallest live grandparent (the previous shortcut pass
-// records it; 0, the smallest label, is always a valid bound).  So a row
-// with mn[u] <= low is skipped and a row stops reading once its running
-// minimum reaches low -- the proposals are exactly the full pull's.  In the
-// first gathering pull of an R-MAT graph most grandparents are already the
-// giant component's label 0: hub lists, which start at the hubs, stop within
-// their first tile, and most rows after one pass.
-__global__ void __launch_bounds__(256, 4)
-cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __restrict__ L_beg,
-             const int64_t* __restrict__ L_end, int64_t nM, const int32_t* __restrict__ M_rows,
-             int64_t nS, const int32_t* __restrict__ S_rows, const int64_t* __restrict__ off,
-             const int32_t* __restrict__ idx, const int* __restrict__ gp,
-             const int* __restrict__ mn, const int* __restrict__ lowp, int* __restrict__ hook) {
-  const int low = *lowp;
+// Bounded min pulls over the row bins (gb_mv_binned.cu's plan: short rows a
+// lane each, medium rows a half-warp each, long rows in 512-entry tiles, 32
+// tiles per warp batch).  A min pull whose consumer only uses a row's result
+// when it is below some per-row value can skip rows and stop reading early
+// given a lower bound `low` on every value the pull can gather:
+//   * a row whose consumer value is <= low cannot change: skipped;
+//   * a row whose running minimum reaches low has its minimum: it stops.
+// Op supplies the value type T, identity(), skip(row), load(p, col),
+// reached(acc) (acc <= low) and emit(row, acc, whole) (whole: the row is
+// complete in this warp; else an atomic min of a partial tile).
+template <class T>
+__device__ __forceinline__ T group_min(unsigned mask, T v, int width) {
+  if constexpr (std::is_same<T, int>::value) {
+    return __reduce_min_sync(mask, v);
+  } else {
+    for (int o = width >> 1; o > 0; o >>= 1) {
+      const T x = __shfl_xor_sync(mask, v, o);
+      v = x < v ? x : v;
+    }
+    return v;
+  }
+}
+
+template <class Op>
+__device__ __forceinline__ void bins_min_pull(int64_t nL, const int32_t* __restrict__ L_row,
+                                              const int64_t* __restrict__ L_beg,
+                                              const int64_t* __restrict__ L_end, int64_t nM,
+                                              const int32_t* __restrict__ M_rows, int64_t nS,
+                                              const int32_t* __restrict__ S_rows,
+                                              const int64_t* __restrict__ off,
+                                              const int32_t* __restrict__ idx, const Op& op) {
+  using T = typename Op::T;
+  const T ident = op.identity();
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
 
-  // ---- long rows: 512-entry tiles; a row that reached `low` in an earlier
-  // tile of the batch skips the rest of its tiles
-  for (int64_t g = w0; g * 32 < nL; g += nw) {
-    const int64_t ti = g * 32 + lane;
+  // ---- long rows: 512-entry tiles in batches of Bt consecutive tiles per
+  // warp (mostly one hub row); a row that reached the bound in an earlier
+  // tile of the batch skips the rest of its tiles.  Bt = 32, halved until
+  // the batches cover every warp (s20: 37 K tiles over 5.9 K warps -- 32-tile
+  // batches had left 80 % of the warps idle and tripled a heavy SSSP pull)
+  int Bt = 32;
+  while (Bt > 1 && (nL + Bt - 1) / Bt < nw) Bt >>= 1;
+  for (int64_t g = w0; g * Bt < nL; g += nw) {
+    const int64_t ti = g * Bt + lane;
     int32_t row = -1;
     int64_t tb = 0, te = 0;
-    if (ti < nL) {
+    if (lane < Bt && ti < nL) {
       row = __ldg(L_row + ti);
       tb = __ldg(L_beg + ti);
       te = __ldg(L_end + ti);
     }
-    uint32_t bal = __ballot_sync(GB_FULL, row >= 0 && __ldg(mn + row) > low);
+    uint32_t bal = __ballot_sync(GB_FULL, row >= 0 && !op.skip(row));
     int32_t done = -1;
     while (bal) {
       const int j = __ffs(bal) - 1;
@@ -466,7 +540,7 @@ cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __res
       const int32_t rr = __shfl_sync(GB_FULL, row, j);
       const int64_t beg = __shfl_sync(GB_FULL, tb, j), end = __shfl_sync(GB_FULL, te, j);
       if (rr == done) continue;
-      int acc = kImax32;
+      T acc = ident;
       for (int64_t base = beg; base < end; base += 256) {
         int32_t c[8];
 #pragma unroll
@@ -474,16 +548,16 @@ cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __res
           const int64_t p = base + 32 * k + lane;
           c[k] = p < end ? ld_stream(idx + p) : -1;
         }
-        int x[8];
+        T x[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = c[k] >= 0 ? ld_gather(gp + c[k]) : kImax32;
+        for (int k = 0; k < 8; ++k) x[k] = c[k] >= 0 ? op.load(base + 32 * k + lane, c[k]) : ident;
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc = x[k] < acc ? x[k] : acc;
-        acc = __reduce_min_sync(GB_FULL, acc);
-        if (acc <= low) break;
+        acc = group_min<T>(GB_FULL, acc, 32);
+        if (op.reached(acc)) break;
       }
-      if (lane == 0 && acc != kImax32) atomicMin(hook + rr, acc);
-      if (acc <= low) done = rr;
+      if (lane == 0) op.emit(rr, acc, false);
+      if (op.reached(acc)) done = rr;
     }
   }
 
@@ -493,7 +567,7 @@ cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __res
   for (int64_t g = w0; g * 32 < nM; g += nw) {
     const int64_t i = g * 32 + lane;
     const int32_t r = i < nM ? __ldg(M_rows + i) : -1;
-    const bool ok = r >= 0 && __ldg(mn + r) > low;
+    const bool ok = r >= 0 && !op.skip(r);
     int64_t lo = 0, hi = 0;
     if (ok) {
       lo = __ldg(off + r);
@@ -510,7 +584,7 @@ cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __res
       const int64_t l = __shfl_sync(GB_FULL, lo, src);
       int64_t h = __shfl_sync(GB_FULL, hi, src);
       if (half && j1 < 0) h = l;  // no second row: the upper half idles
-      int acc = kImax32;
+      T acc = ident;
       for (int64_t base = l; base < h; base += 128) {
         int32_t c[8];
 #pragma unroll
@@ -518,15 +592,15 @@ cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __res
           const int64_t p = base + 16 * k + hl;
           c[k] = p < h ? ld_stream(idx + p) : -1;
         }
-        int x[8];
+        T x[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = c[k] >= 0 ? ld_gather(gp + c[k]) : kImax32;
+        for (int k = 0; k < 8; ++k) x[k] = c[k] >= 0 ? op.load(base + 16 * k + hl, c[k]) : ident;
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc = x[k] < acc ? x[k] : acc;
-        acc = __reduce_min_sync(hmask, acc);
-        if (acc <= low) break;
+        acc = group_min<T>(hmask, acc, 16);
+        if (op.reached(acc)) break;
       }
-      if (hl == 0 && acc != kImax32) hook[rr] = acc;
+      if (hl == 0 && h > l) op.emit(rr, acc, true);
     }
   }
 
@@ -534,44 +608,125 @@ cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __res
   for (int64_t g = w0; g * 32 < nS; g += nw) {
     const int64_t i = g * 32 + lane;
     const int32_t r = i < nS ? __ldg(S_rows + i) : -1;
-    if (r >= 0 && __ldg(mn + r) > low) {
+    if (r >= 0 && !op.skip(r)) {
       const int64_t lo = __ldg(off + r);
       const int len = (int)(__ldg(off + r + 1) - lo);
       int32_t c[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) c[q] = q < len ? __ldg(idx + lo + q) : -1;
-      int acc = kImax32;
+      T acc = ident;
 #pragma unroll
       for (int w = 0; w < 2; ++w) {
-        int x[8];
+        T x[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = c[8 * w + k] >= 0 ? ld_gather(gp + c[8 * w + k]) : kImax32;
+        for (int k = 0; k < 8; ++k)
+          x[k] = c[8 * w + k] >= 0 ? op.load(lo + 8 * w + k, c[8 * w + k]) : ident;
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc = x[k] < acc ? x[k] : acc;
       }
-      if (acc != kImax32) hook[r] = acc;
+      op.emit(r, acc, true);
     }
   }
 }
 
-// the row bins of the CC rows orientation in one cudaMalloc block (*mem, the
-// caller frees it); synchronises.  Leaves *mem null -- full pulls keep the
+// CC: hook[u] only matters through min(mn[u], hook[u]) (cc_hook), and no
+// gathered grandparent is below `low`, the smallest live grandparent (the
+// previous shortcut pass records it; 0, the smallest label, is always a
+// valid bound).  Rows with mn[u] <= low are skipped, a row stops once its
+// minimum reaches low -- the proposals are exactly the full pull's.  In the
+// first gathering pull of an R-MAT graph most grandparents are already the
+// giant component's label 0: hub lists, which start at the hubs, stop within
+// their first tile, and most rows after one pass.
+struct CcBound {
+  using T = int;
+  const int* __restrict__ gp;
+  const int* __restrict__ mn;
+  int low;
+  int* __restrict__ hook;
+  __device__ __forceinline__ int identity() const { return kImax32; }
+  __device__ __forceinline__ bool skip(int32_t r) const { return __ldg(mn + r) <= low; }
+  __device__ __forceinline__ int load(int64_t, int32_t col) const { return ld_gather(gp + col); }
+  __device__ __forceinline__ bool reached(int acc) const { return acc <= low; }
+  __device__ __forceinline__ void emit(int32_t r, int acc, bool whole) const {
+    if (acc == kImax32) return;
+    if (whole) hook[r] = acc;
+    else atomicMin(hook + r, acc);
+  }
+};
+
+__global__ void __launch_bounds__(256, 4)
+cc_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __restrict__ L_beg,
+             const int64_t* __restrict__ L_end, int64_t nM, const int32_t* __restrict__ M_rows,
+             int64_t nS, const int32_t* __restrict__ S_rows, const int64_t* __restrict__ off,
+             const int32_t* __restrict__ idx, const int* __restrict__ gp,
+             const int* __restrict__ mn, const int* __restrict__ lowp, int* __restrict__ hook) {
+  const CcBound op{gp, mn, *lowp, hook};
+  bins_min_pull(nL, L_row, L_beg, L_end, nM, M_rows, nS, S_rows, off, idx, op);
+}
+
+// SSSP: cand[u] = min over in-edges from the frontier of w + d(src) only
+// matters where it is below dist[u] (sssp_pull_apply), and every candidate
+// is at least low = (smallest frontier distance, recorded by the finalize
+// that listed the frontier) + (smallest weight of the matrix).  Rows with
+// dist[u] <= low are settled for this iteration and skipped; a row stops at
+// low.  At R-MAT s20 the heavy pulls after the source skip 37 % / 81 % of the
+// stored entries this way.
+struct SsspBound {
+  using T = double;
+  const void* vals;
+  int dtype;
+  double iso;
+  const double* __restrict__ fvd;
+  const double* __restrict__ dist;
+  double low;
+  long long* __restrict__ cand;
+  __device__ __forceinline__ double identity() const { return INFINITY; }
+  __device__ __forceinline__ bool skip(int32_t r) const { return dist[r] <= low; }
+  __device__ __forceinline__ double load(int64_t p, int32_t col) const {
+    const double u = ld_gather(fvd + col);
+    return u == INFINITY ? INFINITY : ld_weight(vals, dtype, iso, p) + u;
+  }
+  __device__ __forceinline__ bool reached(double acc) const { return acc <= low; }
+  __device__ __forceinline__ void emit(int32_t r, double acc, bool whole) const {
+    if (acc == INFINITY) return;
+    const long long b = __double_as_longlong(acc);
+    if (whole) cand[r] = b;
+    else atomicMin(cand + r, b);
+  }
+};
+
+__global__ void __launch_bounds__(256, 4)
+sssp_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __restrict__ L_beg,
+               const int64_t* __restrict__ L_end, int64_t nM, const int32_t* __restrict__ M_rows,
+               int64_t nS, const int32_t* __restrict__ S_rows, const int64_t* __restrict__ off,
+               const int32_t* __restrict__ idx, const void* vals, int dtype, double iso,
+               const double* __restrict__ fvd, const double* dist, double* const* distp,
+               const long long* __restrict__ fmin_bits, const double* __restrict__ wminp,
+               long long* __restrict__ cand) {
+  // dist: the distances, or null and *distp (the graph loop's state)
+  const SsspBound op{vals, dtype, iso, fvd, dist ? dist : *distp,
+                     __longlong_as_double(*fmin_bits) + *wminp, cand};
+  bins_min_pull(nL, L_row, L_beg, L_end, nM, M_rows, nS, S_rows, off, idx, op);
+}
+
+// the row bins of a pull orientation (CC rows, SSSP in-edges) in one
+// cudaMalloc block (*mem, the caller frees it); synchronises.  Leaves *mem null -- full pulls keep the
 // edge-balanced tiles -- when the degrees are not skewed (rows over 512
 // entries hold under 10 % of the entries: the hubs whose lists stop early are
 // what the bounded pull saves; uniform s24 ran 9.23 vs 8.02 ms with it, R-MAT
-// s24 2.15 vs 3.62 ms), when the rows are empty, or with GB_CC_EXIT=0
-// (GB_CC_EXIT=2: always).
-static int cc_exit_mode() {
-  static const int m = getenv("GB_CC_EXIT") ? atoi(getenv("GB_CC_EXIT")) : 1;
+// s24 2.15 vs 3.62 ms), when the rows are empty, or with GB_PULL_EXIT=0
+// (GB_PULL_EXIT=2: always).
+static int pull_exit_mode() {
+  static const int m = getenv("GB_PULL_EXIT") ? atoi(getenv("GB_PULL_EXIT")) : 1;
   return m;
 }
-static gb_status cc_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem) {
+static gb_status skew_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem) {
   *mem = nullptr;
   *b = gb_bin_plan{};
-  if (cc_exit_mode() == 0 || rows->nrows == 0) return GB_OK;
+  if (pull_exit_mode() == 0 || rows->nrows == 0) return GB_OK;
   int64_t c[3];
   GB_TRY(gb_bin_plan_counts(ctx, rows, c));
-  if (cc_exit_mode() != 2 && (double)c[2] * 512.0 < 0.1 * (double)rows->nnz) return GB_OK;
+  if (pull_exit_mode() != 2 && (double)c[2] * 512.0 < 0.1 * (double)rows->nnz) return GB_OK;
   const size_t bytes = 4 * (size_t)(c[0] + c[1] + c[2]) + 16 * (size_t)c[2] + 64;
   if (cudaMalloc(mem, bytes) != cudaSuccess) {
     cudaGetLastError();
@@ -1470,7 +1625,7 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
     Arena ar(ctx);
     gb_status st = row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &G->plan);
     if (st == GB_OK) st = cc_rows_start_at_min(ctx, rows, G->plan, &G->first_min);
-    if (st == GB_OK) st = cc_bins_build(ctx, rows, &G->bins, &G->binmem);
+    if (st == GB_OK) st = skew_bins_build(ctx, rows, &G->bins, &G->binmem);
     cudaError_t e = st == GB_OK ? cc_graph_build(ctx, G) : cudaSuccess;
     if (st != GB_OK || e != cudaSuccess) {
       cudaGetLastError();
@@ -1526,8 +1681,13 @@ struct SsspState {
   double* dist;
   int32_t policy, has_pull;
   double pull_share;  // a push level relaxing more than this share of nnz runs as the pull
+  double wmin;        // lower bound on the weights (sssp_pull_exit)
+  double exit_share;  // a pull takes sssp_pull_exit above this settled share of nnz
+  int32_t has_bins, pad3_;
   // loop
   int64_t it, K, reached, succ_last, iters;
+  long long fmin;     // bits of the smallest frontier distance (finalize)
+  unsigned long long settled;  // in-edges of settled rows at the last pull (apply)
   unsigned long long cnt[2];  // new frontier, newly reached
   unsigned long long nlong;
   unsigned long long sumdeg;  // out-degrees of the frontier (finalize)
@@ -1541,6 +1701,17 @@ static double sssp_pull_share() {
   static double v = -1.0;
   if (v < 0) {
     const char* e = getenv("GB_SSSP_PULL_SHARE");
+    v = e ? atof(e) : 0.3;
+  }
+  return v;
+}
+
+// A pull takes the bounded row-bin kernel when the previous pull left at
+// least this share of the stored edges in settled rows (GB_SSSP_EXIT_SHARE).
+static double sssp_exit_share() {
+  static double v = -1.0;
+  if (v < 0) {
+    const char* e = getenv("GB_SSSP_EXIT_SHARE");
     v = e ? atof(e) : 0.3;
   }
   return v;
@@ -1589,8 +1760,12 @@ __device__ __forceinline__ unsigned sssp_branch(SsspState* st, int64_t n, int64_
   st->nlong = 0;
   const bool heavy = st->has_pull && (double)st->sumdeg > st->pull_share * (double)nnz;
   st->sumdeg = 0;
-  const unsigned b = dir == GB_DIR_PULL || (st->K > 0 && heavy) ? 0u : (st->K > 0 ? 1u : 2u);
-  st->npull += b == 0;
+  unsigned b = dir == GB_DIR_PULL || (st->K > 0 && heavy) ? 0u : (st->K > 0 ? 1u : 3u);
+  // branch 2: the bounded pull, when the last pull left most stored edges in
+  // settled rows
+  if (b == 0 && st->has_bins && (double)st->settled >= st->exit_share * (double)nnz) b = 2u;
+  if (b == 0 || b == 2) st->settled = 0;  // this pull's apply totals it afresh
+  st->npull += b == 0 || b == 2;
   return b;
 }
 
@@ -1598,49 +1773,42 @@ __global__ void sssp_start_g(SsspState* st, int64_t n, int64_t nnz,
                              cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_dir) {
   st->it = 0;
   st->K = 1;
+  st->fmin = 0;  // the first frontier is the source at distance 0
   st->reached = 1;
   st->succ_last = -1;
   st->iters = 0;
   st->cnt[0] = st->cnt[1] = 0;
   st->sumdeg = 0;
   st->npull = 0;
+  st->settled = 0;
   const bool run = st->max_iters > 0;
-  const unsigned dir = run ? sssp_branch(st, n, nnz) : 2u;
+  const unsigned dir = run ? sssp_branch(st, n, nnz) : 3u;
   cudaGraphSetConditional(h_loop, run ? 1u : 0u);
   cudaGraphSetConditional(h_dir, dir);
 }
 
-__global__ void reset_fvd_g(const SsspState* __restrict__ st, const int32_t* __restrict__ F,
+__global__ void reset_fvd_g(SsspState* __restrict__ st, const int32_t* __restrict__ F,
                             double* __restrict__ fvd) {
   const int64_t K = st->K;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->fmin = kInfBits;  // recorded by the finalize
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K;
        i += (int64_t)gridDim.x * blockDim.x)
     fvd[F[i]] = INFINITY;
 }
 
-__global__ void sssp_pull_apply_g(int64_t n, long long* __restrict__ cand, SsspState* st,
-                                  uint32_t* __restrict__ changed) {
-  double* dist = st->dist;
-  unsigned long long* reached = &st->cnt[1];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const long long c = cand[i];
-    if (c == kInfBits) continue;
-    cand[i] = kInfBits;
-    const double nd = __longlong_as_double(c);
-    const double od = dist[i];
-    if (nd < od) {
-      if (od == INFINITY) atomicAdd(reached, 1ull);
-      dist[i] = nd;
-      atomicOr(changed + (i >> 5), 1u << (i & 31));
-    }
-  }
+__global__ void __launch_bounds__(256)
+sssp_pull_apply_g(int64_t n, long long* __restrict__ cand, SsspState* st,
+                  uint32_t* __restrict__ changed, const int64_t* __restrict__ off) {
+  // the settled share is totalled only when a bounded pull is available
+  // (sssp_branch zeroed it when it chose this pull)
+  sssp_apply_body(n, cand, st->dist, changed, &st->cnt[1], off,
+                  __longlong_as_double(st->fmin) + st->wmin, st->has_bins ? &st->settled : nullptr);
 }
 
 __global__ void sssp_finalize_g(int64_t n, uint32_t* __restrict__ changed, SsspState* st,
                                 int32_t* __restrict__ F, double* __restrict__ Fv,
                                 double* __restrict__ fvd, const int64_t* __restrict__ off) {
-  sssp_finalize_body(n, changed, st->dist, F, Fv, fvd, &st->cnt[0], off, &st->sumdeg);
+  sssp_finalize_body(n, changed, st->dist, F, Fv, fvd, &st->cnt[0], off, &st->sumdeg, &st->fmin);
 }
 
 __global__ void sssp_step_g(SsspState* st, int64_t n, int64_t nnz,
@@ -1657,7 +1825,7 @@ __global__ void sssp_step_g(SsspState* st, int64_t n, int64_t nnz,
   const bool done = reached == st->succ_last && K == 0;
   st->succ_last = reached;
   const bool cont = !done && it + 1 < st->max_iters;
-  const unsigned dir = cont ? sssp_branch(st, n, nnz) : 2u;
+  const unsigned dir = cont ? sssp_branch(st, n, nnz) : 3u;
   cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
   cudaGraphSetConditional(h_dir, dir);
 }
@@ -1672,6 +1840,8 @@ struct SsspGraph {
   long long* cand;
   SsspState* st;
   RowTilesPlan plan;
+  gb_bin_plan bins{};      // row bins of `pull` for sssp_pull_exit (skewed graphs)
+  void* binmem = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
 
@@ -1679,6 +1849,7 @@ static void sssp_graph_free(void* p) {
   auto* g = static_cast<SsspGraph*>(p);
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->mem) cudaFree(g->mem);
+  if (g->binmem) cudaFree(g->binmem);
   delete g;
 }
 
@@ -1703,15 +1874,29 @@ static cudaError_t sssp_graph_build(gb_ctx* ctx, SsspGraph* G) {
     GB_LTRY(add_conditional(s, h_loop, cudaGraphCondTypeWhile, 1, &body));
     return loop_capture_into(body, cs[1], [&]() -> cudaError_t {
       cudaStream_t b = cs[1];
-      cudaGraph_t br[2];
-      GB_LTRY(add_conditional(b, h_dir, cudaGraphCondTypeSwitch, 2, br));
+      // branches: 0 pull over row tiles, 1 push, 2 bounded pull over the
+      // row bins (skewed graphs, most edges in settled rows), 3 (none) skip
+      cudaGraph_t br[3];
+      GB_LTRY(add_conditional(b, h_dir, cudaGraphCondTypeSwitch, 3, br));
       GB_LTRY(loop_capture_into(br[0], cs[2], [&]() -> cudaError_t {
         if (!G->has_pull) return cudaSuccess;
         if (G->plan.R)
           sssp_pull_tiles<<<resident_grid(ctx, sssp_pull_tiles, 256), 256, 0, cs[2]>>>(
               G->plan.R, G->plan.nz_rows, G->plan.nz_off, G->pull.indices, G->plan.tile_first,
               G->pull.values, G->pull.dtype, G->pull.iso_f64, G->fvd, G->cand);
-        sssp_pull_apply_g<<<grid_for(ctx, n, 256), 256, 0, cs[2]>>>(n, G->cand, G->st, G->changed);
+        sssp_pull_apply_g<<<grid_for(ctx, n, 256), 256, 0, cs[2]>>>(n, G->cand, G->st, G->changed,
+                                                                    G->pull.offsets);
+        return cudaGetLastError();
+      }));
+      GB_LTRY(loop_capture_into(br[2], cs[2], [&]() -> cudaError_t {
+        if (!G->has_pull || !G->binmem) return cudaSuccess;
+        sssp_pull_exit<<<resident_grid(ctx, sssp_pull_exit, 256), 256, 0, cs[2]>>>(
+            G->bins.n_long_tiles, G->bins.tile_row, G->bins.tile_beg, G->bins.tile_end,
+            G->bins.n_mid, G->bins.mid_rows, G->bins.n_short, G->bins.short_rows,
+            G->pull.offsets, G->pull.indices, G->pull.values, G->pull.dtype, G->pull.iso_f64,
+            G->fvd, nullptr, &G->st->dist, &G->st->fmin, &G->st->wmin, G->cand);
+        sssp_pull_apply_g<<<grid_for(ctx, n, 256), 256, 0, cs[2]>>>(n, G->cand, G->st, G->changed,
+                                                                    G->pull.offsets);
         return cudaGetLastError();
       }));
       GB_LTRY(loop_capture_into(br[1], cs[2], [&]() -> cudaError_t {
@@ -1739,7 +1924,8 @@ static cudaError_t sssp_graph_build(gb_ctx* ctx, SsspGraph* G) {
 }
 
 static gb_status sssp_graph(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t source,
-                            int64_t max_iters, double ratio, int32_t policy, double* dist,
+                            int64_t max_iters, double ratio, int32_t policy, double wmin,
+                            double* dist,
                             int32_t* log_dir, int64_t* log_nvals, int64_t* log_est,
                             int64_t* iters_out) {
   const int64_t n = push->nrows;
@@ -1788,6 +1974,7 @@ static gb_status sssp_graph(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
       G->plan.tile_first = (int32_t*)(m + o_t);
       Arena ar(ctx);
       st = row_tiles_plan(ctx, ar, n, pull->offsets, pull->nnz, &G->plan);
+      if (st == GB_OK) st = skew_bins_build(ctx, pull, &G->bins, &G->binmem);
     }
     cudaError_t e = st == GB_OK ? sssp_graph_build(ctx, G) : cudaSuccess;
     if (st != GB_OK || e != cudaSuccess) {
@@ -1810,6 +1997,9 @@ static gb_status sssp_graph(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
   h.policy = policy;
   h.has_pull = pull != nullptr;
   h.pull_share = sssp_pull_share();
+  h.wmin = wmin;
+  h.exit_share = sssp_exit_share();
+  h.has_bins = G->binmem != nullptr;
   GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(SsspState, it), cudaMemcpyHostToDevice, s));
   GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
   int64_t iters = 0;
@@ -1850,15 +2040,17 @@ int32_t gb_loop_engine(int32_t engine) {
 }
 
 gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t source,
-                  int64_t max_iters, double ratio, int32_t policy, double* dist,
+                  int64_t max_iters, double ratio, int32_t policy, double min_weight, double* dist,
                   int32_t* log_dir, int64_t* log_nvals, int64_t* log_est, int64_t* iters_out,
                   gb_iter_cb cb, void* user) {
   const int64_t n = push->nrows;
   if (source < 0 || source >= n) return set_error(ctx, GB_ERR_INDEX, "source out of range");
+  // a lower bound on the weights (positive by contract): anything else -> 0
+  const double wmin = min_weight > 0.0 && min_weight < INFINITY ? min_weight : 0.0;
   // device-resident loop unless a per-iteration host callback is requested
   // or the kernels are being timed one by one
   if (!cb && loop_engine() == kLoopGraph && !prof_enabled(ctx)) {
-    const gb_status st = sssp_graph(ctx, push, pull, source, max_iters, ratio, policy, dist,
+    const gb_status st = sssp_graph(ctx, push, pull, source, max_iters, ratio, policy, wmin, dist,
                                     log_dir, log_nvals, log_est, iters_out);
     if (st != GB_ERR_UNSUPPORTED) return st;
   }
@@ -1869,10 +2061,15 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
   int32_t* F = ar.alloc<int32_t>(n);
   double* Fv = ar.alloc<double>(n);
   double* fvd = ar.alloc<double>(n);
-  unsigned long long* cnt = ar.alloc<unsigned long long>(3);  // [frontier, reached, out-degrees]
+  // [frontier, reached, out-degrees, in-edges of settled rows]
+  unsigned long long* cnt = ar.alloc<unsigned long long>(4);
+  long long* fmin = ar.alloc<long long>(1);                   // smallest frontier distance (bits)
+  double* wmin_d = ar.alloc<double>(1);
   GB_ARENA_CHECK(ctx, ar);
+  GB_CUDA(ctx, cudaMemsetAsync(fmin, 0, sizeof(long long), s));  // the source, at 0
+  GB_CUDA(ctx, cudaMemcpyAsync(wmin_d, &wmin, sizeof(double), cudaMemcpyHostToDevice, s));
   GB_CUDA(ctx, cudaMemsetAsync(changed, 0, sizeof(uint32_t) * W, s));
-  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 24, s));
+  GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 32, s));
   sssp_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, dist, fvd, source, F, Fv);
   GB_LAUNCH_CHECK(ctx);
   count_launch(ctx, 3);
@@ -1881,7 +2078,13 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
   GB_CUDA(ctx, cudaMemcpyAsync(fvd + source, &zero, 8, cudaMemcpyHostToDevice, s));
   RowTilesPlan pull_plan;    // built on the first pull iteration
   long long* cand = nullptr;  // pull candidates (+inf bits between iterations)
-  int64_t K = 1, reached = 1, succ_last = -1, iters = 0, sumdeg = 0;
+  gb_bin_plan bins{};         // row bins of `pull` (skewed graphs), with the plan
+  void* binmem = nullptr;
+  struct BinFree {  // cudaFree waits for the work that reads the bins
+    void*& p;
+    ~BinFree() { if (p) cudaFree(p); }
+  } bin_free{binmem};
+  int64_t K = 1, reached = 1, succ_last = -1, iters = 0, sumdeg = 0, settled = 0;
   const double push_iso = push->iso_f64, pull_iso = pull ? pull->iso_f64 : 0.0;
   for (int64_t it = 0; it < max_iters; ++it) {
     int64_t est = 0;
@@ -1901,12 +2104,23 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
         cand = ar.alloc<long long>(n);
         GB_ARENA_CHECK(ctx, ar);
         fill_i64<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, kInfBits, cand);
+        GB_TRY(skew_bins_build(ctx, pull, &bins, &binmem));
       }
-      if (pull_plan.R)
+      // the bounded pull when the last pull left most edges in settled rows
+      const bool bounded = binmem && (double)settled >= sssp_exit_share() * (double)pull->nnz;
+      if (bounded)
+        sssp_pull_exit<<<resident_grid(ctx, sssp_pull_exit, 256), 256, 0, s>>>(
+            bins.n_long_tiles, bins.tile_row, bins.tile_beg, bins.tile_end, bins.n_mid,
+            bins.mid_rows, bins.n_short, bins.short_rows, pull->offsets, pull->indices,
+            pull->values, pull->dtype, pull_iso, fvd, dist, nullptr, fmin, wmin_d, cand);
+      else if (pull_plan.R)
         sssp_pull_tiles<<<resident_grid(ctx, sssp_pull_tiles, 256), 256, 0, s>>>(
             pull_plan.R, pull_plan.nz_rows, pull_plan.nz_off, pull->indices, pull_plan.tile_first,
             pull->values, pull->dtype, pull_iso, fvd, cand);
-      sssp_pull_apply<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, cand, dist, changed, cnt + 1);
+      GB_CUDA(ctx, cudaMemsetAsync(cnt + 3, 0, 8, s));
+      sssp_pull_apply<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, cand, dist, changed, cnt + 1,
+                                                            pull->offsets, fmin, wmin_d,
+                                                            binmem ? cnt + 3 : nullptr);
       prof_end(ctx, ps);
       count_launch(ctx, 2);
     } else if (K > 0) {
@@ -1919,16 +2133,17 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
       prof_end(ctx, ps);
       count_launch(ctx, 5);
     }
-    reset_fvd<<<grid_for(ctx, K > 0 ? K : 1, 256), 256, 0, s>>>(K, F, fvd);
+    reset_fvd<<<grid_for(ctx, K > 0 ? K : 1, 256), 256, 0, s>>>(K, F, fvd, fmin);
     sssp_finalize<<<grid_for(ctx, W, 256), 256, 0, s>>>(n, changed, dist, F, Fv, fvd, cnt,
-                                                         push->offsets, cnt + 2);
+                                                         push->offsets, cnt + 2, fmin);
     GB_LAUNCH_CHECK(ctx);
     count_launch(ctx, 2);
-    int64_t h[3];
-    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 3));
+    int64_t h[4];
+    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 4));
     K = h[0];
     reached += h[1];
     sumdeg = h[2];
+    if (dir == GB_DIR_PULL || heavy) settled = h[3];
     GB_CUDA(ctx, cudaMemsetAsync(cnt + 1, 0, 16, s));
     if (cb) cb(it, user);
     // algorithms.py:114-118: count of finite distances stable and no frontier
@@ -2034,7 +2249,7 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   GB_TRY(cc_rows_start_at_min(ctx, rows, plan, &first_min));
   gb_bin_plan bins;
   void* binmem = nullptr;
-  GB_TRY(cc_bins_build(ctx, rows, &bins, &binmem));
+  GB_TRY(skew_bins_build(ctx, rows, &bins, &binmem));
   struct BinFree {  // cudaFree waits for the work that reads the bins
     void* p;
     ~BinFree() { if (p) cudaFree(p); }

@@ -46,10 +46,10 @@ def test_sssp_stored_labels():
 
 
 @pytest.mark.parametrize("mode", ["0", "2"])
-def test_cc_pull_variants(mode):
-    # full CC pulls: 0 = edge-balanced tiles everywhere, 2 = the bounded
-    # row-bin pull (cc_pull_exit) on every graph, skewed or not (1, the
-    # default, takes it on skewed graphs only)
-    _pytest({"GB_CC_EXIT": mode}, os.path.join(HERE, "test_gpu_algorithms.py"),
+def test_bounded_pull_variants(mode):
+    # CC / SSSP pulls: 0 = edge-balanced tiles everywhere, 2 = the bounded
+    # row-bin pulls (cc_pull_exit, sssp_pull_exit) on every graph, skewed or
+    # not (1, the default, takes them on skewed graphs only)
+    _pytest({"GB_PULL_EXIT": mode}, os.path.join(HERE, "test_gpu_algorithms.py"),
             os.path.join(HERE, "test_gpu_loops.py"), os.path.join(HERE, "test_gpu_pins.py"),
-            "-k", "cc")
+            "-k", "cc or sssp")
