@@ -561,7 +561,10 @@ __device__ __forceinline__ void bins_min_pull(int64_t nL, const int32_t* __restr
     }
   }
 
-  // ---- medium rows: a half-warp per row, two rows at a time, 128 entries a pass
+  // ---- medium rows (17..512 entries): each lane first probes its own row's
+  // first 8 entries -- a row that meets the bound there costs one round trip
+  // (a uniform graph's late pulls: most rows) -- and the rest continue a
+  // half-warp per row, two rows at a time, 128 entries a pass
   const int half = lane >> 4, hl = lane & 15;
   const unsigned hmask = 0xffffu << (16 * half);
   for (int64_t g = w0; g * 32 < nM; g += nw) {
@@ -569,11 +572,23 @@ __device__ __forceinline__ void bins_min_pull(int64_t nL, const int32_t* __restr
     const int32_t r = i < nM ? __ldg(M_rows + i) : -1;
     const bool ok = r >= 0 && !op.skip(r);
     int64_t lo = 0, hi = 0;
+    T pacc = ident;  // the probe's minimum of my row
     if (ok) {
       lo = __ldg(off + r);
       hi = __ldg(off + r + 1);
+      int32_t c[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = __ldg(idx + lo + k);  // rows hold >= 17 entries
+      T x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = op.load(lo + k, c[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pacc = x[k] < pacc ? x[k] : pacc;
+      lo += 8;
     }
-    uint32_t bal = __ballot_sync(GB_FULL, ok);
+    const bool more = ok && !op.reached(pacc);
+    if (ok && !more) op.emit(r, pacc, true);
+    uint32_t bal = __ballot_sync(GB_FULL, more);
     while (bal) {
       const int j0 = __ffs(bal) - 1;
       bal &= bal - 1;
@@ -584,7 +599,7 @@ __device__ __forceinline__ void bins_min_pull(int64_t nL, const int32_t* __restr
       const int64_t l = __shfl_sync(GB_FULL, lo, src);
       int64_t h = __shfl_sync(GB_FULL, hi, src);
       if (half && j1 < 0) h = l;  // no second row: the upper half idles
-      T acc = ident;
+      T acc = __shfl_sync(GB_FULL, pacc, src);
       for (int64_t base = l; base < h; base += 128) {
         int32_t c[8];
 #pragma unroll
@@ -709,16 +724,29 @@ sssp_pull_exit(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
   bins_min_pull(nL, L_row, L_beg, L_end, nM, M_rows, nS, S_rows, off, idx, op);
 }
 
-// the row bins of a pull orientation (CC rows, SSSP in-edges) in one
-// cudaMalloc block (*mem, the caller frees it); synchronises.  Leaves *mem null -- full pulls keep the
-// edge-balanced tiles -- when the degrees are not skewed (rows over 512
-// entries hold under 10 % of the entries: the hubs whose lists stop early are
-// what the bounded pull saves; uniform s24 ran 9.23 vs 8.02 ms with it, R-MAT
-// s24 2.15 vs 3.62 ms), when the rows are empty, or with GB_PULL_EXIT=0
-// (GB_PULL_EXIT=2: always).
+// The row bins of a pull orientation (CC rows, SSSP in-edges) in one
+// cudaMalloc block (*mem, the caller frees it); synchronises.  Leaves *mem
+// null (every pull keeps the edge-balanced tiles) when the rows are empty or
+// with GB_PULL_EXIT=0.  Whether a pull takes the bounded kernel is decided
+// per iteration on the device from a predictor of how much it would skip
+// (CC: live grandparents equal to the bound, cc_count_low; SSSP: edges of
+// settled rows) -- with no early exits the bins' per-row round trips lose to
+// the edge-balanced tiles (uniform s24 CC with bins on every full pull: 9.3
+// vs 8.0 ms).  GB_PULL_EXIT=2 takes the bounded kernel for every CC full
+// pull and every SSSP pull (tests).
 static int pull_exit_mode() {
   static const int m = getenv("GB_PULL_EXIT") ? atoi(getenv("GB_PULL_EXIT")) : 1;
   return m;
+}
+// a full CC pull takes the bounded kernel when at least this share of the
+// vertices have a live grandparent equal to the bound (GB_CC_EXIT_SHARE)
+static double cc_exit_share() {
+  static double v = -1.0;
+  if (v < 0) {
+    const char* e = getenv("GB_CC_EXIT_SHARE");
+    v = pull_exit_mode() == 2 ? 0.0 : (e ? atof(e) : 0.2);
+  }
+  return v;
 }
 static gb_status skew_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem) {
   *mem = nullptr;
@@ -726,7 +754,6 @@ static gb_status skew_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b
   if (pull_exit_mode() == 0 || rows->nrows == 0) return GB_OK;
   int64_t c[3];
   GB_TRY(gb_bin_plan_counts(ctx, rows, c));
-  if (pull_exit_mode() != 2 && (double)c[2] * 512.0 < 0.1 * (double)rows->nnz) return GB_OK;
   const size_t bytes = 4 * (size_t)(c[0] + c[1] + c[2]) + 16 * (size_t)c[2] + 64;
   if (cudaMalloc(mem, bytes) != cudaSuccess) {
     cudaGetLastError();
@@ -1032,6 +1059,27 @@ __global__ void cc_list(int64_t n, const int* __restrict__ gp, int32_t* __restri
       if (l) F[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)k;
       base += __popc(bal);
     }
+  }
+}
+
+// live grandparents equal to the bound the shortcut pass recorded: the
+// share of rows a bounded full pull (cc_pull_exit) stops early in
+__global__ void __launch_bounds__(256)
+cc_count_low(int64_t n, const int* __restrict__ gp, const int* __restrict__ lowp,
+             unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long s_n[8];
+  const int low = *lowp;
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += gp[i] == low && low != kImax32;
+  c = (unsigned long long)warp_sum_ll((long long)c);
+  if ((threadIdx.x & 31) == 0) s_n[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_n[w];
+    if (t) atomicAdd(out, t);
   }
 }
 
@@ -1407,9 +1455,12 @@ struct CcState {
   int64_t max_iters;
   int64_t* log;
   int32_t policy, sparsify;
+  double exit_share;  // a full pull takes cc_pull_exit above this share of grandparents at the bound
+  int32_t has_bins, pad4_;
   // loop
   int64_t it, live, iters;
   unsigned long long cnt[3];  // changed, live, listed
+  unsigned long long nlow;    // live grandparents equal to the bound (cc_count_low)
   unsigned long long nlong;
   int64_t npush;  // iterations that ran the push branch (launch accounting)
   int32_t low;    // smallest live grandparent (cc_pull_exit's bound)
@@ -1433,6 +1484,7 @@ __global__ void cc_start_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditi
   st->it = 0;
   st->live = n;
   st->iters = 0;
+  st->nlow = 0;
   st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
   st->nlong = 0;
   st->npush = 0;
@@ -1462,14 +1514,19 @@ __global__ void cc_step_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditio
   if (changed != 0) st->live = (int64_t)st->cnt[1];
   st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
   st->nlong = 0;
-  unsigned dir = 4;  // no branch
+  const unsigned long long nlow = st->nlow;
+  st->nlow = 0;
+  unsigned dir = 5;  // no branch
   if (cont) {
-    // branch 0: pull, 1: push, 2: pull probing the live bitmap first
+    // branch 0: pull over row tiles, 1: push, 2: pull probing the live
+    // bitmap first, 4: bounded pull over the row bins (enough grandparents
+    // sit at the bound that most rows stop early)
     const int32_t d = log_decision(st->log, it + 1, nnz, n, st->live, st->ratio, st->policy);
     const double live = (double)st->live;
     dir = d != GB_DIR_PULL || (st->has_cols && live < st->push_share * (double)n)
               ? 1u
               : (live < st->live_share * (double)n ? 2u : 0u);
+    if (dir == 0 && st->has_bins && (double)nlow >= st->exit_share * (double)n) dir = 4u;
     st->npush += dir == 1;
   }
   cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
@@ -1521,8 +1578,8 @@ static cudaError_t cc_graph_build(gb_ctx* ctx, CcGraph* G) {
       cudaStream_t b = cs[1];
       copy_i32<<<vec_grid, 256, 0, b>>>(n, G->P, G->pp);
       fill_i32<<<vec_grid, 256, 0, b>>>(n, kImax32, G->hook);
-      cudaGraph_t br[4];
-      GB_LTRY(add_conditional(b, h_dir, cudaGraphCondTypeSwitch, 4, br));
+      cudaGraph_t br[5];
+      GB_LTRY(add_conditional(b, h_dir, cudaGraphCondTypeSwitch, 5, br));
       GB_LTRY(loop_capture_into(br[3], cs[2], [&]() -> cudaError_t {
         // first pull (grandparents are the identity): each row's smallest
         // column id -- its first entry when the rows start at their minimum
@@ -1536,12 +1593,15 @@ static cudaError_t cc_graph_build(gb_ctx* ctx, CcGraph* G) {
       }));
       GB_LTRY(loop_capture_into(br[0], cs[2], [&]() -> cudaError_t {
         // pull: mxv walks rows of A (kernels.py:313-316)
-        if (G->binmem)
-          cc_pull_exit_launch(ctx, cs[2], G->bins, &G->rows, G->gp, G->mn, &G->st->low, G->hook);
-        else if (G->plan.R)
+        if (G->plan.R)
           cc_pull<<<resident_grid(ctx, cc_pull, 256), 256, 0, cs[2]>>>(
               G->plan.R, G->plan.nz_rows, G->plan.nz_off, G->rows.indices, G->plan.tile_first,
               G->gp, G->hook);
+        return cudaGetLastError();
+      }));
+      GB_LTRY(loop_capture_into(br[4], cs[2], [&]() -> cudaError_t {
+        if (G->binmem)
+          cc_pull_exit_launch(ctx, cs[2], G->bins, &G->rows, G->gp, G->mn, &G->st->low, G->hook);
         return cudaGetLastError();
       }));
       GB_LTRY(loop_capture_into(br[2], cs[2], [&]() -> cudaError_t {
@@ -1564,6 +1624,7 @@ static cudaError_t cc_graph_build(gb_ctx* ctx, CcGraph* G) {
       }));
       cc_hook<<<vec_grid, 256, 0, b>>>(n, G->hook, G->mn, G->pp, G->P, &G->st->low);
       cc_shortcut_g<<<vec_grid, 256, 0, b>>>(n, G->P, G->gp, G->gpp, G->st, G->livebm);
+      if (G->binmem) cc_count_low<<<vec_grid, 256, 0, b>>>(n, G->gp, &G->st->low, &G->st->nlow);
       cc_step_g<<<1, 1, 0, b>>>(G->st, n, nnz, h_loop, h_dir);
       return cudaGetLastError();
     });
@@ -1646,6 +1707,8 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
   h.sparsify = sparsify;
   h.live_share = cc_live_share();
   h.push_share = cc_push_share();
+  h.exit_share = cc_exit_share();
+  h.has_bins = G->binmem != nullptr;
   h.has_cols = cols != nullptr;
   GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(CcState, it), cudaMemcpyHostToDevice, s));
   GB_CUDA(ctx, cudaGraphLaunch(G->exec, s));
@@ -1665,8 +1728,9 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
       log_est[i] = lg[3 * i + 2];
     }
   }
-  // per iteration: copy, fill, the branch (1 kernel; push 3), hook, shortcut, step
-  count_launch(ctx, (int)(3 + 6 * iters + 2 * npush));
+  // per iteration: copy, fill, the branch (1 kernel; push 3), hook, shortcut,
+  // (the bound count,) step
+  count_launch(ctx, (int)(3 + (G->binmem ? 7 : 6) * iters + 2 * npush));
   *iters_out = iters;
   return GB_OK;
 }
@@ -1712,7 +1776,7 @@ static double sssp_exit_share() {
   static double v = -1.0;
   if (v < 0) {
     const char* e = getenv("GB_SSSP_EXIT_SHARE");
-    v = e ? atof(e) : 0.3;
+    v = pull_exit_mode() == 2 ? 0.0 : (e ? atof(e) : 0.3);
   }
   return v;
 }
@@ -2239,7 +2303,7 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   int* hook = ar.alloc<int>(n);
   uint32_t* livebm = ar.alloc<uint32_t>((n + 31) / 32 + 1);
   int32_t* F = ar.alloc<int32_t>(n);
-  unsigned long long* cnt = ar.alloc<unsigned long long>(3);  // [changed, live, listed]
+  unsigned long long* cnt = ar.alloc<unsigned long long>(4);  // [changed, live, listed, at bound]
   GB_ARENA_CHECK(ctx, ar);
   int* low = ar.alloc<int>(1);
   GB_ARENA_CHECK(ctx, ar);
@@ -2260,7 +2324,7 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   count_launch(ctx, 1);
   const int pull_grid = resident_grid(ctx, cc_pull, 256);
   const int vec_grid = grid_for(ctx, n, 256, 8);
-  int64_t live = n, iters = 0;
+  int64_t live = n, iters = 0, nlow = 0;
   for (int64_t it = 0; it < max_iters; ++it) {
     int64_t est = 0;
     const int32_t dir = gb_decide_direction(rows->nnz, rows->nrows, live, ratio, policy, &est);
@@ -2283,7 +2347,8 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
       else if (plan.R && (double)live < cc_live_share() * (double)n)
         cc_pull_live<<<resident_grid(ctx, cc_pull_live, 256), 256, 0, s>>>(
             plan.R, plan.nz_rows, plan.nz_off, rows->indices, plan.tile_first, gp, livebm, hook);
-      else if (binmem) cc_pull_exit_launch(ctx, s, bins, rows, gp, mn, low, hook);
+      else if (binmem && (double)nlow >= cc_exit_share() * (double)n)
+        cc_pull_exit_launch(ctx, s, bins, rows, gp, mn, low, hook);
       else if (plan.R) cc_pull<<<pull_grid, 256, 0, s>>>(plan.R, plan.nz_rows, plan.nz_off, rows->indices,
                                                     plan.tile_first, gp, hook);
       count_launch(ctx, 1);
@@ -2303,12 +2368,18 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
     cc_hook<<<vec_grid, 256, 0, s>>>(n, hook, mn, pp, P, low);
     GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
     cc_shortcut<<<vec_grid, 256, 0, s>>>(n, P, gp, gpp, sparsify, cnt, cnt + 1, livebm, low);
+    if (binmem) {
+      GB_CUDA(ctx, cudaMemsetAsync(cnt + 3, 0, 8, s));
+      cc_count_low<<<vec_grid, 256, 0, s>>>(n, gp, low, cnt + 3);
+      count_launch(ctx, 2);
+    }
     GB_LAUNCH_CHECK(ctx);
     count_launch(ctx, 5);
-    int64_t h[2];
-    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 2));
+    int64_t h[4];
+    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 4));
     if (h[0] == 0) break;  // algorithms.py:196-197
     live = h[1];
+    nlow = binmem ? h[3] : 0;
   }
   widen_i32<<<vec_grid, 256, 0, s>>>(n, P, reinterpret_cast<long long*>(parent));
   GB_LAUNCH_CHECK(ctx);
