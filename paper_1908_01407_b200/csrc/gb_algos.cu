@@ -748,7 +748,7 @@ static double cc_exit_share() {
   }
   return v;
 }
-static gb_status skew_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem) {
+static gb_status pull_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem) {
   *mem = nullptr;
   *b = gb_bin_plan{};
   if (pull_exit_mode() == 0 || rows->nrows == 0) return GB_OK;
@@ -1686,7 +1686,7 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
     Arena ar(ctx);
     gb_status st = row_tiles_plan(ctx, ar, n, rows->offsets, rows->nnz, &G->plan);
     if (st == GB_OK) st = cc_rows_start_at_min(ctx, rows, G->plan, &G->first_min);
-    if (st == GB_OK) st = skew_bins_build(ctx, rows, &G->bins, &G->binmem);
+    if (st == GB_OK) st = pull_bins_build(ctx, rows, &G->bins, &G->binmem);
     cudaError_t e = st == GB_OK ? cc_graph_build(ctx, G) : cudaSuccess;
     if (st != GB_OK || e != cudaSuccess) {
       cudaGetLastError();
@@ -2038,7 +2038,7 @@ static gb_status sssp_graph(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull,
       G->plan.tile_first = (int32_t*)(m + o_t);
       Arena ar(ctx);
       st = row_tiles_plan(ctx, ar, n, pull->offsets, pull->nnz, &G->plan);
-      if (st == GB_OK) st = skew_bins_build(ctx, pull, &G->bins, &G->binmem);
+      if (st == GB_OK) st = pull_bins_build(ctx, pull, &G->bins, &G->binmem);
     }
     cudaError_t e = st == GB_OK ? sssp_graph_build(ctx, G) : cudaSuccess;
     if (st != GB_OK || e != cudaSuccess) {
@@ -2168,7 +2168,7 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
         cand = ar.alloc<long long>(n);
         GB_ARENA_CHECK(ctx, ar);
         fill_i64<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, kInfBits, cand);
-        GB_TRY(skew_bins_build(ctx, pull, &bins, &binmem));
+        GB_TRY(pull_bins_build(ctx, pull, &bins, &binmem));
       }
       // the bounded pull when the last pull left most edges in settled rows
       const bool bounded = binmem && (double)settled >= sssp_exit_share() * (double)pull->nnz;
@@ -2313,7 +2313,7 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   GB_TRY(cc_rows_start_at_min(ctx, rows, plan, &first_min));
   gb_bin_plan bins;
   void* binmem = nullptr;
-  GB_TRY(skew_bins_build(ctx, rows, &bins, &binmem));
+  GB_TRY(pull_bins_build(ctx, rows, &bins, &binmem));
   struct BinFree {  // cudaFree waits for the work that reads the bins
     void* p;
     ~BinFree() { if (p) cudaFree(p); }
