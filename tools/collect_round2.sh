@@ -25,7 +25,7 @@ cap mxvm "mv_pull_binned" mxvm 24 1
 cap mxvm_u "mv_pull_binned" mxvm_u 24 4   # uniform: column stripes (4 launches)
 cap pr "pr_spmv|pr_epilogue" pr 22 2
 cap cc "cc_pull|cc_hook|cc_shortcut" cc 24 5   # cc_pull matches cc_pull_exit
-cap sssp "sssp_pull_tiles|lbs_expand" sssp 20 3
+cap sssp "sssp_pull|lbs_expand" sssp 20 5   # tiles, the bounded bins (sssp_pull_exit), push
 cap tc "tc_count" tc 20 1
 cap push "lbs_expand" push 24 1
 cap mxm "mxm_masked_kernel" mxm 20 1
