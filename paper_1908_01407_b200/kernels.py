@@ -229,15 +229,18 @@ _MV_BINS = os.environ.get("GB_MV_BINS", "")
 
 
 # Column stripes for the binned pull (gb_mxv_pull_striped): when the gathered
-# vector is larger than GB_MV_STRIPE_BYTES (default 32 MB, about a quarter of
-# the 126 MB L2) a structure-only matrix whose degrees are not skewed (under
+# vector is larger than GB_MV_STRIPE_BYTES (default 48 MB, under half of the
+# 126 MB L2) a structure-only matrix whose degrees are not skewed (under
 # 10 % of its entries in rows longer than 512) is cut into ceil(8*ncols /
 # that) column stripes, multiplied one after the other, so every stripe's
 # slice of the vector stays L2-resident while it is gathered.  Measured at
 # s24, 50 % mask: uniform 2.68 -> 1.90 ms with 4 stripes; R-MAT 1.27 -> 1.78
 # ms (its gathers concentrate on the hubs, which stay cached anyway, so the
-# extra passes only cost) -- hence the skew test.  0 disables.
-_MV_STRIPE_BYTES = int(os.environ.get("GB_MV_STRIPE_BYTES", str(32 << 20)))
+# extra passes only cost) -- hence the skew test.  Stripe budget at uniform
+# s24 (masked f64, kernel ms): 16 MB (8 stripes) 2.97, 32 MB (4) 1.85, 48 MB
+# (3) 1.80, 64 MB (2) 2.72; the unmasked int64 min-pull 3.04 (32 MB) vs 3.10
+# (48 MB).  0 disables.
+_MV_STRIPE_BYTES = int(os.environ.get("GB_MV_STRIPE_BYTES", str(48 << 20)))
 _MV_STRIPE_SKEW = float(os.environ.get("GB_MV_STRIPE_SKEW", "0.1"))
 
 
