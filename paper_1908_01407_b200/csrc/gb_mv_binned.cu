@@ -42,12 +42,16 @@ constexpr int kBinLong = 512;
 #define GB_MVB_MINB 4
 #endif
 
+
 template <class T>
 __device__ __forceinline__ T bin_aval(const T* vals, T iso, int64_t p) {
   return vals ? __ldg(vals + p) : iso;
 }
 
-template <class T, int ADD, int MUL, bool VALS>
+// QM: medium rows a quarter-warp each, four per round trip (the column
+// stripes of regular graphs: uniform s24 1.81 -> 1.70 ms), else a half-warp
+// each, two per round trip (R-MAT s24: 1.22 vs 1.25 ms quartered)
+template <class T, int ADD, int MUL, bool VALS, bool QM>
 __global__ void __launch_bounds__(256, GB_MVB_MINB)
 mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __restrict__ L_beg,
                const int64_t* __restrict__ L_end, int64_t nM, const int32_t* __restrict__ M_rows,
@@ -139,8 +143,7 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
     }
   }
 
-  // ---- medium rows: a half-warp per allowed row, two rows at a time --------
-  const int half = lane >> 4, hl = lane & 15;
+  // ---- medium rows: a half-warp (QM: quarter-warp) per allowed row ---------
   for (int64_t g = w0; g * 32 < nM; g += nw) {
     const int64_t i = g * 32 + lane;
     const int32_t r = i < nM ? __ldg(M_rows + i) : -1;
@@ -151,7 +154,55 @@ mv_pull_binned(int64_t nL, const int32_t* __restrict__ L_row, const int64_t* __r
       hi = __ldg(off + r + 1);
     }
     uint32_t bal = __ballot_sync(GB_FULL, ok);
-    while (bal) {
+    // QM: a quarter-warp per row, four rows at a time, 64 entries a pass
+    if (QM) while (bal) {
+      int js[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        js[k] = bal ? __ffs(bal) - 1 : -1;
+        if (bal) bal &= bal - 1;
+      }
+      const int qq = lane >> 3, ql = lane & 7;
+      const int mine = qq == 0 ? js[0] : qq == 1 ? js[1] : qq == 2 ? js[2] : js[3];
+      const int src = mine >= 0 ? mine : js[0];
+      const int32_t rr = __shfl_sync(GB_FULL, r, src);
+      int64_t l = __shfl_sync(GB_FULL, lo, src), h = __shfl_sync(GB_FULL, hi, src);
+      if (mine < 0) h = l;  // fewer than four rows left: this quarter idles
+      T acc = ident;
+      int cnt = 0;
+      for (int64_t base = l; base < h; base += 64) {
+        int32_t cols[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int64_t p = base + 8 * k + ql;
+          cols[k] = p < h ? ld_stream(idx + p) : 0;
+        }
+        T x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = base + 8 * k + ql < h ? ld_gather(u + cols[k]) : ident;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fold_one_v(acc, cnt, x[k], base + 8 * k + ql);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) acc = op_fold<T>(add_op, acc, __shfl_xor_sync(GB_FULL, acc, o));
+      cnt = (int)__reduce_add_sync(0xffu << (8 * qq), (unsigned)cnt);
+      if (ql == 0 && h > l) {
+        c_reads += (unsigned long long)(h - l);
+        if (cnt > 0) {
+          c_muls += cnt;
+          if (accumulate) {
+            out[rr] = op_fold<T>(add_op, out[rr], acc);
+            if (hasmul) atomicOr(hasmul + (rr >> 5), 1u << (rr & 31));
+          } else {
+            out[rr] = acc;
+            ++c_rows;
+          }
+        }
+      }
+    }
+    // else a half-warp per row, two rows at a time, 128 entries a pass
+    const int half = lane >> 4, hl = lane & 15;
+    if (!QM) while (bal) {
       const int j0 = __ffs(bal) - 1;
       bal &= bal - 1;
       const int j1 = bal ? __ffs(bal) - 1 : -1;
@@ -322,7 +373,8 @@ template <class T, int ADD, int MUL, bool VALS>
 static void launch_binned_k(gb_ctx* ctx, int add_op, int mult_op, const gb_bin_plan* p,
                             const gb_csr* a, T iso, const T* u, const uint32_t* mask, T* out,
                             unsigned long long* counters, uint32_t* hasmul, int accumulate) {
-  auto k = mv_pull_binned<T, ADD, MUL, VALS>;
+  // striped (regular) matrices: quarter-warp medium rows
+  auto k = accumulate ? mv_pull_binned<T, ADD, MUL, VALS, true> : mv_pull_binned<T, ADD, MUL, VALS, false>;
   k<<<resident_grid(ctx, k, 256), 256, 0, stream_of(ctx)>>>(
       p->n_long_tiles, p->tile_row, p->tile_beg, p->tile_end, p->n_mid, p->mid_rows, p->n_short,
       p->short_rows, a->offsets, a->indices, (const T*)a->values, iso, u, mask, add_op, mult_op,

@@ -22,7 +22,7 @@ cap() {  # name regex algo scale count
 cap bfs_push "bfs_expand_warp" bfs 24 2
 cap bfs_pull "bfs_pull" bfs 24 1
 cap mxvm "mv_pull_binned" mxvm 24 1
-cap mxvm_u "mv_pull_binned" mxvm_u 24 4   # uniform: column stripes (4 launches)
+cap mxvm_u "mv_pull_binned" mxvm_u 24 3   # uniform: column stripes (3 launches)
 cap pr "pr_spmv|pr_epilogue" pr 22 2
 cap cc "cc_pull|cc_hook|cc_shortcut" cc 24 5   # cc_pull matches cc_pull_exit
 cap sssp "sssp_pull|lbs_expand" sssp 20 5   # tiles, the bounded bins (sssp_pull_exit), push
