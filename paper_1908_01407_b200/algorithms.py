@@ -429,12 +429,21 @@ def sssp(A: SparseMatrix, source: int, desc=None, on_iteration=None) -> Vector:
 
 
 def _min_value(A):
+    """Smallest stored value (sssp's positivity check and its pull bound).
+    Cached on the orientation, keyed by the values tensor and its in-place
+    version counter, so repeated calls on one matrix skip the reduction and
+    its host synchronisation (s20: a 50 us pass over 31 M weights per call)."""
     o = A.orient(False)
     if o.values is None:
         return o.iso
+    key = (o.values.data_ptr(), o.values._version, o.nnz)
+    hit = getattr(o, "_min_cache", None)
+    if hit is not None and hit[0] == key:
+        return hit[1]
     lo, hi = C.c_double(), C.c_double()
     _lib.context().call("gb_values_minmax", o.nnz, _lib.ptr(o.values), _lib.dtype_code(o.dt),
                         C.byref(lo), C.byref(hi))
+    o._min_cache = (key, lo.value)
     return lo.value
 
 

@@ -504,6 +504,7 @@ class _Orient:
 
     __slots__ = ("nrows", "ncols", "offsets", "indices", "values", "iso", "dt", "_nonempty",
                  "_plan", "_bins", "_stripes", "_ordered", "_order", "_mv_ordered", "_struct", "gen",
+                 "_min_cache",
                  "__weakref__")
 
     def __init__(self, nrows, ncols, offsets, indices, values, iso, dt):
