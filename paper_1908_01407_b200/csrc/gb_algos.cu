@@ -748,6 +748,16 @@ static double cc_exit_share() {
   }
   return v;
 }
+// ... or when at most this share of the vertices are non-empty rows above
+// the bound (GB_CC_EXIT_ROWS)
+static double cc_exit_rows() {
+  static double v = -1.0;
+  if (v < 0) {
+    const char* e = getenv("GB_CC_EXIT_ROWS");
+    v = e ? atof(e) : 0.1;
+  }
+  return v;
+}
 static gb_status pull_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem) {
   *mem = nullptr;
   *b = gb_bin_plan{};
@@ -1062,24 +1072,42 @@ __global__ void cc_list(int64_t n, const int* __restrict__ gp, int32_t* __restri
   }
 }
 
-// live grandparents equal to the bound the shortcut pass recorded: the
-// share of rows a bounded full pull (cc_pull_exit) stops early in
+// The predictors of the next bounded pull (cc_pull_exit), after the
+// shortcut pass recorded the bound: out[0] = live grandparents equal to it
+// (rows meet it early), out[1] = non-empty rows (the R ids of nz_rows) with
+// mn at or below it (the rows the bounded pull skips) -- counted only when
+// fewer than push_share of the grandparents are live (*livep, from the
+// shortcut), the case where the bounded pull competes with the transposed
+// push; otherwise out[1] stays 0
 __global__ void __launch_bounds__(256)
-cc_count_low(int64_t n, const int* __restrict__ gp, const int* __restrict__ lowp,
+cc_count_low(int64_t n, const int* __restrict__ gp, const int* __restrict__ mn, int64_t R,
+             const int32_t* __restrict__ nz_rows, const int* __restrict__ lowp,
+             const unsigned long long* __restrict__ livep, double push_share,
              unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long s_n[8];
+  __shared__ unsigned long long s_n[8], s_u[8];
   const int low = *lowp;
-  unsigned long long c = 0;
+  const bool rows = (double)*livep < push_share * (double)n;
+  unsigned long long c = 0, u = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
+       i += (int64_t)gridDim.x * blockDim.x) {
     c += gp[i] == low && low != kImax32;
+    if (rows && i < R) u += mn[nz_rows[i]] <= low;
+  }
   c = (unsigned long long)warp_sum_ll((long long)c);
-  if ((threadIdx.x & 31) == 0) s_n[threadIdx.x >> 5] = c;
+  u = (unsigned long long)warp_sum_ll((long long)u);
+  if ((threadIdx.x & 31) == 0) {
+    s_n[threadIdx.x >> 5] = c;
+    s_u[threadIdx.x >> 5] = u;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_n[w];
+    unsigned long long t = 0, tu = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      t += s_n[w];
+      tu += s_u[w];
+    }
     if (t) atomicAdd(out, t);
+    if (tu) atomicAdd(out + 1, tu);
   }
 }
 
@@ -1455,12 +1483,14 @@ struct CcState {
   int64_t max_iters;
   int64_t* log;
   int32_t policy, sparsify;
-  double exit_share;  // a full pull takes cc_pull_exit above this share of grandparents at the bound
+  double exit_share;  // a pull takes cc_pull_exit above this share of grandparents at the bound
+  double exit_rows;   // ... or when at most this share of the rows is above it
+  int64_t nz_rows;    // non-empty rows of the matrix
   int32_t has_bins, pad4_;
   // loop
   int64_t it, live, iters;
   unsigned long long cnt[3];  // changed, live, listed
-  unsigned long long nlow;    // live grandparents equal to the bound (cc_count_low)
+  unsigned long long nlow[2];  // cc_count_low: grandparents at the bound, rows above it
   unsigned long long nlong;
   int64_t npush;  // iterations that ran the push branch (launch accounting)
   int32_t low;    // smallest live grandparent (cc_pull_exit's bound)
@@ -1484,7 +1514,7 @@ __global__ void cc_start_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditi
   st->it = 0;
   st->live = n;
   st->iters = 0;
-  st->nlow = 0;
+  st->nlow[0] = st->nlow[1] = 0;
   st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
   st->nlong = 0;
   st->npush = 0;
@@ -1514,8 +1544,9 @@ __global__ void cc_step_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditio
   if (changed != 0) st->live = (int64_t)st->cnt[1];
   st->cnt[0] = st->cnt[1] = st->cnt[2] = 0;
   st->nlong = 0;
-  const unsigned long long nlow = st->nlow;
-  st->nlow = 0;
+  const unsigned long long nlow = st->nlow[0];
+  const int64_t nup = st->nz_rows - (int64_t)st->nlow[1];  // non-empty rows above the bound
+  st->nlow[0] = st->nlow[1] = 0;
   unsigned dir = 5;  // no branch
   if (cont) {
     // branch 0: pull over row tiles, 1: push, 2: pull probing the live
@@ -1526,7 +1557,13 @@ __global__ void cc_step_g(CcState* st, int64_t n, int64_t nnz, cudaGraphConditio
     dir = d != GB_DIR_PULL || (st->has_cols && live < st->push_share * (double)n)
               ? 1u
               : (live < st->live_share * (double)n ? 2u : 0u);
-    if (dir == 0 && st->has_bins && (double)nlow >= st->exit_share * (double)n) dir = 4u;
+    // a pull the rule chose takes the bounded kernel (4) when most rows meet
+    // the bound early or are skipped outright -- ahead of the live-count
+    // variants: at R-MAT s24 iteration 3 (12 % live, so far the transposed
+    // push) only the rows outside the giant component are left
+    if (d == GB_DIR_PULL && st->has_bins &&
+        ((double)nlow >= st->exit_share * (double)n || (double)nup <= st->exit_rows * (double)n))
+      dir = 4u;
     st->npush += dir == 1;
   }
   cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
@@ -1624,7 +1661,10 @@ static cudaError_t cc_graph_build(gb_ctx* ctx, CcGraph* G) {
       }));
       cc_hook<<<vec_grid, 256, 0, b>>>(n, G->hook, G->mn, G->pp, G->P, &G->st->low);
       cc_shortcut_g<<<vec_grid, 256, 0, b>>>(n, G->P, G->gp, G->gpp, G->st, G->livebm);
-      if (G->binmem) cc_count_low<<<vec_grid, 256, 0, b>>>(n, G->gp, &G->st->low, &G->st->nlow);
+      if (G->binmem)
+        cc_count_low<<<vec_grid, 256, 0, b>>>(n, G->gp, G->mn, G->plan.R, G->plan.nz_rows,
+                                              &G->st->low, &G->st->cnt[1], cc_push_share(),
+                                              G->st->nlow);
       cc_step_g<<<1, 1, 0, b>>>(G->st, n, nnz, h_loop, h_dir);
       return cudaGetLastError();
     });
@@ -1708,6 +1748,8 @@ static gb_status cc_graph(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, i
   h.live_share = cc_live_share();
   h.push_share = cc_push_share();
   h.exit_share = cc_exit_share();
+  h.exit_rows = cc_exit_rows();
+  h.nz_rows = G->plan.R;
   h.has_bins = G->binmem != nullptr;
   h.has_cols = cols != nullptr;
   GB_CUDA(ctx, cudaMemcpyAsync(G->st, &h, offsetof(CcState, it), cudaMemcpyHostToDevice, s));
@@ -2303,7 +2345,8 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   int* hook = ar.alloc<int>(n);
   uint32_t* livebm = ar.alloc<uint32_t>((n + 31) / 32 + 1);
   int32_t* F = ar.alloc<int32_t>(n);
-  unsigned long long* cnt = ar.alloc<unsigned long long>(4);  // [changed, live, listed, at bound]
+  // [changed, live, listed, grandparents at the bound, rows above it]
+  unsigned long long* cnt = ar.alloc<unsigned long long>(5);
   GB_ARENA_CHECK(ctx, ar);
   int* low = ar.alloc<int>(1);
   GB_ARENA_CHECK(ctx, ar);
@@ -2324,7 +2367,7 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   count_launch(ctx, 1);
   const int pull_grid = resident_grid(ctx, cc_pull, 256);
   const int vec_grid = grid_for(ctx, n, 256, 8);
-  int64_t live = n, iters = 0, nlow = 0;
+  int64_t live = n, iters = 0, nlow = 0, nup = n;
   for (int64_t it = 0; it < max_iters; ++it) {
     int64_t est = 0;
     const int32_t dir = gb_decide_direction(rows->nnz, rows->nrows, live, ratio, policy, &est);
@@ -2335,9 +2378,18 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
     GB_CUDA(ctx, cudaMemcpyAsync(pp, P, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
     fill_i32<<<vec_grid, 256, 0, s>>>(n, kImax32, hook);
     const int ps = prof_begin(ctx, PROF_CC, live);
-    // a pull over few live grandparents runs as the transposed push (same hooks)
-    const bool as_push = dir != GB_DIR_PULL || (it > 0 && cols && (double)live < cc_push_share() * (double)n);
-    if (!as_push) {
+    // a pull whose rows mostly meet the bound early or are skipped takes the
+    // bounded kernel; otherwise a pull over few live grandparents runs as
+    // the transposed push (same hooks)
+    const bool bounded = dir == GB_DIR_PULL && it > 0 && binmem &&
+                         ((double)nlow >= cc_exit_share() * (double)n ||
+                          (double)nup <= cc_exit_rows() * (double)n);
+    const bool as_push = !bounded && (dir != GB_DIR_PULL ||
+                                      (it > 0 && cols && (double)live < cc_push_share() * (double)n));
+    if (bounded) {
+      cc_pull_exit_launch(ctx, s, bins, rows, gp, mn, low, hook);
+      count_launch(ctx, 1);
+    } else if (!as_push) {
       // mxv pull walks rows of A (kernels.py:313-316, row_view(False))
       if (it == 0 && first_min)  // grandparents are the identity: each row's first column
         cc_hook_first<<<vec_grid, 256, 0, s>>>(n, rows->offsets, rows->indices, hook);
@@ -2347,8 +2399,6 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
       else if (plan.R && (double)live < cc_live_share() * (double)n)
         cc_pull_live<<<resident_grid(ctx, cc_pull_live, 256), 256, 0, s>>>(
             plan.R, plan.nz_rows, plan.nz_off, rows->indices, plan.tile_first, gp, livebm, hook);
-      else if (binmem && (double)nlow >= cc_exit_share() * (double)n)
-        cc_pull_exit_launch(ctx, s, bins, rows, gp, mn, low, hook);
       else if (plan.R) cc_pull<<<pull_grid, 256, 0, s>>>(plan.R, plan.nz_rows, plan.nz_off, rows->indices,
                                                     plan.tile_first, gp, hook);
       count_launch(ctx, 1);
@@ -2369,17 +2419,19 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
     GB_CUDA(ctx, cudaMemsetAsync(cnt, 0, 16, s));
     cc_shortcut<<<vec_grid, 256, 0, s>>>(n, P, gp, gpp, sparsify, cnt, cnt + 1, livebm, low);
     if (binmem) {
-      GB_CUDA(ctx, cudaMemsetAsync(cnt + 3, 0, 8, s));
-      cc_count_low<<<vec_grid, 256, 0, s>>>(n, gp, low, cnt + 3);
+      GB_CUDA(ctx, cudaMemsetAsync(cnt + 3, 0, 16, s));
+      cc_count_low<<<vec_grid, 256, 0, s>>>(n, gp, mn, plan.R, plan.nz_rows, low, cnt + 1,
+                                            cc_push_share(), cnt + 3);
       count_launch(ctx, 2);
     }
     GB_LAUNCH_CHECK(ctx);
     count_launch(ctx, 5);
-    int64_t h[4];
-    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 4));
+    int64_t h[5];
+    GB_TRY(read_i64(ctx, (const int64_t*)cnt, h, 5));
     if (h[0] == 0) break;  // algorithms.py:196-197
     live = h[1];
     nlow = binmem ? h[3] : 0;
+    nup = binmem ? plan.R - h[4] : n;
   }
   widen_i32<<<vec_grid, 256, 0, s>>>(n, P, reinterpret_cast<long long*>(parent));
   GB_LAUNCH_CHECK(ctx);
