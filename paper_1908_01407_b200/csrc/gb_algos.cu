@@ -1088,10 +1088,26 @@ cc_count_low(int64_t n, const int* __restrict__ gp, const int* __restrict__ mn, 
   const int low = *lowp;
   const bool rows = (double)*livep < push_share * (double)n;
   unsigned long long c = 0, u = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    c += gp[i] == low && low != kImax32;
-    if (rows && i < R) u += mn[nz_rows[i]] <= low;
+  // four independent elements per thread and pass (the mn lookups are
+  // dependent gathers; one at a time the pass was latency-bound)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    int g[4];
+    int32_t r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = i0 + k * stride;
+      g[k] = i < n ? gp[i] : kImax32;
+      r[k] = rows && i < R ? nz_rows[i] : -1;
+    }
+    int m[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m[k] = r[k] >= 0 ? __ldg(mn + r[k]) : kImax32;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      c += g[k] == low && low != kImax32;
+      u += r[k] >= 0 && m[k] <= low;
+    }
   }
   c = (unsigned long long)warp_sum_ll((long long)c);
   u = (unsigned long long)warp_sum_ll((long long)u);
