@@ -758,17 +758,27 @@ static double cc_exit_rows() {
   }
   return v;
 }
-static gb_status pull_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem) {
+// ar: the storage comes from the caller's per-call arena (the host-driven
+// loops; nothing to free, no device-wide synchronisation); null: one
+// cudaMalloc block the caller frees (the cached loop graphs)
+static gb_status pull_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b, void** mem,
+                                 Arena* ar = nullptr) {
   *mem = nullptr;
   *b = gb_bin_plan{};
   if (pull_exit_mode() == 0 || rows->nrows == 0) return GB_OK;
   int64_t c[3];
   GB_TRY(gb_bin_plan_counts(ctx, rows, c));
   const size_t bytes = 4 * (size_t)(c[0] + c[1] + c[2]) + 16 * (size_t)c[2] + 64;
-  if (cudaMalloc(mem, bytes) != cudaSuccess) {
+  if (ar) {
+    *mem = ar->raw(bytes);
+    if (ar->failed || !*mem) {
+      *mem = nullptr;
+      return set_error(ctx, GB_ERR_OOM, "pull bins: scratch allocation of %zu bytes", bytes);
+    }
+  } else if (cudaMalloc(mem, bytes) != cudaSuccess) {
     cudaGetLastError();
     *mem = nullptr;
-    return set_error(ctx, GB_ERR_OOM, "cc bins: cudaMalloc of %zu bytes", bytes);
+    return set_error(ctx, GB_ERR_OOM, "pull bins: cudaMalloc of %zu bytes", bytes);
   }
   char* m = static_cast<char*>(*mem);
   b->n_short = c[0];
@@ -782,7 +792,7 @@ static gb_status pull_bins_build(gb_ctx* ctx, const gb_csr* rows, gb_bin_plan* b
   b->short_rows = r + c[2] + c[1];
   const gb_status st = gb_bin_plan_fill(ctx, rows, b);
   if (st != GB_OK) {
-    cudaFree(*mem);
+    if (!ar) cudaFree(*mem);
     *mem = nullptr;
   }
   return st;
@@ -2202,10 +2212,7 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
   long long* cand = nullptr;  // pull candidates (+inf bits between iterations)
   gb_bin_plan bins{};         // row bins of `pull` (skewed graphs), with the plan
   void* binmem = nullptr;
-  struct BinFree {  // cudaFree waits for the work that reads the bins
-    void*& p;
-    ~BinFree() { if (p) cudaFree(p); }
-  } bin_free{binmem};
+
   int64_t K = 1, reached = 1, succ_last = -1, iters = 0, sumdeg = 0, settled = 0;
   const double push_iso = push->iso_f64, pull_iso = pull ? pull->iso_f64 : 0.0;
   for (int64_t it = 0; it < max_iters; ++it) {
@@ -2226,7 +2233,7 @@ gb_status gb_sssp(gb_ctx* ctx, const gb_csr* push, const gb_csr* pull, int64_t s
         cand = ar.alloc<long long>(n);
         GB_ARENA_CHECK(ctx, ar);
         fill_i64<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, kInfBits, cand);
-        GB_TRY(pull_bins_build(ctx, pull, &bins, &binmem));
+        GB_TRY(pull_bins_build(ctx, pull, &bins, &binmem, &ar));
       }
       // the bounded pull when the last pull left most edges in settled rows
       const bool bounded = binmem && (double)settled >= sssp_exit_share() * (double)pull->nnz;
@@ -2372,11 +2379,7 @@ gb_status gb_cc(gb_ctx* ctx, const gb_csr* rows, const gb_csr* cols, int64_t max
   GB_TRY(cc_rows_start_at_min(ctx, rows, plan, &first_min));
   gb_bin_plan bins;
   void* binmem = nullptr;
-  GB_TRY(pull_bins_build(ctx, rows, &bins, &binmem));
-  struct BinFree {  // cudaFree waits for the work that reads the bins
-    void* p;
-    ~BinFree() { if (p) cudaFree(p); }
-  } bin_free{binmem};
+  GB_TRY(pull_bins_build(ctx, rows, &bins, &binmem, &ar));
   GB_CUDA(ctx, cudaMemsetAsync(low, 0, sizeof(int), s));
   cc_init<<<grid_for(ctx, n, 256), 256, 0, s>>>(n, P, mn, gp, gpp);
   GB_LAUNCH_CHECK(ctx);
